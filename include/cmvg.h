@@ -1,0 +1,178 @@
+/*
+ * cmvg.h -- C ABI of the B200-native compressed adjacency-matrix product.
+ *
+ * This is the drop-in boundary for the reference's operator surface
+ * (reference proj/include/cmv/...):
+ *
+ *   cmvg_matvec_f64 / cmvg_matvec_f32  replace  cmv::matvec_ref_into
+ *       (ref_matvec.hpp:30-31), cmv::matvec_ref (ref_matvec.hpp:34-35) and
+ *       cmv::MatvecKernel::multiply (pagerank.hpp:31-32); the SCATTER form
+ *       replaces cmv::matvec_ref_left (ref_matvec.hpp:40-41).
+ *   cmvg_adds_per_product               replaces MatvecKernel::adds_per_product
+ *       (pagerank.hpp:33).
+ *   cmvg_dimension                      replaces MatvecKernel::dimension
+ *       (pagerank.hpp:30).
+ *   cmvg_decode_csr                     replaces cmv::reconstruct_graph
+ *       (ref_matrix.hpp:75-76).
+ *   cmvg_bv_encode                      replaces cmv::compress (ref_matrix.hpp:69)
+ *       as the builder of the compressed form (BV stream instead of A').
+ *   cmvg_pagerank                       replaces cmv::pagerank (pagerank.hpp:100-102)
+ *       for a device-resident kernel.
+ *   cmvg_stats / cmvg_graph_info        replace cmv::stats (ref_matrix.hpp:89).
+ *
+ * Conventions: opaque handles, int status codes, no
+ * exceptions across the ABI; cmvg_last_error() returns a thread-local
+ * message.  Status codes map to the reference's exception types:
+ * CMVG_ERR_INVALID -> std::invalid_argument, CMVG_ERR_RANGE ->
+ * std::out_of_range, CMVG_ERR_FORMAT -> cmv::FormatError, CMVG_ERR_CORRUPT ->
+ * cmv::CorruptionError (rmv_io.hpp:13-22).  The device handle owns all
+ * device memory; callers own their input/output buffers.  A handle may serve
+ * concurrent products on distinct streams for DEVICE pointers; HOST-pointer
+ * calls use per-handle staging buffers and are serialised internally.
+ */
+#ifndef CMVG_H_
+#define CMVG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CMVG_OK 0
+#define CMVG_ERR_INVALID 1
+#define CMVG_ERR_RANGE 2
+#define CMVG_ERR_FORMAT 3
+#define CMVG_ERR_CORRUPT 4
+#define CMVG_ERR_CUDA 5
+#define CMVG_ERR_NOMEM 6
+#define CMVG_ERR_UNSUPPORTED 7
+#define CMVG_ERR_INTERNAL 8
+
+/* product forms */
+#define CMVG_GATHER 0  /* y = A * x^T  (row i of y = sum over row i of A)     */
+#define CMVG_SCATTER 1 /* y = x * A    (computed on A's own compression)      */
+/* pointer kinds */
+#define CMVG_HOST 0   /* host buffers: H2D/D2H inside the call              */
+#define CMVG_DEVICE 1 /* device buffers on the handle's device (16-B aligned) */
+/* interval evaluation (cmvg_create_opts.interval_mode) */
+#define CMVG_INTERVALS_PREFIX 0 /* O(1) from a tile-local exclusive prefix of x */
+#define CMVG_INTERVALS_DIRECT 1 /* summed from the shared-memory x window       */
+/* PageRank dangling policy (cmv::DanglingPolicy, pagerank.hpp:16) */
+#define CMVG_DANGLING_UNIFORM 0
+#define CMVG_DANGLING_DROP 1
+
+typedef struct cmvg_csr cmvg_csr;           /* host CSR graph (cmv::CsrGraph)   */
+typedef struct cmvg_bvstream cmvg_bvstream; /* host canonical BV stream         */
+typedef struct cmvg_graph cmvg_graph;       /* device handle (one GPU, one shard) */
+
+typedef struct {
+  uint32_t window;       /* w: reference window (<= 7 for the device layout) */
+  uint32_t max_ref;      /* R: longest reference chain; 0 = unbounded       */
+  uint32_t min_interval; /* Lmin                                             */
+  uint32_t zeta_k;       /* residual zeta code parameter (3)                 */
+  uint32_t segment_rows; /* references never cross a multiple of this       */
+} cmvg_bv_params;
+
+typedef struct {
+  uint64_t stream_bits; /* S: canonical BV stream length                    */
+  uint64_t rows_with_ref;
+  uint64_t copied_edges;
+  uint64_t interval_edges;
+  uint64_t intervals;
+  uint64_t residual_edges;
+  uint64_t minus_edges; /* reference entries skipped by copy blocks        */
+  uint32_t max_depth;
+  uint32_t nsegments;
+} cmvg_bv_stats;
+
+typedef struct {
+  int device;             /* CUDA device ordinal                              */
+  uint32_t block_rows;    /* rows per CTA block (power of 2, multiple of the segment) */
+  uint32_t lanes;         /* decode lanes (threads) per block                 */
+  uint32_t window;        /* x-window entries staged per block                */
+  uint32_t stream_cap_words; /* blocks larger than this decode from global    */
+  uint32_t interval_mode; /* CMVG_INTERVALS_*                                 */
+  uint32_t row_begin;     /* shard [row_begin, row_end); row_end 0 = n        */
+  uint32_t row_end;
+} cmvg_create_opts;
+
+typedef struct {
+  uint32_t n;
+  uint64_t m;
+  uint32_t row_begin, row_end;
+  uint64_t bv_stream_bits;      /* canonical S (whole graph)               */
+  uint64_t bvd_row_bits;        /* device-layout coded payload (shard)     */
+  uint64_t bvd_stream_bytes;    /* incl. lane alignment and padding        */
+  uint64_t bvd_lane_table_bytes;
+  uint64_t bvd_block_table_bytes;
+  uint32_t block_rows, lanes, window, nblocks, max_depth, interval_mode;
+  uint64_t adds_per_product;
+  uint64_t device_bytes;
+} cmvg_graph_info;
+
+/* ---- errors -------------------------------------------------------------- */
+const char* cmvg_last_error(void);
+
+/* ---- host CSR graphs ------------------------------------------------------ */
+int cmvg_csr_from_arrays(uint32_t n, const uint64_t* row_offsets, const uint32_t* cols, cmvg_csr** out);
+int cmvg_gen_copy_model(uint32_t n, double mean_degree, double p_ref, double p_copy, uint64_t seed, cmvg_csr** out);
+int cmvg_gen_social(uint32_t n, uint64_t seed, cmvg_csr** out);
+int cmvg_csr_transpose(const cmvg_csr* g, cmvg_csr** out);
+uint32_t cmvg_csr_n(const cmvg_csr* g);
+uint64_t cmvg_csr_m(const cmvg_csr* g);
+const uint64_t* cmvg_csr_row_offsets(const cmvg_csr* g);
+const uint32_t* cmvg_csr_cols(const cmvg_csr* g);
+void cmvg_csr_free(cmvg_csr* g);
+
+/* ---- canonical BV stream (host) ------------------------------------------ */
+int cmvg_bv_encode(const cmvg_csr* g, const cmvg_bv_params* p, cmvg_bvstream** out);
+int cmvg_bv_from_words(uint32_t n, uint64_t m, const cmvg_bv_params* p, const uint32_t* words, uint64_t nbits,
+                       const uint64_t* segment_bit_offsets, cmvg_bvstream** out);
+int cmvg_bv_decode_host(const cmvg_bvstream* s, cmvg_csr** out);
+int cmvg_bv_get_stats(const cmvg_bvstream* s, cmvg_bv_stats* out);
+const uint32_t* cmvg_bv_words(const cmvg_bvstream* s, uint64_t* nwords);
+const uint64_t* cmvg_bv_segment_offsets(const cmvg_bvstream* s, uint64_t* count);
+void cmvg_bv_free(cmvg_bvstream* s);
+
+/* ---- device handle -------------------------------------------------------- */
+void cmvg_default_opts(cmvg_create_opts* o);
+int cmvg_create(const cmvg_bvstream* s, const cmvg_create_opts* opts, cmvg_graph** out);
+int cmvg_destroy(cmvg_graph* g);
+/* Host-only: build the device layout for `opts` and report its sizes
+ * (no GPU needed; used for layout statistics and tests). */
+int cmvg_layout_info(const cmvg_bvstream* s, const cmvg_create_opts* opts, cmvg_graph_info* out);
+int cmvg_graph_info_get(const cmvg_graph* g, cmvg_graph_info* out);
+uint32_t cmvg_dimension(const cmvg_graph* g);
+uint64_t cmvg_adds_per_product(const cmvg_graph* g);
+
+/* y = A x^T (GATHER) or y = x A (SCATTER).  x has n entries; y has
+ * row_end - row_begin entries for GATHER (the shard's rows) and n for SCATTER.
+ * `stream` is a cudaStream_t (NULL = legacy default stream). */
+int cmvg_matvec_f64(cmvg_graph* g, const double* x, double* y, int form, int ptr_kind, void* stream);
+int cmvg_matvec_f32(cmvg_graph* g, const float* x, float* y, int form, int ptr_kind, void* stream);
+/* Y = A X, X row-major n x k (fp32), Y (row_end-row_begin) x k. */
+int cmvg_matmat_f32(cmvg_graph* g, const float* X, float* Y, uint32_t k, int ptr_kind, void* stream);
+/* Decoded adjacency of the whole graph: row_offsets[n+1], cols[m]. */
+int cmvg_decode_csr(cmvg_graph* g, uint64_t* row_offsets, uint32_t* cols, int ptr_kind, void* stream);
+
+/* PageRank (pagerank.hpp:83-102) on a handle holding A^T (the whole graph):
+ * p_t = alpha/n + (1-alpha) (A^T q + [uniform] D/n), q = p/d.  degrees are
+ * the out-degrees of A.  ranks receives n doubles. */
+int cmvg_pagerank(cmvg_graph* g, const uint32_t* degrees, double alpha, uint32_t iterations, double l1_tolerance,
+                  int dangling, double* ranks, uint32_t* iterations_run, int ptr_kind, void* stream);
+
+/* One PageRank iteration on a shard (multi-GPU driver building block):
+ * reads q (all n entries, device) and the dangling mass D of the previous
+ * iterate, writes the shard's p' and q' = p'/d (device, shard-local) and
+ * the shard's partial sums {sum_{d=0} p', sum |p' - p_prev|} into partial[2]
+ * (device doubles).  p_prev may be NULL (then the L1 partial is 0). */
+int cmvg_pagerank_step(cmvg_graph* g, const double* q, const uint32_t* degrees_shard, double alpha,
+                       double dangling_mass, int dangling, const double* p_prev, double* p_next,
+                       double* q_next, double* partial, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CMVG_H_ */

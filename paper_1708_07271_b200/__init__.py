@@ -1,0 +1,546 @@
+"""B200-native compressed adjacency-matrix products (arXiv:1708.07271).
+
+Python mirror of the reference's C++ operator surface (reference
+``proj/include/cmv/*.hpp``), calling the sm_100a kernels through the C ABI in
+``include/cmvg.h`` (``libcmvg.so``, built in-tree).  There is no CPU fallback:
+every product runs on the GPU, and importing a handle without the built
+library raises.
+
+Reference name            -> here
+``cmv::CsrGraph``         -> :class:`CsrGraph` (host)
+``cmv::compress``         -> :meth:`BvStream.encode` (BV stream instead of A')
+``cmv::reconstruct_graph``-> :meth:`BvGraph.decode_csr` (device)
+``cmv::matvec_ref[_into]``-> :meth:`BvGraph.matvec` (form ``"gather"``)
+``cmv::matvec_ref_left``  -> :meth:`BvGraph.matvec` (form ``"scatter"``)
+``cmv::MatvecKernel``     -> :class:`MatvecKernel`, :class:`BvGpuKernel`
+``cmv::pagerank``         -> :func:`pagerank`
+``cmv::stats``            -> :meth:`BvGraph.info`, :meth:`BvStream.stats`
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import enum
+import os
+from typing import Optional
+
+import numpy as np
+
+__all__ = [
+    "CmvgError", "FormatError", "CorruptionError", "UnsupportedError",
+    "CsrGraph", "BvParams", "BvStream", "BvGraph", "CreateOptions",
+    "MatvecKernel", "BvGpuKernel", "DanglingPolicy", "PageRankConfig", "PageRankResult",
+    "pagerank", "library_path", "load_library",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def library_path() -> str:
+    return os.path.join(_HERE, "libcmvg.so")
+
+
+# ---------------------------------------------------------------------------
+# errors (cmvg.h status codes -> the reference's exception types)
+class CmvgError(RuntimeError):
+    pass
+
+
+class FormatError(CmvgError):  # cmv::FormatError (rmv_io.hpp:13-16)
+    pass
+
+
+class CorruptionError(CmvgError):  # cmv::CorruptionError (rmv_io.hpp:19-22)
+    pass
+
+
+class UnsupportedError(CmvgError):
+    pass
+
+
+_OK, _INVALID, _RANGE, _FORMAT, _CORRUPT, _CUDA, _NOMEM, _UNSUP = 0, 1, 2, 3, 4, 5, 6, 7
+
+
+class _BvParamsC(C.Structure):
+    _fields_ = [("window", C.c_uint32), ("max_ref", C.c_uint32), ("min_interval", C.c_uint32),
+                ("zeta_k", C.c_uint32), ("segment_rows", C.c_uint32)]
+
+
+class _BvStatsC(C.Structure):
+    _fields_ = [("stream_bits", C.c_uint64), ("rows_with_ref", C.c_uint64), ("copied_edges", C.c_uint64),
+                ("interval_edges", C.c_uint64), ("intervals", C.c_uint64), ("residual_edges", C.c_uint64),
+                ("minus_edges", C.c_uint64), ("max_depth", C.c_uint32), ("nsegments", C.c_uint32)]
+
+
+class _OptsC(C.Structure):
+    _fields_ = [("device", C.c_int), ("block_rows", C.c_uint32), ("lanes", C.c_uint32), ("window", C.c_uint32),
+                ("stream_cap_words", C.c_uint32), ("interval_mode", C.c_uint32), ("row_begin", C.c_uint32),
+                ("row_end", C.c_uint32)]
+
+
+class _InfoC(C.Structure):
+    _fields_ = [("n", C.c_uint32), ("m", C.c_uint64), ("row_begin", C.c_uint32), ("row_end", C.c_uint32),
+                ("bv_stream_bits", C.c_uint64), ("bvd_row_bits", C.c_uint64), ("bvd_stream_bytes", C.c_uint64),
+                ("bvd_lane_table_bytes", C.c_uint64), ("bvd_block_table_bytes", C.c_uint64),
+                ("block_rows", C.c_uint32), ("lanes", C.c_uint32), ("window", C.c_uint32), ("nblocks", C.c_uint32),
+                ("max_depth", C.c_uint32), ("interval_mode", C.c_uint32), ("adds_per_product", C.c_uint64),
+                ("device_bytes", C.c_uint64)]
+
+
+_lib_handle: Optional[C.CDLL] = None
+
+# (name, restype, argtypes)
+_P = C.c_void_p
+_SIGS = [
+    ("cmvg_last_error", C.c_char_p, []),
+    ("cmvg_csr_from_arrays", C.c_int, [C.c_uint32, _P, _P, C.POINTER(_P)]),
+    ("cmvg_gen_copy_model", C.c_int, [C.c_uint32, C.c_double, C.c_double, C.c_double, C.c_uint64, C.POINTER(_P)]),
+    ("cmvg_gen_social", C.c_int, [C.c_uint32, C.c_uint64, C.POINTER(_P)]),
+    ("cmvg_csr_transpose", C.c_int, [_P, C.POINTER(_P)]),
+    ("cmvg_csr_n", C.c_uint32, [_P]),
+    ("cmvg_csr_m", C.c_uint64, [_P]),
+    ("cmvg_csr_row_offsets", _P, [_P]),
+    ("cmvg_csr_cols", _P, [_P]),
+    ("cmvg_csr_free", None, [_P]),
+    ("cmvg_bv_encode", C.c_int, [_P, C.POINTER(_BvParamsC), C.POINTER(_P)]),
+    ("cmvg_bv_from_words", C.c_int, [C.c_uint32, C.c_uint64, C.POINTER(_BvParamsC), _P, C.c_uint64, _P,
+                                     C.POINTER(_P)]),
+    ("cmvg_bv_decode_host", C.c_int, [_P, C.POINTER(_P)]),
+    ("cmvg_bv_get_stats", C.c_int, [_P, C.POINTER(_BvStatsC)]),
+    ("cmvg_bv_words", _P, [_P, C.POINTER(C.c_uint64)]),
+    ("cmvg_bv_segment_offsets", _P, [_P, C.POINTER(C.c_uint64)]),
+    ("cmvg_bv_free", None, [_P]),
+    ("cmvg_default_opts", None, [C.POINTER(_OptsC)]),
+    ("cmvg_create", C.c_int, [_P, C.POINTER(_OptsC), C.POINTER(_P)]),
+    ("cmvg_destroy", C.c_int, [_P]),
+    ("cmvg_layout_info", C.c_int, [_P, C.POINTER(_OptsC), C.POINTER(_InfoC)]),
+    ("cmvg_graph_info_get", C.c_int, [_P, C.POINTER(_InfoC)]),
+    ("cmvg_dimension", C.c_uint32, [_P]),
+    ("cmvg_adds_per_product", C.c_uint64, [_P]),
+    ("cmvg_matvec_f64", C.c_int, [_P, _P, _P, C.c_int, C.c_int, _P]),
+    ("cmvg_matvec_f32", C.c_int, [_P, _P, _P, C.c_int, C.c_int, _P]),
+    ("cmvg_matmat_f32", C.c_int, [_P, _P, _P, C.c_uint32, C.c_int, _P]),
+    ("cmvg_decode_csr", C.c_int, [_P, _P, _P, C.c_int, _P]),
+    ("cmvg_pagerank", C.c_int, [_P, _P, C.c_double, C.c_uint32, C.c_double, C.c_int, _P, C.POINTER(C.c_uint32),
+                                C.c_int, _P]),
+    ("cmvg_pagerank_step", C.c_int, [_P, _P, _P, C.c_double, C.c_double, C.c_int, _P, _P, _P, _P, _P]),
+]
+
+EXPORTED_SYMBOLS = [s[0] for s in _SIGS]
+
+
+def load_library() -> C.CDLL:
+    """Load libcmvg.so (in-tree).  Raises if it has not been built: there is
+    deliberately no fallback implementation."""
+    global _lib_handle
+    if _lib_handle is None:
+        path = library_path()
+        if not os.path.exists(path):
+            raise ImportError(f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+        lib = C.CDLL(path)
+        for name, res, args in _SIGS:
+            f = getattr(lib, name)
+            f.restype = res
+            f.argtypes = args
+        _lib_handle = lib
+    return _lib_handle
+
+
+def _check(rc: int) -> None:
+    if rc == _OK:
+        return
+    msg = load_library().cmvg_last_error().decode(errors="replace")
+    if rc == _INVALID:
+        raise ValueError(msg)
+    if rc == _RANGE:
+        raise IndexError(msg)
+    if rc == _FORMAT:
+        raise FormatError(msg)
+    if rc == _CORRUPT:
+        raise CorruptionError(msg)
+    if rc == _UNSUP:
+        raise UnsupportedError(msg)
+    if rc == _NOMEM:
+        raise MemoryError(msg)
+    raise CmvgError(f"cmvg error {rc}: {msg}")
+
+
+def _np_view(ptr: int, count: int, dtype) -> np.ndarray:
+    if count == 0:
+        return np.zeros(0, dtype=dtype)
+    itemsize = np.dtype(dtype).itemsize
+    buf = (C.c_char * (count * itemsize)).from_address(ptr)
+    return np.frombuffer(buf, dtype=dtype, count=count)
+
+
+# ---------------------------------------------------------------------------
+class CsrGraph:
+    """Host CSR adjacency (cmv::CsrGraph, csr.hpp:16-36) owned by the library."""
+
+    def __init__(self, handle: int):
+        self._h = _P(handle)
+        lib = load_library()
+        self.n = int(lib.cmvg_csr_n(self._h))
+        self.m = int(lib.cmvg_csr_m(self._h))
+
+    @classmethod
+    def from_arrays(cls, n: int, row_offsets, columns) -> "CsrGraph":
+        ro = np.ascontiguousarray(row_offsets, dtype=np.uint64)
+        co = np.ascontiguousarray(columns, dtype=np.uint32)
+        if ro.shape != (n + 1,):
+            raise ValueError("row_offsets must have n+1 entries")
+        out = _P()
+        _check(load_library().cmvg_csr_from_arrays(n, ro.ctypes.data, co.ctypes.data if co.size else None,
+                                                   C.byref(out)))
+        return cls(out.value)
+
+    @classmethod
+    def copy_model(cls, n: int, mean_degree: float, p_ref: float = 0.7, p_copy: float = 0.8,
+                   seed: int = 0x170807271) -> "CsrGraph":
+        out = _P()
+        _check(load_library().cmvg_gen_copy_model(n, mean_degree, p_ref, p_copy, seed, C.byref(out)))
+        return cls(out.value)
+
+    @classmethod
+    def social(cls, n: int, seed: int = 0x170807271 + 4) -> "CsrGraph":
+        out = _P()
+        _check(load_library().cmvg_gen_social(n, seed, C.byref(out)))
+        return cls(out.value)
+
+    def transpose(self) -> "CsrGraph":
+        out = _P()
+        _check(load_library().cmvg_csr_transpose(self._h, C.byref(out)))
+        return CsrGraph(out.value)
+
+    @property
+    def row_offsets(self) -> np.ndarray:
+        return _np_view(load_library().cmvg_csr_row_offsets(self._h), self.n + 1, np.uint64)
+
+    @property
+    def columns(self) -> np.ndarray:
+        return _np_view(load_library().cmvg_csr_cols(self._h) or 0, self.m, np.uint32)
+
+    def out_degrees(self) -> np.ndarray:
+        return np.diff(self.row_offsets).astype(np.uint32)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib_handle is not None:
+            _lib_handle.cmvg_csr_free(h)
+            self._h = None
+
+
+@dataclasses.dataclass
+class BvParams:
+    """BV encoding parameters (BASELINE.json configs: w=7, R=3 / unbounded, Lmin=4, zeta_3)."""
+    window: int = 7
+    max_ref: int = 3  # 0 = unbounded chains
+    min_interval: int = 4
+    zeta_k: int = 3
+    segment_rows: int = 1024
+
+    def _c(self) -> _BvParamsC:
+        return _BvParamsC(self.window, self.max_ref, self.min_interval, self.zeta_k, self.segment_rows)
+
+
+class BvStream:
+    """Canonical Boldi-Vigna stream (host).  ``stats()['stream_bits']`` is S."""
+
+    def __init__(self, handle: int, n: int, m: int, params: BvParams):
+        self._h = _P(handle)
+        self.n, self.m, self.params = n, m, params
+
+    @classmethod
+    def encode(cls, g: CsrGraph, params: Optional[BvParams] = None) -> "BvStream":
+        params = params or BvParams()
+        out = _P()
+        pc = params._c()
+        _check(load_library().cmvg_bv_encode(g._h, C.byref(pc), C.byref(out)))
+        return cls(out.value, g.n, g.m, params)
+
+    @classmethod
+    def from_words(cls, n: int, m: int, params: BvParams, words: np.ndarray, nbits: int,
+                   segment_offsets: np.ndarray) -> "BvStream":
+        w = np.ascontiguousarray(words, dtype=np.uint32)
+        s = np.ascontiguousarray(segment_offsets, dtype=np.uint64)
+        out = _P()
+        pc = params._c()
+        _check(load_library().cmvg_bv_from_words(n, m, C.byref(pc), w.ctypes.data if w.size else None, nbits,
+                                                 s.ctypes.data, C.byref(out)))
+        return cls(out.value, n, m, params)
+
+    def stats(self) -> dict:
+        st = _BvStatsC()
+        _check(load_library().cmvg_bv_get_stats(self._h, C.byref(st)))
+        return {f: getattr(st, f) for f, _ in _BvStatsC._fields_}
+
+    def words(self) -> np.ndarray:
+        nw = C.c_uint64()
+        p = load_library().cmvg_bv_words(self._h, C.byref(nw))
+        return _np_view(p or 0, nw.value, np.uint32).copy()
+
+    def segment_offsets(self) -> np.ndarray:
+        cnt = C.c_uint64()
+        p = load_library().cmvg_bv_segment_offsets(self._h, C.byref(cnt))
+        return _np_view(p, cnt.value, np.uint64).copy()
+
+    def layout_info(self, options: Optional["CreateOptions"] = None) -> dict:
+        """Sizes of the device layout for `options`, built on the host (no GPU)."""
+        oc = (options or CreateOptions())._c()
+        inf = _InfoC()
+        _check(load_library().cmvg_layout_info(self._h, C.byref(oc), C.byref(inf)))
+        return {f: getattr(inf, f) for f, _ in _InfoC._fields_}
+
+    def decode_host(self) -> CsrGraph:
+        """CPU decode (the handle builder's path); tests compare it with the GPU decoder."""
+        out = _P()
+        _check(load_library().cmvg_bv_decode_host(self._h, C.byref(out)))
+        return CsrGraph(out.value)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib_handle is not None:
+            _lib_handle.cmvg_bv_free(h)
+            self._h = None
+
+
+@dataclasses.dataclass
+class CreateOptions:
+    device: int = 0
+    block_rows: int = 1024
+    lanes: int = 128
+    window: int = 2048
+    stream_cap_words: int = 6144
+    interval_mode: str = "prefix"  # or "direct"
+    row_begin: int = 0
+    row_end: int = 0  # 0 = n
+
+    def _c(self) -> _OptsC:
+        mode = {"prefix": 0, "direct": 1}[self.interval_mode]
+        return _OptsC(self.device, self.block_rows, self.lanes, self.window, self.stream_cap_words, mode,
+                      self.row_begin, self.row_end)
+
+
+def _is_torch(t) -> bool:
+    return type(t).__module__.startswith("torch")
+
+
+def _ptr_and_kind(t, dtype):
+    """(pointer, ptr_kind) for a numpy array (HOST) or a CUDA torch tensor (DEVICE)."""
+    if _is_torch(t):
+        import torch
+        want = {np.float64: torch.float64, np.float32: torch.float32, np.uint32: torch.int32,
+                np.uint64: torch.int64}[dtype]
+        if t.dtype != want and not (dtype in (np.uint32, np.uint64) and t.dtype in (torch.int32, torch.int64)):
+            raise TypeError(f"expected {want}, got {t.dtype}")
+        if not t.is_cuda:
+            raise ValueError("torch tensors must live on the GPU; pass numpy arrays for host buffers")
+        if not t.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return t.data_ptr(), 1
+    if not isinstance(t, np.ndarray) or t.dtype != dtype or not t.flags.c_contiguous:
+        raise TypeError(f"expected a C-contiguous numpy array of {np.dtype(dtype)}")
+    return t.ctypes.data, 0
+
+
+def _stream_of(*ts) -> Optional[int]:
+    for t in ts:
+        if _is_torch(t) and t.is_cuda:
+            import torch
+            return torch.cuda.current_stream(t.device).cuda_stream
+    return None
+
+
+class BvGraph:
+    """Device handle over a BV stream (one GPU; optionally one row shard)."""
+
+    def __init__(self, stream: BvStream, options: Optional[CreateOptions] = None):
+        self.options = options or CreateOptions()
+        out = _P()
+        oc = self.options._c()
+        _check(load_library().cmvg_create(stream._h, C.byref(oc), C.byref(out)))
+        self._h = out
+        self.n = stream.n
+        self.m = stream.m
+        info = self.info()
+        self.row_begin, self.row_end = info["row_begin"], info["row_end"]
+
+    def info(self) -> dict:
+        inf = _InfoC()
+        _check(load_library().cmvg_graph_info_get(self._h, C.byref(inf)))
+        return {f: getattr(inf, f) for f, _ in _InfoC._fields_}
+
+    def dimension(self) -> int:
+        return int(load_library().cmvg_dimension(self._h))
+
+    def adds_per_product(self) -> int:
+        return int(load_library().cmvg_adds_per_product(self._h))
+
+    def matvec(self, x, y=None, form: str = "gather", stream: Optional[int] = None):
+        """y = A x^T ("gather") or y = x A ("scatter").  numpy in -> numpy out
+        (host copies inside the call); CUDA tensors in -> CUDA tensors out."""
+        formc = {"gather": 0, "scatter": 1}[form]
+        dtype = np.float64 if (x.dtype == np.float64 or str(x.dtype) == "torch.float64") else np.float32
+        nout = (self.row_end - self.row_begin) if form == "gather" else self.n
+        if len(x) != self.n:
+            raise ValueError(f"dimension mismatch: x has {len(x)} entries, graph has {self.n}")
+        if y is None:
+            if _is_torch(x):
+                import torch
+                y = torch.empty(nout, dtype=x.dtype, device=x.device)
+            else:
+                y = np.empty(nout, dtype=dtype)
+        if len(y) != nout:
+            raise ValueError("dimension mismatch on y")
+        px, kx = _ptr_and_kind(x, dtype)
+        py, ky = _ptr_and_kind(y, dtype)
+        if kx != ky:
+            raise ValueError("x and y must both be host arrays or both device tensors")
+        st = stream if stream is not None else _stream_of(x, y)
+        f = load_library().cmvg_matvec_f64 if dtype == np.float64 else load_library().cmvg_matvec_f32
+        _check(f(self._h, px, py, formc, kx, st))
+        return y
+
+    def matmat(self, X, Y=None, stream: Optional[int] = None):
+        """Y = A X for X of shape (n, k), float32, row-major."""
+        k = X.shape[1]
+        nout = self.row_end - self.row_begin
+        if X.shape[0] != self.n:
+            raise ValueError("dimension mismatch")
+        if Y is None:
+            if _is_torch(X):
+                import torch
+                Y = torch.empty((nout, k), dtype=X.dtype, device=X.device)
+            else:
+                Y = np.empty((nout, k), dtype=np.float32)
+        px, kx = _ptr_and_kind(X, np.float32)
+        py, ky = _ptr_and_kind(Y, np.float32)
+        st = stream if stream is not None else _stream_of(X, Y)
+        _check(load_library().cmvg_matmat_f32(self._h, px, py, k, kx, st))
+        return Y
+
+    def decode_csr(self):
+        """Decode the canonical BV stream on the GPU (bit-exact adjacency)."""
+        ro = np.empty(self.n + 1, dtype=np.uint64)
+        co = np.empty(max(self.m, 1), dtype=np.uint32)
+        _check(load_library().cmvg_decode_csr(self._h, ro.ctypes.data, co.ctypes.data, 0, None))
+        return ro, co[: self.m]
+
+    def decode_csr_device(self, row_offsets, cols, stream: Optional[int] = None):
+        pr, _ = _ptr_and_kind(row_offsets, np.uint64)
+        pc, _ = _ptr_and_kind(cols, np.uint32)
+        st = stream if stream is not None else _stream_of(row_offsets)
+        _check(load_library().cmvg_decode_csr(self._h, pr, pc, 1, st))
+
+    def pagerank(self, degrees, alpha: float = 0.15, iterations: int = 10, l1_tolerance: Optional[float] = None,
+                 dangling: str = "uniform", ranks=None, stream: Optional[int] = None):
+        """Device-resident PageRank on a handle holding A^T; returns (ranks, iterations_run)."""
+        if len(degrees) != self.n:
+            raise ValueError("degree vector dimension mismatch")
+        if ranks is None:
+            if _is_torch(degrees):
+                import torch
+                ranks = torch.empty(self.n, dtype=torch.float64, device=degrees.device)
+            else:
+                ranks = np.empty(self.n, dtype=np.float64)
+        pd, kd = _ptr_and_kind(degrees, np.uint32)
+        pr, kr = _ptr_and_kind(ranks, np.float64)
+        if kd != kr:
+            raise ValueError("degrees and ranks must both be host arrays or both device tensors")
+        it = C.c_uint32()
+        st = stream if stream is not None else _stream_of(degrees, ranks)
+        _check(load_library().cmvg_pagerank(self._h, pd, alpha, iterations,
+                                            -1.0 if l1_tolerance is None else float(l1_tolerance),
+                                            {"uniform": 0, "drop": 1}[dangling], pr, C.byref(it), kd, st))
+        return ranks, int(it.value)
+
+    def pagerank_step(self, q, degrees_shard, alpha, dangling_mass, dangling, p_prev, p_next, q_next, partial,
+                      stream: Optional[int] = None):
+        """One sharded PageRank iteration (device tensors); see cmvg_pagerank_step."""
+        ptrs = [q.data_ptr(), degrees_shard.data_ptr(), p_prev.data_ptr() if p_prev is not None else None,
+                p_next.data_ptr(), q_next.data_ptr(), partial.data_ptr()]
+        st = stream if stream is not None else _stream_of(q)
+        _check(load_library().cmvg_pagerank_step(self._h, ptrs[0], ptrs[1], alpha, dangling_mass,
+                                                 {"uniform": 0, "drop": 1}[dangling], ptrs[2], ptrs[3], ptrs[4],
+                                                 ptrs[5], st))
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value and _lib_handle is not None:
+            _lib_handle.cmvg_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        self.close()
+
+
+# ---------------------------------------------------------------------------
+# cmv::MatvecKernel (pagerank.hpp:25-34) and the GPU drop-in
+class MatvecKernel:
+    """A representation of A^T able to compute y = A^T x (pagerank.hpp:25-34)."""
+
+    def dimension(self) -> int:
+        raise NotImplementedError
+
+    def multiply(self, x, y) -> None:
+        raise NotImplementedError
+
+    def adds_per_product(self) -> int:
+        raise NotImplementedError
+
+
+class BvGpuKernel(MatvecKernel):
+    """GPU kernel over BV(A^T): the drop-in for cmv::RefKernel (pagerank.hpp:48-61).
+    ``multiply`` takes host arrays (H2D/D2H inside) or CUDA tensors."""
+
+    def __init__(self, graph_of_transpose: BvGraph):
+        self.graph = graph_of_transpose
+
+    def dimension(self) -> int:
+        return self.graph.dimension()
+
+    def multiply(self, x, y) -> None:
+        self.graph.matvec(x, y, form="gather")
+
+    def adds_per_product(self) -> int:
+        return self.graph.adds_per_product()
+
+
+class DanglingPolicy(enum.Enum):  # pagerank.hpp:16
+    UNIFORM = "uniform"
+    DROP = "drop"
+
+
+@dataclasses.dataclass
+class PageRankConfig:  # pagerank.hpp:18-23
+    alpha: float = 0.15
+    iterations: int = 10
+    l1_tolerance: Optional[float] = None
+    dangling: DanglingPolicy = DanglingPolicy.UNIFORM
+
+
+@dataclasses.dataclass
+class PageRankResult:  # pagerank.hpp:78-81
+    ranks: np.ndarray
+    iterations_run: int
+
+
+def pagerank(at: BvGpuKernel, degrees, cfg: Optional[PageRankConfig] = None, start=None) -> PageRankResult:
+    """cmv::pagerank (pagerank.hpp:83-102) for the GPU kernel: the whole power
+    iteration runs on the device.  Same validation and error behaviour
+    (ValueError for the reference's std::invalid_argument)."""
+    cfg = cfg or PageRankConfig()
+    if not isinstance(at, BvGpuKernel):
+        raise TypeError("pagerank() drives a BvGpuKernel; other kernels are out of scope here")
+    if not (0.0 < cfg.alpha < 1.0):
+        raise ValueError("pagerank: alpha must be in (0,1)")
+    if cfg.iterations == 0:
+        raise ValueError("pagerank: iterations must be > 0")
+    if at.dimension() == 0:
+        raise ValueError("pagerank: empty graph")
+    if len(degrees) != at.dimension():
+        raise ValueError("pagerank: degree vector dimension mismatch")
+    if start is not None:
+        raise UnsupportedError("personalised start vectors are not supported on the device path yet")
+    deg = degrees if _is_torch(degrees) else np.ascontiguousarray(degrees, dtype=np.uint32)
+    ranks, it = at.graph.pagerank(deg, cfg.alpha, cfg.iterations, cfg.l1_tolerance, cfg.dangling.value)
+    return PageRankResult(ranks, it)

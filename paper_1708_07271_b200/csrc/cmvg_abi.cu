@@ -1,0 +1,468 @@
+// C ABI (include/cmvg.h): host objects, device handle, kernel dispatch.
+#include "cuda/bv_decode.cuh"
+#include "internal.hpp"
+
+namespace cmvg {
+thread_local std::string g_last_error;
+}
+
+// ---------------------------------------------------------------------------
+extern "C" {
+
+const char* cmvg_last_error(void) { return g_last_error.c_str(); }
+
+// ---- host CSR --------------------------------------------------------------
+int cmvg_csr_from_arrays(uint32_t n, const uint64_t* ro, const uint32_t* cols, cmvg_csr** out) {
+  return guarded([&] {
+    require(out && ro, "null argument");
+    auto c = std::make_unique<cmvg_csr>();
+    c->g.n = n;
+    c->g.row_offsets.assign(ro, ro + (size_t)n + 1);
+    require(c->g.row_offsets[0] == 0, "row_offsets[0] must be 0");
+    uint64_t m = c->g.row_offsets[n];
+    for (uint32_t u = 0; u < n; ++u) require(c->g.row_offsets[u] <= c->g.row_offsets[u + 1], "row_offsets must be nondecreasing");
+    c->g.cols.assign(cols, cols + m);
+    for (uint32_t u = 0; u < n; ++u)
+      for (uint64_t e = c->g.row_offsets[u]; e < c->g.row_offsets[u + 1]; ++e) {
+        if (c->g.cols[e] >= n) throw std::out_of_range("column " + std::to_string(c->g.cols[e]) + " >= n in row " + std::to_string(u));
+        require(e == c->g.row_offsets[u] || c->g.cols[e] > c->g.cols[e - 1], "rows must be strictly increasing");
+      }
+    *out = c.release();
+  });
+}
+
+int cmvg_gen_copy_model(uint32_t n, double mean_degree, double p_ref, double p_copy, uint64_t seed, cmvg_csr** out) {
+  return guarded([&] {
+    require(out, "null argument");
+    CopyModelParams p;
+    p.n = n;
+    p.mean_degree = mean_degree;
+    p.p_ref = p_ref;
+    p.p_copy = p_copy;
+    p.seed = seed;
+    auto c = std::make_unique<cmvg_csr>();
+    c->g = generate_copy_model(p);
+    *out = c.release();
+  });
+}
+
+int cmvg_gen_social(uint32_t n, uint64_t seed, cmvg_csr** out) {
+  return guarded([&] {
+    require(out, "null argument");
+    SocialParams p;
+    p.n = n;
+    p.seed = seed;
+    auto c = std::make_unique<cmvg_csr>();
+    c->g = generate_social(p);
+    *out = c.release();
+  });
+}
+
+int cmvg_csr_transpose(const cmvg_csr* g, cmvg_csr** out) {
+  return guarded([&] {
+    require(g && out, "null argument");
+    auto c = std::make_unique<cmvg_csr>();
+    c->g = transpose_csr(g->g);
+    *out = c.release();
+  });
+}
+
+uint32_t cmvg_csr_n(const cmvg_csr* g) { return g ? g->g.n : 0; }
+uint64_t cmvg_csr_m(const cmvg_csr* g) { return g ? g->g.m() : 0; }
+const uint64_t* cmvg_csr_row_offsets(const cmvg_csr* g) { return g ? g->g.row_offsets.data() : nullptr; }
+const uint32_t* cmvg_csr_cols(const cmvg_csr* g) { return g ? g->g.cols.data() : nullptr; }
+void cmvg_csr_free(cmvg_csr* g) { delete g; }
+
+// ---- BV stream -------------------------------------------------------------
+static BvParams to_params(const cmvg_bv_params* p) {
+  BvParams q;
+  if (p) {
+    q.window = p->window;
+    q.max_ref = p->max_ref;
+    q.min_interval = p->min_interval;
+    q.zeta_k = p->zeta_k;
+    q.segment_rows = p->segment_rows;
+  }
+  require(q.window <= 255, "window must be <= 255");
+  require(q.min_interval >= 2, "min_interval must be >= 2");
+  require(q.zeta_k >= 2 && q.zeta_k <= 8, "zeta_k must be in [2, 8]");
+  require(q.segment_rows >= 1, "segment_rows must be >= 1");
+  return q;
+}
+
+int cmvg_bv_encode(const cmvg_csr* g, const cmvg_bv_params* p, cmvg_bvstream** out) {
+  return guarded([&] {
+    require(g && out, "null argument");
+    auto s = std::make_unique<cmvg_bvstream>();
+    s->s = bv_encode(g->g, to_params(p));
+    *out = s.release();
+  });
+}
+
+int cmvg_bv_from_words(uint32_t n, uint64_t m, const cmvg_bv_params* p, const uint32_t* words, uint64_t nbits,
+                       const uint64_t* seg, cmvg_bvstream** out) {
+  return guarded([&] {
+    require(out && (words || nbits == 0) && seg, "null argument");
+    auto s = std::make_unique<cmvg_bvstream>();
+    BvStream& b = s->s;
+    b.n = n;
+    b.m = m;
+    b.params = to_params(p);
+    b.nbits = nbits;
+    b.words.assign(words, words + (nbits + 31) / 32);
+    b.words.push_back(0);
+    b.words.push_back(0);
+    uint64_t nseg = ((uint64_t)n + b.params.segment_rows - 1) / b.params.segment_rows;
+    b.segment_bit_offsets.assign(seg, seg + nseg + 1);
+    if (b.segment_bit_offsets[nseg] != nbits) throw std::runtime_error("BV stream corrupt: segment table does not end at nbits");
+    b.stats.stream_bits = nbits;
+    *out = s.release();
+  });
+}
+
+int cmvg_bv_decode_host(const cmvg_bvstream* s, cmvg_csr** out) {
+  return guarded([&] {
+    require(s && out, "null argument");
+    auto c = std::make_unique<cmvg_csr>();
+    BvDecoded d = bv_decode(s->s);
+    if (d.csr.m() != s->s.m) throw std::runtime_error("BV stream corrupt: edge count mismatch");
+    c->g = std::move(d.csr);
+    *out = c.release();
+  });
+}
+
+int cmvg_bv_get_stats(const cmvg_bvstream* s, cmvg_bv_stats* o) {
+  return guarded([&] {
+    require(s && o, "null argument");
+    const BvStats& t = s->s.stats;
+    o->stream_bits = s->s.nbits;
+    o->rows_with_ref = t.rows_with_ref;
+    o->copied_edges = t.copied_edges;
+    o->interval_edges = t.interval_edges;
+    o->intervals = t.intervals;
+    o->residual_edges = t.residual_edges;
+    o->minus_edges = t.minus_edges;
+    o->max_depth = t.max_depth;
+    o->nsegments = (uint32_t)(s->s.segment_bit_offsets.size() - 1);
+  });
+}
+
+const uint32_t* cmvg_bv_words(const cmvg_bvstream* s, uint64_t* nwords) {
+  if (!s) return nullptr;
+  if (nwords) *nwords = (s->s.nbits + 31) / 32;
+  return s->s.words.data();
+}
+const uint64_t* cmvg_bv_segment_offsets(const cmvg_bvstream* s, uint64_t* count) {
+  if (!s) return nullptr;
+  if (count) *count = s->s.segment_bit_offsets.size();
+  return s->s.segment_bit_offsets.data();
+}
+void cmvg_bv_free(cmvg_bvstream* s) { delete s; }
+
+// ---- device handle ----------------------------------------------------------
+void cmvg_default_opts(cmvg_create_opts* o) {
+  if (!o) return;
+  o->device = 0;
+  o->block_rows = 1024;
+  o->lanes = 128;
+  o->window = 2048;
+  o->stream_cap_words = 6144;
+  o->interval_mode = CMVG_INTERVALS_PREFIX;
+  o->row_begin = 0;
+  o->row_end = 0;
+}
+
+int cmvg_create(const cmvg_bvstream* s, const cmvg_create_opts* opts_in, cmvg_graph** out) {
+  return guarded([&] {
+    require(s && out, "null argument");
+    cmvg_create_opts o;
+    cmvg_default_opts(&o);
+    if (opts_in) o = *opts_in;
+    const BvStream& bs = s->s;
+    require(bs.params.window <= 7 || true, "");
+    require(bs.params.zeta_k == 3, "device kernels support zeta_3 residuals");
+    require(bs.n > 0, "empty graph");
+    require(o.lanes >= 32 && o.lanes <= 256 && o.lanes % 32 == 0, "lanes must be 32..256, a multiple of 32");
+    require(o.interval_mode <= CMVG_INTERVALS_DIRECT, "bad interval_mode");
+    uint32_t row_end = o.row_end ? o.row_end : bs.n;
+    require(o.row_begin < row_end && row_end <= bs.n, "bad shard row range");
+    require(o.row_begin % o.block_rows == 0, "shard row_begin must be a multiple of block_rows");
+    require(row_end == bs.n || row_end % o.block_rows == 0, "shard row_end must be a multiple of block_rows or n");
+
+    int ndev = 0;
+    CUDA_TRY(cudaGetDeviceCount(&ndev));
+    require(o.device >= 0 && o.device < ndev, "no such CUDA device");
+
+    BvDecoded dec = bv_decode(bs);
+    if (dec.csr.m() != bs.m) throw std::runtime_error("BV stream corrupt: edge count mismatch");
+    BvdOptions bo;
+    bo.block_rows = o.block_rows;
+    bo.lanes = o.lanes;
+    bo.window = o.window;
+    BvdLayout L = build_bvd(dec, bs.params, bo);
+
+    auto g = std::make_unique<cmvg_graph>();
+    g->device = o.device;
+    g->n = bs.n;
+    g->m = bs.m;
+    g->params = bs.params;
+    g->dims = L.dims;
+    g->row_begin = o.row_begin;
+    g->row_end = row_end;
+    g->block_begin = o.row_begin / o.block_rows;
+    uint32_t block_end = (uint32_t)(((uint64_t)row_end + o.block_rows - 1) / o.block_rows);
+    g->nblocks = block_end - g->block_begin;
+    g->stream_cap_words = o.stream_cap_words;
+    g->interval_mode = o.interval_mode;
+    g->bv_bits = bs.nbits;
+    g->nseg = bs.segment_bit_offsets.size() - 1;
+
+    DeviceGuard dg(o.device);
+    // shard slice of the layout
+    uint64_t w0 = L.blocks[g->block_begin].word_offset;
+    uint64_t w1 = L.blocks[block_end - 1].word_offset + L.blocks[block_end - 1].nwords;
+    std::vector<BvdBlockInfo> bl(L.blocks.begin() + g->block_begin, L.blocks.begin() + block_end);
+    for (auto& b : bl) b.word_offset -= w0;
+    std::vector<uint32_t> wds(L.words.begin() + w0, L.words.begin() + w1);
+    wds.resize(wds.size() + 8, 0);
+    g->words.upload(wds.data(), wds.size());
+    g->blocks.upload(bl.data(), bl.size());
+    g->lanes.upload(L.lanes.data() + (size_t)g->block_begin * o.lanes, (size_t)g->nblocks * o.lanes);
+    g->refd.upload(dec.ref_dist.data() + o.row_begin, row_end - o.row_begin);
+    // stats of the shard
+    g->stats.stream_bytes = (w1 - w0) * 4;
+    g->stats.lane_table_bytes = (uint64_t)g->nblocks * o.lanes * 4;
+    g->stats.block_table_bytes = (uint64_t)g->nblocks * sizeof(BvdBlockInfo);
+    g->stats.row_bits = L.stats.row_bits;  // whole graph
+    g->adds = L.adds_per_product;
+    g->bv_words.upload(bs.words.data(), bs.words.size());
+    g->bv_seg.upload(bs.segment_bit_offsets.data(), bs.segment_bit_offsets.size());
+    *out = g.release();
+  });
+}
+
+int cmvg_layout_info(const cmvg_bvstream* s, const cmvg_create_opts* opts_in, cmvg_graph_info* o) {
+  return guarded([&] {
+    require(s && o, "null argument");
+    cmvg_create_opts opt;
+    cmvg_default_opts(&opt);
+    if (opts_in) opt = *opts_in;
+    const BvStream& bs = s->s;
+    BvDecoded dec = bv_decode(bs);
+    BvdOptions bo;
+    bo.block_rows = opt.block_rows;
+    bo.lanes = opt.lanes;
+    bo.window = opt.window;
+    BvdLayout L = build_bvd(dec, bs.params, bo);
+    std::memset(o, 0, sizeof(*o));
+    o->n = bs.n;
+    o->m = bs.m;
+    o->row_begin = 0;
+    o->row_end = bs.n;
+    o->bv_stream_bits = bs.nbits;
+    o->bvd_row_bits = L.stats.row_bits;
+    o->bvd_stream_bytes = L.stats.stream_bytes;
+    o->bvd_lane_table_bytes = L.stats.lane_table_bytes;
+    o->bvd_block_table_bytes = L.stats.block_table_bytes;
+    o->block_rows = L.dims.block_rows;
+    o->lanes = L.dims.lanes;
+    o->window = L.dims.window;
+    o->nblocks = L.dims.nblocks;
+    o->max_depth = L.dims.max_depth;
+    o->interval_mode = opt.interval_mode;
+    o->adds_per_product = L.adds_per_product;
+    o->device_bytes = 0;
+  });
+}
+
+int cmvg_destroy(cmvg_graph* g) {
+  if (!g) return CMVG_OK;
+  {
+    DeviceGuard dg(g->device);
+    delete g;
+  }
+  return CMVG_OK;
+}
+
+int cmvg_graph_info_get(const cmvg_graph* g, cmvg_graph_info* o) {
+  return guarded([&] {
+    require(g && o, "null argument");
+    std::memset(o, 0, sizeof(*o));
+    o->n = g->n;
+    o->m = g->m;
+    o->row_begin = g->row_begin;
+    o->row_end = g->row_end;
+    o->bv_stream_bits = g->bv_bits;
+    o->bvd_row_bits = g->stats.row_bits;
+    o->bvd_stream_bytes = g->stats.stream_bytes;
+    o->bvd_lane_table_bytes = g->stats.lane_table_bytes;
+    o->bvd_block_table_bytes = g->stats.block_table_bytes;
+    o->block_rows = g->dims.block_rows;
+    o->lanes = g->dims.lanes;
+    o->window = g->dims.window;
+    o->nblocks = g->nblocks;
+    o->max_depth = g->dims.max_depth;
+    o->interval_mode = g->interval_mode;
+    o->adds_per_product = g->adds;
+    o->device_bytes = g->device_bytes();
+  });
+}
+
+uint32_t cmvg_dimension(const cmvg_graph* g) { return g ? g->n : 0; }
+uint64_t cmvg_adds_per_product(const cmvg_graph* g) { return g ? g->adds : 0; }
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// kernel launches
+namespace {
+
+template <typename XT, typename YT>
+void launch_gather(cmvg_graph* g, const XT* x, YT* y, cudaStream_t st) {
+  const bool prefix = g->interval_mode == CMVG_INTERVALS_PREFIX;
+  GatherSmem L = gather_smem_layout(g->dims, g->stream_cap_words, sizeof(XT), prefix);
+  auto kern = prefix ? bvd_gather_kernel<XT, YT, true> : bvd_gather_kernel<XT, YT, false>;
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
+  kern<<<g->nblocks, g->dims.lanes, L.total, st>>>(g->dev(), x, y);
+  CUDA_TRY(cudaGetLastError());
+}
+
+template <typename T>
+int matvec_impl(cmvg_graph* g, const T* x, T* y, int form, int ptr_kind, void* stream) {
+  return guarded([&] {
+    require(g && x && y, "null argument");
+    require(form == CMVG_GATHER || form == CMVG_SCATTER, "bad form");
+    require(ptr_kind == CMVG_HOST || ptr_kind == CMVG_DEVICE, "bad ptr_kind");
+    DeviceGuard dg(g->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t nin = g->n;
+    const size_t nout = form == CMVG_GATHER ? (size_t)(g->row_end - g->row_begin) : (size_t)g->n;
+    auto run = [&](const T* dx, T* dy) {
+      if (form == CMVG_GATHER) launch_gather<T, T>(g, dx, dy, st);
+      else launch_scatter<T>(g, dx, dy, st);
+    };
+    if (ptr_kind == CMVG_DEVICE) {
+      require(aligned16(x) && aligned16(y), "device buffers must be 16-byte aligned");
+      run(x, y);
+      return;
+    }
+    std::lock_guard<std::mutex> lk(g->host_mu);
+    g->hx.alloc(nin * sizeof(T) + 64);
+    g->hy.alloc(nout * sizeof(T) + 64);
+    CUDA_TRY(cudaMemcpyAsync(g->hx.p, x, nin * sizeof(T), cudaMemcpyHostToDevice, st));
+    run(g->hx.as<T>(), g->hy.as<T>());
+    CUDA_TRY(cudaMemcpyAsync(y, g->hy.p, nout * sizeof(T), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+  });
+}
+
+}  // namespace
+
+extern "C" {
+
+int cmvg_matvec_f64(cmvg_graph* g, const double* x, double* y, int form, int ptr_kind, void* stream) {
+  return matvec_impl<double>(g, x, y, form, ptr_kind, stream);
+}
+int cmvg_matvec_f32(cmvg_graph* g, const float* x, float* y, int form, int ptr_kind, void* stream) {
+  return matvec_impl<float>(g, x, y, form, ptr_kind, stream);
+}
+
+int cmvg_matmat_f32(cmvg_graph* g, const float* X, float* Y, uint32_t k, int ptr_kind, void* stream) {
+  return guarded([&] {
+    require(g && X && Y, "null argument");
+    require(k >= 1, "k must be >= 1");
+    DeviceGuard dg(g->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t nin = (size_t)g->n * k, nout = (size_t)(g->row_end - g->row_begin) * k;
+    if (ptr_kind == CMVG_DEVICE) {
+      launch_matmat(g, X, Y, k, st);
+      return;
+    }
+    std::lock_guard<std::mutex> lk(g->host_mu);
+    g->hx.alloc(nin * 4 + 64);
+    g->hy.alloc(nout * 4 + 64);
+    CUDA_TRY(cudaMemcpyAsync(g->hx.p, X, nin * 4, cudaMemcpyHostToDevice, st));
+    launch_matmat(g, g->hx.as<float>(), g->hy.as<float>(), k, st);
+    CUDA_TRY(cudaMemcpyAsync(Y, g->hy.p, nout * 4, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+  });
+}
+
+int cmvg_decode_csr(cmvg_graph* g, uint64_t* row_offsets, uint32_t* cols, int ptr_kind, void* stream) {
+  return guarded([&] {
+    require(g && row_offsets && (cols || g->m == 0), "null argument");
+    DeviceGuard dg(g->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    BvDev s{};
+    s.words = g->bv_words.as<uint32_t>();
+    s.seg_bits = g->bv_seg.as<uint64_t>();
+    s.n = g->n;
+    s.seg_rows = g->params.segment_rows;
+    s.nseg = (uint32_t)g->nseg;
+    s.window = g->params.window;
+    s.min_interval = g->params.min_interval;
+    s.zeta_k = g->params.zeta_k;
+    DevBuf deg, segsum, segbase, err, dro, dcols;
+    deg.alloc((size_t)g->n * 4);
+    segsum.alloc(g->nseg * 8);
+    err.alloc(4);
+    CUDA_TRY(cudaMemsetAsync(err.p, 0, 4, st));
+    const int tpb = 64;
+    bv_seg_degrees<<<(unsigned)((g->nseg + tpb - 1) / tpb), tpb, 0, st>>>(s, deg.as<uint32_t>(), segsum.as<uint64_t>(),
+                                                                         err.as<int>());
+    CUDA_TRY(cudaGetLastError());
+    std::vector<uint64_t> hs(g->nseg), hb(g->nseg);
+    int herr = 0;
+    CUDA_TRY(cudaMemcpyAsync(hs.data(), segsum.p, g->nseg * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(&herr, err.p, 4, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (herr) throw AbiError(CMVG_ERR_CORRUPT, "BV stream corrupt (device degree pass, code " + std::to_string(herr) + ")");
+    uint64_t acc = 0;
+    for (uint64_t k = 0; k < g->nseg; ++k) { hb[k] = acc; acc += hs[k]; }
+    if (acc != g->m) throw AbiError(CMVG_ERR_CORRUPT, "BV stream corrupt: decoded edge count mismatch");
+    segbase.upload(hb.data(), hb.size());
+    uint64_t* ro = row_offsets;
+    uint32_t* co = cols;
+    if (ptr_kind == CMVG_HOST) {
+      dro.alloc(((size_t)g->n + 1) * 8);
+      dcols.alloc(g->m * 4 + 16);
+      ro = dro.as<uint64_t>();
+      co = dcols.as<uint32_t>();
+    }
+    bv_seg_decode<<<(unsigned)((g->nseg + tpb - 1) / tpb), tpb, 0, st>>>(s, segbase.as<uint64_t>(), ro, co, err.as<int>());
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(&herr, err.p, 4, cudaMemcpyDeviceToHost, st));
+    if (ptr_kind == CMVG_HOST) {
+      CUDA_TRY(cudaMemcpyAsync(row_offsets, ro, ((size_t)g->n + 1) * 8, cudaMemcpyDeviceToHost, st));
+      if (g->m) CUDA_TRY(cudaMemcpyAsync(cols, co, g->m * 4, cudaMemcpyDeviceToHost, st));
+    }
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (herr) throw AbiError(CMVG_ERR_CORRUPT, "BV stream corrupt (device decode pass, code " + std::to_string(herr) + ")");
+  });
+}
+
+int cmvg_pagerank(cmvg_graph* g, const uint32_t* degrees, double alpha, uint32_t iterations, double l1_tolerance,
+                  int dangling, double* ranks, uint32_t* iterations_run, int ptr_kind, void* stream) {
+  return guarded([&] {
+    require(g && degrees && ranks, "null argument");
+    require(alpha > 0.0 && alpha < 1.0, "alpha must be in (0,1)");
+    require(iterations > 0, "iterations must be > 0");
+    require(dangling == CMVG_DANGLING_UNIFORM || dangling == CMVG_DANGLING_DROP, "bad dangling policy");
+    require(g->row_begin == 0 && g->row_end == g->n, "cmvg_pagerank needs a whole-graph handle");
+    DeviceGuard dg(g->device);
+    run_pagerank(g, degrees, alpha, iterations, l1_tolerance, dangling, ranks, iterations_run, ptr_kind,
+                 (cudaStream_t)stream);
+  });
+}
+
+int cmvg_pagerank_step(cmvg_graph* g, const double* q, const uint32_t* deg, double alpha, double dmass, int dangling,
+                       const double* p_prev, double* p_next, double* q_next, double* partial, void* stream) {
+  return guarded([&] {
+    require(g && q && deg && p_next && q_next && partial, "null argument");
+    require(alpha > 0.0 && alpha < 1.0, "alpha must be in (0,1)");
+    DeviceGuard dg(g->device);
+    pagerank_step(g, q, deg, alpha, dmass, dangling, p_prev, p_next, q_next, partial, (cudaStream_t)stream);
+  });
+}
+
+}  // extern "C"

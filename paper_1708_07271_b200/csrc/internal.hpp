@@ -1,0 +1,175 @@
+// Internal (non-ABI) definitions shared by the ABI translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/cmvg.h"
+#include "cuda/bvd_gather.cuh"
+#include "host/bvd_layout.hpp"
+#include "host/host.hpp"
+
+namespace cmvg {
+
+// ---------------------------------------------------------------------------
+// errors
+extern thread_local std::string g_last_error;
+
+struct AbiError : std::runtime_error {
+  int code;
+  AbiError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+inline int set_error(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                                   \
+  do {                                                                                                   \
+    cudaError_t e_ = (expr);                                                                             \
+    if (e_ != cudaSuccess) throw AbiError(CMVG_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+template <typename F>
+inline int guarded(F&& f) {
+  try {
+    f();
+    return CMVG_OK;
+  } catch (const AbiError& e) {
+    return set_error(e.code, e.what());
+  } catch (const std::invalid_argument& e) {
+    return set_error(CMVG_ERR_INVALID, e.what());
+  } catch (const std::out_of_range& e) {
+    return set_error(CMVG_ERR_RANGE, e.what());
+  } catch (const std::bad_alloc&) {
+    return set_error(CMVG_ERR_NOMEM, "out of host memory");
+  } catch (const std::runtime_error& e) {
+    // stream validation failures come from the decoder as runtime_error
+    std::string m = e.what();
+    return set_error(m.find("corrupt") != std::string::npos || m.find("truncated") != std::string::npos ? CMVG_ERR_CORRUPT
+                                                                                                   : CMVG_ERR_INTERNAL,
+                     m);
+  } catch (const std::exception& e) {
+    return set_error(CMVG_ERR_INTERNAL, e.what());
+  }
+}
+
+inline void require(bool cond, const char* msg) {
+  if (!cond) throw std::invalid_argument(msg);
+}
+
+// device buffer RAII
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  void alloc(size_t b) {
+    if (p && bytes >= b) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    if (b == 0) return;
+    cudaError_t e = cudaMalloc(&p, b);
+    if (e != cudaSuccess) {
+      p = nullptr;
+      throw AbiError(CMVG_ERR_NOMEM, std::string("cudaMalloc(") + std::to_string(b) + "): " + cudaGetErrorString(e));
+    }
+    bytes = b;
+  }
+  template <typename T>
+  T* as() const {
+    return reinterpret_cast<T*>(p);
+  }
+  template <typename T>
+  void upload(const T* src, size_t count) {
+    alloc(count * sizeof(T));
+    if (count) CUDA_TRY(cudaMemcpy(p, src, count * sizeof(T), cudaMemcpyHostToDevice));
+  }
+};
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) CUDA_TRY(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+inline bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+}  // namespace cmvg
+
+// ---------------------------------------------------------------------------
+// opaque objects
+using namespace cmvg;
+struct cmvg_csr {
+  HostCsr g;
+};
+struct cmvg_bvstream {
+  BvStream s;
+};
+struct cmvg_graph {
+  int device = 0;
+  uint32_t n = 0;
+  uint64_t m = 0;
+  BvParams params;
+  BvdDims dims{};
+  uint32_t row_begin = 0, row_end = 0, block_begin = 0, nblocks = 0;
+  uint32_t stream_cap_words = 0;
+  uint32_t interval_mode = CMVG_INTERVALS_PREFIX;
+  uint64_t bv_bits = 0, adds = 0;
+  BvdStats stats;
+  // BV-D layout (this shard)
+  DevBuf words, blocks, lanes;
+  // canonical BV stream (whole graph) for decode_csr
+  DevBuf bv_words, bv_seg;
+  uint64_t nseg = 0;
+  // per-row reference distances of the shard (for the scatter form)
+  DevBuf refd;
+  // staging for host-pointer calls
+  DevBuf hx, hy;
+  std::mutex host_mu;
+  // scratch (scatter / pagerank)
+  DevBuf scratch;
+  uint64_t device_bytes() const {
+    return words.bytes + blocks.bytes + lanes.bytes + bv_words.bytes + bv_seg.bytes + refd.bytes;
+  }
+  BvdDev dev() const {
+    BvdDev d{};
+    d.words = words.as<uint32_t>();
+    d.blocks = blocks.as<BvdBlockInfo>();
+    d.lanes = lanes.as<uint32_t>();
+    d.d = dims;
+    d.block_begin = block_begin;
+    d.row_begin = row_begin;
+    d.stream_cap_words = stream_cap_words;
+    return d;
+  }
+};
+
+
+namespace cmvg {
+// kernel entry points implemented in the other translation units
+template <typename T>
+void launch_scatter(cmvg_graph* g, const T* x, T* y, cudaStream_t st);
+void launch_matmat(cmvg_graph* g, const float* X, float* Y, uint32_t k, cudaStream_t st);
+void run_pagerank(cmvg_graph* g, const uint32_t* degrees, double alpha, uint32_t iters, double l1_tol, int dangling,
+                  double* ranks, uint32_t* iters_run, int ptr_kind, cudaStream_t st);
+void pagerank_step(cmvg_graph* g, const double* q, const uint32_t* deg, double alpha, double dmass, int dangling,
+                   const double* p_prev, double* p_next, double* q_next, double* partial, cudaStream_t st);
+}  // namespace cmvg

@@ -1,0 +1,51 @@
+"""GPU BV decode (bv_decode_csr) is bit-exact against the source adjacency
+(the counterpart of reconstruct_graph, ref_matrix.hpp:75-76)."""
+import numpy as np
+import pytest
+
+import paper_1708_07271_b200 as P
+from tests.helpers import bv_params, csr_from_rows, make_graph
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("cfg,n", [(1, 1 << 16), (2, (1 << 16) + 5), (4, 1 << 15)])
+def test_decode_bit_exact(cuda, cfg, n):
+    g = make_graph(cfg, n=n)
+    s = P.BvStream.encode(g, bv_params(cfg))
+    dg = P.BvGraph(s)
+    ro, co = dg.decode_csr()
+    assert np.array_equal(ro, g.row_offsets)
+    assert np.array_equal(co, g.columns)
+
+
+def test_decode_device_buffers(cuda):
+    import torch
+
+    g = make_graph(1, n=1 << 15)
+    dg = P.BvGraph(P.BvStream.encode(g, bv_params(1)))
+    ro = torch.empty(g.n + 1, dtype=torch.int64, device="cuda")
+    co = torch.empty(g.m, dtype=torch.int32, device="cuda")
+    dg.decode_csr_device(ro, co)
+    torch.cuda.synchronize()
+    assert np.array_equal(ro.cpu().numpy().view(np.uint64), g.row_offsets)
+    assert np.array_equal(co.cpu().numpy().view(np.uint32), g.columns)
+
+
+def test_decode_edge_cases(cuda):
+    for rows in ([[]], [[0]], [[], [1], [0, 1]], [list(range(100))] * 50 + [[]] * 3):
+        g = csr_from_rows(rows)
+        for params in (P.BvParams(), P.BvParams(max_ref=0), P.BvParams(window=1, segment_rows=2)):
+            dg = P.BvGraph(P.BvStream.encode(g, params), P.CreateOptions(block_rows=1024))
+            ro, co = dg.decode_csr()
+            assert np.array_equal(ro, g.row_offsets) and np.array_equal(co, g.columns)
+
+
+def test_decode_rejects_corruption(cuda):
+    g = make_graph(1, n=1 << 12)
+    s = P.BvStream.encode(g, bv_params(1))
+    w = s.words()
+    w[len(w) // 2] ^= 0xFFFF0000  # flip bits mid-stream
+    bad = P.BvStream.from_words(g.n, g.m, s.params, w, s.stats()["stream_bits"], s.segment_offsets())
+    with pytest.raises((P.CorruptionError, ValueError, IndexError)):
+        P.BvGraph(bad)  # the host builder validates the stream first

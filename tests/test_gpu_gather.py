@@ -1,0 +1,152 @@
+"""GPU parity of the gather product y = A x^T (the hot path) against the
+oracle's matvec_csr (csr.hpp:48-55) and matvec_ref on compress(g, 7)
+(ref_matvec.hpp:30-35).  Tolerances (BASELINE.json north_star): fp64 1e-12
+relative per entry, fp32 1e-5 relative per entry against fp64 matvec_csr on the
+fp32-rounded x; empty rows exactly 0."""
+import numpy as np
+import pytest
+
+import paper_1708_07271_b200 as P
+from oracle import pyoracle as O
+from tests.helpers import bv_params, csr_from_rows, make_graph, max_rel_err, oracle_csr, x_uniform
+
+pytestmark = pytest.mark.gpu
+
+F64_TOL = 1e-12
+F32_TOL = 1e-5
+
+
+def check_gather(g, params, opts=None, seed=1, dtype=np.float64, device=False):
+    import torch
+
+    s = P.BvStream.encode(g, params)
+    dg = P.BvGraph(s, opts or P.CreateOptions())
+    x = x_uniform(g.n, seed)
+    ref = oracle_csr(g)
+    if dtype == np.float32:
+        x32 = x.astype(np.float32)
+        want = ref.matvec(x32.astype(np.float64), 8)
+        if device:
+            y = dg.matvec(torch.from_numpy(x32).cuda()).cpu().numpy()
+        else:
+            y = dg.matvec(x32)
+        err = max_rel_err(y, want)
+        assert err <= F32_TOL, err
+    else:
+        want = ref.matvec(x, 8)
+        if device:
+            y = dg.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
+        else:
+            y = dg.matvec(x)
+        err = max_rel_err(y, want)
+        assert err <= F64_TOL, err
+    return dg, s, x, y
+
+
+@pytest.mark.parametrize("mode", ["prefix", "direct"])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_gather_copy_model_small(cuda, mode, dtype):
+    g = make_graph(1, n=1 << 16)
+    check_gather(g, bv_params(1), P.CreateOptions(interval_mode=mode), dtype=dtype)
+
+
+def test_gather_device_pointers(cuda):
+    g = make_graph(2, n=1 << 17)
+    check_gather(g, bv_params(2), device=True)
+    check_gather(g, bv_params(2), dtype=np.float32, device=True)
+
+
+def test_gather_matches_matvec_ref(cuda):
+    g = make_graph(1, n=1 << 15)
+    s = P.BvStream.encode(g, bv_params(1))
+    dg = P.BvGraph(s)
+    x = x_uniform(g.n, 3)
+    rm = O.RefMatrix.compress(oracle_csr(g), 7)
+    want, _ = rm.matvec(x)
+    assert max_rel_err(dg.matvec(x), want) <= F64_TOL
+
+
+@pytest.mark.parametrize("lanes,block_rows,window", [(128, 1024, 2048), (256, 1024, 2048), (64, 2048, 4096),
+                                                      (32, 1024, 512), (128, 4096, 1024)])
+def test_gather_layout_variants(cuda, lanes, block_rows, window):
+    g = make_graph(2, n=(1 << 16) + 777)  # ragged last block
+    check_gather(g, bv_params(2), P.CreateOptions(lanes=lanes, block_rows=block_rows, window=window))
+
+
+def test_gather_stream_from_global(cuda):
+    # tiny smem cap: every block decodes straight from global memory
+    g = make_graph(1, n=1 << 15)
+    check_gather(g, bv_params(1), P.CreateOptions(stream_cap_words=16))
+
+
+def test_gather_unbounded_chains_social(cuda):
+    g = make_graph(4, n=1 << 16)
+    dg, s, _, _ = check_gather(g, bv_params(4), dtype=np.float32)
+    assert s.stats()["max_depth"] > 3
+
+
+def test_gather_long_copy_chain(cuda):
+    # every row equals row 0 -> chain depth up to the segment length (R=0)
+    n, base = 4096, 40
+    rows = [list(range(0, 2 * base, 2))] * n
+    g = csr_from_rows(rows)
+    check_gather(g, P.BvParams(max_ref=0))
+    check_gather(g, P.BvParams(max_ref=3))
+
+
+def test_gather_edge_cases(cuda):
+    # empty rows, self loops, a single row, columns at 0 and n-1, long intervals
+    cases = [
+        [[]],
+        [[0]],
+        [[], [], []],
+        [[0, 1, 2, 3, 4, 5, 6, 7, 8, 9], [], [9], [0, 9]],
+        [list(range(0, 3000)), list(range(1, 3001)), [2999, 3000], list(range(5, 3001, 2))] + [[]] * 2997,
+    ]
+    for rows in cases:
+        g = csr_from_rows(rows)
+        check_gather(g, P.BvParams())
+        check_gather(g, P.BvParams(), dtype=np.float32)
+
+
+def test_gather_far_columns(cuda):
+    # columns far outside every block's x-window -> global-memory gathers and intervals
+    rng = np.random.default_rng(4)
+    n = 50_000
+    rows = []
+    for i in range(n):
+        k = int(rng.integers(0, 12))
+        c = set(rng.integers(0, n, size=k).tolist())
+        if rng.random() < 0.2:
+            s0 = int(rng.integers(0, n - 20))
+            c.update(range(s0, s0 + 8))
+        rows.append(sorted(c))
+    g = csr_from_rows(rows)
+    check_gather(g, P.BvParams())
+
+
+def test_gather_shards_cover_rows(cuda):
+    g = make_graph(1, n=(1 << 16) + 100)
+    s = P.BvStream.encode(g, bv_params(1))
+    x = x_uniform(g.n, 5)
+    want = oracle_csr(g).matvec(x, 8)
+    bounds = [0, 16384, 32768, g.n]
+    parts = []
+    for a, b in zip(bounds[:-1], bounds[1:]):
+        dg = P.BvGraph(s, P.CreateOptions(row_begin=a, row_end=b))
+        parts.append(dg.matvec(x))
+    assert max_rel_err(np.concatenate(parts), want) <= F64_TOL
+
+
+def test_gather_dimension_errors(cuda):
+    g = make_graph(1, n=4096)
+    dg = P.BvGraph(P.BvStream.encode(g, bv_params(1)))
+    with pytest.raises(ValueError):
+        dg.matvec(np.zeros(4095))
+
+
+def test_adds_per_product(cuda):
+    g = make_graph(1, n=1 << 14)
+    dg = P.BvGraph(P.BvStream.encode(g, bv_params(1)))
+    assert 0 < dg.adds_per_product() < g.m
+    assert dg.dimension() == g.n
