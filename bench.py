@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--lanes", type=int, default=128)
     ap.add_argument("--block-rows", type=int, default=1024)
     ap.add_argument("--window", type=int, default=2048)
-    ap.add_argument("--stream-cap-words", type=int, default=6144)
+    ap.add_argument("--stream-cap-words", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")

@@ -92,7 +92,7 @@ typedef struct {
   uint32_t block_rows;    /* rows per CTA block (power of 2, multiple of the segment) */
   uint32_t lanes;         /* decode lanes (threads) per block                 */
   uint32_t window;        /* x-window entries staged per block                */
-  uint32_t stream_cap_words; /* blocks larger than this decode from global    */
+  uint32_t stream_cap_words; /* smem staging cap; larger blocks decode from global; 0 = auto (p99.5) */
   uint32_t interval_mode; /* CMVG_INTERVALS_*                                 */
   uint32_t row_begin;     /* shard [row_begin, row_end); row_end 0 = n        */
   uint32_t row_end;
@@ -110,6 +110,9 @@ typedef struct {
   uint32_t block_rows, lanes, window, nblocks, max_depth, interval_mode;
   uint64_t adds_per_product;
   uint64_t device_bytes;
+  uint64_t bvd_codes;           /* body codes = decode-loop iterations     */
+  uint32_t max_block_words, stream_cap_words;
+  double window_coverage;       /* gathered columns inside the x-window    */
 } cmvg_graph_info;
 
 /* ---- errors -------------------------------------------------------------- */
@@ -143,6 +146,14 @@ int cmvg_destroy(cmvg_graph* g);
 /* Host-only: build the device layout for `opts` and report its sizes
  * (no GPU needed; used for layout statistics and tests). */
 int cmvg_layout_info(const cmvg_bvstream* s, const cmvg_create_opts* opts, cmvg_graph_info* out);
+/* Host-only: build the device layout and copy it out (tests re-decode it on
+ * the CPU).  words: u32[*nwords]; blocks: 4 x u32 per block
+ * {word_offset lo, word_offset hi, nwords, wlo}.  Free with cmvg_layout_free. */
+typedef struct cmvg_layout cmvg_layout;
+int cmvg_layout_export(const cmvg_bvstream* s, const cmvg_create_opts* opts, cmvg_layout** out);
+const uint32_t* cmvg_layout_words(const cmvg_layout* l, uint64_t* nwords);
+const uint32_t* cmvg_layout_blocks(const cmvg_layout* l, uint32_t* nblocks);
+void cmvg_layout_free(cmvg_layout* l);
 int cmvg_graph_info_get(const cmvg_graph* g, cmvg_graph_info* out);
 uint32_t cmvg_dimension(const cmvg_graph* g);
 uint64_t cmvg_adds_per_product(const cmvg_graph* g);

@@ -84,7 +84,8 @@ class _InfoC(C.Structure):
                 ("bvd_lane_table_bytes", C.c_uint64), ("bvd_block_table_bytes", C.c_uint64),
                 ("block_rows", C.c_uint32), ("lanes", C.c_uint32), ("window", C.c_uint32), ("nblocks", C.c_uint32),
                 ("max_depth", C.c_uint32), ("interval_mode", C.c_uint32), ("adds_per_product", C.c_uint64),
-                ("device_bytes", C.c_uint64)]
+                ("device_bytes", C.c_uint64), ("bvd_codes", C.c_uint64), ("max_block_words", C.c_uint32),
+                ("stream_cap_words", C.c_uint32), ("window_coverage", C.c_double)]
 
 
 _lib_handle: Optional[C.CDLL] = None
@@ -114,6 +115,10 @@ _SIGS = [
     ("cmvg_create", C.c_int, [_P, C.POINTER(_OptsC), C.POINTER(_P)]),
     ("cmvg_destroy", C.c_int, [_P]),
     ("cmvg_layout_info", C.c_int, [_P, C.POINTER(_OptsC), C.POINTER(_InfoC)]),
+    ("cmvg_layout_export", C.c_int, [_P, C.POINTER(_OptsC), C.POINTER(_P)]),
+    ("cmvg_layout_words", _P, [_P, C.POINTER(C.c_uint64)]),
+    ("cmvg_layout_blocks", _P, [_P, C.POINTER(C.c_uint32)]),
+    ("cmvg_layout_free", None, [_P]),
     ("cmvg_graph_info_get", C.c_int, [_P, C.POINTER(_InfoC)]),
     ("cmvg_dimension", C.c_uint32, [_P]),
     ("cmvg_adds_per_product", C.c_uint64, [_P]),
@@ -291,6 +296,20 @@ class BvStream:
         _check(load_library().cmvg_layout_info(self._h, C.byref(oc), C.byref(inf)))
         return {f: getattr(inf, f) for f, _ in _InfoC._fields_}
 
+    def layout_export(self, options: Optional["CreateOptions"] = None):
+        """(words u32[], blocks u32[nblocks, 4]) of the device layout, built on the host."""
+        oc = (options or CreateOptions())._c()
+        h = _P()
+        lib = load_library()
+        _check(lib.cmvg_layout_export(self._h, C.byref(oc), C.byref(h)))
+        try:
+            nw, nb = C.c_uint64(), C.c_uint32()
+            w = _np_view(lib.cmvg_layout_words(h, C.byref(nw)), nw.value, np.uint32).copy()
+            b = _np_view(lib.cmvg_layout_blocks(h, C.byref(nb)), nb.value * 4, np.uint32).reshape(-1, 4).copy()
+        finally:
+            lib.cmvg_layout_free(h)
+        return w, b
+
     def decode_host(self) -> CsrGraph:
         """CPU decode (the handle builder's path); tests compare it with the GPU decoder."""
         out = _P()
@@ -310,7 +329,7 @@ class CreateOptions:
     block_rows: int = 1024
     lanes: int = 128
     window: int = 2048
-    stream_cap_words: int = 6144
+    stream_cap_words: int = 0  # 0 = auto (covers 99.5% of blocks)
     interval_mode: str = "prefix"  # or "direct"
     row_begin: int = 0
     row_end: int = 0  # 0 = n

@@ -166,7 +166,7 @@ void cmvg_default_opts(cmvg_create_opts* o) {
   o->block_rows = 1024;
   o->lanes = 128;
   o->window = 2048;
-  o->stream_cap_words = 6144;
+  o->stream_cap_words = 0;
   o->interval_mode = CMVG_INTERVALS_PREFIX;
   o->row_begin = 0;
   o->row_end = 0;
@@ -179,10 +179,10 @@ int cmvg_create(const cmvg_bvstream* s, const cmvg_create_opts* opts_in, cmvg_gr
     cmvg_default_opts(&o);
     if (opts_in) o = *opts_in;
     const BvStream& bs = s->s;
-    require(bs.params.window <= 7 || true, "");
+    require(bs.params.window <= 7, "the device layout supports BV windows w <= 7");
     require(bs.params.zeta_k == 3, "device kernels support zeta_3 residuals");
     require(bs.n > 0, "empty graph");
-    require(o.lanes >= 32 && o.lanes <= 256 && o.lanes % 32 == 0, "lanes must be 32..256, a multiple of 32");
+    require(o.lanes >= 32 && o.lanes <= 256 && o.lanes % 32 == 0, "lanes (threads per block) must be 32..256, a multiple of 32");
     require(o.interval_mode <= CMVG_INTERVALS_DIRECT, "bad interval_mode");
     uint32_t row_end = o.row_end ? o.row_end : bs.n;
     require(o.row_begin < row_end && row_end <= bs.n, "bad shard row range");
@@ -197,7 +197,6 @@ int cmvg_create(const cmvg_bvstream* s, const cmvg_create_opts* opts_in, cmvg_gr
     if (dec.csr.m() != bs.m) throw std::runtime_error("BV stream corrupt: edge count mismatch");
     BvdOptions bo;
     bo.block_rows = o.block_rows;
-    bo.lanes = o.lanes;
     bo.window = o.window;
     BvdLayout L = build_bvd(dec, bs.params, bo);
 
@@ -212,8 +211,13 @@ int cmvg_create(const cmvg_bvstream* s, const cmvg_create_opts* opts_in, cmvg_gr
     g->block_begin = o.row_begin / o.block_rows;
     uint32_t block_end = (uint32_t)(((uint64_t)row_end + o.block_rows - 1) / o.block_rows);
     g->nblocks = block_end - g->block_begin;
-    g->stream_cap_words = o.stream_cap_words;
+    g->stream_cap_words = o.stream_cap_words ? o.stream_cap_words
+                                             : std::max<uint32_t>(1024, (L.stats.p995_block_words + 255) & ~255u);
+    g->stats.codes = L.stats.codes;
+    g->stats.window_coverage = L.stats.window_coverage;
+    g->stats.p995_block_words = L.stats.p995_block_words;
     g->interval_mode = o.interval_mode;
+    g->threads = o.lanes;
     g->bv_bits = bs.nbits;
     g->nseg = bs.segment_bit_offsets.size() - 1;
 
@@ -227,11 +231,9 @@ int cmvg_create(const cmvg_bvstream* s, const cmvg_create_opts* opts_in, cmvg_gr
     wds.resize(wds.size() + 8, 0);
     g->words.upload(wds.data(), wds.size());
     g->blocks.upload(bl.data(), bl.size());
-    g->lanes.upload(L.lanes.data() + (size_t)g->block_begin * o.lanes, (size_t)g->nblocks * o.lanes);
     g->refd.upload(dec.ref_dist.data() + o.row_begin, row_end - o.row_begin);
     // stats of the shard
     g->stats.stream_bytes = (w1 - w0) * 4;
-    g->stats.lane_table_bytes = (uint64_t)g->nblocks * o.lanes * 4;
     g->stats.block_table_bytes = (uint64_t)g->nblocks * sizeof(BvdBlockInfo);
     g->stats.row_bits = L.stats.row_bits;  // whole graph
     g->adds = L.adds_per_product;
@@ -251,7 +253,6 @@ int cmvg_layout_info(const cmvg_bvstream* s, const cmvg_create_opts* opts_in, cm
     BvDecoded dec = bv_decode(bs);
     BvdOptions bo;
     bo.block_rows = opt.block_rows;
-    bo.lanes = opt.lanes;
     bo.window = opt.window;
     BvdLayout L = build_bvd(dec, bs.params, bo);
     std::memset(o, 0, sizeof(*o));
@@ -262,18 +263,50 @@ int cmvg_layout_info(const cmvg_bvstream* s, const cmvg_create_opts* opts_in, cm
     o->bv_stream_bits = bs.nbits;
     o->bvd_row_bits = L.stats.row_bits;
     o->bvd_stream_bytes = L.stats.stream_bytes;
-    o->bvd_lane_table_bytes = L.stats.lane_table_bytes;
+    o->bvd_lane_table_bytes = 0;
     o->bvd_block_table_bytes = L.stats.block_table_bytes;
     o->block_rows = L.dims.block_rows;
-    o->lanes = L.dims.lanes;
+    o->lanes = opt.lanes;
     o->window = L.dims.window;
     o->nblocks = L.dims.nblocks;
     o->max_depth = L.dims.max_depth;
     o->interval_mode = opt.interval_mode;
     o->adds_per_product = L.adds_per_product;
     o->device_bytes = 0;
+    o->bvd_codes = L.stats.codes;
+    o->max_block_words = L.dims.max_block_words;
+    o->stream_cap_words = opt.stream_cap_words ? opt.stream_cap_words
+                                               : std::max<uint32_t>(1024, (L.stats.p995_block_words + 255) & ~255u);
+    o->window_coverage = L.stats.window_coverage;
   });
 }
+
+int cmvg_layout_export(const cmvg_bvstream* s, const cmvg_create_opts* opts_in, cmvg_layout** out) {
+  return guarded([&] {
+    require(s && out, "null argument");
+    cmvg_create_opts opt;
+    cmvg_default_opts(&opt);
+    if (opts_in) opt = *opts_in;
+    BvDecoded dec = bv_decode(s->s);
+    BvdOptions bo;
+    bo.block_rows = opt.block_rows;
+    bo.window = opt.window;
+    auto l = std::make_unique<cmvg_layout>();
+    l->L = build_bvd(dec, s->s.params, bo);
+    *out = l.release();
+  });
+}
+const uint32_t* cmvg_layout_words(const cmvg_layout* l, uint64_t* nwords) {
+  if (!l) return nullptr;
+  if (nwords) *nwords = l->L.words.size();
+  return l->L.words.data();
+}
+const uint32_t* cmvg_layout_blocks(const cmvg_layout* l, uint32_t* nblocks) {
+  if (!l) return nullptr;
+  if (nblocks) *nblocks = (uint32_t)l->L.blocks.size();
+  return reinterpret_cast<const uint32_t*>(l->L.blocks.data());
+}
+void cmvg_layout_free(cmvg_layout* l) { delete l; }
 
 int cmvg_destroy(cmvg_graph* g) {
   if (!g) return CMVG_OK;
@@ -295,16 +328,20 @@ int cmvg_graph_info_get(const cmvg_graph* g, cmvg_graph_info* o) {
     o->bv_stream_bits = g->bv_bits;
     o->bvd_row_bits = g->stats.row_bits;
     o->bvd_stream_bytes = g->stats.stream_bytes;
-    o->bvd_lane_table_bytes = g->stats.lane_table_bytes;
+    o->bvd_lane_table_bytes = 0;
     o->bvd_block_table_bytes = g->stats.block_table_bytes;
     o->block_rows = g->dims.block_rows;
-    o->lanes = g->dims.lanes;
+    o->lanes = g->threads;
     o->window = g->dims.window;
     o->nblocks = g->nblocks;
     o->max_depth = g->dims.max_depth;
     o->interval_mode = g->interval_mode;
     o->adds_per_product = g->adds;
     o->device_bytes = g->device_bytes();
+    o->bvd_codes = g->stats.codes;
+    o->max_block_words = g->dims.max_block_words;
+    o->stream_cap_words = g->stream_cap_words;
+    o->window_coverage = g->stats.window_coverage;
   });
 }
 
@@ -323,7 +360,7 @@ void launch_gather(cmvg_graph* g, const XT* x, YT* y, cudaStream_t st) {
   GatherSmem L = gather_smem_layout(g->dims, g->stream_cap_words, sizeof(XT), prefix);
   auto kern = prefix ? bvd_gather_kernel<XT, YT, true> : bvd_gather_kernel<XT, YT, false>;
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
-  kern<<<g->nblocks, g->dims.lanes, L.total, st>>>(g->dev(), x, y);
+  kern<<<g->nblocks, g->threads, L.total, st>>>(g->dev(), x, y);
   CUDA_TRY(cudaGetLastError());
 }
 

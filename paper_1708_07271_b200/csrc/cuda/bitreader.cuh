@@ -59,6 +59,22 @@ struct DevBits {
     if (L) skip(L);
     return ((1u << L) | low) - 1u;
   }
+  // Z code of the device layout (host/bits.hpp zfix): h zeros, a one, then
+  // v = x + 1 in 3h+3 bits.  Fast path when the whole code is in the window.
+  __device__ __forceinline__ uint32_t zfix() {
+    int h = __clzll(cur);
+    int tot = 4 * h + 4;
+    if (tot <= nb) {
+      uint32_t v = (uint32_t)(cur >> (64 - tot)) - (1u << (3 * h + 3));
+      skip(tot);
+      return v - 1u;
+    }
+    skip(h + 1);
+    int w = 3 * h + 3;
+    uint32_t v = (uint32_t)(cur >> (64 - w));
+    skip(w);
+    return v - 1u;
+  }
   template <int K>
   __device__ __forceinline__ uint32_t zeta() {
     int h = __clzll(cur);

@@ -3,40 +3,30 @@
 // SPEC.md:197-205).
 //
 // One CTA per block of B rows (reference chains never leave a block):
-//   1. one thread issues TMA bulk copies of the block's coded stream and of
-//      the x-window x[wlo, wlo+W) into shared memory (mbarrier completion);
-//   2. [PREFIX] warps build a tile-local (16-entry) exclusive prefix of the
-//      window, tile totals and their prefix, so an interval costs O(1);
-//   3. every thread decodes its lane: a contiguous, cost-balanced range of
-//      rows, computing delta_i = -sum_minus x + sum_intervals x + sum_res x
-//      in fp64 (no reference dependency: deltas are independent);
-//   4. level phases: rows of chain depth d add y of their reference row,
-//      d = 1..max depth (y_i = delta_i + y_{i-r}, the reference's order);
+//   1. thread 0 issues a TMA bulk copy of the block's coded stream into
+//      shared memory (mbarrier completion) while all threads stage the
+//      x-window x[wlo, wlo+W) and build its tile-local double-double prefix;
+//   2. row setup: row bit offsets (scan of body lengths from the headers) and
+//      warp rounds (rows counting-sorted by point-code count, so the 32 rows
+//      a warp decodes together have near-equal work);
+//   3. each warp decodes its rounds, one row per lane: a loop over point
+//      codes (minus -> -x[c], residual -> +x[c]) then a loop over intervals
+//      (O(1) from the prefix); delta_i is accumulated with Neumaier
+//      compensation, so it carries no cancellation error into the chain;
+//   4. level phases over chain depth: y_i = delta_i + y_{i-r} in
+//      double-double (the reference's order, ref_matvec.hpp:23-25);
 //   5. coalesced store of y.
 #pragma once
 #include <cstdint>
 
-#include "../host/layout.hpp"
-#include "bitreader.cuh"
-#include "ptx.cuh"
+#include "bvd_common.cuh"
 
 namespace cmvg {
 
-struct BvdDev {
-  const uint32_t* words;
-  const BvdBlockInfo* blocks;
-  const uint32_t* lanes;
-  BvdDims d;
-  uint32_t block_begin;  // first block of this shard
-  uint32_t row_begin;    // first row of this shard
-  uint32_t stream_cap_words;  // blocks with more words decode from global memory
-  uint32_t pad;
-};
-
-__host__ __device__ inline uint32_t align16(uint32_t v) { return (v + 15u) & ~15u; }
-
 struct GatherSmem {
-  uint32_t off_x, off_p, off_tt, off_q, off_y, off_ref, off_dep, off_bar, total;
+  uint32_t off_x, off_yhi, off_ylo;
+  RowSmem rows;
+  uint32_t total;
 };
 
 __host__ __device__ inline GatherSmem gather_smem_layout(const BvdDims& d, uint32_t stream_cap_words, uint32_t xsize,
@@ -44,23 +34,113 @@ __host__ __device__ inline GatherSmem gather_smem_layout(const BvdDims& d, uint3
   GatherSmem s;
   uint32_t o = align16((stream_cap_words + 8) * 4);
   s.off_x = o;
-  o = align16(o + d.window * xsize + 16);
-  s.off_p = o;
-  if (prefix) o = align16(o + (d.window + 16) * 8);
-  s.off_tt = o;
-  if (prefix) o = align16(o + (d.window / 16 + 1) * 8);
-  s.off_q = o;
-  if (prefix) o = align16(o + (d.window / 16 + 2) * 8);
-  s.off_y = o;
+  o = align16(o + xw_bytes(d.window, xsize, prefix));
+  s.off_yhi = o;
   o = align16(o + d.block_rows * 8);
-  s.off_ref = o;
-  o = align16(o + d.block_rows);
-  s.off_dep = o;
-  o = align16(o + d.block_rows * 2);
-  s.off_bar = o;
-  o = align16(o + 16);
-  s.total = o;
+  s.off_ylo = o;
+  o = align16(o + d.block_rows * 4);
+  s.rows = row_smem_layout(o, d.block_rows);
+  s.total = s.rows.total;
   return s;
+}
+
+// Phase A (point rounds): each warp takes 32 rows of similar point-code count
+// (one per lane) and accumulates -x[c] for minus codes, +x[c] for residual
+// codes; writes delta (hi, lo).  Phase B (interval rounds, after a barrier):
+// the rows that have intervals, grouped by interval count, add their O(1)
+// interval sums to delta.  Every row is owned by one lane in each phase.
+template <class XWinT>
+__device__ __forceinline__ void decode_points(const RowCtx& c, const uint32_t* __restrict__ base, const XWinT& xw,
+                                              int32_t r0, double* s_yhi, float* s_ylo) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const int nesc = c.misc[0];
+  for (;;) {
+    uint32_t rb = 0;  // next round of 32 rows, claimed dynamically (balances the warps)
+    if (lane == 0) rb = 32u * (uint32_t)atomicAdd(&c.misc[3], 1);
+    rb = __shfl_sync(0xffffffffu, rb, 0);
+    if (rb >= c.nr) break;
+    const uint32_t slot = rb + lane;
+    const bool act = slot < c.nr;
+    const uint32_t k = act ? c.perm[slot] : 0u;
+    const uint32_t h = act ? base[k] : 0u;
+    RowCounts rc{0, 0, 0};
+    if (act) rc = row_counts(base, c.B, h, k, nesc);
+    const uint32_t wp = hdr_wp(h);
+    const int32_t i = r0 + (int32_t)k;
+    const uint32_t np = rc.nm + rc.ns;
+    uint32_t off = act ? c.rowoff[k] : 0u;
+    double acc = 0.0, comp = 0.0;
+    const uint32_t tp = __reduce_max_sync(0xffffffffu, np);
+    for (uint32_t t = 0; t < tp; ++t) {
+      double term = 0.0;
+      if (t < np) {
+        const int32_t col = i + unfold32(extract_bits(base, off, wp));
+        const double xv = xw.at(col);
+        term = t < rc.nm ? -xv : xv;
+        off += wp;
+      }
+      nadd(acc, comp, term);
+    }
+    if (act) {
+      const double hi = acc + comp;
+      s_yhi[k] = hi;
+      s_ylo[k] = (float)(comp - (hi - acc));
+    }
+  }
+}
+
+template <class XWinT>
+__device__ __forceinline__ void decode_intervals(const RowCtx& c, const uint32_t* __restrict__ base, const XWinT& xw,
+                                                 int32_t r0, uint32_t lmin, double* s_yhi, float* s_ylo) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const int nesc = c.misc[0];
+  const uint32_t nri = (uint32_t)c.misc[2];
+  for (;;) {
+    uint32_t rb = 0;
+    if (lane == 0) rb = 32u * (uint32_t)atomicAdd(&c.misc[4], 1);
+    rb = __shfl_sync(0xffffffffu, rb, 0);
+    if (rb >= nri) break;
+    const uint32_t slot = rb + lane;
+    const bool act = slot < nri;
+    const uint32_t k = act ? c.permi[slot] : 0u;
+    const uint32_t h = act ? base[k] : 0u;
+    RowCounts rc{0, 0, 0};
+    if (act) rc = row_counts(base, c.B, h, k, nesc);
+    const uint32_t wp = hdr_wp(h), wl = hdr_wl(h);
+    const int32_t i = r0 + (int32_t)k;
+    uint32_t off = act ? c.rowoff[k] + (rc.nm + rc.ns) * wp : 0u;
+    double acc = 0.0, comp = 0.0;
+    const uint32_t ti = __reduce_max_sync(0xffffffffu, rc.ni);
+    for (uint32_t t = 0; t < ti; ++t) {
+      double hi = 0.0, lo = 0.0;
+      if (t < rc.ni) {
+        const int32_t left = i + unfold32(extract_bits(base, off, wp));
+        const uint32_t len = extract_bits(base, off + wp, wl) + lmin;
+        hi = xw.isum(left, len, lo);
+        off += wp + wl;
+      }
+      nadd(acc, comp, hi);
+      comp += lo;
+    }
+    if (act) {
+      double hi = s_yhi[k], lo = (double)s_ylo[k];
+      dd_add(hi, lo, acc, comp);
+      s_yhi[k] = hi;
+      s_ylo[k] = (float)lo;
+    }
+  }
+}
+
+template <typename XT, typename YT, bool PREFIX>
+__device__ __forceinline__ void gather_block(RowCtx& rc, const uint32_t* __restrict__ base, const XWin<XT, PREFIX>& xw,
+                                             const BvdDims& D, uint32_t r0, double* s_yhi, float* s_ylo, YT* yb) {
+  rc.base = base;
+  row_setup(rc);
+  decode_points(rc, base, xw, (int32_t)r0, s_yhi, s_ylo);
+  __syncthreads();
+  decode_intervals(rc, base, xw, (int32_t)r0, D.min_interval, s_yhi, s_ylo);
+  __syncthreads();
+  chain_and_store(s_yhi, s_ylo, rc, yb);
 }
 
 template <typename XT, typename YT, bool PREFIX>
@@ -68,190 +148,29 @@ __global__ void __launch_bounds__(256) bvd_gather_kernel(BvdDev g, const XT* __r
   extern __shared__ __align__(16) unsigned char smem[];
   const BvdDims& D = g.d;
   const GatherSmem L = gather_smem_layout(D, g.stream_cap_words, sizeof(XT), PREFIX);
-  uint32_t* s_stream = reinterpret_cast<uint32_t*>(smem);
-  XT* s_x = reinterpret_cast<XT*>(smem + L.off_x);
-  double* s_p = reinterpret_cast<double*>(smem + L.off_p);
-  double* s_tt = reinterpret_cast<double*>(smem + L.off_tt);
-  double* s_q = reinterpret_cast<double*>(smem + L.off_q);
-  double* s_y = reinterpret_cast<double*>(smem + L.off_y);
-  uint8_t* s_ref = reinterpret_cast<uint8_t*>(smem + L.off_ref);
-  uint16_t* s_dep = reinterpret_cast<uint16_t*>(smem + L.off_dep);
-  uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + L.off_bar);
-  int* s_dmax = reinterpret_cast<int*>(smem + L.off_bar + 8);
-
-  const uint32_t T = blockDim.x;
-  const uint32_t tid = threadIdx.x;
   const uint32_t bl = blockIdx.x;  // index into this shard's tables
   const uint32_t b = g.block_begin + bl;
   const BvdBlockInfo bi = g.blocks[bl];
   const uint32_t r0 = b * D.block_rows;
   const uint32_t nr = min(D.block_rows, D.n - r0);
-  const uint32_t W = D.window;
-  const uint32_t wlo = bi.wlo;
-  const bool staged = bi.nwords <= g.stream_cap_words;
-  const uint32_t xvalid = wlo < D.n ? min(W, D.n - wlo) : 0u;
-  const uint32_t xtma_bytes = (xvalid * (uint32_t)sizeof(XT)) & ~15u;
-  const uint32_t xtma = xtma_bytes / (uint32_t)sizeof(XT);
 
-  if (tid == 0) {
-    mbar_init(s_bar, 1);
-    *s_dmax = 0;
-    uint32_t sbytes = staged ? bi.nwords * 4u : 0u;
-    mbar_arrive_expect_tx(s_bar, sbytes + xtma_bytes);
-    if (sbytes) bulk_g2s(s_stream, g.words + bi.word_offset, sbytes, s_bar);
-    if (xtma_bytes) bulk_g2s(s_x, x + wlo, xtma_bytes, s_bar);
-  }
-  // window tail (not a 16-byte multiple, or past n) and stream guard words
-  for (uint32_t j = xtma + tid; j < W; j += T) s_x[j] = (wlo + j < D.n) ? x[wlo + j] : XT(0);
-  if (tid < 8) s_stream[(staged ? bi.nwords : 0u) + tid] = 0u;
-  __syncthreads();
-  mbar_wait(s_bar, 0);
+  RowCtx rc = carve_rows(smem, L.rows, D.block_rows, nr);
+  uint32_t* s_stream = reinterpret_cast<uint32_t*>(smem);
+  stage_stream_begin(g, bi, s_stream, rc.bar);
+  XWin<XT, PREFIX> xw;
+  xw.carve(smem + L.off_x, D.window);
+  xw.x = x;
+  xw.wlo = bi.wlo;
+  xw.stage(D.n);  // ends with __syncthreads (also publishes the mbarrier init)
+  mbar_wait(rc.bar, 0);
 
-  if constexpr (PREFIX) {
-    // tile-local exclusive prefix (16-entry tiles) with half-warp scans
-    const uint32_t lane = tid & 31u, warp = tid >> 5, nwarps = T >> 5;
-    for (uint32_t base = warp * 32u; base < W; base += nwarps * 32u) {
-      double v = (double)s_x[base + lane];
-      double inc = v;
-#pragma unroll
-      for (int o = 1; o < 16; o <<= 1) {
-        double u = __shfl_up_sync(0xffffffffu, inc, o, 16);
-        if ((int)(lane & 15u) >= o) inc += u;
-      }
-      double ex = __shfl_up_sync(0xffffffffu, inc, 1, 16);
-      if ((lane & 15u) == 0) ex = 0.0;
-      s_p[base + lane] = ex;
-      if ((lane & 15u) == 15u) s_tt[(base + lane) >> 4] = inc;
-    }
-    __syncthreads();
-    if (warp == 0) {
-      const uint32_t ntiles = W >> 4;
-      const uint32_t per = (ntiles + 31u) / 32u;
-      double loc = 0.0;
-      for (uint32_t t = 0; t < per; ++t) {
-        uint32_t k = lane * per + t;
-        if (k < ntiles) loc += s_tt[k];
-      }
-      double inc = loc;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        double u = __shfl_up_sync(0xffffffffu, inc, o);
-        if ((int)lane >= o) inc += u;
-      }
-      double run = __shfl_up_sync(0xffffffffu, inc, 1);
-      if (lane == 0) run = 0.0;
-      for (uint32_t t = 0; t < per; ++t) {
-        uint32_t k = lane * per + t;
-        if (k < ntiles) {
-          s_q[k] = run;
-          run += s_tt[k];
-        }
-      }
-      if (lane == 31) s_q[ntiles] = inc;
-    }
-    __syncthreads();
-  }
-
-  auto X = [&](int32_t c) -> double {
-    uint32_t j = (uint32_t)(c - (int32_t)wlo);
-    return j < W ? (double)s_x[j] : (double)__ldg(x + c);
-  };
-  auto ISUM = [&](int32_t left, uint32_t len) -> double {
-    uint32_t a = (uint32_t)(left - (int32_t)wlo);
-    uint32_t e = a + len;
-    double s = 0.0;
-    if (a < W && e <= W) {
-      if constexpr (PREFIX) {
-        uint32_t ta = a >> 4, tb = e >> 4;
-        if (ta == tb) return s_p[e] - s_p[a];
-        s = s_tt[ta] - s_p[a];
-        if (tb > ta + 1) s += s_q[tb] - s_q[ta + 1];
-        if (e & 15u) s += s_p[e];
-        return s;
-      } else {
-        for (uint32_t t = a; t < e; ++t) s += (double)s_x[t];
-        return s;
-      }
-    }
-    for (uint32_t t = 0; t < len; ++t) s += (double)__ldg(x + left + t);
-    return s;
-  };
-
-  // ---- decode this thread's lane --------------------------------------------
-  const uint32_t rowmask = (1u << D.row_bits) - 1u;
-  const uint32_t* ltab = g.lanes + (size_t)bl * T;
-  const uint32_t lt = ltab[tid];
-  const uint32_t rs = lt & rowmask;
-  const uint32_t re = (tid + 1 < T) ? (ltab[tid + 1] & rowmask) : nr;
-  if (rs < re) {
-    DevBits br;
-    br.init(staged ? s_stream : g.words + bi.word_offset, lt >> D.row_bits);
-    const int ref_bits = (int)D.ref_bits;
-    const uint32_t lmin = D.min_interval;
-    for (uint32_t k = rs; k < re; ++k) {
-      const int32_t i = (int32_t)(r0 + k);
-      const uint32_t r = br.bits(ref_bits);
-      double acc = 0.0;
-      if (r) {
-        uint32_t nm = br.gamma();
-        if (nm) {
-          int32_t c = i + unfold_i32(br.zeta<3>());
-          acc -= X(c);
-          for (uint32_t t = 1; t < nm; ++t) {
-            c += (int32_t)br.zeta<3>() + 1;
-            acc -= X(c);
-          }
-        }
-      }
-      uint32_t ni = br.gamma();
-      if (ni) {
-        int32_t left = i + unfold_i32(br.gamma());
-        uint32_t len = br.gamma() + lmin;
-        acc += ISUM(left, len);
-        int32_t end = left + (int32_t)len;
-        for (uint32_t t = 1; t < ni; ++t) {
-          left = end + (int32_t)br.gamma() + 1;
-          len = br.gamma() + lmin;
-          acc += ISUM(left, len);
-          end = left + (int32_t)len;
-        }
-      }
-      uint32_t nres = br.gamma();
-      if (nres) {
-        int32_t c = i + unfold_i32(br.zeta<3>());
-        acc += X(c);
-        for (uint32_t t = 1; t < nres; ++t) {
-          c += (int32_t)br.zeta<3>() + 1;
-          acc += X(c);
-        }
-      }
-      s_y[k] = acc;
-      s_ref[k] = (uint8_t)r;
-    }
-  }
-  __syncthreads();
-
-  // ---- reference-chain level phases ------------------------------------------
-  int dmax = 0;
-  for (uint32_t k = tid; k < nr; k += T) {
-    uint32_t d = 0, j = k;
-    while (s_ref[j]) {
-      j -= s_ref[j];
-      ++d;
-    }
-    s_dep[k] = (uint16_t)d;
-    dmax = max(dmax, (int)d);
-  }
-  if (dmax) atomicMax(s_dmax, dmax);
-  __syncthreads();
-  dmax = *s_dmax;
-  for (int d = 1; d <= dmax; ++d) {
-    for (uint32_t k = tid; k < nr; k += T)
-      if (s_dep[k] == d) s_y[k] += s_y[k - s_ref[k]];
-    __syncthreads();
-  }
+  double* s_yhi = reinterpret_cast<double*>(smem + L.off_yhi);
+  float* s_ylo = reinterpret_cast<float*>(smem + L.off_ylo);
   YT* yb = y + (r0 - g.row_begin);
-  for (uint32_t k = tid; k < nr; k += T) yb[k] = (YT)s_y[k];
+  if (bi.nwords <= g.stream_cap_words)  // CTA-uniform: shared-memory decode path
+    gather_block<XT, YT, PREFIX>(rc, s_stream, xw, D, r0, s_yhi, s_ylo, yb);
+  else
+    gather_block<XT, YT, PREFIX>(rc, g.words + bi.word_offset, xw, D, r0, s_yhi, s_ylo, yb);
 }
 
 }  // namespace cmvg

@@ -33,6 +33,10 @@ inline int64_t unfold_signed(uint64_t u) {
 }
 
 inline int unary_len(uint64_t x) { return (int)x + 1; }
+// Device-layout zeta_3 variant with a fixed-width payload: h zeros, a one,
+// then v = x + 1 itself in 3h+3 bits (the minimal-binary refinement is dropped
+// so the code length 4h+4 depends on h alone).
+inline int zfix_len(uint64_t x) { return 4 * (ilog2_u64(x + 1) / 3) + 4; }
 inline int gamma_len(uint64_t x) { return 2 * ilog2_u64(x + 1) + 1; }
 inline int zeta_len(uint64_t x, int k) {
   uint64_t v = x + 1;
@@ -78,6 +82,12 @@ class BitWriter {
     unary(h);
     if (r < t) put(r, s - 1);
     else put(r + t, s);
+  }
+  void zfix(uint64_t x) {
+    uint64_t v = x + 1;
+    int h = ilog2_u64(v) / 3;
+    unary(h);
+    put(v, 3 * h + 3);
   }
   void align(int bits) {  // pad with zeros to a multiple of `bits`
     while (nbits % bits) {
@@ -128,6 +138,11 @@ class BitReader {
     if (L > 63) throw std::runtime_error("BV stream corrupt: gamma too long");
     uint64_t low = L ? get((int)L) : 0;
     return ((1ull << L) | low) - 1;
+  }
+  uint64_t zfix() {
+    uint64_t h = unary();
+    if (h > 20) throw std::runtime_error("stream corrupt: zfix too long");
+    return get((int)(3 * h + 3)) - 1;
   }
   uint64_t zeta(int k) {
     uint64_t h = unary();

@@ -15,6 +15,9 @@ struct RowParts {
   std::vector<std::pair<uint32_t, uint32_t>> ints;
 };
 
+// A' row of i against its BV reference i - r: minus = ref minus row, plus = row minus
+// ref split into maximal runs >= Lmin (intervals) and the rest (residuals),
+// which is exactly BV's extra-list split.
 void split_row(const HostCsr& g, uint32_t i, uint32_t r, uint32_t lmin, RowParts& rp, std::vector<uint32_t>& plus) {
   rp.minus.clear();
   rp.res.clear();
@@ -45,12 +48,7 @@ void split_row(const HostCsr& g, uint32_t i, uint32_t r, uint32_t lmin, RowParts
   }
 }
 
-void write_gapped_zeta(BitWriter& bw, const std::vector<uint32_t>& v, uint32_t i, uint32_t k) {
-  for (size_t t = 0; t < v.size(); ++t) {
-    if (t == 0) bw.zeta(fold_signed((int64_t)v[0] - (int64_t)i), k);
-    else bw.zeta(v[t] - v[t - 1] - 1, k);
-  }
-}
+inline uint32_t bits_of(uint64_t v) { return v ? 64u - (uint32_t)__builtin_clzll(v) : 0u; }
 
 }  // namespace
 
@@ -58,129 +56,125 @@ BvdLayout build_bvd(const BvDecoded& dec, const BvParams& bp, const BvdOptions& 
   const HostCsr& g = dec.csr;
   BvdLayout L;
   BvdDims& D = L.dims;
-  uint32_t B = opt.block_rows, T = opt.lanes, W = opt.window;
-  if (B == 0 || (B & (B - 1)) || B % bp.segment_rows) throw std::invalid_argument("block_rows must be a power of two and a multiple of the BV segment");
-  if (T == 0 || T % 32 || T > 1024) throw std::invalid_argument("lanes must be a multiple of 32, <= 1024");
+  const uint32_t B = opt.block_rows, W = opt.window;
+  if (B == 0 || (B & (B - 1)) || B % bp.segment_rows || B > 4096)
+    throw std::invalid_argument("block_rows must be a power of two <= 4096 and a multiple of the BV segment");
   if (W % 16 || W == 0) throw std::invalid_argument("window must be a positive multiple of 16");
+  if (bp.window > 7) throw std::invalid_argument("the device layout supports BV windows w <= 7");
   D.n = g.n;
   D.block_rows = B;
-  D.lanes = T;
-  D.row_bits = 0;
-  while ((1u << D.row_bits) <= B) ++D.row_bits;  // field holds 0..B inclusive
   D.window = W;
-  D.ref_bits = 0;
-  while ((1u << D.ref_bits) <= bp.window) ++D.ref_bits;
   D.min_interval = bp.min_interval;
-  D.zeta_k = bp.zeta_k;
   D.nblocks = (uint32_t)(((uint64_t)g.n + B - 1) / B);
   D.max_depth = 0;
   const uint32_t nb = D.nblocks;
   std::vector<BitWriter> bstream(nb);
   L.blocks.resize(nb);
-  L.lanes.resize((uint64_t)nb * T);
-  std::vector<uint64_t> bbits(nb, 0), badds(nb, 0);
+  std::vector<uint64_t> bbits(nb, 0), badds(nb, 0), bcodes(nb, 0), bgath(nb, 0), bin(nb, 0);
   std::vector<uint32_t> bdepth(nb, 0);
-  const uint32_t max_off = 1u << (32 - D.row_bits);
   parallel_for(nb, [&](uint64_t b0, uint64_t b1) {
     RowParts rp;
-    std::vector<uint32_t> plus, cols, depth(B);
-    std::vector<BitWriter> rows(B);
-    std::vector<uint64_t> cost(B + 1);
+    std::vector<uint32_t> plus, cols, depth(B), hdr(B), escs;
+    BitWriter body;
     for (uint64_t b = b0; b < b1; ++b) {
-      uint32_t r0 = (uint32_t)(b * B), r1 = (uint32_t)std::min<uint64_t>(g.n, (b + 1) * B);
-      uint32_t nr = r1 - r0;
+      const uint32_t r0 = (uint32_t)(b * B), r1 = (uint32_t)std::min<uint64_t>(g.n, (b + 1) * B);
+      const uint32_t nr = r1 - r0;
       cols.clear();
-      cost[0] = 0;
-      uint64_t adds = 0;
+      escs.clear();
+      body.words.clear();
+      body.nbits = 0;
+      uint64_t adds = 0, codes = 0;
+      std::fill(hdr.begin(), hdr.end(), 0u);
       for (uint32_t k = 0; k < nr; ++k) {
-        uint32_t i = r0 + k;
-        uint32_t r = dec.ref_dist[i];
+        const uint32_t i = r0 + k;
+        const uint32_t r = dec.ref_dist[i];
         if (r && k < r) throw std::runtime_error("BV-D: reference crosses a block");
         depth[k] = r ? depth[k - r] + 1 : 0;
         bdepth[b] = std::max(bdepth[b], depth[k]);
         split_row(g, i, r, bp.min_interval, rp, plus);
-        BitWriter& bw = rows[k];
-        bw.words.clear();
-        bw.nbits = 0;
-        bw.put(r, D.ref_bits);
-        if (r) {
-          bw.gamma(rp.minus.size());
-          write_gapped_zeta(bw, rp.minus, i, bp.zeta_k);
+        const uint32_t nm = (uint32_t)rp.minus.size(), ns = (uint32_t)rp.res.size(), ni = (uint32_t)rp.ints.size();
+        uint32_t wp = 0, wl = 0;
+        for (uint32_t c : rp.minus) wp = std::max(wp, bits_of(fold_signed((int64_t)c - (int64_t)i)));
+        for (uint32_t c : rp.res) wp = std::max(wp, bits_of(fold_signed((int64_t)c - (int64_t)i)));
+        for (auto& iv : rp.ints) {
+          wp = std::max(wp, bits_of(fold_signed((int64_t)iv.first - (int64_t)i)));
+          wl = std::max(wl, bits_of(iv.second - bp.min_interval));
         }
-        bw.gamma(rp.ints.size());
-        uint64_t prev_end = 0;
-        for (size_t t = 0; t < rp.ints.size(); ++t) {
-          uint64_t left = rp.ints[t].first;
-          if (t == 0) bw.gamma(fold_signed((int64_t)left - (int64_t)i));
-          else bw.gamma(left - prev_end - 1);
-          bw.gamma(rp.ints[t].second - bp.min_interval);
-          prev_end = left + rp.ints[t].second;
-          cols.push_back((uint32_t)left);
-          cols.push_back((uint32_t)(left + rp.ints[t].second - 1));
+        const bool esc = nm >= kHdrMinusEsc || ns >= kHdrResEsc || ni >= kHdrIntEsc;
+        hdr[k] = make_hdr(r, std::min(nm, kHdrMinusEsc), std::min(ns, kHdrResEsc), std::min(ni, kHdrIntEsc), wp, wl);
+        if (esc) {
+          // all three counts escape together; the real counts go to the escape
+          // table (row, #minus, #residual, #interval) after the headers
+          hdr[k] = make_hdr(r, kHdrMinusEsc, kHdrResEsc, kHdrIntEsc, wp, wl);
+          escs.push_back(k);
+          escs.push_back(nm);
+          escs.push_back(ns);
+          escs.push_back(ni);
         }
-        bw.gamma(rp.res.size());
-        write_gapped_zeta(bw, rp.res, i, bp.zeta_k);
+        for (uint32_t c : rp.minus) body.put(fold_signed((int64_t)c - (int64_t)i), (int)wp);
+        for (uint32_t c : rp.res) body.put(fold_signed((int64_t)c - (int64_t)i), (int)wp);
+        for (auto& iv : rp.ints) {
+          body.put(fold_signed((int64_t)iv.first - (int64_t)i), (int)wp);
+          body.put(iv.second - bp.min_interval, (int)wl);
+          cols.push_back(iv.first);
+          cols.push_back(iv.first + iv.second - 1);
+        }
         for (uint32_t c : rp.minus) cols.push_back(c);
         for (uint32_t c : rp.res) cols.push_back(c);
-        uint64_t ncodes = rp.minus.size() + rp.res.size();
-        cost[k + 1] = cost[k] + 24 + 10 * ncodes + 14 * rp.ints.size();
-        adds += (r ? 1 : 0) + rp.minus.size() + rp.res.size() + 2 * rp.ints.size();
-        bbits[b] += bw.nbits;
+        codes += nm + ns + 2ull * ni;
+        adds += (r ? 1 : 0) + nm + ns + 2ull * ni;
       }
       badds[b] = adds;
-      // contiguous, cost-balanced row ranges per lane
-      std::vector<uint32_t> start(T + 1, nr);
-      start[0] = 0;
-      uint32_t k = 0;
-      for (uint32_t t = 1; t < T; ++t) {
-        uint64_t target = cost[nr] * t / T;
-        while (k < nr && cost[k] < target) ++k;
-        // pick the nearer of k-1 / k
-        uint32_t cut = k;
-        if (k > start[t - 1] && k > 0 && target - cost[k - 1] < cost[k] - target) cut = k - 1;
-        if (cut < start[t - 1]) cut = start[t - 1];
-        start[t] = cut;
-      }
-      start[T] = nr;
+      bcodes[b] = codes;
       BitWriter& out = bstream[b];
-      for (uint32_t t = 0; t < T; ++t) {
-        out.align(8);
-        uint64_t byte = out.nbits / 8;
-        if (byte >= max_off) throw std::runtime_error("BV-D: block stream too large for the lane table");
-        L.lanes[b * T + t] = (uint32_t)(byte << D.row_bits) | start[t];
-        for (uint32_t q = start[t]; q < start[t + 1]; ++q) out.append(rows[q]);
-      }
+      for (uint32_t q = 0; q < B; ++q) out.put(q < nr ? hdr[q] : 0u, 32);
+      for (uint32_t e : escs) out.put(e, 32);
+      bbits[b] = (uint64_t)nr * 32 + escs.size() * 32 + body.nbits;
+      out.append(body);
       out.align(128);
       // x window: the W-range covering the most gathered columns
       std::sort(cols.begin(), cols.end());
-      uint32_t best = 0, best_lo = r0;
+      uint64_t best = 0, best_lo = r0;
       for (size_t a = 0, e = 0; a < cols.size(); ++a) {
         while (e < cols.size() && cols[e] < (uint64_t)cols[a] + W) ++e;
-        if (e - a > best) { best = (uint32_t)(e - a); best_lo = cols[a]; }
+        if (e - a > best) { best = e - a; best_lo = cols[a]; }
       }
-      // centre the covering range inside the window, align to 16
       uint64_t lo = best_lo;
       if (!cols.empty()) {
-        auto hi_it = std::lower_bound(cols.begin(), cols.end(), (uint64_t)best_lo + W);
-        uint32_t hi = *(hi_it - 1);
-        uint64_t slack = (uint64_t)best_lo + W - 1 - hi;
+        auto hi_it = std::lower_bound(cols.begin(), cols.end(), (uint32_t)std::min<uint64_t>(best_lo + W, 0xffffffffu));
+        const uint32_t hi = *(hi_it - 1);
+        const uint64_t slack = best_lo + W - 1 - hi;
         lo = best_lo >= slack / 2 ? best_lo - slack / 2 : 0;
       }
       lo &= ~15ull;
+      uint64_t inwin = 0;
+      for (uint32_t c : cols) inwin += (c >= lo && c < lo + W);
+      bgath[b] = cols.size();
+      bin[b] = inwin;
       L.blocks[b].wlo = (uint32_t)lo;
       L.blocks[b].nwords = (uint32_t)(out.nbits / 32);
     }
   });
-  uint64_t off = 0, maxw = 0;
+  uint64_t off = 0, maxw = 0, g_all = 0, g_in = 0;
   for (uint32_t b = 0; b < nb; ++b) {
     L.blocks[b].word_offset = off;
     off += L.blocks[b].nwords;
     maxw = std::max<uint64_t>(maxw, L.blocks[b].nwords);
     L.stats.row_bits += bbits[b];
+    L.stats.codes += bcodes[b];
     L.adds_per_product += badds[b];
+    g_all += bgath[b];
+    g_in += bin[b];
     D.max_depth = std::max(D.max_depth, bdepth[b]);
   }
   D.max_block_words = (uint32_t)maxw;
+  {
+    std::vector<uint32_t> sz(nb);
+    for (uint32_t b = 0; b < nb; ++b) sz[b] = L.blocks[b].nwords;
+    std::sort(sz.begin(), sz.end());
+    L.stats.p995_block_words = nb ? sz[std::min<uint64_t>(nb - 1, (uint64_t)(nb * 0.995))] : 0;
+  }
+  L.stats.window_coverage = g_all ? (double)g_in / (double)g_all : 1.0;
   L.words.assign(off + 8, 0);  // guard words
   parallel_for(nb, [&](uint64_t b0, uint64_t b1) {
     for (uint64_t b = b0; b < b1; ++b)
@@ -188,7 +182,6 @@ BvdLayout build_bvd(const BvDecoded& dec, const BvParams& bp, const BvdOptions& 
         std::memcpy(L.words.data() + L.blocks[b].word_offset, bstream[b].words.data(), (size_t)L.blocks[b].nwords * 4);
   });
   L.stats.stream_bytes = off * 4;
-  L.stats.lane_table_bytes = (uint64_t)nb * T * 4;
   L.stats.block_table_bytes = (uint64_t)nb * sizeof(BvdBlockInfo);
   return L;
 }

@@ -8,22 +8,22 @@ namespace cmvg {
 
 struct BvdOptions {
   uint32_t block_rows = 1024;
-  uint32_t lanes = 128;
   uint32_t window = 2048;
 };
 
 struct BvdStats {
   uint64_t row_bits = 0;          // sum of row-record bits (the coded payload)
   uint64_t stream_bytes = 0;      // incl. lane alignment and block padding
-  uint64_t lane_table_bytes = 0;
   uint64_t block_table_bytes = 0;
+  uint64_t codes = 0;             // body codes (decode loop iterations)
+  uint32_t p995_block_words = 0;  // block-stream size covering 99.5% of blocks
+  double window_coverage = 1.0;   // fraction of gathered columns inside the x-window
 };
 
 struct BvdLayout {
   BvdDims dims{};
   std::vector<uint32_t> words;
   std::vector<BvdBlockInfo> blocks;
-  std::vector<uint32_t> lanes;
   uint64_t adds_per_product = 0;
   BvdStats stats;
 };

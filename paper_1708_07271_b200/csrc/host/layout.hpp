@@ -1,28 +1,61 @@
 // BV-D: the device layout of a BV-compressed matrix (shared by the host
 // builder and the CUDA kernels; plain types only).
 //
-// What it stores (per row i, in row order) is the reference's differential
-// row (cmv::ReferencedMatrix, reference include/cmv/ref_matrix.hpp:13-52 and
-// PAPER.md:156-196) with BV's codes:
-//   bits(ref_bits)  r: reference distance, 0 = self-coded
-//   if r > 0:       gamma(#minus); minus columns = the reference entries that
-//                   BV's copy blocks skip, zeta_k gap-coded (first sign-folded
-//                   relative to i, then gap-1)
-//   gamma(#intervals); intervals exactly as in the BV stream
-//   gamma(#residuals); residuals exactly as in the BV stream
-// so the product is  y_i = y_{i-r} - sum_minus x + sum_intervals x (O(1) from
-// an exclusive prefix of x) + sum_residuals x  (ref_matvec.hpp:20-31).
+// It stores per row i the reference's differential row (cmv::ReferencedMatrix,
+// reference include/cmv/ref_matrix.hpp:13-52) taken from the
+// BV stream: the BV reference distance r, the minus entries (the reference
+// entries that BV's copy blocks skip) and BV's extra list split exactly as BV
+// splits it, into intervals and residuals.  The product is
+//     y_i = y_{i-r} - sum_minus x + sum_intervals x + sum_residuals x
+// (ref_matvec.hpp:20-31), an interval in O(1) from a prefix of x.
 //
-// Rows are grouped in blocks of `block_rows` (a multiple of the BV segment, so
-// reference chains never leave a block).  Each block's stream is split into
-// `lanes` contiguous row ranges with balanced decode cost; lane k's bits start
-// byte-aligned and the lane table entry packs (byte offset << row_bits) |
-// first row.  Each block also carries an x-window start: the CTA stages
-// x[wlo, wlo + window) (plus a tile-local prefix) in shared memory.
+// The layout is built for the decoder's instruction budget, not for bits (the
+// product is issue-bound, far from the HBM roofline): every code is a
+// fixed-width field whose bit offset is known from the row header, so codes
+// decode independently and rows can be processed in any order.
+//
+// Rows are grouped in blocks of `block_rows` (a multiple of the BV segment,
+// so reference chains never leave a block).  A block's stream is
+//   [row headers: block_rows x u32][row bodies, bit-packed, row order]  (16-B padded)
+// Row header (u32, MSB first):
+//   r (3) | #minus (5, 31 = escape) | #residual (6, 63 = escape) |
+//   #interval (4, 15 = escape) | wp (5) | wl (5) | 0 (4)
+// Row body (bits): [3 x 32-bit counts if any count is escaped]
+//   [#minus + #residual point codes, wp bits each: fold(col - i)]
+//   [#interval x (fold(left - i) in wp bits, len - Lmin in wl bits)]
+// fold(d) = 2d for d >= 0, -2d-1 for d < 0.  The row body length follows from
+// the header, so the kernel computes every row's bit offset with one scan.
+// Each block also carries an x-window start: the CTA stages x[wlo, wlo + W)
+// (plus a tile-local prefix) in shared memory.
 #pragma once
 #include <cstdint>
 
+#ifndef __CUDACC__
+#ifndef __host__
+#define __host__
+#define __device__
+#endif
+#endif
+
 namespace cmvg {
+
+constexpr uint32_t kHdrMinusEsc = 31;
+constexpr uint32_t kHdrResEsc = 63;
+constexpr uint32_t kHdrIntEsc = 15;
+
+__host__ __device__ constexpr uint32_t hdr_r(uint32_t h) { return h >> 29; }
+__host__ __device__ constexpr uint32_t hdr_nm(uint32_t h) { return (h >> 24) & 31u; }
+__host__ __device__ constexpr uint32_t hdr_ns(uint32_t h) { return (h >> 18) & 63u; }
+__host__ __device__ constexpr uint32_t hdr_ni(uint32_t h) { return (h >> 14) & 15u; }
+__host__ __device__ constexpr uint32_t hdr_wp(uint32_t h) { return (h >> 9) & 31u; }
+__host__ __device__ constexpr uint32_t hdr_wl(uint32_t h) { return (h >> 4) & 31u; }
+__host__ __device__ constexpr bool hdr_escaped(uint32_t h) {
+  return hdr_nm(h) == kHdrMinusEsc || hdr_ns(h) == kHdrResEsc || hdr_ni(h) == kHdrIntEsc;
+}
+__host__ __device__ constexpr uint32_t make_hdr(uint32_t r, uint32_t nm, uint32_t ns, uint32_t ni, uint32_t wp,
+                                                uint32_t wl) {
+  return (r << 29) | (nm << 24) | (ns << 18) | (ni << 14) | (wp << 9) | (wl << 4);
+}
 
 struct BvdBlockInfo {
   uint64_t word_offset;  // first u32 word of this block's stream (16-byte aligned)
@@ -33,12 +66,8 @@ struct BvdBlockInfo {
 struct BvdDims {
   uint32_t n;            // rows (== columns)
   uint32_t block_rows;   // B
-  uint32_t lanes;        // T (decode lanes per block = threads per CTA)
-  uint32_t row_bits;     // width of the row field in a lane entry (log2(B)+1)
   uint32_t window;       // x-window entries (multiple of 16)
-  uint32_t ref_bits;     // bits of the reference-distance field
   uint32_t min_interval;
-  uint32_t zeta_k;
   uint32_t nblocks;
   uint32_t max_block_words;
   uint32_t max_depth;    // longest reference chain (drives the level phases)

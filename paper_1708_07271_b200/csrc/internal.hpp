@@ -123,6 +123,9 @@ struct cmvg_csr {
 struct cmvg_bvstream {
   BvStream s;
 };
+struct cmvg_layout {
+  BvdLayout L;
+};
 struct cmvg_graph {
   int device = 0;
   uint32_t n = 0;
@@ -134,8 +137,9 @@ struct cmvg_graph {
   uint32_t interval_mode = CMVG_INTERVALS_PREFIX;
   uint64_t bv_bits = 0, adds = 0;
   BvdStats stats;
+  uint32_t threads = 128;  // threads per CTA
   // BV-D layout (this shard)
-  DevBuf words, blocks, lanes;
+  DevBuf words, blocks;
   // canonical BV stream (whole graph) for decode_csr
   DevBuf bv_words, bv_seg;
   uint64_t nseg = 0;
@@ -147,13 +151,12 @@ struct cmvg_graph {
   // scratch (scatter / pagerank)
   DevBuf scratch;
   uint64_t device_bytes() const {
-    return words.bytes + blocks.bytes + lanes.bytes + bv_words.bytes + bv_seg.bytes + refd.bytes;
+    return words.bytes + blocks.bytes + bv_words.bytes + bv_seg.bytes + refd.bytes;
   }
   BvdDev dev() const {
     BvdDev d{};
     d.words = words.as<uint32_t>();
     d.blocks = blocks.as<BvdBlockInfo>();
-    d.lanes = lanes.as<uint32_t>();
     d.d = dims;
     d.block_begin = block_begin;
     d.row_begin = row_begin;

@@ -67,7 +67,7 @@ def test_gather_matches_matvec_ref(cuda):
 
 
 @pytest.mark.parametrize("lanes,block_rows,window", [(128, 1024, 2048), (256, 1024, 2048), (64, 2048, 4096),
-                                                      (32, 1024, 512), (128, 4096, 1024)])
+                                                      (32, 1024, 512), (128, 4096, 1024), (256, 2048, 1536)])
 def test_gather_layout_variants(cuda, lanes, block_rows, window):
     g = make_graph(2, n=(1 << 16) + 777)  # ragged last block
     check_gather(g, bv_params(2), P.CreateOptions(lanes=lanes, block_rows=block_rows, window=window))
@@ -100,7 +100,7 @@ def test_gather_edge_cases(cuda):
         [[]],
         [[0]],
         [[], [], []],
-        [[0, 1, 2, 3, 4, 5, 6, 7, 8, 9], [], [9], [0, 9]],
+        [[0, 1, 2, 3, 4, 5, 6, 7, 8, 9], [], [9], [0, 9]] + [[]] * 6,
         [list(range(0, 3000)), list(range(1, 3001)), [2999, 3000], list(range(5, 3001, 2))] + [[]] * 2997,
     ]
     for rows in cases:
