@@ -41,9 +41,9 @@ def parse():
     ap.add_argument("--dtype", choices=["f64", "f32"], default="f64")
     ap.add_argument("--form", choices=["gather", "scatter"], default="gather")
     ap.add_argument("--interval-mode", choices=["prefix", "direct"], default="prefix")
-    ap.add_argument("--lanes", type=int, default=128)
+    ap.add_argument("--lanes", type=int, default=256)
     ap.add_argument("--block-rows", type=int, default=1024)
-    ap.add_argument("--window", type=int, default=2048)
+    ap.add_argument("--window", type=int, default=1536)
     ap.add_argument("--stream-cap-words", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")

@@ -147,8 +147,9 @@ int cmvg_destroy(cmvg_graph* g);
  * (no GPU needed; used for layout statistics and tests). */
 int cmvg_layout_info(const cmvg_bvstream* s, const cmvg_create_opts* opts, cmvg_graph_info* out);
 /* Host-only: build the device layout and copy it out (tests re-decode it on
- * the CPU).  words: u32[*nwords]; blocks: 4 x u32 per block
- * {word_offset lo, word_offset hi, nwords, wlo}.  Free with cmvg_layout_free. */
+ * the CPU).  words: u32[*nwords]; blocks: 8 x u32 per block
+ * {word_offset lo, word_offset hi, nwords, wlo, nesc, 0, 0, 0}.  Free with
+ * cmvg_layout_free. */
 typedef struct cmvg_layout cmvg_layout;
 int cmvg_layout_export(const cmvg_bvstream* s, const cmvg_create_opts* opts, cmvg_layout** out);
 const uint32_t* cmvg_layout_words(const cmvg_layout* l, uint64_t* nwords);

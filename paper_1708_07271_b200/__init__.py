@@ -305,7 +305,7 @@ class BvStream:
         try:
             nw, nb = C.c_uint64(), C.c_uint32()
             w = _np_view(lib.cmvg_layout_words(h, C.byref(nw)), nw.value, np.uint32).copy()
-            b = _np_view(lib.cmvg_layout_blocks(h, C.byref(nb)), nb.value * 4, np.uint32).reshape(-1, 4).copy()
+            b = _np_view(lib.cmvg_layout_blocks(h, C.byref(nb)), nb.value * 8, np.uint32).reshape(-1, 8).copy()
         finally:
             lib.cmvg_layout_free(h)
         return w, b
@@ -327,8 +327,8 @@ class BvStream:
 class CreateOptions:
     device: int = 0
     block_rows: int = 1024
-    lanes: int = 128
-    window: int = 2048
+    lanes: int = 256
+    window: int = 1536
     stream_cap_words: int = 0  # 0 = auto (covers 99.5% of blocks)
     interval_mode: str = "prefix"  # or "direct"
     row_begin: int = 0

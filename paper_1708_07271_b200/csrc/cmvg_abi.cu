@@ -164,8 +164,8 @@ void cmvg_default_opts(cmvg_create_opts* o) {
   if (!o) return;
   o->device = 0;
   o->block_rows = 1024;
-  o->lanes = 128;
-  o->window = 2048;
+  o->lanes = 256;
+  o->window = 1536;
   o->stream_cap_words = 0;
   o->interval_mode = CMVG_INTERVALS_PREFIX;
   o->row_begin = 0;
@@ -182,7 +182,9 @@ int cmvg_create(const cmvg_bvstream* s, const cmvg_create_opts* opts_in, cmvg_gr
     require(bs.params.window <= 7, "the device layout supports BV windows w <= 7");
     require(bs.params.zeta_k == 3, "device kernels support zeta_3 residuals");
     require(bs.n > 0, "empty graph");
-    require(o.lanes >= 32 && o.lanes <= 256 && o.lanes % 32 == 0, "lanes (threads per block) must be 32..256, a multiple of 32");
+    require(o.lanes >= 32 && o.lanes <= 256 && (o.lanes & (o.lanes - 1)) == 0,
+            "lanes (threads per block) must be a power of two in [32, 256]");
+    require(o.block_rows <= 4 * o.lanes, "block_rows must be <= 4 x threads per block");
     require(o.interval_mode <= CMVG_INTERVALS_DIRECT, "bad interval_mode");
     uint32_t row_end = o.row_end ? o.row_end : bs.n;
     require(o.row_begin < row_end && row_end <= bs.n, "bad shard row range");
@@ -302,6 +304,7 @@ const uint32_t* cmvg_layout_words(const cmvg_layout* l, uint64_t* nwords) {
   return l->L.words.data();
 }
 const uint32_t* cmvg_layout_blocks(const cmvg_layout* l, uint32_t* nblocks) {
+  static_assert(sizeof(BvdBlockInfo) == 32, "block info is 8 u32");
   if (!l) return nullptr;
   if (nblocks) *nblocks = (uint32_t)l->L.blocks.size();
   return reinterpret_cast<const uint32_t*>(l->L.blocks.data());
@@ -356,9 +359,8 @@ namespace {
 
 template <typename XT, typename YT>
 void launch_gather(cmvg_graph* g, const XT* x, YT* y, cudaStream_t st) {
-  const bool prefix = g->interval_mode == CMVG_INTERVALS_PREFIX;
-  GatherSmem L = gather_smem_layout(g->dims, g->stream_cap_words, sizeof(XT), prefix);
-  auto kern = prefix ? bvd_gather_kernel<XT, YT, true> : bvd_gather_kernel<XT, YT, false>;
+  GatherSmem L = gather_smem_layout(g->dims, g->stream_cap_words, sizeof(XT), true);
+  auto kern = bvd_gather_kernel<XT, YT>;
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
   kern<<<g->nblocks, g->threads, L.total, st>>>(g->dev(), x, y);
   CUDA_TRY(cudaGetLastError());

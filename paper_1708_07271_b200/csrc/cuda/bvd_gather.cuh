@@ -7,13 +7,14 @@
 //      shared memory (mbarrier completion) while all threads stage the
 //      x-window x[wlo, wlo+W) and build its tile-local double-double prefix;
 //   2. row setup: row bit offsets (scan of body lengths from the headers) and
-//      warp rounds (rows counting-sorted by point-code count, so the 32 rows
-//      a warp decodes together have near-equal work);
-//   3. each warp decodes its rounds, one row per lane: a loop over point
-//      codes (minus -> -x[c], residual -> +x[c]) then a loop over intervals
-//      (O(1) from the prefix); delta_i is accumulated with Neumaier
-//      compensation, so it carries no cancellation error into the chain;
-//   4. level phases over chain depth: y_i = delta_i + y_{i-r} in
+//      warp rounds (near rows counting-sorted by point-code count, so the 32
+//      rows a warp decodes together have near-equal work);
+//   3. warps claim rounds dynamically; one row per lane: point codes
+//      (minus -> -x[c], residual -> +x[c]) with no bounds checks; then the
+//      rounds of rows with intervals (O(1) from the prefix); then the rare
+//      `far` rows on a bounds-checked path.  delta_i is accumulated with
+//      TwoSum compensation (no cancellation error enters the chain);
+//   4. level scheduler over chain depth: y_i = delta_i + y_{i-r} in
 //      double-double (the reference's order, ref_matvec.hpp:23-25);
 //   5. coalesced store of y.
 #pragma once
@@ -44,110 +45,131 @@ __host__ __device__ inline GatherSmem gather_smem_layout(const BvdDims& d, uint3
   return s;
 }
 
-// Phase A (point rounds): each warp takes 32 rows of similar point-code count
-// (one per lane) and accumulates -x[c] for minus codes, +x[c] for residual
-// codes; writes delta (hi, lo).  Phase B (interval rounds, after a barrier):
-// the rows that have intervals, grouped by interval count, add their O(1)
-// interval sums to delta.  Every row is owned by one lane in each phase.
-template <class XWinT>
-__device__ __forceinline__ void decode_points(const RowCtx& c, const uint32_t* __restrict__ base, const XWinT& xw,
-                                              int32_t r0, double* s_yhi, float* s_ylo) {
+struct RowDesc {
+  uint32_t k, h, off;
+  RowCounts rc;
+  bool act;
+};
+
+template <class S>
+__device__ __forceinline__ RowDesc round_row(const RowCtx& c, const S& src, const uint16_t* perm, uint32_t slot,
+                                             uint32_t end, int nesc) {
+  RowDesc r;
+  r.act = slot < end;
+  r.k = r.act ? perm[slot] : 0u;
+  r.h = r.act ? src.w(r.k) : 0u;
+  r.rc = RowCounts{0, 0, 0};
+  if (r.act) r.rc = row_counts(src, c.B, r.h, r.k, nesc);
+  r.off = r.act ? c.rowoff[r.k] : 0u;
+  return r;
+}
+
+// Phase 1 (point rounds): one row per lane, rows of similar point-code count
+// per warp.  minus -> -x[c], residual -> +x[c]; `far` rows (some column
+// outside the block's x-window) take the bounds-checked accessor.
+template <class S, class XW>
+__device__ __forceinline__ void gather_points(const RowCtx& c, const S& src, const XW& xw, int32_t r0,
+                                              double* s_yhi, float* s_ylo) {
+  const int nesc = c.misc[kNesc];
   const uint32_t lane = threadIdx.x & 31u;
-  const int nesc = c.misc[0];
   for (;;) {
-    uint32_t rb = 0;  // next round of 32 rows, claimed dynamically (balances the warps)
-    if (lane == 0) rb = 32u * (uint32_t)atomicAdd(&c.misc[3], 1);
-    rb = __shfl_sync(0xffffffffu, rb, 0);
+    const uint32_t rb = next_round(&c.misc[kRoundP]);
     if (rb >= c.nr) break;
-    const uint32_t slot = rb + lane;
-    const bool act = slot < c.nr;
-    const uint32_t k = act ? c.perm[slot] : 0u;
-    const uint32_t h = act ? base[k] : 0u;
-    RowCounts rc{0, 0, 0};
-    if (act) rc = row_counts(base, c.B, h, k, nesc);
-    const uint32_t wp = hdr_wp(h);
-    const int32_t i = r0 + (int32_t)k;
-    const uint32_t np = rc.nm + rc.ns;
-    uint32_t off = act ? c.rowoff[k] : 0u;
+    const RowDesc r = round_row(c, src, c.perm, rb + lane, c.nr, nesc);
+    const uint32_t wp = hdr_wp(r.h);
+    const bool far = hdr_far(r.h);
+    const bool any_far = __any_sync(0xffffffffu, far);
+    // window-relative column of code value v: ib + v
+    const uint32_t ib = (uint32_t)(r0 + (int32_t)r.k - (int32_t)code_bias(wp) - (int32_t)xw.wlo);
+    const uint32_t np = r.rc.nm + r.rc.ns, nm = r.rc.nm;
+    uint32_t off = r.off;
     double acc = 0.0, comp = 0.0;
     const uint32_t tp = __reduce_max_sync(0xffffffffu, np);
-    for (uint32_t t = 0; t < tp; ++t) {
-      double term = 0.0;
-      if (t < np) {
-        const int32_t col = i + unfold32(extract_bits(base, off, wp));
-        const double xv = xw.at(col);
-        term = t < rc.nm ? -xv : xv;
-        off += wp;
+    if (!any_far) {
+#pragma unroll 4
+      for (uint32_t t = 0; t < tp; ++t) {
+        const bool on = t < np;
+        const uint32_t v = extract_bits(src, off, wp);
+        const double xv = xw.at_near(on ? ib + v : 0u);
+        const double term = on ? (t < nm ? -xv : xv) : 0.0;
+        tsum(acc, comp, term);
+        off += on ? wp : 0u;
       }
-      nadd(acc, comp, term);
+    } else {
+      for (uint32_t t = 0; t < tp; ++t) {
+        const bool on = t < np;
+        const uint32_t v = extract_bits(src, off, wp);
+        double xv = 0.0;
+        if (on) xv = far ? xw.at((int32_t)(ib + v) + (int32_t)xw.wlo) : xw.at_near(ib + v);
+        const double term = on ? (t < nm ? -xv : xv) : 0.0;
+        tsum(acc, comp, term);
+        off += on ? wp : 0u;
+      }
     }
-    if (act) {
+    if (r.act) {
       const double hi = acc + comp;
-      s_yhi[k] = hi;
-      s_ylo[k] = (float)(comp - (hi - acc));
+      s_yhi[r.k] = hi;
+      s_ylo[r.k] = (float)(comp - (hi - acc));
     }
   }
 }
 
-template <class XWinT>
-__device__ __forceinline__ void decode_intervals(const RowCtx& c, const uint32_t* __restrict__ base, const XWinT& xw,
-                                                 int32_t r0, uint32_t lmin, double* s_yhi, float* s_ylo) {
+// Phase 2 (after a barrier): rows with intervals, grouped by interval count,
+// add their O(1) interval sums to delta.
+template <class S, class XW>
+__device__ __forceinline__ void gather_intervals(const RowCtx& c, const S& src, const XW& xw, int32_t r0, uint32_t lmin,
+                                                 double* s_yhi, float* s_ylo) {
+  const int nesc = c.misc[kNesc];
+  const uint32_t nri = (uint32_t)c.misc[kNInt];
   const uint32_t lane = threadIdx.x & 31u;
-  const int nesc = c.misc[0];
-  const uint32_t nri = (uint32_t)c.misc[2];
   for (;;) {
-    uint32_t rb = 0;
-    if (lane == 0) rb = 32u * (uint32_t)atomicAdd(&c.misc[4], 1);
-    rb = __shfl_sync(0xffffffffu, rb, 0);
+    const uint32_t rb = next_round(&c.misc[kRoundI]);
     if (rb >= nri) break;
-    const uint32_t slot = rb + lane;
-    const bool act = slot < nri;
-    const uint32_t k = act ? c.permi[slot] : 0u;
-    const uint32_t h = act ? base[k] : 0u;
-    RowCounts rc{0, 0, 0};
-    if (act) rc = row_counts(base, c.B, h, k, nesc);
-    const uint32_t wp = hdr_wp(h), wl = hdr_wl(h);
-    const int32_t i = r0 + (int32_t)k;
-    uint32_t off = act ? c.rowoff[k] + (rc.nm + rc.ns) * wp : 0u;
+    const RowDesc r = round_row(c, src, c.permi, rb + lane, nri, nesc);
+    const uint32_t wp = hdr_wp(r.h), wl = hdr_wl(r.h);
+    const bool far = hdr_far(r.h);
+    const uint32_t ib = (uint32_t)(r0 + (int32_t)r.k - (int32_t)code_bias(wp) - (int32_t)xw.wlo);
+    uint32_t off = r.off + (r.rc.nm + r.rc.ns) * wp;
     double acc = 0.0, comp = 0.0;
-    const uint32_t ti = __reduce_max_sync(0xffffffffu, rc.ni);
+    const uint32_t ti = __reduce_max_sync(0xffffffffu, r.rc.ni);
     for (uint32_t t = 0; t < ti; ++t) {
+      const bool on = t < r.rc.ni;
+      const uint32_t a = ib + extract_bits(src, off, wp);
+      const uint32_t len = extract_bits(src, off + wp, wl) + lmin;
       double hi = 0.0, lo = 0.0;
-      if (t < rc.ni) {
-        const int32_t left = i + unfold32(extract_bits(base, off, wp));
-        const uint32_t len = extract_bits(base, off + wp, wl) + lmin;
-        hi = xw.isum(left, len, lo);
-        off += wp + wl;
+      if (on) {
+        if (!far) hi = xw.isum_near(a, len, lo);
+        else hi = xw.isum((int32_t)a + (int32_t)xw.wlo, len, lo);
       }
-      nadd(acc, comp, hi);
+      tsum(acc, comp, hi);
       comp += lo;
+      off += on ? wp + wl : 0u;
     }
-    if (act) {
-      double hi = s_yhi[k], lo = (double)s_ylo[k];
+    if (r.act) {
+      double hi = s_yhi[r.k], lo = (double)s_ylo[r.k];
       dd_add(hi, lo, acc, comp);
-      s_yhi[k] = hi;
-      s_ylo[k] = (float)lo;
+      s_yhi[r.k] = hi;
+      s_ylo[r.k] = (float)lo;
     }
   }
 }
 
-template <typename XT, typename YT, bool PREFIX>
-__device__ __forceinline__ void gather_block(RowCtx& rc, const uint32_t* __restrict__ base, const XWin<XT, PREFIX>& xw,
-                                             const BvdDims& D, uint32_t r0, double* s_yhi, float* s_ylo, YT* yb) {
-  rc.base = base;
-  row_setup(rc);
-  decode_points(rc, base, xw, (int32_t)r0, s_yhi, s_ylo);
+template <typename XT, typename YT, bool PREFIX, class S>
+__device__ __forceinline__ void gather_block(RowCtx& rc, const S& src, const XWin<XT, PREFIX>& xw, const BvdDims& D,
+                                             uint32_t r0, int nesc, double* s_yhi, float* s_ylo, YT* yb) {
+  row_setup(rc, src, nesc);
+  gather_points(rc, src, xw, (int32_t)r0, s_yhi, s_ylo);
   __syncthreads();
-  decode_intervals(rc, base, xw, (int32_t)r0, D.min_interval, s_yhi, s_ylo);
+  gather_intervals(rc, src, xw, (int32_t)r0, D.min_interval, s_yhi, s_ylo);
   __syncthreads();
   chain_and_store(s_yhi, s_ylo, rc, yb);
 }
 
-template <typename XT, typename YT, bool PREFIX>
+template <typename XT, typename YT>
 __global__ void __launch_bounds__(256) bvd_gather_kernel(BvdDev g, const XT* __restrict__ x, YT* __restrict__ y) {
   extern __shared__ __align__(16) unsigned char smem[];
   const BvdDims& D = g.d;
-  const GatherSmem L = gather_smem_layout(D, g.stream_cap_words, sizeof(XT), PREFIX);
+  const GatherSmem L = gather_smem_layout(D, g.stream_cap_words, sizeof(XT), true);
   const uint32_t bl = blockIdx.x;  // index into this shard's tables
   const uint32_t b = g.block_begin + bl;
   const BvdBlockInfo bi = g.blocks[bl];
@@ -156,8 +178,8 @@ __global__ void __launch_bounds__(256) bvd_gather_kernel(BvdDev g, const XT* __r
 
   RowCtx rc = carve_rows(smem, L.rows, D.block_rows, nr);
   uint32_t* s_stream = reinterpret_cast<uint32_t*>(smem);
-  stage_stream_begin(g, bi, s_stream, rc.bar);
-  XWin<XT, PREFIX> xw;
+  const bool staged = stage_stream_begin(g, bi, s_stream, rc.bar);
+  XWin<XT, true> xw;
   xw.carve(smem + L.off_x, D.window);
   xw.x = x;
   xw.wlo = bi.wlo;
@@ -167,10 +189,13 @@ __global__ void __launch_bounds__(256) bvd_gather_kernel(BvdDev g, const XT* __r
   double* s_yhi = reinterpret_cast<double*>(smem + L.off_yhi);
   float* s_ylo = reinterpret_cast<float*>(smem + L.off_ylo);
   YT* yb = y + (r0 - g.row_begin);
-  if (bi.nwords <= g.stream_cap_words)  // CTA-uniform: shared-memory decode path
-    gather_block<XT, YT, PREFIX>(rc, s_stream, xw, D, r0, s_yhi, s_ylo, yb);
-  else
-    gather_block<XT, YT, PREFIX>(rc, g.words + bi.word_offset, xw, D, r0, s_yhi, s_ylo, yb);
+  if (staged) {  // CTA-uniform
+    const Src<true> src{smem_u32(s_stream)};
+    gather_block<XT, YT, true>(rc, src, xw, D, r0, (int)bi.nesc, s_yhi, s_ylo, yb);
+  } else {
+    const Src<false> src{g.words + bi.word_offset};
+    gather_block<XT, YT, true>(rc, src, xw, D, r0, (int)bi.nesc, s_yhi, s_ylo, yb);
+  }
 }
 
 }  // namespace cmvg

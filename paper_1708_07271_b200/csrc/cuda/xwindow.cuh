@@ -1,12 +1,14 @@
 // The per-block x-window in shared memory: x[wlo, wlo + W) staged with
 // coalesced loads into a padded layout (16-entry tiles at a stride of 17
-// entries, so a thread can walk one tile with 2-way bank conflicts), plus a
-// tile-local exclusive prefix in double-double (hi fp64, lo fp32) and the
-// tile totals.  An interval [a, e) spanning at most two tiles is then
-//     (e tile != a tile ? T[a tile] : 0) - P[a] + P[e]
-// evaluated with two TwoSums -- O(1), branch-free, and accurate to ~1e-30
-// absolute, so interval sums carry no rounding error into the reference
-// chain (the north star's O(1) interval evaluation from an exclusive prefix).
+// entries, so a thread can walk one tile with 2-way bank conflicts), plus an
+// exclusive prefix of the window in double-double, stored two-level: P[j]
+// within j's 16-entry tile and Q[t] over whole tiles (hi fp64, lo fp32).  An
+// interval [a, e) is then
+//     (Q[e>>4] - Q[a>>4]) + (P[e] - P[a])
+// evaluated with three TwoSums -- O(1) for any length, branch-free, and
+// accurate to ~1e-28 absolute, so interval sums carry no rounding error into
+// the reference chain (the north star's O(1) interval evaluation from an
+// exclusive prefix of x).
 #pragma once
 #include <cstdint>
 
@@ -21,8 +23,8 @@ __host__ __device__ inline uint32_t xw_bytes(uint32_t W, uint32_t xsize, bool pr
   if (prefix) {
     b += ((padded * 8u + 15u) & ~15u);          // P hi
     b += ((padded * 4u + 15u) & ~15u);          // P lo
-    b += (((W / 16 + 1) * 8u + 15u) & ~15u);    // T hi
-    b += (((W / 16 + 1) * 4u + 15u) & ~15u);    // T lo
+    b += (((W / 16 + 1) * 8u + 15u) & ~15u);    // Q hi
+    b += (((W / 16 + 1) * 4u + 15u) & ~15u);    // Q lo
   }
   return b;
 }
@@ -80,13 +82,78 @@ struct XWin {
           hi = s;
           lo += e;
         }
-        // renormalise the total
-        const double h2 = hi + lo;
+        const double h2 = hi + lo;  // tile total, renormalised
         s_th[t] = h2;
         s_tl[t] = (float)(lo - (h2 - hi));
       }
+      if (tid == 0) {  // P at the window end (index W) is the start of a tile
+        s_ph[xw_pad(W)] = 0.0;
+        s_pl[xw_pad(W)] = 0.0f;
+      }
+      __syncthreads();
+      if (tid < 32) {  // Q: exclusive double-double prefix of the tile totals (one warp)
+        const uint32_t lane = tid, per = (ntiles + 31u) / 32u;
+        double lh = 0.0, ll = 0.0;
+        for (uint32_t q = 0; q < per; ++q) {
+          const uint32_t t = lane * per + q;
+          if (t < ntiles) {
+            double s, e;
+            two_sum(lh, s_th[t], s, e);
+            lh = s;
+            ll += e + (double)s_tl[t];
+          }
+        }
+        double ih = lh, il = ll;  // inclusive warp scan in double-double
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const double uh = __shfl_up_sync(0xffffffffu, ih, o), ul = __shfl_up_sync(0xffffffffu, il, o);
+          if ((int)lane >= o) {
+            double s, e;
+            two_sum(ih, uh, s, e);
+            ih = s;
+            il += ul + e;
+          }
+        }
+        double rh = __shfl_up_sync(0xffffffffu, ih, 1), rl = __shfl_up_sync(0xffffffffu, il, 1);
+        if (lane == 0) rh = rl = 0.0;
+        for (uint32_t q = 0; q < per; ++q) {
+          const uint32_t t = lane * per + q;
+          if (t < ntiles) {
+            const double th = s_th[t];
+            const float tl = s_tl[t];
+            const double h2 = rh + rl;
+            s_th[t] = h2;  // in place: tile total -> exclusive prefix Q[t]
+            s_tl[t] = (float)(rl - (h2 - rh));
+            double s, e;
+            two_sum(rh, th, s, e);
+            rh = s;
+            rl += e + (double)tl;
+          }
+        }
+        if (lane == 31) {
+          const double h2 = ih + il;
+          s_th[ntiles] = h2;
+          s_tl[ntiles] = (float)(il - (h2 - ih));
+        }
+      }
     }
     __syncthreads();
+  }
+
+  // Unchecked accessors for `near` rows (the builder guarantees the window
+  // holds every column and intervals span at most two tiles): j, a are
+  // window-relative.
+  __device__ __forceinline__ double at_near(uint32_t j) const { return (double)s_x[xw_pad(j)]; }
+  __device__ __forceinline__ double isum_near(uint32_t a, uint32_t len, double& lo) const {
+    const uint32_t e = a + len;
+    const uint32_t ta = a >> 4, tb = e >> 4;
+    const uint32_t pa = xw_pad(a), pe = xw_pad(e);
+    double s1, e1, s2, e2, s3, e3;
+    two_sum(s_th[tb], -s_th[ta], s1, e1);
+    two_sum(s1, s_ph[pe], s2, e2);
+    two_sum(s2, -s_ph[pa], s3, e3);
+    lo = e1 + e2 + e3 + (((double)s_tl[tb] - (double)s_tl[ta]) + ((double)s_pl[pe] - (double)s_pl[pa]));
+    return s3;
   }
 
   __device__ __forceinline__ double at(int32_t c) const {
@@ -102,21 +169,7 @@ struct XWin {
     const uint32_t a = (uint32_t)(left - (int32_t)wlo);
     const uint32_t e = a + len;
     if constexpr (PREFIX) {
-      const uint32_t ta = a >> 4, tb = e >> 4;
-      if (a < W && e <= W && tb <= ta + 1) {
-        const bool two = tb != ta;
-        const bool has_e = (e & 15u) != 0;
-        const uint32_t pa = xw_pad(a), pe = xw_pad(e);
-        const double th = two ? s_th[ta] : 0.0;
-        const float tl = two ? s_tl[ta] : 0.0f;
-        const double peh = has_e ? s_ph[pe] : 0.0;
-        const float pel = has_e ? s_pl[pe] : 0.0f;
-        double s1, e1, s2, e2;
-        two_sum(th, -s_ph[pa], s1, e1);
-        two_sum(s1, peh, s2, e2);
-        lo = e1 + e2 + ((double)tl - (double)s_pl[pa] + (double)pel);
-        return s2;
-      }
+      if (a < W && e <= W) return isum_near(a, len, lo);
     } else {
       if (a < W && e <= W && len <= 32) {
         double s = 0.0, c = 0.0;

@@ -73,7 +73,7 @@ BvdLayout build_bvd(const BvDecoded& dec, const BvParams& bp, const BvdOptions& 
   std::vector<uint64_t> bbits(nb, 0), badds(nb, 0), bcodes(nb, 0), bgath(nb, 0), bin(nb, 0);
   std::vector<uint32_t> bdepth(nb, 0);
   parallel_for(nb, [&](uint64_t b0, uint64_t b1) {
-    RowParts rp;
+    std::vector<RowParts> rps(B);
     std::vector<uint32_t> plus, cols, depth(B), hdr(B), escs;
     BitWriter body;
     for (uint64_t b = b0; b < b1; ++b) {
@@ -85,54 +85,22 @@ BvdLayout build_bvd(const BvDecoded& dec, const BvParams& bp, const BvdOptions& 
       body.nbits = 0;
       uint64_t adds = 0, codes = 0;
       std::fill(hdr.begin(), hdr.end(), 0u);
+      // pass 1: split rows, collect gathered columns, choose the x-window
       for (uint32_t k = 0; k < nr; ++k) {
         const uint32_t i = r0 + k;
         const uint32_t r = dec.ref_dist[i];
         if (r && k < r) throw std::runtime_error("BV-D: reference crosses a block");
         depth[k] = r ? depth[k - r] + 1 : 0;
         bdepth[b] = std::max(bdepth[b], depth[k]);
+        RowParts& rp = rps[k];
         split_row(g, i, r, bp.min_interval, rp, plus);
-        const uint32_t nm = (uint32_t)rp.minus.size(), ns = (uint32_t)rp.res.size(), ni = (uint32_t)rp.ints.size();
-        uint32_t wp = 0, wl = 0;
-        for (uint32_t c : rp.minus) wp = std::max(wp, bits_of(fold_signed((int64_t)c - (int64_t)i)));
-        for (uint32_t c : rp.res) wp = std::max(wp, bits_of(fold_signed((int64_t)c - (int64_t)i)));
         for (auto& iv : rp.ints) {
-          wp = std::max(wp, bits_of(fold_signed((int64_t)iv.first - (int64_t)i)));
-          wl = std::max(wl, bits_of(iv.second - bp.min_interval));
-        }
-        const bool esc = nm >= kHdrMinusEsc || ns >= kHdrResEsc || ni >= kHdrIntEsc;
-        hdr[k] = make_hdr(r, std::min(nm, kHdrMinusEsc), std::min(ns, kHdrResEsc), std::min(ni, kHdrIntEsc), wp, wl);
-        if (esc) {
-          // all three counts escape together; the real counts go to the escape
-          // table (row, #minus, #residual, #interval) after the headers
-          hdr[k] = make_hdr(r, kHdrMinusEsc, kHdrResEsc, kHdrIntEsc, wp, wl);
-          escs.push_back(k);
-          escs.push_back(nm);
-          escs.push_back(ns);
-          escs.push_back(ni);
-        }
-        for (uint32_t c : rp.minus) body.put(fold_signed((int64_t)c - (int64_t)i), (int)wp);
-        for (uint32_t c : rp.res) body.put(fold_signed((int64_t)c - (int64_t)i), (int)wp);
-        for (auto& iv : rp.ints) {
-          body.put(fold_signed((int64_t)iv.first - (int64_t)i), (int)wp);
-          body.put(iv.second - bp.min_interval, (int)wl);
           cols.push_back(iv.first);
           cols.push_back(iv.first + iv.second - 1);
         }
         for (uint32_t c : rp.minus) cols.push_back(c);
         for (uint32_t c : rp.res) cols.push_back(c);
-        codes += nm + ns + 2ull * ni;
-        adds += (r ? 1 : 0) + nm + ns + 2ull * ni;
       }
-      badds[b] = adds;
-      bcodes[b] = codes;
-      BitWriter& out = bstream[b];
-      for (uint32_t q = 0; q < B; ++q) out.put(q < nr ? hdr[q] : 0u, 32);
-      for (uint32_t e : escs) out.put(e, 32);
-      bbits[b] = (uint64_t)nr * 32 + escs.size() * 32 + body.nbits;
-      out.append(body);
-      out.align(128);
-      // x window: the W-range covering the most gathered columns
       std::sort(cols.begin(), cols.end());
       uint64_t best = 0, best_lo = r0;
       for (size_t a = 0, e = 0; a < cols.size(); ++a) {
@@ -147,12 +115,70 @@ BvdLayout build_bvd(const BvDecoded& dec, const BvParams& bp, const BvdOptions& 
         lo = best_lo >= slack / 2 ? best_lo - slack / 2 : 0;
       }
       lo &= ~15ull;
-      uint64_t inwin = 0;
-      for (uint32_t c : cols) inwin += (c >= lo && c < lo + W);
+      auto inwin = [&](uint64_t c) { return c >= lo && c < lo + W; };
+      uint64_t in_cnt = 0;
+      for (uint32_t c : cols) in_cnt += inwin(c);
       bgath[b] = cols.size();
-      bin[b] = inwin;
+      bin[b] = in_cnt;
+      // pass 2: headers (with the far flag) and bodies
+      for (uint32_t k = 0; k < nr; ++k) {
+        const uint32_t i = r0 + k;
+        const uint32_t r = dec.ref_dist[i];
+        const RowParts& rp = rps[k];
+        const uint32_t nm = (uint32_t)rp.minus.size(), ns = (uint32_t)rp.res.size(), ni = (uint32_t)rp.ints.size();
+        int64_t dmin = 0, dmax = 0;
+        bool any = false, far = false;
+        auto see = [&](uint32_t c) {
+          const int64_t d = (int64_t)c - (int64_t)i;
+          dmin = any ? std::min(dmin, d) : d;
+          dmax = any ? std::max(dmax, d) : d;
+          any = true;
+          if (!inwin(c)) far = true;
+        };
+        for (uint32_t c : rp.minus) see(c);
+        for (uint32_t c : rp.res) see(c);
+        uint32_t wl = 0;
+        for (auto& iv : rp.ints) {
+          see(iv.first);
+          if (!inwin((uint64_t)iv.first + iv.second - 1)) far = true;
+          wl = std::max(wl, bits_of(iv.second - bp.min_interval));
+        }
+        // smallest wp with -2^(wp-1) <= d < 2^(wp-1) for every offset d
+        uint32_t wp = 0;
+        if (any)
+          while (!(dmin >= -(int64_t)code_bias(wp) && dmax < (int64_t)(wp ? code_bias(wp) : 1))) ++wp;
+        const int64_t bias = code_bias(wp);
+        const bool esc = nm >= kHdrMinusEsc || ns >= kHdrResEsc || ni >= kHdrIntEsc;
+        if (esc) {
+          // all three counts escape together; the real counts go to the escape table
+          hdr[k] = make_hdr(r, kHdrMinusEsc, kHdrResEsc, kHdrIntEsc, wp, wl, far);
+          escs.push_back(k);
+          escs.push_back(nm);
+          escs.push_back(ns);
+          escs.push_back(ni);
+        } else {
+          hdr[k] = make_hdr(r, nm, ns, ni, wp, wl, far);
+        }
+        for (uint32_t c : rp.minus) body.put((uint64_t)((int64_t)c - (int64_t)i + bias), (int)wp);
+        for (uint32_t c : rp.res) body.put((uint64_t)((int64_t)c - (int64_t)i + bias), (int)wp);
+        for (auto& iv : rp.ints) {
+          body.put((uint64_t)((int64_t)iv.first - (int64_t)i + bias), (int)wp);
+          body.put(iv.second - bp.min_interval, (int)wl);
+        }
+        codes += nm + ns + 2ull * ni;
+        adds += (r ? 1 : 0) + nm + ns + 2ull * ni;
+      }
+      badds[b] = adds;
+      bcodes[b] = codes;
+      BitWriter& out = bstream[b];
+      for (uint32_t q = 0; q < B; ++q) out.put(q < nr ? hdr[q] : 0u, 32);
+      for (uint32_t e : escs) out.put(e, 32);
+      bbits[b] = (uint64_t)nr * 32 + escs.size() * 32 + body.nbits;
+      out.append(body);
+      out.align(128);
       L.blocks[b].wlo = (uint32_t)lo;
       L.blocks[b].nwords = (uint32_t)(out.nbits / 32);
+      L.blocks[b].nesc = (uint32_t)(escs.size() / 4);
     }
   });
   uint64_t off = 0, maxw = 0, g_all = 0, g_in = 0;

@@ -19,12 +19,16 @@
 //   [row headers: block_rows x u32][row bodies, bit-packed, row order]  (16-B padded)
 // Row header (u32, MSB first):
 //   r (3) | #minus (5, 31 = escape) | #residual (6, 63 = escape) |
-//   #interval (4, 15 = escape) | wp (5) | wl (5) | 0 (4)
-// Row body (bits): [3 x 32-bit counts if any count is escaped]
-//   [#minus + #residual point codes, wp bits each: fold(col - i)]
-//   [#interval x (fold(left - i) in wp bits, len - Lmin in wl bits)]
-// fold(d) = 2d for d >= 0, -2d-1 for d < 0.  The row body length follows from
-// the header, so the kernel computes every row's bit offset with one scan.
+//   #interval (4, 15 = escape) | wp (5) | wl (5) | far (1) | 0 (3)
+// (escaped rows keep their real counts in an escape table after the headers:
+// entries (row, #minus, #residual, #interval)).
+// Row body (bits):
+//   [#minus + #residual point codes, wp bits each: col - i + bias]
+//   [#interval x (left - i + bias in wp bits, len - Lmin in wl bits)]
+// with bias = 2^(wp-1) (0 when wp = 0).  `far` marks rows with a column
+// outside the block's x-window; only those rows take the bounds-checked path.  The
+// row body length follows from the header, so the kernel computes every
+// row's bit offset with one scan.
 // Each block also carries an x-window start: the CTA stages x[wlo, wlo + W)
 // (plus a tile-local prefix) in shared memory.
 #pragma once
@@ -49,18 +53,22 @@ __host__ __device__ constexpr uint32_t hdr_ns(uint32_t h) { return (h >> 18) & 6
 __host__ __device__ constexpr uint32_t hdr_ni(uint32_t h) { return (h >> 14) & 15u; }
 __host__ __device__ constexpr uint32_t hdr_wp(uint32_t h) { return (h >> 9) & 31u; }
 __host__ __device__ constexpr uint32_t hdr_wl(uint32_t h) { return (h >> 4) & 31u; }
+__host__ __device__ constexpr bool hdr_far(uint32_t h) { return (h >> 3) & 1u; }
+__host__ __device__ constexpr uint32_t code_bias(uint32_t wp) { return wp ? (1u << (wp - 1)) : 0u; }
 __host__ __device__ constexpr bool hdr_escaped(uint32_t h) {
   return hdr_nm(h) == kHdrMinusEsc || hdr_ns(h) == kHdrResEsc || hdr_ni(h) == kHdrIntEsc;
 }
 __host__ __device__ constexpr uint32_t make_hdr(uint32_t r, uint32_t nm, uint32_t ns, uint32_t ni, uint32_t wp,
-                                                uint32_t wl) {
-  return (r << 29) | (nm << 24) | (ns << 18) | (ni << 14) | (wp << 9) | (wl << 4);
+                                                uint32_t wl, bool far) {
+  return (r << 29) | (nm << 24) | (ns << 18) | (ni << 14) | (wp << 9) | (wl << 4) | ((far ? 1u : 0u) << 3);
 }
 
 struct BvdBlockInfo {
   uint64_t word_offset;  // first u32 word of this block's stream (16-byte aligned)
   uint32_t nwords;       // words in this block's stream (multiple of 4)
   uint32_t wlo;          // x-window start (multiple of 16)
+  uint32_t nesc;         // escaped rows (entries of the escape table)
+  uint32_t pad[3];
 };
 
 struct BvdDims {

@@ -11,7 +11,11 @@ MINUS_ESC, RES_ESC, INT_ESC = 31, 63, 15
 def hdr_fields(h):
     h = int(h)
     return dict(r=h >> 29, nm=(h >> 24) & 31, ns=(h >> 18) & 63, ni=(h >> 14) & 15, wp=(h >> 9) & 31,
-                wl=(h >> 4) & 31)
+                wl=(h >> 4) & 31, far=(h >> 3) & 1)
+
+
+def bias(wp):
+    return (1 << (wp - 1)) if wp else 0
 
 
 def extract(words, off, w):
@@ -27,8 +31,9 @@ def unfold(u):
     return -((u + 1) >> 1) if (u & 1) else (u >> 1)
 
 
-def decode_layout(words, blocks, n, B, lmin):
-    """Returns (refs, rows) per row: (ref distance, sorted adjacency)."""
+def decode_layout(words, blocks, n, B, lmin, W=None):
+    """Returns (refs, rows) per row: (ref distance, sorted adjacency).  With the
+    window size W, also checks the `far` flag against the block's x-window."""
     rows_out = [None] * n
     refs_out = [0] * n
     for b in range(len(blocks)):
@@ -40,6 +45,7 @@ def decode_layout(words, blocks, n, B, lmin):
         hdrs = [hdr_fields(base[k]) for k in range(nr)]
         escaped = [h["nm"] == MINUS_ESC or h["ns"] == RES_ESC or h["ni"] == INT_ESC for h in hdrs]
         nesc = sum(escaped)
+        assert nesc == int(blocks[b, 4])
         esc = {int(base[B + 4 * e]): (int(base[B + 4 * e + 1]), int(base[B + 4 * e + 2]), int(base[B + 4 * e + 3]))
                for e in range(nesc)}
         off = (B + 4 * nesc) * 32
@@ -48,17 +54,23 @@ def decode_layout(words, blocks, n, B, lmin):
             nm, ns, ni = esc[k] if escaped[k] else (h["nm"], h["ns"], h["ni"])
             wp, wl, r = h["wp"], h["wl"], h["r"]
             i = r0 + k
+            ib = i - bias(wp)
             pts = []
             for t in range(nm + ns):
-                pts.append(i + unfold(extract(base, off, wp)))
+                pts.append(ib + extract(base, off, wp))
                 off += wp
             ints = []
             for t in range(ni):
-                left = i + unfold(extract(base, off, wp))
+                left = ib + extract(base, off, wp)
                 ln = extract(base, off + wp, wl) + lmin
                 ints.append((left, ln))
                 off += wp + wl
             minus, res = pts[:nm], pts[nm:]
+            if W is not None:
+                wlo = int(blocks[b, 3])
+                far = any(not (wlo <= c < wlo + W) for c in pts) or any(
+                    not (wlo <= left and left + ln <= wlo + W) for left, ln in ints)
+                assert bool(h["far"]) == far, (i, h, far)
             plus = set(res)
             for left, ln in ints:
                 plus.update(range(left, left + ln))

@@ -100,8 +100,8 @@ def test_bv_params_validation():
 def test_device_layout_decodes_to_adjacency(cfg, n, block_rows):
     g = make_graph(cfg, n=n)
     s = P.BvStream.encode(g, bv_params(cfg))
-    words, blocks = s.layout_export(P.CreateOptions(block_rows=block_rows))
-    refs, rows = decode_layout(words, blocks, g.n, block_rows, 4)
+    words, blocks = s.layout_export(P.CreateOptions(block_rows=block_rows, window=1536))
+    refs, rows = decode_layout(words, blocks, g.n, block_rows, 4, W=1536)
     assert rows == rows_of(g)
 
 
@@ -116,8 +116,8 @@ def test_device_layout_escapes_and_edge_rows():
     rows[2999] = [0, 2999]
     g = csr_from_rows(rows)
     s = P.BvStream.encode(g, P.BvParams())
-    words, blocks = s.layout_export(P.CreateOptions(block_rows=1024))
-    _, got = decode_layout(words, blocks, n, 1024, 4)
+    words, blocks = s.layout_export(P.CreateOptions(block_rows=1024, window=512))
+    _, got = decode_layout(words, blocks, n, 1024, 4, W=512)
     assert got == rows
 
 

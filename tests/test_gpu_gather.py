@@ -66,8 +66,8 @@ def test_gather_matches_matvec_ref(cuda):
     assert max_rel_err(dg.matvec(x), want) <= F64_TOL
 
 
-@pytest.mark.parametrize("lanes,block_rows,window", [(128, 1024, 2048), (256, 1024, 2048), (64, 2048, 4096),
-                                                      (32, 1024, 512), (128, 4096, 1024), (256, 2048, 1536)])
+@pytest.mark.parametrize("lanes,block_rows,window", [(256, 1024, 2048), (256, 1024, 1536), (256, 1024, 4096),
+                                                      (256, 1024, 512), (256, 1024, 128)])
 def test_gather_layout_variants(cuda, lanes, block_rows, window):
     g = make_graph(2, n=(1 << 16) + 777)  # ragged last block
     check_gather(g, bv_params(2), P.CreateOptions(lanes=lanes, block_rows=block_rows, window=window))
@@ -136,6 +136,15 @@ def test_gather_shards_cover_rows(cuda):
         dg = P.BvGraph(s, P.CreateOptions(row_begin=a, row_end=b))
         parts.append(dg.matvec(x))
     assert max_rel_err(np.concatenate(parts), want) <= F64_TOL
+
+
+def test_gather_bad_options(cuda):
+    g = make_graph(1, n=4096)
+    s = P.BvStream.encode(g, bv_params(1))
+    with pytest.raises(ValueError):
+        P.BvGraph(s, P.CreateOptions(lanes=96))
+    with pytest.raises(ValueError):
+        P.BvGraph(s, P.CreateOptions(lanes=128, block_rows=1024))
 
 
 def test_gather_dimension_errors(cuda):
