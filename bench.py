@@ -253,12 +253,12 @@ def run_ours(args):
     alg_bytes = math.ceil(S / 8) + g.n * xsz + g.n * xsz
     peak, peak_src = measured_peak()
     achieved = alg_bytes / (float(times.mean()) * 1e-3) / 1e9
-    traffic = None
+    traffic = None  # dram bytes per launch of this kernel from the committed ncu --set full capture
     prof = os.path.join(ROOT, "profiles", "ncu_gather_summary.json")
     if os.path.exists(prof):
         try:
             pj = json.load(open(prof))
-            key = f"{args.dtype}_{args.form}_{args.interval_mode}_n{args.n_log2}"
+            key = f"{args.form}_{args.dtype}_n{args.n_log2}_t{args.lanes}_w{args.window}"
             if key in pj:
                 traffic = pj[key]["dram_bytes_per_launch"]
         except Exception:

@@ -1,0 +1,104 @@
+"""Summarise an ncu report (or a launch-list CSV) into JSON for profiles/.
+
+usage:
+  python tools/ncu_summary.py report.ncu-rep out.json [key]      # --set full capture
+  python tools/ncu_summary.py --launches launches.csv out.json   # gpu__time_duration list
+"""
+import csv
+import io
+import json
+import subprocess
+import sys
+from collections import defaultdict
+
+
+def raw_rows(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units = rows[0], rows[1]
+    return hdr, units, rows[2:]
+
+
+WANT = {
+    "gpu__time_duration.sum": "duration",
+    "dram__bytes_read.sum": "dram_read",
+    "dram__bytes_write.sum": "dram_write",
+    "sm__warps_active.avg.pct_of_peak_sustained_active": "achieved_occupancy_pct",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_slots_busy_pct",
+    "sm__inst_executed.avg.per_cycle_active": "ipc",
+    "smsp__inst_executed.sum": "warp_instructions",
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed": "dram_throughput_pct",
+    "launch__registers_per_thread": "registers",
+    "launch__shared_mem_per_block_dynamic": "dyn_smem_per_block",
+    "launch__grid_size": "grid",
+    "launch__block_size": "block",
+}
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9,
+         "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1}
+
+
+def full(rep, out, key=None):
+    hdr, units, rows = raw_rows(rep)
+    res = []
+    for r in rows:
+        d = dict(zip(hdr, r))
+        u = dict(zip(hdr, units))
+        e = {"kernel": d.get("Kernel Name", "")}
+        for k, name in WANT.items():
+            if k in d and d[k] not in ("", None):
+                try:
+                    v = float(d[k].replace(",", ""))
+                except ValueError:
+                    continue
+                e[name] = v * SCALE.get(u.get(k, ""), 1)
+        stalls = {}
+        for k, v in d.items():
+            if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio"):
+                try:
+                    stalls[k[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")]] = float(v)
+                except ValueError:
+                    pass
+        e["top_stalls_cycles_per_issue"] = dict(sorted(stalls.items(), key=lambda kv: -kv[1])[:6])
+        if "dram_read" in e and "dram_write" in e:
+            e["dram_bytes_per_launch"] = e["dram_read"] + e["dram_write"]
+        res.append(e)
+    blob = {"report": rep, "kernels": res}
+    if key:
+        prev = {}
+        try:
+            prev = json.load(open(out))
+        except Exception:
+            pass
+        prev[key] = res[0] if len(res) == 1 else res
+        blob = prev
+    json.dump(blob, open(out, "w"), indent=1)
+    print(json.dumps(blob, indent=1)[:3000])
+
+
+def launches(csv_path, out):
+    text = open(csv_path).read()
+    start = text.find('"ID"')
+    rows = list(csv.reader(io.StringIO(text[start:])))
+    hdr = rows[0]
+    idx = {h: i for i, h in enumerate(hdr)}
+    per = defaultdict(lambda: [0, 0.0])
+    for r in rows[1:]:
+        if len(r) < len(hdr) or r[idx["Metric Name"]] != "gpu__time_duration.sum":
+            continue
+        name = r[idx["Kernel Name"]]
+        unit = r[idx["Metric Unit"]]
+        v = float(r[idx["Metric Value"]].replace(",", "")) * SCALE.get(unit, 1)
+        per[name][0] += 1
+        per[name][1] += v
+    total = sum(v[1] for v in per.values())
+    res = sorted(({"kernel": k, "launches": v[0], "total_s": v[1], "share": v[1] / total if total else 0}
+                  for k, v in per.items()), key=lambda e: -e["total_s"])
+    json.dump({"source": csv_path, "total_s": total, "kernels": res}, open(out, "w"), indent=1)
+    print(json.dumps(res, indent=1)[:2000])
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "--launches":
+        launches(sys.argv[2], sys.argv[3])
+    else:
+        full(sys.argv[1], sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else None)
