@@ -362,7 +362,7 @@ void launch_gather(cmvg_graph* g, const XT* x, YT* y, cudaStream_t st) {
   GatherSmem L = gather_smem_layout(g->dims, g->stream_cap_words, sizeof(XT), true);
   auto kern = bvd_gather_kernel<XT, YT>;
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
-  kern<<<g->nblocks, g->threads, L.total, st>>>(g->dev(), x, y);
+  kern<<<g->nblocks, g->threads, L.total, st>>>(g->dev(), x, y, PrArgs{});
   CUDA_TRY(cudaGetLastError());
 }
 

@@ -243,6 +243,65 @@ __device__ __forceinline__ void dd_add(double& hi, double& lo, double bhi, doubl
   lo = e - (hi - s);
 }
 
+// Output stage of the gather: plain y, or the fused PageRank update
+// (pagerank.hpp:83-102, Eq. 1):
+//   p'_i = alpha/n + (1 - alpha) (y_i + D/n)   (D = dangling mass, kUniform;
+//                                                0 for kDrop)
+//   q'_i = p'_i / d_i  (0 for dangling i)
+// plus per-block partials {sum_{d_i = 0} p'_i, sum |p'_i - p_i|}.
+struct PlainEpi {
+  template <typename YT>
+  __device__ __forceinline__ void store(YT* yb, uint32_t k, double y) const {
+    yb[k] = (YT)y;
+  }
+  __device__ __forceinline__ void finish(int*) const {}
+};
+
+struct PageRankEpi {
+  const uint32_t* deg;     // out-degrees of A for this block's rows (shard-relative, offset applied)
+  const double* p_prev;    // may be null
+  double* q_next;          // shard-relative, offset applied
+  double* partial;         // [nblocks][2]
+  double base, scale, dn;  // alpha/n, 1 - alpha, D/n (or 0)
+  uint32_t bl;
+  double dang, l1;         // per-thread partials
+  template <typename YT>
+  __device__ __forceinline__ void store(YT* pb, uint32_t k, double y) {
+    const double pn = base + scale * (y + dn);
+    pb[k] = (YT)pn;
+    const uint32_t d = deg[k];
+    q_next[k] = d ? pn / (double)d : 0.0;
+    if (!d) dang += pn;
+    if (p_prev) l1 += fabs(pn - p_prev[k]);
+  }
+  __device__ __forceinline__ void finish(int* scratch) {
+    // deterministic block reduction: warp sums, then warp 0 in warp order
+    double a = dang, b = l1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_down_sync(0xffffffffu, a, o);
+      b += __shfl_down_sync(0xffffffffu, b, o);
+    }
+    double* ws = reinterpret_cast<double*>(scratch);
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    __syncthreads();
+    if (lane == 0) {
+      ws[2 * warp] = a;
+      ws[2 * warp + 1] = b;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double sa = 0.0, sb = 0.0;
+      for (uint32_t w = 0; w < nw; ++w) {
+        sa += ws[2 * w];
+        sb += ws[2 * w + 1];
+      }
+      partial[2 * bl] = sa;
+      partial[2 * bl + 1] = sb;
+    }
+  }
+};
+
 // Reference-chain resolution -- the level scheduler.  Every row holds
 // (value, pointer) = (delta_i, i - r_i); each level of pointer jumping is one
 // barrier-separated data-parallel step
@@ -252,8 +311,9 @@ __device__ __forceinline__ void dd_add(double& hi, double& lo, double bhi, doubl
 // reference's left-to-right order only below double-double resolution).
 // Bounded chains (R = 3) take two levels; unbounded ones log2(depth).
 // Writes y (YT) with coalesced stores.  Uses c.perm as the pointer array.
-template <typename YT>
-__device__ __forceinline__ void chain_and_store(double* s_yhi, float* s_ylo, RowCtx& c, YT* __restrict__ yb) {
+template <typename YT, class EPI = PlainEpi>
+__device__ __forceinline__ void chain_and_store(double* s_yhi, float* s_ylo, RowCtx& c, YT* __restrict__ yb,
+                                                EPI epi = EPI()) {
   const uint32_t T = blockDim.x, tid = threadIdx.x;
   constexpr uint32_t kMaxPer = 4;  // rows per thread per level (block_rows / threads <= 4)
   constexpr uint16_t kNone = 0xffffu;
@@ -298,7 +358,8 @@ __device__ __forceinline__ void chain_and_store(double* s_yhi, float* s_ylo, Row
     }
     any = __syncthreads_or(more);
   }
-  for (uint32_t k = tid; k < c.nr; k += T) yb[k] = (YT)(s_yhi[k] + (double)s_ylo[k]);
+  for (uint32_t k = tid; k < c.nr; k += T) epi.store(yb, k, s_yhi[k] + (double)s_ylo[k]);
+  epi.finish(c.wscratch);
 }
 
 }  // namespace cmvg

@@ -154,19 +154,33 @@ __device__ __forceinline__ void gather_intervals(const RowCtx& c, const S& src, 
   }
 }
 
-template <typename XT, typename YT, bool PREFIX, class S>
+template <typename XT, typename YT, bool PREFIX, class S, class EPI>
 __device__ __forceinline__ void gather_block(RowCtx& rc, const S& src, const XWin<XT, PREFIX>& xw, const BvdDims& D,
-                                             uint32_t r0, int nesc, double* s_yhi, float* s_ylo, YT* yb) {
+                                             uint32_t r0, int nesc, double* s_yhi, float* s_ylo, YT* yb, EPI& epi) {
   row_setup(rc, src, nesc);
   gather_points(rc, src, xw, (int32_t)r0, s_yhi, s_ylo);
   __syncthreads();
   gather_intervals(rc, src, xw, (int32_t)r0, D.min_interval, s_yhi, s_ylo);
   __syncthreads();
-  chain_and_store(s_yhi, s_ylo, rc, yb);
+  chain_and_store(s_yhi, s_ylo, rc, yb, epi);
 }
 
-template <typename XT, typename YT>
-__global__ void __launch_bounds__(256) bvd_gather_kernel(BvdDev g, const XT* __restrict__ x, YT* __restrict__ y) {
+// PageRank step arguments (shard-relative pointers; see PageRankEpi).
+struct PrArgs {
+  const uint32_t* deg;
+  const double* p_prev;
+  double* q_next;
+  double* partial;
+  const double* dmass;  // device scalar: dangling mass D of the previous iterate (nullptr -> dmass_host)
+  double dmass_host;
+  double alpha;
+  uint32_t n;
+  int uniform;
+};
+
+template <typename XT, typename YT, bool PR = false>
+__global__ void __launch_bounds__(256) bvd_gather_kernel(BvdDev g, const XT* __restrict__ x, YT* __restrict__ y,
+                                                          PrArgs pr) {
   extern __shared__ __align__(16) unsigned char smem[];
   const BvdDims& D = g.d;
   const GatherSmem L = gather_smem_layout(D, g.stream_cap_words, sizeof(XT), true);
@@ -189,12 +203,36 @@ __global__ void __launch_bounds__(256) bvd_gather_kernel(BvdDev g, const XT* __r
   double* s_yhi = reinterpret_cast<double*>(smem + L.off_yhi);
   float* s_ylo = reinterpret_cast<float*>(smem + L.off_ylo);
   YT* yb = y + (r0 - g.row_begin);
-  if (staged) {  // CTA-uniform
-    const Src<true> src{smem_u32(s_stream)};
-    gather_block<XT, YT, true>(rc, src, xw, D, r0, (int)bi.nesc, s_yhi, s_ylo, yb);
+  if constexpr (PR) {
+    const uint32_t sh = r0 - g.row_begin;
+    PageRankEpi epi;
+    epi.deg = pr.deg + sh;
+    epi.p_prev = pr.p_prev ? pr.p_prev + sh : nullptr;
+    epi.q_next = pr.q_next + sh;
+    epi.partial = pr.partial;
+    epi.base = pr.alpha / (double)pr.n;
+    epi.scale = 1.0 - pr.alpha;
+    const double dm = pr.dmass ? *pr.dmass : pr.dmass_host;
+    epi.dn = pr.uniform ? dm / (double)pr.n : 0.0;
+    epi.bl = bl;
+    epi.dang = 0.0;
+    epi.l1 = 0.0;
+    if (staged) {
+      const Src<true> src{smem_u32(s_stream)};
+      gather_block<XT, YT, true>(rc, src, xw, D, r0, (int)bi.nesc, s_yhi, s_ylo, yb, epi);
+    } else {
+      const Src<false> src{g.words + bi.word_offset};
+      gather_block<XT, YT, true>(rc, src, xw, D, r0, (int)bi.nesc, s_yhi, s_ylo, yb, epi);
+    }
   } else {
-    const Src<false> src{g.words + bi.word_offset};
-    gather_block<XT, YT, true>(rc, src, xw, D, r0, (int)bi.nesc, s_yhi, s_ylo, yb);
+    PlainEpi epi;
+    if (staged) {  // CTA-uniform
+      const Src<true> src{smem_u32(s_stream)};
+      gather_block<XT, YT, true>(rc, src, xw, D, r0, (int)bi.nesc, s_yhi, s_ylo, yb, epi);
+    } else {
+      const Src<false> src{g.words + bi.word_offset};
+      gather_block<XT, YT, true>(rc, src, xw, D, r0, (int)bi.nesc, s_yhi, s_ylo, yb, epi);
+    }
   }
 }
 

@@ -12,11 +12,4 @@ template void launch_scatter<float>(cmvg_graph*, const float*, float*, cudaStrea
 void launch_matmat(cmvg_graph*, const float*, float*, uint32_t, cudaStream_t) {
   throw AbiError(CMVG_ERR_UNSUPPORTED, "multi-vector product not implemented yet");
 }
-void run_pagerank(cmvg_graph*, const uint32_t*, double, uint32_t, double, int, double*, uint32_t*, int, cudaStream_t) {
-  throw AbiError(CMVG_ERR_UNSUPPORTED, "pagerank not implemented yet");
-}
-void pagerank_step(cmvg_graph*, const double*, const uint32_t*, double, double, int, const double*, double*, double*,
-                   double*, cudaStream_t) {
-  throw AbiError(CMVG_ERR_UNSUPPORTED, "pagerank not implemented yet");
-}
 }  // namespace cmvg

@@ -1,0 +1,144 @@
+// Device PageRank driver (the reference's cmv::pagerank, pagerank.hpp:83-102,
+// SPEC.md:254-263; Eq. 1) on a handle holding BV(A^T):
+// per iteration one fused kernel (gather y = A^T q + the PageRank update,
+// q' = p'/d, per-block partials) and one deterministic reduction kernel
+// (dangling mass and L1 step), all device resident.
+#include "internal.hpp"
+
+namespace cmvg {
+namespace {
+
+// p0 = 1/n, q0 = p0/d, partials of the dangling mass per block of 1024 rows
+__global__ void pr_init_kernel(const uint32_t* __restrict__ deg, uint32_t n, double* __restrict__ p,
+                               double* __restrict__ q, double* __restrict__ partial) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  const double p0 = 1.0 / (double)n;
+  double dang = 0.0;
+  if (i < n) {
+    const uint32_t d = deg[i];
+    p[i] = p0;
+    q[i] = d ? p0 / (double)d : 0.0;
+    if (!d) dang = p0;
+  }
+  __shared__ double ws[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dang += __shfl_down_sync(0xffffffffu, dang, o);
+  if ((threadIdx.x & 31u) == 0) ws[threadIdx.x >> 5] = dang;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (uint32_t w = 0; w < blockDim.x / 32; ++w) s += ws[w];
+    partial[2 * blockIdx.x] = s;
+    partial[2 * blockIdx.x + 1] = 0.0;
+  }
+}
+
+// sum partial[nb][2] -> out[2] (fixed order: deterministic)
+__global__ void pr_reduce_kernel(const double* __restrict__ partial, uint32_t nb, double* __restrict__ out) {
+  __shared__ double sa[1024], sb[1024];
+  double a = 0.0, b = 0.0;
+  for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) {
+    a += partial[2 * i];
+    b += partial[2 * i + 1];
+  }
+  sa[threadIdx.x] = a;
+  sb[threadIdx.x] = b;
+  __syncthreads();
+  for (uint32_t s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      sa[threadIdx.x] += sa[threadIdx.x + s];
+      sb[threadIdx.x] += sb[threadIdx.x + s];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out[0] = sa[0];
+    out[1] = sb[0];
+  }
+}
+
+void launch_pr_step(cmvg_graph* g, const double* q, PrArgs pr, double* p_next, cudaStream_t st) {
+  GatherSmem L = gather_smem_layout(g->dims, g->stream_cap_words, sizeof(double), true);
+  auto kern = bvd_gather_kernel<double, double, true>;
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
+  kern<<<g->nblocks, g->threads, L.total, st>>>(g->dev(), q, p_next, pr);
+  CUDA_TRY(cudaGetLastError());
+}
+
+}  // namespace
+
+void run_pagerank(cmvg_graph* g, const uint32_t* degrees, double alpha, uint32_t iters, double l1_tol, int dangling,
+                  double* ranks, uint32_t* iters_run, int ptr_kind, cudaStream_t st) {
+  const uint32_t n = g->n;
+  DevBuf ddeg, p0, p1, q0, q1, part, scal;
+  const uint32_t* deg = degrees;
+  if (ptr_kind == CMVG_HOST) {
+    ddeg.upload(degrees, n);
+    deg = ddeg.as<uint32_t>();
+  }
+  p0.alloc((size_t)n * 8 + 64);
+  p1.alloc((size_t)n * 8 + 64);
+  q0.alloc((size_t)n * 8 + 64);
+  q1.alloc((size_t)n * 8 + 64);
+  const uint32_t ib = (n + 1023) / 1024;
+  part.alloc((size_t)std::max(ib, g->nblocks) * 16);
+  scal.alloc(4 * 8);
+  double* p = p0.as<double>();
+  double* pn = p1.as<double>();
+  double* q = q0.as<double>();
+  double* qn = q1.as<double>();
+  double* dm = scal.as<double>();  // [0] dangling mass, [1] l1
+  pr_init_kernel<<<ib, 1024, 0, st>>>(deg, n, p, q, part.as<double>());
+  CUDA_TRY(cudaGetLastError());
+  pr_reduce_kernel<<<1, 1024, 0, st>>>(part.as<double>(), ib, dm);
+  CUDA_TRY(cudaGetLastError());
+  const bool use_tol = l1_tol >= 0.0;
+  uint32_t t = 0;
+  for (t = 1; t <= iters; ++t) {
+    PrArgs pr{};
+    pr.deg = deg;
+    pr.p_prev = use_tol ? p : nullptr;
+    pr.q_next = qn;
+    pr.partial = part.as<double>();
+    pr.dmass = dm;
+    pr.alpha = alpha;
+    pr.n = n;
+    pr.uniform = dangling == CMVG_DANGLING_UNIFORM;
+    launch_pr_step(g, q, pr, pn, st);
+    pr_reduce_kernel<<<1, 1024, 0, st>>>(part.as<double>(), g->nblocks, dm);
+    CUDA_TRY(cudaGetLastError());
+    std::swap(p, pn);
+    std::swap(q, qn);
+    if (use_tol) {
+      double l1 = 0.0;
+      CUDA_TRY(cudaMemcpyAsync(&l1, dm + 1, 8, cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaStreamSynchronize(st));
+      if (l1 <= l1_tol) break;
+    }
+  }
+  if (t > iters) t = iters;
+  if (iters_run) *iters_run = t;
+  CUDA_TRY(cudaMemcpyAsync(ranks, p, (size_t)n * 8, ptr_kind == CMVG_HOST ? cudaMemcpyDeviceToHost
+                                                                            : cudaMemcpyDeviceToDevice, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+}
+
+void pagerank_step(cmvg_graph* g, const double* q, const uint32_t* deg, double alpha, double dmass, int dangling,
+                   const double* p_prev, double* p_next, double* q_next, double* partial, cudaStream_t st) {
+  g->scratch.alloc((size_t)g->nblocks * 16 + 64);
+  PrArgs pr{};
+  pr.deg = deg;
+  pr.p_prev = p_prev;
+  pr.q_next = q_next;
+  pr.partial = g->scratch.as<double>();
+  pr.dmass = nullptr;
+  pr.dmass_host = dmass;
+  pr.alpha = alpha;
+  pr.n = g->n;
+  pr.uniform = dangling == CMVG_DANGLING_UNIFORM;
+  launch_pr_step(g, q, pr, p_next, st);
+  pr_reduce_kernel<<<1, 1024, 0, st>>>(g->scratch.as<double>(), g->nblocks, partial);
+  CUDA_TRY(cudaGetLastError());
+}
+
+}  // namespace cmvg

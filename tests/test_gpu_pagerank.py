@@ -1,0 +1,114 @@
+"""Device PageRank (pagerank.hpp:83-102) on BV(A^T) against the oracle's
+pagerank with CsrKernel(A^T): per-entry relative error <= 1e-12, sum p = 1
+within 1e-10, both dangling policies, early stop on the L1
+tolerance, and the per-shard step used by the multi-GPU driver."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_1708_07271_b200 as P
+from oracle import pyoracle as O
+from tests.helpers import csr_from_rows, make_graph
+
+pytestmark = pytest.mark.gpu
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+def bv_of_transpose(g: P.CsrGraph, **kw):
+    return P.BvStream.encode(g.transpose(), P.BvParams(**kw))
+
+
+def oracle_pr(g: P.CsrGraph, **kw):
+    og = O.Csr.from_arrays(g.n, g.row_offsets, g.columns)
+    return O.pagerank_csr(og.transpose(), og.out_degrees(), **kw)
+
+
+def rel(a, b):
+    return float(np.max(np.abs(a - b) / np.abs(b)))
+
+
+@pytest.mark.parametrize("e", GOLD["pagerank"], ids=lambda e: e["spec"])
+def test_pagerank_golden(cuda, e):
+    rows = [[] for _ in range(e["n"])]
+    for u, v in e["edges"]:
+        rows[u].append(v)
+    g = csr_from_rows([sorted(r) for r in rows])
+    k = P.BvGpuKernel(P.BvGraph(bv_of_transpose(g)))
+    res = P.pagerank(k, g.out_degrees(), P.PageRankConfig(alpha=e["alpha"], iterations=e["iterations"]))
+    assert res.iterations_run == e["iterations"]
+    assert np.max(np.abs(res.ranks - np.asarray(e["want"]))) <= e["tol"]
+
+
+@pytest.mark.parametrize("dangling", ["uniform", "drop"])
+def test_pagerank_matches_oracle(cuda, dangling):
+    g = make_graph(3, n=1 << 16)  # copy model, mean degree 24 (config 3 shape); has dangling rows
+    assert (g.out_degrees() == 0).any()
+    dg = P.BvGraph(bv_of_transpose(g))
+    p, it = dg.pagerank(g.out_degrees(), alpha=0.15, iterations=50, dangling=dangling)
+    want, wit = oracle_pr(g, alpha=0.15, iterations=50, dangling=dangling)
+    assert it == wit == 50
+    assert rel(p, want) <= 1e-12
+    if dangling == "uniform":
+        assert abs(p.sum() - 1.0) <= 1e-10
+
+
+def test_pagerank_l1_tolerance(cuda):
+    g = make_graph(3, n=1 << 14)
+    dg = P.BvGraph(bv_of_transpose(g))
+    p, it = dg.pagerank(g.out_degrees(), iterations=200, l1_tolerance=1e-10)
+    want, wit = oracle_pr(g, iterations=200, l1_tolerance=1e-10)
+    assert it == wit < 200
+    assert rel(p, want) <= 1e-12
+
+
+def test_pagerank_device_buffers_and_errors(cuda):
+    import torch
+
+    g = make_graph(3, n=1 << 14)
+    dg = P.BvGraph(bv_of_transpose(g))
+    deg = torch.from_numpy(g.out_degrees().astype(np.int32)).cuda()
+    p, it = dg.pagerank(deg, iterations=20)
+    want, _ = oracle_pr(g, iterations=20)
+    assert rel(p.cpu().numpy(), want) <= 1e-12
+    k = P.BvGpuKernel(dg)
+    with pytest.raises(ValueError):
+        P.pagerank(k, g.out_degrees(), P.PageRankConfig(alpha=1.5))
+    with pytest.raises(ValueError):
+        P.pagerank(k, g.out_degrees(), P.PageRankConfig(iterations=0))
+    with pytest.raises(ValueError):
+        P.pagerank(k, g.out_degrees()[:-1])
+
+
+def test_pagerank_shard_steps(cuda):
+    """Two row shards of A^T on one GPU, exchanged by hand exactly as the
+    multi-GPU driver does (all_gather of q, sum of the partials)."""
+    import torch
+
+    from paper_1708_07271_b200.distributed import plan_shards
+
+    g = make_graph(3, n=(1 << 15) + 300)
+    n = g.n
+    s = bv_of_transpose(g)
+    plan = plan_shards(n, 2, 1024)
+    deg = torch.from_numpy(g.out_degrees().astype(np.int32)).cuda()
+    shards = []
+    for r in range(2):
+        a, b = plan.bounds(r)
+        shards.append((a, b, P.BvGraph(s, P.CreateOptions(row_begin=a, row_end=b))))
+    p = torch.full((n,), 1.0 / n, dtype=torch.float64, device="cuda")
+    q = torch.where(deg > 0, p / deg.clamp(min=1).double(), torch.zeros_like(p))
+    dmass = float(p[deg == 0].sum())
+    for _ in range(30):
+        p_next, q_next = torch.empty_like(p), torch.empty_like(q)
+        tot = torch.zeros(2, dtype=torch.float64, device="cuda")
+        for a, b, dgs in shards:
+            part = torch.zeros(2, dtype=torch.float64, device="cuda")
+            dgs.pagerank_step(q, deg[a:b], 0.15, dmass, "uniform", p[a:b], p_next[a:b], q_next[a:b], part)
+            tot += part
+        p, q = p_next, q_next
+        dmass = float(tot[0])
+    want, _ = oracle_pr(g, iterations=30)
+    assert rel(p.cpu().numpy(), want) <= 1e-12
