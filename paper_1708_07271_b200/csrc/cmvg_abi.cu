@@ -213,8 +213,11 @@ int cmvg_create(const cmvg_bvstream* s, const cmvg_create_opts* opts_in, cmvg_gr
     g->block_begin = o.row_begin / o.block_rows;
     uint32_t block_end = (uint32_t)(((uint64_t)row_end + o.block_rows - 1) / o.block_rows);
     g->nblocks = block_end - g->block_begin;
-    g->stream_cap_words = o.stream_cap_words ? o.stream_cap_words
-                                             : std::max<uint32_t>(1024, (L.stats.p995_block_words + 255) & ~255u);
+    // staging cap: covers 99.5% of the blocks, at most 12K words (48 KB) so
+    // every kernel's shared-memory plan fits; larger blocks decode from global
+    g->stream_cap_words = o.stream_cap_words
+                              ? o.stream_cap_words
+                              : std::min<uint32_t>(12288, std::max<uint32_t>(1024, (L.stats.p995_block_words + 255) & ~255u));
     g->stats.codes = L.stats.codes;
     g->stats.window_coverage = L.stats.window_coverage;
     g->stats.p995_block_words = L.stats.p995_block_words;
@@ -277,8 +280,9 @@ int cmvg_layout_info(const cmvg_bvstream* s, const cmvg_create_opts* opts_in, cm
     o->device_bytes = 0;
     o->bvd_codes = L.stats.codes;
     o->max_block_words = L.dims.max_block_words;
-    o->stream_cap_words = opt.stream_cap_words ? opt.stream_cap_words
-                                               : std::max<uint32_t>(1024, (L.stats.p995_block_words + 255) & ~255u);
+    o->stream_cap_words = opt.stream_cap_words
+                              ? opt.stream_cap_words
+                              : std::min<uint32_t>(12288, std::max<uint32_t>(1024, (L.stats.p995_block_words + 255) & ~255u));
     o->window_coverage = L.stats.window_coverage;
   });
 }

@@ -51,8 +51,12 @@ __device__ __forceinline__ uint32_t extract_bits(const S& s, uint32_t off, uint3
 }
 
 // ---- row setup scratch -----------------------------------------------------
+// Rows with more codes than this are decoded by a whole warp (lanes stride
+// over the row's fixed-width codes) instead of one lane.
+constexpr uint32_t kHeavyCodes = 96;
+
 struct RowSmem {
-  uint32_t off_rowoff, off_perm, off_permi, off_key, off_ref, off_misc, total;
+  uint32_t off_rowoff, off_perm, off_permi, off_permh, off_key, off_ref, off_misc, total;
 };
 __host__ __device__ inline RowSmem row_smem_layout(uint32_t base, uint32_t B) {
   RowSmem s;
@@ -62,6 +66,8 @@ __host__ __device__ inline RowSmem row_smem_layout(uint32_t base, uint32_t B) {
   s.off_perm = o;
   o = align16(o + B * 2);
   s.off_permi = o;
+  o = align16(o + B * 2);
+  s.off_permh = o;
   o = align16(o + B * 2);
   s.off_key = o;
   o = align16(o + B * 2);
@@ -75,15 +81,19 @@ __host__ __device__ inline RowSmem row_smem_layout(uint32_t base, uint32_t B) {
 
 enum MiscSlot : int {
   kNesc = 0,    // escaped rows in the block
-  kNInt = 2,    // rows with intervals
+  kNInt = 2,    // light rows with intervals
+  kNPts = 3,    // light rows (point rounds)
   kRoundP = 4,  // dynamic round counters
   kRoundI = 5,
+  kNHeavy = 6,  // heavy rows
+  kRoundH = 7,
 };
 
 struct RowCtx {
   uint32_t* rowoff;  // bit offset of each row body
   uint16_t* perm;    // rows by point-code count desc (later: chain pointers)
-  uint16_t* permi;   // rows with intervals, by interval count desc
+  uint16_t* permi;   // light rows with intervals, by interval count desc
+  uint16_t* permh;   // heavy rows (warp-cooperative)
   uint16_t* key;     // per-row sort keys
   uint8_t* ref;      // reference distance per row
   int* misc;
@@ -98,6 +108,7 @@ __device__ __forceinline__ RowCtx carve_rows(unsigned char* smem, const RowSmem&
   c.rowoff = reinterpret_cast<uint32_t*>(smem + L.off_rowoff);
   c.perm = reinterpret_cast<uint16_t*>(smem + L.off_perm);
   c.permi = reinterpret_cast<uint16_t*>(smem + L.off_permi);
+  c.permh = reinterpret_cast<uint16_t*>(smem + L.off_permh);
   c.key = reinterpret_cast<uint16_t*>(smem + L.off_key);
   c.ref = reinterpret_cast<uint8_t*>(smem + L.off_ref);
   c.bar = reinterpret_cast<uint64_t*>(smem + L.off_misc);
@@ -162,7 +173,7 @@ __device__ __forceinline__ int warp_excl_scan(int v, int& total) {
 // both descending so the heaviest rounds are claimed first.
 // Ends with __syncthreads().
 template <class S>
-__device__ __forceinline__ void row_setup(RowCtx& c, const S& src, int nesc) {
+__device__ __forceinline__ void row_setup(RowCtx& c, const S& src, int nesc, bool split_heavy = false) {
   const uint32_t T = blockDim.x, tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5, nwarps = T >> 5;
   const uint32_t B = c.B, nr = c.nr;
   const uint32_t per = (B + T - 1) >> (31 - __clz(T));  // T is a power of 2
@@ -183,9 +194,14 @@ __device__ __forceinline__ void row_setup(RowCtx& c, const S& src, int nesc) {
       loc += (rc.nm + rc.ns + rc.ni) * hdr_wp(h) + rc.ni * hdr_wl(h);
       c.ref[k] = (uint8_t)hdr_r(h);
       const uint32_t kp = min(rc.nm + rc.ns, 63u), ki = min(rc.ni, 63u);
-      c.key[k] = (uint16_t)((ki << 6) | kp);
-      atomicAdd(&hp[kp], 1);
-      if (ki) atomicAdd(&hi[ki], 1);
+      const bool heavy = split_heavy && rc.nm + rc.ns + 2 * rc.ni > kHeavyCodes;
+      c.key[k] = (uint16_t)((heavy ? 0x8000u : 0u) | (ki << 6) | kp);
+      if (heavy) {
+        c.permh[atomicAdd(&c.misc[kNHeavy], 1)] = (uint16_t)k;
+      } else {
+        atomicAdd(&hp[kp], 1);
+        if (ki) atomicAdd(&hi[ki], 1);
+      }
     }
   }
   int wtot;
@@ -199,7 +215,7 @@ __device__ __forceinline__ void row_setup(RowCtx& c, const S& src, int nesc) {
     const int e2 = warp_excl_scan(v0 + v1, tot);
     hb[63 - 2 * lane] = e2;
     hb[62 - 2 * lane] = e2 + v0;
-    if (which == 1 && lane == 0) c.misc[kNInt] = tot;
+    if (lane == 0) c.misc[which == 1 ? kNInt : kNPts] = tot;
   }
   uint32_t wbase = 0;
   for (uint32_t w = 0; w < warp; ++w) wbase += (uint32_t)c.wscratch[w];
@@ -210,8 +226,9 @@ __device__ __forceinline__ void row_setup(RowCtx& c, const S& src, int nesc) {
     if (k < nr) {
       c.rowoff[k] += tbase;
       const uint32_t key = c.key[k];
+      if (key & 0x8000u) continue;  // heavy rows are already listed
       c.perm[atomicAdd(&hp[key & 63u], 1)] = (uint16_t)k;
-      const uint32_t ki = key >> 6;
+      const uint32_t ki = (key >> 6) & 63u;
       if (ki) c.permi[atomicAdd(&hi[ki], 1)] = (uint16_t)k;
     }
   }

@@ -72,10 +72,11 @@ __device__ __forceinline__ void gather_points(const RowCtx& c, const S& src, con
                                               double* s_yhi, float* s_ylo) {
   const int nesc = c.misc[kNesc];
   const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t npts = (uint32_t)c.misc[kNPts];
   for (;;) {
     const uint32_t rb = next_round(&c.misc[kRoundP]);
-    if (rb >= c.nr) break;
-    const RowDesc r = round_row(c, src, c.perm, rb + lane, c.nr, nesc);
+    if (rb >= npts) break;
+    const RowDesc r = round_row(c, src, c.perm, rb + lane, npts, nesc);
     const uint32_t wp = hdr_wp(r.h);
     const bool far = hdr_far(r.h);
     const bool any_far = __any_sync(0xffffffffu, far);
@@ -154,10 +155,59 @@ __device__ __forceinline__ void gather_intervals(const RowCtx& c, const S& src, 
   }
 }
 
+// Heavy rows: one warp per row, lanes stride over the row's codes (fixed
+// width, independently addressable), compensated partial sums combined with a
+// double-double warp reduction.  Writes the full delta (points + intervals).
+template <class S, class XW>
+__device__ __forceinline__ void gather_heavy(const RowCtx& c, const S& src, const XW& xw, int32_t r0, uint32_t lmin,
+                                             double* s_yhi, float* s_ylo) {
+  const int nesc = c.misc[kNesc];
+  const uint32_t nh = (uint32_t)c.misc[kNHeavy];
+  const uint32_t lane = threadIdx.x & 31u;
+  for (;;) {
+    uint32_t q = 0;
+    if (lane == 0) q = (uint32_t)atomicAdd(&c.misc[kRoundH], 1);
+    q = __shfl_sync(0xffffffffu, q, 0);
+    if (q >= nh) break;
+    const uint32_t k = c.permh[q];
+    const uint32_t h = src.w(k);
+    const RowCounts rc = row_counts(src, c.B, h, k, nesc);
+    const uint32_t wp = hdr_wp(h), wl = hdr_wl(h);
+    const int32_t ib = r0 + (int32_t)k - (int32_t)code_bias(wp);
+    const uint32_t off0 = c.rowoff[k], np = rc.nm + rc.ns;
+    double acc = 0.0, comp = 0.0;
+    for (uint32_t t = lane; t < np; t += 32) {
+      const double xv = xw.at(ib + (int32_t)extract_bits(src, off0 + t * wp, wp));
+      tsum(acc, comp, t < rc.nm ? -xv : xv);
+    }
+    const uint32_t ioff = off0 + np * wp;
+    for (uint32_t t = lane; t < rc.ni; t += 32) {
+      const uint32_t o = ioff + t * (wp + wl);
+      const int32_t left = ib + (int32_t)extract_bits(src, o, wp);
+      const uint32_t len = extract_bits(src, o + wp, wl) + lmin;
+      double lo;
+      const double hi = xw.isum(left, len, lo);
+      tsum(acc, comp, hi);
+      comp += lo;
+    }
+    double hi = acc + comp, lo = comp - (hi - acc);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double uh = __shfl_down_sync(0xffffffffu, hi, o), ul = __shfl_down_sync(0xffffffffu, lo, o);
+      dd_add(hi, lo, uh, ul);
+    }
+    if (lane == 0) {
+      s_yhi[k] = hi;
+      s_ylo[k] = (float)lo;
+    }
+  }
+}
+
 template <typename XT, typename YT, bool PREFIX, class S, class EPI>
 __device__ __forceinline__ void gather_block(RowCtx& rc, const S& src, const XWin<XT, PREFIX>& xw, const BvdDims& D,
                                              uint32_t r0, int nesc, double* s_yhi, float* s_ylo, YT* yb, EPI& epi) {
-  row_setup(rc, src, nesc);
+  row_setup(rc, src, nesc, /*split_heavy=*/true);
+  gather_heavy(rc, src, xw, (int32_t)r0, D.min_interval, s_yhi, s_ylo);
   gather_points(rc, src, xw, (int32_t)r0, s_yhi, s_ylo);
   __syncthreads();
   gather_intervals(rc, src, xw, (int32_t)r0, D.min_interval, s_yhi, s_ylo);

@@ -44,9 +44,9 @@ __device__ __forceinline__ void matmat_rows(const RowCtx& c, const S& src, const
     uint32_t rb = 0;
     if (lane == 0) rb = rpw * (uint32_t)atomicAdd(&c.misc[kRoundP], 1);
     rb = __shfl_sync(0xffffffffu, rb, 0);
-    if (rb >= c.nr) break;
+    if (rb >= (uint32_t)c.misc[kNPts]) break;
     const uint32_t slot = rb + sub;
-    const bool act = slot < c.nr;
+    const bool act = slot < (uint32_t)c.misc[kNPts];
     const uint32_t kk = act ? c.perm[slot] : 0u;
     const uint32_t h = act ? src.w(kk) : 0u;
     RowCounts rc{0, 0, 0};

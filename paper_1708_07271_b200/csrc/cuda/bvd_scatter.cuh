@@ -109,9 +109,9 @@ __device__ __forceinline__ void scatter_block(RowCtx& c, const S& src, const Bvd
   const int nesc = c.misc[kNesc];
   for (;;) {
     const uint32_t rb = next_round(&c.misc[kRoundP]);
-    if (rb >= nr) break;
+    if (rb >= (uint32_t)c.misc[kNPts]) break;
     const uint32_t slot = rb + lane;
-    const bool act = slot < nr;
+    const bool act = slot < (uint32_t)c.misc[kNPts];
     const uint32_t k = act ? c.perm[slot] : 0u;
     const uint32_t h = act ? src.w(k) : 0u;
     RowCounts rc{0, 0, 0};
