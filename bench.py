@@ -88,7 +88,7 @@ class ClockSampler:
         try:
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -222,12 +222,23 @@ def run_ours(args):
     def step():
         dg.matvec(x, y, form=args.form, stream=stream.cuda_stream)
 
+    sampler = ClockSampler(local, enabled=not args.no_clocks)
     for _ in range(args.warmup):
         flush.zero_()
         step()
     torch.cuda.synchronize(dev)
 
-    sampler = ClockSampler(local, enabled=not args.no_clocks)
+    def keep_busy(seconds):  # same launches, untimed: lets nvidia-smi sample clocks under this load
+        if args.no_clocks:
+            return
+        t_end = time.time() + seconds
+        while time.time() < t_end:
+            for _ in range(8):
+                flush.zero_()
+                step()
+            torch.cuda.synchronize(dev)
+
+    keep_busy(0.6)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
@@ -240,7 +251,10 @@ def run_ours(args):
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
+    keep_busy(0.4)
     clocks = sampler.stop()
+    if clocks is not None:
+        clocks["how"] = "nvidia-smi -lms 50 across warm-up, the timed steps and surrounding identical untimed launches"
     times = np.array([a.elapsed_time(b) for a, b in evs])  # ms per launch
     t_mean = float(times.mean())
     if world > 1:
