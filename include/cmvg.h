@@ -113,6 +113,12 @@ typedef struct {
   uint64_t bvd_codes;           /* body codes = decode-loop iterations     */
   uint32_t max_block_words, stream_cap_words;
   double window_coverage;       /* gathered columns inside the x-window    */
+  /* BV-S (sliced layout of the gather / PageRank kernels) */
+  uint64_t bvs_stream_bytes;
+  uint32_t bvs_max_block_words, bvs_stream_cap_words, bvs_p995_block_words, bvs_pad;
+  uint64_t bvs_slices, bvs_heavy_rows;
+  uint64_t bvs_lane_words, bvs_lane_words_used; /* slice body words incl. / excl. lane padding */
+  uint64_t bvs_lane_iters, bvs_lane_iters_used; /* slice decode lane-iterations incl. / excl. idle lanes */
 } cmvg_graph_info;
 
 /* ---- errors -------------------------------------------------------------- */
@@ -153,6 +159,9 @@ int cmvg_layout_info(const cmvg_bvstream* s, const cmvg_create_opts* opts, cmvg_
 typedef struct cmvg_layout cmvg_layout;
 int cmvg_layout_export(const cmvg_bvstream* s, const cmvg_create_opts* opts, cmvg_layout** out);
 const uint32_t* cmvg_layout_words(const cmvg_layout* l, uint64_t* nwords);
+/* BV-S words / block table (same 8-u32 block entries) */
+const uint32_t* cmvg_layout_swords(const cmvg_layout* l, uint64_t* nwords);
+const uint32_t* cmvg_layout_sblocks(const cmvg_layout* l, uint32_t* nblocks);
 const uint32_t* cmvg_layout_blocks(const cmvg_layout* l, uint32_t* nblocks);
 void cmvg_layout_free(cmvg_layout* l);
 int cmvg_graph_info_get(const cmvg_graph* g, cmvg_graph_info* out);

@@ -85,7 +85,12 @@ class _InfoC(C.Structure):
                 ("block_rows", C.c_uint32), ("lanes", C.c_uint32), ("window", C.c_uint32), ("nblocks", C.c_uint32),
                 ("max_depth", C.c_uint32), ("interval_mode", C.c_uint32), ("adds_per_product", C.c_uint64),
                 ("device_bytes", C.c_uint64), ("bvd_codes", C.c_uint64), ("max_block_words", C.c_uint32),
-                ("stream_cap_words", C.c_uint32), ("window_coverage", C.c_double)]
+                ("stream_cap_words", C.c_uint32), ("window_coverage", C.c_double),
+                ("bvs_stream_bytes", C.c_uint64), ("bvs_max_block_words", C.c_uint32),
+                ("bvs_stream_cap_words", C.c_uint32), ("bvs_p995_block_words", C.c_uint32), ("bvs_pad", C.c_uint32),
+                ("bvs_slices", C.c_uint64), ("bvs_heavy_rows", C.c_uint64), ("bvs_lane_words", C.c_uint64),
+                ("bvs_lane_words_used", C.c_uint64), ("bvs_lane_iters", C.c_uint64),
+                ("bvs_lane_iters_used", C.c_uint64)]
 
 
 _lib_handle: Optional[C.CDLL] = None
@@ -118,6 +123,8 @@ _SIGS = [
     ("cmvg_layout_export", C.c_int, [_P, C.POINTER(_OptsC), C.POINTER(_P)]),
     ("cmvg_layout_words", _P, [_P, C.POINTER(C.c_uint64)]),
     ("cmvg_layout_blocks", _P, [_P, C.POINTER(C.c_uint32)]),
+    ("cmvg_layout_swords", _P, [_P, C.POINTER(C.c_uint64)]),
+    ("cmvg_layout_sblocks", _P, [_P, C.POINTER(C.c_uint32)]),
     ("cmvg_layout_free", None, [_P]),
     ("cmvg_graph_info_get", C.c_int, [_P, C.POINTER(_InfoC)]),
     ("cmvg_dimension", C.c_uint32, [_P]),
@@ -296,16 +303,19 @@ class BvStream:
         _check(load_library().cmvg_layout_info(self._h, C.byref(oc), C.byref(inf)))
         return {f: getattr(inf, f) for f, _ in _InfoC._fields_}
 
-    def layout_export(self, options: Optional["CreateOptions"] = None):
-        """(words u32[], blocks u32[nblocks, 4]) of the device layout, built on the host."""
+    def layout_export(self, options: Optional["CreateOptions"] = None, sliced: bool = False):
+        """(words u32[], blocks u32[nblocks, 8]) of the device layout (BV-D, or
+        BV-S with sliced=True), built on the host."""
         oc = (options or CreateOptions())._c()
         h = _P()
         lib = load_library()
         _check(lib.cmvg_layout_export(self._h, C.byref(oc), C.byref(h)))
         try:
             nw, nb = C.c_uint64(), C.c_uint32()
-            w = _np_view(lib.cmvg_layout_words(h, C.byref(nw)), nw.value, np.uint32).copy()
-            b = _np_view(lib.cmvg_layout_blocks(h, C.byref(nb)), nb.value * 8, np.uint32).reshape(-1, 8).copy()
+            fw, fb = (lib.cmvg_layout_swords, lib.cmvg_layout_sblocks) if sliced else \
+                (lib.cmvg_layout_words, lib.cmvg_layout_blocks)
+            w = _np_view(fw(h, C.byref(nw)), nw.value, np.uint32).copy()
+            b = _np_view(fb(h, C.byref(nb)), nb.value * 8, np.uint32).reshape(-1, 8).copy()
         finally:
             lib.cmvg_layout_free(h)
         return w, b

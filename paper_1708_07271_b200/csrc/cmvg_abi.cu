@@ -160,6 +160,18 @@ const uint64_t* cmvg_bv_segment_offsets(const cmvg_bvstream* s, uint64_t* count)
 void cmvg_bv_free(cmvg_bvstream* s) { delete s; }
 
 // ---- device handle ----------------------------------------------------------
+static void fill_bvs_info(cmvg_graph_info* o, const BvsStats& st, uint32_t cap) {
+  o->bvs_stream_bytes = st.stream_bytes;
+  o->bvs_max_block_words = st.max_block_words;
+  o->bvs_stream_cap_words = cap;
+  o->bvs_p995_block_words = st.p995_block_words;
+  o->bvs_slices = st.slices;
+  o->bvs_heavy_rows = st.heavy_rows;
+  o->bvs_lane_words = st.lane_words;
+  o->bvs_lane_words_used = st.lane_words_used;
+  o->bvs_lane_iters = st.lane_iters;
+  o->bvs_lane_iters_used = st.lane_iters_used;
+}
 void cmvg_default_opts(cmvg_create_opts* o) {
   if (!o) return;
   o->device = 0;
@@ -236,6 +248,21 @@ int cmvg_create(const cmvg_bvstream* s, const cmvg_create_opts* opts_in, cmvg_gr
     wds.resize(wds.size() + 8, 0);
     g->words.upload(wds.data(), wds.size());
     g->blocks.upload(bl.data(), bl.size());
+    {
+      const uint64_t s0 = L.sblocks[g->block_begin].word_offset;
+      const uint64_t s1 = L.sblocks[block_end - 1].word_offset + L.sblocks[block_end - 1].nwords;
+      std::vector<BvdBlockInfo> sbl(L.sblocks.begin() + g->block_begin, L.sblocks.begin() + block_end);
+      for (auto& b : sbl) b.word_offset -= s0;
+      std::vector<uint32_t> sw(L.swords.begin() + s0, L.swords.begin() + s1);
+      sw.resize(sw.size() + 2 * kBvsGuardWords, 0);
+      g->swords.upload(sw.data(), sw.size());
+      g->sblocks.upload(sbl.data(), sbl.size());
+      g->s_stream_bytes = (s1 - s0) * 4;
+      g->sstats = L.sstats;
+      g->scap_words = o.stream_cap_words ? o.stream_cap_words : bvs_auto_cap(L.dims, L.sstats.p995_block_words);
+      const char* gl = getenv("CMVG_GATHER_LAYOUT");
+      g->gather_bvd = gl && std::string(gl) == "bvd";
+    }
     g->refd.upload(dec.ref_dist.data() + o.row_begin, row_end - o.row_begin);
     // stats of the shard
     g->stats.stream_bytes = (w1 - w0) * 4;
@@ -284,6 +311,8 @@ int cmvg_layout_info(const cmvg_bvstream* s, const cmvg_create_opts* opts_in, cm
                               ? opt.stream_cap_words
                               : std::min<uint32_t>(12288, std::max<uint32_t>(1024, (L.stats.p995_block_words + 255) & ~255u));
     o->window_coverage = L.stats.window_coverage;
+    fill_bvs_info(o, L.sstats, opt.stream_cap_words ? opt.stream_cap_words
+                                                   : bvs_auto_cap(L.dims, L.sstats.p995_block_words));
   });
 }
 
@@ -312,6 +341,16 @@ const uint32_t* cmvg_layout_blocks(const cmvg_layout* l, uint32_t* nblocks) {
   if (!l) return nullptr;
   if (nblocks) *nblocks = (uint32_t)l->L.blocks.size();
   return reinterpret_cast<const uint32_t*>(l->L.blocks.data());
+}
+const uint32_t* cmvg_layout_swords(const cmvg_layout* l, uint64_t* nwords) {
+  if (!l) return nullptr;
+  if (nwords) *nwords = l->L.swords.size();
+  return l->L.swords.data();
+}
+const uint32_t* cmvg_layout_sblocks(const cmvg_layout* l, uint32_t* nblocks) {
+  if (!l) return nullptr;
+  if (nblocks) *nblocks = (uint32_t)l->L.sblocks.size();
+  return reinterpret_cast<const uint32_t*>(l->L.sblocks.data());
 }
 void cmvg_layout_free(cmvg_layout* l) { delete l; }
 
@@ -349,6 +388,8 @@ int cmvg_graph_info_get(const cmvg_graph* g, cmvg_graph_info* o) {
     o->max_block_words = g->dims.max_block_words;
     o->stream_cap_words = g->stream_cap_words;
     o->window_coverage = g->stats.window_coverage;
+    fill_bvs_info(o, g->sstats, g->scap_words);
+    o->bvs_stream_bytes = g->s_stream_bytes;
   });
 }
 
@@ -363,6 +404,14 @@ namespace {
 
 template <typename XT, typename YT>
 void launch_gather(cmvg_graph* g, const XT* x, YT* y, cudaStream_t st) {
+  if (!g->gather_bvd) {
+    const BvsSmem L = bvs_smem_layout(g->dims, g->scap_words, sizeof(XT));
+    auto kern = bvs_gather_kernel<XT, YT>;
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
+    kern<<<g->nblocks, g->threads, L.total, st>>>(g->sdev(), x, y, PrArgs{});
+    CUDA_TRY(cudaGetLastError());
+    return;
+  }
   GatherSmem L = gather_smem_layout(g->dims, g->stream_cap_words, sizeof(XT), true);
   auto kern = bvd_gather_kernel<XT, YT>;
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));

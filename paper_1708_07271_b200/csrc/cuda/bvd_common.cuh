@@ -242,6 +242,12 @@ __device__ __forceinline__ uint32_t next_round(int* counter) {
   if ((threadIdx.x & 31u) == 0) rb = 32u * (uint32_t)atomicAdd(counter, 1);
   return __shfl_sync(0xffffffffu, rb, 0);
 }
+// Split claim: issue the atomic early (lane 0), consume its result later, so
+// the shared-atomic latency overlaps the current round's decode.
+__device__ __forceinline__ uint32_t claim_issue(int* counter) {
+  return (threadIdx.x & 31u) == 0 ? (uint32_t)atomicAdd(counter, 1) : 0u;
+}
+__device__ __forceinline__ uint32_t claim_take(uint32_t ticket) { return 32u * __shfl_sync(0xffffffffu, ticket, 0); }
 
 // Compensated accumulation: TwoSum, error term into `c` (error ~ eps|sum| +
 // n eps^2 sum|t|), so y_i stays accurate when the differential terms cancel.
@@ -330,8 +336,32 @@ struct PageRankEpi {
 // Writes y (YT) with coalesced stores.  Uses c.perm as the pointer array.
 template <typename YT, class EPI = PlainEpi>
 __device__ __forceinline__ void chain_and_store(double* s_yhi, float* s_ylo, RowCtx& c, YT* __restrict__ yb,
-                                                EPI epi = EPI()) {
+                                                EPI epi = EPI(), uint32_t max_depth = 0xffffffffu) {
   const uint32_t T = blockDim.x, tid = threadIdx.x;
+  if (max_depth <= 3) {
+    // Bounded chains (R <= 3): each row walks its <= 3 ancestors and sums
+    // from the root, y = d_i + (d_p1 + (d_p2 + d_p3)) in double-double --
+    // the reference's order, no barriers.
+    for (uint32_t k = tid; k < c.nr; k += T) {
+      const uint32_t r1 = c.ref[k];
+      const uint32_t p1 = k - r1;
+      const uint32_t r2 = r1 ? c.ref[p1] : 0u;
+      const uint32_t p2 = p1 - r2;
+      const uint32_t r3 = r2 ? c.ref[p2] : 0u;
+      const uint32_t p3 = p2 - r3;
+      double hi = 0.0, lo = 0.0;
+      if (r3) {
+        hi = s_yhi[p3];
+        lo = s_ylo[p3];
+      }
+      if (r2) dd_add(hi, lo, s_yhi[p2], s_ylo[p2]);
+      if (r1) dd_add(hi, lo, s_yhi[p1], s_ylo[p1]);
+      dd_add(hi, lo, s_yhi[k], s_ylo[k]);
+      epi.store(yb, k, hi + lo);
+    }
+    epi.finish(c.wscratch);
+    return;
+  }
   constexpr uint32_t kMaxPer = 4;  // rows per thread per level (block_rows / threads <= 4)
   constexpr uint16_t kNone = 0xffffu;
   uint16_t* ptr = c.perm;

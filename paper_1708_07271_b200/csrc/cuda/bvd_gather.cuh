@@ -73,9 +73,9 @@ __device__ __forceinline__ void gather_points(const RowCtx& c, const S& src, con
   const int nesc = c.misc[kNesc];
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t npts = (uint32_t)c.misc[kNPts];
-  for (;;) {
-    const uint32_t rb = next_round(&c.misc[kRoundP]);
-    if (rb >= npts) break;
+  uint32_t rb = claim_take(claim_issue(&c.misc[kRoundP]));
+  while (rb < npts) {
+    const uint32_t ticket = claim_issue(&c.misc[kRoundP]);
     const RowDesc r = round_row(c, src, c.perm, rb + lane, npts, nesc);
     const uint32_t wp = hdr_wp(r.h);
     const bool far = hdr_far(r.h);
@@ -87,15 +87,30 @@ __device__ __forceinline__ void gather_points(const RowCtx& c, const S& src, con
     double acc = 0.0, comp = 0.0;
     const uint32_t tp = __reduce_max_sync(0xffffffffu, np);
     if (!any_far) {
-#pragma unroll 4
-      for (uint32_t t = 0; t < tp; ++t) {
+      // two independent compensated chains (even / odd codes) halve the
+      // dependent FP64 latency per code
+      double acc2 = 0.0, comp2 = 0.0;
+      uint32_t t = 0;
+#pragma unroll 2
+      for (; t + 1 < tp; t += 2) {
+        const bool on0 = t < np, on1 = t + 1 < np;
+        const uint32_t v0 = extract_bits(src, off, wp);
+        const uint32_t off1 = off + (on0 ? wp : 0u);
+        const uint32_t v1 = extract_bits(src, off1, wp);
+        const double x0 = xw.at_near(on0 ? ib + v0 : 0u);
+        const double x1 = xw.at_near(on1 ? ib + v1 : 0u);
+        tsum(acc, comp, on0 ? (t < nm ? -x0 : x0) : 0.0);
+        tsum(acc2, comp2, on1 ? (t + 1 < nm ? -x1 : x1) : 0.0);
+        off = off1 + (on1 ? wp : 0u);
+      }
+      if (t < tp) {
         const bool on = t < np;
         const uint32_t v = extract_bits(src, off, wp);
         const double xv = xw.at_near(on ? ib + v : 0u);
-        const double term = on ? (t < nm ? -xv : xv) : 0.0;
-        tsum(acc, comp, term);
-        off += on ? wp : 0u;
+        tsum(acc, comp, on ? (t < nm ? -xv : xv) : 0.0);
       }
+      tsum(acc, comp, acc2);
+      comp += comp2;
     } else {
       for (uint32_t t = 0; t < tp; ++t) {
         const bool on = t < np;
@@ -112,6 +127,7 @@ __device__ __forceinline__ void gather_points(const RowCtx& c, const S& src, con
       s_yhi[r.k] = hi;
       s_ylo[r.k] = (float)(comp - (hi - acc));
     }
+    rb = claim_take(ticket);
   }
 }
 
@@ -123,9 +139,9 @@ __device__ __forceinline__ void gather_intervals(const RowCtx& c, const S& src, 
   const int nesc = c.misc[kNesc];
   const uint32_t nri = (uint32_t)c.misc[kNInt];
   const uint32_t lane = threadIdx.x & 31u;
-  for (;;) {
-    const uint32_t rb = next_round(&c.misc[kRoundI]);
-    if (rb >= nri) break;
+  uint32_t rb = claim_take(claim_issue(&c.misc[kRoundI]));
+  while (rb < nri) {
+    const uint32_t ticket = claim_issue(&c.misc[kRoundI]);
     const RowDesc r = round_row(c, src, c.permi, rb + lane, nri, nesc);
     const uint32_t wp = hdr_wp(r.h), wl = hdr_wl(r.h);
     const bool far = hdr_far(r.h);
@@ -152,6 +168,7 @@ __device__ __forceinline__ void gather_intervals(const RowCtx& c, const S& src, 
       s_yhi[r.k] = hi;
       s_ylo[r.k] = (float)lo;
     }
+    rb = claim_take(ticket);
   }
 }
 
@@ -204,15 +221,17 @@ __device__ __forceinline__ void gather_heavy(const RowCtx& c, const S& src, cons
 }
 
 template <typename XT, typename YT, bool PREFIX, class S, class EPI>
-__device__ __forceinline__ void gather_block(RowCtx& rc, const S& src, const XWin<XT, PREFIX>& xw, const BvdDims& D,
-                                             uint32_t r0, int nesc, double* s_yhi, float* s_ylo, YT* yb, EPI& epi) {
+__device__ __forceinline__ void gather_block(RowCtx& rc, const S& src, XWin<XT, PREFIX>& xw, const BvdDims& D,
+                                             uint32_t r0, int nesc, double* s_yhi, float* s_ylo, YT* yb, EPI& epi,
+                                             const XT (&xpre)[XWin<XT, PREFIX>::kPre]) {
   row_setup(rc, src, nesc, /*split_heavy=*/true);
+  xw.stage(D.n, xpre);  // ends with __syncthreads
   gather_heavy(rc, src, xw, (int32_t)r0, D.min_interval, s_yhi, s_ylo);
   gather_points(rc, src, xw, (int32_t)r0, s_yhi, s_ylo);
   __syncthreads();
   gather_intervals(rc, src, xw, (int32_t)r0, D.min_interval, s_yhi, s_ylo);
   __syncthreads();
-  chain_and_store(s_yhi, s_ylo, rc, yb, epi);
+  chain_and_store(s_yhi, s_ylo, rc, yb, epi, D.max_depth);
 }
 
 // PageRank step arguments (shard-relative pointers; see PageRankEpi).
@@ -229,7 +248,7 @@ struct PrArgs {
 };
 
 template <typename XT, typename YT, bool PR = false>
-__global__ void __launch_bounds__(256) bvd_gather_kernel(BvdDev g, const XT* __restrict__ x, YT* __restrict__ y,
+__global__ void __launch_bounds__(256, 3) bvd_gather_kernel(BvdDev g, const XT* __restrict__ x, YT* __restrict__ y,
                                                           PrArgs pr) {
   extern __shared__ __align__(16) unsigned char smem[];
   const BvdDims& D = g.d;
@@ -247,7 +266,9 @@ __global__ void __launch_bounds__(256) bvd_gather_kernel(BvdDev g, const XT* __r
   xw.carve(smem + L.off_x, D.window);
   xw.x = x;
   xw.wlo = bi.wlo;
-  xw.stage(D.n);  // ends with __syncthreads (also publishes the mbarrier init)
+  XT xpre[XWin<XT, true>::kPre];
+  xw.prefetch(D.n, xpre);  // in flight across the stream wait and row setup
+  __syncthreads();         // publishes the mbarrier init
   mbar_wait(rc.bar, 0);
 
   double* s_yhi = reinterpret_cast<double*>(smem + L.off_yhi);
@@ -269,19 +290,19 @@ __global__ void __launch_bounds__(256) bvd_gather_kernel(BvdDev g, const XT* __r
     epi.l1 = 0.0;
     if (staged) {
       const Src<true> src{smem_u32(s_stream)};
-      gather_block<XT, YT, true>(rc, src, xw, D, r0, (int)bi.nesc, s_yhi, s_ylo, yb, epi);
+      gather_block<XT, YT, true>(rc, src, xw, D, r0, (int)bi.nesc, s_yhi, s_ylo, yb, epi, xpre);
     } else {
       const Src<false> src{g.words + bi.word_offset};
-      gather_block<XT, YT, true>(rc, src, xw, D, r0, (int)bi.nesc, s_yhi, s_ylo, yb, epi);
+      gather_block<XT, YT, true>(rc, src, xw, D, r0, (int)bi.nesc, s_yhi, s_ylo, yb, epi, xpre);
     }
   } else {
     PlainEpi epi;
     if (staged) {  // CTA-uniform
       const Src<true> src{smem_u32(s_stream)};
-      gather_block<XT, YT, true>(rc, src, xw, D, r0, (int)bi.nesc, s_yhi, s_ylo, yb, epi);
+      gather_block<XT, YT, true>(rc, src, xw, D, r0, (int)bi.nesc, s_yhi, s_ylo, yb, epi, xpre);
     } else {
       const Src<false> src{g.words + bi.word_offset};
-      gather_block<XT, YT, true>(rc, src, xw, D, r0, (int)bi.nesc, s_yhi, s_ylo, yb, epi);
+      gather_block<XT, YT, true>(rc, src, xw, D, r0, (int)bi.nesc, s_yhi, s_ylo, yb, epi, xpre);
     }
   }
 }

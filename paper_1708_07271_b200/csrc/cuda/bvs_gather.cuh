@@ -1,0 +1,304 @@
+// bvs_gather: y = A * x^T on the sliced layout BV-S (host/layout.hpp) -- the
+// gather hot path, replacing the reference's sequential `matvec_ref_into`
+// (include/cmv/ref_matvec.hpp:20-31), and
+// (PR = true) the product + update of one PageRank iteration
+// (pagerank.hpp:83-102).
+//
+// One CTA per block of B rows (reference chains never leave a block):
+//   1. thread 0 issues a TMA bulk copy of the block's sliced stream into
+//      shared memory (mbarrier completion) while all threads stage the
+//      x-window x[wlo, wlo + W) and its two-level double-double prefix;
+//   2. warps claim work dynamically: first heavy rows (one warp per row,
+//      lanes stride over its fixed-width codes), then 32-row slices (one row
+//      per lane; the transcoder already sorted rows into slices of near-equal
+//      work and interleaved their code streams by lane, so there is no row
+//      setup and every code read is a conflict-free shared load).  Points
+//      (minus -> -x[c], residual -> +x[c]) then intervals (O(1) from the
+//      prefix), delta_i accumulated with TwoSum compensation;
+//   3. one barrier, then the reference chains y_i = delta_i + y_{i-r}
+//      (ref_matvec.hpp:23-25) and the coalesced store / PageRank epilogue.
+#pragma once
+#include <cstdint>
+
+#include "bvd_common.cuh"
+#include "bvd_gather.cuh"
+
+namespace cmvg {
+
+constexpr uint32_t kBvsGuardWords = 64;  // zeroed words after a staged block
+
+struct BvsSmem {
+  uint32_t off_x, off_yhi, off_ylo, off_exh, off_exl, off_ptr, off_ref, off_misc, total;
+};
+
+__host__ __device__ inline BvsSmem bvs_smem_layout(const BvdDims& d, uint32_t stream_cap_words, uint32_t xsize) {
+  BvsSmem s;
+  uint32_t o = align16((stream_cap_words + kBvsGuardWords) * 4);
+  s.off_x = o;
+  o = align16(o + xw_bytes(d.window, xsize, true));
+  s.off_yhi = o;
+  o = align16(o + d.block_rows * 8);
+  s.off_ylo = o;
+  o = align16(o + d.block_rows * 4);
+  // extra-unit partials (fold) -- reused as the chain pointers afterwards
+  const uint32_t ex = d.max_extras;
+  s.off_exh = o;
+  s.off_ptr = o;
+  s.off_exl = align16(o + ex * 8);
+  o = max(align16(s.off_exl + ex * 4), align16(o + d.block_rows * 2));
+  s.off_ref = o;
+  o = align16(o + d.block_rows);
+  s.off_misc = o;  // mbarrier (16) + 16 ints + scratch (64 ints)
+  o = align16(o + 16 + 64 + 64 * 4);
+  s.total = o;
+  return s;
+}
+
+// Bits [pos, pos + w) of this lane's stream in a lane-interleaved body.
+template <class S>
+__device__ __forceinline__ uint32_t lane_bits(const S& src, uint32_t body, uint32_t pos, uint32_t w) {
+  const uint32_t a = body + (pos >> 5) * 32u;
+  const uint32_t v = __funnelshift_l(src.w(a + 32u), src.w(a), pos & 31u);
+  return w ? v >> (32u - w) : 0u;
+}
+
+__device__ __forceinline__ uint32_t ticket_issue(int* counter) {
+  return (threadIdx.x & 31u) == 0 ? (uint32_t)atomicAdd(counter, 1) : 0u;
+}
+__device__ __forceinline__ uint32_t ticket_take(uint32_t t) { return __shfl_sync(0xffffffffu, t, 0); }
+
+enum BvsMisc : int { kBvsHeavyCtr = 0, kBvsSliceCtr = 1 };
+
+// Heavy rows: one warp per row (see gather_heavy in bvd_gather.cuh).
+template <class S, class XW>
+__device__ __forceinline__ void bvs_heavy(const S& src, const XW& xw, int32_t r0, uint32_t lmin, int* misc,
+                                          double* s_yhi, float* s_ylo, uint8_t* s_ref) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t nh = src.w(0) >> 16, htab = src.w(1), hbase = src.w(2) * 32u;
+  for (;;) {
+    const uint32_t q = ticket_take(ticket_issue(&misc[kBvsHeavyCtr]));
+    if (q >= nh) break;
+    const uint32_t e = htab + q * kBvsHeavyEntry;
+    const uint32_t sa = src.w(e), nm = src.w(e + 1), ns = src.w(e + 2), ni = src.w(e + 3);
+    const uint32_t off0 = hbase + src.w(e + 4);
+    const uint32_t k = sa_k(sa), wp = sa_wp(sa), wl = sa_wl(sa);
+    const int32_t ib = r0 + (int32_t)k - (int32_t)code_bias(wp);
+    const uint32_t np = nm + ns;
+    double acc = 0.0, comp = 0.0;
+    for (uint32_t t = lane; t < np; t += 32) {
+      const double xv = xw.at(ib + (int32_t)extract_bits(src, off0 + t * wp, wp));
+      tsum(acc, comp, t < nm ? -xv : xv);
+    }
+    const uint32_t ioff = off0 + np * wp;
+    for (uint32_t t = lane; t < ni; t += 32) {
+      const uint32_t o = ioff + t * (wp + wl);
+      const int32_t left = ib + (int32_t)extract_bits(src, o, wp);
+      const uint32_t len = extract_bits(src, o + wp, wl) + lmin;
+      double lo;
+      const double hi = xw.isum(left, len, lo);
+      tsum(acc, comp, hi);
+      comp += lo;
+    }
+    double hi = acc + comp, lo = comp - (hi - acc);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double uh = __shfl_down_sync(0xffffffffu, hi, o), ul = __shfl_down_sync(0xffffffffu, lo, o);
+      dd_add(hi, lo, uh, ul);
+    }
+    if (lane == 0) {
+      s_yhi[k] = hi;
+      s_ylo[k] = (float)lo;
+      s_ref[k] = (uint8_t)sa_r(sa);
+    }
+  }
+}
+
+// x-window index of a class-16 code
+__device__ __forceinline__ uint32_t c16_idx(uint32_t code) { return code - kBvsBias16; }
+// +x, or -x for t < nm (minus codes come first): flip the sign bit when t - nm < 0
+__device__ __forceinline__ double signed_term(double x, uint32_t t, uint32_t nm) {
+  const uint32_t m = (t - nm) & 0x80000000u;
+  return __hiloint2double(__double2hiint(x) ^ (int)m, __double2loint(x));
+}
+
+// Slices: one unit (<= 16 points, <= 2 intervals of one row) per lane.
+template <class S, class XW>
+__device__ __forceinline__ void bvs_slices(const S& src, const XW& xw, uint32_t lmin, int* misc, double* s_yhi,
+                                           float* s_ylo, uint8_t* s_ref, double* s_exh, float* s_exl) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t nsl = src.w(0) & 0xffffu;
+  const uint32_t Z = xw.W;  // zero entry of the window (idle lanes read it)
+  uint32_t s = ticket_take(ticket_issue(&misc[kBvsSliceCtr]));
+  while (s < nsl) {
+    const uint32_t next = ticket_issue(&misc[kBvsSliceCtr]);
+    const uint32_t rec = src.w(kBvsHead + s);
+    const uint32_t meta = src.w(rec);
+    const uint32_t h = src.w(rec + 1u + lane);
+    const uint32_t body = rec + 33u + lane;
+    const uint32_t nm = uh_nm(h), np = uh_np(h), ni = uh_ni(h);
+    const uint32_t mnp = smeta_np(meta), mni = smeta_ni(meta);
+    double acc = 0.0, comp = 0.0;
+    if (!smeta_c32(meta)) {
+      const uint32_t ibase = body + ((np + 1u) >> 1) * 32u;  // this lane's first interval word
+      if (!smeta_far(meta)) {
+        double acc2 = 0.0, comp2 = 0.0;
+#pragma unroll 2
+        for (uint32_t t = 0; t < mnp; t += 2) {
+          const uint32_t w = src.w(body + (t >> 1) * 32u);
+          const uint32_t i0 = t < np ? c16_idx(w >> 16) : Z;
+          const uint32_t i1 = t + 1u < np ? c16_idx(w & 0xffffu) : Z;
+          tsum(acc, comp, signed_term(xw.at_near(i0), t, nm));
+          tsum(acc2, comp2, signed_term(xw.at_near(i1), t + 1u, nm));
+        }
+        tsum(acc, comp, acc2);
+        comp += comp2;
+        for (uint32_t u = 0; u < mni; ++u) {
+          const uint32_t w = src.w(ibase + u * 32u);
+          const bool on = u < ni;
+          double lo;
+          const double hi = xw.isum_near(on ? c16_idx(w >> 16) : 0u, on ? (w & 0xffffu) + lmin : 0u, lo);
+          tsum(acc, comp, hi);
+          comp += lo;
+        }
+      } else {
+        for (uint32_t t = 0; t < mnp; ++t) {
+          const uint32_t w = src.w(body + (t >> 1) * 32u);
+          const uint32_t c = (t & 1u) ? (w & 0xffffu) : (w >> 16);
+          const double xv = t < np ? xw.at((int32_t)c16_idx(c) + (int32_t)xw.wlo) : 0.0;
+          tsum(acc, comp, signed_term(xv, t, nm));
+        }
+        for (uint32_t u = 0; u < mni; ++u) {
+          const uint32_t w = src.w(ibase + u * 32u);
+          double hi = 0.0, lo = 0.0;
+          if (u < ni) hi = xw.isum((int32_t)c16_idx(w >> 16) + (int32_t)xw.wlo, (w & 0xffffu) + lmin, lo);
+          tsum(acc, comp, hi);
+          comp += lo;
+        }
+      }
+    } else {  // class 32: absolute columns, bounds-checked
+      for (uint32_t t = 0; t < mnp; ++t) {
+        const uint32_t c = src.w(body + t * 32u);
+        const double xv = t < np ? xw.at((int32_t)c) : 0.0;
+        tsum(acc, comp, signed_term(xv, t, nm));
+      }
+      const uint32_t ibase = body + np * 32u;
+      for (uint32_t u = 0; u < mni; ++u) {
+        double hi = 0.0, lo = 0.0;
+        if (u < ni) hi = xw.isum((int32_t)src.w(ibase + 2u * u * 32u), src.w(ibase + (2u * u + 1u) * 32u) + lmin, lo);
+        tsum(acc, comp, hi);
+        comp += lo;
+      }
+    }
+    if (uh_valid(h)) {
+      const double hi = acc + comp;
+      const float lo = (float)(comp - (hi - acc));
+      const uint32_t ks = uh_kslot(h);
+      if (uh_primary(h)) {
+        s_yhi[ks] = hi;
+        s_ylo[ks] = lo;
+        s_ref[ks] = (uint8_t)uh_r(h);
+      } else {
+        s_exh[ks] = hi;
+        s_exl[ks] = lo;
+      }
+    }
+    s = ticket_take(next);
+  }
+}
+
+// Fold extra-unit partials into their rows' deltas (after the decode barrier).
+template <class S>
+__device__ __forceinline__ void bvs_fold(const S& src, double* s_yhi, float* s_ylo, const double* s_exh,
+                                         const float* s_exl) {
+  const uint32_t nsl = src.w(0) & 0xffffu, nf = src.w(3) & 0xffffu;
+  for (uint32_t f = threadIdx.x; f < nf; f += blockDim.x) {
+    const uint32_t e = src.w(kBvsHead + nsl + f);
+    const uint32_t k = e & 1023u, first = (e >> 10) & 2047u, cnt = e >> 21;
+    double hi = s_yhi[k], lo = s_ylo[k];
+    for (uint32_t c = 0; c < cnt; ++c) dd_add(hi, lo, s_exh[first + c], s_exl[first + c]);
+    s_yhi[k] = hi;
+    s_ylo[k] = (float)lo;
+  }
+}
+
+template <typename XT, typename YT, bool PR = false>
+__global__ void __launch_bounds__(256, 3) bvs_gather_kernel(BvdDev g, const XT* __restrict__ x, YT* __restrict__ y,
+                                                             PrArgs pr) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const BvdDims& D = g.d;
+  const BvsSmem L = bvs_smem_layout(D, g.stream_cap_words, sizeof(XT));
+  const uint32_t bl = blockIdx.x;  // index into this shard's tables
+  const uint32_t b = g.block_begin + bl;
+  const BvdBlockInfo bi = g.blocks[bl];
+  const uint32_t r0 = b * D.block_rows;
+  const uint32_t nr = min(D.block_rows, D.n - r0);
+
+  uint32_t* s_stream = reinterpret_cast<uint32_t*>(smem);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.off_misc);
+  int* misc = reinterpret_cast<int*>(smem + L.off_misc + 16);
+  const bool staged = bi.nwords <= g.stream_cap_words;
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    const uint32_t sbytes = staged ? bi.nwords * 4u : 0u;
+    mbar_arrive_expect_tx(bar, sbytes);
+    if (sbytes) bulk_g2s(s_stream, g.words + bi.word_offset, sbytes, bar);
+    misc[kBvsHeavyCtr] = 0;
+    misc[kBvsSliceCtr] = 0;
+  }
+  if (threadIdx.x < kBvsGuardWords) s_stream[(staged ? bi.nwords : 0u) + threadIdx.x] = 0u;
+  XWin<XT, true> xw;
+  xw.carve(smem + L.off_x, D.window);
+  xw.x = x;
+  xw.wlo = bi.wlo;
+  XT xpre[XWin<XT, true>::kPre];
+  xw.prefetch(D.n, xpre);
+  __syncthreads();       // publishes the mbarrier init and the counters
+  xw.stage(D.n, xpre);   // ends with __syncthreads
+  mbar_wait(bar, 0);
+
+  double* s_yhi = reinterpret_cast<double*>(smem + L.off_yhi);
+  float* s_ylo = reinterpret_cast<float*>(smem + L.off_ylo);
+  uint8_t* s_ref = smem + L.off_ref;
+  double* s_exh = reinterpret_cast<double*>(smem + L.off_exh);
+  float* s_exl = reinterpret_cast<float*>(smem + L.off_exl);
+  auto decode = [&](const auto& src) {
+    bvs_heavy(src, xw, (int32_t)r0, D.min_interval, misc, s_yhi, s_ylo, s_ref);
+    bvs_slices(src, xw, D.min_interval, misc, s_yhi, s_ylo, s_ref, s_exh, s_exl);
+    __syncthreads();
+    if (src.w(3) & 0xffffu) {  // CTA-uniform
+      bvs_fold(src, s_yhi, s_ylo, s_exh, s_exl);
+      __syncthreads();
+    }
+  };
+  if (staged) decode(Src<true>{smem_u32(s_stream)});  // CTA-uniform
+  else decode(Src<false>{g.words + bi.word_offset});
+
+  RowCtx rc{};
+  rc.ref = s_ref;
+  rc.perm = reinterpret_cast<uint16_t*>(smem + L.off_ptr);
+  rc.wscratch = misc + 16;
+  rc.nr = nr;
+  rc.B = D.block_rows;
+  YT* yb = y + (r0 - g.row_begin);
+  if constexpr (PR) {
+    const uint32_t sh = r0 - g.row_begin;
+    PageRankEpi epi;
+    epi.deg = pr.deg + sh;
+    epi.p_prev = pr.p_prev ? pr.p_prev + sh : nullptr;
+    epi.q_next = pr.q_next + sh;
+    epi.partial = pr.partial;
+    epi.base = pr.alpha / (double)pr.n;
+    epi.scale = 1.0 - pr.alpha;
+    const double dm = pr.dmass ? *pr.dmass : pr.dmass_host;
+    epi.dn = pr.uniform ? dm / (double)pr.n : 0.0;
+    epi.bl = bl;
+    epi.dang = 0.0;
+    epi.l1 = 0.0;
+    chain_and_store(s_yhi, s_ylo, rc, yb, epi, D.max_depth);
+  } else {
+    PlainEpi epi;
+    chain_and_store(s_yhi, s_ylo, rc, yb, epi, D.max_depth);
+  }
+}
+
+}  // namespace cmvg

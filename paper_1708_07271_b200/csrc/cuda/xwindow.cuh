@@ -60,10 +60,32 @@ struct XWin {
     s_tl = reinterpret_cast<float*>(p);
   }
 
+  // Register prefetch of the first kPre*T window entries: issued before the
+  // stream wait and row setup so the global-load latency overlaps them.
+  static constexpr uint32_t kPre = 8;
+  __device__ __forceinline__ void prefetch(uint32_t n, XT (&r)[kPre]) const {
+#pragma unroll
+    for (uint32_t q = 0; q < kPre; ++q) {
+      const uint32_t j = threadIdx.x + q * blockDim.x, c = wlo + j;
+      r[q] = (j < W && c < n) ? __ldg(x + c) : XT(0);
+    }
+  }
+
   // Cooperative staging (all threads of the CTA); ends with __syncthreads().
   __device__ __forceinline__ void stage(uint32_t n) {
+    XT r[kPre];
+    prefetch(n, r);
+    stage(n, r);
+  }
+  __device__ __forceinline__ void stage(uint32_t n, const XT (&r)[kPre]) {
     const uint32_t T = blockDim.x, tid = threadIdx.x;
-    for (uint32_t j = tid; j < W; j += T) {
+#pragma unroll
+    for (uint32_t q = 0; q < kPre; ++q) {
+      const uint32_t j = tid + q * T;
+      if (j < W) s_x[xw_pad(j)] = r[q];
+    }
+    if (tid == 0) s_x[xw_pad(W)] = XT(0);  // zero entry for idle lanes
+    for (uint32_t j = tid + kPre * T; j < W; j += T) {
       const uint32_t c = wlo + j;
       s_x[xw_pad(j)] = c < n ? __ldg(x + c) : XT(0);
     }

@@ -50,6 +50,194 @@ void split_row(const HostCsr& g, uint32_t i, uint32_t r, uint32_t lmin, RowParts
 
 inline uint32_t bits_of(uint64_t v) { return v ? 64u - (uint32_t)__builtin_clzll(v) : 0u; }
 
+struct RowMeta {
+  uint32_t r, nm, ns, ni, wp, wl;
+  bool far;
+  uint64_t bit0, nbits;  // the row's body within the block's BV-D body stream
+};
+
+// 32 bits of `w` starting at bit `pos`, bits at or past `end` zero (MSB first)
+inline uint32_t bits32(const std::vector<uint32_t>& w, uint64_t pos, uint64_t end) {
+  if (pos >= end) return 0u;
+  const uint64_t wi = pos >> 5;
+  const uint32_t sh = (uint32_t)(pos & 31);
+  uint64_t win = (uint64_t)w[wi] << 32;
+  if (wi + 1 < w.size()) win |= w[wi + 1];
+  uint32_t v = (uint32_t)((win << sh) >> 32);
+  const uint64_t left = end - pos;
+  if (left < 32) v &= ~0u << (32 - left);
+  return v;
+}
+
+// BV-S block stream from the block's rows (layout.hpp).
+struct Unit {
+  uint32_t k, j, kslot, r, nm, np, ni;
+  bool primary, c32, far;
+  std::vector<uint32_t> words;
+};
+
+void emit_bvs(const RowParts* rps, const RowMeta* meta, const BitWriter& body, uint32_t r0, uint32_t nr, uint64_t wlo,
+              uint32_t W, uint32_t lmin, std::vector<uint32_t>& so, BvsStats& st, uint32_t& max_extras) {
+  auto nunits = [&](uint32_t k) {
+    const uint32_t np = meta[k].nm + meta[k].ns, ni = meta[k].ni;
+    return std::max<uint32_t>(1, std::max((np + kBvsUnitPts - 1) / kBvsUnitPts, (ni + kBvsUnitInts - 1) / kBvsUnitInts));
+  };
+  std::vector<char> heavy(nr, 0);
+  uint64_t extras = 0;
+  for (uint32_t k = 0; k < nr; ++k) {
+    const RowMeta& m = meta[k];
+    if (m.nm + m.ns + 2 * m.ni > kBvsHeavyCodes) heavy[k] = 1;
+    else extras += nunits(k) - 1;
+  }
+  if (extras > kBvsMaxExtras) {  // move the most-split rows to the warp path
+    std::vector<uint32_t> byu;
+    for (uint32_t k = 0; k < nr; ++k)
+      if (!heavy[k] && nunits(k) > 1) byu.push_back(k);
+    std::stable_sort(byu.begin(), byu.end(), [&](uint32_t a, uint32_t b) { return nunits(a) > nunits(b); });
+    for (uint32_t k : byu) {
+      if (extras <= kBvsMaxExtras) break;
+      heavy[k] = 1;
+      extras -= nunits(k) - 1;
+    }
+  }
+  auto inwin = [&](uint64_t c) { return c >= wlo && c < wlo + W; };
+  std::vector<Unit> units;
+  std::vector<uint32_t> fold, hrows;
+  uint32_t slot = 0;
+  std::vector<uint32_t> pts;
+  for (uint32_t k = 0; k < nr; ++k) {
+    if (heavy[k]) {
+      hrows.push_back(k);
+      continue;
+    }
+    const RowParts& rp = rps[k];
+    pts.assign(rp.minus.begin(), rp.minus.end());
+    pts.insert(pts.end(), rp.res.begin(), rp.res.end());
+    const uint32_t nm = (uint32_t)rp.minus.size(), np = (uint32_t)pts.size(), ni = (uint32_t)rp.ints.size();
+    const uint32_t nu = nunits(k);
+    if (nu > 1) fold.push_back(make_fold(k, slot, nu - 1));
+    for (uint32_t j = 0; j < nu; ++j) {
+      Unit u;
+      u.k = k;
+      u.j = j;
+      u.primary = j == 0;
+      u.kslot = j == 0 ? k : slot++;
+      u.r = meta[k].r;
+      const uint32_t p0 = std::min(np, j * kBvsUnitPts), p1 = std::min(np, p0 + kBvsUnitPts);
+      const uint32_t q0 = std::min(ni, j * kBvsUnitInts), q1 = std::min(ni, q0 + kBvsUnitInts);
+      u.np = p1 - p0;
+      u.ni = q1 - q0;
+      u.nm = nm > p0 ? std::min(nm, p1) - p0 : 0;
+      bool fits16 = true, far = false;
+      auto off_ok = [&](uint32_t c) {
+        const int64_t d = (int64_t)c - (int64_t)wlo;
+        return d >= -(int64_t)kBvsBias16 && d < (int64_t)kBvsBias16;
+      };
+      for (uint32_t t = p0; t < p1; ++t) {
+        fits16 &= off_ok(pts[t]);
+        far |= !inwin(pts[t]);
+      }
+      for (uint32_t t = q0; t < q1; ++t) {
+        const auto& iv = rp.ints[t];
+        fits16 &= off_ok(iv.first) && (iv.second - lmin) < 65536u;
+        far |= !inwin(iv.first) || !inwin((uint64_t)iv.first + iv.second - 1);
+      }
+      u.c32 = !fits16;
+      u.far = far;
+      auto code16 = [&](uint32_t c) { return (uint32_t)((int64_t)c - (int64_t)wlo + kBvsBias16); };
+      if (!u.c32) {
+        for (uint32_t t = p0; t < p1; t += 2) {
+          const uint32_t hi = code16(pts[t]), lo = t + 1 < p1 ? code16(pts[t + 1]) : 0u;
+          u.words.push_back((hi << 16) | lo);
+        }
+        for (uint32_t t = q0; t < q1; ++t) u.words.push_back((code16(rp.ints[t].first) << 16) | (rp.ints[t].second - lmin));
+      } else {
+        for (uint32_t t = p0; t < p1; ++t) u.words.push_back(pts[t]);
+        for (uint32_t t = q0; t < q1; ++t) {
+          u.words.push_back(rp.ints[t].first);
+          u.words.push_back(rp.ints[t].second - lmin);
+        }
+      }
+      units.push_back(std::move(u));
+    }
+  }
+  max_extras = std::max(max_extras, slot);
+  // deal units into slices: groups (class32, far), each by (#intervals, #points) desc
+  std::vector<uint32_t> order(units.size());
+  for (uint32_t q = 0; q < order.size(); ++q) order[q] = q;
+  auto gid = [&](const Unit& u) { return (u.c32 ? 0 : 2) + (u.far ? 0 : 1); };
+  std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
+    const Unit &x = units[a], &y = units[b];
+    if (gid(x) != gid(y)) return gid(x) < gid(y);
+    if (x.ni != y.ni) return x.ni > y.ni;
+    return x.np > y.np;
+  });
+  std::vector<std::pair<size_t, size_t>> slices;
+  for (size_t a = 0; a < order.size();) {
+    size_t e = a;
+    while (e < order.size() && e - a < 32 && gid(units[order[e]]) == gid(units[order[a]])) ++e;
+    slices.push_back({a, e});
+    a = e;
+  }
+  const uint32_t nsl = (uint32_t)slices.size(), nh = (uint32_t)hrows.size(), nf = (uint32_t)fold.size();
+  if (nsl > 0xffffu || nh > 0xffffu || nf > 0xffffu) throw std::runtime_error("BV-S: block too large");
+  so.assign(kBvsHead + nsl, 0u);
+  so[0] = nsl | (nh << 16);
+  so[3] = nf | (slot << 16);
+  so.insert(so.end(), fold.begin(), fold.end());
+  for (uint32_t s = 0; s < nsl; ++s) {
+    so[kBvsHead + s] = (uint32_t)so.size();
+    const size_t a = slices[s].first, e = slices[s].second;
+    uint32_t mnp = 0, mni = 0, nq = 0;
+    for (size_t q = a; q < e; ++q) {
+      const Unit& u = units[order[q]];
+      mnp = std::max(mnp, u.np);
+      mni = std::max(mni, u.ni);
+      nq = std::max<uint32_t>(nq, (uint32_t)u.words.size());
+      st.lane_words_used += u.words.size();
+      st.lane_iters_used += u.np + u.ni;
+    }
+    const Unit& u0 = units[order[a]];
+    so.push_back(make_smeta(mnp, mni, u0.c32, u0.far));
+    for (size_t l = 0; l < 32; ++l) {
+      if (a + l < e) {
+        const Unit& u = units[order[a + l]];
+        so.push_back(make_uh(u.primary, u.kslot, u.r, u.nm, u.np, u.ni));
+      } else {
+        so.push_back(0u);
+      }
+    }
+    const size_t b0 = so.size();
+    so.resize(b0 + (size_t)nq * 32, 0u);
+    for (size_t l = 0; a + l < e; ++l) {
+      const Unit& u = units[order[a + l]];
+      for (size_t q = 0; q < u.words.size(); ++q) so[b0 + q * 32 + l] = u.words[q];
+    }
+    st.lane_words += (uint64_t)nq * 32;
+    st.lane_iters += 32ull * (mnp + mni);
+  }
+  so[1] = (uint32_t)so.size();
+  BitWriter hs;
+  for (uint32_t k : hrows) {
+    const RowMeta& m = meta[k];
+    so.push_back(make_sa(k, m.r, m.wp, m.wl, m.far));
+    so.push_back(m.nm);
+    so.push_back(m.ns);
+    so.push_back(m.ni);
+    so.push_back((uint32_t)hs.nbits);
+    so.push_back(0u);
+    for (uint64_t p = m.bit0, e = m.bit0 + m.nbits; p < e; p += 32) {
+      const uint32_t take = (uint32_t)std::min<uint64_t>(32, e - p);
+      hs.put(bits32(body.words, p, e) >> (32 - take), (int)take);
+    }
+  }
+  so[2] = (uint32_t)so.size();
+  so.insert(so.end(), hs.words.begin(), hs.words.end());
+  while (so.size() % 4) so.push_back(0u);
+  st.slices += nsl;
+  st.heavy_rows += nh;
+}
+
 }  // namespace
 
 BvdLayout build_bvd(const BvDecoded& dec, const BvParams& bp, const BvdOptions& opt) {
@@ -57,8 +245,8 @@ BvdLayout build_bvd(const BvDecoded& dec, const BvParams& bp, const BvdOptions& 
   BvdLayout L;
   BvdDims& D = L.dims;
   const uint32_t B = opt.block_rows, W = opt.window;
-  if (B == 0 || (B & (B - 1)) || B % bp.segment_rows || B > 4096)
-    throw std::invalid_argument("block_rows must be a power of two <= 4096 and a multiple of the BV segment");
+  if (B == 0 || (B & (B - 1)) || B % bp.segment_rows || B > 1024)
+    throw std::invalid_argument("block_rows must be a power of two <= 1024 and a multiple of the BV segment");
   if (W % 16 || W == 0) throw std::invalid_argument("window must be a positive multiple of 16");
   if (bp.window > 7) throw std::invalid_argument("the device layout supports BV windows w <= 7");
   D.n = g.n;
@@ -67,14 +255,19 @@ BvdLayout build_bvd(const BvDecoded& dec, const BvParams& bp, const BvdOptions& 
   D.min_interval = bp.min_interval;
   D.nblocks = (uint32_t)(((uint64_t)g.n + B - 1) / B);
   D.max_depth = 0;
+  D.max_extras = 0;
   const uint32_t nb = D.nblocks;
   std::vector<BitWriter> bstream(nb);
   L.blocks.resize(nb);
   std::vector<uint64_t> bbits(nb, 0), badds(nb, 0), bcodes(nb, 0), bgath(nb, 0), bin(nb, 0);
   std::vector<uint32_t> bdepth(nb, 0);
+  std::vector<std::vector<uint32_t>> sstream(nb);
+  std::vector<BvsStats> bst(nb);
+  std::vector<uint32_t> bmaxex(nb, 0);
   parallel_for(nb, [&](uint64_t b0, uint64_t b1) {
     std::vector<RowParts> rps(B);
     std::vector<uint32_t> plus, cols, depth(B), hdr(B), escs;
+    std::vector<RowMeta> meta(B);
     BitWriter body;
     for (uint64_t b = b0; b < b1; ++b) {
       const uint32_t r0 = (uint32_t)(b * B), r1 = (uint32_t)std::min<uint64_t>(g.n, (b + 1) * B);
@@ -148,6 +341,7 @@ BvdLayout build_bvd(const BvDecoded& dec, const BvParams& bp, const BvdOptions& 
         if (any)
           while (!(dmin >= -(int64_t)code_bias(wp) && dmax < (int64_t)(wp ? code_bias(wp) : 1))) ++wp;
         const int64_t bias = code_bias(wp);
+        meta[k] = RowMeta{r, nm, ns, ni, wp, wl, far, body.nbits, 0};
         const bool esc = nm >= kHdrMinusEsc || ns >= kHdrResEsc || ni >= kHdrIntEsc;
         if (esc) {
           // all three counts escape together; the real counts go to the escape table
@@ -165,6 +359,7 @@ BvdLayout build_bvd(const BvDecoded& dec, const BvParams& bp, const BvdOptions& 
           body.put((uint64_t)((int64_t)iv.first - (int64_t)i + bias), (int)wp);
           body.put(iv.second - bp.min_interval, (int)wl);
         }
+        meta[k].nbits = body.nbits - meta[k].bit0;
         codes += nm + ns + 2ull * ni;
         adds += (r ? 1 : 0) + nm + ns + 2ull * ni;
       }
@@ -179,6 +374,7 @@ BvdLayout build_bvd(const BvDecoded& dec, const BvParams& bp, const BvdOptions& 
       L.blocks[b].wlo = (uint32_t)lo;
       L.blocks[b].nwords = (uint32_t)(out.nbits / 32);
       L.blocks[b].nesc = (uint32_t)(escs.size() / 4);
+      emit_bvs(rps.data(), meta.data(), body, r0, nr, lo, W, bp.min_interval, sstream[b], bst[b], bmaxex[b]);
     }
   });
   uint64_t off = 0, maxw = 0, g_all = 0, g_in = 0;
@@ -208,6 +404,34 @@ BvdLayout build_bvd(const BvDecoded& dec, const BvParams& bp, const BvdOptions& 
         std::memcpy(L.words.data() + L.blocks[b].word_offset, bstream[b].words.data(), (size_t)L.blocks[b].nwords * 4);
   });
   L.stats.stream_bytes = off * 4;
+  // BV-S
+  L.sblocks = L.blocks;
+  uint64_t soff = 0;
+  std::vector<uint32_t> ssz(nb);
+  for (uint32_t b = 0; b < nb; ++b) {
+    L.sblocks[b].word_offset = soff;
+    L.sblocks[b].nwords = (uint32_t)sstream[b].size();
+    L.sblocks[b].nesc = 0;
+    soff += sstream[b].size();
+    ssz[b] = (uint32_t)sstream[b].size();
+    L.sstats.max_block_words = std::max(L.sstats.max_block_words, ssz[b]);
+    L.sstats.slices += bst[b].slices;
+    L.sstats.heavy_rows += bst[b].heavy_rows;
+    L.sstats.lane_words += bst[b].lane_words;
+    L.sstats.lane_words_used += bst[b].lane_words_used;
+    L.sstats.lane_iters += bst[b].lane_iters;
+    L.sstats.lane_iters_used += bst[b].lane_iters_used;
+    D.max_extras = std::max(D.max_extras, bmaxex[b]);
+  }
+  std::sort(ssz.begin(), ssz.end());
+  L.sstats.p995_block_words = nb ? ssz[std::min<uint64_t>(nb - 1, (uint64_t)(nb * 0.995))] : 0;
+  L.swords.assign(soff + 64, 0);  // guard words: lanes read one word past their slice
+  parallel_for(nb, [&](uint64_t b0, uint64_t b1) {
+    for (uint64_t b = b0; b < b1; ++b)
+      if (!sstream[b].empty())
+        std::memcpy(L.swords.data() + L.sblocks[b].word_offset, sstream[b].data(), sstream[b].size() * 4);
+  });
+  L.sstats.stream_bytes = soff * 4;
   L.stats.block_table_bytes = (uint64_t)nb * sizeof(BvdBlockInfo);
   return L;
 }

@@ -20,10 +20,23 @@ struct BvdStats {
   double window_coverage = 1.0;   // fraction of gathered columns inside the x-window
 };
 
+struct BvsStats {
+  uint64_t stream_bytes = 0;
+  uint32_t max_block_words = 0;
+  uint32_t p995_block_words = 0;
+  uint64_t slices = 0, heavy_rows = 0;
+  uint64_t lane_words = 0, lane_words_used = 0;  // slice body words incl. / excl. padding
+  uint64_t lane_iters = 0, lane_iters_used = 0;  // slice decode iterations x 32 / useful lane iterations
+};
+
 struct BvdLayout {
   BvdDims dims{};
   std::vector<uint32_t> words;
   std::vector<BvdBlockInfo> blocks;
+  // BV-S (sliced) stream of the same blocks; same block table fields, same wlo
+  std::vector<uint32_t> swords;
+  std::vector<BvdBlockInfo> sblocks;
+  BvsStats sstats;
   uint64_t adds_per_product = 0;
   BvdStats stats;
 };

@@ -63,6 +63,76 @@ __host__ __device__ constexpr uint32_t make_hdr(uint32_t r, uint32_t nm, uint32_
   return (r << 29) | (nm << 24) | (ns << 18) | (ni << 14) | (wp << 9) | (wl << 4) | ((far ? 1u : 0u) << 3);
 }
 
+// ---------------------------------------------------------------------------
+// BV-S: the sliced variant used by the gather / PageRank kernels.  The same
+// differential rows as BV-D (minus entries, residuals, intervals against the
+// BV reference), re-cut by the transcoder into the kernel's work schedule:
+//   * every light row is split into units of <= kBvsUnitPts point codes
+//     (minus first, then residuals) and <= kBvsUnitInts intervals;
+//   * per block, units are sorted by (code class, far, #intervals, #points)
+//     and dealt into 32-lane slices, so a warp decodes 32 units of near-equal
+//     work (lane utilisation ~85-95% instead of ~60% for whole rows);
+//   * codes are byte aligned and relative to the block's x-window start wlo
+//     (so a unit decodes without its row index): class 16 stores point codes
+//     as 16-bit (col - wlo + 2^15), two per word (first code in the high
+//     half), and an interval as one word (left - wlo + 2^15) << 16 |
+//     (len - Lmin); class 32
+//     stores absolute columns, one word per point, two per interval
+//     (left, len - Lmin).  A slice's lane streams are interleaved: word q of
+//     lane l at body + 32 q + l (one conflict-free shared load per word);
+//   * unit 0 of a row is its primary (writes delta_i and r_i); further units
+//     write partial sums to extra slots, folded into delta_i after decode by
+//     the fold table.  Rows with more than kBvsHeavyCodes codes are decoded
+//     by a whole warp from a row-major, bit-packed heavy stream (BV-D codes).
+// Block stream (u32 words):
+//   [0] nslices | nheavy << 16   [1] heavy table offset   [2] heavy stream offset
+//   [3] nfold | nextra << 16     [4, 4 + nslices) slice record offsets
+//   [4 + nslices, + nfold) fold table: k | first extra slot << 10 | count << 21
+//   slice record: [meta][header x 32][body]
+//     meta: max #points | max #intervals << 5 | class32 << 8 | far << 9
+//     header: valid << 31 | primary << 30 | (k or extra slot) << 20 | r << 17 |
+//             #minus << 12 | #points << 7 | #intervals << 4
+//   heavy table: kBvsHeavyEntry words per heavy row: BV-D-style a-word
+//     (make_sa), #minus, #residual, #interval, bit offset in the heavy stream, 0
+//   heavy stream: the heavy rows' BV-D bodies, bit-packed, MSB first
+constexpr uint32_t kBvsUnitPts = 16;
+constexpr uint32_t kBvsUnitInts = 2;
+constexpr uint32_t kBvsHeavyCodes = 256;
+constexpr uint32_t kBvsMaxExtras = 384;
+constexpr uint32_t kBvsHeavyEntry = 6;
+constexpr uint32_t kBvsHead = 4;
+constexpr uint32_t kBvsBias16 = 32768;
+__host__ __device__ constexpr uint32_t make_sa(uint32_t k, uint32_t r, uint32_t wp, uint32_t wl, bool far) {
+  return k | (r << 12) | (wp << 15) | (wl << 20) | ((far ? 1u : 0u) << 25) | (1u << 31);
+}
+__host__ __device__ constexpr uint32_t sa_k(uint32_t a) { return a & 4095u; }
+__host__ __device__ constexpr uint32_t sa_r(uint32_t a) { return (a >> 12) & 7u; }
+__host__ __device__ constexpr uint32_t sa_wp(uint32_t a) { return (a >> 15) & 31u; }
+__host__ __device__ constexpr uint32_t sa_wl(uint32_t a) { return (a >> 20) & 31u; }
+__host__ __device__ constexpr bool sa_far(uint32_t a) { return (a >> 25) & 1u; }
+
+__host__ __device__ constexpr uint32_t make_uh(bool primary, uint32_t kslot, uint32_t r, uint32_t nm, uint32_t np,
+                                               uint32_t ni) {
+  return (1u << 31) | ((primary ? 1u : 0u) << 30) | (kslot << 20) | (r << 17) | (nm << 12) | (np << 7) | (ni << 4);
+}
+__host__ __device__ constexpr bool uh_valid(uint32_t h) { return h >> 31; }
+__host__ __device__ constexpr bool uh_primary(uint32_t h) { return (h >> 30) & 1u; }
+__host__ __device__ constexpr uint32_t uh_kslot(uint32_t h) { return (h >> 20) & 1023u; }
+__host__ __device__ constexpr uint32_t uh_r(uint32_t h) { return (h >> 17) & 7u; }
+__host__ __device__ constexpr uint32_t uh_nm(uint32_t h) { return (h >> 12) & 31u; }
+__host__ __device__ constexpr uint32_t uh_np(uint32_t h) { return (h >> 7) & 31u; }
+__host__ __device__ constexpr uint32_t uh_ni(uint32_t h) { return (h >> 4) & 7u; }
+__host__ __device__ constexpr uint32_t make_smeta(uint32_t max_np, uint32_t max_ni, bool c32, bool far) {
+  return max_np | (max_ni << 5) | ((c32 ? 1u : 0u) << 8) | ((far ? 1u : 0u) << 9);
+}
+__host__ __device__ constexpr uint32_t smeta_np(uint32_t m) { return m & 31u; }
+__host__ __device__ constexpr uint32_t smeta_ni(uint32_t m) { return (m >> 5) & 7u; }
+__host__ __device__ constexpr bool smeta_c32(uint32_t m) { return (m >> 8) & 1u; }
+__host__ __device__ constexpr bool smeta_far(uint32_t m) { return (m >> 9) & 1u; }
+__host__ __device__ constexpr uint32_t make_fold(uint32_t k, uint32_t first, uint32_t count) {
+  return k | (first << 10) | (count << 21);
+}
+
 struct BvdBlockInfo {
   uint64_t word_offset;  // first u32 word of this block's stream (16-byte aligned)
   uint32_t nwords;       // words in this block's stream (multiple of 4)
@@ -79,7 +149,7 @@ struct BvdDims {
   uint32_t nblocks;
   uint32_t max_block_words;
   uint32_t max_depth;    // longest reference chain (drives the level phases)
-  uint32_t pad;
+  uint32_t max_extras;   // BV-S: most extra-unit slots in one block
 };
 
 }  // namespace cmvg

@@ -9,7 +9,7 @@
 #include <string>
 
 #include "../../include/cmvg.h"
-#include "cuda/bvd_gather.cuh"
+#include "cuda/bvs_gather.cuh"
 #include "host/bvd_layout.hpp"
 #include "host/host.hpp"
 
@@ -138,8 +138,14 @@ struct cmvg_graph {
   uint64_t bv_bits = 0, adds = 0;
   BvdStats stats;
   uint32_t threads = 128;  // threads per CTA
-  // BV-D layout (this shard)
+  // BV-D layout (this shard): scatter, matmat
   DevBuf words, blocks;
+  // BV-S layout (this shard): gather, PageRank
+  DevBuf swords, sblocks;
+  uint32_t scap_words = 0;  // BV-S staging cap
+  uint64_t s_stream_bytes = 0;
+  BvsStats sstats;
+  bool gather_bvd = false;  // dev switch: gather on BV-D (CMVG_GATHER_LAYOUT=bvd)
   // canonical BV stream (whole graph) for decode_csr
   DevBuf bv_words, bv_seg;
   uint64_t nseg = 0;
@@ -151,7 +157,7 @@ struct cmvg_graph {
   // scratch (scatter / pagerank)
   DevBuf scratch;
   uint64_t device_bytes() const {
-    return words.bytes + blocks.bytes + bv_words.bytes + bv_seg.bytes + refd.bytes;
+    return words.bytes + blocks.bytes + swords.bytes + sblocks.bytes + bv_words.bytes + bv_seg.bytes + refd.bytes;
   }
   BvdDev dev() const {
     BvdDev d{};
@@ -163,10 +169,24 @@ struct cmvg_graph {
     d.stream_cap_words = stream_cap_words;
     return d;
   }
+  BvdDev sdev() const {
+    BvdDev d = dev();
+    d.words = swords.as<uint32_t>();
+    d.blocks = sblocks.as<BvdBlockInfo>();
+    d.stream_cap_words = scap_words;
+    return d;
+  }
 };
 
 
 namespace cmvg {
+// BV-S staging cap: the p99.5 block, bounded so three CTAs fit per SM
+inline uint32_t bvs_auto_cap(const BvdDims& d, uint32_t p995_words) {
+  const uint32_t budget = (228u * 1024u - 3u * 1024u) / 3u;
+  const uint32_t other = bvs_smem_layout(d, 0, 8).total;
+  const uint32_t cmax = other < budget ? ((budget - other) / 4u) & ~255u : 1024u;
+  return std::min<uint32_t>(cmax, std::max<uint32_t>(1024, (p995_words + 255) & ~255u));
+}
 // kernel entry points implemented in the other translation units
 template <typename T>
 void launch_scatter(cmvg_graph* g, const T* x, T* y, cudaStream_t st);
