@@ -83,3 +83,114 @@ def decode_layout(words, blocks, n, B, lmin, W=None):
             rows_out[i] = sorted(row)
             refs_out[i] = r
     return refs_out, rows_out
+
+
+# ---------------------------------------------------------------------------
+# BV-S (sliced layout; host/layout.hpp, cuda/bvs_gather.cuh)
+UNIT_PTS, UNIT_INTS, BIAS16 = 16, 2, 32768
+
+
+def decode_sliced(words, blocks, n, B, lmin, W):
+    """Decode the BV-S layout as the gather kernel reads it: heavy rows from the
+    row-major bit stream, units from the lane-interleaved slice bodies, extra
+    units folded into their rows.  Returns (refs, rows) like decode_layout and
+    checks the structural invariants (every row exactly one primary unit,
+    slice metadata = max over lanes, class/far flags consistent)."""
+    rows_out = [None] * n
+    refs_out = [0] * n
+    for b in range(len(blocks)):
+        woff = int(blocks[b, 0]) | (int(blocks[b, 1]) << 32)
+        nw = int(blocks[b, 2])
+        wlo = int(blocks[b, 3])
+        s = [int(v) for v in words[woff:woff + nw + 64]]
+        r0 = b * B
+        nr = min(B, n - r0)
+        nsl, nh = s[0] & 0xFFFF, s[0] >> 16
+        htab, hstr = s[1], s[2]
+        nf, nex = s[3] & 0xFFFF, s[3] >> 16
+        parts = {}   # k -> dict(minus, res, ints, r)
+        extras = {}  # slot -> (minus, res, ints)
+
+        def inwin(c):
+            return wlo <= c < wlo + W
+        for q in range(nh):
+            e = htab + 6 * q
+            sa, nm, ns, ni, boff = s[e], s[e + 1], s[e + 2], s[e + 3], s[e + 4]
+            k, r, wp, wl = sa & 4095, (sa >> 12) & 7, (sa >> 15) & 31, (sa >> 20) & 31
+            off = hstr * 32 + boff
+            ib = r0 + k - bias(wp)
+            pts = []
+            for t in range(nm + ns):
+                pts.append(ib + extract(s, off, wp))
+                off += wp
+            ints = []
+            for t in range(ni):
+                ints.append((ib + extract(s, off, wp), extract(s, off + wp, wl) + lmin))
+                off += wp + wl
+            assert k not in parts
+            parts[k] = dict(minus=pts[:nm], res=pts[nm:], ints=ints, r=r)
+        for sl in range(nsl):
+            rec = s[4 + sl]
+            meta = s[rec]
+            mnp, mni, c32, far = meta & 31, (meta >> 5) & 7, (meta >> 8) & 1, (meta >> 9) & 1
+            seen_np, seen_ni = 0, 0
+            for lane in range(32):
+                h = s[rec + 1 + lane]
+                if not h >> 31:
+                    continue
+                prim, ks, r = (h >> 30) & 1, (h >> 20) & 1023, (h >> 17) & 7
+                nm, npt, ni = (h >> 12) & 31, (h >> 7) & 31, (h >> 4) & 7
+                assert npt <= UNIT_PTS and ni <= UNIT_INTS and nm <= npt
+                seen_np, seen_ni = max(seen_np, npt), max(seen_ni, ni)
+                body = rec + 33 + lane
+                lw = lambda q: s[body + 32 * q]  # noqa: E731
+                pts, ints = [], []
+                if not c32:
+                    for t in range(npt):
+                        w = lw(t >> 1)
+                        pts.append(wlo - BIAS16 + ((w & 0xFFFF) if t & 1 else (w >> 16)))
+                    q0 = (npt + 1) >> 1
+                    for u in range(ni):
+                        w = lw(q0 + u)
+                        ints.append((wlo - BIAS16 + (w >> 16), (w & 0xFFFF) + lmin))
+                else:
+                    pts = [lw(t) for t in range(npt)]
+                    for u in range(ni):
+                        ints.append((lw(npt + 2 * u), lw(npt + 2 * u + 1) + lmin))
+                ufar = any(not inwin(c) for c in pts) or any(
+                    not (inwin(a) and inwin(a + ln - 1)) for a, ln in ints)
+                assert bool(ufar) == bool(far), (b, sl, lane)
+                unit = (pts[:nm], pts[nm:], ints)
+                if prim:
+                    assert ks not in parts
+                    parts[ks] = dict(minus=list(unit[0]), res=list(unit[1]), ints=list(unit[2]), r=r)
+                else:
+                    assert ks not in extras
+                    extras[ks] = unit
+            assert (seen_np, seen_ni) == (mnp, mni), (b, sl)
+        assert len(extras) == nex
+        for f in range(nf):
+            e = s[4 + nsl + f]
+            k, first, cnt = e & 1023, (e >> 10) & 2047, e >> 21
+            for c in range(first, first + cnt):
+                mi, re, it = extras.pop(c)
+                parts[k]["minus"] += mi
+                parts[k]["res"] += re
+                parts[k]["ints"] += it
+        assert not extras
+        assert sorted(parts) == list(range(nr))
+        for k in range(nr):
+            p = parts[k]
+            i = r0 + k
+            plus = set(p["res"])
+            for left, ln in p["ints"]:
+                plus.update(range(left, left + ln))
+            if p["r"]:
+                assert k >= p["r"]
+                row = (set(rows_out[i - p["r"]]) - set(p["minus"])) | plus
+            else:
+                assert not p["minus"]
+                row = plus
+            rows_out[i] = sorted(row)
+            refs_out[i] = p["r"]
+    return refs_out, rows_out

@@ -10,7 +10,7 @@ import pytest
 
 import paper_1708_07271_b200 as P
 from tests.helpers import CONFIGS, bv_params, csr_from_rows, make_graph
-from tests.layout_ref import decode_layout
+from tests.layout_ref import decode_layout, decode_sliced
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -96,13 +96,24 @@ def test_bv_params_validation():
         P.BvStream.encode(g, P.BvParams(min_interval=1))
 
 
-@pytest.mark.parametrize("cfg,n,block_rows", [(1, 5000, 1024), (2, 9000, 2048), (4, 3000, 1024)])
-def test_device_layout_decodes_to_adjacency(cfg, n, block_rows):
+@pytest.mark.parametrize("cfg,n,window", [(1, 5000, 1536), (2, 9000, 2048), (4, 3000, 1536)])
+def test_device_layout_decodes_to_adjacency(cfg, n, window):
     g = make_graph(cfg, n=n)
     s = P.BvStream.encode(g, bv_params(cfg))
-    words, blocks = s.layout_export(P.CreateOptions(block_rows=block_rows, window=1536))
-    refs, rows = decode_layout(words, blocks, g.n, block_rows, 4, W=1536)
+    words, blocks = s.layout_export(P.CreateOptions(block_rows=1024, window=window))
+    refs, rows = decode_layout(words, blocks, g.n, 1024, 4, W=window)
     assert rows == rows_of(g)
+
+
+@pytest.mark.parametrize("cfg,n,window", [(1, 5000, 1536), (2, 9000, 2048), (3, 6000, 1536), (4, 3000, 1536)])
+def test_sliced_layout_decodes_to_adjacency(cfg, n, window):
+    g = make_graph(cfg, n=n)
+    s = P.BvStream.encode(g, bv_params(cfg))
+    words, blocks = s.layout_export(P.CreateOptions(block_rows=1024, window=window), sliced=True)
+    refs, rows = decode_sliced(words, blocks, g.n, 1024, 4, W=window)
+    assert rows == rows_of(g)
+    info = s.layout_info(P.CreateOptions(block_rows=1024, window=window))
+    assert info["bvs_lane_iters_used"] <= info["bvs_lane_iters"]
 
 
 def test_device_layout_escapes_and_edge_rows():
@@ -119,6 +130,9 @@ def test_device_layout_escapes_and_edge_rows():
     words, blocks = s.layout_export(P.CreateOptions(block_rows=1024, window=512))
     _, got = decode_layout(words, blocks, n, 1024, 4, W=512)
     assert got == rows
+    words, blocks = s.layout_export(P.CreateOptions(block_rows=1024, window=512), sliced=True)
+    _, got = decode_sliced(words, blocks, n, 1024, 4, W=512)
+    assert got == rows
 
 
 def test_layout_info_sizes():
@@ -130,3 +144,19 @@ def test_layout_info_sizes():
     assert 1.0 <= li["bvd_row_bits"] / S < 2.0
     assert li["window_coverage"] > 0.99
     assert li["max_depth"] <= 3
+
+
+def test_sliced_layout_extra_budget():
+    # 200 rows of ~120 scattered columns: ~8 units each -> far more extra
+    # slots than kBvsMaxExtras, so the transcoder moves rows to the warp path
+    rng = np.random.default_rng(5)
+    n = 2048
+    rows = [sorted(set(rng.integers(0, n, 120).tolist())) if k % 5 == 0 else sorted(set(rng.integers(0, n, 3).tolist()))
+            for k in range(n)]
+    g = csr_from_rows(rows)
+    s = P.BvStream.encode(g, P.BvParams())
+    words, blocks = s.layout_export(P.CreateOptions(block_rows=1024, window=1536), sliced=True)
+    _, got = decode_sliced(words, blocks, n, 1024, 4, W=1536)
+    assert got == rows
+    info = s.layout_info()
+    assert info["bvs_heavy_rows"] > 0
