@@ -259,7 +259,6 @@ int cmvg_create(const cmvg_bvstream* s, const cmvg_create_opts* opts_in, cmvg_gr
       g->sblocks.upload(sbl.data(), sbl.size());
       g->s_stream_bytes = (s1 - s0) * 4;
       g->sstats = L.sstats;
-      g->scap_words = o.stream_cap_words ? o.stream_cap_words : bvs_auto_cap(L.dims, L.sstats.p995_block_words);
       const char* gl = getenv("CMVG_GATHER_LAYOUT");
       g->gather_bvd = gl && std::string(gl) == "bvd";
     }
@@ -311,8 +310,7 @@ int cmvg_layout_info(const cmvg_bvstream* s, const cmvg_create_opts* opts_in, cm
                               ? opt.stream_cap_words
                               : std::min<uint32_t>(12288, std::max<uint32_t>(1024, (L.stats.p995_block_words + 255) & ~255u));
     o->window_coverage = L.stats.window_coverage;
-    fill_bvs_info(o, L.sstats, opt.stream_cap_words ? opt.stream_cap_words
-                                                   : bvs_auto_cap(L.dims, L.sstats.p995_block_words));
+    fill_bvs_info(o, L.sstats, 0);
   });
 }
 
@@ -388,7 +386,7 @@ int cmvg_graph_info_get(const cmvg_graph* g, cmvg_graph_info* o) {
     o->max_block_words = g->dims.max_block_words;
     o->stream_cap_words = g->stream_cap_words;
     o->window_coverage = g->stats.window_coverage;
-    fill_bvs_info(o, g->sstats, g->scap_words);
+    fill_bvs_info(o, g->sstats, 0);
     o->bvs_stream_bytes = g->s_stream_bytes;
   });
 }
@@ -405,7 +403,7 @@ namespace {
 template <typename XT, typename YT>
 void launch_gather(cmvg_graph* g, const XT* x, YT* y, cudaStream_t st) {
   if (!g->gather_bvd) {
-    const BvsSmem L = bvs_smem_layout(g->dims, g->scap_words, sizeof(XT));
+    const BvsSmem L = bvs_smem_layout(g->dims, sizeof(XT));
     auto kern = bvs_gather_kernel<XT, YT>;
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
     kern<<<g->nblocks, g->threads, L.total, st>>>(g->sdev(), x, y, PrArgs{});

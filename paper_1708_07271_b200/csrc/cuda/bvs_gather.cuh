@@ -4,19 +4,22 @@
 // (PR = true) the product + update of one PageRank iteration
 // (pagerank.hpp:83-102).
 //
-// One CTA per block of B rows (reference chains never leave a block):
-//   1. thread 0 issues a TMA bulk copy of the block's sliced stream into
-//      shared memory (mbarrier completion) while all threads stage the
-//      x-window x[wlo, wlo + W) and its two-level double-double prefix;
+// One CTA per block of B rows (reference chains never leave a block), four
+// CTAs per SM (no stream staging: ~52 KB of shared memory, 64 registers):
+//   1. the block's sliced stream is prefetched into L2 (TMA bulk prefetch)
+//      while all threads stage the x-window x[wlo, wlo + W) and its two-level
+//      double-double prefix in shared memory;
 //   2. warps claim work dynamically: first heavy rows (one warp per row,
-//      lanes stride over its fixed-width codes), then 32-row slices (one row
-//      per lane; the transcoder already sorted rows into slices of near-equal
-//      work and interleaved their code streams by lane, so there is no row
-//      setup and every code read is a conflict-free shared load).  Points
+//      lanes stride over its fixed-width codes), then 32-unit slices (one
+//      unit of <= 16 points / <= 2 intervals per lane; the transcoder already
+//      dealt units into slices of near-equal work and interleaved their words
+//      by lane, so a lane loads its <= 10 words with coalesced 128-B warp
+//      loads straight into registers -- no row setup, no staging).  Points
 //      (minus -> -x[c], residual -> +x[c]) then intervals (O(1) from the
-//      prefix), delta_i accumulated with TwoSum compensation;
-//   3. one barrier, then the reference chains y_i = delta_i + y_{i-r}
-//      (ref_matvec.hpp:23-25) and the coalesced store / PageRank epilogue.
+//      prefix), delta accumulated with TwoSum compensation;
+//   3. a barrier, the fold of split rows' extra units, then the reference
+//      chains y_i = delta_i + y_{i-r} (ref_matvec.hpp:23-25) and the
+//      coalesced store / PageRank epilogue.
 #pragma once
 #include <cstdint>
 
@@ -25,15 +28,15 @@
 
 namespace cmvg {
 
-constexpr uint32_t kBvsGuardWords = 64;  // zeroed words after a staged block
+constexpr uint32_t kBvsGuardWords = 64;  // zero words after the last block (lanes never read past their unit)
 
 struct BvsSmem {
   uint32_t off_x, off_yhi, off_ylo, off_exh, off_exl, off_ptr, off_ref, off_misc, total;
 };
 
-__host__ __device__ inline BvsSmem bvs_smem_layout(const BvdDims& d, uint32_t stream_cap_words, uint32_t xsize) {
+__host__ __device__ inline BvsSmem bvs_smem_layout(const BvdDims& d, uint32_t xsize) {
   BvsSmem s;
-  uint32_t o = align16((stream_cap_words + kBvsGuardWords) * 4);
+  uint32_t o = 0;
   s.off_x = o;
   o = align16(o + xw_bytes(d.window, xsize, true));
   s.off_yhi = o;
@@ -139,45 +142,63 @@ __device__ __forceinline__ void bvs_slices(const S& src, const XW& xw, uint32_t 
     const uint32_t mnp = smeta_np(meta), mni = smeta_ni(meta);
     double acc = 0.0, comp = 0.0;
     if (!smeta_c32(meta)) {
-      const uint32_t ibase = body + ((np + 1u) >> 1) * 32u;  // this lane's first interval word
+      // the lane's words, loaded up front (coalesced across lanes): <= 8
+      // point words (two 16-bit codes each) and <= 2 interval words
+      const uint32_t npw = (np + 1u) >> 1;
+      uint32_t w[kBvsUnitPts / 2];
+#pragma unroll
+      for (uint32_t q = 0; q < kBvsUnitPts / 2; ++q) w[q] = q < npw ? src.w(body + q * 32u) : 0u;
+      const uint32_t wi0 = ni > 0 ? src.w(body + npw * 32u) : 0u;
+      const uint32_t wi1 = ni > 1 ? src.w(body + (npw + 1u) * 32u) : 0u;
       if (!smeta_far(meta)) {
         double acc2 = 0.0, comp2 = 0.0;
-#pragma unroll 2
-        for (uint32_t t = 0; t < mnp; t += 2) {
-          const uint32_t w = src.w(body + (t >> 1) * 32u);
-          const uint32_t i0 = t < np ? c16_idx(w >> 16) : Z;
-          const uint32_t i1 = t + 1u < np ? c16_idx(w & 0xffffu) : Z;
+#pragma unroll
+        for (uint32_t q = 0; q < kBvsUnitPts / 2; ++q) {
+          const uint32_t t = 2u * q;
+          if (t >= mnp) break;  // warp-uniform
+          const uint32_t i0 = t < np ? c16_idx(w[q] >> 16) : Z;
+          const uint32_t i1 = t + 1u < np ? c16_idx(w[q] & 0xffffu) : Z;
           tsum(acc, comp, signed_term(xw.at_near(i0), t, nm));
           tsum(acc2, comp2, signed_term(xw.at_near(i1), t + 1u, nm));
         }
         tsum(acc, comp, acc2);
         comp += comp2;
-        for (uint32_t u = 0; u < mni; ++u) {
-          const uint32_t w = src.w(ibase + u * 32u);
-          const bool on = u < ni;
+        if (mni > 0) {
           double lo;
-          const double hi = xw.isum_near(on ? c16_idx(w >> 16) : 0u, on ? (w & 0xffffu) + lmin : 0u, lo);
+          const double hi = xw.isum_near(ni > 0 ? c16_idx(wi0 >> 16) : 0u, ni > 0 ? (wi0 & 0xffffu) + lmin : 0u, lo);
+          tsum(acc, comp, hi);
+          comp += lo;
+        }
+        if (mni > 1) {
+          double lo;
+          const double hi = xw.isum_near(ni > 1 ? c16_idx(wi1 >> 16) : 0u, ni > 1 ? (wi1 & 0xffffu) + lmin : 0u, lo);
           tsum(acc, comp, hi);
           comp += lo;
         }
       } else {
-        for (uint32_t t = 0; t < mnp; ++t) {
-          const uint32_t w = src.w(body + (t >> 1) * 32u);
-          const uint32_t c = (t & 1u) ? (w & 0xffffu) : (w >> 16);
-          const double xv = t < np ? xw.at((int32_t)c16_idx(c) + (int32_t)xw.wlo) : 0.0;
-          tsum(acc, comp, signed_term(xv, t, nm));
+        const int32_t wlo = (int32_t)xw.wlo;
+#pragma unroll
+        for (uint32_t q = 0; q < kBvsUnitPts / 2; ++q) {
+          const uint32_t t = 2u * q;
+          if (t >= mnp) break;
+          const double x0 = t < np ? xw.at((int32_t)c16_idx(w[q] >> 16) + wlo) : 0.0;
+          const double x1 = t + 1u < np ? xw.at((int32_t)c16_idx(w[q] & 0xffffu) + wlo) : 0.0;
+          tsum(acc, comp, signed_term(x0, t, nm));
+          tsum(acc, comp, signed_term(x1, t + 1u, nm));
         }
-        for (uint32_t u = 0; u < mni; ++u) {
-          const uint32_t w = src.w(ibase + u * 32u);
+#pragma unroll
+        for (uint32_t u = 0; u < kBvsUnitInts; ++u) {
+          if (u >= mni) break;
+          const uint32_t wv = u ? wi1 : wi0;
           double hi = 0.0, lo = 0.0;
-          if (u < ni) hi = xw.isum((int32_t)c16_idx(w >> 16) + (int32_t)xw.wlo, (w & 0xffffu) + lmin, lo);
+          if (u < ni) hi = xw.isum((int32_t)c16_idx(wv >> 16) + wlo, (wv & 0xffffu) + lmin, lo);
           tsum(acc, comp, hi);
           comp += lo;
         }
       }
     } else {  // class 32: absolute columns, bounds-checked
       for (uint32_t t = 0; t < mnp; ++t) {
-        const uint32_t c = src.w(body + t * 32u);
+        const uint32_t c = t < np ? src.w(body + t * 32u) : 0u;
         const double xv = t < np ? xw.at((int32_t)c) : 0.0;
         tsum(acc, comp, signed_term(xv, t, nm));
       }
@@ -222,56 +243,46 @@ __device__ __forceinline__ void bvs_fold(const S& src, double* s_yhi, float* s_y
 }
 
 template <typename XT, typename YT, bool PR = false>
-__global__ void __launch_bounds__(256, 3) bvs_gather_kernel(BvdDev g, const XT* __restrict__ x, YT* __restrict__ y,
+__global__ void __launch_bounds__(256, 4) bvs_gather_kernel(BvdDev g, const XT* __restrict__ x, YT* __restrict__ y,
                                                              PrArgs pr) {
   extern __shared__ __align__(16) unsigned char smem[];
   const BvdDims& D = g.d;
-  const BvsSmem L = bvs_smem_layout(D, g.stream_cap_words, sizeof(XT));
+  const BvsSmem L = bvs_smem_layout(D, sizeof(XT));
   const uint32_t bl = blockIdx.x;  // index into this shard's tables
   const uint32_t b = g.block_begin + bl;
   const BvdBlockInfo bi = g.blocks[bl];
   const uint32_t r0 = b * D.block_rows;
   const uint32_t nr = min(D.block_rows, D.n - r0);
 
-  uint32_t* s_stream = reinterpret_cast<uint32_t*>(smem);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.off_misc);
   int* misc = reinterpret_cast<int*>(smem + L.off_misc + 16);
-  const bool staged = bi.nwords <= g.stream_cap_words;
+  const uint32_t* bs = g.words + bi.word_offset;  // this block's stream (global; read through L1/L2)
   if (threadIdx.x == 0) {
-    mbar_init(bar, 1);
-    const uint32_t sbytes = staged ? bi.nwords * 4u : 0u;
-    mbar_arrive_expect_tx(bar, sbytes);
-    if (sbytes) bulk_g2s(s_stream, g.words + bi.word_offset, sbytes, bar);
     misc[kBvsHeavyCtr] = 0;
     misc[kBvsSliceCtr] = 0;
   }
-  if (threadIdx.x < kBvsGuardWords) s_stream[(staged ? bi.nwords : 0u) + threadIdx.x] = 0u;
+  if (threadIdx.x == 32) bulk_prefetch_l2(bs, bi.nwords * 4u);
   XWin<XT, true> xw;
   xw.carve(smem + L.off_x, D.window);
   xw.x = x;
   xw.wlo = bi.wlo;
   XT xpre[XWin<XT, true>::kPre];
   xw.prefetch(D.n, xpre);
-  __syncthreads();       // publishes the mbarrier init and the counters
-  xw.stage(D.n, xpre);   // ends with __syncthreads
-  mbar_wait(bar, 0);
+  __syncthreads();      // publishes the counters
+  xw.stage(D.n, xpre);  // ends with __syncthreads
 
   double* s_yhi = reinterpret_cast<double*>(smem + L.off_yhi);
   float* s_ylo = reinterpret_cast<float*>(smem + L.off_ylo);
   uint8_t* s_ref = smem + L.off_ref;
   double* s_exh = reinterpret_cast<double*>(smem + L.off_exh);
   float* s_exl = reinterpret_cast<float*>(smem + L.off_exl);
-  auto decode = [&](const auto& src) {
-    bvs_heavy(src, xw, (int32_t)r0, D.min_interval, misc, s_yhi, s_ylo, s_ref);
-    bvs_slices(src, xw, D.min_interval, misc, s_yhi, s_ylo, s_ref, s_exh, s_exl);
+  const Src<false> src{bs};
+  bvs_heavy(src, xw, (int32_t)r0, D.min_interval, misc, s_yhi, s_ylo, s_ref);
+  bvs_slices(src, xw, D.min_interval, misc, s_yhi, s_ylo, s_ref, s_exh, s_exl);
+  __syncthreads();
+  if (src.w(3) & 0xffffu) {  // CTA-uniform
+    bvs_fold(src, s_yhi, s_ylo, s_exh, s_exl);
     __syncthreads();
-    if (src.w(3) & 0xffffu) {  // CTA-uniform
-      bvs_fold(src, s_yhi, s_ylo, s_exh, s_exl);
-      __syncthreads();
-    }
-  };
-  if (staged) decode(Src<true>{smem_u32(s_stream)});  // CTA-uniform
-  else decode(Src<false>{g.words + bi.word_offset});
+  }
 
   RowCtx rc{};
   rc.ref = s_ref;

@@ -142,7 +142,6 @@ struct cmvg_graph {
   DevBuf words, blocks;
   // BV-S layout (this shard): gather, PageRank
   DevBuf swords, sblocks;
-  uint32_t scap_words = 0;  // BV-S staging cap
   uint64_t s_stream_bytes = 0;
   BvsStats sstats;
   bool gather_bvd = false;  // dev switch: gather on BV-D (CMVG_GATHER_LAYOUT=bvd)
@@ -173,20 +172,13 @@ struct cmvg_graph {
     BvdDev d = dev();
     d.words = swords.as<uint32_t>();
     d.blocks = sblocks.as<BvdBlockInfo>();
-    d.stream_cap_words = scap_words;
+    d.stream_cap_words = 0;  // BV-S is read from global memory (L2-prefetched)
     return d;
   }
 };
 
 
 namespace cmvg {
-// BV-S staging cap: the p99.5 block, bounded so three CTAs fit per SM
-inline uint32_t bvs_auto_cap(const BvdDims& d, uint32_t p995_words) {
-  const uint32_t budget = (228u * 1024u - 3u * 1024u) / 3u;
-  const uint32_t other = bvs_smem_layout(d, 0, 8).total;
-  const uint32_t cmax = other < budget ? ((budget - other) / 4u) & ~255u : 1024u;
-  return std::min<uint32_t>(cmax, std::max<uint32_t>(1024, (p995_words + 255) & ~255u));
-}
 // kernel entry points implemented in the other translation units
 template <typename T>
 void launch_scatter(cmvg_graph* g, const T* x, T* y, cudaStream_t st);

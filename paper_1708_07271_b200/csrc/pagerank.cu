@@ -58,7 +58,7 @@ __global__ void pr_reduce_kernel(const double* __restrict__ partial, uint32_t nb
 }
 
 void launch_pr_step(cmvg_graph* g, const double* q, PrArgs pr, double* p_next, cudaStream_t st) {
-  const BvsSmem L = bvs_smem_layout(g->dims, g->scap_words, sizeof(double));
+  const BvsSmem L = bvs_smem_layout(g->dims, sizeof(double));
   auto kern = bvs_gather_kernel<double, double, true>;
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
   kern<<<g->nblocks, g->threads, L.total, st>>>(g->sdev(), q, p_next, pr);

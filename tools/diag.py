@@ -9,11 +9,11 @@ from oracle import pyoracle as O
 
 a = sys.argv + [None] * 8
 nlog = int(a[1] or 20); mode = a[2] or "prefix"; thr = int(a[3] or 128); W = int(a[4] or 2048)
-B = int(a[5] or 1024); dt = a[6] or "f64"
+B = int(a[5] or 1024); dt = a[6] or "f64"; cap = int(a[7] or 0)
 n = 1 << nlog
 g = P.CsrGraph.copy_model(n, 20.0, 0.7, 0.8, seed=0x170807271 + 2)
 s = P.BvStream.encode(g, P.BvParams())
-dg = P.BvGraph(s, P.CreateOptions(interval_mode=mode, lanes=thr, window=W, block_rows=B))
+dg = P.BvGraph(s, P.CreateOptions(interval_mode=mode, lanes=thr, window=W, block_rows=B, stream_cap_words=cap))
 rng = np.random.default_rng(11)
 x = (rng.integers(0, 2**64, size=n, dtype=np.uint64) >> np.uint64(11)).astype(np.float64) * 2.0**-53
 if dt == "f32":
@@ -32,7 +32,7 @@ for _ in range(8):
 info = dg.info()
 alg = s.stats()["stream_bits"] / 8 + n * x.itemsize * 2
 print(f"n=2^{nlog} m={g.m} mode={mode} thr={thr} W={W} B={B} {dt} ms={np.median(ts):.4f} "
-      f"Gedges/s={g.m / np.median(ts) / 1e6:.1f} frac={alg / (np.median(ts) * 1e-3) / 6539.2e9:.3f} cap={info['stream_cap_words']}")
+      f"Gedges/s={g.m / np.median(ts) / 1e6:.1f} frac={alg / (np.median(ts) * 1e-3) / 6539.2e9:.3f} cap={info['bvs_stream_cap_words']}")
 y = yd.double().cpu().numpy()
 want = O.matvec_csr_raw(g.n, g.row_offsets, g.columns, x.astype(np.float64), O.threads())
 nz = want != 0
