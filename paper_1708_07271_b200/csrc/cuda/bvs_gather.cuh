@@ -17,7 +17,7 @@
 //      loads straight into registers -- no row setup, no staging).  Points
 //      (minus -> -x[c], residual -> +x[c]) then intervals (O(1) from the
 //      prefix), delta accumulated with TwoSum compensation;
-//   3. a barrier, the fold of split rows' extra units, then the reference
+//   3. a barrier, then the reference
 //      chains y_i = delta_i + y_{i-r} (ref_matvec.hpp:23-25) and the
 //      coalesced store / PageRank epilogue.
 #pragma once
@@ -31,7 +31,7 @@ namespace cmvg {
 constexpr uint32_t kBvsGuardWords = 64;  // zero words after the last block (lanes never read past their unit)
 
 struct BvsSmem {
-  uint32_t off_x, off_yhi, off_ylo, off_exh, off_exl, off_ptr, off_ref, off_misc, total;
+  uint32_t off_x, off_yhi, off_ylo, off_ptr, off_ref, off_misc, total;
 };
 
 __host__ __device__ inline BvsSmem bvs_smem_layout(const BvdDims& d, uint32_t xsize) {
@@ -43,12 +43,8 @@ __host__ __device__ inline BvsSmem bvs_smem_layout(const BvdDims& d, uint32_t xs
   o = align16(o + d.block_rows * 8);
   s.off_ylo = o;
   o = align16(o + d.block_rows * 4);
-  // extra-unit partials (fold) -- reused as the chain pointers afterwards
-  const uint32_t ex = d.max_extras;
-  s.off_exh = o;
-  s.off_ptr = o;
-  s.off_exl = align16(o + ex * 8);
-  o = max(align16(s.off_exl + ex * 4), align16(o + d.block_rows * 2));
+  s.off_ptr = o;  // chain pointers (unbounded chains only)
+  o = align16(o + d.block_rows * 2);
   s.off_ref = o;
   o = align16(o + d.block_rows);
   s.off_misc = o;  // mbarrier (16) + 16 ints + scratch (64 ints)
@@ -124,10 +120,12 @@ __device__ __forceinline__ double signed_term(double x, uint32_t t, uint32_t nm)
   return __hiloint2double(__double2hiint(x) ^ (int)m, __double2loint(x));
 }
 
-// Slices: one unit (<= 16 points, <= 2 intervals of one row) per lane.
+// Slices: one unit (<= 16 points, <= 2 intervals of one row) per lane; in
+// "multi" slices a row's units occupy adjacent lanes and are combined by a
+// segmented warp reduction.
 template <class S, class XW>
 __device__ __forceinline__ void bvs_slices(const S& src, const XW& xw, uint32_t lmin, int* misc, double* s_yhi,
-                                           float* s_ylo, uint8_t* s_ref, double* s_exh, float* s_exl) {
+                                           float* s_ylo, uint8_t* s_ref) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t nsl = src.w(0) & 0xffffu;
   const uint32_t Z = xw.W;  // zero entry of the window (idle lanes read it)
@@ -210,35 +208,26 @@ __device__ __forceinline__ void bvs_slices(const S& src, const XW& xw, uint32_t 
         comp += lo;
       }
     }
-    if (uh_valid(h)) {
-      const double hi = acc + comp;
-      const float lo = (float)(comp - (hi - acc));
-      const uint32_t ks = uh_kslot(h);
-      if (uh_primary(h)) {
-        s_yhi[ks] = hi;
-        s_ylo[ks] = lo;
-        s_ref[ks] = (uint8_t)uh_r(h);
-      } else {
-        s_exh[ks] = hi;
-        s_exl[ks] = lo;
+    double hi = acc + comp, lo = comp - (hi - acc);
+    if (smeta_multi(meta)) {
+      // a row's units sit in adjacent lanes starting at its primary: segmented
+      // suffix reduction so the primary lane ends with the row's delta
+      const uint32_t heads = __ballot_sync(0xffffffffu, uh_primary(h));
+      const uint32_t above = heads & ~((2u << lane) - 1u);
+      const uint32_t end = above ? (uint32_t)__ffs(above) - 2u : 31u;
+#pragma unroll
+      for (uint32_t o = 1; o < 32; o <<= 1) {
+        const double uh = __shfl_down_sync(0xffffffffu, hi, o), ul = __shfl_down_sync(0xffffffffu, lo, o);
+        if (lane + o <= end) dd_add(hi, lo, uh, ul);
       }
     }
+    if (uh_primary(h)) {
+      const uint32_t k = uh_k(h);
+      s_yhi[k] = hi;
+      s_ylo[k] = (float)lo;
+      s_ref[k] = (uint8_t)uh_r(h);
+    }
     s = ticket_take(next);
-  }
-}
-
-// Fold extra-unit partials into their rows' deltas (after the decode barrier).
-template <class S>
-__device__ __forceinline__ void bvs_fold(const S& src, double* s_yhi, float* s_ylo, const double* s_exh,
-                                         const float* s_exl) {
-  const uint32_t nsl = src.w(0) & 0xffffu, nf = src.w(3) & 0xffffu;
-  for (uint32_t f = threadIdx.x; f < nf; f += blockDim.x) {
-    const uint32_t e = src.w(kBvsHead + nsl + f);
-    const uint32_t k = e & 1023u, first = (e >> 10) & 2047u, cnt = e >> 21;
-    double hi = s_yhi[k], lo = s_ylo[k];
-    for (uint32_t c = 0; c < cnt; ++c) dd_add(hi, lo, s_exh[first + c], s_exl[first + c]);
-    s_yhi[k] = hi;
-    s_ylo[k] = (float)lo;
   }
 }
 
@@ -273,16 +262,10 @@ __global__ void __launch_bounds__(256, 4) bvs_gather_kernel(BvdDev g, const XT* 
   double* s_yhi = reinterpret_cast<double*>(smem + L.off_yhi);
   float* s_ylo = reinterpret_cast<float*>(smem + L.off_ylo);
   uint8_t* s_ref = smem + L.off_ref;
-  double* s_exh = reinterpret_cast<double*>(smem + L.off_exh);
-  float* s_exl = reinterpret_cast<float*>(smem + L.off_exl);
   const Src<false> src{bs};
   bvs_heavy(src, xw, (int32_t)r0, D.min_interval, misc, s_yhi, s_ylo, s_ref);
-  bvs_slices(src, xw, D.min_interval, misc, s_yhi, s_ylo, s_ref, s_exh, s_exl);
+  bvs_slices(src, xw, D.min_interval, misc, s_yhi, s_ylo, s_ref);
   __syncthreads();
-  if (src.w(3) & 0xffffu) {  // CTA-uniform
-    bvs_fold(src, s_yhi, s_ylo, s_exh, s_exl);
-    __syncthreads();
-  }
 
   RowCtx rc{};
   rc.ref = s_ref;

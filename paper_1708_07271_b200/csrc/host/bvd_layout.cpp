@@ -71,81 +71,61 @@ inline uint32_t bits32(const std::vector<uint32_t>& w, uint64_t pos, uint64_t en
 
 // BV-S block stream from the block's rows (layout.hpp).
 struct Unit {
-  uint32_t k, j, kslot, r, nm, np, ni;
-  bool primary, c32, far;
+  uint32_t k, r, nm, np, ni;
+  bool primary;
   std::vector<uint32_t> words;
 };
-
-void emit_bvs(const RowParts* rps, const RowMeta* meta, const BitWriter& body, uint32_t r0, uint32_t nr, uint64_t wlo,
-              uint32_t W, uint32_t lmin, std::vector<uint32_t>& so, BvsStats& st, uint32_t& max_extras) {
-  auto nunits = [&](uint32_t k) {
-    const uint32_t np = meta[k].nm + meta[k].ns, ni = meta[k].ni;
-    return std::max<uint32_t>(1, std::max((np + kBvsUnitPts - 1) / kBvsUnitPts, (ni + kBvsUnitInts - 1) / kBvsUnitInts));
-  };
-  std::vector<char> heavy(nr, 0);
-  uint64_t extras = 0;
-  for (uint32_t k = 0; k < nr; ++k) {
-    const RowMeta& m = meta[k];
-    if (m.nm + m.ns + 2 * m.ni > kBvsHeavyCodes) heavy[k] = 1;
-    else extras += nunits(k) - 1;
-  }
-  if (extras > kBvsMaxExtras) {  // move the most-split rows to the warp path
-    std::vector<uint32_t> byu;
-    for (uint32_t k = 0; k < nr; ++k)
-      if (!heavy[k] && nunits(k) > 1) byu.push_back(k);
-    std::stable_sort(byu.begin(), byu.end(), [&](uint32_t a, uint32_t b) { return nunits(a) > nunits(b); });
-    for (uint32_t k : byu) {
-      if (extras <= kBvsMaxExtras) break;
-      heavy[k] = 1;
-      extras -= nunits(k) - 1;
-    }
-  }
-  auto inwin = [&](uint64_t c) { return c >= wlo && c < wlo + W; };
+struct URow {  // a row's units (adjacent lanes when there is more than one)
+  uint32_t k;
+  bool c32, far;
   std::vector<Unit> units;
-  std::vector<uint32_t> fold, hrows;
-  uint32_t slot = 0;
-  std::vector<uint32_t> pts;
+};
+
+void emit_bvs(const RowParts* rps, const RowMeta* meta, const BitWriter& body, uint32_t nr, uint64_t wlo, uint32_t W,
+              uint32_t lmin, std::vector<uint32_t>& so, BvsStats& st) {
+  auto inwin = [&](uint64_t c) { return c >= wlo && c < wlo + W; };
+  auto off_ok = [&](uint32_t c) {
+    const int64_t d = (int64_t)c - (int64_t)wlo;
+    return d >= -(int64_t)kBvsBias16 && d < (int64_t)kBvsBias16;
+  };
+  auto code16 = [&](uint32_t c) { return (uint32_t)((int64_t)c - (int64_t)wlo + kBvsBias16); };
+  std::vector<URow> single, multi;
+  std::vector<uint32_t> hrows, pts;
   for (uint32_t k = 0; k < nr; ++k) {
-    if (heavy[k]) {
+    const RowParts& rp = rps[k];
+    const uint32_t nm = (uint32_t)rp.minus.size(), np = nm + (uint32_t)rp.res.size(), ni = (uint32_t)rp.ints.size();
+    const uint32_t nu = std::max<uint32_t>(
+        1, std::max((np + kBvsUnitPts - 1) / kBvsUnitPts, (ni + kBvsUnitInts - 1) / kBvsUnitInts));
+    if (nu > kBvsMaxUnits) {
       hrows.push_back(k);
       continue;
     }
-    const RowParts& rp = rps[k];
     pts.assign(rp.minus.begin(), rp.minus.end());
     pts.insert(pts.end(), rp.res.begin(), rp.res.end());
-    const uint32_t nm = (uint32_t)rp.minus.size(), np = (uint32_t)pts.size(), ni = (uint32_t)rp.ints.size();
-    const uint32_t nu = nunits(k);
-    if (nu > 1) fold.push_back(make_fold(k, slot, nu - 1));
+    URow row;
+    row.k = k;
+    row.c32 = false;
+    row.far = false;
+    for (uint32_t c : pts) {
+      row.c32 |= !off_ok(c);
+      row.far |= !inwin(c);
+    }
+    for (const auto& iv : rp.ints) {
+      row.c32 |= !off_ok(iv.first) || (iv.second - lmin) >= 65536u;
+      row.far |= !inwin(iv.first) || !inwin((uint64_t)iv.first + iv.second - 1);
+    }
     for (uint32_t j = 0; j < nu; ++j) {
       Unit u;
       u.k = k;
-      u.j = j;
       u.primary = j == 0;
-      u.kslot = j == 0 ? k : slot++;
       u.r = meta[k].r;
-      const uint32_t p0 = std::min(np, j * kBvsUnitPts), p1 = std::min(np, p0 + kBvsUnitPts);
-      const uint32_t q0 = std::min(ni, j * kBvsUnitInts), q1 = std::min(ni, q0 + kBvsUnitInts);
+      // balanced split: unit j takes points [j np / nu, (j+1) np / nu), same for intervals
+      const uint32_t p0 = (uint32_t)((uint64_t)j * np / nu), p1 = (uint32_t)((uint64_t)(j + 1) * np / nu);
+      const uint32_t q0 = (uint32_t)((uint64_t)j * ni / nu), q1 = (uint32_t)((uint64_t)(j + 1) * ni / nu);
       u.np = p1 - p0;
       u.ni = q1 - q0;
       u.nm = nm > p0 ? std::min(nm, p1) - p0 : 0;
-      bool fits16 = true, far = false;
-      auto off_ok = [&](uint32_t c) {
-        const int64_t d = (int64_t)c - (int64_t)wlo;
-        return d >= -(int64_t)kBvsBias16 && d < (int64_t)kBvsBias16;
-      };
-      for (uint32_t t = p0; t < p1; ++t) {
-        fits16 &= off_ok(pts[t]);
-        far |= !inwin(pts[t]);
-      }
-      for (uint32_t t = q0; t < q1; ++t) {
-        const auto& iv = rp.ints[t];
-        fits16 &= off_ok(iv.first) && (iv.second - lmin) < 65536u;
-        far |= !inwin(iv.first) || !inwin((uint64_t)iv.first + iv.second - 1);
-      }
-      u.c32 = !fits16;
-      u.far = far;
-      auto code16 = [&](uint32_t c) { return (uint32_t)((int64_t)c - (int64_t)wlo + kBvsBias16); };
-      if (!u.c32) {
+      if (!row.c32) {
         for (uint32_t t = p0; t < p1; t += 2) {
           const uint32_t hi = code16(pts[t]), lo = t + 1 < p1 ? code16(pts[t + 1]) : 0u;
           u.words.push_back((hi << 16) | lo);
@@ -158,59 +138,86 @@ void emit_bvs(const RowParts* rps, const RowMeta* meta, const BitWriter& body, u
           u.words.push_back(rp.ints[t].second - lmin);
         }
       }
-      units.push_back(std::move(u));
+      row.units.push_back(std::move(u));
     }
+    (nu == 1 ? single : multi).push_back(std::move(row));
   }
-  max_extras = std::max(max_extras, slot);
-  // deal units into slices: groups (class32, far), each by (#intervals, #points) desc
-  std::vector<uint32_t> order(units.size());
-  for (uint32_t q = 0; q < order.size(); ++q) order[q] = q;
-  auto gid = [&](const Unit& u) { return (u.c32 ? 0 : 2) + (u.far ? 0 : 1); };
-  std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
-    const Unit &x = units[a], &y = units[b];
-    if (gid(x) != gid(y)) return gid(x) < gid(y);
-    if (x.ni != y.ni) return x.ni > y.ni;
-    return x.np > y.np;
+  // slices: lists of (row, unit) lanes; groups (class32, far) never share a slice
+  struct Slice {
+    std::vector<const Unit*> lanes;
+    bool c32, far, multi;
+  };
+  std::vector<Slice> slices;
+  auto gid = [](const URow& r) { return (r.c32 ? 0 : 2) + (r.far ? 0 : 1); };
+  // multi-unit rows: by per-unit load (so a slice's lanes have similar work),
+  // then unit count, packed first-fit
+  auto load = [](const URow& r) {
+    uint32_t p = 0, i = 0;
+    for (const Unit& u : r.units) {
+      p = std::max(p, u.np);
+      i = std::max(i, u.ni);
+    }
+    return p + 2 * i;
+  };
+  std::stable_sort(multi.begin(), multi.end(), [&](const URow& a, const URow& b) {
+    if (gid(a) != gid(b)) return gid(a) < gid(b);
+    if (load(a) != load(b)) return load(a) > load(b);
+    return a.units.size() > b.units.size();
   });
-  std::vector<std::pair<size_t, size_t>> slices;
-  for (size_t a = 0; a < order.size();) {
+  for (size_t a = 0; a < multi.size();) {
     size_t e = a;
-    while (e < order.size() && e - a < 32 && gid(units[order[e]]) == gid(units[order[a]])) ++e;
-    slices.push_back({a, e});
+    while (e < multi.size() && gid(multi[e]) == gid(multi[a])) ++e;
+    const size_t first = slices.size();
+    for (size_t q = a; q < e; ++q) {
+      const URow& row = multi[q];
+      size_t t = first;
+      while (t < slices.size() && slices[t].lanes.size() + row.units.size() > 32) ++t;
+      if (t == slices.size()) slices.push_back(Slice{{}, row.c32, row.far, true});
+      for (const Unit& u : row.units) slices[t].lanes.push_back(&u);
+    }
     a = e;
   }
-  const uint32_t nsl = (uint32_t)slices.size(), nh = (uint32_t)hrows.size(), nf = (uint32_t)fold.size();
-  if (nsl > 0xffffu || nh > 0xffffu || nf > 0xffffu) throw std::runtime_error("BV-S: block too large");
+  // single-unit rows: by (#intervals, #points) desc, dealt 32 per slice
+  std::stable_sort(single.begin(), single.end(), [&](const URow& a, const URow& b) {
+    if (gid(a) != gid(b)) return gid(a) < gid(b);
+    if (a.units[0].ni != b.units[0].ni) return a.units[0].ni > b.units[0].ni;
+    return a.units[0].np > b.units[0].np;
+  });
+  for (size_t a = 0; a < single.size();) {
+    Slice sl{{}, single[a].c32, single[a].far, false};
+    size_t e = a;
+    while (e < single.size() && e - a < 32 && gid(single[e]) == gid(single[a])) sl.lanes.push_back(&single[e++].units[0]);
+    slices.push_back(std::move(sl));
+    a = e;
+  }
+  const uint32_t nsl = (uint32_t)slices.size(), nh = (uint32_t)hrows.size();
+  if (nsl > 0xffffu || nh > 0xffffu) throw std::runtime_error("BV-S: block too large");
   so.assign(kBvsHead + nsl, 0u);
   so[0] = nsl | (nh << 16);
-  so[3] = nf | (slot << 16);
-  so.insert(so.end(), fold.begin(), fold.end());
   for (uint32_t s = 0; s < nsl; ++s) {
+    const Slice& sl = slices[s];
     so[kBvsHead + s] = (uint32_t)so.size();
-    const size_t a = slices[s].first, e = slices[s].second;
     uint32_t mnp = 0, mni = 0, nq = 0;
-    for (size_t q = a; q < e; ++q) {
-      const Unit& u = units[order[q]];
-      mnp = std::max(mnp, u.np);
-      mni = std::max(mni, u.ni);
-      nq = std::max<uint32_t>(nq, (uint32_t)u.words.size());
-      st.lane_words_used += u.words.size();
-      st.lane_iters_used += u.np + u.ni;
+    for (const Unit* u : sl.lanes) {
+      mnp = std::max(mnp, u->np);
+      mni = std::max(mni, u->ni);
+      nq = std::max<uint32_t>(nq, (uint32_t)u->words.size());
+      st.lane_words_used += u->words.size();
+      st.lane_iters_used += u->np + u->ni;
     }
-    const Unit& u0 = units[order[a]];
-    so.push_back(make_smeta(mnp, mni, u0.c32, u0.far));
+    so.push_back(make_smeta(mnp, mni, sl.c32, sl.far, sl.multi));
     for (size_t l = 0; l < 32; ++l) {
-      if (a + l < e) {
-        const Unit& u = units[order[a + l]];
-        so.push_back(make_uh(u.primary, u.kslot, u.r, u.nm, u.np, u.ni));
+      if (l < sl.lanes.size()) {
+        const Unit& u = *sl.lanes[l];
+        so.push_back(make_uh(u.primary, u.primary ? u.k : 0u, u.primary ? u.r : 0u, u.nm, u.np, u.ni));
       } else {
         so.push_back(0u);
       }
     }
     const size_t b0 = so.size();
     so.resize(b0 + (size_t)nq * 32, 0u);
-    for (size_t l = 0; a + l < e; ++l) {
-      const Unit& u = units[order[a + l]];
+    for (size_t l = 0; l < sl.lanes.size(); ++l) {
+      const Unit& u = *sl.lanes[l];
       for (size_t q = 0; q < u.words.size(); ++q) so[b0 + q * 32 + l] = u.words[q];
     }
     st.lane_words += (uint64_t)nq * 32;
@@ -255,7 +262,7 @@ BvdLayout build_bvd(const BvDecoded& dec, const BvParams& bp, const BvdOptions& 
   D.min_interval = bp.min_interval;
   D.nblocks = (uint32_t)(((uint64_t)g.n + B - 1) / B);
   D.max_depth = 0;
-  D.max_extras = 0;
+  D.pad = 0;
   const uint32_t nb = D.nblocks;
   std::vector<BitWriter> bstream(nb);
   L.blocks.resize(nb);
@@ -263,7 +270,6 @@ BvdLayout build_bvd(const BvDecoded& dec, const BvParams& bp, const BvdOptions& 
   std::vector<uint32_t> bdepth(nb, 0);
   std::vector<std::vector<uint32_t>> sstream(nb);
   std::vector<BvsStats> bst(nb);
-  std::vector<uint32_t> bmaxex(nb, 0);
   parallel_for(nb, [&](uint64_t b0, uint64_t b1) {
     std::vector<RowParts> rps(B);
     std::vector<uint32_t> plus, cols, depth(B), hdr(B), escs;
@@ -374,7 +380,7 @@ BvdLayout build_bvd(const BvDecoded& dec, const BvParams& bp, const BvdOptions& 
       L.blocks[b].wlo = (uint32_t)lo;
       L.blocks[b].nwords = (uint32_t)(out.nbits / 32);
       L.blocks[b].nesc = (uint32_t)(escs.size() / 4);
-      emit_bvs(rps.data(), meta.data(), body, r0, nr, lo, W, bp.min_interval, sstream[b], bst[b], bmaxex[b]);
+      emit_bvs(rps.data(), meta.data(), body, nr, lo, W, bp.min_interval, sstream[b], bst[b]);
     }
   });
   uint64_t off = 0, maxw = 0, g_all = 0, g_in = 0;
@@ -421,7 +427,6 @@ BvdLayout build_bvd(const BvDecoded& dec, const BvParams& bp, const BvdOptions& 
     L.sstats.lane_words_used += bst[b].lane_words_used;
     L.sstats.lane_iters += bst[b].lane_iters;
     L.sstats.lane_iters_used += bst[b].lane_iters_used;
-    D.max_extras = std::max(D.max_extras, bmaxex[b]);
   }
   std::sort(ssz.begin(), ssz.end());
   L.sstats.p995_block_words = nb ? ssz[std::min<uint64_t>(nb - 1, (uint64_t)(nb * 0.995))] : 0;

@@ -80,25 +80,26 @@ __host__ __device__ constexpr uint32_t make_hdr(uint32_t r, uint32_t nm, uint32_
 //     stores absolute columns, one word per point, two per interval
 //     (left, len - Lmin).  A slice's lane streams are interleaved: word q of
 //     lane l at body + 32 q + l (one conflict-free shared load per word);
-//   * unit 0 of a row is its primary (writes delta_i and r_i); further units
-//     write partial sums to extra slots, folded into delta_i after decode by
-//     the fold table.  Rows with more than kBvsHeavyCodes codes are decoded
-//     by a whole warp from a row-major, bit-packed heavy stream (BV-D codes).
+//   * a row that needs 2..32 units puts them in adjacent lanes of one
+//     "multi" slice (rows packed first-fit decreasing); the warp combines a
+//     row's lanes with a segmented shuffle reduction and the row's first
+//     unit (its primary) writes delta_i and r_i.  Rows needing more than 32
+//     units are decoded by a whole warp from a row-major, bit-packed heavy
+//     stream (BV-D codes).
 // Block stream (u32 words):
 //   [0] nslices | nheavy << 16   [1] heavy table offset   [2] heavy stream offset
-//   [3] nfold | nextra << 16     [4, 4 + nslices) slice record offsets
-//   [4 + nslices, + nfold) fold table: k | first extra slot << 10 | count << 21
+//   [3] 0                        [4, 4 + nslices) slice record offsets
 //   slice record: [meta][header x 32][body]
-//     meta: max #points | max #intervals << 5 | class32 << 8 | far << 9
-//     header: valid << 31 | primary << 30 | (k or extra slot) << 20 | r << 17 |
+//     meta: max #points | max #intervals << 5 | class32 << 8 | far << 9 |
+//           multi << 10
+//     header: valid << 31 | primary << 30 | k << 20 | r << 17 |
 //             #minus << 12 | #points << 7 | #intervals << 4
 //   heavy table: kBvsHeavyEntry words per heavy row: BV-D-style a-word
 //     (make_sa), #minus, #residual, #interval, bit offset in the heavy stream, 0
 //   heavy stream: the heavy rows' BV-D bodies, bit-packed, MSB first
 constexpr uint32_t kBvsUnitPts = 16;
 constexpr uint32_t kBvsUnitInts = 2;
-constexpr uint32_t kBvsHeavyCodes = 256;
-constexpr uint32_t kBvsMaxExtras = 384;
+constexpr uint32_t kBvsMaxUnits = 32;  // more -> heavy row
 constexpr uint32_t kBvsHeavyEntry = 6;
 constexpr uint32_t kBvsHead = 4;
 constexpr uint32_t kBvsBias16 = 32768;
@@ -111,27 +112,25 @@ __host__ __device__ constexpr uint32_t sa_wp(uint32_t a) { return (a >> 15) & 31
 __host__ __device__ constexpr uint32_t sa_wl(uint32_t a) { return (a >> 20) & 31u; }
 __host__ __device__ constexpr bool sa_far(uint32_t a) { return (a >> 25) & 1u; }
 
-__host__ __device__ constexpr uint32_t make_uh(bool primary, uint32_t kslot, uint32_t r, uint32_t nm, uint32_t np,
+__host__ __device__ constexpr uint32_t make_uh(bool primary, uint32_t k, uint32_t r, uint32_t nm, uint32_t np,
                                                uint32_t ni) {
-  return (1u << 31) | ((primary ? 1u : 0u) << 30) | (kslot << 20) | (r << 17) | (nm << 12) | (np << 7) | (ni << 4);
+  return (1u << 31) | ((primary ? 1u : 0u) << 30) | (k << 20) | (r << 17) | (nm << 12) | (np << 7) | (ni << 4);
 }
 __host__ __device__ constexpr bool uh_valid(uint32_t h) { return h >> 31; }
 __host__ __device__ constexpr bool uh_primary(uint32_t h) { return (h >> 30) & 1u; }
-__host__ __device__ constexpr uint32_t uh_kslot(uint32_t h) { return (h >> 20) & 1023u; }
+__host__ __device__ constexpr uint32_t uh_k(uint32_t h) { return (h >> 20) & 1023u; }
 __host__ __device__ constexpr uint32_t uh_r(uint32_t h) { return (h >> 17) & 7u; }
 __host__ __device__ constexpr uint32_t uh_nm(uint32_t h) { return (h >> 12) & 31u; }
 __host__ __device__ constexpr uint32_t uh_np(uint32_t h) { return (h >> 7) & 31u; }
 __host__ __device__ constexpr uint32_t uh_ni(uint32_t h) { return (h >> 4) & 7u; }
-__host__ __device__ constexpr uint32_t make_smeta(uint32_t max_np, uint32_t max_ni, bool c32, bool far) {
-  return max_np | (max_ni << 5) | ((c32 ? 1u : 0u) << 8) | ((far ? 1u : 0u) << 9);
+__host__ __device__ constexpr uint32_t make_smeta(uint32_t max_np, uint32_t max_ni, bool c32, bool far, bool multi) {
+  return max_np | (max_ni << 5) | ((c32 ? 1u : 0u) << 8) | ((far ? 1u : 0u) << 9) | ((multi ? 1u : 0u) << 10);
 }
 __host__ __device__ constexpr uint32_t smeta_np(uint32_t m) { return m & 31u; }
 __host__ __device__ constexpr uint32_t smeta_ni(uint32_t m) { return (m >> 5) & 7u; }
 __host__ __device__ constexpr bool smeta_c32(uint32_t m) { return (m >> 8) & 1u; }
 __host__ __device__ constexpr bool smeta_far(uint32_t m) { return (m >> 9) & 1u; }
-__host__ __device__ constexpr uint32_t make_fold(uint32_t k, uint32_t first, uint32_t count) {
-  return k | (first << 10) | (count << 21);
-}
+__host__ __device__ constexpr bool smeta_multi(uint32_t m) { return (m >> 10) & 1u; }
 
 struct BvdBlockInfo {
   uint64_t word_offset;  // first u32 word of this block's stream (16-byte aligned)
@@ -149,7 +148,7 @@ struct BvdDims {
   uint32_t nblocks;
   uint32_t max_block_words;
   uint32_t max_depth;    // longest reference chain (drives the level phases)
-  uint32_t max_extras;   // BV-S: most extra-unit slots in one block
+  uint32_t pad;
 };
 
 }  // namespace cmvg

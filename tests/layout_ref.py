@@ -92,10 +92,11 @@ UNIT_PTS, UNIT_INTS, BIAS16 = 16, 2, 32768
 
 def decode_sliced(words, blocks, n, B, lmin, W):
     """Decode the BV-S layout as the gather kernel reads it: heavy rows from the
-    row-major bit stream, units from the lane-interleaved slice bodies, extra
-    units folded into their rows.  Returns (refs, rows) like decode_layout and
-    checks the structural invariants (every row exactly one primary unit,
-    slice metadata = max over lanes, class/far flags consistent)."""
+    row-major bit stream, units from the lane-interleaved slice bodies; in
+    multi slices a row's units occupy adjacent lanes starting at its primary.
+    Returns (refs, rows) like decode_layout and checks the structural
+    invariants (every row exactly one primary unit, slice metadata = max over
+    lanes, class/far flags consistent, units within their limits)."""
     rows_out = [None] * n
     refs_out = [0] * n
     for b in range(len(blocks)):
@@ -107,9 +108,8 @@ def decode_sliced(words, blocks, n, B, lmin, W):
         nr = min(B, n - r0)
         nsl, nh = s[0] & 0xFFFF, s[0] >> 16
         htab, hstr = s[1], s[2]
-        nf, nex = s[3] & 0xFFFF, s[3] >> 16
+        assert s[3] == 0
         parts = {}   # k -> dict(minus, res, ints, r)
-        extras = {}  # slot -> (minus, res, ints)
 
         def inwin(c):
             return wlo <= c < wlo + W
@@ -132,13 +132,15 @@ def decode_sliced(words, blocks, n, B, lmin, W):
         for sl in range(nsl):
             rec = s[4 + sl]
             meta = s[rec]
-            mnp, mni, c32, far = meta & 31, (meta >> 5) & 7, (meta >> 8) & 1, (meta >> 9) & 1
+            mnp, mni, c32, far, multi = meta & 31, (meta >> 5) & 7, (meta >> 8) & 1, (meta >> 9) & 1, (meta >> 10) & 1
             seen_np, seen_ni = 0, 0
+            cur = None
             for lane in range(32):
                 h = s[rec + 1 + lane]
                 if not h >> 31:
+                    cur = None
                     continue
-                prim, ks, r = (h >> 30) & 1, (h >> 20) & 1023, (h >> 17) & 7
+                prim, k, r = (h >> 30) & 1, (h >> 20) & 1023, (h >> 17) & 7
                 nm, npt, ni = (h >> 12) & 31, (h >> 7) & 31, (h >> 4) & 7
                 assert npt <= UNIT_PTS and ni <= UNIT_INTS and nm <= npt
                 seen_np, seen_ni = max(seen_np, npt), max(seen_ni, ni)
@@ -159,25 +161,19 @@ def decode_sliced(words, blocks, n, B, lmin, W):
                         ints.append((lw(npt + 2 * u), lw(npt + 2 * u + 1) + lmin))
                 ufar = any(not inwin(c) for c in pts) or any(
                     not (inwin(a) and inwin(a + ln - 1)) for a, ln in ints)
-                assert bool(ufar) == bool(far), (b, sl, lane)
-                unit = (pts[:nm], pts[nm:], ints)
+                if not far:
+                    assert not ufar, (b, sl, lane)
                 if prim:
-                    assert ks not in parts
-                    parts[ks] = dict(minus=list(unit[0]), res=list(unit[1]), ints=list(unit[2]), r=r)
+                    assert k not in parts
+                    cur = k
+                    parts[k] = dict(minus=pts[:nm], res=pts[nm:], ints=ints, r=r)
                 else:
-                    assert ks not in extras
-                    extras[ks] = unit
+                    assert multi and cur is not None, (b, sl, lane)
+                    assert k == 0 and r == 0
+                    parts[cur]["minus"] += pts[:nm]
+                    parts[cur]["res"] += pts[nm:]
+                    parts[cur]["ints"] += ints
             assert (seen_np, seen_ni) == (mnp, mni), (b, sl)
-        assert len(extras) == nex
-        for f in range(nf):
-            e = s[4 + nsl + f]
-            k, first, cnt = e & 1023, (e >> 10) & 2047, e >> 21
-            for c in range(first, first + cnt):
-                mi, re, it = extras.pop(c)
-                parts[k]["minus"] += mi
-                parts[k]["res"] += re
-                parts[k]["ints"] += it
-        assert not extras
         assert sorted(parts) == list(range(nr))
         for k in range(nr):
             p = parts[k]

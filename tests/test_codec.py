@@ -146,13 +146,18 @@ def test_layout_info_sizes():
     assert li["max_depth"] <= 3
 
 
-def test_sliced_layout_extra_budget():
-    # 200 rows of ~120 scattered columns: ~8 units each -> far more extra
-    # slots than kBvsMaxExtras, so the transcoder moves rows to the warp path
+def test_sliced_layout_multi_and_heavy_rows():
+    # rows of ~120 scattered columns need 8 units (adjacent lanes of a multi
+    # slice); rows of ~700 need > 32 units and take the warp (heavy) path
     rng = np.random.default_rng(5)
     n = 2048
-    rows = [sorted(set(rng.integers(0, n, 120).tolist())) if k % 5 == 0 else sorted(set(rng.integers(0, n, 3).tolist()))
-            for k in range(n)]
+    def row(k):
+        if k % 97 == 0:
+            return sorted(set(rng.integers(0, n, 700).tolist()))
+        if k % 5 == 0:
+            return sorted(set(rng.integers(0, n, 120).tolist()))
+        return sorted(set(rng.integers(0, n, 3).tolist()))
+    rows = [row(k) for k in range(n)]
     g = csr_from_rows(rows)
     s = P.BvStream.encode(g, P.BvParams())
     words, blocks = s.layout_export(P.CreateOptions(block_rows=1024, window=1536), sliced=True)

@@ -159,3 +159,23 @@ def test_adds_per_product(cuda):
     dg = P.BvGraph(P.BvStream.encode(g, bv_params(1)))
     assert 0 < dg.adds_per_product() < g.m
     assert dg.dimension() == g.n
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_gather_multi_unit_and_heavy_rows(cuda, dtype):
+    # rows split across adjacent lanes of multi slices (segmented warp
+    # reduction) and rows beyond 32 units (warp path), mixed with light rows
+    rng = np.random.default_rng(5)
+    n = 4096
+
+    def row(k):
+        if k % 97 == 0:
+            return sorted(set(rng.integers(0, n, 700).tolist()))
+        if k % 5 == 0:
+            return sorted(set(rng.integers(max(0, k - 3000), min(n, k + 3000), 120).tolist()))
+        if k % 7 == 0:
+            return list(range(max(0, k - 40), min(n, k + 40), 2))  # 40 points near the diagonal
+        return sorted(set(rng.integers(0, n, 3).tolist()))
+    g = csr_from_rows([row(k) for k in range(n)])
+    check_gather(g, P.BvParams(), dtype=dtype)
+    check_gather(g, P.BvParams(), P.CreateOptions(window=512), dtype=dtype)
