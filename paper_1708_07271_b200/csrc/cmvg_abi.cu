@@ -259,8 +259,6 @@ int cmvg_create(const cmvg_bvstream* s, const cmvg_create_opts* opts_in, cmvg_gr
       g->sblocks.upload(sbl.data(), sbl.size());
       g->s_stream_bytes = (s1 - s0) * 4;
       g->sstats = L.sstats;
-      const char* gl = getenv("CMVG_GATHER_LAYOUT");
-      g->gather_bvd = gl && std::string(gl) == "bvd";
     }
     g->refd.upload(dec.ref_dist.data() + o.row_begin, row_end - o.row_begin);
     // stats of the shard
@@ -402,18 +400,10 @@ namespace {
 
 template <typename XT, typename YT>
 void launch_gather(cmvg_graph* g, const XT* x, YT* y, cudaStream_t st) {
-  if (!g->gather_bvd) {
-    const BvsSmem L = bvs_smem_layout(g->dims, sizeof(XT));
-    auto kern = bvs_gather_kernel<XT, YT>;
-    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
-    kern<<<g->nblocks, g->threads, L.total, st>>>(g->sdev(), x, y, PrArgs{});
-    CUDA_TRY(cudaGetLastError());
-    return;
-  }
-  GatherSmem L = gather_smem_layout(g->dims, g->stream_cap_words, sizeof(XT), true);
-  auto kern = bvd_gather_kernel<XT, YT>;
+  const BvsSmem L = bvs_smem_layout(g->dims, sizeof(XT));
+  auto kern = bvs_gather_kernel<XT, YT>;
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
-  kern<<<g->nblocks, g->threads, L.total, st>>>(g->dev(), x, y, PrArgs{});
+  kern<<<g->nblocks, g->threads, L.total, st>>>(g->sdev(), x, y, PrArgs{});
   CUDA_TRY(cudaGetLastError());
 }
 

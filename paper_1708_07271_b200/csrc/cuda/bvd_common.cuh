@@ -339,25 +339,22 @@ __device__ __forceinline__ void chain_and_store(double* s_yhi, float* s_ylo, Row
                                                 EPI epi = EPI(), uint32_t max_depth = 0xffffffffu) {
   const uint32_t T = blockDim.x, tid = threadIdx.x;
   if (max_depth <= 3) {
-    // Bounded chains (R <= 3): each row walks its <= 3 ancestors and sums
-    // from the root, y = d_i + (d_p1 + (d_p2 + d_p3)) in double-double --
-    // the reference's order, no barriers.
+    // Bounded chains (R <= 3): each row walks its <= 3 ancestors,
+    // y_i = d_i + d_p1 + d_p2 + d_p3 accumulated with TwoSum (error terms
+    // collected with the low parts), no barriers.
     for (uint32_t k = tid; k < c.nr; k += T) {
-      const uint32_t r1 = c.ref[k];
-      const uint32_t p1 = k - r1;
-      const uint32_t r2 = r1 ? c.ref[p1] : 0u;
-      const uint32_t p2 = p1 - r2;
-      const uint32_t r3 = r2 ? c.ref[p2] : 0u;
-      const uint32_t p3 = p2 - r3;
-      double hi = 0.0, lo = 0.0;
-      if (r3) {
-        hi = s_yhi[p3];
-        lo = s_ylo[p3];
+      double s = s_yhi[k], e = (double)s_ylo[k];
+      uint32_t p = k, r = c.ref[k];
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        if (r) {
+          p -= r;
+          tsum(s, e, s_yhi[p]);
+          e += (double)s_ylo[p];
+          r = c.ref[p];
+        }
       }
-      if (r2) dd_add(hi, lo, s_yhi[p2], s_ylo[p2]);
-      if (r1) dd_add(hi, lo, s_yhi[p1], s_ylo[p1]);
-      dd_add(hi, lo, s_yhi[k], s_ylo[k]);
-      epi.store(yb, k, hi + lo);
+      epi.store(yb, k, s + e);
     }
     epi.finish(c.wscratch);
     return;

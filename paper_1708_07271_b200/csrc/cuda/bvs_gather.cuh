@@ -24,9 +24,21 @@
 #include <cstdint>
 
 #include "bvd_common.cuh"
-#include "bvd_gather.cuh"
 
 namespace cmvg {
+
+// PageRank step arguments (shard-relative pointers; see PageRankEpi).
+struct PrArgs {
+  const uint32_t* deg;
+  const double* p_prev;
+  double* q_next;
+  double* partial;
+  const double* dmass;  // device scalar: dangling mass D of the previous iterate (nullptr -> dmass_host)
+  double dmass_host;
+  double alpha;
+  uint32_t n;
+  int uniform;
+};
 
 constexpr uint32_t kBvsGuardWords = 64;  // zero words after the last block (lanes never read past their unit)
 
@@ -53,14 +65,6 @@ __host__ __device__ inline BvsSmem bvs_smem_layout(const BvdDims& d, uint32_t xs
   return s;
 }
 
-// Bits [pos, pos + w) of this lane's stream in a lane-interleaved body.
-template <class S>
-__device__ __forceinline__ uint32_t lane_bits(const S& src, uint32_t body, uint32_t pos, uint32_t w) {
-  const uint32_t a = body + (pos >> 5) * 32u;
-  const uint32_t v = __funnelshift_l(src.w(a + 32u), src.w(a), pos & 31u);
-  return w ? v >> (32u - w) : 0u;
-}
-
 __device__ __forceinline__ uint32_t ticket_issue(int* counter) {
   return (threadIdx.x & 31u) == 0 ? (uint32_t)atomicAdd(counter, 1) : 0u;
 }
@@ -68,7 +72,7 @@ __device__ __forceinline__ uint32_t ticket_take(uint32_t t) { return __shfl_sync
 
 enum BvsMisc : int { kBvsHeavyCtr = 0, kBvsSliceCtr = 1 };
 
-// Heavy rows: one warp per row (see gather_heavy in bvd_gather.cuh).
+// Heavy rows: one warp per row, lanes stride over the row's fixed-width codes.
 template <class S, class XW>
 __device__ __forceinline__ void bvs_heavy(const S& src, const XW& xw, int32_t r0, uint32_t lmin, int* misc,
                                           double* s_yhi, float* s_ylo, uint8_t* s_ref) {
@@ -88,15 +92,35 @@ __device__ __forceinline__ void bvs_heavy(const S& src, const XW& xw, int32_t r0
       const double xv = xw.at(ib + (int32_t)extract_bits(src, off0 + t * wp, wp));
       tsum(acc, comp, t < nm ? -xv : xv);
     }
+    // intervals: in-window ones O(1) by their lane; the others (long runs
+    // reaching outside the window) summed by the whole warp, coalesced
     const uint32_t ioff = off0 + np * wp;
-    for (uint32_t t = lane; t < ni; t += 32) {
-      const uint32_t o = ioff + t * (wp + wl);
-      const int32_t left = ib + (int32_t)extract_bits(src, o, wp);
-      const uint32_t len = extract_bits(src, o + wp, wl) + lmin;
-      double lo;
-      const double hi = xw.isum(left, len, lo);
-      tsum(acc, comp, hi);
-      comp += lo;
+    for (uint32_t tb = 0; tb < ni; tb += 32) {
+      const uint32_t t = tb + lane;
+      const bool on = t < ni;
+      int32_t left = 0;
+      uint32_t len = 0;
+      if (on) {
+        const uint32_t o = ioff + t * (wp + wl);
+        left = ib + (int32_t)extract_bits(src, o, wp);
+        len = extract_bits(src, o + wp, wl) + lmin;
+      }
+      const uint32_t a = (uint32_t)(left - (int32_t)xw.wlo);
+      const bool nearw = on && a < xw.W && a + len <= xw.W;
+      if (nearw) {
+        double lo;
+        const double hi = xw.isum_near(a, len, lo);
+        tsum(acc, comp, hi);
+        comp += lo;
+      }
+      uint32_t m = __ballot_sync(0xffffffffu, on && !nearw);
+      while (m) {
+        const int sl = __ffs(m) - 1;
+        m &= m - 1u;
+        const int32_t L = __shfl_sync(0xffffffffu, left, sl);
+        const uint32_t N = __shfl_sync(0xffffffffu, len, sl);
+        for (uint32_t e = lane; e < N; e += 32) tsum(acc, comp, xw.at(L + (int32_t)e));
+      }
     }
     double hi = acc + comp, lo = comp - (hi - acc);
 #pragma unroll
@@ -112,8 +136,6 @@ __device__ __forceinline__ void bvs_heavy(const S& src, const XW& xw, int32_t r0
   }
 }
 
-// x-window index of a class-16 code
-__device__ __forceinline__ uint32_t c16_idx(uint32_t code) { return code - kBvsBias16; }
 // +x, or -x for t < nm (minus codes come first): flip the sign bit when t - nm < 0
 __device__ __forceinline__ double signed_term(double x, uint32_t t, uint32_t nm) {
   const uint32_t m = (t - nm) & 0x80000000u;
@@ -122,88 +144,85 @@ __device__ __forceinline__ double signed_term(double x, uint32_t t, uint32_t nm)
 
 // Slices: one unit (<= 16 points, <= 2 intervals of one row) per lane; in
 // "multi" slices a row's units occupy adjacent lanes and are combined by a
-// segmented warp reduction.
-template <class S, class XW>
-__device__ __forceinline__ void bvs_slices(const S& src, const XW& xw, uint32_t lmin, int* misc, double* s_yhi,
-                                           float* s_ylo, uint8_t* s_ref) {
+// segmented warp reduction.  `bs` is the block's stream in global memory.
+template <class XW>
+__device__ __forceinline__ void bvs_slices(const uint32_t* __restrict__ bs, const XW& xw, uint32_t lmin, int* misc,
+                                           double* s_yhi, float* s_ylo, uint8_t* s_ref) {
   const uint32_t lane = threadIdx.x & 31u;
-  const uint32_t nsl = src.w(0) & 0xffffu;
-  const uint32_t Z = xw.W;  // zero entry of the window (idle lanes read it)
+  const uint32_t nsl = __ldg(bs) & 0xffffu;
   uint32_t s = ticket_take(ticket_issue(&misc[kBvsSliceCtr]));
   while (s < nsl) {
     const uint32_t next = ticket_issue(&misc[kBvsSliceCtr]);
-    const uint32_t rec = src.w(kBvsHead + s);
-    const uint32_t meta = src.w(rec);
-    const uint32_t h = src.w(rec + 1u + lane);
-    const uint32_t body = rec + 33u + lane;
-    const uint32_t nm = uh_nm(h), np = uh_np(h), ni = uh_ni(h);
+    const uint32_t* rec = bs + __ldg(bs + kBvsHead + s);
+    const uint32_t meta = __ldg(rec);
+    const uint32_t h = __ldg(rec + 1u + lane);
+    const uint32_t* body = rec + 33u + lane;  // this lane's word q at body[32 q]
     const uint32_t mnp = smeta_np(meta), mni = smeta_ni(meta);
     double acc = 0.0, comp = 0.0;
-    if (!smeta_c32(meta)) {
-      // the lane's words, loaded up front (coalesced across lanes): <= 8
-      // point words (two 16-bit codes each) and <= 2 interval words
-      const uint32_t npw = (np + 1u) >> 1;
+    if (!smeta_c32(meta) && !smeta_far(meta)) {
+      // near class 16 (rectangular): no per-lane counts -- pad codes read the
+      // window's zero entry, empty intervals have length 0
+      const uint32_t mnpw = (mnp + 1u) >> 1;
       uint32_t w[kBvsUnitPts / 2];
 #pragma unroll
-      for (uint32_t q = 0; q < kBvsUnitPts / 2; ++q) w[q] = q < npw ? src.w(body + q * 32u) : 0u;
-      const uint32_t wi0 = ni > 0 ? src.w(body + npw * 32u) : 0u;
-      const uint32_t wi1 = ni > 1 ? src.w(body + (npw + 1u) * 32u) : 0u;
-      if (!smeta_far(meta)) {
-        double acc2 = 0.0, comp2 = 0.0;
+      for (uint32_t q = 0; q < kBvsUnitPts / 2; ++q) w[q] = q < mnpw ? __ldg(body + q * 32u) : 0u;
+      const uint32_t wi0 = mni > 0 ? __ldg(body + mnpw * 32u) : 0u;
+      const uint32_t wi1 = mni > 1 ? __ldg(body + (mnpw + 1u) * 32u) : 0u;
+      double acc2 = 0.0, comp2 = 0.0;
 #pragma unroll
-        for (uint32_t q = 0; q < kBvsUnitPts / 2; ++q) {
-          const uint32_t t = 2u * q;
-          if (t >= mnp) break;  // warp-uniform
-          const uint32_t i0 = t < np ? c16_idx(w[q] >> 16) : Z;
-          const uint32_t i1 = t + 1u < np ? c16_idx(w[q] & 0xffffu) : Z;
-          tsum(acc, comp, signed_term(xw.at_near(i0), t, nm));
-          tsum(acc2, comp2, signed_term(xw.at_near(i1), t + 1u, nm));
+      for (uint32_t q = 0; q < kBvsUnitPts / 2; ++q) {
+        if (q >= mnpw) break;  // warp-uniform
+        const uint32_t v = w[q];
+        const double x0 = xw.at_padded((v >> 16) & 0x7fffu), x1 = xw.at_padded(v & 0x7fffu);
+        // minus codes: flip the sign bit (bit 15 of each code)
+        tsum(acc, comp, __hiloint2double(__double2hiint(x0) ^ (int)(v & 0x80000000u), __double2loint(x0)));
+        tsum(acc2, comp2, __hiloint2double(__double2hiint(x1) ^ (int)((v << 16) & 0x80000000u), __double2loint(x1)));
+      }
+      tsum(acc, comp, acc2);
+      comp += comp2;
+      if (mni > 0) {
+        double lo;
+        const double hi = xw.isum_near(wi0 >> 16, wi0 & 0xffffu, lo);
+        tsum(acc, comp, hi);
+        comp += lo;
+      }
+      if (mni > 1) {
+        double lo;
+        const double hi = xw.isum_near(wi1 >> 16, wi1 & 0xffffu, lo);
+        tsum(acc, comp, hi);
+        comp += lo;
+      }
+    } else if (!smeta_c32(meta)) {
+      // far class 16: biased 16-bit codes, bounds-checked
+      const uint32_t nm = uh_nm(h), np = uh_np(h), ni = uh_ni(h);
+      const int32_t base = (int32_t)xw.wlo - (int32_t)kBvsBias16;
+      const uint32_t npw = (np + 1u) >> 1;
+      for (uint32_t t = 0; t < mnp; ++t) {
+        const uint32_t v = t < np ? __ldg(body + (t >> 1) * 32u) : 0u;
+        const uint32_t c = (t & 1u) ? (v & 0xffffu) : (v >> 16);
+        const double xv = t < np ? xw.at(base + (int32_t)c) : 0.0;
+        tsum(acc, comp, signed_term(xv, t, nm));
+      }
+      for (uint32_t u = 0; u < mni; ++u) {
+        double hi = 0.0, lo = 0.0;
+        if (u < ni) {
+          const uint32_t v = __ldg(body + (npw + u) * 32u);
+          hi = xw.isum(base + (int32_t)(v >> 16), (v & 0xffffu) + lmin, lo);
         }
-        tsum(acc, comp, acc2);
-        comp += comp2;
-        if (mni > 0) {
-          double lo;
-          const double hi = xw.isum_near(ni > 0 ? c16_idx(wi0 >> 16) : 0u, ni > 0 ? (wi0 & 0xffffu) + lmin : 0u, lo);
-          tsum(acc, comp, hi);
-          comp += lo;
-        }
-        if (mni > 1) {
-          double lo;
-          const double hi = xw.isum_near(ni > 1 ? c16_idx(wi1 >> 16) : 0u, ni > 1 ? (wi1 & 0xffffu) + lmin : 0u, lo);
-          tsum(acc, comp, hi);
-          comp += lo;
-        }
-      } else {
-        const int32_t wlo = (int32_t)xw.wlo;
-#pragma unroll
-        for (uint32_t q = 0; q < kBvsUnitPts / 2; ++q) {
-          const uint32_t t = 2u * q;
-          if (t >= mnp) break;
-          const double x0 = t < np ? xw.at((int32_t)c16_idx(w[q] >> 16) + wlo) : 0.0;
-          const double x1 = t + 1u < np ? xw.at((int32_t)c16_idx(w[q] & 0xffffu) + wlo) : 0.0;
-          tsum(acc, comp, signed_term(x0, t, nm));
-          tsum(acc, comp, signed_term(x1, t + 1u, nm));
-        }
-#pragma unroll
-        for (uint32_t u = 0; u < kBvsUnitInts; ++u) {
-          if (u >= mni) break;
-          const uint32_t wv = u ? wi1 : wi0;
-          double hi = 0.0, lo = 0.0;
-          if (u < ni) hi = xw.isum((int32_t)c16_idx(wv >> 16) + wlo, (wv & 0xffffu) + lmin, lo);
-          tsum(acc, comp, hi);
-          comp += lo;
-        }
+        tsum(acc, comp, hi);
+        comp += lo;
       }
     } else {  // class 32: absolute columns, bounds-checked
+      const uint32_t nm = uh_nm(h), np = uh_np(h), ni = uh_ni(h);
       for (uint32_t t = 0; t < mnp; ++t) {
-        const uint32_t c = t < np ? src.w(body + t * 32u) : 0u;
+        const uint32_t c = t < np ? __ldg(body + t * 32u) : 0u;
         const double xv = t < np ? xw.at((int32_t)c) : 0.0;
         tsum(acc, comp, signed_term(xv, t, nm));
       }
-      const uint32_t ibase = body + np * 32u;
       for (uint32_t u = 0; u < mni; ++u) {
         double hi = 0.0, lo = 0.0;
-        if (u < ni) hi = xw.isum((int32_t)src.w(ibase + 2u * u * 32u), src.w(ibase + (2u * u + 1u) * 32u) + lmin, lo);
+        if (u < ni)
+          hi = xw.isum((int32_t)__ldg(body + (np + 2u * u) * 32u), __ldg(body + (np + 2u * u + 1u) * 32u) + lmin, lo);
         tsum(acc, comp, hi);
         comp += lo;
       }
@@ -264,7 +283,7 @@ __global__ void __launch_bounds__(256, 4) bvs_gather_kernel(BvdDev g, const XT* 
   uint8_t* s_ref = smem + L.off_ref;
   const Src<false> src{bs};
   bvs_heavy(src, xw, (int32_t)r0, D.min_interval, misc, s_yhi, s_ylo, s_ref);
-  bvs_slices(src, xw, D.min_interval, misc, s_yhi, s_ylo, s_ref);
+  bvs_slices(bs, xw, D.min_interval, misc, s_yhi, s_ylo, s_ref);
   __syncthreads();
 
   RowCtx rc{};

@@ -1,11 +1,10 @@
 // The per-block x-window in shared memory: x[wlo, wlo + W) staged with
 // coalesced loads into a padded layout (16-entry tiles at a stride of 17
 // entries, so a thread can walk one tile with 2-way bank conflicts), plus an
-// exclusive prefix of the window in double-double, stored two-level: P[j]
-// within j's 16-entry tile and Q[t] over whole tiles (hi fp64, lo fp32).  An
-// interval [a, e) is then
-//     (Q[e>>4] - Q[a>>4]) + (P[e] - P[a])
-// evaluated with three TwoSums -- O(1) for any length, branch-free, and
+// exclusive prefix F of the window in double-double (hi fp64, lo fp32), built
+// in three parallel steps: P[j] within j's 16-entry tile (one thread per
+// tile), Q[t] over whole tiles (one warp), then F[j] = Q[j>>4] + P[j].  An
+// interval [a, e) is then F[e] - F[a]: one TwoSum, O(1) for any length, and
 // accurate to ~1e-28 absolute, so interval sums carry no rounding error into
 // the reference chain (the north star's O(1) interval evaluation from an
 // exclusive prefix of x).
@@ -158,24 +157,34 @@ struct XWin {
           s_tl[ntiles] = (float)(il - (h2 - ih));
         }
       }
+      __syncthreads();
+      // full prefix in place: F[j] = Q[j >> 4] + P[j] (double-double), so an
+      // interval is F[e] - F[a] -- one TwoSum in the decode loop
+      for (uint32_t j = tid; j <= W; j += T) {
+        const uint32_t pj = xw_pad(j), t = j >> 4;
+        double hi = s_th[t], lo = (double)s_tl[t];
+        const double bhi = s_ph[pj], blo = (double)s_pl[pj];
+        double sh, se;
+        two_sum(hi, bhi, sh, se);
+        se += lo + blo;
+        hi = sh + se;
+        s_ph[pj] = hi;
+        s_pl[pj] = (float)(se - (hi - sh));
+      }
     }
     __syncthreads();
   }
 
   // Unchecked accessors for `near` rows (the builder guarantees the window
-  // holds every column and intervals span at most two tiles): j, a are
-  // window-relative.
+  // holds every column): j, a are window-relative, p a padded index.
   __device__ __forceinline__ double at_near(uint32_t j) const { return (double)s_x[xw_pad(j)]; }
+  __device__ __forceinline__ double at_padded(uint32_t p) const { return (double)s_x[p]; }
   __device__ __forceinline__ double isum_near(uint32_t a, uint32_t len, double& lo) const {
-    const uint32_t e = a + len;
-    const uint32_t ta = a >> 4, tb = e >> 4;
-    const uint32_t pa = xw_pad(a), pe = xw_pad(e);
-    double s1, e1, s2, e2, s3, e3;
-    two_sum(s_th[tb], -s_th[ta], s1, e1);
-    two_sum(s1, s_ph[pe], s2, e2);
-    two_sum(s2, -s_ph[pa], s3, e3);
-    lo = e1 + e2 + e3 + (((double)s_tl[tb] - (double)s_tl[ta]) + ((double)s_pl[pe] - (double)s_pl[pa]));
-    return s3;
+    const uint32_t pa = xw_pad(a), pe = xw_pad(a + len);
+    double s, e;
+    two_sum(s_ph[pe], -s_ph[pa], s, e);
+    lo = e + ((double)s_pl[pe] - (double)s_pl[pa]);
+    return s;
   }
 
   __device__ __forceinline__ double at(int32_t c) const {

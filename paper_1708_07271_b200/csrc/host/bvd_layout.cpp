@@ -73,7 +73,9 @@ inline uint32_t bits32(const std::vector<uint32_t>& w, uint64_t pos, uint64_t en
 struct Unit {
   uint32_t k, r, nm, np, ni;
   bool primary;
-  std::vector<uint32_t> words;
+  std::vector<uint32_t> words;  // far / class-32 encodings
+  std::vector<uint16_t> pc;     // near class-16: point codes (padded index | minus << 15)
+  std::vector<uint32_t> iw;     // near class-16: interval words (left - wlo) << 16 | len
 };
 struct URow {  // a row's units (adjacent lanes when there is more than one)
   uint32_t k;
@@ -125,7 +127,12 @@ void emit_bvs(const RowParts* rps, const RowMeta* meta, const BitWriter& body, u
       u.np = p1 - p0;
       u.ni = q1 - q0;
       u.nm = nm > p0 ? std::min(nm, p1) - p0 : 0;
-      if (!row.c32) {
+      if (!row.c32 && !row.far) {
+        for (uint32_t t = p0; t < p1; ++t)
+          u.pc.push_back((uint16_t)(bvs_pad_index((uint32_t)(pts[t] - wlo)) | (t < nm ? 0x8000u : 0u)));
+        for (uint32_t t = q0; t < q1; ++t)
+          u.iw.push_back(((uint32_t)(rp.ints[t].first - wlo) << 16) | rp.ints[t].second);
+      } else if (!row.c32) {
         for (uint32_t t = p0; t < p1; t += 2) {
           const uint32_t hi = code16(pts[t]), lo = t + 1 < p1 ? code16(pts[t + 1]) : 0u;
           u.words.push_back((hi << 16) | lo);
@@ -196,15 +203,17 @@ void emit_bvs(const RowParts* rps, const RowMeta* meta, const BitWriter& body, u
   so[0] = nsl | (nh << 16);
   for (uint32_t s = 0; s < nsl; ++s) {
     const Slice& sl = slices[s];
+    const bool nearc16 = !sl.c32 && !sl.far;
     so[kBvsHead + s] = (uint32_t)so.size();
     uint32_t mnp = 0, mni = 0, nq = 0;
     for (const Unit* u : sl.lanes) {
       mnp = std::max(mnp, u->np);
       mni = std::max(mni, u->ni);
       nq = std::max<uint32_t>(nq, (uint32_t)u->words.size());
-      st.lane_words_used += u->words.size();
+      st.lane_words_used += nearc16 ? (u->np + 1) / 2 + u->ni : u->words.size();
       st.lane_iters_used += u->np + u->ni;
     }
+    if (nearc16) nq = (mnp + 1) / 2 + mni;  // rectangular: points then intervals
     so.push_back(make_smeta(mnp, mni, sl.c32, sl.far, sl.multi));
     for (size_t l = 0; l < 32; ++l) {
       if (l < sl.lanes.size()) {
@@ -216,9 +225,24 @@ void emit_bvs(const RowParts* rps, const RowMeta* meta, const BitWriter& body, u
     }
     const size_t b0 = so.size();
     so.resize(b0 + (size_t)nq * 32, 0u);
-    for (size_t l = 0; l < sl.lanes.size(); ++l) {
-      const Unit& u = *sl.lanes[l];
-      for (size_t q = 0; q < u.words.size(); ++q) so[b0 + q * 32 + l] = u.words[q];
+    if (nearc16) {
+      // every lane: (mnp + 1) / 2 point words (pad codes read the window's
+      // zero entry) then mni interval words (0 = empty interval)
+      const uint32_t zc = bvs_pad_index(W), mnpw = (mnp + 1) / 2;
+      for (size_t l = 0; l < 32; ++l) {
+        const Unit* u = l < sl.lanes.size() ? sl.lanes[l] : nullptr;
+        for (uint32_t q = 0; q < mnpw; ++q) {
+          const uint32_t c0 = u && 2 * q < u->pc.size() ? u->pc[2 * q] : zc;
+          const uint32_t c1 = u && 2 * q + 1 < u->pc.size() ? u->pc[2 * q + 1] : zc;
+          so[b0 + (size_t)q * 32 + l] = (c0 << 16) | c1;
+        }
+        for (uint32_t q = 0; q < mni; ++q) so[b0 + (size_t)(mnpw + q) * 32 + l] = u && q < u->iw.size() ? u->iw[q] : 0u;
+      }
+    } else {
+      for (size_t l = 0; l < sl.lanes.size(); ++l) {
+        const Unit& u = *sl.lanes[l];
+        for (size_t q = 0; q < u.words.size(); ++q) so[b0 + q * 32 + l] = u.words[q];
+      }
     }
     st.lane_words += (uint64_t)nq * 32;
     st.lane_iters += 32ull * (mnp + mni);
@@ -254,7 +278,7 @@ BvdLayout build_bvd(const BvDecoded& dec, const BvParams& bp, const BvdOptions& 
   const uint32_t B = opt.block_rows, W = opt.window;
   if (B == 0 || (B & (B - 1)) || B % bp.segment_rows || B > 1024)
     throw std::invalid_argument("block_rows must be a power of two <= 1024 and a multiple of the BV segment");
-  if (W % 16 || W == 0) throw std::invalid_argument("window must be a positive multiple of 16");
+  if (W % 16 || W == 0 || W > 16384) throw std::invalid_argument("window must be a positive multiple of 16, at most 16384");
   if (bp.window > 7) throw std::invalid_argument("the device layout supports BV windows w <= 7");
   D.n = g.n;
   D.block_rows = B;

@@ -73,10 +73,15 @@ __host__ __device__ constexpr uint32_t make_hdr(uint32_t r, uint32_t nm, uint32_
 //     and dealt into 32-lane slices, so a warp decodes 32 units of near-equal
 //     work (lane utilisation ~85-95% instead of ~60% for whole rows);
 //   * codes are byte aligned and relative to the block's x-window start wlo
-//     (so a unit decodes without its row index): class 16 stores point codes
-//     as 16-bit (col - wlo + 2^15), two per word (first code in the high
-//     half), and an interval as one word (left - wlo + 2^15) << 16 |
-//     (len - Lmin); class 32
+//     (so a unit decodes without its row index).  Near class-16 slices (every
+//     column inside the window -- the common case) are rectangular: each lane
+//     holds ceil(max #points / 2) point words, two 16-bit codes each (first
+//     in the high half), code = padded window index | minus << 15, lanes with
+//     fewer points padded with the window's zero entry; then max #intervals
+//     words (left - wlo) << 16 | len (0 = empty).  Far class-16 units store
+//     16-bit codes col - wlo + 2^15 (two per word) and intervals
+//     (left - wlo + 2^15) << 16 | (len - Lmin), per lane counts from the
+//     header; class 32
 //     stores absolute columns, one word per point, two per interval
 //     (left, len - Lmin).  A slice's lane streams are interleaved: word q of
 //     lane l at body + 32 q + l (one conflict-free shared load per word);
@@ -103,6 +108,8 @@ constexpr uint32_t kBvsMaxUnits = 32;  // more -> heavy row
 constexpr uint32_t kBvsHeavyEntry = 6;
 constexpr uint32_t kBvsHead = 4;
 constexpr uint32_t kBvsBias16 = 32768;
+// padded x-window index (16-entry tiles at a stride of 17; cuda/xwindow.cuh)
+__host__ __device__ constexpr uint32_t bvs_pad_index(uint32_t j) { return j + (j >> 4); }
 __host__ __device__ constexpr uint32_t make_sa(uint32_t k, uint32_t r, uint32_t wp, uint32_t wl, bool far) {
   return k | (r << 12) | (wp << 15) | (wl << 20) | ((far ? 1u : 0u) << 25) | (1u << 31);
 }

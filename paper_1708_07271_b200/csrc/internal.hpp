@@ -144,7 +144,6 @@ struct cmvg_graph {
   DevBuf swords, sblocks;
   uint64_t s_stream_bytes = 0;
   BvsStats sstats;
-  bool gather_bvd = false;  // dev switch: gather on BV-D (CMVG_GATHER_LAYOUT=bvd)
   // canonical BV stream (whole graph) for decode_csr
   DevBuf bv_words, bv_seg;
   uint64_t nseg = 0;

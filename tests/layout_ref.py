@@ -147,7 +147,28 @@ def decode_sliced(words, blocks, n, B, lmin, W):
                 body = rec + 33 + lane
                 lw = lambda q: s[body + 32 * q]  # noqa: E731
                 pts, ints = [], []
-                if not c32:
+                if not c32 and not far:
+                    # near class 16: rectangular, padded window indices, sign in bit 15
+                    zc = W + (W >> 4)
+                    mnpw = (mnp + 1) >> 1
+                    minus, res = [], []
+                    for q in range(mnpw):
+                        w = lw(q)
+                        for c in (w >> 16, w & 0xFFFF):
+                            if c == zc:
+                                continue
+                            pi = c & 0x7FFF
+                            assert pi % 17 != 16
+                            col = wlo + (pi // 17) * 16 + pi % 17
+                            (minus if c >> 15 else res).append(col)
+                    assert (len(minus), len(minus) + len(res)) == (nm, npt), (b, sl, lane)
+                    pts = minus + res
+                    for u in range(mni):
+                        w = lw(mnpw + u)
+                        if w:
+                            ints.append((wlo + (w >> 16), w & 0xFFFF))
+                    assert len(ints) == ni
+                elif not c32:
                     for t in range(npt):
                         w = lw(t >> 1)
                         pts.append(wlo - BIAS16 + ((w & 0xFFFF) if t & 1 else (w >> 16)))
