@@ -335,7 +335,8 @@ def run_ours(args):
                             f"{args.dtype} (BASELINE.json configs[1]); each rank its own graph",
                 "n": g.n, "m": g.m, "bv": "w=7 R=3 Lmin=4 zeta3 segment=1024",
                 "S_bits": S, "bits_per_edge": S / g.m,
-                "device_layout_bytes": info["bvd_stream_bytes"] + info["bvd_lane_table_bytes"]
+                "device_layout": "BV-S (sliced)" if args.form == "gather" else "BV-D",
+                "device_layout_bytes": (info["bvs_stream_bytes"] if args.form == "gather" else info["bvd_stream_bytes"])
                 + info["bvd_block_table_bytes"],
                 "block_rows": args.block_rows, "lanes": args.lanes, "window": args.window,
                 "interval_mode": args.interval_mode, "l2": "flushed (512 MiB write) before every timed launch",
