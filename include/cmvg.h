@@ -119,6 +119,8 @@ typedef struct {
   uint64_t bvs_slices, bvs_heavy_rows;
   uint64_t bvs_lane_words, bvs_lane_words_used; /* slice body words incl. / excl. lane padding */
   uint64_t bvs_lane_iters, bvs_lane_iters_used; /* slice decode lane-iterations incl. / excl. idle lanes */
+  /* BV-T (target-sorted layout of the scatter form) */
+  uint64_t bvt_stream_bytes, bvt_entries, bvt_far_slots, bvt_heavy_targets, bvt_slices;
 } cmvg_graph_info;
 
 /* ---- errors -------------------------------------------------------------- */
@@ -162,6 +164,9 @@ const uint32_t* cmvg_layout_words(const cmvg_layout* l, uint64_t* nwords);
 /* BV-S words / block table (same 8-u32 block entries) */
 const uint32_t* cmvg_layout_swords(const cmvg_layout* l, uint64_t* nwords);
 const uint32_t* cmvg_layout_sblocks(const cmvg_layout* l, uint32_t* nblocks);
+/* BV-T words / block table */
+const uint32_t* cmvg_layout_twords(const cmvg_layout* l, uint64_t* nwords);
+const uint32_t* cmvg_layout_tblocks(const cmvg_layout* l, uint32_t* nblocks);
 const uint32_t* cmvg_layout_blocks(const cmvg_layout* l, uint32_t* nblocks);
 void cmvg_layout_free(cmvg_layout* l);
 int cmvg_graph_info_get(const cmvg_graph* g, cmvg_graph_info* out);

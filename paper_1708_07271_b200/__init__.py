@@ -90,7 +90,8 @@ class _InfoC(C.Structure):
                 ("bvs_stream_cap_words", C.c_uint32), ("bvs_p995_block_words", C.c_uint32), ("bvs_pad", C.c_uint32),
                 ("bvs_slices", C.c_uint64), ("bvs_heavy_rows", C.c_uint64), ("bvs_lane_words", C.c_uint64),
                 ("bvs_lane_words_used", C.c_uint64), ("bvs_lane_iters", C.c_uint64),
-                ("bvs_lane_iters_used", C.c_uint64)]
+                ("bvs_lane_iters_used", C.c_uint64), ("bvt_stream_bytes", C.c_uint64), ("bvt_entries", C.c_uint64),
+                ("bvt_far_slots", C.c_uint64), ("bvt_heavy_targets", C.c_uint64), ("bvt_slices", C.c_uint64)]
 
 
 _lib_handle: Optional[C.CDLL] = None
@@ -125,6 +126,8 @@ _SIGS = [
     ("cmvg_layout_blocks", _P, [_P, C.POINTER(C.c_uint32)]),
     ("cmvg_layout_swords", _P, [_P, C.POINTER(C.c_uint64)]),
     ("cmvg_layout_sblocks", _P, [_P, C.POINTER(C.c_uint32)]),
+    ("cmvg_layout_twords", _P, [_P, C.POINTER(C.c_uint64)]),
+    ("cmvg_layout_tblocks", _P, [_P, C.POINTER(C.c_uint32)]),
     ("cmvg_layout_free", None, [_P]),
     ("cmvg_graph_info_get", C.c_int, [_P, C.POINTER(_InfoC)]),
     ("cmvg_dimension", C.c_uint32, [_P]),
@@ -303,17 +306,20 @@ class BvStream:
         _check(load_library().cmvg_layout_info(self._h, C.byref(oc), C.byref(inf)))
         return {f: getattr(inf, f) for f, _ in _InfoC._fields_}
 
-    def layout_export(self, options: Optional["CreateOptions"] = None, sliced: bool = False):
-        """(words u32[], blocks u32[nblocks, 8]) of the device layout (BV-D, or
-        BV-S with sliced=True), built on the host."""
+    def layout_export(self, options: Optional["CreateOptions"] = None, sliced: bool = False, kind: str = ""):
+        """(words u32[], blocks u32[nblocks, 8]) of a device layout built on the
+        host: BV-D (default), BV-S (sliced=True or kind="bvs") or BV-T
+        (kind="bvt")."""
+        kind = kind or ("bvs" if sliced else "bvd")
         oc = (options or CreateOptions())._c()
         h = _P()
         lib = load_library()
         _check(lib.cmvg_layout_export(self._h, C.byref(oc), C.byref(h)))
         try:
             nw, nb = C.c_uint64(), C.c_uint32()
-            fw, fb = (lib.cmvg_layout_swords, lib.cmvg_layout_sblocks) if sliced else \
-                (lib.cmvg_layout_words, lib.cmvg_layout_blocks)
+            fw, fb = {"bvd": (lib.cmvg_layout_words, lib.cmvg_layout_blocks),
+                      "bvs": (lib.cmvg_layout_swords, lib.cmvg_layout_sblocks),
+                      "bvt": (lib.cmvg_layout_twords, lib.cmvg_layout_tblocks)}[kind]
             w = _np_view(fw(h, C.byref(nw)), nw.value, np.uint32).copy()
             b = _np_view(fb(h, C.byref(nb)), nb.value * 8, np.uint32).reshape(-1, 8).copy()
         finally:

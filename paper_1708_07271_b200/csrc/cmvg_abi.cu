@@ -160,6 +160,13 @@ const uint64_t* cmvg_bv_segment_offsets(const cmvg_bvstream* s, uint64_t* count)
 void cmvg_bv_free(cmvg_bvstream* s) { delete s; }
 
 // ---- device handle ----------------------------------------------------------
+static void fill_bvt_info(cmvg_graph_info* o, const BvtStats& t) {
+  o->bvt_stream_bytes = t.stream_bytes;
+  o->bvt_entries = t.entries;
+  o->bvt_far_slots = t.far_slots;
+  o->bvt_heavy_targets = t.heavy_targets;
+  o->bvt_slices = t.slices;
+}
 static void fill_bvs_info(cmvg_graph_info* o, const BvsStats& st, uint32_t cap) {
   o->bvs_stream_bytes = st.stream_bytes;
   o->bvs_max_block_words = st.max_block_words;
@@ -258,6 +265,24 @@ int cmvg_create(const cmvg_bvstream* s, const cmvg_create_opts* opts_in, cmvg_gr
       g->swords.upload(sw.data(), sw.size());
       g->sblocks.upload(sbl.data(), sbl.size());
       g->s_stream_bytes = (s1 - s0) * 4;
+      // BV-T
+      const uint64_t t0 = L.tblocks[g->block_begin].word_offset;
+      const uint64_t t1 = L.tblocks[block_end - 1].word_offset + L.tblocks[block_end - 1].nwords;
+      std::vector<BvdBlockInfo> tbl(L.tblocks.begin() + g->block_begin, L.tblocks.begin() + block_end);
+      for (auto& b : tbl) b.word_offset -= t0;
+      std::vector<uint32_t> tw(L.twords.begin() + t0, L.twords.begin() + t1);
+      tw.resize(tw.size() + 64, 0);
+      g->twords.upload(tw.data(), tw.size());
+      g->tblocks.upload(tbl.data(), tbl.size());
+      g->t_stream_bytes = (t1 - t0) * 4;
+      g->tstats = L.tstats;
+      g->tfar_begin = L.tblocks[g->block_begin].pad[0];
+      g->tfar_end = block_end < L.tblocks.size() ? L.tblocks[block_end].pad[0] : (uint32_t)L.tstats.far_slots;
+      g->tile_ptr.upload(L.tile_ptr.data(), L.tile_ptr.size());
+      g->tile_blk.upload(L.tile_blk.data(), std::max<size_t>(1, L.tile_blk.size()));
+      g->farp_ptr.upload(L.farp_ptr.data(), L.farp_ptr.size());
+      if (L.farp.empty()) L.farp.assign(2, 0u);
+      g->farp.upload(L.farp.data(), L.farp.size());
       g->sstats = L.sstats;
     }
     g->refd.upload(dec.ref_dist.data() + o.row_begin, row_end - o.row_begin);
@@ -309,6 +334,7 @@ int cmvg_layout_info(const cmvg_bvstream* s, const cmvg_create_opts* opts_in, cm
                               : std::min<uint32_t>(12288, std::max<uint32_t>(1024, (L.stats.p995_block_words + 255) & ~255u));
     o->window_coverage = L.stats.window_coverage;
     fill_bvs_info(o, L.sstats, 0);
+    fill_bvt_info(o, L.tstats);
   });
 }
 
@@ -348,6 +374,16 @@ const uint32_t* cmvg_layout_sblocks(const cmvg_layout* l, uint32_t* nblocks) {
   if (nblocks) *nblocks = (uint32_t)l->L.sblocks.size();
   return reinterpret_cast<const uint32_t*>(l->L.sblocks.data());
 }
+const uint32_t* cmvg_layout_twords(const cmvg_layout* l, uint64_t* nwords) {
+  if (!l) return nullptr;
+  if (nwords) *nwords = l->L.twords.size();
+  return l->L.twords.data();
+}
+const uint32_t* cmvg_layout_tblocks(const cmvg_layout* l, uint32_t* nblocks) {
+  if (!l) return nullptr;
+  if (nblocks) *nblocks = (uint32_t)l->L.tblocks.size();
+  return reinterpret_cast<const uint32_t*>(l->L.tblocks.data());
+}
 void cmvg_layout_free(cmvg_layout* l) { delete l; }
 
 int cmvg_destroy(cmvg_graph* g) {
@@ -386,6 +422,8 @@ int cmvg_graph_info_get(const cmvg_graph* g, cmvg_graph_info* o) {
     o->window_coverage = g->stats.window_coverage;
     fill_bvs_info(o, g->sstats, 0);
     o->bvs_stream_bytes = g->s_stream_bytes;
+    fill_bvt_info(o, g->tstats);
+    o->bvt_stream_bytes = g->t_stream_bytes;
   });
 }
 

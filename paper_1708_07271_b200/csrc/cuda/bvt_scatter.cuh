@@ -1,0 +1,288 @@
+// bvt_scatter: y = x A (the left product, reference matvec_ref_left,
+// ref_matvec.hpp:37-41) on A's OWN differential rows, with atomic-free
+// segmented accumulation (layout: BV-T, host/layout.hpp):
+//     x A = sum_k x_k row_k,  row_k = row_{k-r} + plus_k - minus_k
+//         = sum_k c_k (plus_k - minus_k),  c_k = x_k + sum_{j: j - r_j = k} c_j
+// (the paper's Proposition 1 applied to the transposed product).
+//
+// Kernel 1 (one CTA per chain-closed block of B rows, 4 CTAs/SM):
+//   1. coefficients c_k in double-double: reference distances from the
+//      block's ref table, then levels over chain depth, deepest first, each
+//      row pulling its children (rows k+1..k+7 whose reference is k) in a
+//      fixed order -- the reference-chain level scheduler run in reverse;
+//   2. the block's contributions, grouped by target column by the
+//      transcoder, are summed per target with the gather's slice machinery
+//      (one target unit per lane, codes k | minus << 15 read c_k from shared
+//      memory, TwoSum accumulation, segmented shuffle reduction for targets
+//      split over adjacent lanes, whole warps for heavy targets).  Point
+//      targets and interval difference entries land in shared memory, far
+//      targets in the block's far staging slots;
+//   3. the difference entries are prefix-summed (double-double block scan)
+//      and added to the point sums: the block's partial y over its window,
+//      written densely to a staging buffer.
+// Kernel 2 (one CTA per column tile): y_j = the staged partials of the
+// blocks whose window covers j, in block order, plus j's far slots in
+// (column, slot) order -- a fixed order, so results are deterministic.
+// No atomics anywhere (B200's shared-memory fp64 and 64-bit atomics are CAS
+// loops).
+#pragma once
+#include <cstdint>
+
+#include "bvd_common.cuh"
+
+namespace cmvg {
+
+struct BvtSmem {
+  uint32_t off_ch, off_cl, off_oh, off_ol, off_dep, off_ref, off_misc, total;
+};
+
+__host__ __device__ inline BvtSmem bvt_smem_layout(const BvdDims& d) {
+  BvtSmem s;
+  const uint32_t B = d.block_rows, W = d.window;
+  uint32_t o = 0;
+  s.off_ch = o;
+  o = align16(o + (B + 1) * 8);
+  s.off_cl = o;
+  o = align16(o + (B + 1) * 4);
+  s.off_oh = o;
+  o = align16(o + 2 * W * 8);
+  s.off_ol = o;
+  o = align16(o + 2 * W * 4);
+  s.off_dep = o;
+  o = align16(o + B * 2);
+  s.off_ref = o;
+  o = align16(o + B);
+  s.off_misc = o;  // 16 ints + scratch (64 ints)
+  o = align16(o + 64 + 64 * 4);
+  s.total = o;
+  return s;
+}
+
+struct BvtOut {
+  double* st_hi;  // staging: [block][W] partial y over the block's window
+  float* st_lo;
+  double* far_hi;  // far staging slots (global slot numbering)
+  float* far_lo;
+};
+
+__device__ __forceinline__ void bvt_put(uint32_t t, double hi, double lo, uint32_t W2, double* s_oh, float* s_ol,
+                                        const BvtOut& o, uint32_t fbase) {
+  if (t < W2) {
+    s_oh[t] = hi;
+    s_ol[t] = (float)lo;
+  } else {
+    o.far_hi[fbase + t - W2] = hi;
+    o.far_lo[fbase + t - W2] = (float)lo;
+  }
+}
+
+// +(c_hi, c_lo) or -(c_hi, c_lo) of a code k | minus << 15
+__device__ __forceinline__ void bvt_term(uint32_t code, const double* ch, const float* cl, double& acc, double& comp) {
+  const uint32_t k = code & 0x7fffu;
+  const int sg = (int)((code << 16) & 0x80000000u);
+  const double h = ch[k], l = (double)cl[k];
+  tsum(acc, comp, __hiloint2double(__double2hiint(h) ^ sg, __double2loint(h)));
+  comp += __hiloint2double(__double2hiint(l) ^ sg, __double2loint(l));
+}
+
+template <typename XT>
+__global__ void __launch_bounds__(256, 4) bvt_scatter_kernel(BvdDev g, const XT* __restrict__ x, BvtOut out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const BvdDims& D = g.d;
+  const BvtSmem L = bvt_smem_layout(D);
+  const uint32_t T = blockDim.x, tid = threadIdx.x, lane = tid & 31u;
+  const uint32_t bl = blockIdx.x;
+  const uint32_t b = g.block_begin + bl;
+  const BvdBlockInfo bi = g.blocks[bl];
+  const uint32_t B = D.block_rows, W = D.window, W2 = 2u * W;
+  const uint32_t r0 = b * B;
+  const uint32_t nr = min(B, D.n - r0);
+  const uint32_t* __restrict__ bs = g.words + bi.word_offset;
+  double* ch = reinterpret_cast<double*>(smem + L.off_ch);
+  float* cl = reinterpret_cast<float*>(smem + L.off_cl);
+  double* s_oh = reinterpret_cast<double*>(smem + L.off_oh);
+  float* s_ol = reinterpret_cast<float*>(smem + L.off_ol);
+  uint16_t* dep = reinterpret_cast<uint16_t*>(smem + L.off_dep);
+  uint8_t* ref = smem + L.off_ref;
+  int* misc = reinterpret_cast<int*>(smem + L.off_misc);
+  if (tid == 32) bulk_prefetch_l2(bs, bi.nwords * 4u);
+
+  // ---- 1. coefficients ------------------------------------------------------
+  const uint32_t rt = __ldg(bs + 4);
+  for (uint32_t k = tid; k < nr; k += T) {
+    ref[k] = (uint8_t)((__ldg(bs + rt + (k >> 3)) >> (28u - 4u * (k & 7u))) & 15u);
+    ch[k] = (double)__ldg(x + r0 + k);
+    cl[k] = 0.0f;
+  }
+  for (uint32_t k = nr + tid; k <= B; k += T) {  // the zero coefficient (padding code B) and rows past n
+    ch[k] = 0.0;
+    cl[k] = 0.0f;
+  }
+  for (uint32_t j = tid; j < W2; j += T) {
+    s_oh[j] = 0.0;
+    s_ol[j] = 0.0f;
+  }
+  __syncthreads();
+  // depth (chain length) and children mask (bit r-1: row k + r references k)
+  // per row; only rows with children take part in the levels below
+  int dmax = 0;
+  for (uint32_t k = tid; k < nr; k += T) {
+    uint32_t d = 0, j = k;
+    while (ref[j]) {
+      j -= ref[j];
+      ++d;
+    }
+    uint32_t m = 0;
+#pragma unroll
+    for (uint32_t r = 1; r <= 7; ++r)
+      if (k + r < nr && ref[k + r] == r) m |= 1u << (r - 1);
+    dep[k] = (uint16_t)(min(d, 255u) | (m << 8));
+    dmax = max(dmax, m ? (int)d + 1 : 0);
+  }
+  dmax = __reduce_max_sync(0xffffffffu, dmax);
+  if (lane == 0) misc[tid >> 5] = dmax;
+  __syncthreads();
+  dmax = 0;
+  for (uint32_t w = 0; w < (T >> 5); ++w) dmax = max(dmax, misc[w]);
+  for (int d = dmax - 1; d >= 0; --d) {
+    for (uint32_t k = tid; k < nr; k += T) {
+      const uint32_t e = dep[k];
+      uint32_t m = e >> 8;
+      if ((e & 255u) != (uint32_t)d || !m) continue;
+      double h = ch[k], l = (double)cl[k];
+      while (m) {  // children in increasing distance
+        const uint32_t r = (uint32_t)__ffs(m);
+        m &= m - 1u;
+        dd_add(h, l, ch[k + r], (double)cl[k + r]);
+      }
+      ch[k] = h;
+      cl[k] = (float)l;
+    }
+    __syncthreads();
+  }
+
+  // ---- 2. per-target segmented sums ---------------------------------------
+  const uint32_t fbase = bi.pad[0];
+  const uint32_t h0 = __ldg(bs);
+  const uint32_t nsl = h0 & 0xffffu, nh = h0 >> 16;
+  {  // heavy targets: one warp each, fixed lane order
+    const uint32_t htab = __ldg(bs + 1), hcode = __ldg(bs + 2);
+    for (uint32_t q = tid >> 5; q < nh; q += T >> 5) {
+      const uint32_t e = htab + q * kBvtHeavyEntry;
+      const uint32_t t = __ldg(bs + e), ne = __ldg(bs + e + 1), co = hcode + __ldg(bs + e + 2);
+      double acc = 0.0, comp = 0.0;
+      for (uint32_t i = lane; i < ne; i += 32) {
+        const uint32_t w = __ldg(bs + co + (i >> 1));
+        bvt_term((i & 1u) ? (w & 0xffffu) : (w >> 16), ch, cl, acc, comp);
+      }
+      double hi = acc + comp, lo = comp - (hi - acc);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double uh = __shfl_down_sync(0xffffffffu, hi, o), ul = __shfl_down_sync(0xffffffffu, lo, o);
+        dd_add(hi, lo, uh, ul);
+      }
+      if (lane == 0) bvt_put(t, hi, lo, W2, s_oh, s_ol, out, fbase);
+    }
+  }
+  for (uint32_t s = tid >> 5; s < nsl; s += T >> 5) {  // slices, round-robin (sorted by cost)
+    const uint32_t* rec = bs + __ldg(bs + kBvtHead + s);
+    const uint32_t meta = __ldg(rec);
+    const uint32_t h = __ldg(rec + 1u + lane);
+    const uint32_t* body = rec + 33u + lane;
+    const uint32_t mnw = (tmeta_ne(meta) + 1u) >> 1;
+    double acc = 0.0, comp = 0.0, acc2 = 0.0, comp2 = 0.0;
+#pragma unroll 4
+    for (uint32_t q = 0; q < mnw; ++q) {
+      const uint32_t w = __ldg(body + q * 32u);
+      bvt_term(w >> 16, ch, cl, acc, comp);
+      bvt_term(w & 0xffffu, ch, cl, acc2, comp2);
+    }
+    tsum(acc, comp, acc2);
+    comp += comp2;
+    double hi = acc + comp, lo = comp - (hi - acc);
+    if (tmeta_multi(meta)) {
+      const uint32_t heads = __ballot_sync(0xffffffffu, (h >> 30) & 1u);
+      const uint32_t above = heads & ~((2u << lane) - 1u);
+      const uint32_t end = above ? (uint32_t)__ffs(above) - 2u : 31u;
+#pragma unroll
+      for (uint32_t o = 1; o < 32; o <<= 1) {
+        const double uh = __shfl_down_sync(0xffffffffu, hi, o), ul = __shfl_down_sync(0xffffffffu, lo, o);
+        if (lane + o <= end) dd_add(hi, lo, uh, ul);
+      }
+    }
+    if ((h >> 30) == 3u) bvt_put(th_target(h), hi, lo, W2, s_oh, s_ol, out, fbase);
+  }
+  __syncthreads();
+
+  // ---- 3. window partial = point sums + inclusive prefix of the differences
+  // block scan in double-double: per-thread chunk, warp shuffles, warp totals
+  const uint32_t per = (W + T - 1) / T, j0 = min(W, tid * per), j1 = min(W, j0 + per);
+  double th = 0.0, tl = 0.0;
+  for (uint32_t j = j0; j < j1; ++j) dd_add(th, tl, s_oh[W + j], (double)s_ol[W + j]);
+  double ih = th, il = tl;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double uh = __shfl_up_sync(0xffffffffu, ih, o), ul = __shfl_up_sync(0xffffffffu, il, o);
+    if ((int)lane >= o) dd_add(ih, il, uh, ul);
+  }
+  double* wtot = reinterpret_cast<double*>(misc + 16);  // 8 warps x (hi, lo)
+  const uint32_t warp = tid >> 5, nw = T >> 5;
+  if (lane == 31) {
+    wtot[2 * warp] = ih;
+    wtot[2 * warp + 1] = il;
+  }
+  __syncthreads();
+  double eh = __shfl_up_sync(0xffffffffu, ih, 1), el = __shfl_up_sync(0xffffffffu, il, 1);
+  if (lane == 0) eh = el = 0.0;
+  for (uint32_t w = 0; w < warp && w < nw; ++w) dd_add(eh, el, wtot[2 * w], wtot[2 * w + 1]);
+  double* st_hi = out.st_hi + (size_t)bl * W;
+  float* st_lo = out.st_lo + (size_t)bl * W;
+  for (uint32_t j = j0; j < j1; ++j) {
+    dd_add(eh, el, s_oh[W + j], (double)s_ol[W + j]);  // inclusive prefix of the differences at j
+    double a = s_oh[j], c = (double)s_ol[j];
+    dd_add(a, c, eh, el);
+    st_hi[j] = a;
+    st_lo[j] = (float)c;
+  }
+}
+
+// Kernel 2: combine staged partials per column tile, fixed order.
+template <typename YT>
+__global__ void __launch_bounds__(256) bvt_combine_kernel(BvdDev g, const uint32_t* __restrict__ tile_ptr,
+                                                          const uint32_t* __restrict__ tile_blk,
+                                                          const uint32_t* __restrict__ farp_ptr,
+                                                          const uint32_t* __restrict__ farp, BvtOut out,
+                                                          uint32_t nbl, uint32_t fs0, uint32_t fs1,
+                                                          YT* __restrict__ y) {
+  const BvdDims& D = g.d;
+  const uint32_t B = D.block_rows, W = D.window;
+  const uint32_t t = blockIdx.x;
+  const uint32_t c0 = t * B;
+  const uint32_t q0 = tile_ptr[t], q1 = tile_ptr[t + 1];
+  const uint32_t f0 = farp_ptr[t], f1 = farp_ptr[t + 1];
+  for (uint32_t j = threadIdx.x; j < B && c0 + j < D.n; j += blockDim.x) {
+    const uint32_t col = c0 + j;
+    double hi = 0.0, lo = 0.0;
+    for (uint32_t q = q0; q < q1; ++q) {
+      const uint32_t b = tile_blk[q];
+      if (b < g.block_begin || b - g.block_begin >= nbl) continue;  // another shard's block
+      const uint32_t bl = b - g.block_begin;
+      const uint32_t jj = col - g.blocks[bl].wlo;
+      if (jj < W) dd_add(hi, lo, out.st_hi[(size_t)bl * W + jj], (double)out.st_lo[(size_t)bl * W + jj]);
+    }
+    // far slots of this column: pairs sorted by (column, slot)
+    uint32_t lo_i = f0, hi_i = f1;
+    while (lo_i < hi_i) {
+      const uint32_t mid = (lo_i + hi_i) >> 1;
+      if (farp[2 * mid] < col) lo_i = mid + 1;
+      else hi_i = mid;
+    }
+    for (uint32_t p = lo_i; p < f1 && farp[2 * p] == col; ++p) {
+      const uint32_t slot = farp[2 * p + 1];
+      if (slot >= fs0 && slot < fs1) dd_add(hi, lo, out.far_hi[slot], (double)out.far_lo[slot]);
+    }
+    y[col] = (YT)(hi + lo);
+  }
+}
+
+}  // namespace cmvg

@@ -269,6 +269,156 @@ void emit_bvs(const RowParts* rps, const RowMeta* meta, const BitWriter& body, u
   st.heavy_rows += nh;
 }
 
+// BV-T block stream (layout.hpp): A's differential contributions of the block
+// grouped by target column.
+void emit_bvt(const RowParts* rps, const RowMeta* meta, uint32_t nr, uint32_t B, uint64_t wlo, uint32_t W,
+              std::vector<uint32_t>& so, std::vector<uint32_t>& far_cols, BvtStats& st) {
+  constexpr uint32_t kUnit = 16, kMaxUnits = 32;
+  // target -> codes (k | minus << 15)
+  std::vector<std::vector<uint16_t>> tgt(2 * (size_t)W);
+  std::vector<std::pair<uint32_t, uint16_t>> far;  // (column, code)
+  auto point = [&](uint64_t col, uint32_t code) {
+    if (col >= wlo && col < wlo + W) tgt[col - wlo].push_back((uint16_t)code);
+    else far.push_back({(uint32_t)col, (uint16_t)code});
+  };
+  for (uint32_t k = 0; k < nr; ++k) {
+    const RowParts& rp = rps[k];
+    for (uint32_t c : rp.minus) point(c, k | 0x8000u);
+    for (uint32_t c : rp.res) point(c, k);
+    for (const auto& iv : rp.ints) {
+      const uint64_t a = iv.first, e = (uint64_t)iv.first + iv.second;
+      const uint64_t ia = std::max<uint64_t>(a, wlo), ie = std::min<uint64_t>(e, wlo + W);
+      if (ia < ie) {  // in-window part: two difference entries
+        tgt[W + (ia - wlo)].push_back((uint16_t)k);
+        if (ie < wlo + W) tgt[W + (ie - wlo)].push_back((uint16_t)(k | 0x8000u));
+      }
+      for (uint64_t c = a; c < e; ++c)  // out-of-window part: one far entry per column
+        if (c < ia || c >= ie) far.push_back({(uint32_t)c, (uint16_t)k});
+    }
+  }
+  std::sort(far.begin(), far.end());
+  far_cols.clear();
+  struct T {
+    uint32_t target;
+    std::vector<uint16_t> codes;
+  };
+  std::vector<T> targets;
+  for (uint32_t t = 0; t < 2 * W; ++t)
+    if (!tgt[t].empty()) targets.push_back({t, std::move(tgt[t])});
+  for (size_t q = 0; q < far.size();) {
+    size_t e = q;
+    T t{2 * W + (uint32_t)far_cols.size(), {}};
+    while (e < far.size() && far[e].first == far[q].first) t.codes.push_back(far[e++].second);
+    far_cols.push_back(far[q].first);
+    targets.push_back(std::move(t));
+    q = e;
+  }
+  if (2 * W + far_cols.size() > 0x3fffffffu) throw std::runtime_error("BV-T: too many targets in a block");
+  // units: <= kUnit codes, balanced; 1 unit -> single slices, 2..32 -> multi, more -> heavy
+  struct U {
+    uint32_t target;
+    bool primary;
+    std::vector<uint16_t> codes;
+  };
+  std::vector<std::vector<U>> single_rows, multi_rows;
+  std::vector<const T*> heavy;
+  for (const T& t : targets) {
+    const uint32_t ne = (uint32_t)t.codes.size();
+    st.entries += ne;
+    const uint32_t nu = (ne + kUnit - 1) / kUnit;
+    if (nu > kMaxUnits) {
+      heavy.push_back(&t);
+      continue;
+    }
+    std::vector<U> us;
+    for (uint32_t j = 0; j < nu; ++j) {
+      const uint32_t p0 = (uint32_t)((uint64_t)j * ne / nu), p1 = (uint32_t)((uint64_t)(j + 1) * ne / nu);
+      us.push_back(U{t.target, j == 0, std::vector<uint16_t>(t.codes.begin() + p0, t.codes.begin() + p1)});
+    }
+    (nu == 1 ? single_rows : multi_rows).push_back(std::move(us));
+  }
+  struct Slice {
+    std::vector<const U*> lanes;
+    bool multi;
+  };
+  std::vector<Slice> slices;
+  auto load = [](const std::vector<U>& r) {
+    size_t m = 0;
+    for (const U& u : r) m = std::max(m, u.codes.size());
+    return m;
+  };
+  std::stable_sort(multi_rows.begin(), multi_rows.end(), [&](const std::vector<U>& a, const std::vector<U>& b) {
+    if (load(a) != load(b)) return load(a) > load(b);
+    return a.size() > b.size();
+  });
+  for (const auto& r : multi_rows) {
+    size_t t = 0;
+    while (t < slices.size() && slices[t].lanes.size() + r.size() > 32) ++t;
+    if (t == slices.size()) slices.push_back(Slice{{}, true});
+    for (const U& u : r) slices[t].lanes.push_back(&u);
+  }
+  std::stable_sort(single_rows.begin(), single_rows.end(), [&](const std::vector<U>& a, const std::vector<U>& b) {
+    return a[0].codes.size() > b[0].codes.size();
+  });
+  for (size_t a = 0; a < single_rows.size(); a += 32) {
+    Slice sl{{}, false};
+    for (size_t q = a; q < std::min(single_rows.size(), a + 32); ++q) sl.lanes.push_back(&single_rows[q][0]);
+    slices.push_back(std::move(sl));
+  }
+  const uint32_t nsl = (uint32_t)slices.size(), nh = (uint32_t)heavy.size();
+  if (nsl > 0xffffu || nh > 0xffffu) throw std::runtime_error("BV-T: block too large");
+  so.assign(kBvtHead + nsl, 0u);
+  so[0] = nsl | (nh << 16);
+  so[3] = (uint32_t)far_cols.size();
+  so[4] = (uint32_t)so.size();
+  for (uint32_t k = 0; k < nr; k += 8) {
+    uint32_t w = 0;
+    for (uint32_t q = 0; q < 8 && k + q < nr; ++q) w |= (meta[k + q].r & 15u) << (28 - 4 * q);
+    so.push_back(w);
+  }
+  so[5] = (uint32_t)so.size();
+  so.insert(so.end(), far_cols.begin(), far_cols.end());
+  const uint32_t zc = B;  // padding code: the zero coefficient
+  for (uint32_t s = 0; s < nsl; ++s) {
+    const Slice& sl = slices[s];
+    so[kBvtHead + s] = (uint32_t)so.size();
+    uint32_t mne = 0;
+    for (const U* u : sl.lanes) {
+      mne = std::max<uint32_t>(mne, (uint32_t)u->codes.size());
+      st.lane_iters_used += u->codes.size();
+    }
+    so.push_back(make_tmeta(mne, sl.multi));
+    for (size_t l = 0; l < 32; ++l) so.push_back(l < sl.lanes.size() ? make_th(sl.lanes[l]->primary, sl.lanes[l]->target) : 0u);
+    const uint32_t mnw = (mne + 1) / 2;
+    const size_t b0 = so.size();
+    so.resize(b0 + (size_t)mnw * 32, 0u);
+    for (size_t l = 0; l < 32; ++l) {
+      const U* u = l < sl.lanes.size() ? sl.lanes[l] : nullptr;
+      for (uint32_t q = 0; q < mnw; ++q) {
+        const uint32_t c0 = u && 2 * q < u->codes.size() ? u->codes[2 * q] : zc;
+        const uint32_t c1 = u && 2 * q + 1 < u->codes.size() ? u->codes[2 * q + 1] : zc;
+        so[b0 + (size_t)q * 32 + l] = (c0 << 16) | c1;
+      }
+    }
+    st.lane_iters += 32ull * mne;
+  }
+  so[1] = (uint32_t)so.size();
+  std::vector<uint32_t> hc;
+  for (const T* t : heavy) {
+    so.push_back(t->target);
+    so.push_back((uint32_t)t->codes.size());
+    so.push_back((uint32_t)hc.size());
+    for (size_t q = 0; q < t->codes.size(); q += 2)
+      hc.push_back(((uint32_t)t->codes[q] << 16) | (q + 1 < t->codes.size() ? t->codes[q + 1] : zc));
+  }
+  so[2] = (uint32_t)so.size();
+  so.insert(so.end(), hc.begin(), hc.end());
+  while (so.size() % 4) so.push_back(0u);
+  st.slices += nsl;
+  st.heavy_targets += nh;
+  st.far_slots += far_cols.size();
+}
+
 }  // namespace
 
 BvdLayout build_bvd(const BvDecoded& dec, const BvParams& bp, const BvdOptions& opt) {
@@ -294,6 +444,8 @@ BvdLayout build_bvd(const BvDecoded& dec, const BvParams& bp, const BvdOptions& 
   std::vector<uint32_t> bdepth(nb, 0);
   std::vector<std::vector<uint32_t>> sstream(nb);
   std::vector<BvsStats> bst(nb);
+  std::vector<std::vector<uint32_t>> tstream(nb), tfar(nb);
+  std::vector<BvtStats> tst(nb);
   parallel_for(nb, [&](uint64_t b0, uint64_t b1) {
     std::vector<RowParts> rps(B);
     std::vector<uint32_t> plus, cols, depth(B), hdr(B), escs;
@@ -405,6 +557,7 @@ BvdLayout build_bvd(const BvDecoded& dec, const BvParams& bp, const BvdOptions& 
       L.blocks[b].nwords = (uint32_t)(out.nbits / 32);
       L.blocks[b].nesc = (uint32_t)(escs.size() / 4);
       emit_bvs(rps.data(), meta.data(), body, nr, lo, W, bp.min_interval, sstream[b], bst[b]);
+      emit_bvt(rps.data(), meta.data(), nr, B, lo, W, tstream[b], tfar[b], tst[b]);
     }
   });
   uint64_t off = 0, maxw = 0, g_all = 0, g_in = 0;
@@ -461,6 +614,57 @@ BvdLayout build_bvd(const BvDecoded& dec, const BvParams& bp, const BvdOptions& 
         std::memcpy(L.swords.data() + L.sblocks[b].word_offset, sstream[b].data(), sstream[b].size() * 4);
   });
   L.sstats.stream_bytes = soff * 4;
+  // BV-T + combine tables
+  L.tblocks = L.blocks;
+  uint64_t toff = 0, fslot = 0;
+  for (uint32_t b = 0; b < nb; ++b) {
+    L.tblocks[b].word_offset = toff;
+    L.tblocks[b].nwords = (uint32_t)tstream[b].size();
+    L.tblocks[b].nesc = 0;
+    L.tblocks[b].pad[0] = (uint32_t)fslot;
+    toff += tstream[b].size();
+    fslot += tfar[b].size();
+    L.tstats.slices += tst[b].slices;
+    L.tstats.heavy_targets += tst[b].heavy_targets;
+    L.tstats.far_slots += tst[b].far_slots;
+    L.tstats.entries += tst[b].entries;
+    L.tstats.lane_iters += tst[b].lane_iters;
+    L.tstats.lane_iters_used += tst[b].lane_iters_used;
+  }
+  if (fslot > 0xffffffffull) throw std::runtime_error("BV-T: too many far slots");
+  L.twords.assign(toff + 64, 0);
+  parallel_for(nb, [&](uint64_t b0, uint64_t b1) {
+    for (uint64_t b = b0; b < b1; ++b)
+      if (!tstream[b].empty())
+        std::memcpy(L.twords.data() + L.tblocks[b].word_offset, tstream[b].data(), tstream[b].size() * 4);
+  });
+  L.tstats.stream_bytes = toff * 4;
+  {
+    const uint64_t ntiles = nb;  // column tiles of block_rows columns (the matrix is square)
+    std::vector<std::vector<uint32_t>> tb(ntiles);
+    for (uint32_t b = 0; b < nb; ++b) {
+      const uint64_t w0 = L.blocks[b].wlo, w1 = std::min<uint64_t>(g.n, w0 + W);
+      if (w1 <= w0) continue;
+      for (uint64_t t = w0 / B; t <= (w1 - 1) / B && t < ntiles; ++t) tb[t].push_back(b);
+    }
+    L.tile_ptr.assign(ntiles + 1, 0);
+    for (uint64_t t = 0; t < ntiles; ++t) L.tile_ptr[t + 1] = L.tile_ptr[t] + (uint32_t)tb[t].size();
+    L.tile_blk.clear();
+    for (auto& v : tb) L.tile_blk.insert(L.tile_blk.end(), v.begin(), v.end());
+    std::vector<std::pair<uint32_t, uint32_t>> fp;
+    fp.reserve(fslot);
+    for (uint32_t b = 0; b < nb; ++b)
+      for (size_t f = 0; f < tfar[b].size(); ++f) fp.push_back({tfar[b][f], L.tblocks[b].pad[0] + (uint32_t)f});
+    std::sort(fp.begin(), fp.end());
+    L.farp.resize(fp.size() * 2);
+    L.farp_ptr.assign(ntiles + 1, 0);
+    for (size_t q = 0; q < fp.size(); ++q) {
+      L.farp[2 * q] = fp[q].first;
+      L.farp[2 * q + 1] = fp[q].second;
+      L.farp_ptr[fp[q].first / B + 1]++;
+    }
+    for (uint64_t t = 0; t < ntiles; ++t) L.farp_ptr[t + 1] += L.farp_ptr[t];
+  }
   L.stats.block_table_bytes = (uint64_t)nb * sizeof(BvdBlockInfo);
   return L;
 }

@@ -29,6 +29,12 @@ struct BvsStats {
   uint64_t lane_iters = 0, lane_iters_used = 0;  // slice decode iterations x 32 / useful lane iterations
 };
 
+struct BvtStats {
+  uint64_t stream_bytes = 0;
+  uint64_t slices = 0, heavy_targets = 0, far_slots = 0, entries = 0;
+  uint64_t lane_iters = 0, lane_iters_used = 0;
+};
+
 struct BvdLayout {
   BvdDims dims{};
   std::vector<uint32_t> words;
@@ -37,6 +43,13 @@ struct BvdLayout {
   std::vector<uint32_t> swords;
   std::vector<BvdBlockInfo> sblocks;
   BvsStats sstats;
+  // BV-T (target-sorted scatter stream) + the combine tables
+  std::vector<uint32_t> twords;
+  std::vector<BvdBlockInfo> tblocks;  // pad[0] = first far staging slot
+  BvtStats tstats;
+  std::vector<uint32_t> tile_ptr, tile_blk;  // per 'block_rows' column tile: blocks whose window meets it
+  std::vector<uint32_t> farp_ptr;            // per tile: range in farp
+  std::vector<uint32_t> farp;                // (column, far slot) pairs sorted by column
   uint64_t adds_per_product = 0;
   BvdStats stats;
 };

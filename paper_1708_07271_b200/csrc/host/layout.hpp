@@ -139,6 +139,44 @@ __host__ __device__ constexpr bool smeta_c32(uint32_t m) { return (m >> 8) & 1u;
 __host__ __device__ constexpr bool smeta_far(uint32_t m) { return (m >> 9) & 1u; }
 __host__ __device__ constexpr bool smeta_multi(uint32_t m) { return (m >> 10) & 1u; }
 
+// ---------------------------------------------------------------------------
+// BV-T: the scatter form's stream (y = x A on A's own compression).  Per block
+// the transcoder groups A's differential contributions by TARGET column: row
+// k contributes -c_k at each minus column, +c_k at each residual column, and
+// an interval [a, a + len) becomes two difference entries (+c_k at a, -c_k at
+// a + len) whose running sum covers the run, where c_k = x_k + sum of c over
+// the rows that reference k (Proposition 1 applied to x A).  A target's
+// segment is then summed with the gather's slice machinery -- no atomics:
+//   targets t < W            point sums at window column wlo + t
+//           W <= t < 2W      difference entries at window column wlo + t - W
+//           2W <= t          far column far[t - 2W] (outside the window)
+//   codes: 16-bit k | minus << 15 (k = block row; k = B reads a zero
+//          coefficient -- the padding code), two per word, rectangular slices
+// Block stream (u32 words):
+//   [0] nslices | nheavy << 16  [1] heavy table offset  [2] heavy code offset
+//   [3] nfar  [4] ref table offset  [5] far column list offset  [6, 7] 0
+//   [8, 8 + nslices) slice record offsets
+//   ref table: r_k in 4 bits, word k / 8, bits 28 - 4 (k % 8)
+//   far list: nfar absolute columns, ascending
+//   slice record: [meta][header x 32][body: ceil(max entries / 2) words x 32]
+//     meta: max entries | multi << 10
+//     header: valid << 31 | primary << 30 | target
+//   heavy table: 3 words per heavy target: target, #entries, code word offset
+//   heavy codes: 16-bit codes, two per word
+// Block table entry: word_offset, nwords, wlo as BV-D; pad[0] = first far
+// staging slot of the block.
+constexpr uint32_t kBvtHead = 8;
+constexpr uint32_t kBvtHeavyEntry = 3;
+__host__ __device__ constexpr uint32_t make_th(bool primary, uint32_t target) {
+  return (1u << 31) | ((primary ? 1u : 0u) << 30) | target;
+}
+__host__ __device__ constexpr uint32_t th_target(uint32_t h) { return h & 0x3fffffffu; }
+__host__ __device__ constexpr uint32_t make_tmeta(uint32_t max_ne, bool multi) {
+  return max_ne | ((multi ? 1u : 0u) << 10);
+}
+__host__ __device__ constexpr uint32_t tmeta_ne(uint32_t m) { return m & 1023u; }
+__host__ __device__ constexpr bool tmeta_multi(uint32_t m) { return (m >> 10) & 1u; }
+
 struct BvdBlockInfo {
   uint64_t word_offset;  // first u32 word of this block's stream (16-byte aligned)
   uint32_t nwords;       // words in this block's stream (multiple of 4)

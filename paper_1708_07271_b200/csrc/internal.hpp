@@ -143,6 +143,11 @@ struct cmvg_graph {
   // BV-S layout (this shard): gather, PageRank
   DevBuf swords, sblocks;
   uint64_t s_stream_bytes = 0;
+  // BV-T layout (this shard): scatter; combine tables (whole graph)
+  DevBuf twords, tblocks, tile_ptr, tile_blk, farp_ptr, farp;
+  uint32_t tfar_begin = 0, tfar_end = 0;
+  uint64_t t_stream_bytes = 0;
+  BvtStats tstats;
   BvsStats sstats;
   // canonical BV stream (whole graph) for decode_csr
   DevBuf bv_words, bv_seg;
@@ -155,7 +160,8 @@ struct cmvg_graph {
   // scratch (scatter / pagerank)
   DevBuf scratch;
   uint64_t device_bytes() const {
-    return words.bytes + blocks.bytes + swords.bytes + sblocks.bytes + bv_words.bytes + bv_seg.bytes + refd.bytes;
+    return words.bytes + blocks.bytes + swords.bytes + sblocks.bytes + twords.bytes + tblocks.bytes + tile_ptr.bytes +
+           tile_blk.bytes + farp_ptr.bytes + farp.bytes + bv_words.bytes + bv_seg.bytes + refd.bytes;
   }
   BvdDev dev() const {
     BvdDev d{};
@@ -165,6 +171,13 @@ struct cmvg_graph {
     d.block_begin = block_begin;
     d.row_begin = row_begin;
     d.stream_cap_words = stream_cap_words;
+    return d;
+  }
+  BvdDev tdev() const {
+    BvdDev d = dev();
+    d.words = twords.as<uint32_t>();
+    d.blocks = tblocks.as<BvdBlockInfo>();
+    d.stream_cap_words = 0;
     return d;
   }
   BvdDev sdev() const {

@@ -1,22 +1,35 @@
-// Scatter-form launch (y = x A on A's own compression).
-#include "cuda/bvd_scatter.cuh"
+// Scatter-form launch (y = x A on A's own compression): BV-T segmented sums
+// per block, then the deterministic combine (cuda/bvt_scatter.cuh).
+#include "cuda/bvt_scatter.cuh"
 #include "internal.hpp"
 
 namespace cmvg {
 
 template <typename T>
 void launch_scatter(cmvg_graph* g, const T* x, T* y, cudaStream_t st) {
-  const size_t n = g->n;
-  g->scratch.alloc(2 * n * sizeof(double) + 64);
-  double* hi = g->scratch.as<double>();
-  double* lo = hi + n;
-  CUDA_TRY(cudaMemsetAsync(hi, 0, 2 * n * sizeof(double), st));
-  const ScatterSmem L = scatter_smem_layout(g->dims, g->stream_cap_words);
-  auto kern = bvd_scatter_kernel<T>;
-  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
-  kern<<<g->nblocks, g->threads, L.total, st>>>(g->dev(), x, hi, lo);
+  const size_t W = g->dims.window;
+  const size_t nst = (size_t)g->nblocks * W;
+  const size_t nfar = (size_t)g->tfar_end - g->tfar_begin;
+  // staging: partial windows (hi f64 + lo f32) and the shard's far slots
+  const size_t bytes = nst * 12 + nfar * 12 + 256;
+  g->scratch.alloc(bytes);
+  unsigned char* p = g->scratch.as<unsigned char>();
+  BvtOut o;
+  o.st_hi = reinterpret_cast<double*>(p);
+  o.far_hi = o.st_hi + nst;
+  o.st_lo = reinterpret_cast<float*>(o.far_hi + nfar);
+  o.far_lo = o.st_lo + nst;
+  o.far_hi -= g->tfar_begin;  // indexed by global far slot
+  o.far_lo -= g->tfar_begin;
+  const BvtSmem L = bvt_smem_layout(g->dims);
+  auto k1 = bvt_scatter_kernel<T>;
+  CUDA_TRY(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
+  k1<<<g->nblocks, g->threads, L.total, st>>>(g->tdev(), x, o);
   CUDA_TRY(cudaGetLastError());
-  dd_round_kernel<T><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(hi, lo, y, (uint32_t)n);
+  const uint32_t ntiles = g->dims.nblocks;
+  bvt_combine_kernel<T><<<ntiles, 256, 0, st>>>(g->tdev(), g->tile_ptr.as<uint32_t>(), g->tile_blk.as<uint32_t>(),
+                                                g->farp_ptr.as<uint32_t>(), g->farp.as<uint32_t>(), o, g->nblocks,
+                                                g->tfar_begin, g->tfar_end, y);
   CUDA_TRY(cudaGetLastError());
 }
 

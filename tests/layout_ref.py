@@ -211,3 +211,74 @@ def decode_sliced(words, blocks, n, B, lmin, W):
             rows_out[i] = sorted(row)
             refs_out[i] = p["r"]
     return refs_out, rows_out
+
+
+# ---------------------------------------------------------------------------
+# BV-T (target-sorted scatter layout; host/layout.hpp, cuda/bvt_scatter.cuh)
+def scatter_bvt_int(words, blocks, n, B, W, x):
+    """y = x A evaluated from the BV-T layout exactly as the two scatter kernels
+    do, in integer arithmetic (x integer): coefficients c_k from the ref table,
+    per-target segmented sums of the 16-bit codes, inclusive prefix of the
+    difference targets, far slots, then the window combine.  Also checks the
+    structural invariants (one primary per target, slice metadata)."""
+    x = np.asarray(x, dtype=np.int64)
+    y = np.zeros(n, dtype=np.int64)
+    for b in range(len(blocks)):
+        woff = int(blocks[b, 0]) | (int(blocks[b, 1]) << 32)
+        nw = int(blocks[b, 2])
+        wlo = int(blocks[b, 3])
+        s = [int(v) for v in words[woff:woff + nw + 64]]
+        r0 = b * B
+        nr = min(B, n - r0)
+        nsl, nh = s[0] & 0xFFFF, s[0] >> 16
+        htab, hcode, nfar, rt, fl = s[1], s[2], s[3], s[4], s[5]
+        ref = [(s[rt + k // 8] >> (28 - 4 * (k % 8))) & 15 for k in range(nr)]
+        c = [int(x[r0 + k]) for k in range(nr)] + [0] * (B + 1 - nr)
+        for k in range(nr - 1, -1, -1):  # children have larger indices
+            if ref[k]:
+                c[k - ref[k]] += c[k]
+        far_cols = s[fl:fl + nfar]
+        assert far_cols == sorted(far_cols) and len(set(far_cols)) == nfar
+        assert all(not (wlo <= col < wlo + W) for col in far_cols)
+        out = {}
+
+        def term(code):
+            return -c[code & 0x7FFF] if code >> 15 else c[code & 0x7FFF]
+        for q in range(nh):
+            t, ne, co = s[htab + 3 * q], s[htab + 3 * q + 1], hcode + s[htab + 3 * q + 2]
+            assert ne > 512 and t not in out
+            tot = 0
+            for i in range(ne):
+                w = s[co + i // 2]
+                tot += term((w & 0xFFFF) if i & 1 else (w >> 16))
+            out[t] = tot
+        cur = None
+        for sl in range(nsl):
+            rec = s[8 + sl]
+            meta = s[rec]
+            mne, multi = meta & 1023, (meta >> 10) & 1
+            mnw = (mne + 1) >> 1
+            for lane in range(32):
+                h = s[rec + 1 + lane]
+                if not h >> 31:
+                    continue
+                prim, t = (h >> 30) & 1, h & 0x3FFFFFFF
+                tot = 0
+                for q in range(mnw):
+                    w = s[rec + 33 + lane + 32 * q]
+                    tot += term(w >> 16) + term(w & 0xFFFF)
+                if prim:
+                    assert t not in out
+                    out[t] = tot
+                    cur = t
+                else:
+                    assert multi and t == cur
+                    out[cur] += tot
+        run = 0
+        for j in range(W):
+            run += out.get(W + j, 0)
+            if wlo + j < n:
+                y[wlo + j] += out.get(j, 0) + run
+        for f, col in enumerate(far_cols):
+            y[col] += out.get(2 * W + f, 0)
+    return y

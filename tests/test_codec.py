@@ -10,7 +10,7 @@ import pytest
 
 import paper_1708_07271_b200 as P
 from tests.helpers import CONFIGS, bv_params, csr_from_rows, make_graph
-from tests.layout_ref import decode_layout, decode_sliced
+from tests.layout_ref import decode_layout, decode_sliced, scatter_bvt_int
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -165,3 +165,32 @@ def test_sliced_layout_multi_and_heavy_rows():
     assert got == rows
     info = s.layout_info()
     assert info["bvs_heavy_rows"] > 0
+
+
+@pytest.mark.parametrize("cfg,n,window", [(1, 5000, 1536), (2, 9000, 1536), (4, 3000, 1536), (2, 4000, 256)])
+def test_target_layout_scatter_exact(cfg, n, window):
+    g = make_graph(cfg, n=n)
+    s = P.BvStream.encode(g, bv_params(cfg))
+    words, blocks = s.layout_export(P.CreateOptions(block_rows=1024, window=window), kind="bvt")
+    x = np.random.default_rng(3).integers(0, 1000, g.n)
+    want = np.zeros(g.n, dtype=np.int64)
+    ro, co = g.row_offsets, g.columns
+    for i in range(g.n):
+        want[co[ro[i]:ro[i + 1]]] += x[i]
+    assert np.array_equal(scatter_bvt_int(words, blocks, g.n, 1024, window, x), want)
+
+
+def test_target_layout_heavy_targets():
+    # no references (w = 0): every row hits column 7 -> > 512 entries per block
+    rng = np.random.default_rng(11)
+    n = 3000
+    rows = [sorted({7} | set(rng.integers(0, n, 3).tolist())) for _ in range(n)]
+    g = csr_from_rows(rows)
+    s = P.BvStream.encode(g, P.BvParams(window=0))
+    assert s.layout_info()["bvt_heavy_targets"] > 0
+    words, blocks = s.layout_export(kind="bvt")
+    x = rng.integers(0, 1000, n)
+    want = np.zeros(n, dtype=np.int64)
+    for i, r in enumerate(rows):
+        want[r] += x[i]
+    assert np.array_equal(scatter_bvt_int(words, blocks, n, 1024, 1536, x), want)

@@ -41,6 +41,35 @@ def test_scatter_device_and_edge_cases(cuda):
     assert max_rel_err(y, oracle_left(g, x)) <= 1e-12
 
 
+@pytest.mark.parametrize("dtype,tol", [(np.float64, 1e-12), (np.float32, 1e-5)])
+def test_scatter_heavy_and_split_targets_deterministic(cuda, dtype, tol):
+    # a hub column hit by every row of a block (> 512 contributions: a
+    # warp-wide heavy target), columns split over adjacent lanes, long rows
+    # with far targets, intervals crossing the window edge; the result must be
+    # bit-identical across runs (fixed-order segmented sums, no atomics)
+    rng = np.random.default_rng(11)
+    n = 5000
+
+    def row(k):
+        r = {7} | set(rng.integers(0, n, 3).tolist())
+        if k % 97 == 0:
+            r |= set(rng.integers(0, n, 700).tolist())
+        if k % 13 == 0:
+            a = int(rng.integers(0, n - 600))
+            r |= set(range(a, a + 500))
+        return sorted(r)
+    g = csr_from_rows([row(k) for k in range(n)])
+    x = x_uniform(g.n, 3).astype(dtype)
+    for params in (P.BvParams(), P.BvParams(window=0)):  # window 0: no references, heavy targets
+        s = P.BvStream.encode(g, params)
+        dg = P.BvGraph(s)
+        y1 = dg.matvec(x, form="scatter")
+        y2 = dg.matvec(x, form="scatter")
+        assert np.array_equal(y1.view(np.uint8), y2.view(np.uint8))
+        assert max_rel_err(y1, oracle_left(g, x)) <= tol
+    assert s.layout_info()["bvt_heavy_targets"] > 0
+
+
 def test_scatter_shards_sum(cuda):
     g = make_graph(2, n=(1 << 15) + 10)
     s = P.BvStream.encode(g, bv_params(2))
