@@ -6,10 +6,11 @@
 // (the paper's Proposition 1 applied to the transposed product).
 //
 // Kernel 1 (one CTA per chain-closed block of B rows, 4 CTAs/SM):
-//   1. coefficients c_k in double-double: reference distances from the
-//      block's ref table, then levels over chain depth, deepest first, each
-//      row pulling its children (rows k+1..k+7 whose reference is k) in a
-//      fixed order -- the reference-chain level scheduler run in reverse;
+//   1. coefficients c_k in double-double by the reference-chain level
+//      scheduler run in reverse: the transcoder lists, per chain depth
+//      (deepest first), the rows with children and their children masks;
+//      each level is one barrier-separated data-parallel step in which a row
+//      pulls its children (rows k+1..k+7 referencing it) in a fixed order;
 //   2. the block's contributions, grouped by target column by the
 //      transcoder, are summed per target with the gather's slice machinery
 //      (one target unit per lane, codes k | minus << 15 read c_k from shared
@@ -33,7 +34,7 @@
 namespace cmvg {
 
 struct BvtSmem {
-  uint32_t off_ch, off_cl, off_oh, off_ol, off_dep, off_ref, off_misc, total;
+  uint32_t off_ch, off_cl, off_oh, off_ol, off_misc, total;
 };
 
 __host__ __device__ inline BvtSmem bvt_smem_layout(const BvdDims& d) {
@@ -48,10 +49,6 @@ __host__ __device__ inline BvtSmem bvt_smem_layout(const BvdDims& d) {
   o = align16(o + 2 * W * 8);
   s.off_ol = o;
   o = align16(o + 2 * W * 4);
-  s.off_dep = o;
-  o = align16(o + B * 2);
-  s.off_ref = o;
-  o = align16(o + B);
   s.off_misc = o;  // 16 ints + scratch (64 ints)
   o = align16(o + 64 + 64 * 4);
   s.total = o;
@@ -102,15 +99,11 @@ __global__ void __launch_bounds__(256, 4) bvt_scatter_kernel(BvdDev g, const XT*
   float* cl = reinterpret_cast<float*>(smem + L.off_cl);
   double* s_oh = reinterpret_cast<double*>(smem + L.off_oh);
   float* s_ol = reinterpret_cast<float*>(smem + L.off_ol);
-  uint16_t* dep = reinterpret_cast<uint16_t*>(smem + L.off_dep);
-  uint8_t* ref = smem + L.off_ref;
   int* misc = reinterpret_cast<int*>(smem + L.off_misc);
   if (tid == 32) bulk_prefetch_l2(bs, bi.nwords * 4u);
 
   // ---- 1. coefficients ------------------------------------------------------
-  const uint32_t rt = __ldg(bs + 4);
   for (uint32_t k = tid; k < nr; k += T) {
-    ref[k] = (uint8_t)((__ldg(bs + rt + (k >> 3)) >> (28u - 4u * (k & 7u))) & 15u);
     ch[k] = (double)__ldg(x + r0 + k);
     cl[k] = 0.0f;
   }
@@ -123,42 +116,28 @@ __global__ void __launch_bounds__(256, 4) bvt_scatter_kernel(BvdDev g, const XT*
     s_ol[j] = 0.0f;
   }
   __syncthreads();
-  // depth (chain length) and children mask (bit r-1: row k + r references k)
-  // per row; only rows with children take part in the levels below
-  int dmax = 0;
-  for (uint32_t k = tid; k < nr; k += T) {
-    uint32_t d = 0, j = k;
-    while (ref[j]) {
-      j -= ref[j];
-      ++d;
-    }
-    uint32_t m = 0;
-#pragma unroll
-    for (uint32_t r = 1; r <= 7; ++r)
-      if (k + r < nr && ref[k + r] == r) m |= 1u << (r - 1);
-    dep[k] = (uint16_t)(min(d, 255u) | (m << 8));
-    dmax = max(dmax, m ? (int)d + 1 : 0);
-  }
-  dmax = __reduce_max_sync(0xffffffffu, dmax);
-  if (lane == 0) misc[tid >> 5] = dmax;
-  __syncthreads();
-  dmax = 0;
-  for (uint32_t w = 0; w < (T >> 5); ++w) dmax = max(dmax, misc[w]);
-  for (int d = dmax - 1; d >= 0; --d) {
-    for (uint32_t k = tid; k < nr; k += T) {
-      const uint32_t e = dep[k];
-      uint32_t m = e >> 8;
-      if ((e & 255u) != (uint32_t)d || !m) continue;
-      double h = ch[k], l = (double)cl[k];
-      while (m) {  // children in increasing distance
-        const uint32_t r = (uint32_t)__ffs(m);
-        m &= m - 1u;
-        dd_add(h, l, ch[k + r], (double)cl[k + r]);
+  {  // the transcoder's schedule: per level (deepest first) the rows with
+     // children; each pulls its children's c in increasing distance
+    const uint32_t* cs = bs + __ldg(bs + 4);
+    const uint32_t nlev = __ldg(cs);
+    const uint32_t* ent = cs + nlev + 2;
+    for (uint32_t lv = 0; lv < nlev; ++lv) {
+      const uint32_t e0 = __ldg(cs + 1 + lv), e1 = __ldg(cs + 2 + lv);
+      for (uint32_t i = e0 + tid; i < e1; i += T) {
+        const uint32_t e = __ldg(ent + i);
+        const uint32_t k = e & 1023u;
+        uint32_t m = e >> 10;
+        double h = ch[k], l = (double)cl[k];
+        while (m) {
+          const uint32_t r = (uint32_t)__ffs(m);
+          m &= m - 1u;
+          dd_add(h, l, ch[k + r], (double)cl[k + r]);
+        }
+        ch[k] = h;
+        cl[k] = (float)l;
       }
-      ch[k] = h;
-      cl[k] = (float)l;
+      __syncthreads();
     }
-    __syncthreads();
   }
 
   // ---- 2. per-target segmented sums ---------------------------------------

@@ -370,11 +370,32 @@ void emit_bvt(const RowParts* rps, const RowMeta* meta, uint32_t nr, uint32_t B,
   so.assign(kBvtHead + nsl, 0u);
   so[0] = nsl | (nh << 16);
   so[3] = (uint32_t)far_cols.size();
+  // coefficient schedule: rows with children, deepest level first, each
+  // entry k | children mask << 10 (bit r-1: row k + r references k)
   so[4] = (uint32_t)so.size();
-  for (uint32_t k = 0; k < nr; k += 8) {
-    uint32_t w = 0;
-    for (uint32_t q = 0; q < 8 && k + q < nr; ++q) w |= (meta[k + q].r & 15u) << (28 - 4 * q);
-    so.push_back(w);
+  {
+    std::vector<uint32_t> dep(nr), mask(nr, 0);
+    uint32_t dmax = 0;
+    for (uint32_t k = 0; k < nr; ++k) {
+      const uint32_t r = meta[k].r;
+      dep[k] = r ? dep[k - r] + 1 : 0;
+      if (r) mask[k - r] |= 1u << (r - 1);
+    }
+    std::vector<std::vector<uint32_t>> lv;
+    for (uint32_t k = 0; k < nr; ++k)
+      if (mask[k]) {
+        if (dep[k] >= lv.size()) lv.resize(dep[k] + 1);
+        lv[dep[k]].push_back(k | (mask[k] << 10));
+        dmax = std::max(dmax, dep[k] + 1);
+      }
+    so.push_back(dmax);
+    uint32_t acc = 0;
+    for (uint32_t d = dmax; d-- > 0;) {  // level starts, processing order
+      so.push_back(acc);
+      acc += (uint32_t)lv[d].size();
+    }
+    so.push_back(acc);
+    for (uint32_t d = dmax; d-- > 0;) so.insert(so.end(), lv[d].begin(), lv[d].end());
   }
   so[5] = (uint32_t)so.size();
   so.insert(so.end(), far_cols.begin(), far_cols.end());

@@ -154,9 +154,11 @@ __host__ __device__ constexpr bool smeta_multi(uint32_t m) { return (m >> 10) & 
 //          coefficient -- the padding code), two per word, rectangular slices
 // Block stream (u32 words):
 //   [0] nslices | nheavy << 16  [1] heavy table offset  [2] heavy code offset
-//   [3] nfar  [4] ref table offset  [5] far column list offset  [6, 7] 0
-//   [8, 8 + nslices) slice record offsets
-//   ref table: r_k in 4 bits, word k / 8, bits 28 - 4 (k % 8)
+//   [3] nfar  [4] coefficient schedule offset  [5] far column list offset
+//   [6, 7] 0  [8, 8 + nslices) slice record offsets
+//   coefficient schedule: [nlev][nlev + 1 level starts][entries]; levels
+//     deepest first, entry = k | children mask << 10 (bit r-1: row k + r
+//     references k), rows without children omitted
 //   far list: nfar absolute columns, ascending
 //   slice record: [meta][header x 32][body: ceil(max entries / 2) words x 32]
 //     meta: max entries | multi << 10

@@ -231,12 +231,18 @@ def scatter_bvt_int(words, blocks, n, B, W, x):
         r0 = b * B
         nr = min(B, n - r0)
         nsl, nh = s[0] & 0xFFFF, s[0] >> 16
-        htab, hcode, nfar, rt, fl = s[1], s[2], s[3], s[4], s[5]
-        ref = [(s[rt + k // 8] >> (28 - 4 * (k % 8))) & 15 for k in range(nr)]
+        htab, hcode, nfar, cs, fl = s[1], s[2], s[3], s[4], s[5]
         c = [int(x[r0 + k]) for k in range(nr)] + [0] * (B + 1 - nr)
-        for k in range(nr - 1, -1, -1):  # children have larger indices
-            if ref[k]:
-                c[k - ref[k]] += c[k]
+        nlev = s[cs]
+        starts = s[cs + 1:cs + nlev + 2]
+        ent = cs + nlev + 2
+        for lv in range(nlev):  # deepest level first; rows pull their children
+            for i in range(starts[lv], starts[lv + 1]):
+                e = s[ent + i]
+                k, m = e & 1023, e >> 10
+                for r in range(1, 8):
+                    if m >> (r - 1) & 1:
+                        c[k] += c[k + r]
         far_cols = s[fl:fl + nfar]
         assert far_cols == sorted(far_cols) and len(set(far_cols)) == nfar
         assert all(not (wlo <= col < wlo + W) for col in far_cols)
