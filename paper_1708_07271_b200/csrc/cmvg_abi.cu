@@ -251,10 +251,7 @@ int cmvg_create(const cmvg_bvstream* s, const cmvg_create_opts* opts_in, cmvg_gr
     uint64_t w1 = L.blocks[block_end - 1].word_offset + L.blocks[block_end - 1].nwords;
     std::vector<BvdBlockInfo> bl(L.blocks.begin() + g->block_begin, L.blocks.begin() + block_end);
     for (auto& b : bl) b.word_offset -= w0;
-    std::vector<uint32_t> wds(L.words.begin() + w0, L.words.begin() + w1);
-    wds.resize(wds.size() + 8, 0);
-    g->words.upload(wds.data(), wds.size());
-    g->blocks.upload(bl.data(), bl.size());
+    (void)bl;  // BV-D stays on the host (layout export); the kernels read BV-S / BV-T
     {
       const uint64_t s0 = L.sblocks[g->block_begin].word_offset;
       const uint64_t s1 = L.sblocks[block_end - 1].word_offset + L.sblocks[block_end - 1].nwords;
@@ -265,6 +262,12 @@ int cmvg_create(const cmvg_bvstream* s, const cmvg_create_opts* opts_in, cmvg_gr
       g->swords.upload(sw.data(), sw.size());
       g->sblocks.upload(sbl.data(), sbl.size());
       g->s_stream_bytes = (s1 - s0) * 4;
+      g->win_need.resize(sbl.size());
+      uint64_t pm = 0;
+      for (size_t q = 0; q < sbl.size(); ++q) {
+        pm = std::max<uint64_t>(pm, (uint64_t)sbl[q].wlo + L.dims.window);
+        g->win_need[q] = (uint32_t)std::min<uint64_t>(pm, bs.n);
+      }
       // BV-T
       const uint64_t t0 = L.tblocks[g->block_begin].word_offset;
       const uint64_t t1 = L.tblocks[block_end - 1].word_offset + L.tblocks[block_end - 1].nwords;
@@ -285,7 +288,6 @@ int cmvg_create(const cmvg_bvstream* s, const cmvg_create_opts* opts_in, cmvg_gr
       g->farp.upload(L.farp.data(), L.farp.size());
       g->sstats = L.sstats;
     }
-    g->refd.upload(dec.ref_dist.data() + o.row_begin, row_end - o.row_begin);
     // stats of the shard
     g->stats.stream_bytes = (w1 - w0) * 4;
     g->stats.block_table_bytes = (uint64_t)g->nblocks * sizeof(BvdBlockInfo);
@@ -437,12 +439,66 @@ uint64_t cmvg_adds_per_product(const cmvg_graph* g) { return g ? g->adds : 0; }
 namespace {
 
 template <typename XT, typename YT>
-void launch_gather(cmvg_graph* g, const XT* x, YT* y, cudaStream_t st) {
+void launch_gather(cmvg_graph* g, const XT* x, YT* y, cudaStream_t st, const XT* xfar = nullptr,
+                   uint32_t b0 = 0, uint32_t b1 = 0xffffffffu) {
+  b1 = std::min(b1, g->nblocks);
+  if (b0 >= b1) return;
   const BvsSmem L = bvs_smem_layout(g->dims, sizeof(XT));
   auto kern = bvs_gather_kernel<XT, YT>;
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
-  kern<<<g->nblocks, g->threads, L.total, st>>>(g->sdev(), x, y, PrArgs{});
+  BvdDev d = g->sdev();
+  d.blocks += b0;  // blocks [b0, b1) of this shard
+  d.block_begin += b0;
+  kern<<<b1 - b0, g->threads, L.total, st>>>(d, x, xfar ? xfar : x, y, PrArgs{});
   CUDA_TRY(cudaGetLastError());
+}
+
+// Mapped device address of a pinned host buffer, or nullptr (pageable memory).
+const void* mapped_host(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return nullptr;
+  }
+  return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
+}
+
+// Pipelined host-pointer gather (pinned x and y): x is uploaded in chunks in
+// row order; blocks run as soon as their x-window has arrived, reading the
+// rare columns outside the window (`far`) straight from the mapped host x;
+// each chunk's y rows go back while later chunks upload -- H2D, compute and
+// D2H overlap across chunks (PCIe is full duplex).
+template <typename T>
+void gather_host_pipelined(cmvg_graph* g, const T* x, T* y, const T* xmapped) {
+  const uint32_t nb = g->nblocks, B = g->dims.block_rows;
+  const uint32_t C = std::min<uint32_t>(16, nb);
+  if (!g->s_in) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&g->s_in, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&g->s_comp, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&g->s_out, cudaStreamNonBlocking));
+    for (int i = 0; i < 32; ++i) CUDA_TRY(cudaEventCreateWithFlags(&g->ev[i], cudaEventDisableTiming));
+  }
+  const size_t nrows = (size_t)g->row_end - g->row_begin;
+  T* hx = g->hx.as<T>();
+  T* hy = g->hy.as<T>();
+  size_t xdone = 0;
+  for (uint32_t c = 0; c < C; ++c) {
+    const uint32_t b0 = (uint32_t)((uint64_t)nb * c / C), b1 = (uint32_t)((uint64_t)nb * (c + 1) / C);
+    // x needed by blocks < b1: their windows (prefix max), everything for the last chunk
+    size_t need = c + 1 == C ? g->n : std::min<size_t>(g->n, g->win_need[b1 - 1]);
+    if (need > xdone) {
+      CUDA_TRY(cudaMemcpyAsync(hx + xdone, x + xdone, (need - xdone) * sizeof(T), cudaMemcpyHostToDevice, g->s_in));
+      xdone = need;
+    }
+    CUDA_TRY(cudaEventRecord(g->ev[2 * c], g->s_in));
+    CUDA_TRY(cudaStreamWaitEvent(g->s_comp, g->ev[2 * c], 0));
+    launch_gather<T, T>(g, hx, hy, g->s_comp, xmapped, b0, b1);
+    CUDA_TRY(cudaEventRecord(g->ev[2 * c + 1], g->s_comp));
+    CUDA_TRY(cudaStreamWaitEvent(g->s_out, g->ev[2 * c + 1], 0));
+    const size_t r0 = (size_t)b0 * B, r1 = std::min(nrows, (size_t)b1 * B);
+    CUDA_TRY(cudaMemcpyAsync(y + r0, hy + r0, (r1 - r0) * sizeof(T), cudaMemcpyDeviceToHost, g->s_out));
+  }
+  CUDA_TRY(cudaStreamSynchronize(g->s_out));
 }
 
 template <typename T>
@@ -467,6 +523,14 @@ int matvec_impl(cmvg_graph* g, const T* x, T* y, int form, int ptr_kind, void* s
     std::lock_guard<std::mutex> lk(g->host_mu);
     g->hx.alloc(nin * sizeof(T) + 64);
     g->hy.alloc(nout * sizeof(T) + 64);
+    if (form == CMVG_GATHER) {
+      const T* xm = static_cast<const T*>(mapped_host(x));
+      if (xm && mapped_host(y)) {
+        if (st) CUDA_TRY(cudaStreamSynchronize(st));  // the caller's prior work on x / y
+        gather_host_pipelined<T>(g, x, y, xm);
+        return;
+      }
+    }
     CUDA_TRY(cudaMemcpyAsync(g->hx.p, x, nin * sizeof(T), cudaMemcpyHostToDevice, st));
     run(g->hx.as<T>(), g->hy.as<T>());
     CUDA_TRY(cudaMemcpyAsync(y, g->hy.p, nout * sizeof(T), cudaMemcpyDeviceToHost, st));

@@ -193,31 +193,45 @@ __device__ __forceinline__ void bvs_slices(const uint32_t* __restrict__ bs, cons
         comp += lo;
       }
     } else if (!smeta_c32(meta)) {
-      // far class 16: biased 16-bit codes, bounds-checked
+      // far class 16: biased 16-bit codes, bounds-checked; words loaded up front
       const uint32_t nm = uh_nm(h), np = uh_np(h), ni = uh_ni(h);
       const int32_t base = (int32_t)xw.wlo - (int32_t)kBvsBias16;
       const uint32_t npw = (np + 1u) >> 1;
-      for (uint32_t t = 0; t < mnp; ++t) {
-        const uint32_t v = t < np ? __ldg(body + (t >> 1) * 32u) : 0u;
-        const uint32_t c = (t & 1u) ? (v & 0xffffu) : (v >> 16);
-        const double xv = t < np ? xw.at(base + (int32_t)c) : 0.0;
-        tsum(acc, comp, signed_term(xv, t, nm));
+      uint32_t w[kBvsUnitPts / 2];
+#pragma unroll
+      for (uint32_t q = 0; q < kBvsUnitPts / 2; ++q) w[q] = q < npw ? __ldg(body + q * 32u) : 0u;
+      const uint32_t wi0 = ni > 0 ? __ldg(body + npw * 32u) : 0u;
+      const uint32_t wi1 = ni > 1 ? __ldg(body + (npw + 1u) * 32u) : 0u;
+#pragma unroll
+      for (uint32_t q = 0; q < kBvsUnitPts / 2; ++q) {
+        const uint32_t t = 2u * q;
+        if (t >= mnp) break;  // warp-uniform
+        const double x0 = t < np ? xw.at(base + (int32_t)(w[q] >> 16)) : 0.0;
+        const double x1 = t + 1u < np ? xw.at(base + (int32_t)(w[q] & 0xffffu)) : 0.0;
+        tsum(acc, comp, signed_term(x0, t, nm));
+        tsum(acc, comp, signed_term(x1, t + 1u, nm));
       }
-      for (uint32_t u = 0; u < mni; ++u) {
+#pragma unroll
+      for (uint32_t u = 0; u < kBvsUnitInts; ++u) {
+        if (u >= mni) break;
+        const uint32_t v = u ? wi1 : wi0;
         double hi = 0.0, lo = 0.0;
-        if (u < ni) {
-          const uint32_t v = __ldg(body + (npw + u) * 32u);
-          hi = xw.isum(base + (int32_t)(v >> 16), (v & 0xffffu) + lmin, lo);
-        }
+        if (u < ni) hi = xw.isum(base + (int32_t)(v >> 16), (v & 0xffffu) + lmin, lo);
         tsum(acc, comp, hi);
         comp += lo;
       }
-    } else {  // class 32: absolute columns, bounds-checked
+    } else {  // class 32: absolute columns, bounds-checked; words loaded 4 at a time
       const uint32_t nm = uh_nm(h), np = uh_np(h), ni = uh_ni(h);
-      for (uint32_t t = 0; t < mnp; ++t) {
-        const uint32_t c = t < np ? __ldg(body + t * 32u) : 0u;
-        const double xv = t < np ? xw.at((int32_t)c) : 0.0;
-        tsum(acc, comp, signed_term(xv, t, nm));
+      for (uint32_t t0 = 0; t0 < mnp; t0 += 4) {
+        uint32_t c[4];
+#pragma unroll
+        for (uint32_t j = 0; j < 4; ++j) c[j] = t0 + j < np ? __ldg(body + (t0 + j) * 32u) : 0u;
+#pragma unroll
+        for (uint32_t j = 0; j < 4; ++j) {
+          const uint32_t t = t0 + j;
+          const double xv = t < np ? xw.at((int32_t)c[j]) : 0.0;
+          tsum(acc, comp, signed_term(xv, t, nm));
+        }
       }
       for (uint32_t u = 0; u < mni; ++u) {
         double hi = 0.0, lo = 0.0;
@@ -251,8 +265,8 @@ __device__ __forceinline__ void bvs_slices(const uint32_t* __restrict__ bs, cons
 }
 
 template <typename XT, typename YT, bool PR = false>
-__global__ void __launch_bounds__(256, 4) bvs_gather_kernel(BvdDev g, const XT* __restrict__ x, YT* __restrict__ y,
-                                                             PrArgs pr) {
+__global__ void __launch_bounds__(256, 4) bvs_gather_kernel(BvdDev g, const XT* __restrict__ x, const XT* xfar,
+                                                             YT* __restrict__ y, PrArgs pr) {
   extern __shared__ __align__(16) unsigned char smem[];
   const BvdDims& D = g.d;
   const BvsSmem L = bvs_smem_layout(D, sizeof(XT));
@@ -272,6 +286,7 @@ __global__ void __launch_bounds__(256, 4) bvs_gather_kernel(BvdDev g, const XT* 
   XWin<XT, true> xw;
   xw.carve(smem + L.off_x, D.window);
   xw.x = x;
+  xw.xfar = xfar;
   xw.wlo = bi.wlo;
   XT xpre[XWin<XT, true>::kPre];
   xw.prefetch(D.n, xpre);
@@ -286,12 +301,11 @@ __global__ void __launch_bounds__(256, 4) bvs_gather_kernel(BvdDev g, const XT* 
   bvs_slices(bs, xw, D.min_interval, misc, s_yhi, s_ylo, s_ref);
   __syncthreads();
 
-  RowCtx rc{};
+  ChainCtx rc;
   rc.ref = s_ref;
-  rc.perm = reinterpret_cast<uint16_t*>(smem + L.off_ptr);
+  rc.ptr = reinterpret_cast<uint16_t*>(smem + L.off_ptr);
   rc.wscratch = misc + 16;
   rc.nr = nr;
-  rc.B = D.block_rows;
   YT* yb = y + (r0 - g.row_begin);
   if constexpr (PR) {
     const uint32_t sh = r0 - g.row_begin;

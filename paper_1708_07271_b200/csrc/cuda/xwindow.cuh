@@ -42,6 +42,7 @@ struct XWin {
   double* s_th;
   float* s_tl;
   const XT* __restrict__ x;
+  const XT* xfar;  // full x for columns outside the window (device memory, or mapped host memory)
   uint32_t wlo, W;
 
   __device__ __forceinline__ void carve(unsigned char* base, uint32_t Wn) {
@@ -191,7 +192,7 @@ struct XWin {
     const uint32_t j = (uint32_t)(c - (int32_t)wlo);
     const bool in = j < W;
     XT v = s_x[xw_pad(in ? j : 0u)];
-    if (!in) v = __ldg(x + c);  // rare: column outside the window
+    if (!in) v = __ldg(xfar + c);  // rare: column outside the window (read-only during the kernel)
     return (double)v;
   }
 
@@ -218,7 +219,7 @@ struct XWin {
     double s = 0.0, c = 0.0;
     for (uint32_t t = 0; t < len; ++t) {
       double u, er;
-      two_sum(s, (double)__ldg(x + left + t), u, er);
+      two_sum(s, (double)__ldg(xfar + left + t), u, er);
       s = u;
       c += er;
     }

@@ -152,16 +152,26 @@ struct cmvg_graph {
   // canonical BV stream (whole graph) for decode_csr
   DevBuf bv_words, bv_seg;
   uint64_t nseg = 0;
-  // per-row reference distances of the shard (for the scatter form)
-  DevBuf refd;
-  // staging for host-pointer calls
+  // staging for host-pointer calls; streams/events of the pipelined gather
   DevBuf hx, hy;
+  std::vector<uint32_t> win_need;  // per block: x prefix its window needs (prefix max)
+  cudaStream_t s_in = nullptr, s_comp = nullptr, s_out = nullptr;
+  cudaEvent_t ev[32] = {};
+  cmvg_graph() = default;
+  cmvg_graph(const cmvg_graph&) = delete;
+  cmvg_graph& operator=(const cmvg_graph&) = delete;
+  ~cmvg_graph() {
+    for (cudaEvent_t e : ev)
+      if (e) cudaEventDestroy(e);
+    for (cudaStream_t s : {s_in, s_comp, s_out})
+      if (s) cudaStreamDestroy(s);
+  }
   std::mutex host_mu;
   // scratch (scatter / pagerank)
   DevBuf scratch;
   uint64_t device_bytes() const {
     return words.bytes + blocks.bytes + swords.bytes + sblocks.bytes + twords.bytes + tblocks.bytes + tile_ptr.bytes +
-           tile_blk.bytes + farp_ptr.bytes + farp.bytes + bv_words.bytes + bv_seg.bytes + refd.bytes;
+           tile_blk.bytes + farp_ptr.bytes + farp.bytes + bv_words.bytes + bv_seg.bytes;
   }
   BvdDev dev() const {
     BvdDev d{};

@@ -61,7 +61,7 @@ void launch_pr_step(cmvg_graph* g, const double* q, PrArgs pr, double* p_next, c
   const BvsSmem L = bvs_smem_layout(g->dims, sizeof(double));
   auto kern = bvs_gather_kernel<double, double, true>;
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
-  kern<<<g->nblocks, g->threads, L.total, st>>>(g->sdev(), q, p_next, pr);
+  kern<<<g->nblocks, g->threads, L.total, st>>>(g->sdev(), q, q, p_next, pr);
   CUDA_TRY(cudaGetLastError());
 }
 

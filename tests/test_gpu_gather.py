@@ -179,3 +179,26 @@ def test_gather_multi_unit_and_heavy_rows(cuda, dtype):
     g = csr_from_rows([row(k) for k in range(n)])
     check_gather(g, P.BvParams(), dtype=dtype)
     check_gather(g, P.BvParams(), P.CreateOptions(window=512), dtype=dtype)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("cfg,n,window", [(2, (1 << 17) + 333, 1536), (4, 1 << 15, 1536), (2, 1 << 16, 256)])
+def test_gather_host_pinned_pipelined(cuda, dtype, cfg, n, window):
+    # pinned host x / y take the pipelined path (chunked H2D, blocks launched as
+    # their window arrives, far columns read from mapped host memory, chunked
+    # D2H); pageable buffers the plain path -- both must match the oracle
+    import torch
+
+    g = make_graph(cfg, n=n)
+    dg = P.BvGraph(P.BvStream.encode(g, bv_params(cfg)), P.CreateOptions(window=window))
+    x = x_uniform(g.n, 5).astype(dtype)
+    want = oracle_csr(g).matvec(x.astype(np.float64), 8)
+    tol = F64_TOL if dtype == np.float64 else F32_TOL
+    xp = torch.from_numpy(x).pin_memory()
+    yp = torch.empty(g.n, dtype=xp.dtype).pin_memory()
+    yn = yp.numpy()
+    for _ in range(2):
+        yn[:] = np.nan
+        dg.matvec(xp.numpy(), yn)
+        assert max_rel_err(yn, want) <= tol
+    assert max_rel_err(dg.matvec(x), want) <= tol
