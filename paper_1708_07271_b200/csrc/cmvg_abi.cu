@@ -445,7 +445,11 @@ void launch_gather(cmvg_graph* g, const XT* x, YT* y, cudaStream_t st, const XT*
   if (b0 >= b1) return;
   const BvsSmem L = bvs_smem_layout(g->dims, sizeof(XT));
   auto kern = bvs_gather_kernel<XT, YT>;
-  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
+  const unsigned bit = sizeof(XT) == 8 ? 1u : 2u;  // the attribute call is not free: once per handle and type
+  if (!(g->gather_attr & bit)) {
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
+    g->gather_attr |= bit;
+  }
   BvdDev d = g->sdev();
   d.blocks += b0;  // blocks [b0, b1) of this shard
   d.block_begin += b0;
@@ -471,7 +475,7 @@ const void* mapped_host(const void* p) {
 template <typename T>
 void gather_host_pipelined(cmvg_graph* g, const T* x, T* y, const T* xmapped) {
   const uint32_t nb = g->nblocks, B = g->dims.block_rows;
-  const uint32_t C = std::min<uint32_t>(16, nb);
+  const uint32_t C = std::min<uint32_t>(16, nb);  // 2 events per chunk: g->ev has 32
   if (!g->s_in) {
     CUDA_TRY(cudaStreamCreateWithFlags(&g->s_in, cudaStreamNonBlocking));
     CUDA_TRY(cudaStreamCreateWithFlags(&g->s_comp, cudaStreamNonBlocking));

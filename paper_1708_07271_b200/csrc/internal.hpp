@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -157,6 +158,7 @@ struct cmvg_graph {
   std::vector<uint32_t> win_need;  // per block: x prefix its window needs (prefix max)
   cudaStream_t s_in = nullptr, s_comp = nullptr, s_out = nullptr;
   cudaEvent_t ev[32] = {};
+  std::atomic<unsigned> gather_attr{0};  // kernel attributes set (bit per x type)
   cmvg_graph() = default;
   cmvg_graph(const cmvg_graph&) = delete;
   cmvg_graph& operator=(const cmvg_graph&) = delete;
