@@ -170,6 +170,12 @@ const uint32_t* cmvg_layout_tblocks(const cmvg_layout* l, uint32_t* nblocks);
 const uint32_t* cmvg_layout_blocks(const cmvg_layout* l, uint32_t* nblocks);
 void cmvg_layout_free(cmvg_layout* l);
 int cmvg_graph_info_get(const cmvg_graph* g, cmvg_graph_info* out);
+/* Columns of x (sorted, unique) that this handle's gather / PageRank step
+ * reads: its blocks' x-windows plus their out-of-window columns.  A sharded
+ * PageRank only needs these entries of q from the other shards (halo
+ * exchange).  *count is always set; cols is filled when cap >= *count. */
+int cmvg_read_set(const cmvg_graph* g, uint32_t* cols, uint64_t cap, uint64_t* count);
+
 uint32_t cmvg_dimension(const cmvg_graph* g);
 uint64_t cmvg_adds_per_product(const cmvg_graph* g);
 

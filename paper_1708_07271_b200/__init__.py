@@ -138,6 +138,7 @@ _SIGS = [
     ("cmvg_decode_csr", C.c_int, [_P, _P, _P, C.c_int, _P]),
     ("cmvg_pagerank", C.c_int, [_P, _P, C.c_double, C.c_uint32, C.c_double, C.c_int, _P, C.POINTER(C.c_uint32),
                                 C.c_int, _P]),
+    ("cmvg_read_set", C.c_int, [_P, _P, C.c_uint64, C.POINTER(C.c_uint64)]),
     ("cmvg_pagerank_step", C.c_int, [_P, _P, _P, C.c_double, C.c_double, C.c_int, _P, _P, _P, _P, _P]),
 ]
 
@@ -498,6 +499,16 @@ class BvGraph:
         _check(load_library().cmvg_pagerank_step(self._h, ptrs[0], ptrs[1], alpha, dangling_mass,
                                                  {"uniform": 0, "drop": 1}[dangling], ptrs[2], ptrs[3], ptrs[4],
                                                  ptrs[5], st))
+
+    def read_set(self) -> np.ndarray:
+        """Sorted columns of x this handle's gather reads (x-windows + out-of-window
+        columns): what a sharded PageRank must receive from the other shards."""
+        lib = load_library()
+        cnt = C.c_uint64()
+        _check(lib.cmvg_read_set(self._h, None, 0, C.byref(cnt)))
+        out = np.empty(cnt.value, dtype=np.uint32)
+        _check(lib.cmvg_read_set(self._h, out.ctypes.data if cnt.value else None, cnt.value, C.byref(cnt)))
+        return out
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value and _lib_handle is not None:

@@ -262,6 +262,17 @@ int cmvg_create(const cmvg_bvstream* s, const cmvg_create_opts* opts_in, cmvg_gr
       g->swords.upload(sw.data(), sw.size());
       g->sblocks.upload(sbl.data(), sbl.size());
       g->s_stream_bytes = (s1 - s0) * 4;
+      {  // read set: the blocks' x-windows and their out-of-window columns
+        std::vector<uint32_t>& rs = g->read_set;
+        rs.clear();
+        for (uint32_t b = g->block_begin; b < block_end; ++b) {
+          const uint64_t w0 = L.sblocks[b].wlo, w1 = std::min<uint64_t>(bs.n, w0 + L.dims.window);
+          for (uint64_t c = w0; c < w1; ++c) rs.push_back((uint32_t)c);
+          rs.insert(rs.end(), L.rfar.begin() + L.rfar_ptr[b], L.rfar.begin() + L.rfar_ptr[b + 1]);
+        }
+        std::sort(rs.begin(), rs.end());
+        rs.erase(std::unique(rs.begin(), rs.end()), rs.end());
+      }
       g->win_need.resize(sbl.size());
       uint64_t pm = 0;
       for (size_t q = 0; q < sbl.size(); ++q) {
@@ -426,6 +437,14 @@ int cmvg_graph_info_get(const cmvg_graph* g, cmvg_graph_info* o) {
     o->bvs_stream_bytes = g->s_stream_bytes;
     fill_bvt_info(o, g->tstats);
     o->bvt_stream_bytes = g->t_stream_bytes;
+  });
+}
+
+int cmvg_read_set(const cmvg_graph* g, uint32_t* cols, uint64_t cap, uint64_t* count) {
+  return guarded([&] {
+    require(g && count, "null argument");
+    *count = g->read_set.size();
+    if (cols && cap >= g->read_set.size()) std::memcpy(cols, g->read_set.data(), g->read_set.size() * 4);
   });
 }
 

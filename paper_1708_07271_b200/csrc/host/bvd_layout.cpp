@@ -465,7 +465,7 @@ BvdLayout build_bvd(const BvDecoded& dec, const BvParams& bp, const BvdOptions& 
   std::vector<uint32_t> bdepth(nb, 0);
   std::vector<std::vector<uint32_t>> sstream(nb);
   std::vector<BvsStats> bst(nb);
-  std::vector<std::vector<uint32_t>> tstream(nb), tfar(nb);
+  std::vector<std::vector<uint32_t>> tstream(nb), tfar(nb), bfar(nb);
   std::vector<BvtStats> tst(nb);
   parallel_for(nb, [&](uint64_t b0, uint64_t b1) {
     std::vector<RowParts> rps(B);
@@ -578,6 +578,23 @@ BvdLayout build_bvd(const BvDecoded& dec, const BvParams& bp, const BvdOptions& 
       L.blocks[b].nwords = (uint32_t)(out.nbits / 32);
       L.blocks[b].nesc = (uint32_t)(escs.size() / 4);
       emit_bvs(rps.data(), meta.data(), body, nr, lo, W, bp.min_interval, sstream[b], bst[b]);
+      {  // columns this block reads outside its x-window (read set of a shard)
+        std::vector<uint32_t>& fc = bfar[b];
+        fc.clear();
+        auto out = [&](uint64_t c) { return c < lo || c >= lo + W; };
+        for (uint32_t k = 0; k < nr; ++k) {
+          const RowParts& rp = rps[k];
+          for (uint32_t c : rp.minus)
+            if (out(c)) fc.push_back(c);
+          for (uint32_t c : rp.res)
+            if (out(c)) fc.push_back(c);
+          for (const auto& iv : rp.ints)
+            for (uint64_t c = iv.first; c < (uint64_t)iv.first + iv.second; ++c)
+              if (out(c)) fc.push_back((uint32_t)c);
+        }
+        std::sort(fc.begin(), fc.end());
+        fc.erase(std::unique(fc.begin(), fc.end()), fc.end());
+      }
       emit_bvt(rps.data(), meta.data(), nr, B, lo, W, tstream[b], tfar[b], tst[b]);
     }
   });
@@ -635,6 +652,11 @@ BvdLayout build_bvd(const BvDecoded& dec, const BvParams& bp, const BvdOptions& 
         std::memcpy(L.swords.data() + L.sblocks[b].word_offset, sstream[b].data(), sstream[b].size() * 4);
   });
   L.sstats.stream_bytes = soff * 4;
+  // per-block out-of-window read columns
+  L.rfar_ptr.assign(nb + 1, 0);
+  for (uint32_t b = 0; b < nb; ++b) L.rfar_ptr[b + 1] = L.rfar_ptr[b] + bfar[b].size();
+  L.rfar.resize(L.rfar_ptr[nb]);
+  for (uint32_t b = 0; b < nb; ++b) std::copy(bfar[b].begin(), bfar[b].end(), L.rfar.begin() + L.rfar_ptr[b]);
   // BV-T + combine tables
   L.tblocks = L.blocks;
   uint64_t toff = 0, fslot = 0;

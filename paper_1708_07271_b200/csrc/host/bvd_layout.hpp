@@ -50,6 +50,9 @@ struct BvdLayout {
   std::vector<uint32_t> tile_ptr, tile_blk;  // per 'block_rows' column tile: blocks whose window meets it
   std::vector<uint32_t> farp_ptr;            // per tile: range in farp
   std::vector<uint32_t> farp;                // (column, far slot) pairs sorted by column
+  // columns each block reads outside its x-window, sorted (CSR by block)
+  std::vector<uint64_t> rfar_ptr;
+  std::vector<uint32_t> rfar;
   uint64_t adds_per_product = 0;
   BvdStats stats;
 };

@@ -156,6 +156,7 @@ struct cmvg_graph {
   // staging for host-pointer calls; streams/events of the pipelined gather
   DevBuf hx, hy;
   std::vector<uint32_t> win_need;  // per block: x prefix its window needs (prefix max)
+  std::vector<uint32_t> read_set;  // sorted columns of x this shard's gather reads
   cudaStream_t s_in = nullptr, s_comp = nullptr, s_out = nullptr;
   cudaEvent_t ev[32] = {};
   std::atomic<unsigned> gather_attr{0};  // kernel attributes set (bit per x type)

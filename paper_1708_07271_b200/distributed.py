@@ -3,9 +3,15 @@
 Sharding: rows are split into contiguous, block-aligned
 shards; reference chains never leave a block, so every shard is
 self-contained and the products need no data-path collective.  PageRank
-(config 3) exchanges, per iteration, the new q = p/d of every shard
-(all_gather into one n-vector laid out in row order) and two scalars
-(dangling mass, L1 step) with all_reduce -- the only collectives.
+(config 3) exchanges, per iteration, the new q = p/d and two scalars
+(dangling mass, L1 step, all_reduce).  The q exchange is either
+  * full: all_gather of every shard's q into one n-vector (the correctness
+    path), or
+  * halo: each rank receives only the q entries its gather reads from other
+    shards (`BvGraph.read_set()`: its blocks' x-windows -- mostly its own rows
+    plus a slab at each edge -- and the rare out-of-window columns), with one
+    all_to_all_single of precomputed index lists (`plan_halo`).  For the
+    copy-model A^T of config 3 that is a small fraction of the full vector.
 
 The per-shard compute is `BvGraph.pagerank_step` (one fused sm_100a kernel +
 a reduction).  `step_fn` can be replaced for CPU testing of the exchange logic
@@ -38,14 +44,52 @@ def plan_shards(n: int, world: int, block_rows: int) -> ShardPlan:
     return ShardPlan(n=n, world=world, block_rows=block_rows, chunk=per * block_rows)
 
 
+@dataclasses.dataclass
+class HaloPlan:
+    """Per-rank index lists of the halo exchange (see plan_halo)."""
+    send_idx: object      # int64 tensor: local rows of my q to send, grouped by destination rank
+    send_counts: list     # per destination rank
+    recv_cols: object     # int64 tensor: global columns I receive, grouped by source rank
+    recv_counts: list     # per source rank
+
+    @property
+    def recv_entries(self) -> int:
+        return int(sum(self.recv_counts))
+
+
+def plan_halo(read_set, plan: ShardPlan, rank: int, device=None, group=None) -> HaloPlan:
+    """Exchange, once, which q entries each rank needs from each owner: the
+    columns of `read_set` (sorted, unique) outside this rank's rows, grouped by
+    owner shard.  Collective over the group."""
+    import torch
+    import torch.distributed as dist
+
+    a, b = plan.bounds(rank)
+    rs = np.asarray(read_set, dtype=np.int64)
+    remote = rs[(rs < a) | (rs >= b)]
+    owner = remote // plan.chunk  # sorted columns -> grouped by owner
+    req_counts = np.bincount(owner, minlength=plan.world).astype(np.int64)
+    req = torch.from_numpy(req_counts).to(device)
+    got = torch.empty_like(req)
+    dist.all_to_all_single(got, req, group=group)
+    send_counts = [int(v) for v in got.cpu().tolist()]
+    recv_counts = [int(v) for v in req_counts.tolist()]
+    recv_cols = torch.from_numpy(remote).to(device)
+    incoming = torch.empty(sum(send_counts), dtype=torch.int64, device=device)
+    dist.all_to_all_single(incoming, recv_cols, output_split_sizes=send_counts, input_split_sizes=recv_counts,
+                           group=group)
+    return HaloPlan(send_idx=incoming - a, send_counts=send_counts, recv_cols=recv_cols, recv_counts=recv_counts)
+
+
 def sharded_pagerank(step_fn: Callable, degrees_shard, n: int, plan: ShardPlan, rank: int, alpha: float = 0.15,
                      iterations: int = 10, l1_tolerance: Optional[float] = None, dangling: str = "uniform",
-                     device=None, group=None):
+                     device=None, group=None, halo: Optional[HaloPlan] = None):
     """Power iteration p_t = alpha/n + (1-alpha)(A^T q + D/n) over row shards.
 
     step_fn(q_full, alpha, dmass, p_prev_shard, p_next_shard, q_next_shard, partial) computes this shard's
     p_next / q_next and partial = [sum of p_next over dangling rows, L1 step] (device tensors).
-    Returns (p_shard, iterations_run)."""
+    With `halo`, q_full holds correct values only at this rank's rows and its
+    read set (all the step reads).  Returns (p_shard, iterations_run)."""
     import torch
     import torch.distributed as dist
 
@@ -58,7 +102,20 @@ def sharded_pagerank(step_fn: Callable, degrees_shard, n: int, plan: ShardPlan, 
     q_loc = torch.where(deg > 0, p / deg.clamp(min=1).to(dt), torch.zeros_like(p))
     q_send = torch.zeros(plan.chunk, dtype=dt, device=device)
     q_send[:rows] = q_loc
-    dist.all_gather_into_tensor(q_pad, q_send, group=group)
+    if halo is not None:
+        recv = torch.empty(halo.recv_entries, dtype=dt, device=device)
+
+    def exchange(q_shard):
+        if halo is None:
+            dist.all_gather_into_tensor(q_pad, q_shard, group=group)
+            return
+        q_pad[a:b] = q_shard[:rows]
+        send = q_shard.index_select(0, halo.send_idx)
+        dist.all_to_all_single(recv, send, output_split_sizes=halo.recv_counts, input_split_sizes=halo.send_counts,
+                               group=group)
+        q_pad.index_copy_(0, halo.recv_cols, recv)
+
+    exchange(q_send)
     part = torch.zeros(2, dtype=dt, device=device)
     part[0] = p[deg == 0].sum()
     dist.all_reduce(part, group=group)
@@ -69,7 +126,7 @@ def sharded_pagerank(step_fn: Callable, degrees_shard, n: int, plan: ShardPlan, 
     for it in range(1, iterations + 1):
         q_next.zero_()
         step_fn(q_pad[:n], alpha, dmass, p if l1_tolerance is not None else None, p_next, q_next[:rows], part)
-        dist.all_gather_into_tensor(q_pad, q_next, group=group)
+        exchange(q_next)
         dist.all_reduce(part, group=group)
         dmass = float(part[0].item())
         l1 = float(part[1].item())

@@ -12,7 +12,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from oracle import pyoracle as O
-from paper_1708_07271_b200.distributed import plan_shards, sharded_pagerank
+from paper_1708_07271_b200.distributed import plan_halo, plan_shards, sharded_pagerank
 
 
 def _free_port():
@@ -33,7 +33,7 @@ def _graph(n, seed):
     return O.Csr.build(edges, n)
 
 
-def _worker(rank, world, port, n, block_rows, iters, tol, out):
+def _worker(rank, world, port, n, block_rows, iters, tol, out, use_halo=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     g = _graph(n, 5)
@@ -54,7 +54,23 @@ def _worker(rank, world, port, n, block_rows, iters, tol, out):
         part[0] = float(pn[d == 0].sum())
         part[1] = float(np.abs(pn - p_prev.numpy()).sum()) if p_prev is not None else 0.0
 
-    p, it = sharded_pagerank(step, torch.from_numpy(deg[a:b].astype(np.int64)), n, plan, rank, 0.15, iters, tol)
+    halo = None
+    if use_halo:
+        # the columns this shard's step reads (the GPU path gets them from BvGraph.read_set())
+        rs = np.unique(co[ro[a]:ro[b]]).astype(np.uint32)
+        halo = plan_halo(rs, plan, rank)
+        assert halo.recv_entries < n  # strictly less than a full all_gather
+
+    def poisoned_step(q_full, *args):
+        if halo is not None:  # entries outside the read set and own rows must not be used
+            keep = torch.zeros(n, dtype=torch.bool)
+            keep[a:b] = True
+            keep[torch.from_numpy(np.unique(co[ro[a]:ro[b]]).astype(np.int64))] = True
+            q_full = torch.where(keep, q_full, torch.full_like(q_full, float("nan")))
+        step(q_full, *args)
+
+    p, it = sharded_pagerank(poisoned_step, torch.from_numpy(deg[a:b].astype(np.int64)), n, plan, rank, 0.15, iters,
+                             tol, halo=halo)
     full = torch.zeros(plan.world * plan.chunk, dtype=torch.float64)
     buf = torch.zeros(plan.chunk, dtype=torch.float64)
     buf[: b - a] = p
@@ -64,11 +80,14 @@ def _worker(rank, world, port, n, block_rows, iters, tol, out):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,n,block_rows,iters,tol", [(2, 5000, 1024, 30, None), (2, 3000, 1024, 200, 1e-9),
-                                                          (3, 4100, 512, 20, None)])
-def test_sharded_pagerank_matches_oracle(tmp_path, world, n, block_rows, iters, tol):
+@pytest.mark.parametrize("world,n,block_rows,iters,tol,halo", [(2, 5000, 1024, 30, None, False),
+                                                               (2, 3000, 1024, 200, 1e-9, False),
+                                                               (3, 4100, 512, 20, None, False),
+                                                               (2, 5000, 1024, 30, None, True),
+                                                               (3, 4100, 512, 40, 1e-9, True)])
+def test_sharded_pagerank_matches_oracle(tmp_path, world, n, block_rows, iters, tol, halo):
     out = str(tmp_path / "p.npy")
-    mp.spawn(_worker, args=(world, _free_port(), n, block_rows, iters, tol, out), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), n, block_rows, iters, tol, out, halo), nprocs=world, join=True)
     got = np.load(out)
     p, it = got[:n], int(got[n])
     g = _graph(n, 5)

@@ -112,3 +112,46 @@ def test_pagerank_shard_steps(cuda):
         dmass = float(tot[0])
     want, _ = oracle_pr(g, iterations=30)
     assert rel(p.cpu().numpy(), want) <= 1e-12
+
+
+@pytest.mark.parametrize("window", [1536, 256])
+def test_pagerank_shard_steps_halo_read_set(cuda, window):
+    """Each shard's step sees q only at its own rows and its read_set() (every
+    other entry NaN): the halo exchange's contract.  Results must match the
+    oracle, and the halo must be much smaller than the full vector."""
+    import torch
+
+    from paper_1708_07271_b200.distributed import plan_shards
+
+    g = make_graph(3, n=(1 << 16) + 300)
+    n = g.n
+    s = bv_of_transpose(g)
+    plan = plan_shards(n, 3, 1024)
+    deg = torch.from_numpy(g.out_degrees().astype(np.int32)).cuda()
+    shards = []
+    for r in range(3):
+        a, b = plan.bounds(r)
+        dgs = P.BvGraph(s, P.CreateOptions(row_begin=a, row_end=b, window=window))
+        rs = torch.from_numpy(dgs.read_set().astype(np.int64)).cuda()
+        keep = torch.zeros(n, dtype=torch.bool, device="cuda")
+        keep[a:b] = True
+        keep[rs] = True
+        halo = int(keep.sum()) - (b - a)
+        assert halo < n // 2
+        shards.append((a, b, dgs, keep))
+    p = torch.full((n,), 1.0 / n, dtype=torch.float64, device="cuda")
+    q = torch.where(deg > 0, p / deg.clamp(min=1).double(), torch.zeros_like(p))
+    dmass = float(p[deg == 0].sum())
+    nan = torch.full_like(q, float("nan"))
+    for _ in range(20):
+        p_next, q_next = torch.empty_like(p), torch.empty_like(q)
+        tot = torch.zeros(2, dtype=torch.float64, device="cuda")
+        for a, b, dgs, keep in shards:
+            part = torch.zeros(2, dtype=torch.float64, device="cuda")
+            dgs.pagerank_step(torch.where(keep, q, nan), deg[a:b], 0.15, dmass, "uniform", p[a:b], p_next[a:b],
+                              q_next[a:b], part)
+            tot += part
+        p, q = p_next, q_next
+        dmass = float(tot[0])
+    want, _ = oracle_pr(g, iterations=20)
+    assert rel(p.cpu().numpy(), want) <= 1e-12
