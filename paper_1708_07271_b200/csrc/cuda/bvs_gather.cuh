@@ -42,8 +42,10 @@ struct PrArgs {
 
 constexpr uint32_t kBvsGuardWords = 64;  // zero words after the last block (lanes never read past their unit)
 
+constexpr uint32_t kBvsSliceTab = 128;  // slice-table entries staged in shared memory
+
 struct BvsSmem {
-  uint32_t off_x, off_yhi, off_ylo, off_ptr, off_ref, off_misc, total;
+  uint32_t off_x, off_yhi, off_ylo, off_ptr, off_ref, off_tab, off_misc, total;
 };
 
 __host__ __device__ inline BvsSmem bvs_smem_layout(const BvdDims& d, uint32_t xsize) {
@@ -59,6 +61,8 @@ __host__ __device__ inline BvsSmem bvs_smem_layout(const BvdDims& d, uint32_t xs
   o = align16(o + d.block_rows * 2);
   s.off_ref = o;
   o = align16(o + d.block_rows);
+  s.off_tab = o;
+  o = align16(o + kBvsSliceTab * 8);
   s.off_misc = o;  // mbarrier (16) + 16 ints + scratch (64 ints)
   o = align16(o + 16 + 64 + 64 * 4);
   s.total = o;
@@ -142,19 +146,55 @@ __device__ __forceinline__ double signed_term(double x, uint32_t t, uint32_t nm)
   return __hiloint2double(__double2hiint(x) ^ (int)m, __double2loint(x));
 }
 
+// A slice's epilogue: segmented reduction of a multi slice, then the primary
+// lane writes delta_i and r_i.
+__device__ __forceinline__ void bvs_slice_epilogue(uint32_t lane, uint32_t meta, uint32_t h, double hi, double lo,
+                                                   double* s_yhi, float* s_ylo, uint8_t* s_ref) {
+  if (smeta_multi(meta)) {
+    // a row's units sit in adjacent lanes starting at its primary: segmented
+    // suffix reduction so the primary lane ends with the row's delta
+    const uint32_t heads = __ballot_sync(0xffffffffu, uh_primary(h));
+    const uint32_t above = heads & ~((2u << lane) - 1u);
+    const uint32_t end = above ? (uint32_t)__ffs(above) - 2u : 31u;
+#pragma unroll
+    for (uint32_t o = 1; o < 32; o <<= 1) {
+      const double uh = __shfl_down_sync(0xffffffffu, hi, o), ul = __shfl_down_sync(0xffffffffu, lo, o);
+      if (lane + o <= end) dd_add(hi, lo, uh, ul);
+    }
+  }
+  if (uh_primary(h)) {
+    const uint32_t k = uh_k(h);
+    s_yhi[k] = hi;
+    s_ylo[k] = (float)lo;
+    s_ref[k] = (uint8_t)uh_r(h);
+  }
+}
+
 // Slices: one unit (<= 16 points, <= 2 intervals of one row) per lane; in
 // "multi" slices a row's units occupy adjacent lanes and are combined by a
 // segmented warp reduction.  `bs` is the block's stream in global memory.
 template <class XW>
 __device__ __forceinline__ void bvs_slices(const uint32_t* __restrict__ bs, const XW& xw, uint32_t lmin, int* misc,
-                                           double* s_yhi, float* s_ylo, uint8_t* s_ref) {
+                                           double* s_yhi, float* s_ylo, uint8_t* s_ref, const uint32_t* s_tab) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t nsl = __ldg(bs) & 0xffffu;
+  bool have_prev = false;
+  uint32_t prev_meta = 0, prev_h = 0;
+  double prev_hi = 0.0, prev_lo = 0.0;
   uint32_t s = ticket_take(ticket_issue(&misc[kBvsSliceCtr]));
   while (s < nsl) {
     const uint32_t next = ticket_issue(&misc[kBvsSliceCtr]);
-    const uint32_t* rec = bs + __ldg(bs + kBvsHead + s);
-    const uint32_t meta = __ldg(rec);
+    // slice table entry from shared memory (staged per block) when it fits:
+    // header, meta and body words then come in one round of global loads
+    uint32_t roff, meta;
+    if (nsl <= kBvsSliceTab) {
+      roff = s_tab[2 * s];
+      meta = s_tab[2 * s + 1];
+    } else {
+      roff = __ldg(bs + kBvsHead + 2 * s);
+      meta = __ldg(bs + kBvsHead + 2 * s + 1);
+    }
+    const uint32_t* rec = bs + roff;
     const uint32_t h = __ldg(rec + 1u + lane);
     const uint32_t* body = rec + 33u + lane;  // this lane's word q at body[32 q]
     const uint32_t mnp = smeta_np(meta), mni = smeta_ni(meta);
@@ -168,6 +208,10 @@ __device__ __forceinline__ void bvs_slices(const uint32_t* __restrict__ bs, cons
       for (uint32_t q = 0; q < kBvsUnitPts / 2; ++q) w[q] = q < mnpw ? __ldg(body + q * 32u) : 0u;
       const uint32_t wi0 = mni > 0 ? __ldg(body + mnpw * 32u) : 0u;
       const uint32_t wi1 = mni > 1 ? __ldg(body + (mnpw + 1u) * 32u) : 0u;
+      if (have_prev) {  // the previous slice's epilogue while these loads are in flight
+        bvs_slice_epilogue(lane, prev_meta, prev_h, prev_hi, prev_lo, s_yhi, s_ylo, s_ref);
+        have_prev = false;
+      }
       double acc2 = 0.0, comp2 = 0.0;
 #pragma unroll
       for (uint32_t q = 0; q < kBvsUnitPts / 2; ++q) {
@@ -241,27 +285,17 @@ __device__ __forceinline__ void bvs_slices(const uint32_t* __restrict__ bs, cons
         comp += lo;
       }
     }
-    double hi = acc + comp, lo = comp - (hi - acc);
-    if (smeta_multi(meta)) {
-      // a row's units sit in adjacent lanes starting at its primary: segmented
-      // suffix reduction so the primary lane ends with the row's delta
-      const uint32_t heads = __ballot_sync(0xffffffffu, uh_primary(h));
-      const uint32_t above = heads & ~((2u << lane) - 1u);
-      const uint32_t end = above ? (uint32_t)__ffs(above) - 2u : 31u;
-#pragma unroll
-      for (uint32_t o = 1; o < 32; o <<= 1) {
-        const double uh = __shfl_down_sync(0xffffffffu, hi, o), ul = __shfl_down_sync(0xffffffffu, lo, o);
-        if (lane + o <= end) dd_add(hi, lo, uh, ul);
-      }
-    }
-    if (uh_primary(h)) {
-      const uint32_t k = uh_k(h);
-      s_yhi[k] = hi;
-      s_ylo[k] = (float)lo;
-      s_ref[k] = (uint8_t)uh_r(h);
-    }
+    // this slice's epilogue runs after the next slice's loads are issued (it
+    // hides their latency): keep its state
+    if (have_prev) bvs_slice_epilogue(lane, prev_meta, prev_h, prev_hi, prev_lo, s_yhi, s_ylo, s_ref);
+    prev_hi = acc + comp;
+    prev_lo = comp - (prev_hi - acc);
+    prev_h = h;
+    prev_meta = meta;
+    have_prev = true;
     s = ticket_take(next);
   }
+  if (have_prev) bvs_slice_epilogue(lane, prev_meta, prev_h, prev_hi, prev_lo, s_yhi, s_ylo, s_ref);
 }
 
 template <typename XT, typename YT, bool PR = false>
@@ -283,6 +317,12 @@ __global__ void __launch_bounds__(256, 4) bvs_gather_kernel(BvdDev g, const XT* 
     misc[kBvsSliceCtr] = 0;
   }
   if (threadIdx.x == 32) bulk_prefetch_l2(bs, bi.nwords * 4u);
+  uint32_t* s_tab = reinterpret_cast<uint32_t*>(smem + L.off_tab);
+  {
+    const uint32_t nsl = __ldg(bs) & 0xffffu;
+    if (nsl <= kBvsSliceTab)
+      for (uint32_t i = threadIdx.x; i < 2 * nsl; i += blockDim.x) s_tab[i] = __ldg(bs + kBvsHead + i);
+  }
   XWin<XT, true> xw;
   xw.carve(smem + L.off_x, D.window);
   xw.x = x;
@@ -298,7 +338,7 @@ __global__ void __launch_bounds__(256, 4) bvs_gather_kernel(BvdDev g, const XT* 
   uint8_t* s_ref = smem + L.off_ref;
   const Src<false> src{bs};
   bvs_heavy(src, xw, (int32_t)r0, D.min_interval, misc, s_yhi, s_ylo, s_ref);
-  bvs_slices(bs, xw, D.min_interval, misc, s_yhi, s_ylo, s_ref);
+  bvs_slices(bs, xw, D.min_interval, misc, s_yhi, s_ylo, s_ref, s_tab);
   __syncthreads();
 
   ChainCtx rc;

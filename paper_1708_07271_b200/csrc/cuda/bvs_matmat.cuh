@@ -152,8 +152,8 @@ __device__ __forceinline__ void mm_slices(const uint32_t* __restrict__ bs, const
   uint32_t s = ticket_take(ticket_issue(&misc[kBvsSliceCtr]));
   while (s < nsl) {
     const uint32_t next = ticket_issue(&misc[kBvsSliceCtr]);
-    const uint32_t* rec = bs + __ldg(bs + kBvsHead + s);
-    const uint32_t meta = __ldg(rec);
+    const uint32_t* rec = bs + __ldg(bs + kBvsHead + 2 * s);
+    const uint32_t meta = __ldg(bs + kBvsHead + 2 * s + 1);
     const uint32_t h = __ldg(rec + 1u + lane);
     const uint32_t* body = rec + 33u + lane;
     const uint32_t mnp = smeta_np(meta), mni = smeta_ni(meta);

@@ -199,12 +199,12 @@ void emit_bvs(const RowParts* rps, const RowMeta* meta, const BitWriter& body, u
   }
   const uint32_t nsl = (uint32_t)slices.size(), nh = (uint32_t)hrows.size();
   if (nsl > 0xffffu || nh > 0xffffu) throw std::runtime_error("BV-S: block too large");
-  so.assign(kBvsHead + nsl, 0u);
+  so.assign(kBvsHead + 2 * nsl, 0u);
   so[0] = nsl | (nh << 16);
   for (uint32_t s = 0; s < nsl; ++s) {
     const Slice& sl = slices[s];
     const bool nearc16 = !sl.c32 && !sl.far;
-    so[kBvsHead + s] = (uint32_t)so.size();
+    so[kBvsHead + 2 * s] = (uint32_t)so.size();
     uint32_t mnp = 0, mni = 0, nq = 0;
     for (const Unit* u : sl.lanes) {
       mnp = std::max(mnp, u->np);
@@ -215,6 +215,7 @@ void emit_bvs(const RowParts* rps, const RowMeta* meta, const BitWriter& body, u
     }
     if (nearc16) nq = (mnp + 1) / 2 + mni;  // rectangular: points then intervals
     so.push_back(make_smeta(mnp, mni, sl.c32, sl.far, sl.multi));
+    so[kBvsHead + 2 * s + 1] = so.back();  // the table repeats the meta word
     for (size_t l = 0; l < 32; ++l) {
       if (l < sl.lanes.size()) {
         const Unit& u = *sl.lanes[l];

@@ -93,7 +93,8 @@ __host__ __device__ constexpr uint32_t make_hdr(uint32_t r, uint32_t nm, uint32_
 //     stream (BV-D codes).
 // Block stream (u32 words):
 //   [0] nslices | nheavy << 16   [1] heavy table offset   [2] heavy stream offset
-//   [3] 0                        [4, 4 + nslices) slice record offsets
+//   [3] 0                        [4, 4 + 2 nslices) slice table: (record
+//                                offset, meta) per slice
 //   slice record: [meta][header x 32][body]
 //     meta: max #points | max #intervals << 5 | class32 << 8 | far << 9 |
 //           multi << 10

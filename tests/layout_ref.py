@@ -130,8 +130,9 @@ def decode_sliced(words, blocks, n, B, lmin, W):
             assert k not in parts
             parts[k] = dict(minus=pts[:nm], res=pts[nm:], ints=ints, r=r)
         for sl in range(nsl):
-            rec = s[4 + sl]
+            rec = s[4 + 2 * sl]
             meta = s[rec]
+            assert s[4 + 2 * sl + 1] == meta
             mnp, mni, c32, far, multi = meta & 31, (meta >> 5) & 7, (meta >> 8) & 1, (meta >> 9) & 1, (meta >> 10) & 1
             seen_np, seen_ni = 0, 0
             cur = None
