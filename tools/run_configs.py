@@ -107,7 +107,7 @@ def main():
         r["bits_per_edge"] = st["stream_bits"] / g.m
         r["max_depth"] = st["max_depth"]
         t0 = time.time()
-        dg = P.BvGraph(s, P.CreateOptions(window=4096 if cfg == 4 else 1536))
+        dg = P.BvGraph(s, P.CreateOptions(window=1536))
         r["handle_s"] = time.time() - t0
         info = dg.info()
         r["device_layout_bytes"] = info["bvd_stream_bytes"] + info["bvd_block_table_bytes"]
