@@ -40,15 +40,13 @@ def parse():
     ap.add_argument("--degree", type=float, default=20.0)
     ap.add_argument("--dtype", choices=["f64", "f32"], default="f64")
     ap.add_argument("--form", choices=["gather", "scatter"], default="gather")
-    ap.add_argument("--interval-mode", choices=["prefix", "direct"], default="prefix")
     ap.add_argument("--lanes", type=int, default=256)
     ap.add_argument("--block-rows", type=int, default=1024)
     ap.add_argument("--window", type=int, default=1536)
-    ap.add_argument("--stream-cap-words", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
-    ap.add_argument("--secondary", action="store_true", help="also time f32 / scatter / direct variants (stderr)")
+    ap.add_argument("--secondary", action="store_true", help="also time the f32 / scatter variants (stderr)")
     ap.add_argument("--cpu-sample-seconds", type=float, default=20.0)
     return ap.parse_args()
 
@@ -205,8 +203,7 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=dev)
 
     g, s = make_workload(args, rank)
-    opts = P.CreateOptions(device=local, block_rows=args.block_rows, lanes=args.lanes, window=args.window,
-                           stream_cap_words=args.stream_cap_words, interval_mode=args.interval_mode)
+    opts = P.CreateOptions(device=local, block_rows=args.block_rows, lanes=args.lanes, window=args.window)
     t0 = time.time()
     dg = P.BvGraph(s, opts)
     info = dg.info()
@@ -339,7 +336,7 @@ def run_ours(args):
                 "device_layout_bytes": (info["bvs_stream_bytes"] if args.form == "gather" else info["bvd_stream_bytes"])
                 + info["bvd_block_table_bytes"],
                 "block_rows": args.block_rows, "lanes": args.lanes, "window": args.window,
-                "interval_mode": args.interval_mode, "l2": "flushed (512 MiB write) before every timed launch",
+                "l2": "flushed (512 MiB write) before every timed launch",
                 "parallelism": f"weak replicas x{world}",
             },
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -370,30 +367,29 @@ def run_secondary(args, g, s, dev):
     res = {}
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
     for dtype in ("f64", "f32"):
-        for mode in ("prefix", "direct"):
-            for form in ("gather", "scatter"):
-                try:
-                    dg = P.BvGraph(s, P.CreateOptions(device=dev.index, interval_mode=mode, lanes=args.lanes,
-                                                      block_rows=args.block_rows, window=args.window))
-                    xh = x_uniform(g.n, 11, dtype)
-                    x = torch.from_numpy(xh).to(dev)
-                    y = torch.empty(g.n, dtype=x.dtype, device=dev)
-                    for _ in range(3):
-                        dg.matvec(x, y, form=form)
-                    ts = []
-                    for _ in range(10):
-                        flush.zero_()
-                        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                        a.record()
-                        dg.matvec(x, y, form=form)
-                        b.record()
-                        torch.cuda.synchronize()
-                        ts.append(a.elapsed_time(b))
-                    t = float(np.mean(ts))
-                    res[f"{form}_{dtype}_{mode}"] = {"ms": t, "Gedges_s": g.m / t / 1e6}
-                    dg.close()
-                except Exception as e:  # noqa: BLE001 (report, do not hide)
-                    res[f"{form}_{dtype}_{mode}"] = {"error": str(e)[:200]}
+        for form in ("gather", "scatter"):
+            try:
+                dg = P.BvGraph(s, P.CreateOptions(device=dev.index, lanes=args.lanes, block_rows=args.block_rows,
+                                                  window=args.window))
+                xh = x_uniform(g.n, 11, dtype)
+                x = torch.from_numpy(xh).to(dev)
+                y = torch.empty(g.n, dtype=x.dtype, device=dev)
+                for _ in range(3):
+                    dg.matvec(x, y, form=form)
+                ts = []
+                for _ in range(10):
+                    flush.zero_()
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record()
+                    dg.matvec(x, y, form=form)
+                    b.record()
+                    torch.cuda.synchronize()
+                    ts.append(a.elapsed_time(b))
+                t = float(np.mean(ts))
+                res[f"{form}_{dtype}"] = {"ms": t, "Gedges_s": g.m / t / 1e6}
+                dg.close()
+            except Exception as e:  # noqa: BLE001 (report, do not hide)
+                res[f"{form}_{dtype}"] = {"error": str(e)[:200]}
     log(json.dumps(res))
     return res
 

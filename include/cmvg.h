@@ -92,8 +92,8 @@ typedef struct {
   uint32_t block_rows;    /* rows per CTA block (power of 2, multiple of the segment) */
   uint32_t lanes;         /* decode lanes (threads) per block                 */
   uint32_t window;        /* x-window entries staged per block                */
-  uint32_t stream_cap_words; /* smem staging cap; larger blocks decode from global; 0 = auto (p99.5) */
-  uint32_t interval_mode; /* CMVG_INTERVALS_*                                 */
+  uint32_t stream_cap_words; /* reserved (ignored): the sliced streams are read through L2 */
+  uint32_t interval_mode; /* reserved (ignored): intervals always use the x-window prefix */
   uint32_t row_begin;     /* shard [row_begin, row_end); row_end 0 = n        */
   uint32_t row_end;
 } cmvg_create_opts;

@@ -23,20 +23,9 @@ struct BvdDev {
 
 __host__ __device__ inline uint32_t align16(uint32_t v) { return (v + 15u) & ~15u; }
 
-// ---- coded-stream sources --------------------------------------------------
-// Staged blocks are read with 32-bit shared-window addresses (LDS), large
-// blocks straight from global memory.
+// ---- coded-stream source: the block's words in global memory (read through L1/L2)
 template <bool STAGED>
 struct Src;
-template <>
-struct Src<true> {
-  uint32_t sbase;  // shared address of word 0
-  __device__ __forceinline__ uint32_t w(uint32_t i) const {
-    uint32_t v;
-    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(sbase + 4u * i));
-    return v;
-  }
-};
 template <>
 struct Src<false> {
   const uint32_t* __restrict__ p;
