@@ -219,7 +219,7 @@ __device__ __forceinline__ void mm_slices(const uint32_t* __restrict__ bs, const
   }
 }
 
-__global__ void __launch_bounds__(256, 2) bvs_matmat_kernel(BvdDev g, const float* __restrict__ X,
+__global__ void __launch_bounds__(512, 2) bvs_matmat_kernel(BvdDev g, const float* __restrict__ X,
                                                              float* __restrict__ Y, uint32_t ld, uint32_t kk) {
   extern __shared__ __align__(16) unsigned char smem[];
   const BvdDims& D = g.d;

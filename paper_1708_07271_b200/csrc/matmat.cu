@@ -10,7 +10,7 @@ void launch_matmat(cmvg_graph* g, const float* X, float* Y, uint32_t k, cudaStre
   CUDA_TRY(cudaFuncSetAttribute(bvs_matmat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
   for (uint32_t c0 = 0; c0 < k; c0 += kMmCols) {
     const uint32_t kk = std::min(kMmCols, k - c0);
-    bvs_matmat_kernel<<<g->nblocks, 256, L.total, st>>>(g->sdev(), X + c0, Y + c0, k, kk);
+    bvs_matmat_kernel<<<g->nblocks, 512, L.total, st>>>(g->sdev(), X + c0, Y + c0, k, kk);
     CUDA_TRY(cudaGetLastError());
   }
 }
