@@ -33,6 +33,8 @@
 
 namespace cmvg {
 
+constexpr uint32_t kBvtSliceTab = 128;  // slice-table entries staged in shared memory
+
 struct BvtSmem {
   uint32_t off_ch, off_cl, off_oh, off_ol, off_misc, total;
 };
@@ -49,8 +51,8 @@ __host__ __device__ inline BvtSmem bvt_smem_layout(const BvdDims& d) {
   o = align16(o + 2 * W * 8);
   s.off_ol = o;
   o = align16(o + 2 * W * 4);
-  s.off_misc = o;  // 16 ints + scratch (64 ints)
-  o = align16(o + 64 + 64 * 4);
+  s.off_misc = o;  // 16 ints + warp totals (32 ints) + slice table (kBvtSliceTab x 2 words)
+  o = align16(o + 48 * 4 + kBvtSliceTab * 8);
   s.total = o;
   return s;
 }
@@ -103,17 +105,37 @@ __global__ void __launch_bounds__(256, 4) bvt_scatter_kernel(BvdDev g, const XT*
   if (tid == 32) bulk_prefetch_l2(bs, bi.nwords * 4u);
 
   // ---- 1. coefficients ------------------------------------------------------
-  for (uint32_t k = tid; k < nr; k += T) {
+  constexpr uint32_t kPer = 4;  // rows per thread (block_rows <= 4 x threads): loads first, stores later
+  XT xv[kPer];
+#pragma unroll
+  for (uint32_t q = 0; q < kPer; ++q) {
+    const uint32_t k = tid + q * T;
+    xv[q] = k < nr ? __ldg(x + r0 + k) : XT(0);
+  }
+  const uint32_t h0 = __ldg(bs);
+  const uint32_t nsl = h0 & 0xffffu, nh = h0 >> 16;
+  uint32_t* s_tab = reinterpret_cast<uint32_t*>(misc + 48);  // slice table (offset, meta), when it fits
+  if (nsl <= kBvtSliceTab)
+    for (uint32_t i = tid; i < 2 * nsl; i += T) s_tab[i] = __ldg(bs + kBvtHead + i);
+  for (uint32_t j = tid; j < W2; j += T) {
+    s_oh[j] = 0.0;
+    s_ol[j] = 0.0f;
+  }
+#pragma unroll
+  for (uint32_t q = 0; q < kPer; ++q) {
+    const uint32_t k = tid + q * T;
+    if (k < nr) {
+      ch[k] = (double)xv[q];
+      cl[k] = 0.0f;
+    }
+  }
+  for (uint32_t k = kPer * T + tid; k < nr; k += T) {  // block_rows > 4 x threads
     ch[k] = (double)__ldg(x + r0 + k);
     cl[k] = 0.0f;
   }
   for (uint32_t k = nr + tid; k <= B; k += T) {  // the zero coefficient (padding code B) and rows past n
     ch[k] = 0.0;
     cl[k] = 0.0f;
-  }
-  for (uint32_t j = tid; j < W2; j += T) {
-    s_oh[j] = 0.0;
-    s_ol[j] = 0.0f;
   }
   __syncthreads();
   {  // the transcoder's schedule: per level (deepest first) the rows with
@@ -142,8 +164,6 @@ __global__ void __launch_bounds__(256, 4) bvt_scatter_kernel(BvdDev g, const XT*
 
   // ---- 2. per-target segmented sums ---------------------------------------
   const uint32_t fbase = bi.pad[0];
-  const uint32_t h0 = __ldg(bs);
-  const uint32_t nsl = h0 & 0xffffu, nh = h0 >> 16;
   {  // heavy targets: one warp each, fixed lane order
     const uint32_t htab = __ldg(bs + 1), hcode = __ldg(bs + 2);
     for (uint32_t q = tid >> 5; q < nh; q += T >> 5) {
@@ -164,8 +184,15 @@ __global__ void __launch_bounds__(256, 4) bvt_scatter_kernel(BvdDev g, const XT*
     }
   }
   for (uint32_t s = tid >> 5; s < nsl; s += T >> 5) {  // slices, round-robin (sorted by cost)
-    const uint32_t* rec = bs + __ldg(bs + kBvtHead + s);
-    const uint32_t meta = __ldg(rec);
+    uint32_t roff, meta;
+    if (nsl <= kBvtSliceTab) {
+      roff = s_tab[2 * s];
+      meta = s_tab[2 * s + 1];
+    } else {
+      roff = __ldg(bs + kBvtHead + 2 * s);
+      meta = __ldg(bs + kBvtHead + 2 * s + 1);
+    }
+    const uint32_t* rec = bs + roff;
     const uint32_t h = __ldg(rec + 1u + lane);
     const uint32_t* body = rec + 33u + lane;
     const uint32_t mnw = (tmeta_ne(meta) + 1u) >> 1;

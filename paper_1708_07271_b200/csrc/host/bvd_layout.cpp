@@ -368,7 +368,7 @@ void emit_bvt(const RowParts* rps, const RowMeta* meta, uint32_t nr, uint32_t B,
   }
   const uint32_t nsl = (uint32_t)slices.size(), nh = (uint32_t)heavy.size();
   if (nsl > 0xffffu || nh > 0xffffu) throw std::runtime_error("BV-T: block too large");
-  so.assign(kBvtHead + nsl, 0u);
+  so.assign(kBvtHead + 2 * nsl, 0u);
   so[0] = nsl | (nh << 16);
   so[3] = (uint32_t)far_cols.size();
   // coefficient schedule: rows with children, deepest level first, each
@@ -403,13 +403,14 @@ void emit_bvt(const RowParts* rps, const RowMeta* meta, uint32_t nr, uint32_t B,
   const uint32_t zc = B;  // padding code: the zero coefficient
   for (uint32_t s = 0; s < nsl; ++s) {
     const Slice& sl = slices[s];
-    so[kBvtHead + s] = (uint32_t)so.size();
+    so[kBvtHead + 2 * s] = (uint32_t)so.size();
     uint32_t mne = 0;
     for (const U* u : sl.lanes) {
       mne = std::max<uint32_t>(mne, (uint32_t)u->codes.size());
       st.lane_iters_used += u->codes.size();
     }
     so.push_back(make_tmeta(mne, sl.multi));
+    so[kBvtHead + 2 * s + 1] = so.back();  // the table repeats the meta word
     for (size_t l = 0; l < 32; ++l) so.push_back(l < sl.lanes.size() ? make_th(sl.lanes[l]->primary, sl.lanes[l]->target) : 0u);
     const uint32_t mnw = (mne + 1) / 2;
     const size_t b0 = so.size();

@@ -156,7 +156,7 @@ __host__ __device__ constexpr bool smeta_multi(uint32_t m) { return (m >> 10) & 
 // Block stream (u32 words):
 //   [0] nslices | nheavy << 16  [1] heavy table offset  [2] heavy code offset
 //   [3] nfar  [4] coefficient schedule offset  [5] far column list offset
-//   [6, 7] 0  [8, 8 + nslices) slice record offsets
+//   [6, 7] 0  [8, 8 + 2 nslices) slice table: (record offset, meta) per slice
 //   coefficient schedule: [nlev][nlev + 1 level starts][entries]; levels
 //     deepest first, entry = k | children mask << 10 (bit r-1: row k + r
 //     references k), rows without children omitted

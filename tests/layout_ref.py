@@ -261,8 +261,9 @@ def scatter_bvt_int(words, blocks, n, B, W, x):
             out[t] = tot
         cur = None
         for sl in range(nsl):
-            rec = s[8 + sl]
+            rec = s[8 + 2 * sl]
             meta = s[rec]
+            assert s[8 + 2 * sl + 1] == meta
             mne, multi = meta & 1023, (meta >> 10) & 1
             mnw = (mne + 1) >> 1
             for lane in range(32):
