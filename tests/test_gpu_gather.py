@@ -202,3 +202,20 @@ def test_gather_host_pinned_pipelined(cuda, dtype, cfg, n, window):
         dg.matvec(xp.numpy(), yn)
         assert max_rel_err(yn, want) <= tol
     assert max_rel_err(dg.matvec(x), want) <= tol
+
+
+def test_gather_host_pinned_pipelined_shard(cuda):
+    # a row shard (not starting at 0) on the pipelined host path: y holds the
+    # shard's rows; x is the full vector
+    import torch
+
+    g = make_graph(2, n=(1 << 17) + 99)
+    s = P.BvStream.encode(g, bv_params(2))
+    a, b = 32768, g.n
+    dg = P.BvGraph(s, P.CreateOptions(row_begin=a, row_end=b))
+    x = x_uniform(g.n, 6)
+    want = oracle_csr(g).matvec(x, 8)[a:b]
+    xp = torch.from_numpy(x).pin_memory()
+    yp = torch.empty(b - a, dtype=torch.float64).pin_memory()
+    dg.matvec(xp.numpy(), yp.numpy())
+    assert max_rel_err(yp.numpy(), want) <= F64_TOL
