@@ -204,6 +204,18 @@ int cmvg_pagerank_step(cmvg_graph* g, const double* q, const uint32_t* degrees_s
                        double dangling_mass, int dangling, const double* p_prev, double* p_next,
                        double* q_next, double* partial, void* stream);
 
+/* cmvg_pagerank_step with the halo exchange fused into the kernel (multi-GPU
+ * over NVLink peer memory): each new q'_k is also stored, at its global
+ * column, into push_dst[p] for every bit p set in push_mask[k] (device
+ * arrays: push_mask one byte per shard row, push_dst up to 8 device pointers
+ * -- the peers' q buffers, e.g. CUDA IPC / symmetric memory).  The stores are
+ * complete (system-scope fence) when the kernel completes; the caller orders
+ * the peers' next step after it (e.g. the scalar all_reduce). */
+int cmvg_pagerank_step_push(cmvg_graph* g, const double* q, const uint32_t* degrees_shard, double alpha,
+                            double dangling_mass, int dangling, const double* p_prev, double* p_next,
+                            double* q_next, double* partial, const uint8_t* push_mask, double* const* push_dst,
+                            void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -139,6 +139,7 @@ _SIGS = [
     ("cmvg_pagerank", C.c_int, [_P, _P, C.c_double, C.c_uint32, C.c_double, C.c_int, _P, C.POINTER(C.c_uint32),
                                 C.c_int, _P]),
     ("cmvg_read_set", C.c_int, [_P, _P, C.c_uint64, C.POINTER(C.c_uint64)]),
+    ("cmvg_pagerank_step_push", C.c_int, [_P, _P, _P, C.c_double, C.c_double, C.c_int, _P, _P, _P, _P, _P, _P, _P]),
     ("cmvg_pagerank_step", C.c_int, [_P, _P, _P, C.c_double, C.c_double, C.c_int, _P, _P, _P, _P, _P]),
 ]
 
@@ -491,14 +492,23 @@ class BvGraph:
         return ranks, int(it.value)
 
     def pagerank_step(self, q, degrees_shard, alpha, dangling_mass, dangling, p_prev, p_next, q_next, partial,
-                      stream: Optional[int] = None):
-        """One sharded PageRank iteration (device tensors); see cmvg_pagerank_step."""
+                      stream: Optional[int] = None, push_mask=None, push_dst=None):
+        """One sharded PageRank iteration (device tensors); see cmvg_pagerank_step.
+        With push_mask (uint8 per shard row) and push_dst (int64 device tensor
+        of peer q-buffer pointers) the halo exchange is fused into the kernel
+        (cmvg_pagerank_step_push)."""
         ptrs = [q.data_ptr(), degrees_shard.data_ptr(), p_prev.data_ptr() if p_prev is not None else None,
                 p_next.data_ptr(), q_next.data_ptr(), partial.data_ptr()]
         st = stream if stream is not None else _stream_of(q)
-        _check(load_library().cmvg_pagerank_step(self._h, ptrs[0], ptrs[1], alpha, dangling_mass,
-                                                 {"uniform": 0, "drop": 1}[dangling], ptrs[2], ptrs[3], ptrs[4],
-                                                 ptrs[5], st))
+        lib = load_library()
+        dang = {"uniform": 0, "drop": 1}[dangling]
+        if push_mask is None:
+            _check(lib.cmvg_pagerank_step(self._h, ptrs[0], ptrs[1], alpha, dangling_mass, dang, ptrs[2], ptrs[3],
+                                          ptrs[4], ptrs[5], st))
+        else:
+            _check(lib.cmvg_pagerank_step_push(self._h, ptrs[0], ptrs[1], alpha, dangling_mass, dang, ptrs[2],
+                                               ptrs[3], ptrs[4], ptrs[5], push_mask.data_ptr(), push_dst.data_ptr(),
+                                               st))
 
     def read_set(self) -> np.ndarray:
         """Sorted columns of x this handle's gather reads (x-windows + out-of-window

@@ -86,16 +86,32 @@ struct PageRankEpi {
   double base, scale, dn;  // alpha/n, 1 - alpha, D/n (or 0)
   uint32_t bl;
   double dang, l1;         // per-thread partials
+  // fused halo push (multi-GPU): q'_k also goes to every peer whose bit is set
+  // in push_mask[k], stored at its global column in that peer's q buffer
+  // (NVLink peer memory) -- the exchange rides on the epilogue's stores
+  const uint8_t* push_mask;    // shard-relative, offset applied; null = no push
+  double* const* push_dst;     // device array: peer q buffers, indexed by global column
+  uint32_t grow0;              // global row of this block's row 0
   template <typename YT>
   __device__ __forceinline__ void store(YT* pb, uint32_t k, double y) {
     const double pn = base + scale * (y + dn);
     pb[k] = (YT)pn;
     const uint32_t d = deg[k];
-    q_next[k] = d ? pn / (double)d : 0.0;
+    const double qn = d ? pn / (double)d : 0.0;
+    q_next[k] = qn;
+    if (push_mask) {
+      uint32_t m = push_mask[k];
+      while (m) {
+        const uint32_t p = (uint32_t)__ffs(m) - 1u;
+        m &= m - 1u;
+        push_dst[p][grow0 + k] = qn;
+      }
+    }
     if (!d) dang += pn;
     if (p_prev) l1 += fabs(pn - p_prev[k]);
   }
   __device__ __forceinline__ void finish(int* scratch) {
+    if (push_mask) __threadfence_system();  // peer stores performed before the kernel's completion is observed
     // deterministic block reduction: warp sums, then warp 0 in warp order
     double a = dang, b = l1;
 #pragma unroll

@@ -38,6 +38,8 @@ struct PrArgs {
   double alpha;
   uint32_t n;
   int uniform;
+  const uint8_t* push_mask;  // fused halo push (see PageRankEpi); null = none
+  double* const* push_dst;
 };
 
 constexpr uint32_t kBvsGuardWords = 64;  // zero words after the last block (lanes never read past their unit)
@@ -361,6 +363,9 @@ __global__ void __launch_bounds__(256, 4) bvs_gather_kernel(BvdDev g, const XT* 
     epi.bl = bl;
     epi.dang = 0.0;
     epi.l1 = 0.0;
+    epi.push_mask = pr.push_mask ? pr.push_mask + sh : nullptr;
+    epi.push_dst = pr.push_dst;
+    epi.grow0 = r0;
     chain_and_store(s_yhi, s_ylo, rc, yb, epi, D.max_depth);
   } else {
     PlainEpi epi;

@@ -124,9 +124,12 @@ void run_pagerank(cmvg_graph* g, const uint32_t* degrees, double alpha, uint32_t
 }
 
 void pagerank_step(cmvg_graph* g, const double* q, const uint32_t* deg, double alpha, double dmass, int dangling,
-                   const double* p_prev, double* p_next, double* q_next, double* partial, cudaStream_t st) {
+                   const double* p_prev, double* p_next, double* q_next, double* partial, cudaStream_t st,
+                   const uint8_t* push_mask, double* const* push_dst) {
   g->scratch.alloc((size_t)g->nblocks * 16 + 64);
   PrArgs pr{};
+  pr.push_mask = push_mask;
+  pr.push_dst = push_dst;
   pr.deg = deg;
   pr.p_prev = p_prev;
   pr.q_next = q_next;

@@ -11,7 +11,12 @@ self-contained and the products need no data-path collective.  PageRank
     shards (`BvGraph.read_set()`: its blocks' x-windows -- mostly its own rows
     plus a slab at each edge -- and the rare out-of-window columns), with one
     all_to_all_single of precomputed index lists (`plan_halo`).  For the
-    copy-model A^T of config 3 that is a small fraction of the full vector.
+    copy-model A^T of config 3 that is a small fraction of the full vector;
+  * push: the halo exchange fused into the step kernel -- its epilogue stores
+    each new q'_k straight into the q buffers of the peers that read row k
+    (`plan_push` masks, NVLink peer memory from torch symmetric memory), so
+    no separate collective moves q at all; the scalar all_reduce orders the
+    iterations.
 
 The per-shard compute is `BvGraph.pagerank_step` (one fused sm_100a kernel +
 a reduction).  `step_fn` can be replaced for CPU testing of the exchange logic
@@ -81,6 +86,22 @@ def plan_halo(read_set, plan: ShardPlan, rank: int, device=None, group=None) -> 
     return HaloPlan(send_idx=incoming - a, send_counts=send_counts, recv_cols=recv_cols, recv_counts=recv_counts)
 
 
+def plan_push(halo: HaloPlan, plan: ShardPlan, rank: int, device=None):
+    """Per shard row, the bit mask of the peer ranks that read it (from the
+    halo plan's send lists): the fused push's destinations."""
+    import torch
+
+    a, b = plan.bounds(rank)
+    mask = torch.zeros(b - a, dtype=torch.uint8, device=device)
+    off = 0
+    for p, c in enumerate(halo.send_counts):
+        if c:
+            idx = halo.send_idx[off:off + c].to(device)
+            mask.index_put_((idx,), mask.index_select(0, idx) | (1 << p))
+        off += c
+    return mask
+
+
 def sharded_pagerank(step_fn: Callable, degrees_shard, n: int, plan: ShardPlan, rank: int, alpha: float = 0.15,
                      iterations: int = 10, l1_tolerance: Optional[float] = None, dangling: str = "uniform",
                      device=None, group=None, halo: Optional[HaloPlan] = None):
@@ -134,6 +155,70 @@ def sharded_pagerank(step_fn: Callable, degrees_shard, n: int, plan: ShardPlan, 
         if l1_tolerance is not None and l1 <= l1_tolerance:
             break
     return p, it
+
+
+class PushExchange:
+    """State of the fused exchange (world <= 8): two q buffers per rank in
+    torch symmetric memory (peer-mapped over NVLink), the peer pointer tables
+    for each parity and this shard's push masks.  Build once, run many."""
+
+    def __init__(self, n: int, plan: ShardPlan, rank: int, halo: HaloPlan, device=None, group=None):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+
+        if plan.world > 8:
+            raise ValueError("the fused push addresses at most 8 peers")
+        self.n, self.plan, self.rank, self.halo, self.device, self.group = n, plan, rank, halo, device, group
+        self.buf = symm_mem.empty(2 * n, dtype=torch.float64, device=device)
+        self.buf.zero_()
+        hdl = symm_mem.rendezvous(self.buf, (group or dist.group.WORLD).group_name)
+        ptrs = [int(hdl.buffer_ptrs[p]) for p in range(plan.world)]
+        self.dst = [torch.tensor([ptrs[p] + par * n * 8 for p in range(plan.world)], dtype=torch.int64,
+                                 device=device) for par in (0, 1)]
+        self.qb = [self.buf[:n], self.buf[n:]]
+        self.mask = plan_push(halo, plan, rank, device)
+        self.recv = torch.empty(halo.recv_entries, dtype=torch.float64, device=device)
+
+    def run(self, graph, degrees_shard, alpha: float = 0.15, iterations: int = 10,
+            l1_tolerance: Optional[float] = None, dangling: str = "uniform"):
+        """sharded_pagerank with the exchange fused into the step kernel:
+        iteration t reads buffer t % 2; the kernel writes its rows of buffer
+        (t+1) % 2 locally and into every peer that reads them
+        (cmvg_pagerank_step_push).  The scalar all_reduce after each step
+        orders it before any peer's next step, so two buffers suffice.
+        Returns (p_shard, iterations_run)."""
+        import torch
+        import torch.distributed as dist
+
+        n, plan, halo, dev, group = self.n, self.plan, self.halo, self.device, self.group
+        a, b = plan.bounds(self.rank)
+        dt = torch.float64
+        deg = degrees_shard
+        p = torch.full((b - a,), 1.0 / n, dtype=dt, device=dev)
+        q0 = self.qb[0]
+        q0[a:b] = torch.where(deg > 0, p / deg.clamp(min=1).to(dt), torch.zeros_like(p))
+        # iteration 0's halo: one all_to_all (every later one is pushed by the kernel)
+        dist.all_to_all_single(self.recv, q0[a:b].index_select(0, halo.send_idx),
+                               output_split_sizes=halo.recv_counts, input_split_sizes=halo.send_counts, group=group)
+        q0.index_copy_(0, halo.recv_cols, self.recv)
+        part = torch.zeros(2, dtype=dt, device=dev)
+        part[0] = p[deg == 0].sum()
+        dist.all_reduce(part, group=group)
+        dmass = float(part[0].item())
+        p_next = torch.empty_like(p)
+        it = 0
+        for it in range(1, iterations + 1):
+            cur, nxt = (it - 1) % 2, it % 2
+            graph.pagerank_step(self.qb[cur], deg, alpha, dmass, dangling, p if l1_tolerance is not None else None,
+                                p_next, self.qb[nxt][a:b], part, push_mask=self.mask, push_dst=self.dst[nxt])
+            dist.all_reduce(part, group=group)
+            dmass = float(part[0].item())
+            l1 = float(part[1].item())
+            p, p_next = p_next, p
+            if l1_tolerance is not None and l1 <= l1_tolerance:
+                break
+        return p, it
 
 
 def gpu_step_fn(graph, degrees_shard, dangling: str = "uniform"):

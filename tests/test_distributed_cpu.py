@@ -104,3 +104,43 @@ def test_shard_plan_block_aligned():
     for (a, b), (c, d) in zip(bounds, bounds[1:]):
         assert b == c and a % 1024 == 0
     assert plan.chunk % 1024 == 0
+
+
+def _push_worker(rank, world, port, n, out):
+    from paper_1708_07271_b200.distributed import plan_push
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    g = _graph(n, 5)
+    at = g.transpose()
+    plan = plan_shards(n, world, 512)
+    a, b = plan.bounds(rank)
+    ro, co = at.row_offsets, at.cols
+    rs = np.unique(co[ro[a]:ro[b]]).astype(np.uint32)
+    mask = plan_push(plan_halo(rs, plan, rank), plan, rank)
+    full = [None] * world
+    dist.all_gather_object(full, (rank, rs.tolist(), mask.numpy().tolist()))
+    if rank == 0:
+        import pickle
+
+        pickle.dump(full, open(out, "wb"))
+    dist.destroy_process_group()
+
+
+def test_push_masks_match_read_sets(tmp_path):
+    """plan_push: bit p of shard-row k is set exactly when rank p's read set
+    holds that global row (and p is not the owner)."""
+    import pickle
+
+    world, n = 3, 4000
+    out = str(tmp_path / "m.pkl")
+    mp.spawn(_push_worker, args=(world, _free_port(), n, out), nprocs=world, join=True)
+    full = sorted(pickle.load(open(out, "rb")))
+    plan = plan_shards(n, world, 512)
+    reads = [set(r) for _, r, _ in full]
+    for rank, _, mask in full:
+        a, b = plan.bounds(rank)
+        assert len(mask) == b - a
+        for k, m in enumerate(mask):
+            want = sum(1 << p for p in range(world) if p != rank and (a + k) in reads[p])
+            assert m == want, (rank, k, m, want)

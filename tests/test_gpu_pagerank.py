@@ -155,3 +155,70 @@ def test_pagerank_shard_steps_halo_read_set(cuda, window):
         dmass = float(tot[0])
     want, _ = oracle_pr(g, iterations=20)
     assert rel(p.cpu().numpy(), want) <= 1e-12
+
+
+def test_pagerank_shard_steps_fused_push(cuda):
+    """The fused exchange (cmvg_pagerank_step_push): three shards on one GPU,
+    each with its own pair of q buffers; a shard's kernel writes its q' rows
+    locally and stores them into the buffers of the shards whose read set
+    holds them (here plain local buffers stand in for NVLink peer memory --
+    the kernel only sees pointers).  Nothing else moves q; every entry outside
+    a shard's rows and read set stays NaN."""
+    import torch
+
+    from paper_1708_07271_b200.distributed import plan_shards
+
+    g = make_graph(3, n=(1 << 16) + 300)
+    n = g.n
+    s = bv_of_transpose(g)
+    world = 3
+    plan = plan_shards(n, world, 1024)
+    deg = torch.from_numpy(g.out_degrees().astype(np.int32)).cuda()
+    shards, reads = [], []
+    for r in range(world):
+        a, b = plan.bounds(r)
+        dgs = P.BvGraph(s, P.CreateOptions(row_begin=a, row_end=b))
+        shards.append((a, b, dgs))
+        reads.append(torch.from_numpy(dgs.read_set().astype(np.int64)).cuda())
+    masks = []
+    for r in range(world):  # bit p of row k: shard p reads global row a_r + k
+        a, b = plan.bounds(r)
+        m = torch.zeros(b - a, dtype=torch.uint8, device="cuda")
+        for p_ in range(world):
+            if p_ == r:
+                continue
+            rs = reads[p_]
+            rs = rs[(rs >= a) & (rs < b)] - a
+            m[rs] |= 1 << p_
+        masks.append(m)
+    nan = float("nan")
+    qb = [[torch.full((n,), nan, dtype=torch.float64, device="cuda") for _ in range(2)] for _ in range(world)]
+    dst = [torch.tensor([qb[p_][par].data_ptr() for p_ in range(world)], dtype=torch.int64, device="cuda")
+           for par in (0, 1)]
+    p = torch.full((n,), 1.0 / n, dtype=torch.float64, device="cuda")
+    q0 = torch.where(deg > 0, p / deg.clamp(min=1).double(), torch.zeros_like(p))
+    for r in range(world):  # iteration 0: own rows and read set (what the halo all_to_all delivers)
+        a, b = plan.bounds(r)
+        qb[r][0][a:b] = q0[a:b]
+        qb[r][0][reads[r]] = q0[reads[r]]
+    dmass = float(p[deg == 0].sum())
+    for it in range(1, 21):
+        cur, nxt = (it - 1) % 2, it % 2
+        p_next = torch.empty_like(p)
+        tot = torch.zeros(2, dtype=torch.float64, device="cuda")
+        for r, (a, b, dgs) in enumerate(shards):
+            part = torch.zeros(2, dtype=torch.float64, device="cuda")
+            dgs.pagerank_step(qb[r][cur], deg[a:b], 0.15, dmass, "uniform", p[a:b], p_next[a:b], qb[r][nxt][a:b],
+                              part, push_mask=masks[r], push_dst=dst[nxt])
+            tot += part
+        for r in range(world):  # the next iteration reads only pushed / own entries: poison the rest
+            a, b = plan.bounds(r)
+            keep = torch.zeros(n, dtype=torch.bool, device="cuda")
+            keep[a:b] = True
+            keep[reads[r]] = True
+            qb[r][nxt].masked_fill_(~keep, nan)
+            qb[r][cur].fill_(nan)
+        p = p_next
+        dmass = float(tot[0])
+    want, _ = oracle_pr(g, iterations=20)
+    assert rel(p.cpu().numpy(), want) <= 1e-12

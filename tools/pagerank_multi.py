@@ -1,11 +1,12 @@
 """Sharded PageRank on config 3 (A^T of a copy model), one process per GPU.
 
     python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 \\
-        --master-port 29511 tools/pagerank_multi.py [--n-log2 26] [--iters 50] [--exchange halo|full]
+        --master-port 29511 tools/pagerank_multi.py [--n-log2 26] [--iters 50] [--exchange push|halo|full]
 
 Each rank builds the BV stream of A^T (deterministic), owns a block-aligned
-row shard (`plan_shards`), and runs `sharded_pagerank` with the fused GPU step;
-the q exchange is the full all_gather or the halo all_to_all.  Rank 0 prints
+row shard (`plan_shards`), and runs the fused GPU step; the q exchange is the
+kernel's own push into the peers' symmetric-memory buffers (default), the halo
+all_to_all, or the full all_gather.  Rank 0 prints
 one JSON line: iterations/s (device time, max over ranks), the halo volume,
 and -- for n <= 2^22 -- parity against the CPU oracle.
 """
@@ -24,13 +25,14 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n-log2", type=int, default=26)
     ap.add_argument("--iters", type=int, default=50)
-    ap.add_argument("--exchange", choices=["halo", "full"], default="halo")
+    ap.add_argument("--exchange", choices=["push", "halo", "full"], default="push")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
 
     import paper_1708_07271_b200 as P
-    from paper_1708_07271_b200.distributed import gather_to_rank0, gpu_step_fn, plan_halo, plan_shards, sharded_pagerank
+    from paper_1708_07271_b200.distributed import (PushExchange, gather_to_rank0, gpu_step_fn, plan_halo,
+                                                   plan_shards, sharded_pagerank)
 
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
@@ -49,14 +51,20 @@ def main():
     build_s = time.time() - t0
     deg_all = g.out_degrees()
     deg = torch.from_numpy(deg_all[a:b].astype(np.int32)).to(dev)
-    halo = plan_halo(dg.read_set(), plan, rank, device=dev) if args.exchange == "halo" else None
+    halo = plan_halo(dg.read_set(), plan, rank, device=dev) if args.exchange != "full" else None
     step = gpu_step_fn(dg, deg)
-    sharded_pagerank(step, deg, n, plan, rank, iterations=2, device=dev, halo=halo)  # warm-up
+    push = PushExchange(n, plan, rank, halo, device=dev) if args.exchange == "push" else None
+
+    def run(iters):
+        if push is not None:
+            return push.run(dg, deg, iterations=iters)
+        return sharded_pagerank(step, deg, n, plan, rank, iterations=iters, device=dev, halo=halo)
+    run(2)  # warm-up
     torch.cuda.synchronize()
     dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    p, it = sharded_pagerank(step, deg, n, plan, rank, iterations=args.iters, device=dev, halo=halo)
+    p, it = run(args.iters)
     e1.record()
     torch.cuda.synchronize()
     ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
