@@ -634,7 +634,12 @@ int cmvg_decode_csr(cmvg_graph* g, uint64_t* row_offsets, uint32_t* cols, int pt
       ro = dro.as<uint64_t>();
       co = dcols.as<uint32_t>();
     }
-    bv_seg_decode<<<(unsigned)((g->nseg + tpb - 1) / tpb), tpb, 0, st>>>(s, segbase.as<uint64_t>(), ro, co, err.as<int>());
+    if (getenv("CMVG_SERIAL_DECODE"))  // the serial decoder, for tests
+      bv_seg_decode<<<(unsigned)((g->nseg + tpb - 1) / tpb), tpb, 0, st>>>(s, segbase.as<uint64_t>(), ro, co,
+                                                                          err.as<int>());
+    else
+      bv_seg_decode_warp<<<(unsigned)((g->nseg + 3) / 4), 128, 0, st>>>(s, segbase.as<uint64_t>(), ro, co,
+                                                                        err.as<int>());
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaMemcpyAsync(&herr, err.p, 4, cudaMemcpyDeviceToHost, st));
     if (ptr_kind == CMVG_HOST) {

@@ -30,6 +30,10 @@ struct DevBits {
     nb = 64 - skip;
     fill();
   }
+  // absolute bit position of the next unread bit (stream base `base`)
+  __device__ __forceinline__ uint64_t bitpos(const uint32_t* base) const {
+    return ((uint64_t)(p - base) << 5) - (uint64_t)nb;
+  }
   __device__ __forceinline__ void fill() {
     if (nb <= 32) {
       cur |= (uint64_t)(*p++) << (32 - nb);

@@ -49,3 +49,22 @@ def test_decode_rejects_corruption(cuda):
     bad = P.BvStream.from_words(g.n, g.m, s.params, w, s.stats()["stream_bits"], s.segment_offsets())
     with pytest.raises((P.CorruptionError, ValueError, IndexError)):
         P.BvGraph(bad)  # the host builder validates the stream first
+
+
+def test_decode_warp_fallbacks_and_lists(cuda):
+    """The warp-cooperative decoder's per-warp lists overflow on purpose:
+    > 512 residuals, > 1024 copied entries, > 64 intervals, > 128 copy blocks
+    (serial row fallback), next to rows that fit; bit-exact either way."""
+    rng = np.random.default_rng(21)
+    n = 6000
+    rows = [sorted(set(rng.integers(0, n, 5).tolist())) for _ in range(n)]
+    big = sorted(set(rng.integers(0, n, 2600).tolist()))
+    rows[100] = big                                     # > 512 residuals
+    rows[101] = big[:-3]                                # copies > 1024 entries of row 100
+    rows[102] = big[::2]                                # many alternating copy blocks vs row 100
+    rows[2000] = sorted(set(x for a in range(0, 5000, 60) for x in range(a, a + 5)))  # > 64 intervals
+    rows[2001] = rows[2000][:-40] + [5990]
+    g = csr_from_rows(rows)
+    s = P.BvStream.encode(g, P.BvParams())
+    ro, co = P.BvGraph(s).decode_csr()
+    assert np.array_equal(ro, g.row_offsets) and np.array_equal(co, g.columns)
