@@ -7,6 +7,11 @@
 
 #include "bits.hpp"
 
+#include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 namespace cmvg {
 namespace {
 
@@ -50,6 +55,26 @@ void split_row(const HostCsr& g, uint32_t i, uint32_t r, uint32_t lmin, RowParts
 
 inline uint32_t bits_of(uint64_t v) { return v ? 64u - (uint32_t)__builtin_clzll(v) : 0u; }
 
+// LSD radix sort (two 16-bit digits): the per-block column lists (~10^4
+// entries) sort ~5x faster than with std::sort
+void radix_sort_u32(std::vector<uint32_t>& v) {
+  if (v.size() < 256) {
+    std::sort(v.begin(), v.end());
+    return;
+  }
+  thread_local std::vector<uint32_t> tmp;
+  thread_local std::vector<uint32_t> cnt;
+  tmp.resize(v.size());
+  for (int pass = 0; pass < 2; ++pass) {
+    const int sh = 16 * pass;
+    cnt.assign(65537, 0);
+    for (uint32_t x : v) ++cnt[((x >> sh) & 0xffffu) + 1];
+    for (size_t d = 0; d < 65536; ++d) cnt[d + 1] += cnt[d];
+    for (uint32_t x : v) tmp[cnt[(x >> sh) & 0xffffu]++] = x;
+    v.swap(tmp);
+  }
+}
+
 struct RowMeta {
   uint32_t r, nm, ns, ni, wp, wl;
   bool far;
@@ -69,18 +94,16 @@ inline uint32_t bits32(const std::vector<uint32_t>& w, uint64_t pos, uint64_t en
   return v;
 }
 
-// BV-S block stream from the block's rows (layout.hpp).
+// BV-S block stream from the block's rows (layout.hpp).  Units and their
+// codes live in flat per-block arrays (no per-unit allocations).
 struct Unit {
   uint32_t k, r, nm, np, ni;
   bool primary;
-  std::vector<uint32_t> words;  // far / class-32 encodings
-  std::vector<uint16_t> pc;     // near class-16: point codes (padded index | minus << 15)
-  std::vector<uint32_t> iw;     // near class-16: interval words (left - wlo) << 16 | len
+  uint32_t pc0, iw0, w0, nw;  // near: codes at pcs[pc0, +np), intervals at iws[iw0, +ni); else words at wds[w0, +nw)
 };
 struct URow {  // a row's units (adjacent lanes when there is more than one)
-  uint32_t k;
+  uint32_t k, u0, nu;
   bool c32, far;
-  std::vector<Unit> units;
 };
 
 void emit_bvs(const RowParts* rps, const RowMeta* meta, const BitWriter& body, uint32_t nr, uint64_t wlo, uint32_t W,
@@ -91,8 +114,17 @@ void emit_bvs(const RowParts* rps, const RowMeta* meta, const BitWriter& body, u
     return d >= -(int64_t)kBvsBias16 && d < (int64_t)kBvsBias16;
   };
   auto code16 = [&](uint32_t c) { return (uint32_t)((int64_t)c - (int64_t)wlo + kBvsBias16); };
-  std::vector<URow> single, multi;
-  std::vector<uint32_t> hrows, pts;
+  thread_local std::vector<Unit> units;
+  thread_local std::vector<uint16_t> pcs;
+  thread_local std::vector<uint32_t> iws, wds;
+  thread_local std::vector<URow> single, multi;
+  units.clear();
+  pcs.clear();
+  iws.clear();
+  wds.clear();
+  single.clear();
+  multi.clear();
+  std::vector<uint32_t> hrows;
   for (uint32_t k = 0; k < nr; ++k) {
     const RowParts& rp = rps[k];
     const uint32_t nm = (uint32_t)rp.minus.size(), np = nm + (uint32_t)rp.res.size(), ni = (uint32_t)rp.ints.size();
@@ -102,22 +134,18 @@ void emit_bvs(const RowParts* rps, const RowMeta* meta, const BitWriter& body, u
       hrows.push_back(k);
       continue;
     }
-    pts.assign(rp.minus.begin(), rp.minus.end());
-    pts.insert(pts.end(), rp.res.begin(), rp.res.end());
-    URow row;
-    row.k = k;
-    row.c32 = false;
-    row.far = false;
-    for (uint32_t c : pts) {
-      row.c32 |= !off_ok(c);
-      row.far |= !inwin(c);
+    auto pt = [&](uint32_t t) { return t < nm ? rp.minus[t] : rp.res[t - nm]; };
+    URow row{k, (uint32_t)units.size(), nu, false, false};
+    for (uint32_t t = 0; t < np; ++t) {
+      row.c32 |= !off_ok(pt(t));
+      row.far |= !inwin(pt(t));
     }
     for (const auto& iv : rp.ints) {
       row.c32 |= !off_ok(iv.first) || (iv.second - lmin) >= 65536u;
       row.far |= !inwin(iv.first) || !inwin((uint64_t)iv.first + iv.second - 1);
     }
     for (uint32_t j = 0; j < nu; ++j) {
-      Unit u;
+      Unit u{};
       u.k = k;
       u.primary = j == 0;
       u.r = meta[k].r;
@@ -127,49 +155,52 @@ void emit_bvs(const RowParts* rps, const RowMeta* meta, const BitWriter& body, u
       u.np = p1 - p0;
       u.ni = q1 - q0;
       u.nm = nm > p0 ? std::min(nm, p1) - p0 : 0;
+      u.pc0 = (uint32_t)pcs.size();
+      u.iw0 = (uint32_t)iws.size();
+      u.w0 = (uint32_t)wds.size();
       if (!row.c32 && !row.far) {
         for (uint32_t t = p0; t < p1; ++t)
-          u.pc.push_back((uint16_t)(bvs_pad_index((uint32_t)(pts[t] - wlo)) | (t < nm ? 0x8000u : 0u)));
-        for (uint32_t t = q0; t < q1; ++t)
-          u.iw.push_back(((uint32_t)(rp.ints[t].first - wlo) << 16) | rp.ints[t].second);
+          pcs.push_back((uint16_t)(bvs_pad_index((uint32_t)(pt(t) - wlo)) | (t < nm ? 0x8000u : 0u)));
+        for (uint32_t t = q0; t < q1; ++t) iws.push_back(((uint32_t)(rp.ints[t].first - wlo) << 16) | rp.ints[t].second);
       } else if (!row.c32) {
         for (uint32_t t = p0; t < p1; t += 2) {
-          const uint32_t hi = code16(pts[t]), lo = t + 1 < p1 ? code16(pts[t + 1]) : 0u;
-          u.words.push_back((hi << 16) | lo);
+          const uint32_t hi = code16(pt(t)), lo = t + 1 < p1 ? code16(pt(t + 1)) : 0u;
+          wds.push_back((hi << 16) | lo);
         }
-        for (uint32_t t = q0; t < q1; ++t) u.words.push_back((code16(rp.ints[t].first) << 16) | (rp.ints[t].second - lmin));
+        for (uint32_t t = q0; t < q1; ++t) wds.push_back((code16(rp.ints[t].first) << 16) | (rp.ints[t].second - lmin));
       } else {
-        for (uint32_t t = p0; t < p1; ++t) u.words.push_back(pts[t]);
+        for (uint32_t t = p0; t < p1; ++t) wds.push_back(pt(t));
         for (uint32_t t = q0; t < q1; ++t) {
-          u.words.push_back(rp.ints[t].first);
-          u.words.push_back(rp.ints[t].second - lmin);
+          wds.push_back(rp.ints[t].first);
+          wds.push_back(rp.ints[t].second - lmin);
         }
       }
-      row.units.push_back(std::move(u));
+      u.nw = (uint32_t)wds.size() - u.w0;
+      units.push_back(u);
     }
-    (nu == 1 ? single : multi).push_back(std::move(row));
+    (nu == 1 ? single : multi).push_back(row);
   }
-  // slices: lists of (row, unit) lanes; groups (class32, far) never share a slice
+  // slices: lists of unit lanes; groups (class32, far) never share a slice
   struct Slice {
-    std::vector<const Unit*> lanes;
+    std::vector<uint32_t> lanes;  // unit indices
     bool c32, far, multi;
   };
   std::vector<Slice> slices;
   auto gid = [](const URow& r) { return (r.c32 ? 0 : 2) + (r.far ? 0 : 1); };
   // multi-unit rows: by per-unit load (so a slice's lanes have similar work),
   // then unit count, packed first-fit
-  auto load = [](const URow& r) {
+  auto load = [&](const URow& r) {
     uint32_t p = 0, i = 0;
-    for (const Unit& u : r.units) {
-      p = std::max(p, u.np);
-      i = std::max(i, u.ni);
+    for (uint32_t q = 0; q < r.nu; ++q) {
+      p = std::max(p, units[r.u0 + q].np);
+      i = std::max(i, units[r.u0 + q].ni);
     }
     return p + 2 * i;
   };
   std::stable_sort(multi.begin(), multi.end(), [&](const URow& a, const URow& b) {
     if (gid(a) != gid(b)) return gid(a) < gid(b);
     if (load(a) != load(b)) return load(a) > load(b);
-    return a.units.size() > b.units.size();
+    return a.nu > b.nu;
   });
   for (size_t a = 0; a < multi.size();) {
     size_t e = a;
@@ -178,22 +209,23 @@ void emit_bvs(const RowParts* rps, const RowMeta* meta, const BitWriter& body, u
     for (size_t q = a; q < e; ++q) {
       const URow& row = multi[q];
       size_t t = first;
-      while (t < slices.size() && slices[t].lanes.size() + row.units.size() > 32) ++t;
+      while (t < slices.size() && slices[t].lanes.size() + row.nu > 32) ++t;
       if (t == slices.size()) slices.push_back(Slice{{}, row.c32, row.far, true});
-      for (const Unit& u : row.units) slices[t].lanes.push_back(&u);
+      for (uint32_t u = 0; u < row.nu; ++u) slices[t].lanes.push_back(row.u0 + u);
     }
     a = e;
   }
   // single-unit rows: by (#intervals, #points) desc, dealt 32 per slice
   std::stable_sort(single.begin(), single.end(), [&](const URow& a, const URow& b) {
     if (gid(a) != gid(b)) return gid(a) < gid(b);
-    if (a.units[0].ni != b.units[0].ni) return a.units[0].ni > b.units[0].ni;
-    return a.units[0].np > b.units[0].np;
+    const Unit &ua = units[a.u0], &ub = units[b.u0];
+    if (ua.ni != ub.ni) return ua.ni > ub.ni;
+    return ua.np > ub.np;
   });
   for (size_t a = 0; a < single.size();) {
     Slice sl{{}, single[a].c32, single[a].far, false};
     size_t e = a;
-    while (e < single.size() && e - a < 32 && gid(single[e]) == gid(single[a])) sl.lanes.push_back(&single[e++].units[0]);
+    while (e < single.size() && e - a < 32 && gid(single[e]) == gid(single[a])) sl.lanes.push_back(single[e++].u0);
     slices.push_back(std::move(sl));
     a = e;
   }
@@ -206,19 +238,20 @@ void emit_bvs(const RowParts* rps, const RowMeta* meta, const BitWriter& body, u
     const bool nearc16 = !sl.c32 && !sl.far;
     so[kBvsHead + 2 * s] = (uint32_t)so.size();
     uint32_t mnp = 0, mni = 0, nq = 0;
-    for (const Unit* u : sl.lanes) {
-      mnp = std::max(mnp, u->np);
-      mni = std::max(mni, u->ni);
-      nq = std::max<uint32_t>(nq, (uint32_t)u->words.size());
-      st.lane_words_used += nearc16 ? (u->np + 1) / 2 + u->ni : u->words.size();
-      st.lane_iters_used += u->np + u->ni;
+    for (uint32_t ui : sl.lanes) {
+      const Unit& u = units[ui];
+      mnp = std::max(mnp, u.np);
+      mni = std::max(mni, u.ni);
+      nq = std::max<uint32_t>(nq, u.nw);
+      st.lane_words_used += nearc16 ? (u.np + 1) / 2 + u.ni : u.nw;
+      st.lane_iters_used += u.np + u.ni;
     }
     if (nearc16) nq = (mnp + 1) / 2 + mni;  // rectangular: points then intervals
     so.push_back(make_smeta(mnp, mni, sl.c32, sl.far, sl.multi));
     so[kBvsHead + 2 * s + 1] = so.back();  // the table repeats the meta word
     for (size_t l = 0; l < 32; ++l) {
       if (l < sl.lanes.size()) {
-        const Unit& u = *sl.lanes[l];
+        const Unit& u = units[sl.lanes[l]];
         so.push_back(make_uh(u.primary, u.primary ? u.k : 0u, u.primary ? u.r : 0u, u.nm, u.np, u.ni));
       } else {
         so.push_back(0u);
@@ -231,18 +264,18 @@ void emit_bvs(const RowParts* rps, const RowMeta* meta, const BitWriter& body, u
       // zero entry) then mni interval words (0 = empty interval)
       const uint32_t zc = bvs_pad_index(W), mnpw = (mnp + 1) / 2;
       for (size_t l = 0; l < 32; ++l) {
-        const Unit* u = l < sl.lanes.size() ? sl.lanes[l] : nullptr;
+        const Unit* u = l < sl.lanes.size() ? &units[sl.lanes[l]] : nullptr;
         for (uint32_t q = 0; q < mnpw; ++q) {
-          const uint32_t c0 = u && 2 * q < u->pc.size() ? u->pc[2 * q] : zc;
-          const uint32_t c1 = u && 2 * q + 1 < u->pc.size() ? u->pc[2 * q + 1] : zc;
+          const uint32_t c0 = u && 2 * q < u->np ? pcs[u->pc0 + 2 * q] : zc;
+          const uint32_t c1 = u && 2 * q + 1 < u->np ? pcs[u->pc0 + 2 * q + 1] : zc;
           so[b0 + (size_t)q * 32 + l] = (c0 << 16) | c1;
         }
-        for (uint32_t q = 0; q < mni; ++q) so[b0 + (size_t)(mnpw + q) * 32 + l] = u && q < u->iw.size() ? u->iw[q] : 0u;
+        for (uint32_t q = 0; q < mni; ++q) so[b0 + (size_t)(mnpw + q) * 32 + l] = u && q < u->ni ? iws[u->iw0 + q] : 0u;
       }
     } else {
       for (size_t l = 0; l < sl.lanes.size(); ++l) {
-        const Unit& u = *sl.lanes[l];
-        for (size_t q = 0; q < u.words.size(); ++q) so[b0 + q * 32 + l] = u.words[q];
+        const Unit& u = units[sl.lanes[l]];
+        for (uint32_t q = 0; q < u.nw; ++q) so[b0 + (size_t)q * 32 + l] = wds[u.w0 + q];
       }
     }
     st.lane_words += (uint64_t)nq * 32;
@@ -275,95 +308,122 @@ void emit_bvs(const RowParts* rps, const RowMeta* meta, const BitWriter& body, u
 void emit_bvt(const RowParts* rps, const RowMeta* meta, uint32_t nr, uint32_t B, uint64_t wlo, uint32_t W,
               std::vector<uint32_t>& so, std::vector<uint32_t>& far_cols, BvtStats& st) {
   constexpr uint32_t kUnit = 16, kMaxUnits = 32;
-  // target -> codes (k | minus << 15)
-  std::vector<std::vector<uint16_t>> tgt(2 * (size_t)W);
-  std::vector<std::pair<uint32_t, uint16_t>> far;  // (column, code)
-  auto point = [&](uint64_t col, uint32_t code) {
-    if (col >= wlo && col < wlo + W) tgt[col - wlo].push_back((uint16_t)code);
-    else far.push_back({(uint32_t)col, (uint16_t)code});
-  };
-  for (uint32_t k = 0; k < nr; ++k) {
-    const RowParts& rp = rps[k];
-    for (uint32_t c : rp.minus) point(c, k | 0x8000u);
-    for (uint32_t c : rp.res) point(c, k);
-    for (const auto& iv : rp.ints) {
-      const uint64_t a = iv.first, e = (uint64_t)iv.first + iv.second;
-      const uint64_t ia = std::max<uint64_t>(a, wlo), ie = std::min<uint64_t>(e, wlo + W);
-      if (ia < ie) {  // in-window part: two difference entries
-        tgt[W + (ia - wlo)].push_back((uint16_t)k);
-        if (ie < wlo + W) tgt[W + (ie - wlo)].push_back((uint16_t)(k | 0x8000u));
+  // contributions grouped by target with flat arrays (counting sort for the
+  // 2W window targets, a sort for the few far columns); codes k | minus << 15
+  // stay in row order within a target
+  const uint32_t W2 = 2 * W;
+  thread_local std::vector<uint32_t> cnt;
+  thread_local std::vector<uint16_t> flat;
+  thread_local std::vector<std::pair<uint32_t, uint16_t>> far;
+  cnt.assign(W2 + 1, 0);
+  far.clear();
+  auto near_t = [&](uint64_t col) { return (uint32_t)(col - wlo); };
+  auto inwin = [&](uint64_t col) { return col >= wlo && col < wlo + W; };
+  for (int pass = 0; pass < 2; ++pass) {
+    auto put = [&](uint32_t t, uint32_t code) {
+      if (pass == 0) ++cnt[t + 1];
+      else flat[cnt[t]++] = (uint16_t)code;
+    };
+    for (uint32_t k = 0; k < nr; ++k) {
+      const RowParts& rp = rps[k];
+      for (uint32_t c : rp.minus) {
+        if (inwin(c)) put(near_t(c), k | 0x8000u);
+        else if (pass == 0) far.push_back({c, (uint16_t)(k | 0x8000u)});
       }
-      for (uint64_t c = a; c < e; ++c)  // out-of-window part: one far entry per column
-        if (c < ia || c >= ie) far.push_back({(uint32_t)c, (uint16_t)k});
+      for (uint32_t c : rp.res) {
+        if (inwin(c)) put(near_t(c), k);
+        else if (pass == 0) far.push_back({c, (uint16_t)k});
+      }
+      for (const auto& iv : rp.ints) {
+        const uint64_t a0 = iv.first, e0 = (uint64_t)iv.first + iv.second;
+        const uint64_t ia = std::max<uint64_t>(a0, wlo), ie = std::min<uint64_t>(e0, wlo + W);
+        if (ia < ie) {  // in-window part: two difference entries
+          put(W + near_t(ia), k);
+          if (ie < wlo + W) put(W + near_t(ie), k | 0x8000u);
+        }
+        if (pass == 0)
+          for (uint64_t c = a0; c < e0; ++c)  // out-of-window part: one far entry per column
+            if (c < ia || c >= ie) far.push_back({(uint32_t)c, (uint16_t)k});
+      }
+    }
+    if (pass == 0) {
+      for (uint32_t t = 0; t < W2; ++t) cnt[t + 1] += cnt[t];
+      flat.resize(cnt[W2] + far.size());
+    } else {
+      for (uint32_t t = W2; t > 0; --t) cnt[t] = cnt[t - 1];  // restore the starts
+      cnt[0] = 0;
     }
   }
   std::sort(far.begin(), far.end());
   far_cols.clear();
   struct T {
-    uint32_t target;
-    std::vector<uint16_t> codes;
+    uint32_t target, start, count;
   };
   std::vector<T> targets;
-  for (uint32_t t = 0; t < 2 * W; ++t)
-    if (!tgt[t].empty()) targets.push_back({t, std::move(tgt[t])});
-  for (size_t q = 0; q < far.size();) {
-    size_t e = q;
-    T t{2 * W + (uint32_t)far_cols.size(), {}};
-    while (e < far.size() && far[e].first == far[q].first) t.codes.push_back(far[e++].second);
-    far_cols.push_back(far[q].first);
-    targets.push_back(std::move(t));
-    q = e;
+  for (uint32_t t = 0; t < W2; ++t)
+    if (cnt[t + 1] > cnt[t]) targets.push_back({t, cnt[t], cnt[t + 1] - cnt[t]});
+  {
+    uint32_t pos = cnt[W2];
+    for (size_t q = 0; q < far.size();) {
+      size_t e = q;
+      const uint32_t start = pos;
+      while (e < far.size() && far[e].first == far[q].first) flat[pos++] = far[e++].second;
+      targets.push_back({W2 + (uint32_t)far_cols.size(), start, pos - start});
+      far_cols.push_back(far[q].first);
+      q = e;
+    }
   }
-  if (2 * W + far_cols.size() > 0x3fffffffu) throw std::runtime_error("BV-T: too many targets in a block");
+  if (W2 + far_cols.size() > 0x3fffffffu) throw std::runtime_error("BV-T: too many targets in a block");
   // units: <= kUnit codes, balanced; 1 unit -> single slices, 2..32 -> multi, more -> heavy
   struct U {
-    uint32_t target;
+    uint32_t target, start, count;
     bool primary;
-    std::vector<uint16_t> codes;
   };
-  std::vector<std::vector<U>> single_rows, multi_rows;
+  std::vector<U> units;
+  std::vector<uint32_t> singles;                       // unit index
+  std::vector<std::pair<uint32_t, uint32_t>> multis;   // (first unit, #units)
   std::vector<const T*> heavy;
   for (const T& t : targets) {
-    const uint32_t ne = (uint32_t)t.codes.size();
+    const uint32_t ne = t.count;
     st.entries += ne;
     const uint32_t nu = (ne + kUnit - 1) / kUnit;
     if (nu > kMaxUnits) {
       heavy.push_back(&t);
       continue;
     }
-    std::vector<U> us;
+    const uint32_t first = (uint32_t)units.size();
     for (uint32_t j = 0; j < nu; ++j) {
       const uint32_t p0 = (uint32_t)((uint64_t)j * ne / nu), p1 = (uint32_t)((uint64_t)(j + 1) * ne / nu);
-      us.push_back(U{t.target, j == 0, std::vector<uint16_t>(t.codes.begin() + p0, t.codes.begin() + p1)});
+      units.push_back(U{t.target, t.start + p0, p1 - p0, j == 0});
     }
-    (nu == 1 ? single_rows : multi_rows).push_back(std::move(us));
+    if (nu == 1) singles.push_back(first);
+    else multis.push_back({first, nu});
   }
   struct Slice {
     std::vector<const U*> lanes;
     bool multi;
   };
   std::vector<Slice> slices;
-  auto load = [](const std::vector<U>& r) {
-    size_t m = 0;
-    for (const U& u : r) m = std::max(m, u.codes.size());
+  auto load = [&](const std::pair<uint32_t, uint32_t>& r) {
+    uint32_t m = 0;
+    for (uint32_t q = 0; q < r.second; ++q) m = std::max(m, units[r.first + q].count);
     return m;
   };
-  std::stable_sort(multi_rows.begin(), multi_rows.end(), [&](const std::vector<U>& a, const std::vector<U>& b) {
+  std::stable_sort(multis.begin(), multis.end(), [&](const auto& a, const auto& b) {
     if (load(a) != load(b)) return load(a) > load(b);
-    return a.size() > b.size();
+    return a.second > b.second;
   });
-  for (const auto& r : multi_rows) {
+  for (const auto& r : multis) {
     size_t t = 0;
-    while (t < slices.size() && slices[t].lanes.size() + r.size() > 32) ++t;
+    while (t < slices.size() && slices[t].lanes.size() + r.second > 32) ++t;
     if (t == slices.size()) slices.push_back(Slice{{}, true});
-    for (const U& u : r) slices[t].lanes.push_back(&u);
+    for (uint32_t q = 0; q < r.second; ++q) slices[t].lanes.push_back(&units[r.first + q]);
   }
-  std::stable_sort(single_rows.begin(), single_rows.end(), [&](const std::vector<U>& a, const std::vector<U>& b) {
-    return a[0].codes.size() > b[0].codes.size();
-  });
-  for (size_t a = 0; a < single_rows.size(); a += 32) {
+  std::stable_sort(singles.begin(), singles.end(),
+                   [&](uint32_t a, uint32_t b) { return units[a].count > units[b].count; });
+  for (size_t a = 0; a < singles.size(); a += 32) {
     Slice sl{{}, false};
-    for (size_t q = a; q < std::min(single_rows.size(), a + 32); ++q) sl.lanes.push_back(&single_rows[q][0]);
+    for (size_t q = a; q < std::min(singles.size(), a + 32); ++q) sl.lanes.push_back(&units[singles[q]]);
     slices.push_back(std::move(sl));
   }
   const uint32_t nsl = (uint32_t)slices.size(), nh = (uint32_t)heavy.size();
@@ -406,8 +466,8 @@ void emit_bvt(const RowParts* rps, const RowMeta* meta, uint32_t nr, uint32_t B,
     so[kBvtHead + 2 * s] = (uint32_t)so.size();
     uint32_t mne = 0;
     for (const U* u : sl.lanes) {
-      mne = std::max<uint32_t>(mne, (uint32_t)u->codes.size());
-      st.lane_iters_used += u->codes.size();
+      mne = std::max<uint32_t>(mne, u->count);
+      st.lane_iters_used += u->count;
     }
     so.push_back(make_tmeta(mne, sl.multi));
     so[kBvtHead + 2 * s + 1] = so.back();  // the table repeats the meta word
@@ -418,8 +478,8 @@ void emit_bvt(const RowParts* rps, const RowMeta* meta, uint32_t nr, uint32_t B,
     for (size_t l = 0; l < 32; ++l) {
       const U* u = l < sl.lanes.size() ? sl.lanes[l] : nullptr;
       for (uint32_t q = 0; q < mnw; ++q) {
-        const uint32_t c0 = u && 2 * q < u->codes.size() ? u->codes[2 * q] : zc;
-        const uint32_t c1 = u && 2 * q + 1 < u->codes.size() ? u->codes[2 * q + 1] : zc;
+        const uint32_t c0 = u && 2 * q < u->count ? flat[u->start + 2 * q] : zc;
+        const uint32_t c1 = u && 2 * q + 1 < u->count ? flat[u->start + 2 * q + 1] : zc;
         so[b0 + (size_t)q * 32 + l] = (c0 << 16) | c1;
       }
     }
@@ -429,10 +489,10 @@ void emit_bvt(const RowParts* rps, const RowMeta* meta, uint32_t nr, uint32_t B,
   std::vector<uint32_t> hc;
   for (const T* t : heavy) {
     so.push_back(t->target);
-    so.push_back((uint32_t)t->codes.size());
+    so.push_back(t->count);
     so.push_back((uint32_t)hc.size());
-    for (size_t q = 0; q < t->codes.size(); q += 2)
-      hc.push_back(((uint32_t)t->codes[q] << 16) | (q + 1 < t->codes.size() ? t->codes[q + 1] : zc));
+    for (uint32_t q = 0; q < t->count; q += 2)
+      hc.push_back(((uint32_t)flat[t->start + q] << 16) | (q + 1 < t->count ? flat[t->start + q + 1] : zc));
   }
   so[2] = (uint32_t)so.size();
   so.insert(so.end(), hc.begin(), hc.end());
@@ -441,6 +501,8 @@ void emit_bvt(const RowParts* rps, const RowMeta* meta, uint32_t nr, uint32_t B,
   st.heavy_targets += nh;
   st.far_slots += far_cols.size();
 }
+
+std::atomic<long long> g_tim[4];
 
 }  // namespace
 
@@ -483,6 +545,7 @@ BvdLayout build_bvd(const BvDecoded& dec, const BvParams& bp, const BvdOptions& 
       body.nbits = 0;
       uint64_t adds = 0, codes = 0;
       std::fill(hdr.begin(), hdr.end(), 0u);
+      auto tA = std::chrono::steady_clock::now();
       // pass 1: split rows, collect gathered columns, choose the x-window
       for (uint32_t k = 0; k < nr; ++k) {
         const uint32_t i = r0 + k;
@@ -499,7 +562,7 @@ BvdLayout build_bvd(const BvDecoded& dec, const BvParams& bp, const BvdOptions& 
         for (uint32_t c : rp.minus) cols.push_back(c);
         for (uint32_t c : rp.res) cols.push_back(c);
       }
-      std::sort(cols.begin(), cols.end());
+      radix_sort_u32(cols);
       uint64_t best = 0, best_lo = r0;
       for (size_t a = 0, e = 0; a < cols.size(); ++a) {
         while (e < cols.size() && cols[e] < (uint64_t)cols[a] + W) ++e;
@@ -579,7 +642,9 @@ BvdLayout build_bvd(const BvDecoded& dec, const BvParams& bp, const BvdOptions& 
       L.blocks[b].wlo = (uint32_t)lo;
       L.blocks[b].nwords = (uint32_t)(out.nbits / 32);
       L.blocks[b].nesc = (uint32_t)(escs.size() / 4);
+      auto tB = std::chrono::steady_clock::now();
       emit_bvs(rps.data(), meta.data(), body, nr, lo, W, bp.min_interval, sstream[b], bst[b]);
+      auto tC = std::chrono::steady_clock::now();
       {  // columns this block reads outside its x-window (read set of a shard)
         std::vector<uint32_t>& fc = bfar[b];
         fc.clear();
@@ -597,7 +662,13 @@ BvdLayout build_bvd(const BvDecoded& dec, const BvParams& bp, const BvdOptions& 
         std::sort(fc.begin(), fc.end());
         fc.erase(std::unique(fc.begin(), fc.end()), fc.end());
       }
+      auto tD = std::chrono::steady_clock::now();
       emit_bvt(rps.data(), meta.data(), nr, B, lo, W, tstream[b], tfar[b], tst[b]);
+      auto tE = std::chrono::steady_clock::now();
+      g_tim[0] += std::chrono::duration_cast<std::chrono::microseconds>(tB - tA).count();
+      g_tim[1] += std::chrono::duration_cast<std::chrono::microseconds>(tC - tB).count();
+      g_tim[2] += std::chrono::duration_cast<std::chrono::microseconds>(tD - tC).count();
+      g_tim[3] += std::chrono::duration_cast<std::chrono::microseconds>(tE - tD).count();
     }
   });
   uint64_t off = 0, maxw = 0, g_all = 0, g_in = 0;
@@ -711,6 +782,9 @@ BvdLayout build_bvd(const BvDecoded& dec, const BvParams& bp, const BvdOptions& 
     for (uint64_t t = 0; t < ntiles; ++t) L.farp_ptr[t + 1] += L.farp_ptr[t];
   }
   L.stats.block_table_bytes = (uint64_t)nb * sizeof(BvdBlockInfo);
+  if (getenv("CMVG_BUILD_TIMING"))
+    fprintf(stderr, "build_bvd thread-us: bvd %lld bvs %lld readset %lld bvt %lld\n", (long long)g_tim[0],
+            (long long)g_tim[1], (long long)g_tim[2], (long long)g_tim[3]);
   return L;
 }
 
