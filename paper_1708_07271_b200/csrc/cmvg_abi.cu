@@ -262,16 +262,18 @@ int cmvg_create(const cmvg_bvstream* s, const cmvg_create_opts* opts_in, cmvg_gr
       g->swords.upload(sw.data(), sw.size());
       g->sblocks.upload(sbl.data(), sbl.size());
       g->s_stream_bytes = (s1 - s0) * 4;
-      {  // read set: the blocks' x-windows and their out-of-window columns
-        std::vector<uint32_t>& rs = g->read_set;
-        rs.clear();
+      {  // read set: the blocks' x-windows and their out-of-window columns (bitmap, O(n))
+        std::vector<uint64_t> bm(((uint64_t)bs.n + 63) / 64, 0);
+        auto mark = [&](uint64_t c) { bm[c >> 6] |= 1ull << (c & 63); };
         for (uint32_t b = g->block_begin; b < block_end; ++b) {
           const uint64_t w0 = L.sblocks[b].wlo, w1 = std::min<uint64_t>(bs.n, w0 + L.dims.window);
-          for (uint64_t c = w0; c < w1; ++c) rs.push_back((uint32_t)c);
-          rs.insert(rs.end(), L.rfar.begin() + L.rfar_ptr[b], L.rfar.begin() + L.rfar_ptr[b + 1]);
+          for (uint64_t c = w0; c < w1; ++c) mark(c);
+          for (uint64_t q = L.rfar_ptr[b]; q < L.rfar_ptr[b + 1]; ++q) mark(L.rfar[q]);
         }
-        std::sort(rs.begin(), rs.end());
-        rs.erase(std::unique(rs.begin(), rs.end()), rs.end());
+        std::vector<uint32_t>& rs = g->read_set;
+        rs.clear();
+        for (uint64_t wi = 0; wi < bm.size(); ++wi)
+          for (uint64_t v = bm[wi]; v; v &= v - 1) rs.push_back((uint32_t)(wi * 64 + __builtin_ctzll(v)));
       }
       g->win_need.resize(sbl.size());
       uint64_t pm = 0;
