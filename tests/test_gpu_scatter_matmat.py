@@ -103,3 +103,24 @@ def test_matmat_device_and_social(cuda):
     og = oracle_csr(g)
     for c in (0, 7, 15):
         assert max_rel_err(Y[:, c], og.matvec(X[:, c].astype(np.float64), 8)) <= 1e-5
+
+
+@pytest.mark.parametrize("params", [dict(window=1, max_ref=1, min_interval=2, segment_rows=256),
+                                    dict(window=3, max_ref=0, min_interval=3, segment_rows=512),
+                                    dict(window=7, max_ref=2, min_interval=6, segment_rows=1024),
+                                    dict(window=0, max_ref=3, min_interval=4, segment_rows=1024)])
+def test_products_across_bv_params(cuda, params):
+    # every product on streams encoded with other BV parameters (window w,
+    # chain bound R, minimum interval Lmin, segment length)
+    g = make_graph(2, n=(1 << 15) + 123)
+    s = P.BvStream.encode(g, P.BvParams(**params))
+    dg = P.BvGraph(s)
+    x = x_uniform(g.n, 17)
+    assert max_rel_err(dg.matvec(x), oracle_csr(g).matvec(x, 8)) <= 1e-12
+    assert max_rel_err(dg.matvec(x, form="scatter"), oracle_left(g, x)) <= 1e-12
+    X = np.stack([x_uniform(g.n, 30 + c) for c in range(3)], 1).astype(np.float32)
+    Y = dg.matmat(X)
+    for c in range(3):
+        assert max_rel_err(Y[:, c], oracle_csr(g).matvec(X[:, c].astype(np.float64), 8)) <= 1e-5
+    ro, co = dg.decode_csr()
+    assert np.array_equal(ro, g.row_offsets) and np.array_equal(co, g.columns)
