@@ -167,7 +167,7 @@ __device__ __forceinline__ void mm_slices(const uint32_t* __restrict__ bs, const
           const uint32_t c = half ? (v & 0xffffu) : (v >> 16);
           if (c != zc) {
             const uint32_t p = c & 0x7fffu;
-            mm_add_near(m, p - p / 17u, (c >> 15) != 0, acc);
+            mm_add_near(m, p - p / 9u, (c >> 15) != 0, acc);
           }
         }
       }

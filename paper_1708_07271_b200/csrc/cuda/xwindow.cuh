@@ -1,29 +1,33 @@
 // The per-block x-window in shared memory: x[wlo, wlo + W) staged with
-// coalesced loads into a padded layout (16-entry tiles at a stride of 17
-// entries, so a thread can walk one tile with 2-way bank conflicts), plus an
-// exclusive prefix F of the window in double-double (hi fp64, lo fp32), built
-// in three parallel steps: P[j] within j's 16-entry tile (one thread per
-// tile), Q[t] over whole tiles (one warp), then F[j] = Q[j>>4] + P[j].  An
-// interval [a, e) is then F[e] - F[a]: one TwoSum, O(1) for any length, and
-// accurate to ~1e-28 absolute, so interval sums carry no rounding error into
-// the reference chain (the north star's O(1) interval evaluation from an
-// exclusive prefix of x).
+// coalesced loads into a padded layout (8-entry tiles at a stride of 9
+// entries, so a thread walks one tile with at most 2-way bank conflicts), plus
+// an exclusive prefix F of the window in double-double (hi fp64, lo fp32),
+// built in three parallel steps: the 8-entry tile totals (one thread per
+// tile), their exclusive prefix Q (one warp), then F within each tile
+// starting from Q (one thread per tile) -- x is read twice and F written
+// once.  An interval [a, e) is then F[e] - F[a]: one TwoSum, O(1) for any
+// length, and accurate to ~1e-28 absolute, so interval sums carry no rounding
+// error into the reference chain (the north star's O(1) interval evaluation
+// from an exclusive prefix of x).
 #pragma once
 #include <cstdint>
 
+#include "../host/layout.hpp"
+
 namespace cmvg {
 
-__host__ __device__ constexpr uint32_t xw_pad(uint32_t j) { return j + (j >> 4); }
+constexpr uint32_t kXwTile = 8;  // entries per tile (bvs_pad_index: stride 9)
+__host__ __device__ constexpr uint32_t xw_pad(uint32_t j) { return bvs_pad_index(j); }
 
 // bytes of the x-window region for W entries of type XT
 __host__ __device__ inline uint32_t xw_bytes(uint32_t W, uint32_t xsize, bool prefix) {
   const uint32_t padded = xw_pad(W) + 1;
   uint32_t b = ((padded * xsize + 15u) & ~15u);
   if (prefix) {
-    b += ((padded * 8u + 15u) & ~15u);          // P hi
-    b += ((padded * 4u + 15u) & ~15u);          // P lo
-    b += (((W / 16 + 1) * 8u + 15u) & ~15u);    // Q hi
-    b += (((W / 16 + 1) * 4u + 15u) & ~15u);    // Q lo
+    b += ((padded * 8u + 15u) & ~15u);                // F hi
+    b += ((padded * 4u + 15u) & ~15u);                // F lo
+    b += (((W / kXwTile + 1) * 8u + 15u) & ~15u);    // Q hi
+    b += (((W / kXwTile + 1) * 4u + 15u) & ~15u);    // Q lo
   }
   return b;
 }
@@ -56,7 +60,7 @@ struct XWin {
     s_pl = reinterpret_cast<float*>(p);
     p += (padded * 4u + 15u) & ~15u;
     s_th = reinterpret_cast<double*>(p);
-    p += ((Wn / 16 + 1) * 8u + 15u) & ~15u;
+    p += ((Wn / kXwTile + 1) * 8u + 15u) & ~15u;
     s_tl = reinterpret_cast<float*>(p);
   }
 
@@ -91,26 +95,20 @@ struct XWin {
     }
     if constexpr (PREFIX) {
       __syncthreads();
-      const uint32_t ntiles = W >> 4;
-      for (uint32_t t = tid; t < ntiles; t += T) {
-        const uint32_t base = t * 17u;
+      const uint32_t ntiles = W / kXwTile;
+      for (uint32_t t = tid; t < ntiles; t += T) {  // tile totals
+        const uint32_t base = t * (kXwTile + 1);
         double hi = 0.0, lo = 0.0;
 #pragma unroll
-        for (uint32_t j = 0; j < 16; ++j) {
-          s_ph[base + j] = hi;
-          s_pl[base + j] = (float)lo;
+        for (uint32_t j = 0; j < kXwTile; ++j) {
           double s, e;
           two_sum(hi, (double)s_x[base + j], s, e);
           hi = s;
           lo += e;
         }
-        const double h2 = hi + lo;  // tile total, renormalised
+        const double h2 = hi + lo;
         s_th[t] = h2;
         s_tl[t] = (float)(lo - (h2 - hi));
-      }
-      if (tid == 0) {  // P at the window end (index W) is the start of a tile
-        s_ph[xw_pad(W)] = 0.0;
-        s_pl[xw_pad(W)] = 0.0f;
       }
       __syncthreads();
       if (tid < 32) {  // Q: exclusive double-double prefix of the tile totals (one warp)
@@ -159,18 +157,23 @@ struct XWin {
         }
       }
       __syncthreads();
-      // full prefix in place: F[j] = Q[j >> 4] + P[j] (double-double), so an
-      // interval is F[e] - F[a] -- one TwoSum in the decode loop
-      for (uint32_t j = tid; j <= W; j += T) {
-        const uint32_t pj = xw_pad(j), t = j >> 4;
+      for (uint32_t t = tid; t < ntiles; t += T) {  // F within each tile, from Q[t]
+        const uint32_t base = t * (kXwTile + 1);
         double hi = s_th[t], lo = (double)s_tl[t];
-        const double bhi = s_ph[pj], blo = (double)s_pl[pj];
-        double sh, se;
-        two_sum(hi, bhi, sh, se);
-        se += lo + blo;
-        hi = sh + se;
-        s_ph[pj] = hi;
-        s_pl[pj] = (float)(se - (hi - sh));
+#pragma unroll
+        for (uint32_t j = 0; j < kXwTile; ++j) {
+          const double h2 = hi + lo;
+          s_ph[base + j] = h2;
+          s_pl[base + j] = (float)(lo - (h2 - hi));
+          double s, e;
+          two_sum(hi, (double)s_x[base + j], s, e);
+          hi = s;
+          lo += e;
+        }
+      }
+      if (tid == 0) {  // F at the window end: the total
+        s_ph[xw_pad(W)] = s_th[ntiles];
+        s_pl[xw_pad(W)] = s_tl[ntiles];
       }
     }
     __syncthreads();

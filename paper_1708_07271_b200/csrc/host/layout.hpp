@@ -109,8 +109,8 @@ constexpr uint32_t kBvsMaxUnits = 32;  // more -> heavy row
 constexpr uint32_t kBvsHeavyEntry = 6;
 constexpr uint32_t kBvsHead = 4;
 constexpr uint32_t kBvsBias16 = 32768;
-// padded x-window index (16-entry tiles at a stride of 17; cuda/xwindow.cuh)
-__host__ __device__ constexpr uint32_t bvs_pad_index(uint32_t j) { return j + (j >> 4); }
+// padded x-window index (8-entry tiles at a stride of 9; cuda/xwindow.cuh)
+__host__ __device__ constexpr uint32_t bvs_pad_index(uint32_t j) { return j + (j >> 3); }
 __host__ __device__ constexpr uint32_t make_sa(uint32_t k, uint32_t r, uint32_t wp, uint32_t wl, bool far) {
   return k | (r << 12) | (wp << 15) | (wl << 20) | ((far ? 1u : 0u) << 25) | (1u << 31);
 }

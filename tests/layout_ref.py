@@ -150,7 +150,7 @@ def decode_sliced(words, blocks, n, B, lmin, W):
                 pts, ints = [], []
                 if not c32 and not far:
                     # near class 16: rectangular, padded window indices, sign in bit 15
-                    zc = W + (W >> 4)
+                    zc = W + (W >> 3)
                     mnpw = (mnp + 1) >> 1
                     minus, res = [], []
                     for q in range(mnpw):
@@ -159,8 +159,8 @@ def decode_sliced(words, blocks, n, B, lmin, W):
                             if c == zc:
                                 continue
                             pi = c & 0x7FFF
-                            assert pi % 17 != 16
-                            col = wlo + (pi // 17) * 16 + pi % 17
+                            assert pi % 9 != 8
+                            col = wlo + (pi // 9) * 8 + pi % 9
                             (minus if c >> 15 else res).append(col)
                     assert (len(minus), len(minus) + len(res)) == (nm, npt), (b, sl, lane)
                     pts = minus + res
