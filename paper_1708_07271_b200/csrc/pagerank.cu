@@ -94,6 +94,62 @@ void run_pagerank(cmvg_graph* g, const uint32_t* degrees, double alpha, uint32_t
   CUDA_TRY(cudaGetLastError());
   const bool use_tol = l1_tol >= 0.0;
   uint32_t t = 0;
+  auto step = [&](double* pc, double* pnx, double* qc, double* qnx) {
+    PrArgs pr{};
+    pr.deg = deg;
+    pr.p_prev = use_tol ? pc : nullptr;
+    pr.q_next = qnx;
+    pr.partial = part.as<double>();
+    pr.dmass = dm;
+    pr.alpha = alpha;
+    pr.n = n;
+    pr.uniform = dangling == CMVG_DANGLING_UNIFORM;
+    launch_pr_step(g, qc, pr, pnx, st);
+    pr_reduce_kernel<<<1, 1024, 0, st>>>(part.as<double>(), g->nblocks, dm);
+    CUDA_TRY(cudaGetLastError());
+  };
+  if (!use_tol && iters >= 4) {
+    // fixed iteration count: two iterations (ping-pong) captured once as a
+    // CUDA graph and replayed -- no per-kernel launch overhead for small graphs
+    step(p, pn, q, qn);  // first launch outside the capture (kernel attributes)
+    std::swap(p, pn);
+    std::swap(q, qn);
+    cudaStream_t cs = st;
+    bool own = false;
+    if (cs == nullptr) {  // the legacy default stream cannot be captured
+      CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+      own = true;
+      CUDA_TRY(cudaStreamSynchronize(st));
+    }
+    cudaStream_t saved = st;
+    st = cs;
+    cudaGraph_t graph;
+    cudaGraphExec_t exec;
+    CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    step(p, pn, q, qn);
+    step(pn, p, qn, q);
+    CUDA_TRY(cudaStreamEndCapture(cs, &graph));
+    CUDA_TRY(cudaGraphInstantiate(&exec, graph, 0));
+    const uint32_t pairs = (iters - 1) / 2;
+    for (uint32_t k = 0; k < pairs; ++k) CUDA_TRY(cudaGraphLaunch(exec, cs));
+    if ((iters - 1) % 2) {
+      step(p, pn, q, qn);
+      std::swap(p, pn);
+      std::swap(q, qn);
+    }
+    CUDA_TRY(cudaGraphExecDestroy(exec));
+    CUDA_TRY(cudaGraphDestroy(graph));
+    st = saved;
+    if (own) {
+      CUDA_TRY(cudaStreamSynchronize(cs));
+      CUDA_TRY(cudaStreamDestroy(cs));
+    }
+    if (iters_run) *iters_run = iters;
+    CUDA_TRY(cudaMemcpyAsync(ranks, p, (size_t)n * 8, ptr_kind == CMVG_HOST ? cudaMemcpyDeviceToHost
+                                                                              : cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return;
+  }
   for (t = 1; t <= iters; ++t) {
     PrArgs pr{};
     pr.deg = deg;
