@@ -54,7 +54,7 @@ __host__ __device__ inline BvsSmem bvs_smem_layout(const BvdDims& d, uint32_t xs
   BvsSmem s;
   uint32_t o = 0;
   s.off_x = o;
-  o = align16(o + xw_bytes(d.window, xsize, true));
+  o = align16(o + xw_bytes(d.window, xsize));
   s.off_yhi = o;
   o = align16(o + d.block_rows * 8);
   s.off_ylo = o;
@@ -325,12 +325,12 @@ __global__ void __launch_bounds__(256, 4) bvs_gather_kernel(BvdDev g, const XT* 
     if (nsl <= kBvsSliceTab)
       for (uint32_t i = threadIdx.x; i < 2 * nsl; i += blockDim.x) s_tab[i] = __ldg(bs + kBvsHead + i);
   }
-  XWin<XT, true> xw;
+  XWin<XT> xw;
   xw.carve(smem + L.off_x, D.window);
   xw.x = x;
   xw.xfar = xfar;
   xw.wlo = bi.wlo;
-  XT xpre[XWin<XT, true>::kPre];
+  XT xpre[XWin<XT>::kPre];
   xw.prefetch(D.n, xpre);
   __syncthreads();      // publishes the counters
   xw.stage(D.n, xpre);  // ends with __syncthreads

@@ -19,16 +19,14 @@ namespace cmvg {
 constexpr uint32_t kXwTile = 8;  // entries per tile (bvs_pad_index: stride 9)
 __host__ __device__ constexpr uint32_t xw_pad(uint32_t j) { return bvs_pad_index(j); }
 
-// bytes of the x-window region for W entries of type XT
-__host__ __device__ inline uint32_t xw_bytes(uint32_t W, uint32_t xsize, bool prefix) {
+// bytes of the x-window region for W entries of type XT (x, F hi / lo, Q hi / lo)
+__host__ __device__ inline uint32_t xw_bytes(uint32_t W, uint32_t xsize) {
   const uint32_t padded = xw_pad(W) + 1;
   uint32_t b = ((padded * xsize + 15u) & ~15u);
-  if (prefix) {
-    b += ((padded * 8u + 15u) & ~15u);                // F hi
-    b += ((padded * 4u + 15u) & ~15u);                // F lo
-    b += (((W / kXwTile + 1) * 8u + 15u) & ~15u);    // Q hi
-    b += (((W / kXwTile + 1) * 4u + 15u) & ~15u);    // Q lo
-  }
+  b += ((padded * 8u + 15u) & ~15u);                // F hi
+  b += ((padded * 4u + 15u) & ~15u);                // F lo
+  b += (((W / kXwTile + 1) * 8u + 15u) & ~15u);    // Q hi
+  b += (((W / kXwTile + 1) * 4u + 15u) & ~15u);    // Q lo
   return b;
 }
 
@@ -38,7 +36,7 @@ __device__ __forceinline__ void two_sum(double a, double b, double& s, double& e
   e = (a - (s - bb)) + (b - bb);
 }
 
-template <typename XT, bool PREFIX>
+template <typename XT>
 struct XWin {
   XT* s_x;
   double* s_ph;
@@ -93,7 +91,7 @@ struct XWin {
       const uint32_t c = wlo + j;
       s_x[xw_pad(j)] = c < n ? __ldg(x + c) : XT(0);
     }
-    if constexpr (PREFIX) {
+    {
       __syncthreads();
       const uint32_t ntiles = W / kXwTile;
       for (uint32_t t = tid; t < ntiles; t += T) {  // tile totals
@@ -199,26 +197,11 @@ struct XWin {
     return (double)v;
   }
 
-  // sum of x[left, left+len) as (hi, lo)
+  // sum of x[left, left+len) as (hi, lo): O(1) from the prefix inside the
+  // window, a compensated sum from memory otherwise
   __device__ __forceinline__ double isum(int32_t left, uint32_t len, double& lo) const {
     const uint32_t a = (uint32_t)(left - (int32_t)wlo);
-    const uint32_t e = a + len;
-    if constexpr (PREFIX) {
-      if (a < W && e <= W) return isum_near(a, len, lo);
-    } else {
-      if (a < W && e <= W && len <= 32) {
-        double s = 0.0, c = 0.0;
-        for (uint32_t t = a; t < e; ++t) {
-          double u, er;
-          two_sum(s, (double)s_x[xw_pad(t)], u, er);
-          s = u;
-          c += er;
-        }
-        lo = c;
-        return s;
-      }
-    }
-    // long or out-of-window interval: compensated sum from global memory
+    if (a < W && a + len <= W) return isum_near(a, len, lo);
     double s = 0.0, c = 0.0;
     for (uint32_t t = 0; t < len; ++t) {
       double u, er;
