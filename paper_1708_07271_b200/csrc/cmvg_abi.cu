@@ -496,7 +496,21 @@ const void* mapped_host(const void* p) {
 template <typename T>
 void gather_host_pipelined(cmvg_graph* g, const T* x, T* y, const T* xmapped) {
   const uint32_t nb = g->nblocks, B = g->dims.block_rows;
+  // chunk boundaries (in blocks): 12 equal chunks, then 1/2, 1/4, 1/8, 1/8 of
+  // one -- a short last chunk keeps the tail (last kernel + last D2H) small
   const uint32_t C = std::min<uint32_t>(16, nb);  // 2 events per chunk: g->ev has 32
+  std::vector<uint32_t> cut(C + 1, 0);
+  {
+    static const double w[16] = {1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 0.5, 0.25, 0.125, 0.125};
+    double tot = 0.0, acc = 0.0;
+    for (uint32_t c = 0; c < C; ++c) tot += C == 16 ? w[c] : 1.0;
+    for (uint32_t c = 0; c < C; ++c) {
+      acc += C == 16 ? w[c] : 1.0;
+      cut[c + 1] = std::min<uint32_t>(nb, (uint32_t)((double)nb * acc / tot + 0.5));
+    }
+    cut[C] = nb;
+    for (uint32_t c = 1; c <= C; ++c) cut[c] = std::max(cut[c], cut[c - 1]);
+  }
   if (!g->s_in) {
     CUDA_TRY(cudaStreamCreateWithFlags(&g->s_in, cudaStreamNonBlocking));
     CUDA_TRY(cudaStreamCreateWithFlags(&g->s_comp, cudaStreamNonBlocking));
@@ -508,7 +522,8 @@ void gather_host_pipelined(cmvg_graph* g, const T* x, T* y, const T* xmapped) {
   T* hy = g->hy.as<T>();
   size_t xdone = 0;
   for (uint32_t c = 0; c < C; ++c) {
-    const uint32_t b0 = (uint32_t)((uint64_t)nb * c / C), b1 = (uint32_t)((uint64_t)nb * (c + 1) / C);
+    const uint32_t b0 = cut[c], b1 = cut[c + 1];
+    if (b0 == b1 && c + 1 < C) continue;
     // x needed by blocks < b1: their windows (prefix max), everything for the last chunk
     size_t need = c + 1 == C ? g->n : std::min<size_t>(g->n, g->win_need[b1 - 1]);
     if (need > xdone) {
