@@ -496,12 +496,13 @@ const void* mapped_host(const void* p) {
 template <typename T>
 void gather_host_pipelined(cmvg_graph* g, const T* x, T* y, const T* xmapped) {
   const uint32_t nb = g->nblocks, B = g->dims.block_rows;
-  // chunk boundaries (in blocks): 12 equal chunks, then 1/2, 1/4, 1/8, 1/8 of
-  // one -- a short last chunk keeps the tail (last kernel + last D2H) small
+  // chunk boundaries (in blocks): a ramp up (1/4, 1/2, 3/4 of a chunk: the
+  // first D2H starts early), equal chunks, then 1/2, 1/4, 1/8, 1/8 (a short
+  // last chunk keeps the tail -- last kernel + last D2H -- small)
   const uint32_t C = std::min<uint32_t>(16, nb);  // 2 events per chunk: g->ev has 32
   std::vector<uint32_t> cut(C + 1, 0);
   {
-    static const double w[16] = {1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 0.5, 0.25, 0.125, 0.125};
+    static const double w[16] = {0.25, 0.5, 0.75, 1, 1, 1, 1, 1, 1, 1, 1, 1, 0.5, 0.25, 0.125, 0.125};
     double tot = 0.0, acc = 0.0;
     for (uint32_t c = 0; c < C; ++c) tot += C == 16 ? w[c] : 1.0;
     for (uint32_t c = 0; c < C; ++c) {
