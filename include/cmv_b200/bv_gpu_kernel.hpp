@@ -87,13 +87,18 @@ class BvGpuKernel final : public MatvecKernel {
   void multiply_device_f32(const float* x, float* y, void* stream = nullptr) const {
     cmvg_throw_if(cmvg_matvec_f32(g_, x, y, CMVG_GATHER, CMVG_DEVICE, stream));
   }
-  PageRankResult pagerank_device(const DegreeVector& degrees, const PageRankConfig& cfg) const {
+  // cmv::pagerank (pagerank.hpp:100-102) with the power iteration on the
+  // device; `start` as in the reference (starting and restart distribution)
+  PageRankResult pagerank_device(const DegreeVector& degrees, const PageRankConfig& cfg,
+                                 const RankVector* start = nullptr) const {
+    if (degrees.size() != dimension()) throw std::invalid_argument("pagerank: degree vector dimension mismatch");
+    if (start && start->size() != dimension()) throw std::invalid_argument("pagerank: start dimension mismatch");
     PageRankResult r;
     r.ranks.resize(dimension());
     const int pol = cfg.dangling == DanglingPolicy::kUniform ? CMVG_DANGLING_UNIFORM : CMVG_DANGLING_DROP;
-    cmvg_throw_if(cmvg_pagerank(g_, degrees.data(), cfg.alpha, cfg.iterations,
-                                cfg.l1_tolerance ? *cfg.l1_tolerance : -1.0, pol, r.ranks.data(),
-                                &r.iterations_run, CMVG_HOST, nullptr));
+    cmvg_throw_if(cmvg_pagerank_ex(g_, degrees.data(), cfg.alpha, cfg.iterations,
+                                   cfg.l1_tolerance ? *cfg.l1_tolerance : -1.0, pol, start ? start->data() : nullptr,
+                                   r.ranks.data(), &r.iterations_run, CMVG_HOST, nullptr));
     return r;
   }
   cmvg_graph* handle() const { return g_; }

@@ -194,6 +194,14 @@ int cmvg_decode_csr(cmvg_graph* g, uint64_t* row_offsets, uint32_t* cols, int pt
  * the out-degrees of A.  ranks receives n doubles. */
 int cmvg_pagerank(cmvg_graph* g, const uint32_t* degrees, double alpha, uint32_t iterations, double l1_tolerance,
                   int dangling, double* ranks, uint32_t* iterations_run, int ptr_kind, void* stream);
+/* cmvg_pagerank with a start vector (pagerank.hpp:100-102 `start`): the power
+ * iteration starts from it and it is also the restart distribution,
+ * p_t = alpha * start + (1 - alpha) * (A^T q + D/n).  It must be a
+ * probability vector (non-negative, sum 1 within 1e-9; else
+ * CMVG_ERR_INVALID).  start == NULL is the uniform 1/n.  start uses ptr_kind. */
+int cmvg_pagerank_ex(cmvg_graph* g, const uint32_t* degrees, double alpha, uint32_t iterations, double l1_tolerance,
+                     int dangling, const double* start, double* ranks, uint32_t* iterations_run, int ptr_kind,
+                     void* stream);
 
 /* One PageRank iteration on a shard (multi-GPU driver building block):
  * reads q (all n entries, device) and the dangling mass D of the previous

@@ -139,6 +139,8 @@ _SIGS = [
     ("cmvg_pagerank", C.c_int, [_P, _P, C.c_double, C.c_uint32, C.c_double, C.c_int, _P, C.POINTER(C.c_uint32),
                                 C.c_int, _P]),
     ("cmvg_read_set", C.c_int, [_P, _P, C.c_uint64, C.POINTER(C.c_uint64)]),
+    ("cmvg_pagerank_ex", C.c_int, [_P, _P, C.c_double, C.c_uint32, C.c_double, C.c_int, _P, _P,
+                                   C.POINTER(C.c_uint32), C.c_int, _P]),
     ("cmvg_pagerank_step_push", C.c_int, [_P, _P, _P, C.c_double, C.c_double, C.c_int, _P, _P, _P, _P, _P, _P, _P]),
     ("cmvg_pagerank_step", C.c_int, [_P, _P, _P, C.c_double, C.c_double, C.c_int, _P, _P, _P, _P, _P]),
 ]
@@ -470,8 +472,10 @@ class BvGraph:
         _check(load_library().cmvg_decode_csr(self._h, pr, pc, 1, st))
 
     def pagerank(self, degrees, alpha: float = 0.15, iterations: int = 10, l1_tolerance: Optional[float] = None,
-                 dangling: str = "uniform", ranks=None, stream: Optional[int] = None):
-        """Device-resident PageRank on a handle holding A^T; returns (ranks, iterations_run)."""
+                 dangling: str = "uniform", ranks=None, stream: Optional[int] = None, start=None):
+        """Device-resident PageRank on a handle holding A^T; returns (ranks, iterations_run).
+        `start` (a probability vector, host array or device tensor like
+        `degrees`) is the starting and restart distribution (cmvg_pagerank_ex)."""
         if len(degrees) != self.n:
             raise ValueError("degree vector dimension mismatch")
         if ranks is None:
@@ -486,9 +490,18 @@ class BvGraph:
             raise ValueError("degrees and ranks must both be host arrays or both device tensors")
         it = C.c_uint32()
         st = stream if stream is not None else _stream_of(degrees, ranks)
-        _check(load_library().cmvg_pagerank(self._h, pd, alpha, iterations,
-                                            -1.0 if l1_tolerance is None else float(l1_tolerance),
-                                            {"uniform": 0, "drop": 1}[dangling], pr, C.byref(it), kd, st))
+        ps = None
+        if start is not None:
+            if len(start) != self.n:
+                raise ValueError("pagerank: start dimension mismatch")
+            if not _is_torch(start):
+                start = np.ascontiguousarray(start, dtype=np.float64)
+            ps, ks = _ptr_and_kind(start, np.float64)
+            if ks != kd:
+                raise ValueError("start must live where degrees live (host or device)")
+        _check(load_library().cmvg_pagerank_ex(self._h, pd, alpha, iterations,
+                                               -1.0 if l1_tolerance is None else float(l1_tolerance),
+                                               {"uniform": 0, "drop": 1}[dangling], ps, pr, C.byref(it), kd, st))
         return ranks, int(it.value)
 
     def pagerank_step(self, q, degrees_shard, alpha, dangling_mass, dangling, p_prev, p_next, q_next, partial,
@@ -595,8 +608,8 @@ def pagerank(at: BvGpuKernel, degrees, cfg: Optional[PageRankConfig] = None, sta
         raise ValueError("pagerank: empty graph")
     if len(degrees) != at.dimension():
         raise ValueError("pagerank: degree vector dimension mismatch")
-    if start is not None:
-        raise UnsupportedError("personalised start vectors are not supported on the device path yet")
     deg = degrees if _is_torch(degrees) else np.ascontiguousarray(degrees, dtype=np.uint32)
-    ranks, it = at.graph.pagerank(deg, cfg.alpha, cfg.iterations, cfg.l1_tolerance, cfg.dangling.value)
+    if start is not None and not _is_torch(deg):
+        start = np.ascontiguousarray(start, dtype=np.float64)
+    ranks, it = at.graph.pagerank(deg, cfg.alpha, cfg.iterations, cfg.l1_tolerance, cfg.dangling.value, start=start)
     return PageRankResult(ranks, it)

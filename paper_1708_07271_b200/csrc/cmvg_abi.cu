@@ -2,6 +2,8 @@
 #include "cuda/bv_decode.cuh"
 #include "internal.hpp"
 
+#include <cmath>
+
 namespace cmvg {
 thread_local std::string g_last_error;
 }
@@ -669,8 +671,9 @@ int cmvg_decode_csr(cmvg_graph* g, uint64_t* row_offsets, uint32_t* cols, int pt
   });
 }
 
-int cmvg_pagerank(cmvg_graph* g, const uint32_t* degrees, double alpha, uint32_t iterations, double l1_tolerance,
-                  int dangling, double* ranks, uint32_t* iterations_run, int ptr_kind, void* stream) {
+int cmvg_pagerank_ex(cmvg_graph* g, const uint32_t* degrees, double alpha, uint32_t iterations, double l1_tolerance,
+                     int dangling, const double* start, double* ranks, uint32_t* iterations_run, int ptr_kind,
+                     void* stream) {
   return guarded([&] {
     require(g && degrees && ranks, "null argument");
     require(alpha > 0.0 && alpha < 1.0, "alpha must be in (0,1)");
@@ -678,9 +681,30 @@ int cmvg_pagerank(cmvg_graph* g, const uint32_t* degrees, double alpha, uint32_t
     require(dangling == CMVG_DANGLING_UNIFORM || dangling == CMVG_DANGLING_DROP, "bad dangling policy");
     require(g->row_begin == 0 && g->row_end == g->n, "cmvg_pagerank needs a whole-graph handle");
     DeviceGuard dg(g->device);
-    run_pagerank(g, degrees, alpha, iterations, l1_tolerance, dangling, ranks, iterations_run, ptr_kind,
+    if (start) {  // a probability vector (pagerank.hpp:97; the same check as the reference)
+      std::vector<double> hs;
+      const double* sp = start;
+      if (ptr_kind == CMVG_DEVICE) {
+        hs.resize(g->n);
+        CUDA_TRY(cudaMemcpy(hs.data(), start, (size_t)g->n * 8, cudaMemcpyDeviceToHost));
+        sp = hs.data();
+      }
+      double sum = 0.0;
+      for (uint32_t i = 0; i < g->n; ++i) {
+        require(sp[i] >= 0.0, "pagerank: start has a negative entry");
+        sum += sp[i];
+      }
+      require(std::fabs(sum - 1.0) <= 1e-9, "pagerank: start is not a probability vector");
+    }
+    run_pagerank(g, degrees, alpha, iterations, l1_tolerance, dangling, start, ranks, iterations_run, ptr_kind,
                  (cudaStream_t)stream);
   });
+}
+
+int cmvg_pagerank(cmvg_graph* g, const uint32_t* degrees, double alpha, uint32_t iterations, double l1_tolerance,
+                  int dangling, double* ranks, uint32_t* iterations_run, int ptr_kind, void* stream) {
+  return cmvg_pagerank_ex(g, degrees, alpha, iterations, l1_tolerance, dangling, nullptr, ranks, iterations_run,
+                          ptr_kind, stream);
 }
 
 int cmvg_pagerank_step(cmvg_graph* g, const double* q, const uint32_t* deg, double alpha, double dmass, int dangling,

@@ -84,17 +84,19 @@ struct PageRankEpi {
   double* q_next;          // shard-relative, offset applied
   double* partial;         // [nblocks][2]
   double base, scale, dn;  // alpha/n, 1 - alpha, D/n (or 0)
+  double alpha_p0;         // alpha (multiplies p0 when a restart distribution is given)
   uint32_t bl;
   double dang, l1;         // per-thread partials
   // fused halo push (multi-GPU): q'_k also goes to every peer whose bit is set
   // in push_mask[k], stored at its global column in that peer's q buffer
   // (NVLink peer memory) -- the exchange rides on the epilogue's stores
+  const double* p0;            // restart distribution of this block's rows (offset applied); null = uniform
   const uint8_t* push_mask;    // shard-relative, offset applied; null = no push
   double* const* push_dst;     // device array: peer q buffers, indexed by global column
   uint32_t grow0;              // global row of this block's row 0
   template <typename YT>
   __device__ __forceinline__ void store(YT* pb, uint32_t k, double y) {
-    const double pn = base + scale * (y + dn);
+    const double pn = (p0 ? alpha_p0 * p0[k] : base) + scale * (y + dn);
     pb[k] = (YT)pn;
     const uint32_t d = deg[k];
     const double qn = d ? pn / (double)d : 0.0;

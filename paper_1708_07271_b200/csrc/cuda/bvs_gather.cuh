@@ -40,6 +40,7 @@ struct PrArgs {
   int uniform;
   const uint8_t* push_mask;  // fused halo push (see PageRankEpi); null = none
   double* const* push_dst;
+  const double* p0;          // restart distribution (start vector), global rows; null = uniform 1/n
 };
 
 constexpr uint32_t kBvsGuardWords = 64;  // zero words after the last block (lanes never read past their unit)
@@ -357,6 +358,7 @@ __global__ void __launch_bounds__(256, 4) bvs_gather_kernel(BvdDev g, const XT* 
     epi.q_next = pr.q_next + sh;
     epi.partial = pr.partial;
     epi.base = pr.alpha / (double)pr.n;
+    epi.alpha_p0 = pr.alpha;
     epi.scale = 1.0 - pr.alpha;
     const double dm = pr.dmass ? *pr.dmass : pr.dmass_host;
     epi.dn = pr.uniform ? dm / (double)pr.n : 0.0;
@@ -364,6 +366,7 @@ __global__ void __launch_bounds__(256, 4) bvs_gather_kernel(BvdDev g, const XT* 
     epi.dang = 0.0;
     epi.l1 = 0.0;
     epi.push_mask = pr.push_mask ? pr.push_mask + sh : nullptr;
+    epi.p0 = pr.p0 ? pr.p0 + r0 : nullptr;
     epi.push_dst = pr.push_dst;
     epi.grow0 = r0;
     chain_and_store(s_yhi, s_ylo, rc, yb, epi, D.max_depth);

@@ -8,13 +8,14 @@
 namespace cmvg {
 namespace {
 
-// p0 = 1/n, q0 = p0/d, partials of the dangling mass per block of 1024 rows
-__global__ void pr_init_kernel(const uint32_t* __restrict__ deg, uint32_t n, double* __restrict__ p,
-                               double* __restrict__ q, double* __restrict__ partial) {
+// p0 = 1/n (or the start vector), q0 = p0/d, partials of the dangling mass
+// per block of 1024 rows
+__global__ void pr_init_kernel(const uint32_t* __restrict__ deg, uint32_t n, const double* __restrict__ start,
+                               double* __restrict__ p, double* __restrict__ q, double* __restrict__ partial) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  const double p0 = 1.0 / (double)n;
   double dang = 0.0;
   if (i < n) {
+    const double p0 = start ? start[i] : 1.0 / (double)n;
     const uint32_t d = deg[i];
     p[i] = p0;
     q[i] = d ? p0 / (double)d : 0.0;
@@ -68,13 +69,19 @@ void launch_pr_step(cmvg_graph* g, const double* q, PrArgs pr, double* p_next, c
 }  // namespace
 
 void run_pagerank(cmvg_graph* g, const uint32_t* degrees, double alpha, uint32_t iters, double l1_tol, int dangling,
-                  double* ranks, uint32_t* iters_run, int ptr_kind, cudaStream_t st) {
+                  const double* start, double* ranks, uint32_t* iters_run, int ptr_kind, cudaStream_t st) {
   const uint32_t n = g->n;
   DevBuf ddeg, p0, p1, q0, q1, part, scal;
   const uint32_t* deg = degrees;
+  DevBuf dstart;
+  const double* p0v = start;  // restart distribution (null = uniform)
   if (ptr_kind == CMVG_HOST) {
     ddeg.upload(degrees, n);
     deg = ddeg.as<uint32_t>();
+    if (start) {
+      dstart.upload(start, n);
+      p0v = dstart.as<double>();
+    }
   }
   p0.alloc((size_t)n * 8 + 64);
   p1.alloc((size_t)n * 8 + 64);
@@ -88,7 +95,7 @@ void run_pagerank(cmvg_graph* g, const uint32_t* degrees, double alpha, uint32_t
   double* q = q0.as<double>();
   double* qn = q1.as<double>();
   double* dm = scal.as<double>();  // [0] dangling mass, [1] l1
-  pr_init_kernel<<<ib, 1024, 0, st>>>(deg, n, p, q, part.as<double>());
+  pr_init_kernel<<<ib, 1024, 0, st>>>(deg, n, p0v, p, q, part.as<double>());
   CUDA_TRY(cudaGetLastError());
   pr_reduce_kernel<<<1, 1024, 0, st>>>(part.as<double>(), ib, dm);
   CUDA_TRY(cudaGetLastError());
@@ -104,6 +111,7 @@ void run_pagerank(cmvg_graph* g, const uint32_t* degrees, double alpha, uint32_t
     pr.alpha = alpha;
     pr.n = n;
     pr.uniform = dangling == CMVG_DANGLING_UNIFORM;
+    pr.p0 = p0v;
     launch_pr_step(g, qc, pr, pnx, st);
     pr_reduce_kernel<<<1, 1024, 0, st>>>(part.as<double>(), g->nblocks, dm);
     CUDA_TRY(cudaGetLastError());
@@ -151,18 +159,7 @@ void run_pagerank(cmvg_graph* g, const uint32_t* degrees, double alpha, uint32_t
     return;
   }
   for (t = 1; t <= iters; ++t) {
-    PrArgs pr{};
-    pr.deg = deg;
-    pr.p_prev = use_tol ? p : nullptr;
-    pr.q_next = qn;
-    pr.partial = part.as<double>();
-    pr.dmass = dm;
-    pr.alpha = alpha;
-    pr.n = n;
-    pr.uniform = dangling == CMVG_DANGLING_UNIFORM;
-    launch_pr_step(g, q, pr, pn, st);
-    pr_reduce_kernel<<<1, 1024, 0, st>>>(part.as<double>(), g->nblocks, dm);
-    CUDA_TRY(cudaGetLastError());
+    step(p, pn, q, qn);
     std::swap(p, pn);
     std::swap(q, qn);
     if (use_tol) {

@@ -222,3 +222,32 @@ def test_pagerank_shard_steps_fused_push(cuda):
         dmass = float(tot[0])
     want, _ = oracle_pr(g, iterations=20)
     assert rel(p.cpu().numpy(), want) <= 1e-12
+
+
+@pytest.mark.parametrize("tol", [None, 1e-10])
+def test_pagerank_start_vector(cuda, tol):
+    """`start` (pagerank.hpp:86-102): the starting and restart distribution,
+    validated as a probability vector -- against the oracle's pagerank with
+    the same start, host and device buffers."""
+    import torch
+
+    g = make_graph(3, n=1 << 14)
+    rng = np.random.default_rng(4)
+    start = rng.random(g.n)
+    start /= start.sum()
+    dg = P.BvGraph(bv_of_transpose(g))
+    og = O.Csr.from_arrays(g.n, g.row_offsets, g.columns)
+    want, wit = O.pagerank_csr(og.transpose(), og.out_degrees(), 0.15, 40, l1_tolerance=tol, start=start)
+    res = P.pagerank(P.BvGpuKernel(dg), g.out_degrees(), P.PageRankConfig(iterations=40, l1_tolerance=tol),
+                     start=start)
+    assert res.iterations_run == wit
+    assert rel(res.ranks, want) <= 1e-12
+    deg = torch.from_numpy(g.out_degrees().astype(np.int32)).cuda()
+    p, it = dg.pagerank(deg, iterations=40, l1_tolerance=tol, start=torch.from_numpy(start).cuda())
+    assert it == wit and rel(p.cpu().numpy(), want) <= 1e-12
+    with pytest.raises(ValueError):
+        P.pagerank(P.BvGpuKernel(dg), g.out_degrees(), P.PageRankConfig(iterations=5), start=start * 2)
+    bad = start.copy()
+    bad[0] = -bad[0]
+    with pytest.raises(ValueError):
+        P.pagerank(P.BvGpuKernel(dg), g.out_degrees(), P.PageRankConfig(iterations=5), start=bad)
