@@ -22,6 +22,7 @@ import ctypes as C
 import dataclasses
 import enum
 import os
+import warnings
 from typing import Optional
 
 import numpy as np
@@ -30,7 +31,8 @@ __all__ = [
     "CmvgError", "FormatError", "CorruptionError", "UnsupportedError",
     "CsrGraph", "BvParams", "BvStream", "BvGraph", "CreateOptions",
     "MatvecKernel", "BvGpuKernel", "DanglingPolicy", "PageRankConfig", "PageRankResult",
-    "pagerank", "library_path", "load_library",
+    "pagerank", "library_path", "load_library", "CompressionStats", "compression_stats", "PageRankEquivalence",
+    "pagerank_equivalence_check",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -613,3 +615,94 @@ def pagerank(at: BvGpuKernel, degrees, cfg: Optional[PageRankConfig] = None, sta
         start = np.ascontiguousarray(start, dtype=np.float64)
     ranks, it = at.graph.pagerank(deg, cfg.alpha, cfg.iterations, cfg.l1_tolerance, cfg.dangling.value, start=start)
     return PageRankResult(ranks, it)
+
+
+# ---------------------------------------------------------------------------
+# cmv::stats / cmv::pagerank_equivalence_check (ref_matrix.hpp:78-89,
+# pagerank.hpp:104-118)
+@dataclasses.dataclass
+class CompressionStats:  # ref_matrix.hpp:78-86
+    n: int = 0
+    m: int = 0
+    m_prime: int = 0                 # entries of A' (plus + minus)
+    ratio: float = 1.0               # m / m_prime
+    ratio_by_convention: bool = False  # m_prime == 0
+    rows_self_coded: int = 0         # rows without a reference
+    max_chain: int = 0               # longest reference chain
+
+
+def compression_stats(stream: "BvStream") -> CompressionStats:
+    """cmv::stats for a BV stream: A' = per row the reference's skipped entries
+    (minus) plus BV's extra list (intervals + residuals)."""
+    st = stream.stats()
+    mp = int(st["interval_edges"] + st["residual_edges"] + st["minus_edges"])
+    return CompressionStats(n=stream.n, m=stream.m, m_prime=mp, ratio=(stream.m / mp) if mp else 1.0,
+                            ratio_by_convention=mp == 0, rows_self_coded=int(stream.n - st["rows_with_ref"]),
+                            max_chain=int(st["max_depth"]))
+
+
+@dataclasses.dataclass
+class PageRankEquivalence:  # pagerank.hpp:106-114
+    linf: float = 0.0        # max |csr - ref| over vertices
+    iterations_run: int = 0
+    csr_seconds: float = 0.0
+    ref_seconds: float = 0.0
+    csr_adds: int = 0        # per product
+    ref_adds: int = 0        # per product
+    compression: CompressionStats = dataclasses.field(default_factory=CompressionStats)
+
+
+def pagerank_equivalence_check(g: "CsrGraph", cfg: Optional[PageRankConfig] = None, window: int = 7,
+                               device: int = 0) -> PageRankEquivalence:
+    """cmv::pagerank_equivalence_check: the same PageRank with the baseline CSR
+    kernel and the differential kernel, both on the GPU.  The CSR side is a
+    plain sparse product of CSR(A^T) (cuSPARSE through torch, fp64) in the
+    same power iteration; the differential side is this library's device
+    PageRank on BV(A^T) with BV window `window`.  Timings are device time of
+    the iterations."""
+    import torch
+
+    cfg = cfg or PageRankConfig()
+    if window < 1:
+        raise ValueError("pagerank_equivalence_check: window must be >= 1")
+    dev = torch.device("cuda", device)
+    at = g.transpose()
+    stream = BvStream.encode(at, BvParams(window=min(window, 7)))
+    dg = BvGraph(stream, CreateOptions(device=device))
+    deg_np = g.out_degrees()
+    deg = torch.from_numpy(deg_np.astype(np.int32)).to(dev)
+    dg.pagerank(deg, cfg.alpha, 2, None, cfg.dangling.value)  # warm-up
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    p_ref, it_ref = dg.pagerank(deg, cfg.alpha, cfg.iterations, cfg.l1_tolerance, cfg.dangling.value)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    ref_s = e0.elapsed_time(e1) * 1e-3
+    # baseline: CSR(A^T) y = A^T q (cuSPARSE), identical recurrence to the reference's pagerank
+    n = g.n
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", UserWarning)  # torch's "sparse CSR is beta" notices
+        A = torch.sparse_csr_tensor(torch.from_numpy(at.row_offsets.astype(np.int64)),
+                                    torch.from_numpy(at.columns.astype(np.int64)),
+                                    torch.ones(at.m, dtype=torch.float64), size=(n, n)).to(dev)
+    d = deg.to(torch.float64)
+    alpha = cfg.alpha
+    p = torch.full((n,), 1.0 / n, dtype=torch.float64, device=dev)
+    e0.record()
+    it = 0
+    for it in range(1, cfg.iterations + 1):
+        q = torch.where(d > 0, p / d.clamp(min=1), torch.zeros_like(p))
+        dm = p[d == 0].sum() if cfg.dangling == DanglingPolicy.UNIFORM else torch.zeros((), dtype=torch.float64,
+                                                                                     device=dev)
+        y = torch.mv(A, q)
+        nxt = alpha / n + (1.0 - alpha) * (y + dm / n)
+        l1 = float((nxt - p).abs().sum()) if cfg.l1_tolerance is not None else None
+        p = nxt
+        if cfg.l1_tolerance is not None and l1 <= cfg.l1_tolerance:
+            break
+    e1.record()
+    torch.cuda.synchronize(dev)
+    csr_s = e0.elapsed_time(e1) * 1e-3
+    return PageRankEquivalence(linf=float((p - p_ref).abs().max()), iterations_run=int(it_ref), csr_seconds=csr_s,
+                               ref_seconds=ref_s, csr_adds=int(at.m), ref_adds=int(dg.adds_per_product()),
+                               compression=compression_stats(stream))

@@ -194,3 +194,20 @@ def test_target_layout_heavy_targets():
     for i, r in enumerate(rows):
         want[r] += x[i]
     assert np.array_equal(scatter_bvt_int(words, blocks, n, 1024, 1536, x), want)
+
+
+def test_compression_stats():
+    """cmv::stats mirror (ref_matrix.hpp:78-89) on a BV stream: A' = minus
+    entries + extra entries; without references A' = A and the ratio is 1."""
+    g = make_graph(2, n=1 << 13)
+    s = P.BvStream.encode(g, P.BvParams())
+    st, c = s.stats(), P.compression_stats(s)
+    assert c.n == g.n and c.m == g.m
+    assert c.m_prime == g.m - st["copied_edges"] + st["minus_edges"]
+    assert c.m_prime < c.m and abs(c.ratio - c.m / c.m_prime) < 1e-12 and not c.ratio_by_convention
+    assert c.rows_self_coded == g.n - st["rows_with_ref"] and c.max_chain == st["max_depth"]
+    c0 = P.compression_stats(P.BvStream.encode(g, P.BvParams(window=0)))
+    assert c0.m_prime == g.m and c0.ratio == 1.0 and c0.rows_self_coded == g.n and c0.max_chain == 0
+    e = P.compression_stats(P.BvStream.encode(csr_from_rows([[]] * 5),
+                                              P.BvParams()))
+    assert e.m_prime == 0 and e.ratio == 1.0 and e.ratio_by_convention

@@ -251,3 +251,19 @@ def test_pagerank_start_vector(cuda, tol):
     bad[0] = -bad[0]
     with pytest.raises(ValueError):
         P.pagerank(P.BvGpuKernel(dg), g.out_degrees(), P.PageRankConfig(iterations=5), start=bad)
+
+
+def test_pagerank_equivalence_check(cuda):
+    """cmv::pagerank_equivalence_check (pagerank.hpp:104-118): the CSR and the
+    differential kernel give the same PageRank; the differential one needs
+    fewer adds; compression stats as cmv::stats (ref_matrix.hpp:78-89)."""
+    g = make_graph(3, n=1 << 15)
+    eq = P.pagerank_equivalence_check(g, P.PageRankConfig(iterations=30), window=7)
+    assert eq.iterations_run == 30
+    assert eq.linf <= 1e-14
+    assert eq.csr_adds == g.m and 0 < eq.ref_adds < eq.csr_adds
+    c = eq.compression
+    assert c.n == g.n and c.m == g.m and c.m_prime < c.m and abs(c.ratio - c.m / c.m_prime) < 1e-12
+    assert 0 < c.rows_self_coded < g.n and 1 <= c.max_chain <= 3
+    eq2 = P.pagerank_equivalence_check(g, P.PageRankConfig(iterations=200, l1_tolerance=1e-10), window=3)
+    assert eq2.iterations_run < 200 and eq2.linf <= 1e-13
