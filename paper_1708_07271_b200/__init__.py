@@ -39,7 +39,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 
 
 def library_path() -> str:
-    return os.path.join(_HERE, "libcmvg.so")
+    """The in-tree libcmvg.so (CMVG_LIBRARY overrides it: A/B builds of the same sources)."""
+    return os.environ.get("CMVG_LIBRARY") or os.path.join(_HERE, "libcmvg.so")
 
 
 # ---------------------------------------------------------------------------
