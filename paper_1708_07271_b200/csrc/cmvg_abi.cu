@@ -3,6 +3,8 @@
 #include "internal.hpp"
 
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 namespace cmvg {
 thread_local std::string g_last_error;
@@ -524,6 +526,13 @@ void gather_host_pipelined(cmvg_graph* g, const T* x, T* y, const T* xmapped) {
   T* hx = g->hx.as<T>();
   T* hy = g->hy.as<T>();
   size_t xdone = 0;
+  // CMVG_PIPE_TRACE=1 (dev): timing events per chunk, the timeline on stderr
+  static const bool trace = std::getenv("CMVG_PIPE_TRACE") != nullptr;
+  cudaEvent_t tev[3 * 16 + 1];
+  if (trace) {
+    for (auto& e : tev) CUDA_TRY(cudaEventCreate(&e));
+    CUDA_TRY(cudaEventRecord(tev[3 * 16], g->s_in));
+  }
   for (uint32_t c = 0; c < C; ++c) {
     const uint32_t b0 = cut[c], b1 = cut[c + 1];
     if (b0 == b1 && c + 1 < C) continue;
@@ -534,14 +543,31 @@ void gather_host_pipelined(cmvg_graph* g, const T* x, T* y, const T* xmapped) {
       xdone = need;
     }
     CUDA_TRY(cudaEventRecord(g->ev[2 * c], g->s_in));
+    if (trace) CUDA_TRY(cudaEventRecord(tev[3 * c], g->s_in));
     CUDA_TRY(cudaStreamWaitEvent(g->s_comp, g->ev[2 * c], 0));
     launch_gather<T, T>(g, hx, hy, g->s_comp, xmapped, b0, b1);
     CUDA_TRY(cudaEventRecord(g->ev[2 * c + 1], g->s_comp));
+    if (trace) CUDA_TRY(cudaEventRecord(tev[3 * c + 1], g->s_comp));
     CUDA_TRY(cudaStreamWaitEvent(g->s_out, g->ev[2 * c + 1], 0));
     const size_t r0 = (size_t)b0 * B, r1 = std::min(nrows, (size_t)b1 * B);
     CUDA_TRY(cudaMemcpyAsync(y + r0, hy + r0, (r1 - r0) * sizeof(T), cudaMemcpyDeviceToHost, g->s_out));
+    if (trace) CUDA_TRY(cudaEventRecord(tev[3 * c + 2], g->s_out));
   }
   CUDA_TRY(cudaStreamSynchronize(g->s_out));
+  if (trace) {
+    for (uint32_t c = 0; c < C; ++c) {
+      float a = 0, b = 0, d = 0;
+      if (cudaEventElapsedTime(&a, tev[3 * 16], tev[3 * c]) != cudaSuccess ||
+          cudaEventElapsedTime(&b, tev[3 * 16], tev[3 * c + 1]) != cudaSuccess ||
+          cudaEventElapsedTime(&d, tev[3 * 16], tev[3 * c + 2]) != cudaSuccess) {
+        (void)cudaGetLastError();  // a skipped (empty) chunk
+        continue;
+      }
+      std::fprintf(stderr, "chunk %2u blocks [%u,%u) h2d_end %.3f kern_end %.3f d2h_end %.3f ms\n", c, cut[c],
+                   cut[c + 1], a, b, d);
+    }
+    for (auto& e : tev) cudaEventDestroy(e);
+  }
 }
 
 template <typename T>

@@ -44,7 +44,7 @@ struct XWin {
   double* s_th;
   float* s_tl;
   const XT* __restrict__ x;
-  const XT* xfar;  // full x for columns outside the window (device memory, or mapped host memory)
+  const XT* xfar;  // x at the columns outside the window (only those are read from it)
   uint32_t wlo, W;
 
   __device__ __forceinline__ void carve(unsigned char* base, uint32_t Wn) {
@@ -198,14 +198,16 @@ struct XWin {
   }
 
   // sum of x[left, left+len) as (hi, lo): O(1) from the prefix inside the
-  // window, a compensated sum from memory otherwise
+  // window, otherwise a compensated sum entry by entry (window entries from
+  // shared memory, the others from xfar: xfar need only hold the columns
+  // outside the window)
   __device__ __forceinline__ double isum(int32_t left, uint32_t len, double& lo) const {
     const uint32_t a = (uint32_t)(left - (int32_t)wlo);
     if (a < W && a + len <= W) return isum_near(a, len, lo);
     double s = 0.0, c = 0.0;
     for (uint32_t t = 0; t < len; ++t) {
       double u, er;
-      two_sum(s, (double)__ldg(xfar + left + t), u, er);
+      two_sum(s, at(left + (int32_t)t), u, er);  // a run may straddle the window edge
       s = u;
       c += er;
     }
