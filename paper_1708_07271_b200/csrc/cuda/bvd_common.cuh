@@ -99,7 +99,16 @@ struct PageRankEpi {
     const double pn = (p0 ? alpha_p0 * p0[k] : base) + scale * (y + dn);
     pb[k] = (YT)pn;
     const uint32_t d = deg[k];
+#if CMVG_QDIV == 1
+    const double qn = d ? pn * __drcp_rn((double)d) : 0.0;
+#elif CMVG_QDIV == 2
+    double r = (double)__frcp_rn((float)d);
+    r = r * fma(-(double)d, r, 2.0);
+    r = r * fma(-(double)d, r, 2.0);
+    const double qn = d ? pn * r : 0.0;
+#else
     const double qn = d ? pn / (double)d : 0.0;
+#endif
     q_next[k] = qn;
     if (push_mask) {
       uint32_t m = push_mask[k];

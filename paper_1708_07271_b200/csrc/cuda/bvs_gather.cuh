@@ -159,8 +159,11 @@ __device__ __forceinline__ void bvs_slice_epilogue(uint32_t lane, uint32_t meta,
     const uint32_t heads = __ballot_sync(0xffffffffu, uh_primary(h));
     const uint32_t above = heads & ~((2u << lane) - 1u);
     const uint32_t end = above ? (uint32_t)__ffs(above) - 2u : 31u;
+    const uint32_t rounds = smeta_rounds(meta);  // ceil(log2(most units of a row)): often 1
 #pragma unroll
-    for (uint32_t o = 1; o < 32; o <<= 1) {
+    for (uint32_t i = 0; i < 5; ++i) {
+      if (i >= rounds) break;  // warp-uniform
+      const uint32_t o = 1u << i;
       const double uh = __shfl_down_sync(0xffffffffu, hi, o), ul = __shfl_down_sync(0xffffffffu, lo, o);
       if (lane + o <= end) dd_add(hi, lo, uh, ul);
     }

@@ -201,8 +201,11 @@ __device__ __forceinline__ void mm_slices(const uint32_t* __restrict__ bs, const
       const uint32_t heads = __ballot_sync(0xffffffffu, uh_primary(h));
       const uint32_t above = heads & ~((2u << lane) - 1u);
       const uint32_t end = above ? (uint32_t)__ffs(above) - 2u : 31u;
+      const uint32_t rounds = smeta_rounds(meta);
 #pragma unroll
-      for (uint32_t o = 1; o < 32; o <<= 1) {
+      for (uint32_t i = 0; i < 5; ++i) {
+        if (i >= rounds) break;  // warp-uniform
+        const uint32_t o = 1u << i;
 #pragma unroll
         for (uint32_t c = 0; c < kMmCols; ++c) {
           const double u = __shfl_down_sync(0xffffffffu, acc[c], o);

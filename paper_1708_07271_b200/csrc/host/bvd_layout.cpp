@@ -184,6 +184,7 @@ void emit_bvs(const RowParts* rps, const RowMeta* meta, const BitWriter& body, u
   struct Slice {
     std::vector<uint32_t> lanes;  // unit indices
     bool c32, far, multi;
+    uint32_t maxnu = 1;           // most units of one row in the slice
   };
   std::vector<Slice> slices;
   auto gid = [](const URow& r) { return (r.c32 ? 0 : 2) + (r.far ? 0 : 1); };
@@ -212,6 +213,7 @@ void emit_bvs(const RowParts* rps, const RowMeta* meta, const BitWriter& body, u
       while (t < slices.size() && slices[t].lanes.size() + row.nu > 32) ++t;
       if (t == slices.size()) slices.push_back(Slice{{}, row.c32, row.far, true});
       for (uint32_t u = 0; u < row.nu; ++u) slices[t].lanes.push_back(row.u0 + u);
+      slices[t].maxnu = std::max(slices[t].maxnu, row.nu);
     }
     a = e;
   }
@@ -247,7 +249,9 @@ void emit_bvs(const RowParts* rps, const RowMeta* meta, const BitWriter& body, u
       st.lane_iters_used += u.np + u.ni;
     }
     if (nearc16) nq = (mnp + 1) / 2 + mni;  // rectangular: points then intervals
-    so.push_back(make_smeta(mnp, mni, sl.c32, sl.far, sl.multi));
+    uint32_t rounds = 0;
+    while ((1u << rounds) < sl.maxnu) ++rounds;
+    so.push_back(make_smeta(mnp, mni, sl.c32, sl.far, sl.multi, rounds));
     so[kBvsHead + 2 * s + 1] = so.back();  // the table repeats the meta word
     for (size_t l = 0; l < 32; ++l) {
       if (l < sl.lanes.size()) {

@@ -131,14 +131,19 @@ __host__ __device__ constexpr uint32_t uh_r(uint32_t h) { return (h >> 17) & 7u;
 __host__ __device__ constexpr uint32_t uh_nm(uint32_t h) { return (h >> 12) & 31u; }
 __host__ __device__ constexpr uint32_t uh_np(uint32_t h) { return (h >> 7) & 31u; }
 __host__ __device__ constexpr uint32_t uh_ni(uint32_t h) { return (h >> 4) & 7u; }
-__host__ __device__ constexpr uint32_t make_smeta(uint32_t max_np, uint32_t max_ni, bool c32, bool far, bool multi) {
-  return max_np | (max_ni << 5) | ((c32 ? 1u : 0u) << 8) | ((far ? 1u : 0u) << 9) | ((multi ? 1u : 0u) << 10);
+// rounds: shuffle rounds of a multi slice's segmented reduction,
+// ceil(log2(max units of one row in the slice)) (0 for single-unit slices)
+__host__ __device__ constexpr uint32_t make_smeta(uint32_t max_np, uint32_t max_ni, bool c32, bool far, bool multi,
+                                                  uint32_t rounds = 0) {
+  return max_np | (max_ni << 5) | ((c32 ? 1u : 0u) << 8) | ((far ? 1u : 0u) << 9) | ((multi ? 1u : 0u) << 10) |
+         (rounds << 11);
 }
 __host__ __device__ constexpr uint32_t smeta_np(uint32_t m) { return m & 31u; }
 __host__ __device__ constexpr uint32_t smeta_ni(uint32_t m) { return (m >> 5) & 7u; }
 __host__ __device__ constexpr bool smeta_c32(uint32_t m) { return (m >> 8) & 1u; }
 __host__ __device__ constexpr bool smeta_far(uint32_t m) { return (m >> 9) & 1u; }
 __host__ __device__ constexpr bool smeta_multi(uint32_t m) { return (m >> 10) & 1u; }
+__host__ __device__ constexpr uint32_t smeta_rounds(uint32_t m) { return (m >> 11) & 7u; }
 
 // ---------------------------------------------------------------------------
 // BV-T: the scatter form's stream (y = x A on A's own compression).  Per block

@@ -134,12 +134,15 @@ def decode_sliced(words, blocks, n, B, lmin, W):
             meta = s[rec]
             assert s[4 + 2 * sl + 1] == meta
             mnp, mni, c32, far, multi = meta & 31, (meta >> 5) & 7, (meta >> 8) & 1, (meta >> 9) & 1, (meta >> 10) & 1
+            rounds = (meta >> 11) & 7
             seen_np, seen_ni = 0, 0
             cur = None
+            run, max_run = 0, 0  # units of the current row, most units of one row
             for lane in range(32):
                 h = s[rec + 1 + lane]
                 if not h >> 31:
                     cur = None
+                    run = 0
                     continue
                 prim, k, r = (h >> 30) & 1, (h >> 20) & 1023, (h >> 17) & 7
                 nm, npt, ni = (h >> 12) & 31, (h >> 7) & 31, (h >> 4) & 7
@@ -185,6 +188,8 @@ def decode_sliced(words, blocks, n, B, lmin, W):
                     not (inwin(a) and inwin(a + ln - 1)) for a, ln in ints)
                 if not far:
                     assert not ufar, (b, sl, lane)
+                run = 1 if prim else run + 1
+                max_run = max(max_run, run)
                 if prim:
                     assert k not in parts
                     cur = k
@@ -196,6 +201,8 @@ def decode_sliced(words, blocks, n, B, lmin, W):
                     parts[cur]["res"] += pts[nm:]
                     parts[cur]["ints"] += ints
             assert (seen_np, seen_ni) == (mnp, mni), (b, sl)
+            # the segmented reduction's rounds cover the longest row: 2^rounds >= units
+            assert (1 << rounds) >= max_run and (rounds == 0 or (1 << (rounds - 1)) < max_run), (b, sl, rounds, max_run)
         assert sorted(parts) == list(range(nr))
         for k in range(nr):
             p = parts[k]

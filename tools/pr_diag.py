@@ -30,3 +30,18 @@ torch.cuda.synchronize()
 ms = a.elapsed_time(b)
 print(f"n=2^{nlog} m={g.m} iters={it} ms/iter={ms / it:.3f} iter/s={it / ms * 1e3:.1f} build_s={tb:.1f} "
       f"Gedges/s={g.m * it / ms / 1e6:.1f}")
+if os.environ.get("PR_DIAG_INFO"):
+    inf = dg.info()
+    print({k: v for k, v in inf.items() if k.startswith(("bvs", "window", "max_depth", "nblocks"))})
+    x = torch.rand(n, dtype=torch.float64, device="cuda")
+    y = torch.empty_like(x)
+    for _ in range(3):
+        dg.matvec(x, y)
+    torch.cuda.synchronize()
+    a.record()
+    for _ in range(10):
+        dg.matvec(x, y)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / 10
+    print(f"gather A^T (x resident, L2 warm-ish): ms={ms:.3f} Gedges/s={g.m / ms / 1e6:.1f}")
