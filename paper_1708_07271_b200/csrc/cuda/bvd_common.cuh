@@ -70,9 +70,15 @@ __device__ __forceinline__ void dd_add(double& hi, double& lo, double bhi, doubl
 //                                                0 for kDrop)
 //   q'_i = p'_i / d_i  (0 for dangling i)
 // plus per-block partials {sum_{d_i = 0} p'_i, sum |p'_i - p_i|}.
+// An epilogue's per-row inputs are loaded for a thread's kEpiPre rows at
+// once (prefetch), before their chain walks, so the global-load latency
+// overlaps the walks instead of stalling each row's store.
+constexpr uint32_t kEpiPre = 4;
+
 struct PlainEpi {
+  __device__ __forceinline__ void prefetch(uint32_t, uint32_t, uint32_t) {}
   template <typename YT>
-  __device__ __forceinline__ void store(YT* yb, uint32_t k, double y) const {
+  __device__ __forceinline__ void store(YT* yb, uint32_t k, double y, uint32_t) const {
     yb[k] = (YT)y;
   }
   __device__ __forceinline__ void finish(int*) const {}
@@ -94,21 +100,20 @@ struct PageRankEpi {
   const uint8_t* push_mask;    // shard-relative, offset applied; null = no push
   double* const* push_dst;     // device array: peer q buffers, indexed by global column
   uint32_t grow0;              // global row of this block's row 0
+  uint32_t dpre[kEpiPre];      // prefetched d_k of the thread's next rows (p0 / p_prev are optional: loaded in place)
+  __device__ __forceinline__ void prefetch(uint32_t k0, uint32_t T, uint32_t nr) {
+#pragma unroll
+    for (uint32_t q = 0; q < kEpiPre; ++q) {
+      const uint32_t k = k0 + q * T;
+      dpre[q] = k < nr ? __ldg(deg + k) : 0u;
+    }
+  }
   template <typename YT>
-  __device__ __forceinline__ void store(YT* pb, uint32_t k, double y) {
+  __device__ __forceinline__ void store(YT* pb, uint32_t k, double y, uint32_t q) {
     const double pn = (p0 ? alpha_p0 * p0[k] : base) + scale * (y + dn);
     pb[k] = (YT)pn;
-    const uint32_t d = deg[k];
-#if CMVG_QDIV == 1
-    const double qn = d ? pn * __drcp_rn((double)d) : 0.0;
-#elif CMVG_QDIV == 2
-    double r = (double)__frcp_rn((float)d);
-    r = r * fma(-(double)d, r, 2.0);
-    r = r * fma(-(double)d, r, 2.0);
-    const double qn = d ? pn * r : 0.0;
-#else
+    const uint32_t d = dpre[q];
     const double qn = d ? pn / (double)d : 0.0;
-#endif
     q_next[k] = qn;
     if (push_mask) {
       uint32_t m = push_mask[k];
@@ -167,19 +172,25 @@ __device__ __forceinline__ void chain_and_store(double* s_yhi, float* s_ylo, con
     // Bounded chains (R <= 3): each row walks its <= 3 ancestors,
     // y_i = d_i + d_p1 + d_p2 + d_p3 accumulated with TwoSum (error terms
     // collected with the low parts), no barriers.
-    for (uint32_t k = tid; k < c.nr; k += T) {
-      double s = s_yhi[k], e = (double)s_ylo[k];
-      uint32_t p = k, r = c.ref[k];
+    for (uint32_t kb = tid; kb < c.nr; kb += kEpiPre * T) {
+      epi.prefetch(kb, T, c.nr);
 #pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        if (r) {
-          p -= r;
-          tsum(s, e, s_yhi[p]);
-          e += (double)s_ylo[p];
-          r = c.ref[p];
+      for (uint32_t q = 0; q < kEpiPre; ++q) {
+        const uint32_t k = kb + q * T;
+        if (k >= c.nr) break;
+        double s = s_yhi[k], e = (double)s_ylo[k];
+        uint32_t p = k, r = c.ref[k];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          if (r) {
+            p -= r;
+            tsum(s, e, s_yhi[p]);
+            e += (double)s_ylo[p];
+            r = c.ref[p];
+          }
         }
+        epi.store(yb, k, s + e, q);
       }
-      epi.store(yb, k, s + e);
     }
     epi.finish(c.wscratch);
     return;
@@ -227,7 +238,14 @@ __device__ __forceinline__ void chain_and_store(double* s_yhi, float* s_ylo, con
     }
     any = __syncthreads_or(more);
   }
-  for (uint32_t k = tid; k < c.nr; k += T) epi.store(yb, k, s_yhi[k] + (double)s_ylo[k]);
+  for (uint32_t kb = tid; kb < c.nr; kb += kEpiPre * T) {
+    epi.prefetch(kb, T, c.nr);
+#pragma unroll
+    for (uint32_t q = 0; q < kEpiPre; ++q) {
+      const uint32_t k = kb + q * T;
+      if (k < c.nr) epi.store(yb, k, s_yhi[k] + (double)s_ylo[k], q);
+    }
+  }
   epi.finish(c.wscratch);
 }
 
