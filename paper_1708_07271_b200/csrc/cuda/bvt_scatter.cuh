@@ -84,6 +84,27 @@ __device__ __forceinline__ void bvt_term(uint32_t code, const double* ch, const 
   comp += __hiloint2double(__double2hiint(l) ^ sg, __double2loint(l));
 }
 
+// A slice's epilogue: segmented reduction of a multi slice (its round count
+// from the meta word), then the primary lane stores the target's sum.
+__device__ __forceinline__ void bvt_slice_epilogue(uint32_t lane, uint32_t meta, uint32_t h, double hi, double lo,
+                                                   uint32_t W2, double* s_oh, float* s_ol, const BvtOut& out,
+                                                   uint32_t fbase) {
+  if (tmeta_multi(meta)) {
+    const uint32_t heads = __ballot_sync(0xffffffffu, (h >> 30) & 1u);
+    const uint32_t above = heads & ~((2u << lane) - 1u);
+    const uint32_t end = above ? (uint32_t)__ffs(above) - 2u : 31u;
+    const uint32_t rounds = tmeta_rounds(meta);
+#pragma unroll
+    for (uint32_t i = 0; i < 5; ++i) {
+      if (i >= rounds) break;  // warp-uniform
+      const uint32_t o = 1u << i;
+      const double uh = __shfl_down_sync(0xffffffffu, hi, o), ul = __shfl_down_sync(0xffffffffu, lo, o);
+      if (lane + o <= end) dd_add(hi, lo, uh, ul);
+    }
+  }
+  if ((h >> 30) == 3u) bvt_put(th_target(h), hi, lo, W2, s_oh, s_ol, out, fbase);
+}
+
 template <typename XT>
 __global__ void __launch_bounds__(256, 4) bvt_scatter_kernel(BvdDev g, const XT* __restrict__ x, BvtOut out) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -183,7 +204,13 @@ __global__ void __launch_bounds__(256, 4) bvt_scatter_kernel(BvdDev g, const XT*
       if (lane == 0) bvt_put(t, hi, lo, W2, s_oh, s_ol, out, fbase);
     }
   }
-  for (uint32_t s = tid >> 5; s < nsl; s += T >> 5) {  // slices, round-robin (sorted by cost)
+  // slices, round-robin (sorted by cost), software-pipelined: a slice's words
+  // are loaded into registers, and the previous slice's reduction and store
+  // run while those loads are in flight
+  bool have_prev = false;
+  uint32_t prev_meta = 0, prev_h = 0;
+  double prev_hi = 0.0, prev_lo = 0.0;
+  for (uint32_t s = tid >> 5; s < nsl; s += T >> 5) {
     uint32_t roff, meta;
     if (nsl <= kBvtSliceTab) {
       roff = s_tab[2 * s];
@@ -196,28 +223,26 @@ __global__ void __launch_bounds__(256, 4) bvt_scatter_kernel(BvdDev g, const XT*
     const uint32_t h = __ldg(rec + 1u + lane);
     const uint32_t* body = rec + 33u + lane;
     const uint32_t mnw = (tmeta_ne(meta) + 1u) >> 1;
+    uint32_t w[kBvtUnitCodes / 2];
+#pragma unroll
+    for (uint32_t q = 0; q < kBvtUnitCodes / 2; ++q) w[q] = q < mnw ? __ldg(body + q * 32u) : 0u;
+    if (have_prev) bvt_slice_epilogue(lane, prev_meta, prev_h, prev_hi, prev_lo, W2, s_oh, s_ol, out, fbase);
     double acc = 0.0, comp = 0.0, acc2 = 0.0, comp2 = 0.0;
-#pragma unroll 4
-    for (uint32_t q = 0; q < mnw; ++q) {
-      const uint32_t w = __ldg(body + q * 32u);
-      bvt_term(w >> 16, ch, cl, acc, comp);
-      bvt_term(w & 0xffffu, ch, cl, acc2, comp2);
+#pragma unroll
+    for (uint32_t q = 0; q < kBvtUnitCodes / 2; ++q) {
+      if (q >= mnw) break;  // warp-uniform
+      bvt_term(w[q] >> 16, ch, cl, acc, comp);
+      bvt_term(w[q] & 0xffffu, ch, cl, acc2, comp2);
     }
     tsum(acc, comp, acc2);
     comp += comp2;
-    double hi = acc + comp, lo = comp - (hi - acc);
-    if (tmeta_multi(meta)) {
-      const uint32_t heads = __ballot_sync(0xffffffffu, (h >> 30) & 1u);
-      const uint32_t above = heads & ~((2u << lane) - 1u);
-      const uint32_t end = above ? (uint32_t)__ffs(above) - 2u : 31u;
-#pragma unroll
-      for (uint32_t o = 1; o < 32; o <<= 1) {
-        const double uh = __shfl_down_sync(0xffffffffu, hi, o), ul = __shfl_down_sync(0xffffffffu, lo, o);
-        if (lane + o <= end) dd_add(hi, lo, uh, ul);
-      }
-    }
-    if ((h >> 30) == 3u) bvt_put(th_target(h), hi, lo, W2, s_oh, s_ol, out, fbase);
+    prev_hi = acc + comp;
+    prev_lo = comp - (prev_hi - acc);
+    prev_h = h;
+    prev_meta = meta;
+    have_prev = true;
   }
+  if (have_prev) bvt_slice_epilogue(lane, prev_meta, prev_h, prev_hi, prev_lo, W2, s_oh, s_ol, out, fbase);
   __syncthreads();
 
   // ---- 3. window partial = point sums + inclusive prefix of the differences

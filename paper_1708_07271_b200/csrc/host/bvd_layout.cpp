@@ -311,7 +311,7 @@ void emit_bvs(const RowParts* rps, const RowMeta* meta, const BitWriter& body, u
 // grouped by target column.
 void emit_bvt(const RowParts* rps, const RowMeta* meta, uint32_t nr, uint32_t B, uint64_t wlo, uint32_t W,
               std::vector<uint32_t>& so, std::vector<uint32_t>& far_cols, BvtStats& st) {
-  constexpr uint32_t kUnit = 16, kMaxUnits = 32;
+  constexpr uint32_t kUnit = kBvtUnitCodes, kMaxUnits = kBvtMaxUnits;
   // contributions grouped by target with flat arrays (counting sort for the
   // 2W window targets, a sort for the few far columns); codes k | minus << 15
   // stay in row order within a target
@@ -406,6 +406,7 @@ void emit_bvt(const RowParts* rps, const RowMeta* meta, uint32_t nr, uint32_t B,
   struct Slice {
     std::vector<const U*> lanes;
     bool multi;
+    uint32_t maxnu = 1;  // most units of one target in the slice
   };
   std::vector<Slice> slices;
   auto load = [&](const std::pair<uint32_t, uint32_t>& r) {
@@ -422,6 +423,7 @@ void emit_bvt(const RowParts* rps, const RowMeta* meta, uint32_t nr, uint32_t B,
     while (t < slices.size() && slices[t].lanes.size() + r.second > 32) ++t;
     if (t == slices.size()) slices.push_back(Slice{{}, true});
     for (uint32_t q = 0; q < r.second; ++q) slices[t].lanes.push_back(&units[r.first + q]);
+    slices[t].maxnu = std::max(slices[t].maxnu, r.second);
   }
   std::stable_sort(singles.begin(), singles.end(),
                    [&](uint32_t a, uint32_t b) { return units[a].count > units[b].count; });
@@ -473,7 +475,9 @@ void emit_bvt(const RowParts* rps, const RowMeta* meta, uint32_t nr, uint32_t B,
       mne = std::max<uint32_t>(mne, u->count);
       st.lane_iters_used += u->count;
     }
-    so.push_back(make_tmeta(mne, sl.multi));
+    uint32_t rounds = 0;
+    while ((1u << rounds) < sl.maxnu) ++rounds;
+    so.push_back(make_tmeta(mne, sl.multi, rounds));
     so[kBvtHead + 2 * s + 1] = so.back();  // the table repeats the meta word
     for (size_t l = 0; l < 32; ++l) so.push_back(l < sl.lanes.size() ? make_th(sl.lanes[l]->primary, sl.lanes[l]->target) : 0u);
     const uint32_t mnw = (mne + 1) / 2;

@@ -174,16 +174,20 @@ __host__ __device__ constexpr uint32_t smeta_rounds(uint32_t m) { return (m >> 1
 // Block table entry: word_offset, nwords, wlo as BV-D; pad[0] = first far
 // staging slot of the block.
 constexpr uint32_t kBvtHead = 8;
+constexpr uint32_t kBvtUnitCodes = 16;  // codes per target unit
+constexpr uint32_t kBvtMaxUnits = 32;   // units of a slice target (more: heavy target)
 constexpr uint32_t kBvtHeavyEntry = 3;
 __host__ __device__ constexpr uint32_t make_th(bool primary, uint32_t target) {
   return (1u << 31) | ((primary ? 1u : 0u) << 30) | target;
 }
 __host__ __device__ constexpr uint32_t th_target(uint32_t h) { return h & 0x3fffffffu; }
-__host__ __device__ constexpr uint32_t make_tmeta(uint32_t max_ne, bool multi) {
-  return max_ne | ((multi ? 1u : 0u) << 10);
+// rounds: as smeta_rounds (segmented-reduction rounds of a multi slice)
+__host__ __device__ constexpr uint32_t make_tmeta(uint32_t max_ne, bool multi, uint32_t rounds = 0) {
+  return max_ne | ((multi ? 1u : 0u) << 10) | (rounds << 11);
 }
 __host__ __device__ constexpr uint32_t tmeta_ne(uint32_t m) { return m & 1023u; }
 __host__ __device__ constexpr bool tmeta_multi(uint32_t m) { return (m >> 10) & 1u; }
+__host__ __device__ constexpr uint32_t tmeta_rounds(uint32_t m) { return (m >> 11) & 7u; }
 
 struct BvdBlockInfo {
   uint64_t word_offset;  // first u32 word of this block's stream (16-byte aligned)

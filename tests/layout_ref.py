@@ -271,13 +271,17 @@ def scatter_bvt_int(words, blocks, n, B, W, x):
             rec = s[8 + 2 * sl]
             meta = s[rec]
             assert s[8 + 2 * sl + 1] == meta
-            mne, multi = meta & 1023, (meta >> 10) & 1
+            mne, multi, rounds = meta & 1023, (meta >> 10) & 1, (meta >> 11) & 7
             mnw = (mne + 1) >> 1
+            run, max_run = 0, 0  # units of the current target, most units of one target
             for lane in range(32):
                 h = s[rec + 1 + lane]
                 if not h >> 31:
+                    run = 0
                     continue
                 prim, t = (h >> 30) & 1, h & 0x3FFFFFFF
+                run = 1 if prim else run + 1
+                max_run = max(max_run, run)
                 tot = 0
                 for q in range(mnw):
                     w = s[rec + 33 + lane + 32 * q]
@@ -289,6 +293,7 @@ def scatter_bvt_int(words, blocks, n, B, W, x):
                 else:
                     assert multi and t == cur
                     out[cur] += tot
+            assert (1 << rounds) >= max_run and (rounds == 0 or (1 << (rounds - 1)) < max_run)
         run = 0
         for j in range(W):
             run += out.get(W + j, 0)
