@@ -277,7 +277,13 @@ __global__ void __launch_bounds__(256, 4) bvt_scatter_kernel(BvdDev g, const XT*
   }
 }
 
-// Kernel 2: combine staged partials per column tile, fixed order.
+// Kernel 2: combine staged partials per column tile, fixed order.  The
+// tile's covering blocks (their window offsets) and its far (column, slot)
+// pairs are staged in shared memory first, so a column's sum issues its
+// staging loads back to back instead of walking global tables.
+constexpr uint32_t kCombCover = 32;   // covering blocks staged per tile
+constexpr uint32_t kCombFar = 2048;   // far pairs staged per tile
+
 template <typename YT>
 __global__ void __launch_bounds__(256) bvt_combine_kernel(BvdDev g, const uint32_t* __restrict__ tile_ptr,
                                                           const uint32_t* __restrict__ tile_blk,
@@ -285,31 +291,72 @@ __global__ void __launch_bounds__(256) bvt_combine_kernel(BvdDev g, const uint32
                                                           const uint32_t* __restrict__ farp, BvtOut out,
                                                           uint32_t nbl, uint32_t fs0, uint32_t fs1,
                                                           YT* __restrict__ y) {
+  __shared__ uint32_t s_bl[kCombCover], s_wlo[kCombCover], s_far[2 * kCombFar];
+  __shared__ uint32_t s_nc;
   const BvdDims& D = g.d;
-  const uint32_t B = D.block_rows, W = D.window;
+  const uint32_t B = D.block_rows, W = D.window, tid = threadIdx.x;
   const uint32_t t = blockIdx.x;
   const uint32_t c0 = t * B;
   const uint32_t q0 = tile_ptr[t], q1 = tile_ptr[t + 1];
   const uint32_t f0 = farp_ptr[t], f1 = farp_ptr[t + 1];
-  for (uint32_t j = threadIdx.x; j < B && c0 + j < D.n; j += blockDim.x) {
+  const bool staged = q1 - q0 <= kCombCover && f1 - f0 <= kCombFar;
+  if (staged) {
+    if (tid < 32) {  // this shard's covering blocks, in block order
+      const uint32_t q = q0 + tid;
+      uint32_t b = 0;
+      bool mine = false;
+      if (q < q1) {
+        b = tile_blk[q];
+        mine = b >= g.block_begin && b - g.block_begin < nbl;
+      }
+      const uint32_t m = __ballot_sync(0xffffffffu, mine);
+      if (mine) {
+        const uint32_t i = __popc(m & ((1u << tid) - 1u)), bl = b - g.block_begin;
+        s_bl[i] = bl;
+        s_wlo[i] = g.blocks[bl].wlo;
+      }
+      if (tid == 0) s_nc = __popc(m);
+    }
+    for (uint32_t i = tid; i < 2 * (f1 - f0); i += blockDim.x) s_far[i] = farp[2 * f0 + i];
+    __syncthreads();
+  }
+  for (uint32_t j = tid; j < B && c0 + j < D.n; j += blockDim.x) {
     const uint32_t col = c0 + j;
     double hi = 0.0, lo = 0.0;
-    for (uint32_t q = q0; q < q1; ++q) {
-      const uint32_t b = tile_blk[q];
-      if (b < g.block_begin || b - g.block_begin >= nbl) continue;  // another shard's block
-      const uint32_t bl = b - g.block_begin;
-      const uint32_t jj = col - g.blocks[bl].wlo;
-      if (jj < W) dd_add(hi, lo, out.st_hi[(size_t)bl * W + jj], (double)out.st_lo[(size_t)bl * W + jj]);
+    uint32_t p0 = 0, pe = 0;
+    const uint32_t* fp;
+    if (staged) {
+      const uint32_t nc = s_nc;
+      for (uint32_t i = 0; i < nc; ++i) {
+        const uint32_t jj = col - s_wlo[i];
+        if (jj < W) {
+          const size_t o = (size_t)s_bl[i] * W + jj;
+          dd_add(hi, lo, out.st_hi[o], (double)out.st_lo[o]);
+        }
+      }
+      fp = s_far;
+      pe = f1 - f0;
+    } else {
+      for (uint32_t q = q0; q < q1; ++q) {
+        const uint32_t b = tile_blk[q];
+        if (b < g.block_begin || b - g.block_begin >= nbl) continue;  // another shard's block
+        const uint32_t bl = b - g.block_begin;
+        const uint32_t jj = col - g.blocks[bl].wlo;
+        if (jj < W) dd_add(hi, lo, out.st_hi[(size_t)bl * W + jj], (double)out.st_lo[(size_t)bl * W + jj]);
+      }
+      fp = farp;
+      p0 = f0;
+      pe = f1;
     }
     // far slots of this column: pairs sorted by (column, slot)
-    uint32_t lo_i = f0, hi_i = f1;
-    while (lo_i < hi_i) {
-      const uint32_t mid = (lo_i + hi_i) >> 1;
-      if (farp[2 * mid] < col) lo_i = mid + 1;
-      else hi_i = mid;
+    uint32_t a = p0, e = pe;
+    while (a < e) {
+      const uint32_t mid = (a + e) >> 1;
+      if (fp[2 * mid] < col) a = mid + 1;
+      else e = mid;
     }
-    for (uint32_t p = lo_i; p < f1 && farp[2 * p] == col; ++p) {
-      const uint32_t slot = farp[2 * p + 1];
+    for (uint32_t p = a; p < pe && fp[2 * p] == col; ++p) {
+      const uint32_t slot = fp[2 * p + 1];
       if (slot >= fs0 && slot < fs1) dd_add(hi, lo, out.far_hi[slot], (double)out.far_lo[slot]);
     }
     y[col] = (YT)(hi + lo);

@@ -23,7 +23,11 @@ void launch_scatter(cmvg_graph* g, const T* x, T* y, cudaStream_t st) {
   o.far_lo -= g->tfar_begin;
   const BvtSmem L = bvt_smem_layout(g->dims);
   auto k1 = bvt_scatter_kernel<T>;
-  CUDA_TRY(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
+  const unsigned bit = sizeof(T) == 8 ? 4u : 8u;  // the attribute call is not free: once per handle and type
+  if (!(g->gather_attr & bit)) {
+    CUDA_TRY(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
+    g->gather_attr |= bit;
+  }
   k1<<<g->nblocks, g->threads, L.total, st>>>(g->tdev(), x, o);
   CUDA_TRY(cudaGetLastError());
   const uint32_t ntiles = g->dims.nblocks;
