@@ -23,11 +23,13 @@ deg = torch.from_numpy(g.out_degrees().astype(np.int32)).cuda()
 dg.pagerank(deg, alpha=0.15, iterations=3)
 torch.cuda.synchronize()
 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-a.record()
-p, it = dg.pagerank(deg, alpha=0.15, iterations=iters)
-b.record()
-torch.cuda.synchronize()
-ms = a.elapsed_time(b)
+ms = float("inf")
+for _ in range(int(os.environ.get("PR_DIAG_REPS", "1"))):  # min over repetitions
+    a.record()
+    p, it = dg.pagerank(deg, alpha=0.15, iterations=iters)
+    b.record()
+    torch.cuda.synchronize()
+    ms = min(ms, a.elapsed_time(b))
 print(f"n=2^{nlog} m={g.m} iters={it} ms/iter={ms / it:.3f} iter/s={it / ms * 1e3:.1f} build_s={tb:.1f} "
       f"Gedges/s={g.m * it / ms / 1e6:.1f}")
 if os.environ.get("PR_DIAG_INFO"):
