@@ -1,16 +1,19 @@
-// The per-block x-window in shared memory: x[wlo, wlo + W) staged with
-// coalesced loads into a padded layout (8-entry tiles at a stride of 9
-// entries, so a thread walks one tile with at most 2-way bank conflicts), plus
-// an exclusive prefix F of the window in double-double (hi fp64, lo fp32),
-// built in three parallel steps: the 8-entry tile totals (one thread per
-// tile), their exclusive prefix Q (one warp), then F within each tile
-// starting from Q (one thread per tile) -- x is read twice and F written
-// once.  An interval [a, e) is then F[e] - F[a]: one TwoSum, O(1) for any
-// length, and accurate to ~1e-28 absolute, so interval sums carry no rounding
-// error into the reference chain (the north star's O(1) interval evaluation
-// from an exclusive prefix of x).
+// The per-block x-window in shared memory: x[wlo, wlo + W) in a padded layout
+// (8-entry tiles at a stride of 9 entries; the transcoder's codes are padded
+// indices), plus an exclusive prefix F of the window in double-double (hi
+// fp64, lo fp32).  Staging is one pass per round of T x E entries (E <= 8
+// contiguous entries per thread, E = W / T = 6 at the default W = 1536,
+// T = 256): each thread loads its chunk with paired (16-B) loads issued before
+// the CTA's first barrier, sums it in double-double, the chunk totals are
+// scanned with warp shuffles and one barrier for the warp totals, and each
+// thread then writes its x entries and their prefix values F from registers.
+// An interval [a, e) is then F[e] - F[a]: one TwoSum, O(1) for any length,
+// and accurate to ~1e-28 absolute, so interval sums carry no rounding error
+// into the reference chain (the north star's O(1) interval evaluation from an
+// exclusive prefix of x).
 #pragma once
 #include <cstdint>
+#include <type_traits>
 
 #include "../host/layout.hpp"
 
@@ -19,14 +22,16 @@ namespace cmvg {
 constexpr uint32_t kXwTile = 8;  // entries per tile (bvs_pad_index: stride 9)
 __host__ __device__ constexpr uint32_t xw_pad(uint32_t j) { return bvs_pad_index(j); }
 
-// bytes of the x-window region for W entries of type XT (x, F hi / lo, Q hi / lo)
+// warp-total scratch of the staging scan (2 doubles per warp, <= 32 warps, + carry)
+constexpr uint32_t kXwScratch = 2 * 32 + 2;
+
+// bytes of the x-window region for W entries of type XT (x, F hi / lo, scratch)
 __host__ __device__ inline uint32_t xw_bytes(uint32_t W, uint32_t xsize) {
   const uint32_t padded = xw_pad(W) + 1;
   uint32_t b = ((padded * xsize + 15u) & ~15u);
-  b += ((padded * 8u + 15u) & ~15u);                // F hi
-  b += ((padded * 4u + 15u) & ~15u);                // F lo
-  b += (((W / kXwTile + 1) * 8u + 15u) & ~15u);    // Q hi
-  b += (((W / kXwTile + 1) * 4u + 15u) & ~15u);    // Q lo
+  b += ((padded * 8u + 15u) & ~15u);  // F hi
+  b += ((padded * 4u + 15u) & ~15u);  // F lo
+  b += kXwScratch * 8u;               // warp totals
   return b;
 }
 
@@ -41,8 +46,7 @@ struct XWin {
   XT* s_x;
   double* s_ph;
   float* s_pl;
-  double* s_th;
-  float* s_tl;
+  double* s_wt;  // staging scratch: warp totals, carry
   const XT* __restrict__ x;
   const XT* xfar;  // x at the columns outside the window (only those are read from it)
   uint32_t wlo, W;
@@ -57,20 +61,45 @@ struct XWin {
     p += (padded * 8u + 15u) & ~15u;
     s_pl = reinterpret_cast<float*>(p);
     p += (padded * 4u + 15u) & ~15u;
-    s_th = reinterpret_cast<double*>(p);
-    p += ((Wn / kXwTile + 1) * 8u + 15u) & ~15u;
-    s_tl = reinterpret_cast<float*>(p);
+    s_wt = reinterpret_cast<double*>(p);
   }
 
-  // Register prefetch of the first kPre*T window entries: issued before the
-  // stream wait and row setup so the global-load latency overlaps them.
+  // entries per thread per round: ceil(W / T) capped at kPre, rounded up to
+  // even (paired loads); T = blockDim.x is a power of two
   static constexpr uint32_t kPre = 8;
-  __device__ __forceinline__ void prefetch(uint32_t n, XT (&r)[kPre]) const {
+  __device__ __forceinline__ uint32_t chunk() const {
+    const uint32_t lg = (uint32_t)__ffs((int)blockDim.x) - 1u;
+    const uint32_t e = min(kPre, (W + blockDim.x - 1u) >> lg);
+    return (e + 1u) & ~1u;
+  }
+
+  // Loads of a thread's chunk [j0, j0 + E) of the window (zeros past W or n),
+  // two entries per load when x is aligned for it.
+  __device__ __forceinline__ void load_chunk(uint32_t n, uint32_t j0, uint32_t E, XT (&r)[kPre]) const {
+    using P2 = typename std::conditional<sizeof(XT) == 8, double2, float2>::type;
+    const bool vec = (reinterpret_cast<uintptr_t>(x) & (2 * sizeof(XT) - 1)) == 0;
 #pragma unroll
-    for (uint32_t q = 0; q < kPre; ++q) {
-      const uint32_t j = threadIdx.x + q * blockDim.x, c = wlo + j;
-      r[q] = (j < W && c < n) ? __ldg(x + c) : XT(0);
+    for (uint32_t q = 0; q < kPre / 2; ++q) {
+      r[2 * q] = XT(0);
+      r[2 * q + 1] = XT(0);
+      const uint32_t j = j0 + 2 * q, c = wlo + j;
+      if (2 * q < E && j < W) {  // W is a multiple of 16 and j even: j + 1 < W
+        if (vec && c + 1 < n) {
+          const P2 v = __ldg(reinterpret_cast<const P2*>(x + c));
+          r[2 * q] = v.x;
+          r[2 * q + 1] = v.y;
+        } else {
+          if (c < n) r[2 * q] = __ldg(x + c);
+          if (c + 1 < n) r[2 * q + 1] = __ldg(x + c + 1);
+        }
+      }
     }
+  }
+
+  // Register prefetch of the first round's chunk: issued before the CTA's
+  // other setup so the global-load latency overlaps it.
+  __device__ __forceinline__ void prefetch(uint32_t n, XT (&r)[kPre]) const {
+    load_chunk(n, threadIdx.x * chunk(), chunk(), r);
   }
 
   // Cooperative staging (all threads of the CTA); ends with __syncthreads().
@@ -79,102 +108,93 @@ struct XWin {
     prefetch(n, r);
     stage(n, r);
   }
-  __device__ __forceinline__ void stage(uint32_t n, const XT (&r)[kPre]) {
-    const uint32_t T = blockDim.x, tid = threadIdx.x;
+  __device__ __forceinline__ void stage(uint32_t n, const XT (&r0)[kPre]) {
+    const uint32_t T = blockDim.x, tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const uint32_t E = chunk(), per_round = T * E;
+    double ch = 0.0, cl = 0.0;  // carry: the window total before this round (double-double)
+    XT r[kPre];
 #pragma unroll
-    for (uint32_t q = 0; q < kPre; ++q) {
-      const uint32_t j = tid + q * T;
-      if (j < W) s_x[xw_pad(j)] = r[q];
-    }
-    if (tid == 0) s_x[xw_pad(W)] = XT(0);  // zero entry for idle lanes
-    for (uint32_t j = tid + kPre * T; j < W; j += T) {
-      const uint32_t c = wlo + j;
-      s_x[xw_pad(j)] = c < n ? __ldg(x + c) : XT(0);
-    }
-    {
-      __syncthreads();
-      const uint32_t ntiles = W / kXwTile;
-      for (uint32_t t = tid; t < ntiles; t += T) {  // tile totals
-        const uint32_t base = t * (kXwTile + 1);
-        double hi = 0.0, lo = 0.0;
+    for (uint32_t k = 0; k < kPre; ++k) r[k] = r0[k];
+    if (tid == 0) s_x[xw_pad(W)] = XT(0);  // zero entry for padding codes and idle lanes
+    for (uint32_t rb = 0; rb < W; rb += per_round) {
+      const uint32_t j0 = rb + tid * E;
+      if (rb) load_chunk(n, j0, E, r);
+      // chunk total (double-double)
+      double h = 0.0, l = 0.0;
 #pragma unroll
-        for (uint32_t j = 0; j < kXwTile; ++j) {
+      for (uint32_t k = 0; k < kPre; ++k) {
+        if (k < E) {
           double s, e;
-          two_sum(hi, (double)s_x[base + j], s, e);
-          hi = s;
-          lo += e;
-        }
-        const double h2 = hi + lo;
-        s_th[t] = h2;
-        s_tl[t] = (float)(lo - (h2 - hi));
-      }
-      __syncthreads();
-      if (tid < 32) {  // Q: exclusive double-double prefix of the tile totals (one warp)
-        const uint32_t lane = tid, per = (ntiles + 31u) / 32u;
-        double lh = 0.0, ll = 0.0;
-        for (uint32_t q = 0; q < per; ++q) {
-          const uint32_t t = lane * per + q;
-          if (t < ntiles) {
-            double s, e;
-            two_sum(lh, s_th[t], s, e);
-            lh = s;
-            ll += e + (double)s_tl[t];
-          }
-        }
-        double ih = lh, il = ll;  // inclusive warp scan in double-double
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const double uh = __shfl_up_sync(0xffffffffu, ih, o), ul = __shfl_up_sync(0xffffffffu, il, o);
-          if ((int)lane >= o) {
-            double s, e;
-            two_sum(ih, uh, s, e);
-            ih = s;
-            il += ul + e;
-          }
-        }
-        double rh = __shfl_up_sync(0xffffffffu, ih, 1), rl = __shfl_up_sync(0xffffffffu, il, 1);
-        if (lane == 0) rh = rl = 0.0;
-        for (uint32_t q = 0; q < per; ++q) {
-          const uint32_t t = lane * per + q;
-          if (t < ntiles) {
-            const double th = s_th[t];
-            const float tl = s_tl[t];
-            const double h2 = rh + rl;
-            s_th[t] = h2;  // in place: tile total -> exclusive prefix Q[t]
-            s_tl[t] = (float)(rl - (h2 - rh));
-            double s, e;
-            two_sum(rh, th, s, e);
-            rh = s;
-            rl += e + (double)tl;
-          }
-        }
-        if (lane == 31) {
-          const double h2 = ih + il;
-          s_th[ntiles] = h2;
-          s_tl[ntiles] = (float)(il - (h2 - ih));
+          two_sum(h, (double)r[k], s, e);
+          h = s;
+          l += e;
         }
       }
-      __syncthreads();
-      for (uint32_t t = tid; t < ntiles; t += T) {  // F within each tile, from Q[t]
-        const uint32_t base = t * (kXwTile + 1);
-        double hi = s_th[t], lo = (double)s_tl[t];
+      // inclusive warp scan of the chunk totals
 #pragma unroll
-        for (uint32_t j = 0; j < kXwTile; ++j) {
-          const double h2 = hi + lo;
-          s_ph[base + j] = h2;
-          s_pl[base + j] = (float)(lo - (h2 - hi));
+      for (uint32_t o = 1; o < 32; o <<= 1) {
+        const double uh = __shfl_up_sync(0xffffffffu, h, o), ul = __shfl_up_sync(0xffffffffu, l, o);
+        if (lane >= o) {
           double s, e;
-          two_sum(hi, (double)s_x[base + j], s, e);
-          hi = s;
-          lo += e;
+          two_sum(h, uh, s, e);
+          h = s;
+          l += ul + e;
         }
       }
-      if (tid == 0) {  // F at the window end: the total
-        s_ph[xw_pad(W)] = s_th[ntiles];
-        s_pl[xw_pad(W)] = s_tl[ntiles];
+      if (lane == 31) {
+        s_wt[2 * warp] = h;
+        s_wt[2 * warp + 1] = l;
+      }
+      double ph = __shfl_up_sync(0xffffffffu, h, 1), pl = __shfl_up_sync(0xffffffffu, l, 1);
+      if (lane == 0) ph = pl = 0.0;
+      __syncthreads();
+      // + the totals of the warps before this one, + the carry
+      {
+        double s, e;
+        two_sum(ph, ch, s, e);
+        ph = s;
+        pl += cl + e;
+        for (uint32_t w = 0; w < warp; ++w) {
+          two_sum(ph, s_wt[2 * w], s, e);
+          ph = s;
+          pl += s_wt[2 * w + 1] + e;
+        }
+      }
+      // x and F from registers
+#pragma unroll
+      for (uint32_t k = 0; k < kPre; ++k) {
+        const uint32_t j = j0 + k;
+        if (k < E && j < W) {
+          const uint32_t p = xw_pad(j);
+          s_x[p] = r[k];
+          const double hi = ph + pl;
+          s_ph[p] = hi;
+          s_pl[p] = (float)(pl - (hi - ph));
+          double s, e;
+          two_sum(ph, (double)r[k], s, e);
+          ph = s;
+          pl += e;
+        }
+      }
+      // the last thread's running sum is the window total through this round:
+      // F[W] after the last round, else the next round's carry
+      const bool last = rb + per_round >= W;
+      if (tid == T - 1u) {
+        if (last) {
+          const double hi = ph + pl;
+          s_ph[xw_pad(W)] = hi;
+          s_pl[xw_pad(W)] = (float)(pl - (hi - ph));
+        } else {
+          s_wt[2 * 32] = ph;
+          s_wt[2 * 32 + 1] = pl;
+        }
+      }
+      __syncthreads();
+      if (!last) {
+        ch = s_wt[2 * 32];
+        cl = s_wt[2 * 32 + 1];
       }
     }
-    __syncthreads();
   }
 
   // Unchecked accessors for `near` rows (the builder guarantees the window
