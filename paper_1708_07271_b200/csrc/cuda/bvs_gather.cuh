@@ -182,17 +182,25 @@ __device__ __forceinline__ void bvs_slice_epilogue(uint32_t lane, uint32_t meta,
 template <class XW>
 __device__ __forceinline__ void bvs_slices(const uint32_t* __restrict__ bs, const XW& xw, uint32_t lmin, int* misc,
                                            double* s_yhi, float* s_ylo, uint8_t* s_ref, const uint32_t* s_tab) {
+  constexpr bool kExact = sizeof(typename XW::value_type) == 8;  // compensated point sums for fp64 x
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t nsl = __ldg(bs) & 0xffffu;
   bool have_prev = false;
   uint32_t prev_meta = 0, prev_h = 0;
   double prev_hi = 0.0, prev_lo = 0.0;
-  // static round-robin over the warps: the transcoder balanced the slices'
-  // work, and no ticket round trip sits in front of each slice's loads
-  const uint32_t nwarp = blockDim.x >> 5;
-  uint32_t s = threadIdx.x >> 5;
-  while (s < nsl) {
-    const uint32_t next = s + nwarp;
+  // static schedule: with kBvsWarps warps each takes the contiguous table
+  // range the transcoder's LPT assignment gave it (header words 4..8), else
+  // round-robin; no ticket round trip sits in front of a slice's loads
+  const uint32_t nwarp = blockDim.x >> 5, warp = threadIdx.x >> 5;
+  uint32_t s = warp, s_end = nsl, step = nwarp;
+  if (nwarp == kBvsWarps) {
+    const uint16_t* starts = reinterpret_cast<const uint16_t*>(bs + kBvsWarpTab);
+    s = __ldg(starts + warp);
+    s_end = __ldg(starts + warp + 1);
+    step = 1;
+  }
+  while (s < s_end) {
+    const uint32_t next = s + step;
     // slice table entry from shared memory (staged per block) when it fits:
     // header, meta and body words then come in one round of global loads
     uint32_t roff, meta;
@@ -228,10 +236,18 @@ __device__ __forceinline__ void bvs_slices(const uint32_t* __restrict__ bs, cons
         const uint32_t v = w[q];
         const double x0 = xw.at_padded((v >> 16) & 0x7fffu), x1 = xw.at_padded(v & 0x7fffu);
         // minus codes: flip the sign bit (bit 15 of each code)
-        // TwoSum, not plain adds: plain fp64 here measured 1.7e-11 relative
-        // error on C2 (rows whose copy list cancels most of the reference row)
-        tsum(acc, comp, __hiloint2double(__double2hiint(x0) ^ (int)(v & 0x80000000u), __double2loint(x0)));
-        tsum(acc2, comp2, __hiloint2double(__double2hiint(x1) ^ (int)((v << 16) & 0x80000000u), __double2loint(x1)));
+        // fp64 x: TwoSum, not plain adds: plain fp64 here measured 1.7e-11
+        // relative error on C2 (rows whose copy list cancels most of the
+        // reference row)
+        const double t0 = __hiloint2double(__double2hiint(x0) ^ (int)(v & 0x80000000u), __double2loint(x0));
+        const double t1 = __hiloint2double(__double2hiint(x1) ^ (int)((v << 16) & 0x80000000u), __double2loint(x1));
+        if constexpr (kExact) {
+          tsum(acc, comp, t0);
+          tsum(acc2, comp2, t1);
+        } else {  // fp32 x: plain fp64 sums (error ~1e-16 x cancellation, far inside the fp32 tolerance)
+          acc += t0;
+          acc2 += t1;
+        }
       }
       tsum(acc, comp, acc2);
       comp += comp2;

@@ -43,6 +43,7 @@ __device__ __forceinline__ void two_sum(double a, double b, double& s, double& e
 
 template <typename XT>
 struct XWin {
+  using value_type = XT;
   XT* s_x;
   double* s_ph;
   float* s_pl;

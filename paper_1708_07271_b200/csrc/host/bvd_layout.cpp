@@ -233,7 +233,44 @@ void emit_bvs(const RowParts* rps, const RowMeta* meta, const BitWriter& body, u
   }
   const uint32_t nsl = (uint32_t)slices.size(), nh = (uint32_t)hrows.size();
   if (nsl > 0xffffu || nh > 0xffffu) throw std::runtime_error("BV-S: block too large");
-  so.assign(kBvsHead + 2 * nsl, 0u);
+  {
+    // Static warp schedule: longest-processing-time assignment of the slices
+    // to the kBvsWarps warps of a CTA by an instruction-count estimate, the
+    // table reordered so warp w owns entries [start_w, start_{w+1}) -- no
+    // ticket round trips, and the warps reach the chain barrier together.
+    std::vector<uint32_t> cost(nsl), ord(nsl);
+    for (uint32_t s = 0; s < nsl; ++s) {
+      const Slice& sl = slices[s];
+      uint32_t mnp = 0, mni = 0;
+      for (uint32_t ui : sl.lanes) {
+        mnp = std::max(mnp, units[ui].np);
+        mni = std::max(mni, units[ui].ni);
+      }
+      uint32_t rounds = 0;
+      while ((1u << rounds) < sl.maxnu) ++rounds;
+      const bool nearc16 = !sl.c32 && !sl.far;
+      cost[s] = 110u + (nearc16 ? 27u * ((mnp + 1) / 2) + 35u * mni : 22u * mnp + 60u * mni) + 30u * rounds;
+      ord[s] = s;
+    }
+    std::stable_sort(ord.begin(), ord.end(), [&](uint32_t a, uint32_t b) { return cost[a] > cost[b]; });
+    std::vector<std::vector<uint32_t>> bins(kBvsWarps);
+    std::vector<uint64_t> loadw(kBvsWarps, 0);
+    for (uint32_t s : ord) {
+      const uint32_t w = (uint32_t)(std::min_element(loadw.begin(), loadw.end()) - loadw.begin());
+      bins[w].push_back(s);
+      loadw[w] += cost[s];
+    }
+    std::vector<Slice> sorted;
+    sorted.reserve(nsl);
+    so.assign(kBvsHead + 2 * nsl, 0u);
+    uint16_t* starts = reinterpret_cast<uint16_t*>(&so[kBvsWarpTab]);
+    for (uint32_t w = 0; w < kBvsWarps; ++w) {
+      starts[w] = (uint16_t)sorted.size();
+      for (uint32_t s : bins[w]) sorted.push_back(std::move(slices[s]));
+    }
+    starts[kBvsWarps] = (uint16_t)sorted.size();
+    slices.swap(sorted);
+  }
   so[0] = nsl | (nh << 16);
   for (uint32_t s = 0; s < nsl; ++s) {
     const Slice& sl = slices[s];

@@ -93,8 +93,11 @@ __host__ __device__ constexpr uint32_t make_hdr(uint32_t r, uint32_t nm, uint32_
 //     stream (BV-D codes).
 // Block stream (u32 words):
 //   [0] nslices | nheavy << 16   [1] heavy table offset   [2] heavy stream offset
-//   [3] 0                        [4, 4 + 2 nslices) slice table: (record
-//                                offset, meta) per slice
+//   [3] 0   [4, 9) u16 start of warp w's slices in the table (w < 8), then
+//   the table size: the static warp schedule (longest-processing-time
+//   assignment by an instruction estimate; warp w decodes entries
+//   [start_w, start_{w+1}))   [9] 0
+//   [10, 10 + 2 nslices) slice table: (record offset, meta) per slice
 //   slice record: [meta][header x 32][body]
 //     meta: max #points | max #intervals << 5 | class32 << 8 | far << 9 |
 //           multi << 10
@@ -107,7 +110,9 @@ constexpr uint32_t kBvsUnitPts = 16;
 constexpr uint32_t kBvsUnitInts = 2;
 constexpr uint32_t kBvsMaxUnits = 32;  // more -> heavy row
 constexpr uint32_t kBvsHeavyEntry = 6;
-constexpr uint32_t kBvsHead = 4;
+constexpr uint32_t kBvsWarps = 8;     // warps of the gather CTA the static schedule is built for
+constexpr uint32_t kBvsWarpTab = 4;   // header words [4, 9): u16 slice-table start per warp, + end
+constexpr uint32_t kBvsHead = 10;
 constexpr uint32_t kBvsBias16 = 32768;
 // padded x-window index (8-entry tiles at a stride of 9; cuda/xwindow.cuh)
 __host__ __device__ constexpr uint32_t bvs_pad_index(uint32_t j) { return j + (j >> 3); }

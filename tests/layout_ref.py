@@ -109,6 +109,9 @@ def decode_sliced(words, blocks, n, B, lmin, W):
         nsl, nh = s[0] & 0xFFFF, s[0] >> 16
         htab, hstr = s[1], s[2]
         assert s[3] == 0
+        # static warp schedule: u16 table starts of the 8 warps, then the table size
+        starts = [(s[4 + q // 2] >> (16 * (q % 2))) & 0xFFFF for q in range(9)]
+        assert starts[0] == 0 and starts[8] == nsl and all(a <= b for a, b in zip(starts, starts[1:]))
         parts = {}   # k -> dict(minus, res, ints, r)
 
         def inwin(c):
@@ -130,9 +133,9 @@ def decode_sliced(words, blocks, n, B, lmin, W):
             assert k not in parts
             parts[k] = dict(minus=pts[:nm], res=pts[nm:], ints=ints, r=r)
         for sl in range(nsl):
-            rec = s[4 + 2 * sl]
+            rec = s[10 + 2 * sl]
             meta = s[rec]
-            assert s[4 + 2 * sl + 1] == meta
+            assert s[10 + 2 * sl + 1] == meta
             mnp, mni, c32, far, multi = meta & 31, (meta >> 5) & 7, (meta >> 8) & 1, (meta >> 9) & 1, (meta >> 10) & 1
             rounds = (meta >> 11) & 7
             seen_np, seen_ni = 0, 0
