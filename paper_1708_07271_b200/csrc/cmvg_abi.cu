@@ -469,7 +469,10 @@ void launch_gather(cmvg_graph* g, const XT* x, YT* y, cudaStream_t st, const XT*
   b1 = std::min(b1, g->nblocks);
   if (b0 >= b1) return;
   const BvsSmem L = bvs_smem_layout(g->dims, sizeof(XT));
-  auto kern = bvs_gather_kernel<XT, YT>;
+  const bool dflt = g->dims.window == kGatherDefault.W && g->dims.block_rows == kGatherDefault.B &&
+                    g->threads == kGatherDefault.T;
+  auto kern = dflt ? bvs_gather_kernel<XT, YT, false, kGatherDefault.W, kGatherDefault.B, kGatherDefault.T>
+                   : bvs_gather_kernel<XT, YT>;
   const unsigned bit = sizeof(XT) == 8 ? 1u : 2u;  // the attribute call is not free: once per handle and type
   if (!(g->gather_attr & bit)) {
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
@@ -478,6 +481,7 @@ void launch_gather(cmvg_graph* g, const XT* x, YT* y, cudaStream_t st, const XT*
   BvdDev d = g->sdev();
   d.blocks += b0;  // blocks [b0, b1) of this shard
   d.block_begin += b0;
+  d.nlaunch = b1 - b0;
   kern<<<b1 - b0, g->threads, L.total, st>>>(d, x, xfar ? xfar : x, y, PrArgs{});
   CUDA_TRY(cudaGetLastError());
 }

@@ -18,7 +18,7 @@ struct BvdDev {
   uint32_t block_begin;       // first block of this shard
   uint32_t row_begin;         // first row of this shard
   uint32_t stream_cap_words;  // blocks with more words decode from global memory
-  uint32_t pad;
+  uint32_t nlaunch;           // blocks of this launch (`blocks` is offset to its first); persistent kernels
 };
 
 __host__ __device__ inline uint32_t align16(uint32_t v) { return (v + 15u) & ~15u; }
@@ -166,8 +166,9 @@ struct PageRankEpi {
 // Writes y (YT) with coalesced stores.  Uses c.ptr as the pointer array.
 template <typename YT, class EPI = PlainEpi>
 __device__ __forceinline__ void chain_and_store(double* s_yhi, float* s_ylo, const ChainCtx& c, YT* __restrict__ yb,
-                                                EPI epi = EPI(), uint32_t max_depth = 0xffffffffu) {
-  const uint32_t T = blockDim.x, tid = threadIdx.x;
+                                                EPI epi = EPI(), uint32_t max_depth = 0xffffffffu,
+                                                uint32_t T = blockDim.x) {
+  const uint32_t tid = threadIdx.x;
   if (max_depth <= 3) {
     // Bounded chains (R <= 3): each row walks its <= 3 ancestors,
     // y_i = d_i + d_p1 + d_p2 + d_p3 accumulated with TwoSum (error terms

@@ -51,19 +51,19 @@ struct BvsSmem {
   uint32_t off_x, off_yhi, off_ylo, off_ptr, off_ref, off_tab, off_misc, total;
 };
 
-__host__ __device__ inline BvsSmem bvs_smem_layout(const BvdDims& d, uint32_t xsize) {
+__host__ __device__ inline BvsSmem bvs_smem_layout(uint32_t W, uint32_t B, uint32_t xsize) {
   BvsSmem s;
   uint32_t o = 0;
   s.off_x = o;
-  o = align16(o + xw_bytes(d.window, xsize));
+  o = align16(o + xw_bytes(W, xsize));
   s.off_yhi = o;
-  o = align16(o + d.block_rows * 8);
+  o = align16(o + B * 8);
   s.off_ylo = o;
-  o = align16(o + d.block_rows * 4);
+  o = align16(o + B * 4);
   s.off_ptr = o;  // chain pointers (unbounded chains only)
-  o = align16(o + d.block_rows * 2);
+  o = align16(o + B * 2);
   s.off_ref = o;
-  o = align16(o + d.block_rows);
+  o = align16(o + B);
   s.off_tab = o;
   o = align16(o + kBvsSliceTab * 8);
   s.off_misc = o;  // mbarrier (16) + 16 ints + scratch (64 ints)
@@ -71,6 +71,19 @@ __host__ __device__ inline BvsSmem bvs_smem_layout(const BvdDims& d, uint32_t xs
   s.total = o;
   return s;
 }
+__host__ __device__ inline BvsSmem bvs_smem_layout(const BvdDims& d, uint32_t xsize) {
+  return bvs_smem_layout(d.window, d.block_rows, xsize);
+}
+
+// Compile-time shape of the specialised gather kernels (x-window W, block
+// rows B, threads T); 0 = read at run time.  The default options
+// (W = 1536, B = 1024, T = 256) get the specialised kernel: its shared-memory
+// layout, chunking and loop bounds are constants (no address arithmetic
+// rematerialised under the 64-register cap).
+struct GatherShape {
+  uint32_t W, B, T;
+};
+constexpr GatherShape kGatherDefault{1536, 1024, 256};
 
 __device__ __forceinline__ uint32_t ticket_issue(int* counter) {
   return (threadIdx.x & 31u) == 0 ? (uint32_t)atomicAdd(counter, 1) : 0u;
@@ -181,7 +194,8 @@ __device__ __forceinline__ void bvs_slice_epilogue(uint32_t lane, uint32_t meta,
 // segmented warp reduction.  `bs` is the block's stream in global memory.
 template <class XW>
 __device__ __forceinline__ void bvs_slices(const uint32_t* __restrict__ bs, const XW& xw, uint32_t lmin, int* misc,
-                                           double* s_yhi, float* s_ylo, uint8_t* s_ref, const uint32_t* s_tab) {
+                                           double* s_yhi, float* s_ylo, uint8_t* s_ref, const uint32_t* s_tab,
+                                           uint32_t T) {
   constexpr bool kExact = sizeof(typename XW::value_type) == 8;  // compensated point sums for fp64 x
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t nsl = __ldg(bs) & 0xffffu;
@@ -191,7 +205,7 @@ __device__ __forceinline__ void bvs_slices(const uint32_t* __restrict__ bs, cons
   // static schedule: with kBvsWarps warps each takes the contiguous table
   // range the transcoder's LPT assignment gave it (header words 4..8), else
   // round-robin; no ticket round trip sits in front of a slice's loads
-  const uint32_t nwarp = blockDim.x >> 5, warp = threadIdx.x >> 5;
+  const uint32_t nwarp = T >> 5, warp = threadIdx.x >> 5;
   uint32_t s = warp, s_end = nsl, step = nwarp;
   if (nwarp == kBvsWarps) {
     const uint16_t* starts = reinterpret_cast<const uint16_t*>(bs + kBvsWarpTab);
@@ -325,17 +339,18 @@ __device__ __forceinline__ void bvs_slices(const uint32_t* __restrict__ bs, cons
   if (have_prev) bvs_slice_epilogue(lane, prev_meta, prev_h, prev_hi, prev_lo, s_yhi, s_ylo, s_ref);
 }
 
-template <typename XT, typename YT, bool PR = false>
+template <typename XT, typename YT, bool PR = false, uint32_t CW = 0, uint32_t CB = 0, uint32_t CT = 0>
 __global__ void __launch_bounds__(256, 4) bvs_gather_kernel(BvdDev g, const XT* __restrict__ x, const XT* xfar,
                                                              YT* __restrict__ y, PrArgs pr) {
   extern __shared__ __align__(16) unsigned char smem[];
   const BvdDims& D = g.d;
-  const BvsSmem L = bvs_smem_layout(D, sizeof(XT));
+  const uint32_t W = CW ? CW : D.window, B = CB ? CB : D.block_rows, T = CT ? CT : blockDim.x;
+  const BvsSmem L = bvs_smem_layout(W, B, sizeof(XT));
   const uint32_t bl = blockIdx.x;  // index into this shard's tables
   const uint32_t b = g.block_begin + bl;
   const BvdBlockInfo bi = g.blocks[bl];
-  const uint32_t r0 = b * D.block_rows;
-  const uint32_t nr = min(D.block_rows, D.n - r0);
+  const uint32_t r0 = b * B;
+  const uint32_t nr = min(B, D.n - r0);
 
   int* misc = reinterpret_cast<int*>(smem + L.off_misc + 16);
   const uint32_t* bs = g.words + bi.word_offset;  // this block's stream (global; read through L1/L2)
@@ -347,10 +362,10 @@ __global__ void __launch_bounds__(256, 4) bvs_gather_kernel(BvdDev g, const XT* 
   {
     const uint32_t nsl = __ldg(bs) & 0xffffu;
     if (nsl <= kBvsSliceTab)
-      for (uint32_t i = threadIdx.x; i < 2 * nsl; i += blockDim.x) s_tab[i] = __ldg(bs + kBvsHead + i);
+      for (uint32_t i = threadIdx.x; i < 2 * nsl; i += T) s_tab[i] = __ldg(bs + kBvsHead + i);
   }
   XWin<XT> xw;
-  xw.carve(smem + L.off_x, D.window);
+  xw.carve(smem + L.off_x, W, T);
   xw.x = x;
   xw.xfar = xfar;
   xw.wlo = bi.wlo;
@@ -364,7 +379,7 @@ __global__ void __launch_bounds__(256, 4) bvs_gather_kernel(BvdDev g, const XT* 
   uint8_t* s_ref = smem + L.off_ref;
   const Src<false> src{bs};
   bvs_heavy(src, xw, (int32_t)r0, D.min_interval, misc, s_yhi, s_ylo, s_ref);
-  bvs_slices(bs, xw, D.min_interval, misc, s_yhi, s_ylo, s_ref, s_tab);
+  bvs_slices(bs, xw, D.min_interval, misc, s_yhi, s_ylo, s_ref, s_tab, T);
   __syncthreads();
 
   ChainCtx rc;
@@ -392,10 +407,10 @@ __global__ void __launch_bounds__(256, 4) bvs_gather_kernel(BvdDev g, const XT* 
     epi.p0 = pr.p0 ? pr.p0 + r0 : nullptr;
     epi.push_dst = pr.push_dst;
     epi.grow0 = r0;
-    chain_and_store(s_yhi, s_ylo, rc, yb, epi, D.max_depth);
+    chain_and_store(s_yhi, s_ylo, rc, yb, epi, D.max_depth, T);
   } else {
     PlainEpi epi;
-    chain_and_store(s_yhi, s_ylo, rc, yb, epi, D.max_depth);
+    chain_and_store(s_yhi, s_ylo, rc, yb, epi, D.max_depth, T);
   }
 }
 

@@ -51,9 +51,11 @@ struct XWin {
   const XT* __restrict__ x;
   const XT* xfar;  // x at the columns outside the window (only those are read from it)
   uint32_t wlo, W;
+  uint32_t T;  // threads of the CTA (a power of two; a compile-time constant in the specialised kernels)
 
-  __device__ __forceinline__ void carve(unsigned char* base, uint32_t Wn) {
+  __device__ __forceinline__ void carve(unsigned char* base, uint32_t Wn, uint32_t threads) {
     W = Wn;
+    T = threads;
     const uint32_t padded = xw_pad(Wn) + 1;
     unsigned char* p = base;
     s_x = reinterpret_cast<XT*>(p);
@@ -66,11 +68,11 @@ struct XWin {
   }
 
   // entries per thread per round: ceil(W / T) capped at kPre, rounded up to
-  // even (paired loads); T = blockDim.x is a power of two
+  // even (paired loads); T is a power of two
   static constexpr uint32_t kPre = 8;
   __device__ __forceinline__ uint32_t chunk() const {
-    const uint32_t lg = (uint32_t)__ffs((int)blockDim.x) - 1u;
-    const uint32_t e = min(kPre, (W + blockDim.x - 1u) >> lg);
+    const uint32_t lg = (uint32_t)__ffs((int)T) - 1u;
+    const uint32_t e = min(kPre, (W + T - 1u) >> lg);
     return (e + 1u) & ~1u;
   }
 
@@ -110,7 +112,7 @@ struct XWin {
     stage(n, r);
   }
   __device__ __forceinline__ void stage(uint32_t n, const XT (&r0)[kPre]) {
-    const uint32_t T = blockDim.x, tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t E = chunk(), per_round = T * E;
     double ch = 0.0, cl = 0.0;  // carry: the window total before this round (double-double)
     XT r[kPre];

@@ -184,6 +184,7 @@ struct cmvg_graph {
     d.block_begin = block_begin;
     d.row_begin = row_begin;
     d.stream_cap_words = stream_cap_words;
+    d.nlaunch = nblocks;
     return d;
   }
   BvdDev tdev() const {

@@ -60,7 +60,10 @@ __global__ void pr_reduce_kernel(const double* __restrict__ partial, uint32_t nb
 
 void launch_pr_step(cmvg_graph* g, const double* q, PrArgs pr, double* p_next, cudaStream_t st) {
   const BvsSmem L = bvs_smem_layout(g->dims, sizeof(double));
-  auto kern = bvs_gather_kernel<double, double, true>;
+  const bool dflt = g->dims.window == kGatherDefault.W && g->dims.block_rows == kGatherDefault.B &&
+                    g->threads == kGatherDefault.T;
+  auto kern = dflt ? bvs_gather_kernel<double, double, true, kGatherDefault.W, kGatherDefault.B, kGatherDefault.T>
+                   : bvs_gather_kernel<double, double, true>;
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
   kern<<<g->nblocks, g->threads, L.total, st>>>(g->sdev(), q, q, p_next, pr);
   CUDA_TRY(cudaGetLastError());
