@@ -482,6 +482,7 @@ void launch_gather(cmvg_graph* g, const XT* x, YT* y, cudaStream_t st, const XT*
   d.blocks += b0;  // blocks [b0, b1) of this shard
   d.block_begin += b0;
   d.nlaunch = b1 - b0;
+  d.ahead = resident_ctas(kern, (int)g->threads, L.total, g->device, g->gather_res[sizeof(XT) == 8 ? 0 : 1]);
   kern<<<b1 - b0, g->threads, L.total, st>>>(d, x, xfar ? xfar : x, y, PrArgs{});
   CUDA_TRY(cudaGetLastError());
 }

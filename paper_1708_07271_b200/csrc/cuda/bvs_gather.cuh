@@ -48,7 +48,7 @@ constexpr uint32_t kBvsGuardWords = 64;  // zero words after the last block (lan
 constexpr uint32_t kBvsSliceTab = 128;  // slice-table entries staged in shared memory
 
 struct BvsSmem {
-  uint32_t off_x, off_yhi, off_ylo, off_ptr, off_ref, off_tab, off_misc, total;
+  uint32_t off_x, off_yhi, off_ylo, off_ptr, off_ref, off_tab, off_pref, off_misc, total;
 };
 
 __host__ __device__ inline BvsSmem bvs_smem_layout(uint32_t W, uint32_t B, uint32_t xsize) {
@@ -66,6 +66,8 @@ __host__ __device__ inline BvsSmem bvs_smem_layout(uint32_t W, uint32_t B, uint3
   o = align16(o + B);
   s.off_tab = o;
   o = align16(o + kBvsSliceTab * 8);
+  s.off_pref = o;  // block-table entry of the block `ahead` blocks on (L2 prefetch)
+  o = align16(o + 16);
   s.off_misc = o;  // mbarrier (16) + 16 ints + scratch (64 ints)
   o = align16(o + 16 + 64 + 64 * 4);
   s.total = o;
@@ -357,7 +359,17 @@ __global__ void __launch_bounds__(256, 4) bvs_gather_kernel(BvdDev g, const XT* 
   if (threadIdx.x == 0) {
     misc[kBvsHeavyCtr] = 0;
   }
-  if (threadIdx.x == 32) bulk_prefetch_l2(bs, bi.nwords * 4u);
+  // L2 prefetch a launch-wide wave ahead: this CTA fetches (cp.async, no
+  // register or stall) the table entry of block bl + ahead -- about the block
+  // whose CTA takes this slot when this one retires -- and after its decode
+  // issues bulk L2 prefetches of that block's stream and x-window, so the
+  // later CTA's dependent setup loads hit L2.
+  BvdBlockInfo* s_pref = reinterpret_cast<BvdBlockInfo*>(smem + L.off_pref);
+  const bool ahead = g.ahead && bl + g.ahead < g.nlaunch;
+  if (threadIdx.x == 32) {
+    bulk_prefetch_l2(bs, bi.nwords * 4u);
+    if (ahead) cp_async<16>(s_pref, g.blocks + bl + g.ahead);
+  }
   uint32_t* s_tab = reinterpret_cast<uint32_t*>(smem + L.off_tab);
   {
     const uint32_t nsl = __ldg(bs) & 0xffffu;
@@ -381,6 +393,15 @@ __global__ void __launch_bounds__(256, 4) bvs_gather_kernel(BvdDev g, const XT* 
   bvs_heavy(src, xw, (int32_t)r0, D.min_interval, misc, s_yhi, s_ylo, s_ref);
   bvs_slices(bs, xw, D.min_interval, misc, s_yhi, s_ylo, s_ref, s_tab, T);
   __syncthreads();
+  if (threadIdx.x == 32 && ahead) {
+    cp_async_wait_all();
+    const uint64_t wo = s_pref->word_offset;
+    const uint32_t nw = s_pref->nwords, wl = s_pref->wlo;
+    bulk_prefetch_l2(g.words + wo, nw * 4u);
+    const uint32_t xe = min(wl + W, D.n);
+    const uint32_t xb = ((xe > wl ? xe - wl : 0u) * (uint32_t)sizeof(XT)) & ~15u;
+    if (xb && (reinterpret_cast<uintptr_t>(x) & 15u) == 0) bulk_prefetch_l2(x + wl, xb);
+  }
 
   ChainCtx rc;
   rc.ref = s_ref;

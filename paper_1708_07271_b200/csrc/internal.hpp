@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -160,6 +161,7 @@ struct cmvg_graph {
   cudaStream_t s_in = nullptr, s_comp = nullptr, s_out = nullptr;
   cudaEvent_t ev[32] = {};
   std::atomic<unsigned> gather_attr{0};  // kernel attributes set (bit per x type)
+  std::atomic<uint32_t> gather_res[3] = {};  // resident CTAs of the gather variants (f64, f32, PageRank)
   cmvg_graph() = default;
   cmvg_graph(const cmvg_graph&) = delete;
   cmvg_graph& operator=(const cmvg_graph&) = delete;
@@ -205,6 +207,23 @@ struct cmvg_graph {
 
 
 namespace cmvg {
+// Resident CTAs of a kernel on the device (occupancy x SMs): the gather's L2
+// prefetch distance.  Computed once per handle (after the dynamic
+// shared-memory attribute is set); CMVG_PREFETCH_AHEAD overrides (0 = off).
+template <class K>
+inline uint32_t resident_ctas(K kern, int threads, size_t smem, int device, std::atomic<uint32_t>& cache) {
+  uint32_t c = cache.load();
+  if (!c) {
+    int occ = 0, sms = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem) != cudaSuccess) occ = 1;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) sms = 1;
+    c = (uint32_t)(occ > 0 ? occ : 1) * (uint32_t)(sms > 0 ? sms : 1);
+    if (const char* e = std::getenv("CMVG_PREFETCH_AHEAD")) c = (uint32_t)std::strtoul(e, nullptr, 10) | 0x80000000u;
+    cache.store(c | 0x80000000u);
+  }
+  return c & 0x7fffffffu;
+}
+
 // kernel entry points implemented in the other translation units
 template <typename T>
 void launch_scatter(cmvg_graph* g, const T* x, T* y, cudaStream_t st);

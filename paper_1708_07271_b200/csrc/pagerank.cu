@@ -65,7 +65,9 @@ void launch_pr_step(cmvg_graph* g, const double* q, PrArgs pr, double* p_next, c
   auto kern = dflt ? bvs_gather_kernel<double, double, true, kGatherDefault.W, kGatherDefault.B, kGatherDefault.T>
                    : bvs_gather_kernel<double, double, true>;
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
-  kern<<<g->nblocks, g->threads, L.total, st>>>(g->sdev(), q, q, p_next, pr);
+  BvdDev d = g->sdev();
+  d.ahead = resident_ctas(kern, (int)g->threads, L.total, g->device, g->gather_res[2]);
+  kern<<<g->nblocks, g->threads, L.total, st>>>(d, q, q, p_next, pr);
   CUDA_TRY(cudaGetLastError());
 }
 
