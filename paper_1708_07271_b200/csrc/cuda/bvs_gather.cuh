@@ -236,9 +236,21 @@ __device__ __forceinline__ void bvs_slices(const uint32_t* __restrict__ bs, cons
       // near class 16 (rectangular): no per-lane counts -- pad codes read the
       // window's zero entry, empty intervals have length 0
       const uint32_t mnpw = (mnp + 1u) >> 1;
+      // exactly mnpw point words (warp-uniform): a jump into the unrolled
+      // loads instead of eight predicated ones; words past mnpw are never read
       uint32_t w[kBvsUnitPts / 2];
-#pragma unroll
-      for (uint32_t q = 0; q < kBvsUnitPts / 2; ++q) w[q] = q < mnpw ? __ldg(body + q * 32u) : 0u;
+      static_assert(kBvsUnitPts / 2 == 8, "unrolled loads");
+      switch (mnpw) {
+        default: w[7] = __ldg(body + 7u * 32u); [[fallthrough]];
+        case 7: w[6] = __ldg(body + 6u * 32u); [[fallthrough]];
+        case 6: w[5] = __ldg(body + 5u * 32u); [[fallthrough]];
+        case 5: w[4] = __ldg(body + 4u * 32u); [[fallthrough]];
+        case 4: w[3] = __ldg(body + 3u * 32u); [[fallthrough]];
+        case 3: w[2] = __ldg(body + 2u * 32u); [[fallthrough]];
+        case 2: w[1] = __ldg(body + 1u * 32u); [[fallthrough]];
+        case 1: w[0] = __ldg(body); [[fallthrough]];
+        case 0: break;
+      }
       const uint32_t wi0 = mni > 0 ? __ldg(body + mnpw * 32u) : 0u;
       const uint32_t wi1 = mni > 1 ? __ldg(body + (mnpw + 1u) * 32u) : 0u;
       if (have_prev) {  // the previous slice's epilogue while these loads are in flight
