@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--no-csr", action="store_true", help="skip the uncompressed GPU CSR comparison")
     ap.add_argument("--secondary", action="store_true", help="also time the f32 / scatter variants (stderr)")
     ap.add_argument("--cpu-sample-seconds", type=float, default=20.0)
     return ap.parse_args()
@@ -317,6 +318,41 @@ def run_ours(args):
             nz = want != 0
             parity = float(np.max(np.abs(got[nz] - want[nz]) / np.abs(want[nz])))
 
+    # uncompressed comparison point at equal hardware: the reference's
+    # matvec_csr as a hand-written CSR kernel on the same GPU (PAPER.md:217's
+    # S = t/t'), same x, same L2 flush; rank 0, outside the timed region
+    csr_base = None
+    if rank == 0 and args.form == "gather" and args.dtype == "f64" and not args.no_csr:
+        ro = torch.from_numpy(g.row_offsets.astype(np.int64)).to(dev)
+        co = torch.from_numpy(g.columns.view(np.int32)).to(dev)
+        yc = torch.empty_like(x)
+        for _ in range(args.warmup):
+            flush.zero_()
+            P.csr_matvec_device(ro, co, x, yc, stream=stream.cuda_stream)
+        cevs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        for a, b in cevs:
+            flush.zero_()
+            a.record(stream)
+            P.csr_matvec_device(ro, co, x, yc, stream=stream.cuda_stream)
+            b.record(stream)
+        torch.cuda.synchronize(dev)
+        tc = float(np.mean([a.elapsed_time(b) for a, b in cevs]))
+        csr_bytes = 4 * g.m + 8 * (g.n + 1) + 16 * g.n
+        pk, _ = measured_peak()
+        csr_base = {"ms": tc, "gedges_s": g.m / (tc * 1e-3) / 1e9, "bv_speedup": tc / float(times.mean()),
+                    "bytes_per_launch": csr_bytes, "gbs": csr_bytes / (tc * 1e-3) / 1e9,
+                    "roofline_ms": csr_bytes / (pk * 1e9) * 1e3,
+                    "bv_speedup_vs_csr_roofline": csr_bytes / (pk * 1e9) / (float(times.mean()) * 1e-3),
+                    "what": "hand-written GPU CSR product (u64 row offsets, u32 columns, fp64; matvec_csr, "
+                            "csr.hpp:48-55) on the same B200: bv_speedup = t_csr / t_compressed, the paper's "
+                            "S = t/t' (PAPER.md:217) at equal hardware; roofline_ms = the CSR bytes at peak HBM "
+                            "bandwidth (an ideal CSR kernel), bv_speedup_vs_csr_roofline = roofline_ms / t_compressed"}
+        if parity is not None:
+            wc = yc.cpu().numpy()
+            nz = want != 0
+            csr_base["parity_max_rel_err"] = float(np.max(np.abs(wc[nz] - want[nz]) / np.abs(want[nz])))
+        del ro, co, yc
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         x64 = np.ascontiguousarray(xh, dtype=np.float64)
@@ -353,6 +389,7 @@ def run_ours(args):
             "gpu_launches": args.steps,
             "clocks": clocks,
             "parity_max_rel_err_vs_matvec_csr": parity,
+            "csr_baseline": csr_base,
             "kernel_ms": {"mean": float(times.mean()), "median": float(np.median(times)),
                           "min": float(times.min()), "max": float(times.max())},
         }

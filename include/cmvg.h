@@ -189,6 +189,14 @@ int cmvg_matmat_f32(cmvg_graph* g, const float* X, float* Y, uint32_t k, int ptr
 /* Decoded adjacency of the whole graph: row_offsets[n+1], cols[m]. */
 int cmvg_decode_csr(cmvg_graph* g, uint64_t* row_offsets, uint32_t* cols, int ptr_kind, void* stream);
 
+/* Uncompressed comparison point (replaces cmv::matvec_csr, csr.hpp:48-55, on
+ * the GPU): y = A x^T from the reference's CsrGraph arrays (row_offsets[n+1]
+ * u64, cols[m] u32), fp64, DEVICE pointers on the current device.  Used to
+ * report the compressed product against plain CSR at equal hardware (the
+ * paper's S = t/t' column). */
+int cmvg_csr_matvec_f64(uint32_t n, uint64_t m, const uint64_t* row_offsets, const uint32_t* cols, const double* x,
+                        double* y, void* stream);
+
 /* PageRank (pagerank.hpp:83-102) on a handle holding A^T (the whole graph):
  * p_t = alpha/n + (1-alpha) (A^T q + [uniform] D/n), q = p/d.  degrees are
  * the out-degrees of A.  ranks receives n doubles. */

@@ -146,6 +146,7 @@ _SIGS = [
                                    C.POINTER(C.c_uint32), C.c_int, _P]),
     ("cmvg_pagerank_step_push", C.c_int, [_P, _P, _P, C.c_double, C.c_double, C.c_int, _P, _P, _P, _P, _P, _P, _P]),
     ("cmvg_pagerank_step", C.c_int, [_P, _P, _P, C.c_double, C.c_double, C.c_int, _P, _P, _P, _P, _P]),
+    ("cmvg_csr_matvec_f64", C.c_int, [C.c_uint32, C.c_uint64, _P, _P, _P, _P, _P]),
 ]
 
 EXPORTED_SYMBOLS = [s[0] for s in _SIGS]
@@ -391,6 +392,28 @@ def _stream_of(*ts) -> Optional[int]:
             import torch
             return torch.cuda.current_stream(t.device).cuda_stream
     return None
+
+
+def csr_matvec_device(row_offsets, cols, x, y=None, stream: Optional[int] = None):
+    """Uncompressed y = A x^T on the GPU (the reference's matvec_csr,
+    csr.hpp:48-55) from CUDA tensors: row_offsets int64[n+1], cols int32[m],
+    x float64[n].  The comparison point for the compressed product at equal
+    hardware (PAPER.md:217)."""
+    import torch
+    for t in (row_offsets, cols, x):
+        if not (_is_torch(t) and t.is_cuda and t.is_contiguous()):
+            raise ValueError("csr_matvec_device takes contiguous CUDA tensors")
+    if row_offsets.dtype != torch.int64 or cols.dtype != torch.int32 or x.dtype != torch.float64:
+        raise TypeError("expected int64 row offsets, int32 columns, float64 x")
+    n = row_offsets.numel() - 1
+    if x.numel() != n:
+        raise ValueError(f"x has {x.numel()} entries, the matrix {n} columns")
+    if y is None:
+        y = torch.empty(n, dtype=torch.float64, device=x.device)
+    st = stream if stream is not None else _stream_of(x)
+    _check(load_library().cmvg_csr_matvec_f64(n, cols.numel(), row_offsets.data_ptr(), cols.data_ptr(),
+                                              x.data_ptr(), y.data_ptr(), st))
+    return y
 
 
 class BvGraph:

@@ -219,3 +219,19 @@ def test_gather_host_pinned_pipelined_shard(cuda):
     yp = torch.empty(b - a, dtype=torch.float64).pin_memory()
     dg.matvec(xp.numpy(), yp.numpy())
     assert max_rel_err(yp.numpy(), want) <= F64_TOL
+
+
+@pytest.mark.parametrize("deg", [3.0, 12.0, 40.0, 150.0])
+def test_csr_baseline_matches_oracle(cuda, deg):
+    """The uncompressed comparison kernel (matvec_csr on the GPU, csr.hpp:48-55)
+    against the oracle, for every sub-warp width it picks by mean degree."""
+    import torch
+
+    g = P.CsrGraph.copy_model(1 << 14, deg, seed=5)
+    x = x_uniform(g.n, 3)
+    want = oracle_csr(g).matvec(x, 8)
+    ro = torch.from_numpy(g.row_offsets.astype(np.int64)).cuda()
+    co = torch.from_numpy(g.columns.view(np.int32)).cuda()
+    y = P.csr_matvec_device(ro, co, torch.from_numpy(x).cuda()).cpu().numpy()
+    assert max_rel_err(y, want) <= F64_TOL
+    assert np.all(y[want == 0] == 0)
