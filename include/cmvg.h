@@ -139,6 +139,20 @@ void cmvg_csr_free(cmvg_csr* g);
 
 /* ---- canonical BV stream (host) ------------------------------------------ */
 int cmvg_bv_encode(const cmvg_csr* g, const cmvg_bv_params* p, cmvg_bvstream** out);
+/* CBV1 container: the BV stream on disk (modelled on the reference's RMV1,
+ * rmv_io.hpp:31-49: save_rmv / load_rmv / encode_rmv / decode_rmv).  Load
+ * validates everything and returns CMVG_ERR_FORMAT for an unrecognised
+ * container (bad magic or version, cmv::FormatError) and CMVG_ERR_CORRUPT for
+ * inconsistent contents (truncation, trailing bytes, checksum, invariants, a
+ * stream that does not decode to m edges; cmv::CorruptionError).  Equal
+ * streams give identical bytes.  cmvg_bv_serialize sets *size and fills buf
+ * when cap >= *size. */
+int cmvg_bv_save(const cmvg_bvstream* s, const char* path);
+int cmvg_bv_load(const char* path, cmvg_bvstream** out);
+int cmvg_bv_serialize(const cmvg_bvstream* s, uint8_t* buf, uint64_t cap, uint64_t* size);
+/* n, m and the encoding parameters of a stream (e.g. one just loaded). */
+int cmvg_bv_describe(const cmvg_bvstream* s, uint32_t* n, uint64_t* m, cmvg_bv_params* p);
+int cmvg_bv_deserialize(const uint8_t* buf, uint64_t size, cmvg_bvstream** out);
 int cmvg_bv_from_words(uint32_t n, uint64_t m, const cmvg_bv_params* p, const uint32_t* words, uint64_t nbits,
                        const uint64_t* segment_bit_offsets, cmvg_bvstream** out);
 int cmvg_bv_decode_host(const cmvg_bvstream* s, cmvg_csr** out);

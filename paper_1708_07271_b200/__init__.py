@@ -147,6 +147,11 @@ _SIGS = [
     ("cmvg_pagerank_step_push", C.c_int, [_P, _P, _P, C.c_double, C.c_double, C.c_int, _P, _P, _P, _P, _P, _P, _P]),
     ("cmvg_pagerank_step", C.c_int, [_P, _P, _P, C.c_double, C.c_double, C.c_int, _P, _P, _P, _P, _P]),
     ("cmvg_csr_matvec_f64", C.c_int, [C.c_uint32, C.c_uint64, _P, _P, _P, _P, _P]),
+    ("cmvg_bv_save", C.c_int, [_P, C.c_char_p]),
+    ("cmvg_bv_load", C.c_int, [C.c_char_p, C.POINTER(_P)]),
+    ("cmvg_bv_serialize", C.c_int, [_P, _P, C.c_uint64, C.POINTER(C.c_uint64)]),
+    ("cmvg_bv_deserialize", C.c_int, [_P, C.c_uint64, C.POINTER(_P)]),
+    ("cmvg_bv_describe", C.c_int, [_P, C.POINTER(C.c_uint32), C.POINTER(C.c_uint64), C.POINTER(_BvParamsC)]),
 ]
 
 EXPORTED_SYMBOLS = [s[0] for s in _SIGS]
@@ -291,6 +296,46 @@ class BvStream:
         _check(load_library().cmvg_bv_from_words(n, m, C.byref(pc), w.ctypes.data if w.size else None, nbits,
                                                  s.ctypes.data, C.byref(out)))
         return cls(out.value, n, m, params)
+
+    # ---- CBV1 container (the reference's RMV1 model: save_rmv / load_rmv /
+    # encode_rmv / decode_rmv, rmv_io.hpp:31-49) ----
+    @classmethod
+    def _adopt(cls, handle: int) -> "BvStream":
+        n, m, pc = C.c_uint32(), C.c_uint64(), _BvParamsC()
+        lib = load_library()
+        rc = lib.cmvg_bv_describe(_P(handle), C.byref(n), C.byref(m), C.byref(pc))
+        if rc:
+            lib.cmvg_bv_free(_P(handle))
+            _check(rc)
+        return cls(handle, n.value, m.value, BvParams(pc.window, pc.max_ref, pc.min_interval, pc.zeta_k,
+                                                      pc.segment_rows))
+
+    def save(self, path: str) -> None:
+        """Write the stream as a CBV1 container (deterministic bytes)."""
+        _check(load_library().cmvg_bv_save(self._h, os.fsencode(path)))
+
+    @classmethod
+    def load(cls, path: str) -> "BvStream":
+        """Read a CBV1 container; FormatError (bad magic / version) or
+        CorruptionError (truncation, trailing bytes, checksum, invariants)."""
+        out = _P()
+        _check(load_library().cmvg_bv_load(os.fsencode(path), C.byref(out)))
+        return cls._adopt(out.value)
+
+    def to_bytes(self) -> bytes:
+        size = C.c_uint64()
+        lib = load_library()
+        _check(lib.cmvg_bv_serialize(self._h, None, 0, C.byref(size)))
+        buf = (C.c_uint8 * size.value)()
+        _check(lib.cmvg_bv_serialize(self._h, buf, size.value, C.byref(size)))
+        return bytes(buf)
+
+    @classmethod
+    def from_bytes(cls, data: bytes) -> "BvStream":
+        out = _P()
+        buf = (C.c_uint8 * len(data)).from_buffer_copy(data) if data else None
+        _check(load_library().cmvg_bv_deserialize(buf, len(data), C.byref(out)))
+        return cls._adopt(out.value)
 
     def stats(self) -> dict:
         st = _BvStatsC()

@@ -124,6 +124,53 @@ int cmvg_bv_from_words(uint32_t n, uint64_t m, const cmvg_bv_params* p, const ui
   });
 }
 
+int cmvg_bv_save(const cmvg_bvstream* s, const char* path) {
+  return guarded([&] {
+    require(s && path, "null argument");
+    save_bv_container(s->s, path);
+  });
+}
+
+int cmvg_bv_load(const char* path, cmvg_bvstream** out) {
+  return guarded([&] {
+    require(path && out, "null argument");
+    auto s = std::make_unique<cmvg_bvstream>();
+    s->s = load_bv_container(path);
+    *out = s.release();
+  });
+}
+
+int cmvg_bv_describe(const cmvg_bvstream* s, uint32_t* n, uint64_t* m, cmvg_bv_params* p) {
+  return guarded([&] {
+    require(s && n && m && p, "null argument");
+    *n = s->s.n;
+    *m = s->s.m;
+    p->window = s->s.params.window;
+    p->max_ref = s->s.params.max_ref;
+    p->min_interval = s->s.params.min_interval;
+    p->zeta_k = s->s.params.zeta_k;
+    p->segment_rows = s->s.params.segment_rows;
+  });
+}
+
+int cmvg_bv_serialize(const cmvg_bvstream* s, uint8_t* buf, uint64_t cap, uint64_t* size) {
+  return guarded([&] {
+    require(s && size, "null argument");
+    const std::vector<uint8_t> b = encode_bv_container(s->s);
+    *size = b.size();
+    if (buf && cap >= b.size()) std::memcpy(buf, b.data(), b.size());
+  });
+}
+
+int cmvg_bv_deserialize(const uint8_t* buf, uint64_t size, cmvg_bvstream** out) {
+  return guarded([&] {
+    require((buf || size == 0) && out, "null argument");
+    auto s = std::make_unique<cmvg_bvstream>();
+    s->s = decode_bv_container(buf, (size_t)size);
+    *out = s.release();
+  });
+}
+
 int cmvg_bv_decode_host(const cmvg_bvstream* s, cmvg_csr** out) {
   return guarded([&] {
     require(s && out, "null argument");

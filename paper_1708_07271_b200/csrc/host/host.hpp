@@ -7,6 +7,7 @@
 #include <exception>
 #include <cstdint>
 #include <functional>
+#include <stdexcept>
 #include <string>
 #include <thread>
 #include <vector>
@@ -136,5 +137,18 @@ HostCsr generate_social(const SocialParams& p);
 BvStream bv_encode(const HostCsr& g, const BvParams& p);
 BvDecoded bv_decode(const BvStream& s);
 HostCsr transpose_csr(const HostCsr& g);
+
+// ---- CBV1 container (bv_io.cpp): the BV stream on disk ----------------------
+// The reference's container error types (rmv_io.hpp:13-22).
+struct FormatError : std::runtime_error {  // unrecognised container: bad magic or version
+  using std::runtime_error::runtime_error;
+};
+struct CorruptionError : std::runtime_error {  // recognised container, inconsistent contents
+  using std::runtime_error::runtime_error;
+};
+std::vector<uint8_t> encode_bv_container(const BvStream& s);
+BvStream decode_bv_container(const uint8_t* p, size_t len);
+void save_bv_container(const BvStream& s, const std::string& path);
+BvStream load_bv_container(const std::string& path);
 
 }  // namespace cmvg

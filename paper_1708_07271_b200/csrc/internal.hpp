@@ -48,6 +48,10 @@ inline int guarded(F&& f) {
     return set_error(CMVG_ERR_INVALID, e.what());
   } catch (const std::out_of_range& e) {
     return set_error(CMVG_ERR_RANGE, e.what());
+  } catch (const FormatError& e) {
+    return set_error(CMVG_ERR_FORMAT, e.what());
+  } catch (const CorruptionError& e) {
+    return set_error(CMVG_ERR_CORRUPT, e.what());
   } catch (const std::bad_alloc&) {
     return set_error(CMVG_ERR_NOMEM, "out of host memory");
   } catch (const std::runtime_error& e) {
