@@ -39,9 +39,8 @@ struct BvtSmem {
   uint32_t off_ch, off_cl, off_oh, off_ol, off_misc, total;
 };
 
-__host__ __device__ inline BvtSmem bvt_smem_layout(const BvdDims& d) {
+__host__ __device__ inline BvtSmem bvt_smem_layout(uint32_t B, uint32_t W) {
   BvtSmem s;
-  const uint32_t B = d.block_rows, W = d.window;
   uint32_t o = 0;
   s.off_ch = o;
   o = align16(o + (B + 1) * 8);
@@ -56,6 +55,7 @@ __host__ __device__ inline BvtSmem bvt_smem_layout(const BvdDims& d) {
   s.total = o;
   return s;
 }
+__host__ __device__ inline BvtSmem bvt_smem_layout(const BvdDims& d) { return bvt_smem_layout(d.block_rows, d.window); }
 
 struct BvtOut {
   double* st_hi;  // staging: [block][W] partial y over the block's window
@@ -75,13 +75,21 @@ __device__ __forceinline__ void bvt_put(uint32_t t, double hi, double lo, uint32
   }
 }
 
-// +(c_hi, c_lo) or -(c_hi, c_lo) of a code k | minus << 15
+// +(c_hi, c_lo) or -(c_hi, c_lo) of a code k | minus << 15; EXACT = false
+// (fp32 x): plain fp64 sums of c_hi (error ~1e-16 x cancellation, far inside
+// the fp32 tolerance)
+template <bool EXACT = true>
 __device__ __forceinline__ void bvt_term(uint32_t code, const double* ch, const float* cl, double& acc, double& comp) {
   const uint32_t k = code & 0x7fffu;
   const int sg = (int)((code << 16) & 0x80000000u);
-  const double h = ch[k], l = (double)cl[k];
-  tsum(acc, comp, __hiloint2double(__double2hiint(h) ^ sg, __double2loint(h)));
-  comp += __hiloint2double(__double2hiint(l) ^ sg, __double2loint(l));
+  const double h = ch[k];
+  if constexpr (EXACT) {
+    const double l = (double)cl[k];
+    tsum(acc, comp, __hiloint2double(__double2hiint(h) ^ sg, __double2loint(h)));
+    comp += __hiloint2double(__double2hiint(l) ^ sg, __double2loint(l));
+  } else {
+    acc += __hiloint2double(__double2hiint(h) ^ sg, __double2loint(h));
+  }
 }
 
 // A slice's epilogue: segmented reduction of a multi slice (its round count
@@ -105,16 +113,19 @@ __device__ __forceinline__ void bvt_slice_epilogue(uint32_t lane, uint32_t meta,
   if ((h >> 30) == 3u) bvt_put(th_target(h), hi, lo, W2, s_oh, s_ol, out, fbase);
 }
 
-template <typename XT>
+// CW, CB, CT: compile-time window, block rows and threads of the specialised
+// kernel (0 = read at run time; see GatherShape)
+template <typename XT, uint32_t CW = 0, uint32_t CB = 0, uint32_t CT = 0>
 __global__ void __launch_bounds__(256, 4) bvt_scatter_kernel(BvdDev g, const XT* __restrict__ x, BvtOut out) {
   extern __shared__ __align__(16) unsigned char smem[];
+  constexpr bool kExact = sizeof(XT) == 8;
   const BvdDims& D = g.d;
-  const BvtSmem L = bvt_smem_layout(D);
-  const uint32_t T = blockDim.x, tid = threadIdx.x, lane = tid & 31u;
+  const uint32_t B = CB ? CB : D.block_rows, W = CW ? CW : D.window, W2 = 2u * W;
+  const BvtSmem L = bvt_smem_layout(B, W);
+  const uint32_t T = CT ? CT : blockDim.x, tid = threadIdx.x, lane = tid & 31u;
   const uint32_t bl = blockIdx.x;
   const uint32_t b = g.block_begin + bl;
   const BvdBlockInfo bi = g.blocks[bl];
-  const uint32_t B = D.block_rows, W = D.window, W2 = 2u * W;
   const uint32_t r0 = b * B;
   const uint32_t nr = min(B, D.n - r0);
   const uint32_t* __restrict__ bs = g.words + bi.word_offset;
@@ -231,8 +242,8 @@ __global__ void __launch_bounds__(256, 4) bvt_scatter_kernel(BvdDev g, const XT*
 #pragma unroll
     for (uint32_t q = 0; q < kBvtUnitCodes / 2; ++q) {
       if (q >= mnw) break;  // warp-uniform
-      bvt_term(w[q] >> 16, ch, cl, acc, comp);
-      bvt_term(w[q] & 0xffffu, ch, cl, acc2, comp2);
+      bvt_term<kExact>(w[q] >> 16, ch, cl, acc, comp);
+      bvt_term<kExact>(w[q] & 0xffffu, ch, cl, acc2, comp2);
     }
     tsum(acc, comp, acc2);
     comp += comp2;

@@ -22,7 +22,9 @@ void launch_scatter(cmvg_graph* g, const T* x, T* y, cudaStream_t st) {
   o.far_hi -= g->tfar_begin;  // indexed by global far slot
   o.far_lo -= g->tfar_begin;
   const BvtSmem L = bvt_smem_layout(g->dims);
-  auto k1 = bvt_scatter_kernel<T>;
+  const bool dflt = g->dims.window == kGatherDefault.W && g->dims.block_rows == kGatherDefault.B &&
+                    g->threads == kGatherDefault.T;
+  auto k1 = dflt ? bvt_scatter_kernel<T, kGatherDefault.W, kGatherDefault.B, kGatherDefault.T> : bvt_scatter_kernel<T>;
   const unsigned bit = sizeof(T) == 8 ? 4u : 8u;  // the attribute call is not free: once per handle and type
   if (!(g->gather_attr & bit)) {
     CUDA_TRY(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
