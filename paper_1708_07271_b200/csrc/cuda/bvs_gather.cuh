@@ -239,18 +239,18 @@ __device__ __forceinline__ void bvs_slices(const uint32_t* __restrict__ bs, cons
       // exactly mnpw point words (warp-uniform): a jump into the unrolled
       // loads instead of eight predicated ones; words past mnpw are never read
       uint32_t w[kBvsUnitPts / 2];
-      static_assert(kBvsUnitPts / 2 == 8, "unrolled loads");
+      static_assert(kBvsUnitPts / 2 <= 16, "unrolled loads");
+#define CMVG_LD(q) \
+  case q + 1:      \
+    if (q < kBvsUnitPts / 2) w[q] = __ldg(body + (q)*32u); /* fall through */
       switch (mnpw) {
-        default: w[7] = __ldg(body + 7u * 32u); [[fallthrough]];
-        case 7: w[6] = __ldg(body + 6u * 32u); [[fallthrough]];
-        case 6: w[5] = __ldg(body + 5u * 32u); [[fallthrough]];
-        case 5: w[4] = __ldg(body + 4u * 32u); [[fallthrough]];
-        case 4: w[3] = __ldg(body + 3u * 32u); [[fallthrough]];
-        case 3: w[2] = __ldg(body + 2u * 32u); [[fallthrough]];
-        case 2: w[1] = __ldg(body + 1u * 32u); [[fallthrough]];
-        case 1: w[0] = __ldg(body); [[fallthrough]];
-        case 0: break;
+        default:
+          CMVG_LD(15) CMVG_LD(14) CMVG_LD(13) CMVG_LD(12) CMVG_LD(11) CMVG_LD(10) CMVG_LD(9) CMVG_LD(8) CMVG_LD(7)
+          CMVG_LD(6) CMVG_LD(5) CMVG_LD(4) CMVG_LD(3) CMVG_LD(2) CMVG_LD(1) CMVG_LD(0)
+        case 0:
+          break;
       }
+#undef CMVG_LD
       const uint32_t wi0 = mni > 0 ? __ldg(body + mnpw * 32u) : 0u;
       const uint32_t wi1 = mni > 1 ? __ldg(body + (mnpw + 1u) * 32u) : 0u;
       if (have_prev) {  // the previous slice's epilogue while these loads are in flight

@@ -106,7 +106,10 @@ __host__ __device__ constexpr uint32_t make_hdr(uint32_t r, uint32_t nm, uint32_
 //   heavy table: kBvsHeavyEntry words per heavy row: BV-D-style a-word
 //     (make_sa), #minus, #residual, #interval, bit offset in the heavy stream, 0
 //   heavy stream: the heavy rows' BV-D bodies, bit-packed, MSB first
-constexpr uint32_t kBvsUnitPts = 16;
+#ifndef CMVG_UNIT_PTS  // build-time override for A/B experiments (<= 31: the 5-bit count fields)
+#define CMVG_UNIT_PTS 16
+#endif
+constexpr uint32_t kBvsUnitPts = CMVG_UNIT_PTS;
 constexpr uint32_t kBvsUnitInts = 2;
 constexpr uint32_t kBvsMaxUnits = 32;  // more -> heavy row
 constexpr uint32_t kBvsHeavyEntry = 6;
