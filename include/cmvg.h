@@ -211,6 +211,39 @@ int cmvg_decode_csr(cmvg_graph* g, uint64_t* row_offsets, uint32_t* cols, int pt
 int cmvg_csr_matvec_f64(uint32_t n, uint64_t m, const uint64_t* row_offsets, const uint32_t* cols, const double* x,
                         double* y, void* stream);
 
+/* Biclique covers (reference include/cmv/biclique.hpp): an
+ * edge-disjoint decomposition of A's edges into bicliques (S_r, C_r) plus
+ * residual edges, and its product on the GPU.
+ *   cmvg_bicover_extract     replaces cmv::extract_greedy (biclique.hpp:58-61);
+ *                            per_round = 1 emits the best candidate per round
+ *                            (the reference's rule), 0 every still-valid one.
+ *   cmvg_bicover_verify      replaces cmv::verify_cover (biclique.hpp:63-64).
+ *   cmvg_bicover_save/load   replace cmv::save_cover / load_cover (BCV1 text,
+ *                            biclique.hpp:66-73); load returns CMVG_ERR_FORMAT
+ *                            for a wrong header, CMVG_ERR_CORRUPT otherwise.
+ *   cmvg_bicover_matvec_f64  replaces cmv::matvec_biclique_into
+ *                            (biclique.hpp:39-46): y = A x (n entries each).
+ *   cmvg_bicover_sizes       compressed_size = sum |S_r|+|C_r| + |residual|
+ *                            (biclique.hpp:33-34) = the product's adds.
+ * Arrays: sources / targets of biclique r at [off[r], off[r+1]), residual as
+ * (u, v) pairs; ids strictly ascending per side, residual sorted.  The device
+ * operands are built on the first product, on the current device. */
+typedef struct cmvg_bicover cmvg_bicover;
+int cmvg_bicover_extract(const cmvg_csr* g, uint64_t min_gain, uint64_t max_rounds, uint32_t per_round,
+                         cmvg_bicover** out);
+int cmvg_bicover_from_arrays(uint32_t n, uint64_t nb, const uint64_t* src_off, const uint32_t* src,
+                             const uint64_t* tgt_off, const uint32_t* tgt, uint64_t nres, const uint32_t* res_uv,
+                             cmvg_bicover** out);
+int cmvg_bicover_sizes(const cmvg_bicover* h, uint32_t* n, uint64_t* nb, uint64_t* nsrc, uint64_t* ntgt,
+                       uint64_t* nres, uint64_t* compressed_size);
+int cmvg_bicover_export(const cmvg_bicover* h, uint64_t* src_off, uint32_t* src, uint64_t* tgt_off, uint32_t* tgt,
+                        uint32_t* res_uv);
+int cmvg_bicover_verify(const cmvg_bicover* h, const cmvg_csr* g, int* ok);
+int cmvg_bicover_save(const cmvg_bicover* h, const char* path);
+int cmvg_bicover_load(const char* path, cmvg_bicover** out);
+int cmvg_bicover_matvec_f64(cmvg_bicover* h, const double* x, double* y, int ptr_kind, void* stream);
+void cmvg_bicover_free(cmvg_bicover* h);
+
 /* PageRank (pagerank.hpp:83-102) on a handle holding A^T (the whole graph):
  * p_t = alpha/n + (1-alpha) (A^T q + [uniform] D/n), q = p/d.  degrees are
  * the out-degrees of A.  ranks receives n doubles. */

@@ -262,3 +262,47 @@ def pagerank_ref(rm: RefMatrix, degrees, alpha=0.15, iterations=10, l1_tolerance
                                    0 if dangling == "uniform" else 1, None if st is None else _ptr(st), _ptr(out),
                                    C.byref(it)))
     return out, it.value
+
+
+# ---- biclique covers (reference include/cmv/biclique.hpp) ----
+# Test infrastructure: sequential restatements used only as the checker.
+
+def matvec_biclique(n, bicliques, residual, x):
+    """cmv::matvec_biclique_into (biclique.hpp:39-46, SPEC.md:310-318): y = 0;
+    per biclique r, c_r = sum of x over C_r (in order), added to y[i] for
+    every i in S_r; per residual edge (i, j), y[i] += x[j].  Returns
+    (y, c, adds) with adds = compressed_size = sum |S_r| + |C_r| + |residual|."""
+    x = np.asarray(x, dtype=np.float64)
+    if len(x) != n:
+        raise ValueError("matvec_biclique: dimension mismatch")
+    y = np.zeros(n)
+    cs = []
+    adds = 0
+    for sources, targets in bicliques:
+        c = 0.0
+        for j in targets:
+            c += x[j]
+        cs.append(c)
+        for i in sources:
+            y[i] += c
+        adds += len(sources) + len(targets)
+    for i, j in residual:
+        y[i] += x[j]
+        adds += 1
+    return y, cs, adds
+
+
+def verify_cover(n, bicliques, residual, rows):
+    """cmv::verify_cover (biclique.hpp:63-64, SPEC.md:330-338): materialise the
+    cover's edge multiset and compare it with the graph's (duplicates across
+    parts make it differ)."""
+    if len(rows) != n:
+        return False
+    got = []
+    for sources, targets in bicliques:
+        if len(sources) == 0 or len(targets) == 0:
+            return False
+        got.extend((int(i), int(j)) for i in sources for j in targets)
+    got.extend((int(i), int(j)) for i, j in residual)
+    want = [(u, int(v)) for u in range(n) for v in rows[u]]
+    return sorted(got) == sorted(want)

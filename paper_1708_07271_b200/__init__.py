@@ -29,7 +29,7 @@ import numpy as np
 
 __all__ = [
     "CmvgError", "FormatError", "CorruptionError", "UnsupportedError",
-    "CsrGraph", "BvParams", "BvStream", "BvGraph", "CreateOptions",
+    "CsrGraph", "BvParams", "BvStream", "BvGraph", "CreateOptions", "BicliqueCover", "BicliqueKernel",
     "MatvecKernel", "BvGpuKernel", "DanglingPolicy", "PageRankConfig", "PageRankResult",
     "pagerank", "library_path", "load_library", "CompressionStats", "compression_stats", "PageRankEquivalence",
     "pagerank_equivalence_check",
@@ -152,6 +152,15 @@ _SIGS = [
     ("cmvg_bv_serialize", C.c_int, [_P, _P, C.c_uint64, C.POINTER(C.c_uint64)]),
     ("cmvg_bv_deserialize", C.c_int, [_P, C.c_uint64, C.POINTER(_P)]),
     ("cmvg_bv_describe", C.c_int, [_P, C.POINTER(C.c_uint32), C.POINTER(C.c_uint64), C.POINTER(_BvParamsC)]),
+    ("cmvg_bicover_extract", C.c_int, [_P, C.c_uint64, C.c_uint64, C.c_uint32, C.POINTER(_P)]),
+    ("cmvg_bicover_from_arrays", C.c_int, [C.c_uint32, C.c_uint64, _P, _P, _P, _P, C.c_uint64, _P, C.POINTER(_P)]),
+    ("cmvg_bicover_sizes", C.c_int, [_P] + [C.POINTER(C.c_uint32)] + [C.POINTER(C.c_uint64)] * 5),
+    ("cmvg_bicover_export", C.c_int, [_P, _P, _P, _P, _P, _P]),
+    ("cmvg_bicover_verify", C.c_int, [_P, _P, C.POINTER(C.c_int)]),
+    ("cmvg_bicover_save", C.c_int, [_P, C.c_char_p]),
+    ("cmvg_bicover_load", C.c_int, [C.c_char_p, C.POINTER(_P)]),
+    ("cmvg_bicover_matvec_f64", C.c_int, [_P, _P, _P, C.c_int, _P]),
+    ("cmvg_bicover_free", None, [_P]),
 ]
 
 EXPORTED_SYMBOLS = [s[0] for s in _SIGS]
@@ -459,6 +468,131 @@ def csr_matvec_device(row_offsets, cols, x, y=None, stream: Optional[int] = None
     _check(load_library().cmvg_csr_matvec_f64(n, cols.numel(), row_offsets.data_ptr(), cols.data_ptr(),
                                               x.data_ptr(), y.data_ptr(), st))
     return y
+
+
+UNBOUNDED_ROUNDS = (1 << 64) - 1  # cmv::kUnboundedRounds (biclique.hpp:46-47)
+
+
+class BicliqueCover:
+    """Edge-disjoint biclique cover of a graph plus residual edges (the
+    reference's cmv::BicliqueCover, biclique.hpp:24-38) with its GPU product.
+    ``compressed_size`` = sum |S_r| + |C_r| + |residual|, the adds of one
+    product (biclique.hpp:33-34)."""
+
+    def __init__(self, handle: int):
+        self._h = _P(handle)
+        self._sz = None  # the cover is immutable: sizes cached on first use
+
+    @classmethod
+    def extract_greedy(cls, g: CsrGraph, min_gain: int = 1, max_rounds: int = UNBOUNDED_ROUNDS,
+                       per_round: int = 1) -> "BicliqueCover":
+        """cmv::extract_greedy (biclique.hpp:58-61).  per_round=1 emits the
+        best candidate per round (the reference's rule); 0 emits every
+        still-valid candidate of a round in gain order (large graphs)."""
+        out = _P()
+        _check(load_library().cmvg_bicover_extract(g._h, min_gain, max_rounds, per_round, C.byref(out)))
+        return cls(out.value)
+
+    @classmethod
+    def from_lists(cls, n: int, bicliques, residual) -> "BicliqueCover":
+        """From [(sources, targets), ...] and [(u, v), ...] (ids ascending)."""
+        src = [np.asarray(s, dtype=np.uint32) for s, _ in bicliques]
+        tgt = [np.asarray(t, dtype=np.uint32) for _, t in bicliques]
+        so = np.zeros(len(src) + 1, dtype=np.uint64)
+        to = np.zeros(len(tgt) + 1, dtype=np.uint64)
+        so[1:] = np.cumsum([len(a) for a in src]) if src else []
+        to[1:] = np.cumsum([len(a) for a in tgt]) if tgt else []
+        sa = np.concatenate(src) if src else np.zeros(1, dtype=np.uint32)
+        ta = np.concatenate(tgt) if tgt else np.zeros(1, dtype=np.uint32)
+        res = np.ascontiguousarray(np.asarray(residual, dtype=np.uint32).reshape(-1, 2))
+        out = _P()
+        _check(load_library().cmvg_bicover_from_arrays(
+            n, len(src), so.ctypes.data, sa.ctypes.data, to.ctypes.data, ta.ctypes.data, len(res),
+            res.ctypes.data if len(res) else None, C.byref(out)))
+        return cls(out.value)
+
+    def _sizes(self):
+        if self._sz is None:
+            n, v = C.c_uint32(), [C.c_uint64() for _ in range(5)]
+            _check(load_library().cmvg_bicover_sizes(self._h, C.byref(n), *[C.byref(a) for a in v]))
+            self._sz = (n.value,) + tuple(a.value for a in v)
+        return self._sz
+
+    @property
+    def n(self) -> int:
+        return self._sizes()[0]
+
+    @property
+    def compressed_size(self) -> int:
+        return self._sizes()[5]
+
+    def lists(self):
+        """([(sources, targets), ...], residual (k, 2) uint32)."""
+        n, nb, ns, nt, nr, _ = self._sizes()
+        so, to = np.zeros(nb + 1, dtype=np.uint64), np.zeros(nb + 1, dtype=np.uint64)
+        sa, ta = np.zeros(max(ns, 1), dtype=np.uint32), np.zeros(max(nt, 1), dtype=np.uint32)
+        res = np.zeros((max(nr, 1), 2), dtype=np.uint32)
+        _check(load_library().cmvg_bicover_export(self._h, so.ctypes.data, sa.ctypes.data, to.ctypes.data,
+                                                  ta.ctypes.data, res.ctypes.data))
+        bl = [(sa[so[r]:so[r + 1]].copy(), ta[to[r]:to[r + 1]].copy()) for r in range(nb)]
+        return bl, res[:nr].copy()
+
+    def verify(self, g: CsrGraph) -> bool:
+        """cmv::verify_cover (biclique.hpp:63-64)."""
+        ok = C.c_int()
+        _check(load_library().cmvg_bicover_verify(self._h, g._h, C.byref(ok)))
+        return bool(ok.value)
+
+    def save(self, path: str) -> None:
+        _check(load_library().cmvg_bicover_save(self._h, os.fsencode(path)))
+
+    @classmethod
+    def load(cls, path: str) -> "BicliqueCover":
+        out = _P()
+        _check(load_library().cmvg_bicover_load(os.fsencode(path), C.byref(out)))
+        return cls(out.value)
+
+    def matvec(self, x, y=None, stream: Optional[int] = None):
+        """y = A x on the GPU (cmv::matvec_biclique_into, biclique.hpp:39-46):
+        numpy in/out (HOST) or CUDA torch tensors (DEVICE)."""
+        n = self.n
+        if len(x) != n:
+            raise ValueError(f"x has {len(x)} entries, the cover {n} vertices")
+        if y is None:
+            if _is_torch(x):
+                import torch
+                y = torch.empty(n, dtype=torch.float64, device=x.device)
+            else:
+                y = np.empty(n, dtype=np.float64)
+        xp, kind = _ptr_and_kind(x, np.float64)
+        yp, kind2 = _ptr_and_kind(y, np.float64)
+        if kind != kind2:
+            raise ValueError("x and y must both be host arrays or both CUDA tensors")
+        st = stream if stream is not None else _stream_of(x, y)
+        _check(load_library().cmvg_bicover_matvec_f64(self._h, xp, yp, kind, st))
+        return y
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib_handle is not None:
+            _lib_handle.cmvg_bicover_free(h)
+            self._h = None
+
+
+class BicliqueKernel:
+    """MatvecKernel over a biclique cover of A^T (for pagerank)."""
+
+    def __init__(self, cover_of_transpose: BicliqueCover):
+        self.cover = cover_of_transpose
+
+    def dimension(self) -> int:
+        return self.cover.n
+
+    def multiply(self, x, y) -> None:
+        self.cover.matvec(x, y)
+
+    def adds_per_product(self) -> int:
+        return self.cover.compressed_size
 
 
 class BvGraph:

@@ -138,6 +138,33 @@ BvStream bv_encode(const HostCsr& g, const BvParams& p);
 BvDecoded bv_decode(const BvStream& s);
 HostCsr transpose_csr(const HostCsr& g);
 
+// ---- biclique covers (biclique.cpp; reference include/cmv/biclique.hpp) ----
+struct Biclique {                  // complete directed bipartite edge set sources x targets
+  std::vector<uint32_t> sources;   // strictly ascending
+  std::vector<uint32_t> targets;   // strictly ascending
+};
+struct BicliqueCover {             // edge-disjoint bicliques + residual edges, union = E
+  uint32_t n = 0;
+  std::vector<Biclique> bicliques;                    // emission order
+  std::vector<std::pair<uint32_t, uint32_t>> residual;  // sorted (u, v)
+  uint64_t compressed_size() const;                   // sum |S|+|C| + |residual| (biclique.hpp:33-34)
+};
+// Device operands of the product y = M [x ; T x] (csrc/bicover.cu).
+struct CoverLayout {
+  uint32_t n = 0;
+  uint64_t nb = 0;
+  std::vector<uint64_t> t_off, m_off;  // nb + 1, n + 1
+  std::vector<uint32_t> t_cols, m_cols;
+};
+BicliqueCover extract_greedy(const HostCsr& g, uint64_t min_gain, uint64_t max_rounds, uint32_t per_round);
+void validate_cover_structure(const BicliqueCover& c);
+bool verify_cover(const BicliqueCover& c, const HostCsr& g);
+std::string save_cover_text(const BicliqueCover& c);
+BicliqueCover load_cover_text(const std::string& text);
+void save_cover_file(const BicliqueCover& c, const std::string& path);
+BicliqueCover load_cover_file(const std::string& path);
+void build_cover_layout(const BicliqueCover& c, CoverLayout& L);
+
 // ---- CBV1 container (bv_io.cpp): the BV stream on disk ----------------------
 // The reference's container error types (rmv_io.hpp:13-22).
 struct FormatError : std::runtime_error {  // unrecognised container: bad magic or version

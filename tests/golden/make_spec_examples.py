@@ -83,6 +83,28 @@ ex = {
         {"spec": "SPEC.md:263", "n": 3, "edges": [[0, 1], [1, 2]], "alpha": 0.15, "iterations": 50,
          "dangling": "uniform", "want": dense_pagerank(3, [[0, 1], [1, 2]], 0.15, 50), "tol": 1e-10},
     ],
+    # biclique module (reference include/cmv/biclique.hpp)
+    "matvec_biclique": [
+        {"spec": "SPEC.md:317", "n": 4, "bicliques": [[[0, 1], [2, 3]]], "residual": [], "x": [0, 0, 1, 1],
+         "c": [2], "y": [2, 2, 0, 0], "adds": 4, "m": 4},
+        {"spec": "SPEC.md:318", "n": 6, "bicliques": [[[0, 1, 2], [3, 4, 5]]], "residual": [],
+         "x": [0, 0, 0, 1, 1, 1], "c": [3], "y": [3, 3, 3, 0, 0, 0], "adds": 6, "m": 9},
+        {"spec": "SPEC.md:316", "n": 3, "bicliques": [], "residual": [[0, 1], [1, 2], [2, 0]], "x": [1, 2, 3],
+         "c": [], "y": [2, 3, 1], "adds": 3, "m": 3},
+    ],
+    "extract_greedy": [
+        {"spec": "SPEC.md:326", "n": 6, "edges": [[u, v] for u in range(3) for v in range(3, 6)],
+         "bicliques": [[[0, 1, 2], [3, 4, 5]]], "residual": [], "compressed_size": 6, "m": 9},
+        {"spec": "SPEC.md:328", "n": 8, "edges": sorted({(u, v) for u in range(3) for v in range(4, 8)}
+                                                        | {(u, v) for u in range(1, 4) for v in range(5, 8)}),
+         "verify": True},
+    ],
+    "verify_cover": [
+        {"spec": "SPEC.md:335", "n": 3, "edges": [[0, 1], [1, 2]], "bicliques": [], "residual": [[0, 1], [1, 2]],
+         "want": True},
+        {"spec": "SPEC.md:337", "n": 4, "edges": [[0, 2], [0, 3], [1, 2], [1, 3]], "bicliques": [[[0, 1], [2, 3]]],
+         "residual": [[0, 2]], "want": False},
+    ],
 }
 
 if __name__ == "__main__":
