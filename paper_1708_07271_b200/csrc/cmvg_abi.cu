@@ -512,7 +512,7 @@ namespace {
 
 template <typename XT, typename YT>
 void launch_gather(cmvg_graph* g, const XT* x, YT* y, cudaStream_t st, const XT* xfar = nullptr,
-                   uint32_t b0 = 0, uint32_t b1 = 0xffffffffu) {
+                   uint32_t b0 = 0, uint32_t b1 = 0xffffffffu, uint32_t xdev_limit = 0xffffffffu) {
   b1 = std::min(b1, g->nblocks);
   if (b0 >= b1) return;
   const BvsSmem L = bvs_smem_layout(g->dims, sizeof(XT));
@@ -529,6 +529,7 @@ void launch_gather(cmvg_graph* g, const XT* x, YT* y, cudaStream_t st, const XT*
   d.blocks += b0;  // blocks [b0, b1) of this shard
   d.block_begin += b0;
   d.nlaunch = b1 - b0;
+  d.xdev_limit = xdev_limit;
   d.ahead = resident_ctas(kern, (int)g->threads, L.total, g->device, g->gather_res[sizeof(XT) == 8 ? 0 : 1]);
   kern<<<b1 - b0, g->threads, L.total, st>>>(d, x, xfar ? xfar : x, y, PrArgs{});
   CUDA_TRY(cudaGetLastError());
@@ -588,8 +589,11 @@ void gather_host_pipelined(cmvg_graph* g, const T* x, T* y, const T* xmapped) {
   for (uint32_t c = 0; c < C; ++c) {
     const uint32_t b0 = cut[c], b1 = cut[c + 1];
     if (b0 == b1 && c + 1 < C) continue;
-    // x needed by blocks < b1: their windows (prefix max), everything for the last chunk
-    size_t need = c + 1 == C ? g->n : std::min<size_t>(g->n, g->win_need[b1 - 1]);
+    // x needed by blocks < b1: their windows (prefix max) plus a lookahead
+    // that covers most out-of-window columns (512 KB of fp64: ~10 us of
+    // PCIe), everything for the last chunk
+    constexpr size_t kLookahead = size_t(1) << 16;
+    size_t need = c + 1 == C ? g->n : std::min<size_t>(g->n, g->win_need[b1 - 1] + kLookahead);
     if (need > xdone) {
       CUDA_TRY(cudaMemcpyAsync(hx + xdone, x + xdone, (need - xdone) * sizeof(T), cudaMemcpyHostToDevice, g->s_in));
       xdone = need;
@@ -597,7 +601,10 @@ void gather_host_pipelined(cmvg_graph* g, const T* x, T* y, const T* xmapped) {
     CUDA_TRY(cudaEventRecord(g->ev[2 * c], g->s_in));
     if (trace) CUDA_TRY(cudaEventRecord(tev[3 * c], g->s_in));
     CUDA_TRY(cudaStreamWaitEvent(g->s_comp, g->ev[2 * c], 0));
-    launch_gather<T, T>(g, hx, hy, g->s_comp, xmapped, b0, b1);
+    // columns outside a block's window: from the device copy when already
+    // uploaded (column < xdone), else from the mapped host x -- a PCIe round
+    // trip that queues behind the H2D stream, so the lookahead keeps it rare
+    launch_gather<T, T>(g, hx, hy, g->s_comp, xmapped, b0, b1, (uint32_t)std::min<size_t>(xdone, 0xffffffffu));
     CUDA_TRY(cudaEventRecord(g->ev[2 * c + 1], g->s_comp));
     if (trace) CUDA_TRY(cudaEventRecord(tev[3 * c + 1], g->s_comp));
     CUDA_TRY(cudaStreamWaitEvent(g->s_out, g->ev[2 * c + 1], 0));

@@ -392,6 +392,7 @@ __global__ void __launch_bounds__(256, 4) bvs_gather_kernel(BvdDev g, const XT* 
   xw.carve(smem + L.off_x, W, T);
   xw.x = x;
   xw.xfar = xfar;
+  xw.xlim = g.xdev_limit;
   xw.wlo = bi.wlo;
   XT xpre[XWin<XT>::kPre];
   xw.prefetch(D.n, xpre);

@@ -191,6 +191,7 @@ struct cmvg_graph {
     d.row_begin = row_begin;
     d.stream_cap_words = stream_cap_words;
     d.nlaunch = nblocks;
+    d.xdev_limit = 0xffffffffu;  // every column of x is on the device
     return d;
   }
   BvdDev tdev() const {
