@@ -42,12 +42,28 @@ __device__ __forceinline__ uint32_t extract_bits(const S& s, uint32_t off, uint3
   return w ? (uint32_t)(win >> (64u - w)) : 0u;
 }
 
+// ---- a block row's record in shared memory: its delta (double-double, lo
+// rounded to fp32) and reference distance, 16 bytes, so the slice epilogue
+// writes it with one 16-byte store and the chain walk reads an ancestor with
+// one 16-byte load
+struct __align__(16) RowRec {
+  double hi;
+  float lo;
+  uint32_t ref;
+};
+__device__ __forceinline__ void put_row(RowRec* rows, uint32_t k, double hi, double lo, uint32_t r) {
+  double2 v;
+  v.x = hi;
+  v.y = __hiloint2double((int)r, __float_as_int((float)lo));  // {lo, ref} as the record's second 8 bytes
+  *reinterpret_cast<double2*>(rows + k) = v;
+}
+
 // ---- reference-chain context of a block (chain_and_store) --------------------
 struct ChainCtx {
-  const uint8_t* ref;  // reference distance per row of the block
-  uint16_t* ptr;       // scratch: chain pointers (unbounded chains only)
-  int* wscratch;       // 64 ints: epilogue reductions
-  uint32_t nr;         // rows in the block
+  RowRec* rows;    // per row of the block: delta and reference distance
+  uint16_t* ptr;   // scratch: chain pointers (unbounded chains only)
+  int* wscratch;   // 64 ints: epilogue reductions
+  uint32_t nr;     // rows in the block
 };
 
 // Compensated accumulation: TwoSum, error term into `c` (error ~ eps|sum| +
@@ -168,29 +184,31 @@ struct PageRankEpi {
 // Bounded chains (R = 3) take two levels; unbounded ones log2(depth).
 // Writes y (YT) with coalesced stores.  Uses c.ptr as the pointer array.
 template <typename YT, class EPI = PlainEpi>
-__device__ __forceinline__ void chain_and_store(double* s_yhi, float* s_ylo, const ChainCtx& c, YT* __restrict__ yb,
-                                                EPI epi = EPI(), uint32_t max_depth = 0xffffffffu,
-                                                uint32_t T = blockDim.x) {
+__device__ __forceinline__ void chain_and_store(const ChainCtx& c, YT* __restrict__ yb, EPI epi = EPI(),
+                                                uint32_t max_depth = 0xffffffffu, uint32_t T = blockDim.x) {
   const uint32_t tid = threadIdx.x;
+  RowRec* rows = c.rows;
   if (max_depth <= 3) {
     // Bounded chains (R <= 3): each row walks its <= 3 ancestors,
     // y_i = d_i + d_p1 + d_p2 + d_p3 accumulated with TwoSum (error terms
-    // collected with the low parts), no barriers.
+    // collected with the low parts), no barriers; one 16-byte load per row.
     for (uint32_t kb = tid; kb < c.nr; kb += kEpiPre * T) {
       epi.prefetch(kb, T, c.nr);
 #pragma unroll
       for (uint32_t q = 0; q < kEpiPre; ++q) {
         const uint32_t k = kb + q * T;
         if (k >= c.nr) break;
-        double s = s_yhi[k], e = (double)s_ylo[k];
-        uint32_t p = k, r = c.ref[k];
+        const RowRec rk = rows[k];
+        double s = rk.hi, e = (double)rk.lo;
+        uint32_t p = k, r = rk.ref;
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
           if (r) {
             p -= r;
-            tsum(s, e, s_yhi[p]);
-            e += (double)s_ylo[p];
-            r = c.ref[p];
+            const RowRec rp = rows[p];
+            tsum(s, e, rp.hi);
+            e += (double)rp.lo;
+            r = rp.ref;
           }
         }
         epi.store(yb, k, s + e, q);
@@ -204,7 +222,7 @@ __device__ __forceinline__ void chain_and_store(double* s_yhi, float* s_ylo, con
   uint16_t* ptr = c.ptr;
   int any = 0;
   for (uint32_t k = tid; k < c.nr; k += T) {
-    const uint32_t r = c.ref[k];
+    const uint32_t r = rows[k].ref;
     ptr[k] = r ? (uint16_t)(k - r) : kNone;
     any |= (r != 0);
   }
@@ -218,10 +236,10 @@ __device__ __forceinline__ void chain_and_store(double* s_yhi, float* s_ylo, con
       const uint32_t k = tid + q * T;
       if (k < c.nr) {
         const uint32_t p = ptr[k];
-        double h = s_yhi[k], l = s_ylo[k];
+        double h = rows[k].hi, l = rows[k].lo;
         uint16_t pn = kNone;
         if (p != kNone) {
-          dd_add(h, l, s_yhi[p], s_ylo[p]);
+          dd_add(h, l, rows[p].hi, rows[p].lo);
           pn = ptr[p];
         }
         nh[q] = h;
@@ -235,8 +253,8 @@ __device__ __forceinline__ void chain_and_store(double* s_yhi, float* s_ylo, con
     for (uint32_t q = 0; q < kMaxPer; ++q) {
       const uint32_t k = tid + q * T;
       if (k < c.nr) {
-        s_yhi[k] = nh[q];
-        s_ylo[k] = (float)nl[q];
+        rows[k].hi = nh[q];
+        rows[k].lo = (float)nl[q];
         ptr[k] = np_[q];
       }
     }
@@ -247,7 +265,7 @@ __device__ __forceinline__ void chain_and_store(double* s_yhi, float* s_ylo, con
 #pragma unroll
     for (uint32_t q = 0; q < kEpiPre; ++q) {
       const uint32_t k = kb + q * T;
-      if (k < c.nr) epi.store(yb, k, s_yhi[k] + (double)s_ylo[k], q);
+      if (k < c.nr) epi.store(yb, k, rows[k].hi + (double)rows[k].lo, q);
     }
   }
   epi.finish(c.wscratch);

@@ -48,7 +48,7 @@ constexpr uint32_t kBvsGuardWords = 64;  // zero words after the last block (lan
 constexpr uint32_t kBvsSliceTab = 128;  // slice-table entries staged in shared memory
 
 struct BvsSmem {
-  uint32_t off_x, off_yhi, off_ylo, off_ptr, off_ref, off_tab, off_pref, off_misc, total;
+  uint32_t off_x, off_rows, off_ptr, off_tab, off_pref, off_misc, total;
 };
 
 __host__ __device__ inline BvsSmem bvs_smem_layout(uint32_t W, uint32_t B, uint32_t xsize) {
@@ -56,14 +56,10 @@ __host__ __device__ inline BvsSmem bvs_smem_layout(uint32_t W, uint32_t B, uint3
   uint32_t o = 0;
   s.off_x = o;
   o = align16(o + xw_bytes(W, xsize));
-  s.off_yhi = o;
-  o = align16(o + B * 8);
-  s.off_ylo = o;
-  o = align16(o + B * 4);
+  s.off_rows = o;  // RowRec per row: delta and reference distance
+  o = align16(o + B * (uint32_t)sizeof(RowRec));
   s.off_ptr = o;  // chain pointers (unbounded chains only)
   o = align16(o + B * 2);
-  s.off_ref = o;
-  o = align16(o + B);
   s.off_tab = o;
   o = align16(o + kBvsSliceTab * 8);
   s.off_pref = o;  // block-table entry of the block `ahead` blocks on (L2 prefetch)
@@ -97,7 +93,7 @@ enum BvsMisc : int { kBvsHeavyCtr = 0, kBvsSliceCtr = 1 };
 // Heavy rows: one warp per row, lanes stride over the row's fixed-width codes.
 template <class S, class XW>
 __device__ __forceinline__ void bvs_heavy(const S& src, const XW& xw, int32_t r0, uint32_t lmin, int* misc,
-                                          double* s_yhi, float* s_ylo, uint8_t* s_ref) {
+                                          RowRec* s_rows) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t nh = src.w(0) >> 16, htab = src.w(1), hbase = src.w(2) * 32u;
   for (;;) {
@@ -150,11 +146,7 @@ __device__ __forceinline__ void bvs_heavy(const S& src, const XW& xw, int32_t r0
       const double uh = __shfl_down_sync(0xffffffffu, hi, o), ul = __shfl_down_sync(0xffffffffu, lo, o);
       dd_add(hi, lo, uh, ul);
     }
-    if (lane == 0) {
-      s_yhi[k] = hi;
-      s_ylo[k] = (float)lo;
-      s_ref[k] = (uint8_t)sa_r(sa);
-    }
+    if (lane == 0) put_row(s_rows, k, hi, lo, sa_r(sa));
   }
 }
 
@@ -167,7 +159,7 @@ __device__ __forceinline__ double signed_term(double x, uint32_t t, uint32_t nm)
 // A slice's epilogue: segmented reduction of a multi slice, then the primary
 // lane writes delta_i and r_i.
 __device__ __forceinline__ void bvs_slice_epilogue(uint32_t lane, uint32_t meta, uint32_t h, double hi, double lo,
-                                                   double* s_yhi, float* s_ylo, uint8_t* s_ref) {
+                                                   RowRec* s_rows) {
   if (smeta_multi(meta)) {
     // a row's units sit in adjacent lanes starting at its primary: segmented
     // suffix reduction so the primary lane ends with the row's delta
@@ -183,12 +175,7 @@ __device__ __forceinline__ void bvs_slice_epilogue(uint32_t lane, uint32_t meta,
       if (lane + o <= end) dd_add(hi, lo, uh, ul);
     }
   }
-  if (uh_primary(h)) {
-    const uint32_t k = uh_k(h);
-    s_yhi[k] = hi;
-    s_ylo[k] = (float)lo;
-    s_ref[k] = (uint8_t)uh_r(h);
-  }
+  if (uh_primary(h)) put_row(s_rows, uh_k(h), hi, lo, uh_r(h));
 }
 
 // Slices: one unit (<= 16 points, <= 2 intervals of one row) per lane; in
@@ -196,8 +183,7 @@ __device__ __forceinline__ void bvs_slice_epilogue(uint32_t lane, uint32_t meta,
 // segmented warp reduction.  `bs` is the block's stream in global memory.
 template <class XW>
 __device__ __forceinline__ void bvs_slices(const uint32_t* __restrict__ bs, const XW& xw, uint32_t lmin, int* misc,
-                                           double* s_yhi, float* s_ylo, uint8_t* s_ref, const uint32_t* s_tab,
-                                           uint32_t T) {
+                                           RowRec* s_rows, const uint32_t* s_tab, uint32_t T) {
   constexpr bool kExact = sizeof(typename XW::value_type) == 8;  // compensated point sums for fp64 x
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t nsl = __ldg(bs) & 0xffffu;
@@ -254,7 +240,7 @@ __device__ __forceinline__ void bvs_slices(const uint32_t* __restrict__ bs, cons
       const uint32_t wi0 = mni > 0 ? __ldg(body + mnpw * 32u) : 0u;
       const uint32_t wi1 = mni > 1 ? __ldg(body + (mnpw + 1u) * 32u) : 0u;
       if (have_prev) {  // the previous slice's epilogue while these loads are in flight
-        bvs_slice_epilogue(lane, prev_meta, prev_h, prev_hi, prev_lo, s_yhi, s_ylo, s_ref);
+        bvs_slice_epilogue(lane, prev_meta, prev_h, prev_hi, prev_lo, s_rows);
         have_prev = false;
       }
       double acc2 = 0.0, comp2 = 0.0;
@@ -342,7 +328,7 @@ __device__ __forceinline__ void bvs_slices(const uint32_t* __restrict__ bs, cons
     }
     // this slice's epilogue runs after the next slice's loads are issued (it
     // hides their latency): keep its state
-    if (have_prev) bvs_slice_epilogue(lane, prev_meta, prev_h, prev_hi, prev_lo, s_yhi, s_ylo, s_ref);
+    if (have_prev) bvs_slice_epilogue(lane, prev_meta, prev_h, prev_hi, prev_lo, s_rows);
     prev_hi = acc + comp;
     prev_lo = comp - (prev_hi - acc);
     prev_h = h;
@@ -350,7 +336,7 @@ __device__ __forceinline__ void bvs_slices(const uint32_t* __restrict__ bs, cons
     have_prev = true;
     s = next;
   }
-  if (have_prev) bvs_slice_epilogue(lane, prev_meta, prev_h, prev_hi, prev_lo, s_yhi, s_ylo, s_ref);
+  if (have_prev) bvs_slice_epilogue(lane, prev_meta, prev_h, prev_hi, prev_lo, s_rows);
 }
 
 template <typename XT, typename YT, bool PR = false, uint32_t CW = 0, uint32_t CB = 0, uint32_t CT = 0>
@@ -399,12 +385,10 @@ __global__ void __launch_bounds__(256, 4) bvs_gather_kernel(BvdDev g, const XT* 
   __syncthreads();      // publishes the counters
   xw.stage(D.n, xpre);  // ends with __syncthreads
 
-  double* s_yhi = reinterpret_cast<double*>(smem + L.off_yhi);
-  float* s_ylo = reinterpret_cast<float*>(smem + L.off_ylo);
-  uint8_t* s_ref = smem + L.off_ref;
+  RowRec* s_rows = reinterpret_cast<RowRec*>(smem + L.off_rows);
   const Src<false> src{bs};
-  bvs_heavy(src, xw, (int32_t)r0, D.min_interval, misc, s_yhi, s_ylo, s_ref);
-  bvs_slices(bs, xw, D.min_interval, misc, s_yhi, s_ylo, s_ref, s_tab, T);
+  bvs_heavy(src, xw, (int32_t)r0, D.min_interval, misc, s_rows);
+  bvs_slices(bs, xw, D.min_interval, misc, s_rows, s_tab, T);
   __syncthreads();
   if (threadIdx.x == 32 && ahead) {
     cp_async_wait_all();
@@ -417,7 +401,7 @@ __global__ void __launch_bounds__(256, 4) bvs_gather_kernel(BvdDev g, const XT* 
   }
 
   ChainCtx rc;
-  rc.ref = s_ref;
+  rc.rows = s_rows;
   rc.ptr = reinterpret_cast<uint16_t*>(smem + L.off_ptr);
   rc.wscratch = misc + 16;
   rc.nr = nr;
@@ -441,10 +425,10 @@ __global__ void __launch_bounds__(256, 4) bvs_gather_kernel(BvdDev g, const XT* 
     epi.p0 = pr.p0 ? pr.p0 + r0 : nullptr;
     epi.push_dst = pr.push_dst;
     epi.grow0 = r0;
-    chain_and_store(s_yhi, s_ylo, rc, yb, epi, D.max_depth, T);
+    chain_and_store(rc, yb, epi, D.max_depth, T);
   } else {
     PlainEpi epi;
-    chain_and_store(s_yhi, s_ylo, rc, yb, epi, D.max_depth, T);
+    chain_and_store(rc, yb, epi, D.max_depth, T);
   }
 }
 
