@@ -21,13 +21,26 @@
 // whatever the cancellation in the differential rows.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 
 #include "bvd_common.cuh"
 #include "bvs_gather.cuh"
 
 namespace cmvg {
 
-constexpr uint32_t kMmCols = 8;
+// Columns per pass and the staging type: KC = 8 columns staged as fp32 (the
+// fp32 -> fp64 conversions then run per use, on the XU pipe), or KC = 4
+// columns staged as fp64 (converted once per staged row; twice the passes,
+// no conversions in the decode).  Both stage 32 bytes per window row.  KC = 8
+// is the default: at the C5 shape (n = 2^24, k = 16) it measured 3.03 ms
+// against 4.60 ms for KC = 4 -- the per-pass decode costs more than the
+// conversions it would save.
+#ifndef CMVG_MM_COLS
+#define CMVG_MM_COLS 8
+#endif
+constexpr uint32_t kMmCols = CMVG_MM_COLS;
+using MmStage = typename std::conditional<kMmCols == 4, double, float>::type;
+static_assert(kMmCols * sizeof(MmStage) == 32, "32-byte staged rows");
 
 struct BvsMmSmem {
   uint32_t off_x, off_d, off_ref, off_misc, total;
@@ -36,8 +49,8 @@ struct BvsMmSmem {
 __host__ __device__ inline BvsMmSmem bvs_mm_smem_layout(const BvdDims& d) {
   BvsMmSmem s;
   uint32_t o = 0;
-  s.off_x = o;  // [W][KC] fp32: the X rows of the block's window, this column chunk
-  o = align16(o + d.window * kMmCols * 4);
+  s.off_x = o;  // [W][KC] MmStage: the X rows of the block's window, this column chunk
+  o = align16(o + d.window * 32u);
   s.off_d = o;  // [B][KC] fp64 deltas
   o = align16(o + d.block_rows * kMmCols * 8);
   s.off_ref = o;  // 4-bit reference distances
@@ -51,8 +64,8 @@ __host__ __device__ inline BvsMmSmem bvs_mm_smem_layout(const BvdDims& d) {
 struct MmCtx {
   const float* __restrict__ X;  // column chunk base (X + c0)
   uint32_t ld, kk;              // leading dimension, columns in this chunk (<= KC)
-  bool vec;                     // kk == KC and 16-byte aligned rows: float4 loads
-  const float4* xs;             // staged window rows (2 float4 per row), zero-padded columns
+  bool vec;                     // kk == KC and 16-byte aligned rows: vector loads
+  const float4* xs;             // staged window rows (32 bytes each), zero-padded columns
   uint32_t wlo, W;
 };
 
@@ -61,11 +74,19 @@ struct MmCtx {
 // its sustained rate); fp64 staging would need 96 KB and one CTA per SM,
 // measured slower.
 __device__ __forceinline__ void mm_add_near(const MmCtx& m, uint32_t j, bool neg, double (&acc)[kMmCols]) {
-  const float4 a = m.xs[2 * j], b = m.xs[2 * j + 1];
-  const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
   const double sg = neg ? -1.0 : 1.0;
+  if constexpr (kMmCols == 4) {
+    const double2* r = reinterpret_cast<const double2*>(m.xs + 2 * j);
+    const double2 a = r[0], b = r[1];
+    const double v[4] = {a.x, a.y, b.x, b.y};
 #pragma unroll
-  for (uint32_t c = 0; c < kMmCols; ++c) acc[c] = fma(sg, (double)v[c], acc[c]);
+    for (uint32_t c = 0; c < 4; ++c) acc[c] = fma(sg, v[c], acc[c]);
+  } else {
+    const float4 a = m.xs[2 * j], b = m.xs[2 * j + 1];
+    const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+    for (uint32_t c = 0; c < kMmCols; ++c) acc[c] = fma(sg, (double)v[c], acc[c]);
+  }
 }
 
 // acc[0..KC) += sgn * X[row, 0..kk) from global memory (far columns)
@@ -73,9 +94,13 @@ __device__ __forceinline__ void mm_add_row(const MmCtx& m, uint32_t row, bool ne
   const float* p = m.X + (size_t)row * m.ld;
   const double sg = neg ? -1.0 : 1.0;
   if (m.vec) {
+    float v[8];
     const float4 a = __ldg(reinterpret_cast<const float4*>(p));
-    const float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
-    const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    v[0] = a.x, v[1] = a.y, v[2] = a.z, v[3] = a.w;
+    if constexpr (kMmCols == 8) {
+      const float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+      v[4] = b.x, v[5] = b.y, v[6] = b.z, v[7] = b.w;
+    }
 #pragma unroll
     for (uint32_t c = 0; c < kMmCols; ++c) acc[c] = fma(sg, (double)v[c], acc[c]);
   } else {
@@ -254,21 +279,42 @@ __global__ void __launch_bounds__(512, 2) bvs_matmat_kernel(BvdDev g, const floa
   {  // stage the window's X rows (this column chunk), coalesced; columns >= kk and rows >= n are 0
     float4* xs = reinterpret_cast<float4*>(smem + L.off_x);
     m.xs = xs;
-    for (uint32_t e = tid; e < 2u * D.window; e += T) {
-      const uint32_t row = bi.wlo + (e >> 1), c0 = (e & 1u) * 4u;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (row < D.n) {
-        const float* p = X + (size_t)row * ld + c0;
-        if (m.vec) {
-          v = __ldg(reinterpret_cast<const float4*>(p));
-        } else {
-          if (c0 + 0 < kk) v.x = __ldg(p + 0);
-          if (c0 + 1 < kk) v.y = __ldg(p + 1);
-          if (c0 + 2 < kk) v.z = __ldg(p + 2);
-          if (c0 + 3 < kk) v.w = __ldg(p + 3);
+    if constexpr (kMmCols == 4) {  // one 16-byte fp32 load per row, stored as 4 fp64 (32 bytes)
+      for (uint32_t e = tid; e < D.window; e += T) {
+        const uint32_t row = bi.wlo + e;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (row < D.n) {
+          const float* p = X + (size_t)row * ld;
+          if (m.vec) {
+            v = __ldg(reinterpret_cast<const float4*>(p));
+          } else {
+            if (0 < kk) v.x = __ldg(p + 0);
+            if (1 < kk) v.y = __ldg(p + 1);
+            if (2 < kk) v.z = __ldg(p + 2);
+            if (3 < kk) v.w = __ldg(p + 3);
+          }
         }
+        double2* d = reinterpret_cast<double2*>(xs + 2 * e);
+        d[0] = make_double2(v.x, v.y);
+        d[1] = make_double2(v.z, v.w);
       }
-      xs[e] = v;
+    } else {
+      for (uint32_t e = tid; e < 2u * D.window; e += T) {
+        const uint32_t row = bi.wlo + (e >> 1), c0 = (e & 1u) * 4u;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (row < D.n) {
+          const float* p = X + (size_t)row * ld + c0;
+          if (m.vec) {
+            v = __ldg(reinterpret_cast<const float4*>(p));
+          } else {
+            if (c0 + 0 < kk) v.x = __ldg(p + 0);
+            if (c0 + 1 < kk) v.y = __ldg(p + 1);
+            if (c0 + 2 < kk) v.z = __ldg(p + 2);
+            if (c0 + 3 < kk) v.w = __ldg(p + 3);
+          }
+        }
+        xs[e] = v;
+      }
     }
     __syncthreads();
   }
