@@ -327,10 +327,14 @@ int cmvg_create(const cmvg_bvstream* s, const cmvg_create_opts* opts_in, cmvg_gr
           for (uint64_t v = bm[wi]; v; v &= v - 1) rs.push_back((uint32_t)(wi * 64 + __builtin_ctzll(v)));
       }
       g->win_need.resize(sbl.size());
-      uint64_t pm = 0;
+      g->far_need.resize(sbl.size());
+      uint64_t pm = 0, fm = 0;
       for (size_t q = 0; q < sbl.size(); ++q) {
         pm = std::max<uint64_t>(pm, (uint64_t)sbl[q].wlo + L.dims.window);
         g->win_need[q] = (uint32_t)std::min<uint64_t>(pm, bs.n);
+        const uint32_t b = g->block_begin + (uint32_t)q;
+        for (uint64_t r = L.rfar_ptr[b]; r < L.rfar_ptr[b + 1]; ++r) fm = std::max<uint64_t>(fm, (uint64_t)L.rfar[r] + 1);
+        g->far_need[q] = (uint32_t)std::min<uint64_t>(fm, bs.n);
       }
       // BV-T
       const uint64_t t0 = L.tblocks[g->block_begin].word_offset;
@@ -512,7 +516,7 @@ namespace {
 
 template <typename XT, typename YT>
 void launch_gather(cmvg_graph* g, const XT* x, YT* y, cudaStream_t st, const XT* xfar = nullptr,
-                   uint32_t b0 = 0, uint32_t b1 = 0xffffffffu, uint32_t xdev_limit = 0xffffffffu) {
+                   uint32_t b0 = 0, uint32_t b1 = 0xffffffffu) {
   b1 = std::min(b1, g->nblocks);
   if (b0 >= b1) return;
   const BvsSmem L = bvs_smem_layout(g->dims, sizeof(XT));
@@ -529,7 +533,6 @@ void launch_gather(cmvg_graph* g, const XT* x, YT* y, cudaStream_t st, const XT*
   d.blocks += b0;  // blocks [b0, b1) of this shard
   d.block_begin += b0;
   d.nlaunch = b1 - b0;
-  d.xdev_limit = xdev_limit;
   d.ahead = resident_ctas(kern, (int)g->threads, L.total, g->device, g->gather_res[sizeof(XT) == 8 ? 0 : 1]);
   kern<<<b1 - b0, g->threads, L.total, st>>>(d, x, xfar ? xfar : x, y, PrArgs{});
   CUDA_TRY(cudaGetLastError());
@@ -601,10 +604,12 @@ void gather_host_pipelined(cmvg_graph* g, const T* x, T* y, const T* xmapped) {
     CUDA_TRY(cudaEventRecord(g->ev[2 * c], g->s_in));
     if (trace) CUDA_TRY(cudaEventRecord(tev[3 * c], g->s_in));
     CUDA_TRY(cudaStreamWaitEvent(g->s_comp, g->ev[2 * c], 0));
-    // columns outside a block's window: from the device copy when already
-    // uploaded (column < xdone), else from the mapped host x -- a PCIe round
-    // trip that queues behind the H2D stream, so the lookahead keeps it rare
-    launch_gather<T, T>(g, hx, hy, g->s_comp, xmapped, b0, b1, (uint32_t)std::min<size_t>(xdone, 0xffffffffu));
+    // columns outside the blocks' windows: from the device copy when all of
+    // them are already uploaded (the lookahead makes that the common case),
+    // else from the mapped host x -- PCIe round trips that queue behind the
+    // H2D stream
+    const bool far_on_device = g->far_need.empty() || g->far_need[b1 - 1] <= xdone;
+    launch_gather<T, T>(g, hx, hy, g->s_comp, far_on_device ? hx : xmapped, b0, b1);
     CUDA_TRY(cudaEventRecord(g->ev[2 * c + 1], g->s_comp));
     if (trace) CUDA_TRY(cudaEventRecord(tev[3 * c + 1], g->s_comp));
     CUDA_TRY(cudaStreamWaitEvent(g->s_out, g->ev[2 * c + 1], 0));

@@ -20,8 +20,7 @@ struct BvdDev {
   uint32_t stream_cap_words;  // blocks with more words decode from global memory
   uint32_t nlaunch;           // blocks of this launch (`blocks` is offset to its first)
   uint32_t ahead;             // L2 prefetch distance in blocks (resident CTAs of the launch; 0 = none)
-  uint32_t xdev_limit;        // out-of-window columns c < xdev_limit read the device x, the others xfar
-  uint32_t pad_[2];
+  uint32_t pad_[3];
 };
 
 __host__ __device__ inline uint32_t align16(uint32_t v) { return (v + 15u) & ~15u; }

@@ -181,7 +181,7 @@ __device__ __forceinline__ void bvs_slice_epilogue(uint32_t lane, uint32_t meta,
 // Slices: one unit (<= 16 points, <= 2 intervals of one row) per lane; in
 // "multi" slices a row's units occupy adjacent lanes and are combined by a
 // segmented warp reduction.  `bs` is the block's stream in global memory.
-template <class XW>
+template <bool DYN, class XW>
 __device__ __forceinline__ void bvs_slices(const uint32_t* __restrict__ bs, const XW& xw, uint32_t lmin, int* misc,
                                            RowRec* s_rows, const uint32_t* s_tab, uint32_t T) {
   constexpr bool kExact = sizeof(typename XW::value_type) == 8;  // compensated point sums for fp64 x
@@ -193,15 +193,22 @@ __device__ __forceinline__ void bvs_slices(const uint32_t* __restrict__ bs, cons
   // static schedule: with kBvsWarps warps each takes the contiguous table
   // range the transcoder's LPT assignment gave it (header words 4..8), else
   // round-robin; no ticket round trip sits in front of a slice's loads
+  // Blocks with heavy rows (DYN) take slices dynamically: a warp still busy
+  // with a hub row must not hold a static share of the slices (C4's
+  // power-law rows); the others use the transcoder's static LPT ranges.
   const uint32_t nwarp = T >> 5, warp = threadIdx.x >> 5;
+  constexpr bool dyn = DYN;
   uint32_t s = warp, s_end = nsl, step = nwarp;
-  if (nwarp == kBvsWarps) {
+  if (dyn) {
+    s = ticket_take(ticket_issue(&misc[kBvsSliceCtr]));
+  } else if (nwarp == kBvsWarps) {
     const uint16_t* starts = reinterpret_cast<const uint16_t*>(bs + kBvsWarpTab);
     s = __ldg(starts + warp);
     s_end = __ldg(starts + warp + 1);
     step = 1;
   }
   while (s < s_end) {
+    const uint32_t tk = dyn ? ticket_issue(&misc[kBvsSliceCtr]) : 0u;  // the next ticket, one slice ahead
     const uint32_t next = s + step;
     // slice table entry from shared memory (staged per block) when it fits:
     // header, meta and body words then come in one round of global loads
@@ -334,7 +341,7 @@ __device__ __forceinline__ void bvs_slices(const uint32_t* __restrict__ bs, cons
     prev_h = h;
     prev_meta = meta;
     have_prev = true;
-    s = next;
+    s = dyn ? ticket_take(tk) : next;
   }
   if (have_prev) bvs_slice_epilogue(lane, prev_meta, prev_h, prev_hi, prev_lo, s_rows);
 }
@@ -356,6 +363,7 @@ __global__ void __launch_bounds__(256, 4) bvs_gather_kernel(BvdDev g, const XT* 
   const uint32_t* bs = g.words + bi.word_offset;  // this block's stream (global; read through L1/L2)
   if (threadIdx.x == 0) {
     misc[kBvsHeavyCtr] = 0;
+    misc[kBvsSliceCtr] = 0;
   }
   // L2 prefetch a launch-wide wave ahead: this CTA fetches (cp.async, no
   // register or stall) the table entry of block bl + ahead -- about the block
@@ -378,7 +386,6 @@ __global__ void __launch_bounds__(256, 4) bvs_gather_kernel(BvdDev g, const XT* 
   xw.carve(smem + L.off_x, W, T);
   xw.x = x;
   xw.xfar = xfar;
-  xw.xlim = g.xdev_limit;
   xw.wlo = bi.wlo;
   XT xpre[XWin<XT>::kPre];
   xw.prefetch(D.n, xpre);
@@ -388,7 +395,10 @@ __global__ void __launch_bounds__(256, 4) bvs_gather_kernel(BvdDev g, const XT* 
   RowRec* s_rows = reinterpret_cast<RowRec*>(smem + L.off_rows);
   const Src<false> src{bs};
   bvs_heavy(src, xw, (int32_t)r0, D.min_interval, misc, s_rows);
-  bvs_slices(bs, xw, D.min_interval, misc, s_rows, s_tab, T);
+  if (__ldg(bs) >> 16)  // heavy rows in this block: slices dynamically
+    bvs_slices<true>(bs, xw, D.min_interval, misc, s_rows, s_tab, T);
+  else
+    bvs_slices<false>(bs, xw, D.min_interval, misc, s_rows, s_tab, T);
   __syncthreads();
   if (threadIdx.x == 32 && ahead) {
     cp_async_wait_all();

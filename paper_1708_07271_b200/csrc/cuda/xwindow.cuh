@@ -50,7 +50,6 @@ struct XWin {
   double* s_wt;  // staging scratch: warp totals, carry
   const XT* __restrict__ x;
   const XT* xfar;  // x at the columns outside the window (only those are read from it)
-  uint32_t xlim;   // out-of-window columns below xlim are read from x (device), the others from xfar
   uint32_t wlo, W;
   uint32_t T;  // threads of the CTA (a power of two; a compile-time constant in the specialised kernels)
 
@@ -217,7 +216,7 @@ struct XWin {
     const uint32_t j = (uint32_t)(c - (int32_t)wlo);
     const bool in = j < W;
     XT v = s_x[xw_pad(in ? j : 0u)];
-    if (!in) v = __ldg(((uint32_t)c < xlim ? x : xfar) + c);  // rare: a column outside the window
+    if (!in) v = __ldg(xfar + c);  // rare: column outside the window (read-only during the kernel)
     return (double)v;
   }
 

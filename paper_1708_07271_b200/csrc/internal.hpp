@@ -161,6 +161,7 @@ struct cmvg_graph {
   // staging for host-pointer calls; streams/events of the pipelined gather
   DevBuf hx, hy;
   std::vector<uint32_t> win_need;  // per block: x prefix its window needs (prefix max)
+  std::vector<uint32_t> far_need;  // per block: x prefix its out-of-window columns need (prefix max)
   std::vector<uint32_t> read_set;  // sorted columns of x this shard's gather reads
   cudaStream_t s_in = nullptr, s_comp = nullptr, s_out = nullptr;
   cudaEvent_t ev[32] = {};
@@ -191,7 +192,6 @@ struct cmvg_graph {
     d.row_begin = row_begin;
     d.stream_cap_words = stream_cap_words;
     d.nlaunch = nblocks;
-    d.xdev_limit = 0xffffffffu;  // every column of x is on the device
     return d;
   }
   BvdDev tdev() const {
