@@ -300,8 +300,12 @@ __device__ __forceinline__ void bvs_slices(const uint32_t* __restrict__ bs, cons
         if (t >= mnp) break;  // warp-uniform
         const double x0 = t < np ? xw.at(base + (int32_t)(w[q] >> 16)) : 0.0;
         const double x1 = t + 1u < np ? xw.at(base + (int32_t)(w[q] & 0xffffu)) : 0.0;
-        tsum(acc, comp, signed_term(x0, t, nm));
-        tsum(acc, comp, signed_term(x1, t + 1u, nm));
+        if constexpr (kExact) {
+          tsum(acc, comp, signed_term(x0, t, nm));
+          tsum(acc, comp, signed_term(x1, t + 1u, nm));
+        } else {
+          acc += signed_term(x0, t, nm) + signed_term(x1, t + 1u, nm);
+        }
       }
 #pragma unroll
       for (uint32_t u = 0; u < kBvsUnitInts; ++u) {
@@ -312,17 +316,19 @@ __device__ __forceinline__ void bvs_slices(const uint32_t* __restrict__ bs, cons
         tsum(acc, comp, hi);
         comp += lo;
       }
-    } else {  // class 32: absolute columns, bounds-checked; words loaded 4 at a time
+    } else {  // class 32: absolute columns, bounds-checked; 8 columns, then their 8 x loads, in flight together
       const uint32_t nm = uh_nm(h), np = uh_np(h), ni = uh_ni(h);
-      for (uint32_t t0 = 0; t0 < mnp; t0 += 4) {
-        uint32_t c[4];
+      for (uint32_t t0 = 0; t0 < mnp; t0 += 8) {
+        uint32_t c[8];
 #pragma unroll
-        for (uint32_t j = 0; j < 4; ++j) c[j] = t0 + j < np ? __ldg(body + (t0 + j) * 32u) : 0u;
+        for (uint32_t j = 0; j < 8; ++j) c[j] = t0 + j < np ? __ldg(body + (t0 + j) * 32u) : 0u;
+        double xv[8];
 #pragma unroll
-        for (uint32_t j = 0; j < 4; ++j) {
-          const uint32_t t = t0 + j;
-          const double xv = t < np ? xw.at((int32_t)c[j]) : 0.0;
-          tsum(acc, comp, signed_term(xv, t, nm));
+        for (uint32_t j = 0; j < 8; ++j) xv[j] = t0 + j < np ? xw.at((int32_t)c[j]) : 0.0;
+#pragma unroll
+        for (uint32_t j = 0; j < 8; ++j) {
+          if constexpr (kExact) tsum(acc, comp, signed_term(xv[j], t0 + j, nm));
+          else acc += signed_term(xv[j], t0 + j, nm);
         }
       }
       for (uint32_t u = 0; u < mni; ++u) {
