@@ -17,6 +17,7 @@ extern "C" int cmvg_csr_matvec_f64(uint32_t n, uint64_t m, const uint64_t* row_o
                                    const double* x, double* y, void* stream) {
   using namespace cmvg;
   return guarded([&] {
+    if (n == 0) return;  // nothing to compute (empty vectors may have null data pointers)
     require(row_offsets && x && y && (cols || m == 0), "null argument");
     CUDA_TRY(launch_csr_stream<false>(n, row_offsets, cols, x, n, nullptr, y, (cudaStream_t)stream));
   });

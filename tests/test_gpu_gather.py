@@ -227,7 +227,7 @@ def test_csr_baseline_matches_oracle(cuda, deg):
     against the oracle, for every sub-warp width it picks by mean degree."""
     import torch
 
-    g = P.CsrGraph.copy_model(1 << 14, deg, seed=5)
+    g = P.CsrGraph.copy_model((1 << 14) + 3, deg, seed=5)  # a partial last block of rows
     x = x_uniform(g.n, 3)
     want = oracle_csr(g).matvec(x, 8)
     ro = torch.from_numpy(g.row_offsets.astype(np.int64)).cuda()
@@ -235,3 +235,7 @@ def test_csr_baseline_matches_oracle(cuda, deg):
     y = P.csr_matvec_device(ro, co, torch.from_numpy(x).cuda()).cpu().numpy()
     assert max_rel_err(y, want) <= F64_TOL
     assert np.all(y[want == 0] == 0)
+    e = P.csr_matvec_device(torch.zeros(1, dtype=torch.int64, device="cuda"),
+                            torch.zeros(0, dtype=torch.int32, device="cuda"),
+                            torch.zeros(0, dtype=torch.float64, device="cuda"))
+    assert e.numel() == 0  # n = 0
