@@ -81,7 +81,10 @@ __host__ __device__ inline BvsSmem bvs_smem_layout(const BvdDims& d, uint32_t xs
 struct GatherShape {
   uint32_t W, B, T;
 };
-constexpr GatherShape kGatherDefault{1536, 1024, 256};
+#ifndef CMVG_DEFAULT_W  // build-time override for A/B experiments
+#define CMVG_DEFAULT_W 1536
+#endif
+constexpr GatherShape kGatherDefault{CMVG_DEFAULT_W, 1024, 256};
 
 __device__ __forceinline__ uint32_t ticket_issue(int* counter) {
   return (threadIdx.x & 31u) == 0 ? (uint32_t)atomicAdd(counter, 1) : 0u;
