@@ -312,6 +312,7 @@ int cmvg_create(const cmvg_bvstream* s, const cmvg_create_opts* opts_in, cmvg_gr
       sw.resize(sw.size() + 2 * kBvsGuardWords, 0);
       g->swords.upload(sw.data(), sw.size());
       g->sblocks.upload(sbl.data(), sbl.size());
+      g->hpart.alloc(std::max<uint64_t>(1, L.sstats.heavy_chunks) * 16);
       g->s_stream_bytes = (s1 - s0) * 4;
       {  // read set: the blocks' x-windows and their out-of-window columns (bitmap, O(n))
         std::vector<uint64_t> bm(((uint64_t)bs.n + 63) / 64, 0);

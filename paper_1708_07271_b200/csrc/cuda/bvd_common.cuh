@@ -21,6 +21,7 @@ struct BvdDev {
   uint32_t nlaunch;           // blocks of this launch (`blocks` is offset to its first)
   uint32_t ahead;             // L2 prefetch distance in blocks (resident CTAs of the launch; 0 = none)
   uint32_t pad_[3];
+  double2* hpart;             // heavy-row work-item partial sums (BV-S), indexed by the global item number
 };
 
 __host__ __device__ inline uint32_t align16(uint32_t v) { return (v + 15u) & ~15u; }

@@ -93,54 +93,73 @@ __device__ __forceinline__ uint32_t ticket_take(uint32_t t) { return __shfl_sync
 
 enum BvsMisc : int { kBvsHeavyCtr = 0, kBvsSliceCtr = 1 };
 
-// Heavy rows: one warp per row, lanes stride over the row's fixed-width codes.
+// Heavy rows (more than 32 units): their points are cut into work items of
+// kBvsHeavyChunk codes (the transcoder numbers them per block, header word 3
+// and heavy-table word 5), taken by any warp through a ticket, lanes striding
+// over the item's fixed-width codes; item 0 of a row also sums the row's
+// intervals (in-window ones O(1) by their lane, the others by the whole warp,
+// coalesced).  Each item's warp-reduced double-double sum goes to its slot in
+// g.hpart; bvs_heavy_finish combines a row's items in item order after the
+// decode barrier, so a hub row is spread over the CTA and the result does not
+// depend on which warp took which item.
 template <class S, class XW>
 __device__ __forceinline__ void bvs_heavy(const S& src, const XW& xw, int32_t r0, uint32_t lmin, int* misc,
-                                          RowRec* s_rows) {
+                                          double2* hpart) {
   const uint32_t lane = threadIdx.x & 31u;
-  const uint32_t nh = src.w(0) >> 16, htab = src.w(1), hbase = src.w(2) * 32u;
+  const uint32_t nh = src.w(0) >> 16;
+  if (!nh) return;
+  const uint32_t htab = src.w(1), hbase = src.w(2) * 32u, ibase = src.w(3);
+  const uint32_t el = htab + (nh - 1u) * kBvsHeavyEntry;
+  const uint32_t nitems = src.w(el + 5) + heavy_chunks(src.w(el + 1) + src.w(el + 2));
   for (;;) {
-    const uint32_t q = ticket_take(ticket_issue(&misc[kBvsHeavyCtr]));
-    if (q >= nh) break;
-    const uint32_t e = htab + q * kBvsHeavyEntry;
+    const uint32_t item = ticket_take(ticket_issue(&misc[kBvsHeavyCtr]));
+    if (item >= nitems) break;
+    uint32_t lo_q = 0, hi_q = nh - 1u;  // the row: last entry whose first item <= item
+    while (lo_q < hi_q) {
+      const uint32_t mid = (lo_q + hi_q + 1u) >> 1;
+      if (src.w(htab + mid * kBvsHeavyEntry + 5) <= item) lo_q = mid;
+      else hi_q = mid - 1u;
+    }
+    const uint32_t e = htab + lo_q * kBvsHeavyEntry;
     const uint32_t sa = src.w(e), nm = src.w(e + 1), ns = src.w(e + 2), ni = src.w(e + 3);
-    const uint32_t off0 = hbase + src.w(e + 4);
+    const uint32_t off0 = hbase + src.w(e + 4), j = item - src.w(e + 5);
     const uint32_t k = sa_k(sa), wp = sa_wp(sa), wl = sa_wl(sa);
     const int32_t ib = r0 + (int32_t)k - (int32_t)code_bias(wp);
     const uint32_t np = nm + ns;
     double acc = 0.0, comp = 0.0;
-    for (uint32_t t = lane; t < np; t += 32) {
+    const uint32_t t1 = min(np, (j + 1u) * kBvsHeavyChunk);
+    for (uint32_t t = j * kBvsHeavyChunk + lane; t < t1; t += 32) {
       const double xv = xw.at(ib + (int32_t)extract_bits(src, off0 + t * wp, wp));
       tsum(acc, comp, t < nm ? -xv : xv);
     }
-    // intervals: in-window ones O(1) by their lane; the others (long runs
-    // reaching outside the window) summed by the whole warp, coalesced
-    const uint32_t ioff = off0 + np * wp;
-    for (uint32_t tb = 0; tb < ni; tb += 32) {
-      const uint32_t t = tb + lane;
-      const bool on = t < ni;
-      int32_t left = 0;
-      uint32_t len = 0;
-      if (on) {
-        const uint32_t o = ioff + t * (wp + wl);
-        left = ib + (int32_t)extract_bits(src, o, wp);
-        len = extract_bits(src, o + wp, wl) + lmin;
-      }
-      const uint32_t a = (uint32_t)(left - (int32_t)xw.wlo);
-      const bool nearw = on && a < xw.W && a + len <= xw.W;
-      if (nearw) {
-        double lo;
-        const double hi = xw.isum_near(a, len, lo);
-        tsum(acc, comp, hi);
-        comp += lo;
-      }
-      uint32_t m = __ballot_sync(0xffffffffu, on && !nearw);
-      while (m) {
-        const int sl = __ffs(m) - 1;
-        m &= m - 1u;
-        const int32_t L = __shfl_sync(0xffffffffu, left, sl);
-        const uint32_t N = __shfl_sync(0xffffffffu, len, sl);
-        for (uint32_t e = lane; e < N; e += 32) tsum(acc, comp, xw.at(L + (int32_t)e));
+    if (j == 0) {
+      const uint32_t ioff = off0 + np * wp;
+      for (uint32_t tb = 0; tb < ni; tb += 32) {
+        const uint32_t t = tb + lane;
+        const bool on = t < ni;
+        int32_t left = 0;
+        uint32_t len = 0;
+        if (on) {
+          const uint32_t o = ioff + t * (wp + wl);
+          left = ib + (int32_t)extract_bits(src, o, wp);
+          len = extract_bits(src, o + wp, wl) + lmin;
+        }
+        const uint32_t a = (uint32_t)(left - (int32_t)xw.wlo);
+        const bool nearw = on && a < xw.W && a + len <= xw.W;
+        if (nearw) {
+          double lo;
+          const double hi = xw.isum_near(a, len, lo);
+          tsum(acc, comp, hi);
+          comp += lo;
+        }
+        uint32_t m = __ballot_sync(0xffffffffu, on && !nearw);
+        while (m) {
+          const int sl = __ffs(m) - 1;
+          m &= m - 1u;
+          const int32_t L = __shfl_sync(0xffffffffu, left, sl);
+          const uint32_t N = __shfl_sync(0xffffffffu, len, sl);
+          for (uint32_t e2 = lane; e2 < N; e2 += 32) tsum(acc, comp, xw.at(L + (int32_t)e2));
+        }
       }
     }
     double hi = acc + comp, lo = comp - (hi - acc);
@@ -149,8 +168,30 @@ __device__ __forceinline__ void bvs_heavy(const S& src, const XW& xw, int32_t r0
       const double uh = __shfl_down_sync(0xffffffffu, hi, o), ul = __shfl_down_sync(0xffffffffu, lo, o);
       dd_add(hi, lo, uh, ul);
     }
-    if (lane == 0) put_row(s_rows, k, hi, lo, sa_r(sa));
+    if (lane == 0) hpart[ibase + item] = make_double2(hi, lo);
   }
+}
+
+// After the decode barrier: each heavy row's items, combined in item order
+// (one thread per heavy row), become the row's record.  Block-uniform: only
+// blocks with heavy rows take the extra barrier.
+template <class S>
+__device__ __forceinline__ void bvs_heavy_finish(const S& src, const double2* hpart, RowRec* s_rows, uint32_t T) {
+  const uint32_t nh = src.w(0) >> 16;
+  if (!nh) return;
+  const uint32_t htab = src.w(1), ibase = src.w(3);
+  for (uint32_t q = threadIdx.x; q < nh; q += T) {
+    const uint32_t e = htab + q * kBvsHeavyEntry;
+    const uint32_t sa = src.w(e), i0 = ibase + src.w(e + 5);
+    const uint32_t nit = heavy_chunks(src.w(e + 1) + src.w(e + 2));
+    double hi = 0.0, lo = 0.0;
+    for (uint32_t i = 0; i < nit; ++i) {
+      const double2 v = hpart[i0 + i];
+      dd_add(hi, lo, v.x, v.y);
+    }
+    put_row(s_rows, sa_k(sa), hi, lo, sa_r(sa));
+  }
+  __syncthreads();
 }
 
 // +x, or -x for t < nm (minus codes come first): flip the sign bit when t - nm < 0
@@ -403,12 +444,13 @@ __global__ void __launch_bounds__(256, 4) bvs_gather_kernel(BvdDev g, const XT* 
 
   RowRec* s_rows = reinterpret_cast<RowRec*>(smem + L.off_rows);
   const Src<false> src{bs};
-  bvs_heavy(src, xw, (int32_t)r0, D.min_interval, misc, s_rows);
+  bvs_heavy(src, xw, (int32_t)r0, D.min_interval, misc, g.hpart);
   if (__ldg(bs) >> 16)  // heavy rows in this block: slices dynamically
     bvs_slices<true>(bs, xw, D.min_interval, misc, s_rows, s_tab, T);
   else
     bvs_slices<false>(bs, xw, D.min_interval, misc, s_rows, s_tab, T);
   __syncthreads();
+  bvs_heavy_finish(src, g.hpart, s_rows, T);
   if (threadIdx.x == 32 && ahead) {
     cp_async_wait_all();
     const uint64_t wo = s_pref->word_offset;

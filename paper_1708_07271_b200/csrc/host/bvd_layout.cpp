@@ -324,6 +324,7 @@ void emit_bvs(const RowParts* rps, const RowMeta* meta, const BitWriter& body, u
   }
   so[1] = (uint32_t)so.size();
   BitWriter hs;
+  uint32_t items = 0;
   for (uint32_t k : hrows) {
     const RowMeta& m = meta[k];
     so.push_back(make_sa(k, m.r, m.wp, m.wl, m.far));
@@ -331,7 +332,8 @@ void emit_bvs(const RowParts* rps, const RowMeta* meta, const BitWriter& body, u
     so.push_back(m.ns);
     so.push_back(m.ni);
     so.push_back((uint32_t)hs.nbits);
-    so.push_back(0u);
+    so.push_back(items);
+    items += heavy_chunks(m.nm + m.ns);
     for (uint64_t p = m.bit0, e = m.bit0 + m.nbits; p < e; p += 32) {
       const uint32_t take = (uint32_t)std::min<uint64_t>(32, e - p);
       hs.put(bits32(body.words, p, e) >> (32 - take), (int)take);
@@ -342,6 +344,7 @@ void emit_bvs(const RowParts* rps, const RowMeta* meta, const BitWriter& body, u
   while (so.size() % 4) so.push_back(0u);
   st.slices += nsl;
   st.heavy_rows += nh;
+  st.heavy_chunks += items;
 }
 
 // BV-T block stream (layout.hpp): A's differential contributions of the block
@@ -747,10 +750,15 @@ BvdLayout build_bvd(const BvDecoded& dec, const BvParams& bp, const BvdOptions& 
   L.sblocks = L.blocks;
   uint64_t soff = 0;
   std::vector<uint32_t> ssz(nb);
+  uint64_t hitems = 0;
   for (uint32_t b = 0; b < nb; ++b) {
     L.sblocks[b].word_offset = soff;
     L.sblocks[b].nwords = (uint32_t)sstream[b].size();
     L.sblocks[b].nesc = 0;
+    if (hitems > 0xffffffffull) throw std::runtime_error("BV-S: too many heavy-row work items");
+    sstream[b][3] = (uint32_t)hitems;  // the block's first heavy work item (global)
+    hitems += bst[b].heavy_chunks;
+    L.sstats.heavy_chunks += bst[b].heavy_chunks;
     soff += sstream[b].size();
     ssz[b] = (uint32_t)sstream[b].size();
     L.sstats.max_block_words = std::max(L.sstats.max_block_words, ssz[b]);

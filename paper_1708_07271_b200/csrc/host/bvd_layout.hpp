@@ -25,6 +25,7 @@ struct BvsStats {
   uint32_t max_block_words = 0;
   uint32_t p995_block_words = 0;
   uint64_t slices = 0, heavy_rows = 0;
+  uint64_t heavy_chunks = 0;                      // work items of the heavy rows (kBvsHeavyChunk points each)
   uint64_t lane_words = 0, lane_words_used = 0;  // slice body words incl. / excl. padding
   uint64_t lane_iters = 0, lane_iters_used = 0;  // slice decode iterations x 32 / useful lane iterations
 };

@@ -93,7 +93,8 @@ __host__ __device__ constexpr uint32_t make_hdr(uint32_t r, uint32_t nm, uint32_
 //     stream (BV-D codes).
 // Block stream (u32 words):
 //   [0] nslices | nheavy << 16   [1] heavy table offset   [2] heavy stream offset
-//   [3] 0   [4, 9) u16 start of warp w's slices in the table (w < 8), then
+//   [3] the block's first heavy-row work item (global numbering: the
+//   partial-sum slot of its chunk 0)   [4, 9) u16 start of warp w's slices in the table (w < 8), then
 //   the table size: the static warp schedule (longest-processing-time
 //   assignment by an instruction estimate; warp w decodes entries
 //   [start_w, start_{w+1}))   [9] 0
@@ -104,7 +105,10 @@ __host__ __device__ constexpr uint32_t make_hdr(uint32_t r, uint32_t nm, uint32_
 //     header: valid << 31 | primary << 30 | k << 20 | r << 17 |
 //             #minus << 12 | #points << 7 | #intervals << 4
 //   heavy table: kBvsHeavyEntry words per heavy row: BV-D-style a-word
-//     (make_sa), #minus, #residual, #interval, bit offset in the heavy stream, 0
+//     (make_sa), #minus, #residual, #interval, bit offset in the heavy stream,
+//     first work item of the row within the block (a heavy row's points are
+//     cut into heavy_chunks(#points) items of kBvsHeavyChunk, decoded by any
+//     warp; their partial sums are combined in item order)
 //   heavy stream: the heavy rows' BV-D bodies, bit-packed, MSB first
 #ifndef CMVG_UNIT_PTS  // build-time override for A/B experiments (<= 31: the 5-bit count fields)
 #define CMVG_UNIT_PTS 16
@@ -113,6 +117,10 @@ constexpr uint32_t kBvsUnitPts = CMVG_UNIT_PTS;
 constexpr uint32_t kBvsUnitInts = 2;
 constexpr uint32_t kBvsMaxUnits = 32;  // more -> heavy row
 constexpr uint32_t kBvsHeavyEntry = 6;
+constexpr uint32_t kBvsHeavyChunk = 512;  // points per work item of a heavy row (16 per lane)
+__host__ __device__ constexpr uint32_t heavy_chunks(uint32_t np) {
+  return np > kBvsHeavyChunk ? (np + kBvsHeavyChunk - 1) / kBvsHeavyChunk : 1u;
+}
 constexpr uint32_t kBvsWarps = 8;     // warps of the gather CTA the static schedule is built for
 constexpr uint32_t kBvsWarpTab = 4;   // header words [4, 9): u16 slice-table start per warp, + end
 constexpr uint32_t kBvsHead = 10;

@@ -146,8 +146,8 @@ struct cmvg_graph {
   uint32_t threads = 128;  // threads per CTA
   // BV-D layout (this shard): scatter, matmat
   DevBuf words, blocks;
-  // BV-S layout (this shard): gather, PageRank
-  DevBuf swords, sblocks;
+  // BV-S layout (this shard): gather, PageRank; heavy-row partial sums (whole graph's items)
+  DevBuf swords, sblocks, hpart;
   uint64_t s_stream_bytes = 0;
   // BV-T layout (this shard): scatter; combine tables (whole graph)
   DevBuf twords, tblocks, tile_ptr, tile_blk, farp_ptr, farp;
@@ -180,7 +180,7 @@ struct cmvg_graph {
   // scratch (scatter / pagerank)
   DevBuf scratch;
   uint64_t device_bytes() const {
-    return words.bytes + blocks.bytes + swords.bytes + sblocks.bytes + twords.bytes + tblocks.bytes + tile_ptr.bytes +
+    return words.bytes + blocks.bytes + swords.bytes + sblocks.bytes + hpart.bytes + twords.bytes + tblocks.bytes + tile_ptr.bytes +
            tile_blk.bytes + farp_ptr.bytes + farp.bytes + bv_words.bytes + bv_seg.bytes;
   }
   BvdDev dev() const {
@@ -205,6 +205,7 @@ struct cmvg_graph {
     BvdDev d = dev();
     d.words = swords.as<uint32_t>();
     d.blocks = sblocks.as<BvdBlockInfo>();
+    d.hpart = hpart.as<double2>();
     d.stream_cap_words = 0;  // BV-S is read from global memory (L2-prefetched)
     return d;
   }

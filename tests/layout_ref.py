@@ -99,6 +99,7 @@ def decode_sliced(words, blocks, n, B, lmin, W):
     lanes, class/far flags consistent, units within their limits)."""
     rows_out = [None] * n
     refs_out = [0] * n
+    heavy_items = 0
     for b in range(len(blocks)):
         woff = int(blocks[b, 0]) | (int(blocks[b, 1]) << 32)
         nw = int(blocks[b, 2])
@@ -108,7 +109,7 @@ def decode_sliced(words, blocks, n, B, lmin, W):
         nr = min(B, n - r0)
         nsl, nh = s[0] & 0xFFFF, s[0] >> 16
         htab, hstr = s[1], s[2]
-        assert s[3] == 0
+        assert s[3] == heavy_items  # the block's first heavy work item (global numbering)
         # static warp schedule: u16 table starts of the 8 warps, then the table size
         starts = [(s[4 + q // 2] >> (16 * (q % 2))) & 0xFFFF for q in range(9)]
         assert starts[0] == 0 and starts[8] == nsl and all(a <= b for a, b in zip(starts, starts[1:]))
@@ -116,9 +117,12 @@ def decode_sliced(words, blocks, n, B, lmin, W):
 
         def inwin(c):
             return wlo <= c < wlo + W
+        item0 = 0
         for q in range(nh):
             e = htab + 6 * q
             sa, nm, ns, ni, boff = s[e], s[e + 1], s[e + 2], s[e + 3], s[e + 4]
+            assert s[e + 5] == item0
+            item0 += max(1, -(-(nm + ns) // 512))
             k, r, wp, wl = sa & 4095, (sa >> 12) & 7, (sa >> 15) & 31, (sa >> 20) & 31
             off = hstr * 32 + boff
             ib = r0 + k - bias(wp)
@@ -132,6 +136,7 @@ def decode_sliced(words, blocks, n, B, lmin, W):
                 off += wp + wl
             assert k not in parts
             parts[k] = dict(minus=pts[:nm], res=pts[nm:], ints=ints, r=r)
+        heavy_items += item0
         for sl in range(nsl):
             rec = s[10 + 2 * sl]
             meta = s[rec]

@@ -239,3 +239,26 @@ def test_csr_baseline_matches_oracle(cuda, deg):
                             torch.zeros(0, dtype=torch.int32, device="cuda"),
                             torch.zeros(0, dtype=torch.float64, device="cuda"))
     assert e.numel() == 0  # n = 0
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_gather_hub_rows_split_into_items(cuda, dtype):
+    """Rows far beyond 32 units are cut into 512-point work items taken by any
+    warp and combined in item order (bvs_heavy / bvs_heavy_finish): hub rows of
+    several items, with intervals and a reference, plus ordinary rows."""
+    rng = np.random.default_rng(21)
+    n = 6000
+    rows = []
+    for i in range(n):
+        if i % 997 == 5:  # hub: thousands of random columns plus a run (interval)
+            cols = set(rng.choice(n, size=int(rng.integers(1500, 4000)), replace=False).tolist())
+            cols.update(range(100, 140))
+        elif i % 997 == 6:  # references the hub above (copy with deletions)
+            cols = set(c for c in rows[i - 1] if rng.random() < 0.7)
+        else:
+            cols = set((i + rng.geometric(1 / 40, size=int(rng.integers(0, 25)))) % n)
+        rows.append(sorted(cols))
+    g = csr_from_rows(rows)
+    dg, s, _, _ = check_gather(g, bv_params(2), dtype=dtype)
+    assert dg.info()["bvs_heavy_rows"] >= 6  # the hubs take the work-item path
+    check_gather(g, bv_params(2), dtype=dtype, device=True)
