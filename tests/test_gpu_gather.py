@@ -262,3 +262,18 @@ def test_gather_hub_rows_split_into_items(cuda, dtype):
     dg, s, _, _ = check_gather(g, bv_params(2), dtype=dtype)
     assert dg.info()["bvs_heavy_rows"] >= 6  # the hubs take the work-item path
     check_gather(g, bv_params(2), dtype=dtype, device=True)
+
+
+def test_gather_from_loaded_container(cuda, tmp_path):
+    """A BV stream written to and read back from a CBV1 container drives the
+    device handle exactly like the encoder's stream."""
+    g = P.CsrGraph.copy_model(1 << 13, 12.0, seed=31)
+    s = P.BvStream.encode(g, P.BvParams())
+    p = tmp_path / "g.cbv"
+    s.save(str(p))
+    t = P.BvStream.load(str(p))
+    x = x_uniform(g.n, 9)
+    y0 = P.BvGraph(s).matvec(x)
+    y1 = P.BvGraph(t).matvec(x)
+    assert np.array_equal(y0, y1)
+    assert max_rel_err(y1, oracle_csr(g).matvec(x, 8)) <= F64_TOL
