@@ -397,7 +397,10 @@ __device__ __forceinline__ void bvs_slices(const uint32_t* __restrict__ bs, cons
 }
 
 template <typename XT, typename YT, bool PR = false, uint32_t CW = 0, uint32_t CB = 0, uint32_t CT = 0>
-__global__ void __launch_bounds__(256, 4) bvs_gather_kernel(BvdDev g, const XT* __restrict__ x, const XT* xfar,
+#ifndef CMVG_GATHER_MINB  // CTAs per SM the register budget is sized for (build-time A/B)
+#define CMVG_GATHER_MINB 4
+#endif
+__global__ void __launch_bounds__(256, CMVG_GATHER_MINB) bvs_gather_kernel(BvdDev g, const XT* __restrict__ x, const XT* xfar,
                                                              YT* __restrict__ y, PrArgs pr) {
   extern __shared__ __align__(16) unsigned char smem[];
   const BvdDims& D = g.d;
