@@ -312,7 +312,7 @@ int cmvg_create(const cmvg_bvstream* s, const cmvg_create_opts* opts_in, cmvg_gr
       sw.resize(sw.size() + 2 * kBvsGuardWords, 0);
       g->swords.upload(sw.data(), sw.size());
       g->sblocks.upload(sbl.data(), sbl.size());
-      g->hpart.alloc(std::max<uint64_t>(1, L.sstats.heavy_chunks) * 16);
+      g->heavy_items = L.sstats.heavy_chunks;
       g->s_stream_bytes = (s1 - s0) * 4;
       {  // read set: the blocks' x-windows and their out-of-window columns (bitmap, O(n))
         std::vector<uint64_t> bm(((uint64_t)bs.n + 63) / 64, 0);
@@ -535,6 +535,8 @@ void launch_gather(cmvg_graph* g, const XT* x, YT* y, cudaStream_t st, const XT*
   d.block_begin += b0;
   d.nlaunch = b1 - b0;
   d.ahead = resident_ctas(kern, (int)g->threads, L.total, g->device, g->gather_res[sizeof(XT) == 8 ? 0 : 1]);
+  HeavyScratch hs(g, st);
+  d.hpart = hs.get();
   kern<<<b1 - b0, g->threads, L.total, st>>>(d, x, xfar ? xfar : x, y, PrArgs{});
   CUDA_TRY(cudaGetLastError());
 }

@@ -146,8 +146,9 @@ struct cmvg_graph {
   uint32_t threads = 128;  // threads per CTA
   // BV-D layout (this shard): scatter, matmat
   DevBuf words, blocks;
-  // BV-S layout (this shard): gather, PageRank; heavy-row partial sums (whole graph's items)
-  DevBuf swords, sblocks, hpart;
+  // BV-S layout (this shard): gather, PageRank
+  DevBuf swords, sblocks;
+  uint64_t heavy_items = 0;  // heavy-row work items of the whole graph (partial-sum slots per launch)
   uint64_t s_stream_bytes = 0;
   // BV-T layout (this shard): scatter; combine tables (whole graph)
   DevBuf twords, tblocks, tile_ptr, tile_blk, farp_ptr, farp;
@@ -180,7 +181,7 @@ struct cmvg_graph {
   // scratch (scatter / pagerank)
   DevBuf scratch;
   uint64_t device_bytes() const {
-    return words.bytes + blocks.bytes + swords.bytes + sblocks.bytes + hpart.bytes + twords.bytes + tblocks.bytes + tile_ptr.bytes +
+    return words.bytes + blocks.bytes + swords.bytes + sblocks.bytes + twords.bytes + tblocks.bytes + tile_ptr.bytes +
            tile_blk.bytes + farp_ptr.bytes + farp.bytes + bv_words.bytes + bv_seg.bytes;
   }
   BvdDev dev() const {
@@ -205,7 +206,6 @@ struct cmvg_graph {
     BvdDev d = dev();
     d.words = swords.as<uint32_t>();
     d.blocks = sblocks.as<BvdBlockInfo>();
-    d.hpart = hpart.as<double2>();
     d.stream_cap_words = 0;  // BV-S is read from global memory (L2-prefetched)
     return d;
   }
@@ -229,6 +229,34 @@ inline uint32_t resident_ctas(K kern, int threads, size_t smem, int device, std:
   }
   return c & 0x7fffffffu;
 }
+
+// Stream-ordered scratch for one gather launch's heavy-row partial sums
+// (cudaMallocAsync from the device's pool, freed on the same stream after the
+// launch): each launch has its own slots, so concurrent products on distinct
+// streams never share them, and a captured CUDA graph gets memory nodes.
+// No-op for layouts without heavy rows.
+struct HeavyScratch {
+  void* p = nullptr;
+  cudaStream_t st = nullptr;
+  HeavyScratch(const cmvg_graph* g, cudaStream_t s) : st(s) {
+    if (!g->heavy_items) return;
+    static std::atomic<bool> pool_kept{false};  // keep freed blocks in the pool (no OS round trip per launch)
+    if (!pool_kept.exchange(true)) {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, g->device) == cudaSuccess) {
+        uint64_t keep = ~0ull;
+        (void)cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+    }
+    CUDA_TRY(cudaMallocAsync(&p, g->heavy_items * 16, st));
+  }
+  double2* get() const { return static_cast<double2*>(p); }
+  ~HeavyScratch() {
+    if (p) (void)cudaFreeAsync(p, st);
+  }
+  HeavyScratch(const HeavyScratch&) = delete;
+  HeavyScratch& operator=(const HeavyScratch&) = delete;
+};
 
 // kernel entry points implemented in the other translation units
 template <typename T>

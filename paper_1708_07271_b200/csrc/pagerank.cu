@@ -67,6 +67,8 @@ void launch_pr_step(cmvg_graph* g, const double* q, PrArgs pr, double* p_next, c
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
   BvdDev d = g->sdev();
   d.ahead = resident_ctas(kern, (int)g->threads, L.total, g->device, g->gather_res[2]);
+  HeavyScratch hs(g, st);
+  d.hpart = hs.get();
   kern<<<g->nblocks, g->threads, L.total, st>>>(d, q, q, p_next, pr);
   CUDA_TRY(cudaGetLastError());
 }

@@ -267,3 +267,16 @@ def test_pagerank_equivalence_check(cuda):
     assert 0 < c.rows_self_coded < g.n and 1 <= c.max_chain <= 3
     eq2 = P.pagerank_equivalence_check(g, P.PageRankConfig(iterations=200, l1_tolerance=1e-10), window=3)
     assert eq2.iterations_run < 200 and eq2.linf <= 1e-13
+
+
+def test_pagerank_hub_rows_graph_capture(cuda):
+    """PageRank on A^T of a power-law graph: hub rows (popular targets) take the
+    heavy work-item path, whose stream-ordered scratch is captured into the
+    device loop's CUDA graph; results match the oracle."""
+    h = P.CsrGraph.social(1 << 15, seed=78)  # A^T: its hub rows are A's popular targets
+    g = h.transpose()  # A
+    dg = P.BvGraph(P.BvStream.encode(h, P.BvParams(max_ref=0)))
+    assert dg.info()["bvs_heavy_rows"] > 0
+    p, it = dg.pagerank(g.out_degrees(), alpha=0.15, iterations=30)
+    want, _ = oracle_pr(g, alpha=0.15, iterations=30, dangling="uniform")
+    assert it == 30 and rel(p, want) <= 1e-12
