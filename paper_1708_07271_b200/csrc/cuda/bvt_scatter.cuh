@@ -171,26 +171,57 @@ __global__ void __launch_bounds__(256, 4) bvt_scatter_kernel(BvdDev g, const XT*
   }
   __syncthreads();
   {  // the transcoder's schedule: per level (deepest first) the rows with
-     // children; each pulls its children's c in increasing distance
+     // children; each pulls its children's c in increasing distance.  Common
+     // case (<= 4 levels, <= 2 entries per thread and level): the level
+     // bounds and every entry this thread will use are loaded up front in two
+     // rounds of independent loads, so the level barriers wait on shared
+     // memory only, not on a chain of 2 x levels global-load round trips.
     const uint32_t* cs = bs + __ldg(bs + 4);
-    const uint32_t nlev = __ldg(cs);
+    constexpr uint32_t kLv = 4, kPer = 2;
+    uint32_t lvs[kLv + 2];
+#pragma unroll
+    for (uint32_t l = 0; l < kLv + 2; ++l) lvs[l] = __ldg(cs + l);  // nlev, then level starts (stream words)
+    const uint32_t nlev = lvs[0];
     const uint32_t* ent = cs + nlev + 2;
-    for (uint32_t lv = 0; lv < nlev; ++lv) {
-      const uint32_t e0 = __ldg(cs + 1 + lv), e1 = __ldg(cs + 2 + lv);
-      for (uint32_t i = e0 + tid; i < e1; i += T) {
-        const uint32_t e = __ldg(ent + i);
-        const uint32_t k = e & 1023u;
-        uint32_t m = e >> 10;
-        double h = ch[k], l = (double)cl[k];
-        while (m) {
-          const uint32_t r = (uint32_t)__ffs(m);
-          m &= m - 1u;
-          dd_add(h, l, ch[k + r], (double)cl[k + r]);
-        }
-        ch[k] = h;
-        cl[k] = (float)l;
+    auto pull = [&](uint32_t e) {
+      const uint32_t k = e & 1023u;
+      uint32_t m = e >> 10;
+      double h = ch[k], l = (double)cl[k];
+      while (m) {
+        const uint32_t r = (uint32_t)__ffs(m);
+        m &= m - 1u;
+        dd_add(h, l, ch[k + r], (double)cl[k + r]);
       }
-      __syncthreads();
+      ch[k] = h;
+      cl[k] = (float)l;
+    };
+    bool fast = nlev <= kLv;
+#pragma unroll
+    for (uint32_t l = 0; l < kLv; ++l)
+      if (l < nlev && lvs[l + 2] - lvs[l + 1] > kPer * T) fast = false;
+    if (fast) {
+      uint32_t pre[kLv][kPer];
+#pragma unroll
+      for (uint32_t l = 0; l < kLv; ++l)
+#pragma unroll
+        for (uint32_t j = 0; j < kPer; ++j) {
+          const uint32_t i = lvs[l + 1] + tid + j * T;
+          pre[l][j] = (l < nlev && i < lvs[l + 2]) ? __ldg(ent + i) : 0xffffffffu;
+        }
+#pragma unroll
+      for (uint32_t l = 0; l < kLv; ++l) {
+        if (l >= nlev) break;  // block-uniform
+#pragma unroll
+        for (uint32_t j = 0; j < kPer; ++j)
+          if (pre[l][j] != 0xffffffffu) pull(pre[l][j]);
+        __syncthreads();
+      }
+    } else {
+      for (uint32_t lv = 0; lv < nlev; ++lv) {
+        const uint32_t e0 = __ldg(cs + 1 + lv), e1 = __ldg(cs + 2 + lv);
+        for (uint32_t i = e0 + tid; i < e1; i += T) pull(__ldg(ent + i));
+        __syncthreads();
+      }
     }
   }
 
