@@ -147,8 +147,10 @@ __global__ void __launch_bounds__(256, 4) bvt_scatter_kernel(BvdDev g, const XT*
   const uint32_t h0 = __ldg(bs);
   const uint32_t nsl = h0 & 0xffffu, nh = h0 >> 16;
   uint32_t* s_tab = reinterpret_cast<uint32_t*>(misc + 48);  // slice table (offset, meta), when it fits
-  if (nsl <= kBvtSliceTab)
-    for (uint32_t i = tid; i < 2 * nsl; i += T) s_tab[i] = __ldg(bs + kBvtHead + i);
+  // staged without waiting for the slice count (bounded by the block's stream
+  // length); used only when nsl <= kBvtSliceTab
+  for (uint32_t i = tid; i < 2 * kBvtSliceTab; i += T)
+    if (kBvtHead + i < bi.nwords) s_tab[i] = __ldg(bs + kBvtHead + i);
   for (uint32_t j = tid; j < W2; j += T) {
     s_oh[j] = 0.0;
     s_ol[j] = 0.0f;
