@@ -181,7 +181,8 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": g.m / v * 1e3 * cores,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "impl": "reference",
-        "config": {"workload": "C2 copy-model n=2^24 deg20 y=A·x^T fp64 (BASELINE.json configs[1])",
+        "config": {"workload": f"C2 copy-model n=2^{args.n_log2} deg{args.degree:g} y=A·x^T fp64 "
+                               f"(BASELINE.json configs[1])",
                    "n": g.n, "m": g.m, "reference_format": "compress(g,7) A' (ref_matrix.hpp:69)"},
         "cpu_baseline": {"value": gv, "unit": "Gedges/s", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": gv, "unit": "Gedges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
