@@ -121,6 +121,9 @@ typedef struct {
   uint64_t bvs_lane_iters, bvs_lane_iters_used; /* slice decode lane-iterations incl. / excl. idle lanes */
   /* BV-T (target-sorted layout of the scatter form) */
   uint64_t bvt_stream_bytes, bvt_entries, bvt_far_slots, bvt_heavy_targets, bvt_slices;
+  /* BV-F (flat term stream of the gather / PageRank kernels) */
+  uint64_t bvf_stream_bytes, bvf_terms, bvf_pad_terms, bvf_slot_terms, bvf_esc_terms, bvf_esc_blocks;
+  uint32_t bvf_max_K, bvf_min_cbits;
 } cmvg_graph_info;
 
 /* ---- errors -------------------------------------------------------------- */
@@ -180,6 +183,9 @@ const uint32_t* cmvg_layout_swords(const cmvg_layout* l, uint64_t* nwords);
 const uint32_t* cmvg_layout_sblocks(const cmvg_layout* l, uint32_t* nblocks);
 /* BV-T words / block table */
 const uint32_t* cmvg_layout_twords(const cmvg_layout* l, uint64_t* nwords);
+/* BV-F words / block table (8 u32 per block: BvfBlockInfo, host/layout.hpp) */
+const uint32_t* cmvg_layout_fwords(const cmvg_layout* l, uint64_t* nwords);
+const uint32_t* cmvg_layout_fblocks(const cmvg_layout* l, uint32_t* nblocks);
 const uint32_t* cmvg_layout_tblocks(const cmvg_layout* l, uint32_t* nblocks);
 const uint32_t* cmvg_layout_blocks(const cmvg_layout* l, uint32_t* nblocks);
 void cmvg_layout_free(cmvg_layout* l);

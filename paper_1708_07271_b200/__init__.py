@@ -94,7 +94,10 @@ class _InfoC(C.Structure):
                 ("bvs_slices", C.c_uint64), ("bvs_heavy_rows", C.c_uint64), ("bvs_lane_words", C.c_uint64),
                 ("bvs_lane_words_used", C.c_uint64), ("bvs_lane_iters", C.c_uint64),
                 ("bvs_lane_iters_used", C.c_uint64), ("bvt_stream_bytes", C.c_uint64), ("bvt_entries", C.c_uint64),
-                ("bvt_far_slots", C.c_uint64), ("bvt_heavy_targets", C.c_uint64), ("bvt_slices", C.c_uint64)]
+                ("bvt_far_slots", C.c_uint64), ("bvt_heavy_targets", C.c_uint64), ("bvt_slices", C.c_uint64),
+                ("bvf_stream_bytes", C.c_uint64), ("bvf_terms", C.c_uint64), ("bvf_pad_terms", C.c_uint64),
+                ("bvf_slot_terms", C.c_uint64), ("bvf_esc_terms", C.c_uint64), ("bvf_esc_blocks", C.c_uint64),
+                ("bvf_max_K", C.c_uint32), ("bvf_min_cbits", C.c_uint32)]
 
 
 _lib_handle: Optional[C.CDLL] = None
@@ -131,6 +134,8 @@ _SIGS = [
     ("cmvg_layout_sblocks", _P, [_P, C.POINTER(C.c_uint32)]),
     ("cmvg_layout_twords", _P, [_P, C.POINTER(C.c_uint64)]),
     ("cmvg_layout_tblocks", _P, [_P, C.POINTER(C.c_uint32)]),
+    ("cmvg_layout_fwords", _P, [_P, C.POINTER(C.c_uint64)]),
+    ("cmvg_layout_fblocks", _P, [_P, C.POINTER(C.c_uint32)]),
     ("cmvg_layout_free", None, [_P]),
     ("cmvg_graph_info_get", C.c_int, [_P, C.POINTER(_InfoC)]),
     ("cmvg_dimension", C.c_uint32, [_P]),
@@ -370,8 +375,8 @@ class BvStream:
 
     def layout_export(self, options: Optional["CreateOptions"] = None, sliced: bool = False, kind: str = ""):
         """(words u32[], blocks u32[nblocks, 8]) of a device layout built on the
-        host: BV-D (default), BV-S (sliced=True or kind="bvs") or BV-T
-        (kind="bvt")."""
+        host: BV-D (default), BV-S (sliced=True or kind="bvs"), BV-F
+        (kind="bvf") or BV-T (kind="bvt")."""
         kind = kind or ("bvs" if sliced else "bvd")
         oc = (options or CreateOptions())._c()
         h = _P()
@@ -381,6 +386,7 @@ class BvStream:
             nw, nb = C.c_uint64(), C.c_uint32()
             fw, fb = {"bvd": (lib.cmvg_layout_words, lib.cmvg_layout_blocks),
                       "bvs": (lib.cmvg_layout_swords, lib.cmvg_layout_sblocks),
+                      "bvf": (lib.cmvg_layout_fwords, lib.cmvg_layout_fblocks),
                       "bvt": (lib.cmvg_layout_twords, lib.cmvg_layout_tblocks)}[kind]
             w = _np_view(fw(h, C.byref(nw)), nw.value, np.uint32).copy()
             b = _np_view(fb(h, C.byref(nb)), nb.value * 8, np.uint32).reshape(-1, 8).copy()

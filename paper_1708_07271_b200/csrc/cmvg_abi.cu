@@ -218,6 +218,16 @@ static void fill_bvt_info(cmvg_graph_info* o, const BvtStats& t) {
   o->bvt_heavy_targets = t.heavy_targets;
   o->bvt_slices = t.slices;
 }
+static void fill_bvf_info(cmvg_graph_info* o, const BvfStats& f) {
+  o->bvf_stream_bytes = f.stream_bytes;
+  o->bvf_terms = f.terms;
+  o->bvf_pad_terms = f.pad_terms;
+  o->bvf_slot_terms = f.slot_terms;
+  o->bvf_esc_terms = f.esc_terms;
+  o->bvf_esc_blocks = f.esc_blocks;
+  o->bvf_max_K = f.max_K;
+  o->bvf_min_cbits = f.min_cbits;
+}
 static void fill_bvs_info(cmvg_graph_info* o, const BvsStats& st, uint32_t cap) {
   o->bvs_stream_bytes = st.stream_bytes;
   o->bvs_max_block_words = st.max_block_words;
@@ -255,6 +265,7 @@ int cmvg_create(const cmvg_bvstream* s, const cmvg_create_opts* opts_in, cmvg_gr
     require(o.lanes >= 32 && o.lanes <= 256 && (o.lanes & (o.lanes - 1)) == 0,
             "lanes (threads per block) must be a power of two in [32, 256]");
     require(o.block_rows <= 4 * o.lanes, "block_rows must be <= 4 x threads per block");
+    require(o.window <= kBvfXPer * kBvfThreads, "window must be <= 2048 entries");
     require(o.interval_mode <= CMVG_INTERVALS_DIRECT, "bad interval_mode");
     uint32_t row_end = o.row_end ? o.row_end : bs.n;
     require(o.row_begin < row_end && row_end <= bs.n, "bad shard row range");
@@ -356,6 +367,17 @@ int cmvg_create(const cmvg_bvstream* s, const cmvg_create_opts* opts_in, cmvg_gr
       if (L.farp.empty()) L.farp.assign(2, 0u);
       g->farp.upload(L.farp.data(), L.farp.size());
       g->sstats = L.sstats;
+      // BV-F
+      const uint64_t f0 = L.fblocks[g->block_begin].word_offset;
+      const uint64_t f1 = L.fblocks[block_end - 1].word_offset + L.fblocks[block_end - 1].nwords;
+      std::vector<BvfBlockInfo> fbl(L.fblocks.begin() + g->block_begin, L.fblocks.begin() + block_end);
+      for (auto& b : fbl) b.word_offset -= f0;
+      std::vector<uint32_t> fw(L.fwords.begin() + f0, L.fwords.begin() + f1);
+      fw.resize(fw.size() + 64, 0);
+      g->fwords.upload(fw.data(), fw.size());
+      g->fblocks.upload(fbl.data(), fbl.size());
+      g->f_stream_bytes = (f1 - f0) * 4;
+      g->fstats = L.fstats;
     }
     // stats of the shard
     g->stats.stream_bytes = (w1 - w0) * 4;
@@ -406,6 +428,7 @@ int cmvg_layout_info(const cmvg_bvstream* s, const cmvg_create_opts* opts_in, cm
     o->window_coverage = L.stats.window_coverage;
     fill_bvs_info(o, L.sstats, 0);
     fill_bvt_info(o, L.tstats);
+    fill_bvf_info(o, L.fstats);
   });
 }
 
@@ -455,6 +478,16 @@ const uint32_t* cmvg_layout_tblocks(const cmvg_layout* l, uint32_t* nblocks) {
   if (nblocks) *nblocks = (uint32_t)l->L.tblocks.size();
   return reinterpret_cast<const uint32_t*>(l->L.tblocks.data());
 }
+const uint32_t* cmvg_layout_fwords(const cmvg_layout* l, uint64_t* nwords) {
+  if (!l) return nullptr;
+  if (nwords) *nwords = l->L.fwords.size();
+  return l->L.fwords.data();
+}
+const uint32_t* cmvg_layout_fblocks(const cmvg_layout* l, uint32_t* nblocks) {
+  if (!l) return nullptr;
+  if (nblocks) *nblocks = (uint32_t)l->L.fblocks.size();
+  return reinterpret_cast<const uint32_t*>(l->L.fblocks.data());
+}
 void cmvg_layout_free(cmvg_layout* l) { delete l; }
 
 int cmvg_destroy(cmvg_graph* g) {
@@ -495,6 +528,8 @@ int cmvg_graph_info_get(const cmvg_graph* g, cmvg_graph_info* o) {
     o->bvs_stream_bytes = g->s_stream_bytes;
     fill_bvt_info(o, g->tstats);
     o->bvt_stream_bytes = g->t_stream_bytes;
+    fill_bvf_info(o, g->fstats);
+    o->bvf_stream_bytes = g->f_stream_bytes;
   });
 }
 
@@ -516,29 +551,9 @@ uint64_t cmvg_adds_per_product(const cmvg_graph* g) { return g ? g->adds : 0; }
 namespace {
 
 template <typename XT, typename YT>
-void launch_gather(cmvg_graph* g, const XT* x, YT* y, cudaStream_t st, const XT* xfar = nullptr,
-                   uint32_t b0 = 0, uint32_t b1 = 0xffffffffu) {
-  b1 = std::min(b1, g->nblocks);
-  if (b0 >= b1) return;
-  const BvsSmem L = bvs_smem_layout(g->dims, sizeof(XT));
-  const bool dflt = g->dims.window == kGatherDefault.W && g->dims.block_rows == kGatherDefault.B &&
-                    g->threads == kGatherDefault.T;
-  auto kern = dflt ? bvs_gather_kernel<XT, YT, false, kGatherDefault.W, kGatherDefault.B, kGatherDefault.T>
-                   : bvs_gather_kernel<XT, YT>;
-  const unsigned bit = sizeof(XT) == 8 ? 1u : 2u;  // the attribute call is not free: once per handle and type
-  if (!(g->gather_attr & bit)) {
-    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
-    g->gather_attr |= bit;
-  }
-  BvdDev d = g->sdev();
-  d.blocks += b0;  // blocks [b0, b1) of this shard
-  d.block_begin += b0;
-  d.nlaunch = b1 - b0;
-  d.ahead = resident_ctas(kern, (int)g->threads, L.total, g->device, g->gather_res[sizeof(XT) == 8 ? 0 : 1]);
-  HeavyScratch hs(g, st);
-  d.hpart = hs.get();
-  kern<<<b1 - b0, g->threads, L.total, st>>>(d, x, xfar ? xfar : x, y, PrArgs{});
-  CUDA_TRY(cudaGetLastError());
+void launch_gather(cmvg_graph* g, const XT* x, YT* y, cudaStream_t st, const XT* xfar = nullptr, uint32_t b0 = 0,
+                   uint32_t b1 = 0xffffffffu) {
+  launch_bvf<XT, YT, false>(g, x, xfar, y, PrArgs{}, st, b0, b1);
 }
 
 // Mapped device address of a pinned host buffer, or nullptr (pageable memory).
@@ -592,14 +607,18 @@ void gather_host_pipelined(cmvg_graph* g, const T* x, T* y, const T* xmapped) {
     for (auto& e : tev) CUDA_TRY(cudaEventCreate(&e));
     CUDA_TRY(cudaEventRecord(tev[3 * 16], g->s_in));
   }
-  for (uint32_t c = 0; c < C; ++c) {
+  // the last non-empty chunk uploads the rest of x
+  uint32_t last = C - 1;
+  while (last > 0 && cut[last] == cut[last + 1]) --last;
+  try {
+  for (uint32_t c = 0; c <= last; ++c) {
     const uint32_t b0 = cut[c], b1 = cut[c + 1];
-    if (b0 == b1 && c + 1 < C) continue;
+    if (b0 == b1) continue;  // empty chunk (rounding of the chunk weights)
     // x needed by blocks < b1: their windows (prefix max) plus a lookahead
     // that covers most out-of-window columns (512 KB of fp64: ~10 us of
     // PCIe), everything for the last chunk
     constexpr size_t kLookahead = size_t(1) << 16;
-    size_t need = c + 1 == C ? g->n : std::min<size_t>(g->n, g->win_need[b1 - 1] + kLookahead);
+    size_t need = c == last ? g->n : std::min<size_t>(g->n, g->win_need[b1 - 1] + kLookahead);
     if (need > xdone) {
       CUDA_TRY(cudaMemcpyAsync(hx + xdone, x + xdone, (need - xdone) * sizeof(T), cudaMemcpyHostToDevice, g->s_in));
       xdone = need;
@@ -616,9 +635,16 @@ void gather_host_pipelined(cmvg_graph* g, const T* x, T* y, const T* xmapped) {
     CUDA_TRY(cudaEventRecord(g->ev[2 * c + 1], g->s_comp));
     if (trace) CUDA_TRY(cudaEventRecord(tev[3 * c + 1], g->s_comp));
     CUDA_TRY(cudaStreamWaitEvent(g->s_out, g->ev[2 * c + 1], 0));
-    const size_t r0 = (size_t)b0 * B, r1 = std::min(nrows, (size_t)b1 * B);
-    CUDA_TRY(cudaMemcpyAsync(y + r0, hy + r0, (r1 - r0) * sizeof(T), cudaMemcpyDeviceToHost, g->s_out));
+    const size_t r0 = std::min(nrows, (size_t)b0 * B), r1 = std::min(nrows, (size_t)b1 * B);
+    if (r1 > r0) CUDA_TRY(cudaMemcpyAsync(y + r0, hy + r0, (r1 - r0) * sizeof(T), cudaMemcpyDeviceToHost, g->s_out));
     if (trace) CUDA_TRY(cudaEventRecord(tev[3 * c + 2], g->s_out));
+  }
+  } catch (...) {
+    // copies already queued must not outlive the call (they read the caller's buffers)
+    (void)cudaStreamSynchronize(g->s_in);
+    (void)cudaStreamSynchronize(g->s_comp);
+    (void)cudaStreamSynchronize(g->s_out);
+    throw;
   }
   CUDA_TRY(cudaStreamSynchronize(g->s_out));
   if (trace) {

@@ -1,0 +1,553 @@
+// bvf_gather: y = A * x^T on the flat term layout BV-F (host/layout.hpp) -- the
+// gather hot path replacing the reference's sequential `matvec_ref_into`
+// (include/cmv/ref_matvec.hpp:20-31), and
+// (PR = true) the product + update of one PageRank iteration
+// (pagerank.hpp:83-102).
+//
+// One CTA of 256 threads per block of B rows (reference chains never leave a
+// block), 3 CTAs per SM:
+//   1. staging: the x-window x[wlo, wlo + W) and the block's far columns go to
+//      a shared-memory table; each x is split exactly at a block-wide grid
+//      G = 2^(E - cbits) (E: the block's largest exponent) into
+//      h = (x + s) - s, a multiple of G, and l = x - h (both exact), and the
+//      window's exclusive prefix F = (sum h, sum l) is written after it.  Sums
+//      of h are EXACT in fp64 (the transcoder bounds every partial sum below
+//      2^53 G), so the differential evaluation loses nothing to cancellation
+//      in the h part -- the rounding left is that of the small l sums
+//      (|l| <= G/2) -- and reference chains, carries and prefix differences
+//      are plain adds (no TwoSum);
+//   2. terms: thread t sums chunk t of the block's flat term list (K terms,
+//      coalesced word loads straight into registers), +-table[index] split as
+//      above, and stores a row's differential sum when the row's last term
+//      passes -- every thread has the same work whatever the row lengths;
+//   3. a row cut by a chunk boundary gets the preceding chunks' tails (carry);
+//   4. reference chains y_i = delta_i + y_{i-r} (ref_matvec.hpp:23-25) and the
+//      coalesced store or the fused PageRank epilogue.
+#pragma once
+#include <cstdint>
+#include <type_traits>
+
+#include "bvs_gather.cuh"
+
+namespace cmvg {
+
+struct BvfDev {
+  const uint32_t* words;
+  const BvfBlockInfo* blocks;
+  uint32_t n, B, W, max_depth;
+  uint32_t block_begin;  // first block of this launch (global numbering)
+  uint32_t row_begin;    // first row of the shard (y is shard-relative)
+  uint32_t nlaunch;
+  uint32_t ahead;  // L2 prefetch distance in blocks (about the CTAs resident at once; 0 = none)
+};
+
+struct __align__(16) RowD {
+  double hi, lo;
+};
+
+constexpr uint32_t kBvfThreads = 256;
+constexpr uint32_t kBvfXPer = 8;  // window entries per thread (W <= 2048)
+
+struct BvfSmem {
+  uint32_t off_tab, off_flo, off_rows, off_rn, off_misc, total;
+};
+// The x/F table region is dead after the term loop; the pointer-jumping chain
+// reuses it.
+__host__ __device__ inline BvfSmem bvf_smem_layout(uint32_t W, uint32_t B, bool lo) {
+  BvfSmem s;
+  uint32_t o = 0;
+  s.off_tab = o;  // x window, far slots, zero entry, F hi
+  o = align16(o + (bvf_f0(W) + W + 1) * 8u);
+  s.off_flo = o;  // F lo (split mode)
+  o = align16(o + (lo ? (W + 1) * 8u : 0u));
+  s.off_rows = o;
+  o = align16(o + B * 16u);
+  s.off_rn = o;  // r per row, one byte each
+  o = align16(o + kBvfRnWords * 8u);
+  s.off_misc = o;  // warp maxima / totals / carries / epilogue scratch
+  o = align16(o + 64 * 8);
+  s.total = o;
+  return s;
+}
+
+// reference distance of block row k (bytes in shared memory, expanded from the stream's nibbles)
+__device__ __forceinline__ uint32_t bvf_r(const uint8_t* r8, uint32_t k) { return r8[k]; }
+__device__ __forceinline__ uint32_t bvf_slot(uint32_t k) { return k; }
+
+// flip the sign of v when bit 31 of m is set
+__device__ __forceinline__ double flip_sign(double v, uint32_t m) {
+  return __hiloint2double(__double2hiint(v) ^ (int)(m & 0x80000000u), __double2loint(v));
+}
+
+// shared-memory accesses by 32-bit shared address (the hot loop keeps one
+// uniform base per table and adds the term's byte offset)
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_f64x2(uint32_t a, double x, double y) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(x), "d"(y) : "memory");
+}
+
+template <typename XT, bool SPLIT, bool ESC>
+struct BvfTerms {
+  uint32_t tab;    // shared address: x / slots / zero / F hi, 8 bytes per term index
+  uint32_t flo_b;  // shared address of F lo minus F0 * 8 (the term's byte offset indexes it)
+  const uint32_t* esc;  // escape columns of this chunk (ESC)
+  const XT* xfar;
+  double sigma;
+  uint32_t f0b;  // F0 * 8
+  // one term: +-table[index] split at the block grid; bit 31 of `signw` is the
+  // term's minus flag; a row end stores the row's sum at rowp and moves on
+  __device__ __forceinline__ void term(uint32_t c, uint32_t signw, double& ah, double& al, uint32_t& rowp) const {
+    const uint32_t off = (c << 3) & (kBvfIdxMask << 3);
+    const bool e = ESC && (c & kBvfEsc);
+    double v;
+    if (e) v = (double)__ldg(xfar + __ldg(esc + (off >> 3)));
+    else v = lds_f64(tab + off);
+    const double sg = __hiloint2double((int)((signw & 0x80000000u) | 0x3ff00000u), 0);  // +-1
+    if (SPLIT) {
+      double wl = 0.0;
+      if (off >= f0b && !e) wl = lds_f64(flo_b + off);
+      const double h = (v + sigma) - sigma;
+      ah = fma(sg, h, ah);
+      al = fma(sg, (v - h) + wl, al);
+    } else {
+      ah = fma(sg, v, ah);
+    }
+    if (c & kBvfEnd) {
+      sts_f64x2(rowp, ah, al);
+      ah = 0.0;
+      al = 0.0;
+      rowp += 16;
+    }
+  }
+  __device__ __forceinline__ void word(uint32_t w, double& ah, double& al, uint32_t& rowp) const {
+    term(w & 0xffffu, w << 16, ah, al, rowp);
+    term(w >> 16, w, ah, al, rowp);
+  }
+};
+
+template <typename XT, bool SPLIT, bool ESC>
+__device__ __forceinline__ void bvf_chunk(const BvfTerms<XT, SPLIT, ESC>& tm, const uint32_t* __restrict__ cw,
+                                          uint32_t nact, uint32_t nwords, const uint32_t (&w0)[8], double& ah,
+                                          double& al, uint32_t& rowp) {
+  uint32_t w[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) w[i] = w0[i];
+  for (uint32_t q = 8;; q += 8) {
+    uint32_t nx[8];
+    const bool more = q < nwords;
+    if (more) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) nx[i] = __ldg(cw + (size_t)(q + i) * nact);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) tm.word(w[i], ah, al, rowp);
+    if (!more) break;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w[i] = nx[i];
+  }
+}
+
+// CW, CB: compile-time window and block rows (0 = from BvfDev): the default
+// shape gets constant loop bounds and shared-memory offsets.
+template <typename XT, typename YT, bool PR, uint32_t CW = 0, uint32_t CB = 0>
+__global__ void __launch_bounds__(kBvfThreads, 4)
+    bvf_gather_kernel(BvfDev g, const XT* __restrict__ x, const XT* xfar, YT* __restrict__ y, PrArgs pr) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr bool kSplit = sizeof(XT) == 8;  // fp32 x: plain fp64 sums (error far inside the fp32 tolerance)
+  const uint32_t W = CW ? CW : g.W, B = CB ? CB : g.B;
+  const BvfSmem L = bvf_smem_layout(W, B, kSplit);
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  const uint32_t bl = blockIdx.x, b = g.block_begin + bl;
+  const BvfBlockInfo bi = g.blocks[bl];
+  const uint32_t r0 = b * B, nr = min(B, g.n - r0);
+  const uint32_t* bs = g.words + bi.word_offset;
+  const uint32_t K = bi.K, nact = bi.nact, nslot = bi.nslot;
+  const uint32_t F0 = bvf_f0(W);
+  double* tab = reinterpret_cast<double*>(smem + L.off_tab);
+  double* flo = reinterpret_cast<double*>(smem + L.off_flo);
+  char* rows = reinterpret_cast<char*>(smem + L.off_rows);
+  uint8_t* r8 = reinterpret_cast<uint8_t*>(smem + L.off_rn);
+  double* misc = reinterpret_cast<double*>(smem + L.off_misc);
+  uint32_t* misc_u = reinterpret_cast<uint32_t*>(smem + L.off_misc);
+
+  // ---- loads: code words of this chunk, x window chunk, far slots, r
+  const bool active = tid < nact;
+  const uint32_t* cw = bs + bi.codes_off + tid;
+  if (tid == 32) {
+    // the rest of this block's terms into L2 now (the loop's later word loads
+    // then hit L2); and a wave ahead, the stream, window and table entry of the
+    // block whose CTA will take this slot, so its dependent setup loads hit L2
+    const uint32_t cb = bi.nwords - bi.codes_off;
+    if (cb > 8 * nact) bulk_prefetch_l2(bs + bi.codes_off + 8 * nact, ((cb - 8 * nact) * 4u) & ~15u);
+    if (g.ahead && bl + g.ahead < g.nlaunch) {
+      const BvfBlockInfo* nb = g.blocks + bl + g.ahead;
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(nb));
+    }
+  }
+  if (tid == 64 && g.ahead && bl + g.ahead / 2 < g.nlaunch) {
+    // half a wave ahead (its table entry was prefetched half a wave ago)
+    const BvfBlockInfo nb = g.blocks[bl + g.ahead / 2];
+    bulk_prefetch_l2(g.words + nb.word_offset, nb.nwords * 4u);
+    const uint32_t xe = min(nb.wlo + W, g.n);
+    const uint32_t xb = ((xe > nb.wlo ? xe - nb.wlo : 0u) * (uint32_t)sizeof(XT)) & ~15u;
+    if (xb && (reinterpret_cast<uintptr_t>(x + nb.wlo) & 15u) == 0) bulk_prefetch_l2(x + nb.wlo, xb);
+  }
+  uint32_t w0[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) w0[i] = active ? __ldg(cw + (size_t)i * nact) : 0u;
+  const uint32_t srow = active ? (uint32_t)reinterpret_cast<const uint16_t*>(bs)[tid] : 0u;
+  const uint32_t E = CW ? (CW + kBvfThreads - 1) / kBvfThreads : (W + kBvfThreads - 1) / kBvfThreads;  // <= kBvfXPer
+  const uint32_t j0 = tid * E;
+  // a full chunk of an even count: paired 16-byte loads and stores
+  const bool full = !(E & 1u) && j0 + E <= W && bi.wlo + j0 + E <= g.n && !(bi.wlo & 1u) &&
+                    (reinterpret_cast<uintptr_t>(x) & (2 * sizeof(XT) - 1)) == 0;
+  double xv[kBvfXPer];
+  {
+    using P2 = typename std::conditional<sizeof(XT) == 8, double2, float2>::type;
+#pragma unroll
+    for (uint32_t k = 0; k < kBvfXPer; k += 2) {
+      const uint32_t j = j0 + k, c = bi.wlo + j;
+      xv[k] = xv[k + 1] = 0.0;
+      if (k < E) {
+        if (full) {
+          const P2 v2 = __ldg(reinterpret_cast<const P2*>(x + c));
+          xv[k] = (double)v2.x;
+          xv[k + 1] = (double)v2.y;
+        } else {
+          if (j < W && c < g.n) xv[k] = (double)__ldg(x + c);
+          if (k + 1 < E && j + 1 < W && c + 1 < g.n) xv[k + 1] = (double)__ldg(x + c + 1);
+        }
+      }
+    }
+  }
+  double fv = 0.0;
+  const uint32_t far_off = bvf_far_off(nact);
+  if (tid < nslot) fv = (double)__ldg(xfar + __ldg(bs + far_off + tid));
+  const uint32_t rnw = tid < kBvfRnWords ? __ldg(bs + bvf_rn_off(nact) + tid) : 0u;  // stored after the loop
+
+  // ---- block exponent (finite values), non-finite flag; the x table
+  uint32_t emax = 0, nonfin = 0;
+  auto see = [&](double v) {
+    const uint32_t e = ((uint32_t)__double2hiint(v) >> 20) & 0x7ffu;
+    if (e == 0x7ffu) nonfin = 1;
+    else emax = max(emax, e);
+  };
+#pragma unroll
+  for (uint32_t k = 0; k < kBvfXPer; k += 2) {
+    see(xv[k]);
+    see(xv[k + 1]);
+    const uint32_t j = j0 + k;
+    if (k < E) {
+      if (full) {
+        *reinterpret_cast<double2*>(tab + j) = make_double2(xv[k], xv[k + 1]);
+      } else {
+        if (j < W) tab[j] = xv[k];
+        if (k + 1 < E && j + 1 < W) tab[j + 1] = xv[k + 1];
+      }
+    }
+  }
+  see(fv);
+  if (tid < nslot) tab[W + tid] = fv;
+  if (kSplit && (bi.flags & kBvfFlagEsc)) {  // escaped columns take part in the exponent
+    const uint32_t* escs = bs + bi.esc_off;
+    const uint32_t nesc = __ldg(escs + nact);
+    const uint32_t* ecol = escs + bvf_align4(nact + 1);
+    for (uint32_t i = tid; i < nesc; i += kBvfThreads) see((double)__ldg(xfar + __ldg(ecol + i)));
+  }
+  if (tid == 0) tab[bvf_zero(W)] = 0.0;
+  emax = __reduce_max_sync(0xffffffffu, emax);
+  nonfin = __any_sync(0xffffffffu, nonfin);
+  if (lane == 0) misc_u[warp] = emax | (nonfin << 16);
+  __syncthreads();  // #1
+  uint32_t em = 0, nf = 0;
+#pragma unroll
+  for (uint32_t w = 0; w < kBvfThreads / 32; ++w) {
+    const uint32_t v = misc_u[w];
+    em = max(em, v & 0xffffu);
+    nf |= v >> 16;
+  }
+  // sigma = 1.5 * 2^(g + 52), g = E - cbits, E = em - 1023 + 1: h = (x + sigma) - sigma
+  // rounds x to a multiple of 2^g; a non-finite block sums plainly (sigma = 0)
+  double sigma = 0.0;
+  if (kSplit && !nf) {
+    int ef = (int)em + 1 + 52 - (int)bi.cbits;
+    ef = max(ef, 1);
+    sigma = __hiloint2double((ef << 20) | 0x80000, 0);
+  }
+
+  // ---- window prefix F (exclusive): F hi = sum h (exact), F lo = sum l
+  {
+    double sh = 0.0, sl = 0.0;
+#pragma unroll
+    for (uint32_t k = 0; k < kBvfXPer; ++k) {
+      if (k < E) {
+        const double v = xv[k];
+        if (kSplit) {
+          const double h = (v + sigma) - sigma;
+          sh += h;
+          sl += v - h;
+        } else {
+          sh += v;
+        }
+      }
+    }
+    // inclusive warp scan of the chunk totals
+    double ih = sh, il = sl;
+#pragma unroll
+    for (uint32_t o = 1; o < 32; o <<= 1) {
+      const double uh = __shfl_up_sync(0xffffffffu, ih, o);
+      const double ul = kSplit ? __shfl_up_sync(0xffffffffu, il, o) : 0.0;
+      if (lane >= o) {
+        ih += uh;
+        il += ul;
+      }
+    }
+    if (lane == 31) {
+      misc[16 + 2 * warp] = ih;
+      misc[16 + 2 * warp + 1] = il;
+    }
+    __syncthreads();  // #2
+    double bh = ih - sh, blo = il - sl;  // exclusive within the warp
+    for (uint32_t w = 0; w < warp; ++w) {
+      bh += misc[16 + 2 * w];
+      blo += misc[16 + 2 * w + 1];
+    }
+    double* fhi = tab + F0;
+#pragma unroll
+    for (uint32_t k = 0; k < kBvfXPer; k += 2) {
+      const uint32_t j = j0 + k;
+      double h0 = bh, l0 = blo;
+      if (k < E) {
+        const double v = xv[k];
+        if (kSplit) {
+          const double h = (v + sigma) - sigma;
+          bh += h;
+          blo += v - h;
+        } else {
+          bh += v;
+        }
+      }
+      double h1 = bh, l1 = blo;
+      if (k + 1 < E) {
+        const double v = xv[k + 1];
+        if (kSplit) {
+          const double h = (v + sigma) - sigma;
+          bh += h;
+          blo += v - h;
+        } else {
+          bh += v;
+        }
+      }
+      if (k < E) {
+        if (full) {
+          *reinterpret_cast<double2*>(fhi + j) = make_double2(h0, h1);
+          if (kSplit) *reinterpret_cast<double2*>(flo + j) = make_double2(l0, l1);
+        } else {
+          if (j < W) {
+            fhi[j] = h0;
+            if (kSplit) flo[j] = l0;
+          }
+          if (k + 1 < E && j + 1 < W) {
+            fhi[j + 1] = h1;
+            if (kSplit) flo[j + 1] = l1;
+          }
+        }
+      }
+    }
+    if (j0 < W && j0 + E >= W) {  // the thread holding the window's last entry writes F[W]
+      fhi[W] = bh;
+      if (kSplit) flo[W] = blo;
+    }
+  }
+  __syncthreads();  // #3
+
+  // ---- terms
+  double ah = 0.0, al = 0.0;
+  const uint32_t rows_s = smem_u32(rows);
+  uint32_t rowp = rows_s + srow * 16u;
+  if (active) {
+    const uint32_t tabc = smem_u32(tab);
+    const uint32_t flob = smem_u32(flo) - F0 * 8u;
+    if (bi.flags & kBvfFlagEsc) {
+      BvfTerms<XT, kSplit, true> te{tabc, flob, bs + bi.esc_off + bvf_align4(nact + 1) + __ldg(bs + bi.esc_off + tid),
+                                    xfar, sigma, F0 * 8u};
+      bvf_chunk(te, cw, nact, K / 2, w0, ah, al, rowp);
+    } else {
+      BvfTerms<XT, kSplit, false> tm{tabc, flob, nullptr, xfar, sigma, F0 * 8u};
+      bvf_chunk(tm, cw, nact, K / 2, w0, ah, al, rowp);
+    }
+  }
+  if (tid < kBvfRnWords) {  // r nibbles -> bytes
+    uint32_t lo = 0, hi = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      lo |= ((rnw >> (4 * q)) & 15u) << (8 * q);
+      hi |= ((rnw >> (4 * q + 16)) & 15u) << (8 * q);
+    }
+    reinterpret_cast<uint2*>(r8)[tid] = make_uint2(lo, hi);
+  }
+  // ---- carries: a row cut by chunk boundaries gets the tails of the chunks
+  // before its end -- a segmented scan of the tails (segments start at the
+  // chunks that end a row) in the warp, then across warps
+  const bool has_end = active && rowp != rows_s + srow * 16u;
+  double sh = ah, sl = al;
+  bool sf = has_end;
+  if (!__all_sync(0xffffffffu, has_end || !active)) {  // a chunk inside one row: segmented scan
+#pragma unroll
+    for (uint32_t o = 1; o < 32; o <<= 1) {
+      const double uh = __shfl_up_sync(0xffffffffu, sh, o), ul = __shfl_up_sync(0xffffffffu, sl, o);
+      const bool uf = __shfl_up_sync(0xffffffffu, sf, o);
+      if (lane >= o) {
+        if (!sf) {
+          sh += uh;
+          sl += ul;
+        }
+        sf = sf || uf;
+      }
+    }
+  }
+  if (lane == 31) {
+    misc[32 + 2 * warp] = sh;
+    misc[32 + 2 * warp + 1] = sl;
+    misc_u[8 + warp] = sf;
+  }
+  // carry into this lane's first row: the segment value of the lane before
+  double ch = __shfl_up_sync(0xffffffffu, sh, 1), cl = __shfl_up_sync(0xffffffffu, sl, 1);
+  const bool cf = __shfl_up_sync(0xffffffffu, sf, 1);
+  if (lane == 0) ch = cl = 0.0;
+  __syncthreads();  // #4
+  if (has_end) {
+    if (lane == 0 || !cf) {  // the segment reaches back past this warp's first lane
+      for (int w = (int)warp - 1; w >= 0; --w) {
+        ch += misc[32 + 2 * w];
+        cl += misc[32 + 2 * w + 1];
+        if (misc_u[8 + w]) break;
+      }
+    }
+    double2* rr = reinterpret_cast<double2*>(rows + bvf_slot(srow) * 16u);
+    double2 v = *rr;
+    v.x += ch;
+    v.y += cl;
+    *rr = v;
+  }
+  __syncthreads();  // #5
+
+  // ---- reference chains and the store
+  auto rec = [&](uint32_t k) { return *reinterpret_cast<const double2*>(rows + bvf_slot(k) * 16u); };
+  YT* yb = y + (r0 - g.row_begin);
+  auto walk = [&](auto& epi) {
+    if (g.max_depth <= 3) {
+      for (uint32_t kb = tid; kb < nr; kb += kEpiPre * kBvfThreads) {
+        epi.prefetch(kb, kBvfThreads, nr);
+#pragma unroll
+        for (uint32_t q = 0; q < kEpiPre; ++q) {
+          const uint32_t k = kb + q * kBvfThreads;
+          if (k >= nr) break;
+          const double2 rk = rec(k);
+          double hs = rk.x, ls = rk.y;
+          uint32_t p = k, r = bvf_r(r8, k);
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            if (r) {
+              p -= r;
+              const double2 rp = rec(p);
+              hs += rp.x;
+              ls += rp.y;
+              r = bvf_r(r8, p);
+            }
+          }
+          epi.store(yb, k, hs + ls, q);
+        }
+      }
+    } else {
+      // unbounded chains: pointer jumping, one barrier-separated level per step
+      constexpr uint32_t kMaxPer = 4;  // B <= 1024 rows
+      constexpr uint16_t kNone = 0xffffu;
+      uint16_t* ptr = reinterpret_cast<uint16_t*>(tab);  // the table is dead after the terms
+      int any = 0;
+      for (uint32_t k = tid; k < nr; k += kBvfThreads) {
+        const uint32_t r = bvf_r(r8, k);
+        ptr[k] = r ? (uint16_t)(k - r) : kNone;
+        any |= (r != 0);
+      }
+      any = __syncthreads_or(any);
+      while (any) {
+        double nh[kMaxPer], nl[kMaxPer];
+        uint16_t np_[kMaxPer];
+        int more = 0;
+#pragma unroll
+        for (uint32_t q = 0; q < kMaxPer; ++q) {
+          const uint32_t k = tid + q * kBvfThreads;
+          if (k < nr) {
+            const uint32_t p = ptr[k];
+            const double2 rk = rec(k);
+            double h = rk.x, l = rk.y;
+            uint16_t pn = kNone;
+            if (p != kNone) {
+              const double2 rp = rec(p);
+              h += rp.x;
+              l += rp.y;
+              pn = ptr[p];
+            }
+            nh[q] = h;
+            nl[q] = l;
+            np_[q] = pn;
+            more |= (pn != kNone);
+          }
+        }
+        __syncthreads();
+#pragma unroll
+        for (uint32_t q = 0; q < kMaxPer; ++q) {
+          const uint32_t k = tid + q * kBvfThreads;
+          if (k < nr) {
+            *reinterpret_cast<double2*>(rows + bvf_slot(k) * 16u) = make_double2(nh[q], nl[q]);
+            ptr[k] = np_[q];
+          }
+        }
+        any = __syncthreads_or(more);
+      }
+      for (uint32_t kb = tid; kb < nr; kb += kEpiPre * kBvfThreads) {
+        epi.prefetch(kb, kBvfThreads, nr);
+#pragma unroll
+        for (uint32_t q = 0; q < kEpiPre; ++q) {
+          const uint32_t k = kb + q * kBvfThreads;
+          if (k < nr) {
+            const double2 rk = rec(k);
+            epi.store(yb, k, rk.x + rk.y, q);
+          }
+        }
+      }
+    }
+    epi.finish(reinterpret_cast<int*>(misc));
+  };
+  if constexpr (PR) {
+    const uint32_t sh0 = r0 - g.row_begin;
+    PageRankEpi epi;
+    epi.deg = pr.deg + sh0;
+    epi.p_prev = pr.p_prev ? pr.p_prev + sh0 : nullptr;
+    epi.q_next = pr.q_next + sh0;
+    epi.partial = pr.partial;
+    epi.base = pr.alpha / (double)pr.n;
+    epi.alpha_p0 = pr.alpha;
+    epi.scale = 1.0 - pr.alpha;
+    const double dm = pr.dmass ? *pr.dmass : pr.dmass_host;
+    epi.dn = pr.uniform ? dm / (double)pr.n : 0.0;
+    epi.bl = bl;
+    epi.dang = 0.0;
+    epi.l1 = 0.0;
+    epi.push_mask = pr.push_mask ? pr.push_mask + sh0 : nullptr;
+    epi.p0 = pr.p0 ? pr.p0 + r0 : nullptr;
+    epi.push_dst = pr.push_dst;
+    epi.grow0 = r0;
+    walk(epi);
+  } else {
+    PlainEpi epi;
+    walk(epi);
+  }
+}
+
+}  // namespace cmvg

@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(512, 2) bvs_matmat_kernel(BvdDev g, const floa
   __syncthreads();
   // chains: one (row, column) per thread, walking the row's ancestors
   // (<= 3 for bounded chains; the full chain otherwise)
-  float* yb = Y + (size_t)r0 * ld;
+  float* yb = Y + (size_t)(r0 - g.row_begin) * ld;  // Y holds the shard's rows
   for (uint32_t e = tid; e < nr * kMmCols; e += T) {
     const uint32_t k = e / kMmCols, c = e % kMmCols;
     double y = s_d[e];

@@ -30,6 +30,17 @@ struct BvsStats {
   uint64_t lane_iters = 0, lane_iters_used = 0;  // slice decode iterations x 32 / useful lane iterations
 };
 
+struct BvfStats {
+  uint64_t stream_bytes = 0;
+  uint64_t terms = 0;         // useful terms (x entries, interval ends, refs not counted)
+  uint64_t pad_terms = 0;     // padding terms (empty rows, chunk tails)
+  uint64_t slot_terms = 0;    // terms on far slots
+  uint64_t esc_terms = 0;     // terms read from global memory (slots exhausted)
+  uint64_t esc_blocks = 0;
+  uint32_t max_K = 0;
+  uint32_t min_cbits = 64;
+};
+
 struct BvtStats {
   uint64_t stream_bytes = 0;
   uint64_t slices = 0, heavy_targets = 0, far_slots = 0, entries = 0;
@@ -44,6 +55,10 @@ struct BvdLayout {
   std::vector<uint32_t> swords;
   std::vector<BvdBlockInfo> sblocks;
   BvsStats sstats;
+  // BV-F (flat term stream; gather / PageRank)
+  std::vector<uint32_t> fwords;
+  std::vector<BvfBlockInfo> fblocks;
+  BvfStats fstats;
   // BV-T (target-sorted scatter stream) + the combine tables
   std::vector<uint32_t> twords;
   std::vector<BvdBlockInfo> tblocks;  // pad[0] = first far staging slot

@@ -205,6 +205,61 @@ __host__ __device__ constexpr uint32_t tmeta_ne(uint32_t m) { return m & 1023u; 
 __host__ __device__ constexpr bool tmeta_multi(uint32_t m) { return (m >> 10) & 1u; }
 __host__ __device__ constexpr uint32_t tmeta_rounds(uint32_t m) { return (m >> 11) & 7u; }
 
+// ---------------------------------------------------------------------------
+// BV-F: the flat term stream of the gather / PageRank kernels
+// (cuda/bvf_gather.cuh).  The same differential rows as BV-D (reference
+// include/cmv/ref_matrix.hpp:13-52; y_i = y_{i-r} - sum_minus x + sum_plus x,
+// ref_matvec.hpp:20-31), written as one flat list of 16-bit TERMS per block in
+// row order.  A term is one signed entry of a per-block shared-memory table:
+//   table[0, W)                x[wlo + j]            (the block's x-window)
+//   table[W, W + nslot)        x[far[s]]             (columns outside the window)
+//   table[W + kBvfSlots]       0                     (padding / empty rows)
+//   table[F0 + j], j <= W      F[j] = sum_{t < j} x[wlo + t]   (F0 = W + kBvfSlots + 1)
+// so a minus entry is -x[c], a residual +x[c] and an interval [a, a + len)
+// inside the window the two terms +F[a - wlo + len], -F[a - wlo] (O(1),
+// PAPER.md:198-206).  Intervals reaching outside the window are written as
+// their columns.  Term (16 bits): index (13) | escape << 13 | end << 14 |
+// minus << 15; `end` marks a row's last term (every row has >= 1 term: an
+// empty row gets one padding term).  Escape terms (blocks whose far columns
+// exceed the slots) read x[esc[escstart_t + index]] from global memory.
+// Work split: the block's N terms are cut into nact chunks of K terms
+// (K = 16 ceil(N / 4096), nact = ceil(N / K) <= 256; the last chunk padded);
+// thread t sums chunk t, so every thread has the same work whatever the row
+// lengths (hub rows need no special path); a row cut by a chunk boundary is
+// completed by the next thread that ends it (carry).
+// Block stream (u32 words):
+//   [0, align4(ceil(nact/2)))   u16 first row of each chunk
+//   [.., + kBvfRnWords)         reference distance r of each row, 4 bits (8 per word)
+//   [.., + align4(nslot))       far slot columns
+//   esc_off: (escape blocks) u32 first escape of each chunk [align4(nact)], then
+//                            the escape columns [align4(nesc)]
+//   codes_off: K/2 x nact words, word q of chunk t at codes_off + q nact + t
+//     (two terms per word, the first in the low half: coalesced loads)
+constexpr uint32_t kBvfSlots = 127;    // far slots per block (the next entry is the zero entry; odd: F0 even)
+constexpr uint32_t kBvfMaxThreads = 256;
+constexpr uint32_t kBvfRnWords = 128;  // 1024 rows x 4 bits
+constexpr uint32_t kBvfIdxMask = 0x1fffu;
+constexpr uint32_t kBvfEsc = 0x2000u, kBvfEnd = 0x4000u, kBvfMinus = 0x8000u;
+constexpr uint32_t kBvfFlagEsc = 1u;  // BvfBlockInfo::flags: the block has escape terms
+__host__ __device__ constexpr uint32_t bvf_f0(uint32_t W) { return W + kBvfSlots + 1; }
+__host__ __device__ constexpr uint32_t bvf_zero(uint32_t W) { return W + kBvfSlots; }
+__host__ __device__ constexpr uint32_t bvf_align4(uint32_t v) { return (v + 3u) & ~3u; }
+__host__ __device__ constexpr uint32_t bvf_rn_off(uint32_t nact) { return bvf_align4((nact + 1u) / 2u); }
+__host__ __device__ constexpr uint32_t bvf_far_off(uint32_t nact) { return bvf_rn_off(nact) + kBvfRnWords; }
+
+struct BvfBlockInfo {
+  uint64_t word_offset;  // first u32 word of the block's stream (16-byte aligned)
+  uint32_t wlo;          // x-window start
+  uint16_t K, nact;      // terms per chunk, chunks (active threads)
+  uint16_t nslot;        // far slots used
+  uint8_t cbits;         // grid of the exact split: G = 2^(E - cbits), E = block max exponent
+  uint8_t flags;
+  uint32_t codes_off;    // word offset of the term words
+  uint32_t esc_off;      // word offset of the escape tables (escape blocks)
+  uint32_t nwords;
+};
+static_assert(sizeof(BvfBlockInfo) == 32, "BvfBlockInfo is 32 bytes");
+
 struct BvdBlockInfo {
   uint64_t word_offset;  // first u32 word of this block's stream (16-byte aligned)
   uint32_t nwords;       // words in this block's stream (multiple of 4)

@@ -11,7 +11,7 @@
 #include <string>
 
 #include "../../include/cmvg.h"
-#include "cuda/bvs_gather.cuh"
+#include "cuda/bvf_gather.cuh"
 #include "host/bvd_layout.hpp"
 #include "host/host.hpp"
 
@@ -150,6 +150,12 @@ struct cmvg_graph {
   DevBuf swords, sblocks;
   uint64_t heavy_items = 0;  // heavy-row work items of the whole graph (partial-sum slots per launch)
   uint64_t s_stream_bytes = 0;
+  // BV-F layout (this shard): gather, PageRank
+  DevBuf fwords, fblocks;
+  uint64_t f_stream_bytes = 0;
+  BvfStats fstats;
+  std::atomic<unsigned> fgather_attr{0};
+  std::atomic<uint32_t> fgather_res{0};  // resident CTAs of the BV-F gather (L2 prefetch distance)
   // BV-T layout (this shard): scatter; combine tables (whole graph)
   DevBuf twords, tblocks, tile_ptr, tile_blk, farp_ptr, farp;
   uint32_t tfar_begin = 0, tfar_end = 0;
@@ -178,10 +184,9 @@ struct cmvg_graph {
       if (s) cudaStreamDestroy(s);
   }
   std::mutex host_mu;
-  // scratch (scatter / pagerank)
-  DevBuf scratch;
   uint64_t device_bytes() const {
-    return words.bytes + blocks.bytes + swords.bytes + sblocks.bytes + twords.bytes + tblocks.bytes + tile_ptr.bytes +
+    return words.bytes + blocks.bytes + swords.bytes + sblocks.bytes + fwords.bytes + fblocks.bytes + twords.bytes +
+           tblocks.bytes + tile_ptr.bytes +
            tile_blk.bytes + farp_ptr.bytes + farp.bytes + bv_words.bytes + bv_seg.bytes;
   }
   BvdDev dev() const {
@@ -230,35 +235,47 @@ inline uint32_t resident_ctas(K kern, int threads, size_t smem, int device, std:
   return c & 0x7fffffffu;
 }
 
-// Stream-ordered scratch for one gather launch's heavy-row partial sums
-// (cudaMallocAsync from the device's pool, freed on the same stream after the
-// launch): each launch has its own slots, so concurrent products on distinct
-// streams never share them, and a captured CUDA graph gets memory nodes.
-// No-op for layouts without heavy rows.
-struct HeavyScratch {
+// Keep freed blocks in a device's default memory pool (no OS round trip per
+// stream-ordered allocation); once per device.
+inline void keep_pool(int device) {
+  static std::atomic<uint64_t> done{0};
+  const uint64_t bit = 1ull << (device & 63);
+  if (done.fetch_or(bit) & bit) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t keep = ~0ull;
+    (void)cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+}
+
+// Stream-ordered scratch for one launch (cudaMallocAsync from the device's
+// pool, freed on the same stream after the launch): each launch has its own
+// memory, so concurrent products on distinct streams of one handle never share
+// it (cmvg.h: a handle serves concurrent DEVICE-pointer products), and a
+// captured CUDA graph gets memory nodes.
+struct StreamScratch {
   void* p = nullptr;
   cudaStream_t st = nullptr;
-  HeavyScratch(const cmvg_graph* g, cudaStream_t s) : st(s) {
-    if (!g->heavy_items) return;
-    static std::atomic<bool> pool_kept{false};  // keep freed blocks in the pool (no OS round trip per launch)
-    if (!pool_kept.exchange(true)) {
-      cudaMemPool_t pool;
-      if (cudaDeviceGetDefaultMemPool(&pool, g->device) == cudaSuccess) {
-        uint64_t keep = ~0ull;
-        (void)cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-      }
-    }
-    CUDA_TRY(cudaMallocAsync(&p, g->heavy_items * 16, st));
+  StreamScratch(int device, size_t bytes, cudaStream_t s) : st(s) {
+    if (!bytes) return;
+    keep_pool(device);
+    CUDA_TRY(cudaMallocAsync(&p, bytes, st));
   }
-  double2* get() const { return static_cast<double2*>(p); }
-  ~HeavyScratch() {
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+  ~StreamScratch() {
     if (p) (void)cudaFreeAsync(p, st);
   }
-  HeavyScratch(const HeavyScratch&) = delete;
-  HeavyScratch& operator=(const HeavyScratch&) = delete;
+  StreamScratch(const StreamScratch&) = delete;
+  StreamScratch& operator=(const StreamScratch&) = delete;
 };
 
 // kernel entry points implemented in the other translation units
+template <typename XT, typename YT, bool PR>
+void launch_bvf(cmvg_graph* g, const XT* x, const XT* xfar, YT* y, const PrArgs& pr, cudaStream_t st, uint32_t b0 = 0,
+                uint32_t b1 = 0xffffffffu);
 template <typename T>
 void launch_scatter(cmvg_graph* g, const T* x, T* y, cudaStream_t st);
 void launch_matmat(cmvg_graph* g, const float* X, float* Y, uint32_t k, cudaStream_t st);

@@ -59,18 +59,7 @@ __global__ void pr_reduce_kernel(const double* __restrict__ partial, uint32_t nb
 }
 
 void launch_pr_step(cmvg_graph* g, const double* q, PrArgs pr, double* p_next, cudaStream_t st) {
-  const BvsSmem L = bvs_smem_layout(g->dims, sizeof(double));
-  const bool dflt = g->dims.window == kGatherDefault.W && g->dims.block_rows == kGatherDefault.B &&
-                    g->threads == kGatherDefault.T;
-  auto kern = dflt ? bvs_gather_kernel<double, double, true, kGatherDefault.W, kGatherDefault.B, kGatherDefault.T>
-                   : bvs_gather_kernel<double, double, true>;
-  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
-  BvdDev d = g->sdev();
-  d.ahead = resident_ctas(kern, (int)g->threads, L.total, g->device, g->gather_res[2]);
-  HeavyScratch hs(g, st);
-  d.hpart = hs.get();
-  kern<<<g->nblocks, g->threads, L.total, st>>>(d, q, q, p_next, pr);
-  CUDA_TRY(cudaGetLastError());
+  launch_bvf<double, double, true>(g, q, q, p_next, pr, st);
 }
 
 }  // namespace
@@ -186,21 +175,21 @@ void run_pagerank(cmvg_graph* g, const uint32_t* degrees, double alpha, uint32_t
 void pagerank_step(cmvg_graph* g, const double* q, const uint32_t* deg, double alpha, double dmass, int dangling,
                    const double* p_prev, double* p_next, double* q_next, double* partial, cudaStream_t st,
                    const uint8_t* push_mask, double* const* push_dst) {
-  g->scratch.alloc((size_t)g->nblocks * 16 + 64);
+  StreamScratch scratch(g->device, (size_t)g->nblocks * 16 + 64, st);  // per launch (concurrent steps)
   PrArgs pr{};
   pr.push_mask = push_mask;
   pr.push_dst = push_dst;
   pr.deg = deg;
   pr.p_prev = p_prev;
   pr.q_next = q_next;
-  pr.partial = g->scratch.as<double>();
+  pr.partial = scratch.as<double>();
   pr.dmass = nullptr;
   pr.dmass_host = dmass;
   pr.alpha = alpha;
   pr.n = g->n;
   pr.uniform = dangling == CMVG_DANGLING_UNIFORM;
   launch_pr_step(g, q, pr, p_next, st);
-  pr_reduce_kernel<<<1, 1024, 0, st>>>(g->scratch.as<double>(), g->nblocks, partial);
+  pr_reduce_kernel<<<1, 1024, 0, st>>>(scratch.as<double>(), g->nblocks, partial);
   CUDA_TRY(cudaGetLastError());
 }
 

@@ -12,8 +12,8 @@ void launch_scatter(cmvg_graph* g, const T* x, T* y, cudaStream_t st) {
   const size_t nfar = (size_t)g->tfar_end - g->tfar_begin;
   // staging: partial windows (hi f64 + lo f32) and the shard's far slots
   const size_t bytes = nst * 12 + nfar * 12 + 256;
-  g->scratch.alloc(bytes);
-  unsigned char* p = g->scratch.as<unsigned char>();
+  StreamScratch scratch(g->device, bytes, st);  // per launch: concurrent scatters never share it
+  unsigned char* p = scratch.as<unsigned char>();
   BvtOut o;
   o.st_hi = reinterpret_cast<double*>(p);
   o.far_hi = o.st_hi + nst;

@@ -310,3 +310,139 @@ def scatter_bvt_int(words, blocks, n, B, W, x):
         for f, col in enumerate(far_cols):
             y[col] += out.get(2 * W + f, 0)
     return y
+
+
+# ---------------------------------------------------------------------------
+# BV-F (flat term stream; host/layout.hpp, cuda/bvf_gather.cuh)
+BVF_SLOTS, BVF_IDX, BVF_ESC, BVF_END, BVF_MINUS, BVF_FLAG_ESC = 127, 0x1FFF, 0x2000, 0x4000, 0x8000, 1
+
+
+def _align4(v):
+    return (v + 3) & ~3
+
+
+def bvf_block(words, blk):
+    """Fields of one BV-F block: info dict, start rows, r per row, slot columns,
+    escape starts and columns, and the terms of each chunk (list of lists)."""
+    woff = int(blk[0]) | (int(blk[1]) << 32)
+    info = dict(wlo=int(blk[2]), K=int(blk[3]) & 0xFFFF, nact=int(blk[3]) >> 16, nslot=int(blk[4]) & 0xFFFF,
+                cbits=(int(blk[4]) >> 16) & 0xFF, flags=int(blk[4]) >> 24, codes_off=int(blk[5]),
+                esc_off=int(blk[6]), nwords=int(blk[7]))
+    s = words[woff:woff + info["nwords"]]
+    nact, K = info["nact"], info["K"]
+    sr = s[:(nact + 1) // 2].view(np.uint16)[:nact].astype(np.int64) if nact else np.zeros(0, np.int64)
+    rn_off = _align4((nact + 1) // 2)
+    rn = s[rn_off:rn_off + 128]
+    r = np.array([(int(rn[k >> 3]) >> (4 * (k & 7))) & 15 for k in range(1024)], np.int64)
+    far_off = rn_off + 128
+    slots = s[far_off:far_off + info["nslot"]].astype(np.int64)
+    escstart, esccol = None, None
+    if info["flags"] & BVF_FLAG_ESC:
+        eo = info["esc_off"]
+        escstart = s[eo:eo + nact + 1].astype(np.int64)
+        c0 = eo + _align4(nact + 1)
+        esccol = s[c0:c0 + int(escstart[nact])].astype(np.int64)
+    co = info["codes_off"]
+    cw = s[co:co + (K // 2) * nact].reshape(K // 2, nact)  # word q of chunk t at [q, t]
+    chunks = []
+    for t in range(nact):
+        wt = cw[:, t]
+        codes = np.empty(K, np.int64)
+        codes[0::2] = wt & 0xFFFF
+        codes[1::2] = wt >> 16
+        chunks.append(codes)
+    return info, sr, r, slots, escstart, esccol, chunks
+
+
+def gather_bvf(words, blocks, n, B, W, x, max_depth=3):
+    """y = A x with the BV-F kernel's arithmetic (exact split at the block grid,
+    chunk sums with row ends, carries, reference chains) in fp64."""
+    x = np.asarray(x, np.float64)
+    y = np.zeros(n)
+    F0, ZERO = W + BVF_SLOTS + 1, W + BVF_SLOTS
+    for b in range(len(blocks)):
+        info, sr, r, slots, escstart, esccol, chunks = bvf_block(words, blocks[b])
+        r0, nr, wlo = b * B, min(B, n - b * B), info["wlo"]
+        tab = np.zeros(F0 + W + 1)
+        flo = np.zeros(W + 1)
+        win = np.zeros(W)
+        hi_c = min(n, wlo + W)
+        if hi_c > wlo:
+            win[:hi_c - wlo] = x[wlo:hi_c]
+        tab[:W] = win
+        tab[W:W + len(slots)] = x[slots]
+        vals = np.concatenate([win, x[slots]] + ([x[esccol]] if esccol is not None else []))
+        fin = vals[np.isfinite(vals)]
+        nonfin = len(fin) != len(vals)
+        em = int(np.max((fin.view(np.uint64) >> np.uint64(52)) & np.uint64(0x7FF))) if len(fin) else 0
+        sigma = 0.0
+        if not nonfin:
+            ef = max(em + 1 + 52 - info["cbits"], 1)
+            sigma = float(np.array([(ef << 52) | (1 << 51)], np.uint64).view(np.float64)[0])
+        sh = sl = 0.0
+        for j in range(W):
+            tab[F0 + j], flo[j] = sh, sl
+            h = (win[j] + sigma) - sigma
+            sh += h
+            sl += win[j] - h
+        tab[F0 + W], flo[W] = sh, sl
+        rows = np.zeros((B, 2))
+        tails, has_end = [], []
+        for t, codes in enumerate(chunks):
+            ah = al = 0.0
+            row = int(sr[t])
+            for c in codes:
+                c = int(c)
+                idx = c & BVF_IDX
+                if c & BVF_ESC:
+                    v = x[esccol[escstart[t] + idx]]
+                    wl = 0.0
+                else:
+                    v = tab[idx]
+                    wl = flo[idx - F0] if idx >= F0 else 0.0
+                if c & BVF_MINUS:
+                    v, wl = -v, -wl
+                h = (v + sigma) - sigma
+                ah += h
+                al += (v - h) + wl
+                if c & BVF_END:
+                    rows[row] = (ah, al)
+                    ah = al = 0.0
+                    row += 1
+            tails.append((ah, al))
+            has_end.append(row > int(sr[t]))
+        for t in range(1, len(chunks)):
+            if not has_end[t]:
+                continue
+            ch = cl = 0.0
+            j = t - 1
+            while True:
+                ch += tails[j][0]
+                cl += tails[j][1]
+                if j == 0 or has_end[j]:
+                    break
+                j -= 1
+            rows[int(sr[t])] += (ch, cl)
+        if max_depth <= 3:
+            for k in range(nr):
+                s_h, s_l = rows[k]
+                p, rr = k, r[k]
+                for _ in range(3):
+                    if rr:
+                        p -= rr
+                        s_h += rows[p][0]
+                        s_l += rows[p][1]
+                        rr = r[p]
+                y[r0 + k] = s_h + s_l
+        else:
+            vals2 = rows[:nr].copy()
+            ptr = [k - r[k] if r[k] else -1 for k in range(nr)]
+            while any(p >= 0 for p in ptr):
+                nv, np_ = vals2.copy(), list(ptr)
+                for k in range(nr):
+                    if ptr[k] >= 0:
+                        nv[k] += vals2[ptr[k]]
+                        np_[k] = ptr[ptr[k]]
+                vals2, ptr = nv, np_
+            y[r0:r0 + nr] = vals2[:, 0] + vals2[:, 1]
+    return y
