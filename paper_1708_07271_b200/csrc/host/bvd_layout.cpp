@@ -102,9 +102,11 @@ inline uint32_t bits32(const std::vector<uint32_t>& w, uint64_t pos, uint64_t en
 // chunking and the row ends do not move) greedily per phase, the most
 // constrained lane first, each lane taking the term whose bank pair is least
 // loaded in its phase (a term at an entry already loaded is free: broadcast).
-// Measured on the C2 generator: 5.6 -> 2.95 wavefronts per warp load (ideal 2).
+// F terms also load F lo (a second, predicated load): their placement counts
+// that load's conflicts plus one for opening it in a phase.  Measured on the
+// C2 generator: 5.6 + 2.4 -> 3.0 + 1.6 wavefronts per term step (ideal 2).
 void bvf_schedule_terms(std::vector<uint16_t>& codes, std::vector<uint32_t>& ecol, const std::vector<uint32_t>& rstart,
-                        uint32_t N, uint32_t K, uint32_t nact) {
+                        uint32_t N, uint32_t K, uint32_t nact, uint32_t F0) {
   const uint32_t nrows = (uint32_t)rstart.size();
   std::vector<uint32_t> rowof(N);
   for (uint32_t k = 0; k < nrows; ++k) {
@@ -118,8 +120,8 @@ void bvf_schedule_terms(std::vector<uint16_t>& codes, std::vector<uint32_t>& eco
   std::vector<uint32_t> pend(nrows);
   for (uint32_t k = 0; k < nrows; ++k) pend[k] = k + 1 < nrows ? rstart[k + 1] : N;
   uint32_t lanes[16];
-  uint16_t seen[16][8];
-  uint8_t nseen[16];
+  uint16_t seen[16][8], fseen[16][8];
+  uint8_t nseen[16], nfseen[16];
   for (uint32_t j = 0; j < K; ++j) {
     for (uint32_t h0 = 0; h0 < nact; h0 += 16) {
       uint32_t nl = 0;
@@ -131,6 +133,8 @@ void bvf_schedule_terms(std::vector<uint16_t>& codes, std::vector<uint32_t>& eco
         return pend[ra] - rstart[ra] < pend[rb] - rstart[rb];
       });
       std::memset(nseen, 0, sizeof(nseen));
+      std::memset(nfseen, 0, sizeof(nfseen));
+      uint32_t nf = 0;  // F terms in this phase: their second (lo) load is a separate, predicated one
       for (uint32_t q = 0; q < nl; ++q) {
         const size_t pos = (size_t)lanes[q] * K + j;
         const uint32_t k = rowof[pos];
@@ -149,6 +153,12 @@ void bvf_schedule_terms(std::vector<uint16_t>& codes, std::vector<uint32_t>& eco
                 cost = 0;
                 dup = true;
               }
+            if (idx >= F0) {  // the F lo load: a first F term opens a wavefront, later ones may conflict
+              uint32_t fc = nfseen[bk];
+              for (uint32_t s = 0; s < std::min<uint32_t>(nfseen[bk], 8); ++s)
+                if (fseen[bk][s] == idx) fc = 0;
+              cost += fc + (nf == 0 ? 1u : 0u);
+            }
           }
           if (cost < bcost) {
             bcost = cost;
@@ -169,6 +179,16 @@ void bvf_schedule_terms(std::vector<uint16_t>& codes, std::vector<uint32_t>& eco
           const uint32_t bk = (c & kBvfIdxMask) & 15u;
           if (nseen[bk] < 8) seen[bk][nseen[bk]] = (uint16_t)(c & kBvfIdxMask);
           ++nseen[bk];
+        }
+        if (!(c & kBvfEsc) && (c & kBvfIdxMask) >= F0) {
+          const uint32_t idx = c & kBvfIdxMask, bk = idx & 15u;
+          bool have = false;
+          for (uint32_t s = 0; s < std::min<uint32_t>(nfseen[bk], 8); ++s) have |= fseen[bk][s] == idx;
+          if (!have) {
+            if (nfseen[bk] < 8) fseen[bk][nfseen[bk]] = (uint16_t)idx;
+            ++nfseen[bk];
+          }
+          ++nf;
         }
       }
     }
@@ -278,7 +298,7 @@ void emit_bvf(const RowParts* rps, const RowMeta* meta, uint32_t nr, uint64_t wl
   pad_terms += (uint64_t)nact * K - N;
   codes.resize((size_t)nact * K, (uint16_t)ZERO);
   ecol.resize((size_t)nact * K, 0);
-  bvf_schedule_terms(codes, ecol, rstart, (uint32_t)N, K, nact);
+  bvf_schedule_terms(codes, ecol, rstart, (uint32_t)N, K, nact, F0);
   // escape terms: index within the chunk's escape segment
   std::vector<uint32_t> escstart(nact + 1, 0), escc;
   for (uint32_t t = 0; t < nact; ++t) {
