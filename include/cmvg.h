@@ -285,6 +285,16 @@ int cmvg_pagerank_step_push(cmvg_graph* g, const double* q, const uint32_t* degr
                             double* q_next, double* partial, const uint8_t* push_mask, double* const* push_dst,
                             void* stream);
 
+/* cmvg_pagerank_step / _push with the dangling mass read from DEVICE memory
+ * (dangling_mass_dev[0], e.g. element 0 of the previous step's all-reduced
+ * partial sums): no host round trip between iterations, so a multi-GPU driver
+ * can queue step -> all_reduce -> step ... (or capture them in a CUDA graph).
+ * push_mask / push_dst may be NULL (no fused push). */
+int cmvg_pagerank_step_dev(cmvg_graph* g, const double* q, const uint32_t* degrees_shard, double alpha,
+                           const double* dangling_mass_dev, int dangling, const double* p_prev, double* p_next,
+                           double* q_next, double* partial, const uint8_t* push_mask, double* const* push_dst,
+                           void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -306,3 +306,57 @@ def verify_cover(n, bicliques, residual, rows):
     got.extend((int(i), int(j)) for i, j in residual)
     want = [(u, int(v)) for u in range(n) for v in rows[u]]
     return sorted(got) == sorted(want)
+
+
+# ---------------------------------------------------------------------------
+# workload generators (oracle/_build/libcmv_gen.so: the product's host generator
+# source compiled alone), so bench.py's CPU reference arm never loads libcmvg.so
+_GEN = os.path.join(_HERE, "_build", "libcmv_gen.so")
+_gen = None
+
+
+def gen_lib() -> C.CDLL:
+    global _gen
+    if _gen is None:
+        if not os.path.exists(_GEN):
+            build()
+        L = C.CDLL(_GEN)
+        for k, (r, a) in {
+            "gen_copy_model": (C.c_int, [C.c_uint32, C.c_double, C.c_double, C.c_double, C.c_uint64, C.POINTER(_P)]),
+            "gen_social": (C.c_int, [C.c_uint32, C.c_uint64, C.POINTER(_P)]),
+            "gen_n": (C.c_uint32, [_P]),
+            "gen_m": (C.c_uint64, [_P]),
+            "gen_row_offsets": (_P, [_P]),
+            "gen_cols": (_P, [_P]),
+            "gen_free": (None, [_P]),
+        }.items():
+            f = getattr(L, k)
+            f.restype, f.argtypes = r, a
+        _gen = L
+    return _gen
+
+
+def _gen_arrays(h):
+    L = gen_lib()
+    try:
+        n, m = int(L.gen_n(h)), int(L.gen_m(h))
+        ro = _view(L.gen_row_offsets(h), n + 1, np.uint64).copy()
+        co = _view(L.gen_cols(h), m, np.uint32).copy()
+    finally:
+        L.gen_free(h)
+    return n, ro, co
+
+
+def generate_copy_model(n, mean_degree, p_ref=0.7, p_copy=0.8, seed=0x170807271):
+    """(n, row_offsets u64[n+1], columns u32[m]) of the seeded copy model."""
+    h = _P()
+    if gen_lib().gen_copy_model(n, mean_degree, p_ref, p_copy, seed, C.byref(h)):
+        raise RuntimeError("gen_copy_model failed")
+    return _gen_arrays(h)
+
+
+def generate_social(n, seed=0x170807271 + 4):
+    h = _P()
+    if gen_lib().gen_social(n, seed, C.byref(h)):
+        raise RuntimeError("gen_social failed")
+    return _gen_arrays(h)

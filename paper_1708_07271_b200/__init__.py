@@ -151,6 +151,7 @@ _SIGS = [
                                    C.POINTER(C.c_uint32), C.c_int, _P]),
     ("cmvg_pagerank_step_push", C.c_int, [_P, _P, _P, C.c_double, C.c_double, C.c_int, _P, _P, _P, _P, _P, _P, _P]),
     ("cmvg_pagerank_step", C.c_int, [_P, _P, _P, C.c_double, C.c_double, C.c_int, _P, _P, _P, _P, _P]),
+    ("cmvg_pagerank_step_dev", C.c_int, [_P, _P, _P, C.c_double, _P, C.c_int, _P, _P, _P, _P, _P, _P, _P]),
     ("cmvg_csr_matvec_f64", C.c_int, [C.c_uint32, C.c_uint64, _P, _P, _P, _P, _P]),
     ("cmvg_bv_save", C.c_int, [_P, C.c_char_p]),
     ("cmvg_bv_load", C.c_int, [C.c_char_p, C.POINTER(_P)]),
@@ -733,6 +734,18 @@ class BvGraph:
             _check(lib.cmvg_pagerank_step_push(self._h, ptrs[0], ptrs[1], alpha, dangling_mass, dang, ptrs[2],
                                                ptrs[3], ptrs[4], ptrs[5], push_mask.data_ptr(), push_dst.data_ptr(),
                                                st))
+
+    def pagerank_step_dev(self, q, degrees_shard, alpha, dangling_mass, dangling, p_prev, p_next, q_next, partial,
+                          stream: Optional[int] = None, push_mask=None, push_dst=None):
+        """pagerank_step with the dangling mass a DEVICE tensor (its element 0;
+        cmvg_pagerank_step_dev): no host synchronisation between iterations."""
+        st = stream if stream is not None else _stream_of(q)
+        dang = {"uniform": 0, "drop": 1}[dangling]
+        _check(load_library().cmvg_pagerank_step_dev(
+            self._h, q.data_ptr(), degrees_shard.data_ptr(), alpha, dangling_mass.data_ptr(), dang,
+            p_prev.data_ptr() if p_prev is not None else None, p_next.data_ptr(), q_next.data_ptr(),
+            partial.data_ptr(), push_mask.data_ptr() if push_mask is not None else None,
+            push_dst.data_ptr() if push_dst is not None else None, st))
 
     def read_set(self) -> np.ndarray:
         """Sorted columns of x this handle's gather reads (x-windows + out-of-window

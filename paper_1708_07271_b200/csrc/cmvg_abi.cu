@@ -849,4 +849,17 @@ int cmvg_pagerank_step_push(cmvg_graph* g, const double* q, const uint32_t* deg,
   });
 }
 
+int cmvg_pagerank_step_dev(cmvg_graph* g, const double* q, const uint32_t* deg, double alpha, const double* dmass_dev,
+                           int dangling, const double* p_prev, double* p_next, double* q_next, double* partial,
+                           const uint8_t* push_mask, double* const* push_dst, void* stream) {
+  return guarded([&] {
+    require(g && q && deg && dmass_dev && p_next && q_next && partial, "null argument");
+    require(alpha > 0.0 && alpha < 1.0, "alpha must be in (0,1)");
+    require((push_mask == nullptr) == (push_dst == nullptr), "push_mask and push_dst go together");
+    DeviceGuard dg(g->device);
+    pagerank_step(g, q, deg, alpha, 0.0, dangling, p_prev, p_next, q_next, partial, (cudaStream_t)stream, push_mask,
+                  push_dst, dmass_dev);
+  });
+}
+
 }  // extern "C"

@@ -283,5 +283,6 @@ void run_pagerank(cmvg_graph* g, const uint32_t* degrees, double alpha, uint32_t
                   const double* start, double* ranks, uint32_t* iters_run, int ptr_kind, cudaStream_t st);
 void pagerank_step(cmvg_graph* g, const double* q, const uint32_t* deg, double alpha, double dmass, int dangling,
                    const double* p_prev, double* p_next, double* q_next, double* partial, cudaStream_t st,
-                   const uint8_t* push_mask = nullptr, double* const* push_dst = nullptr);
+                   const uint8_t* push_mask = nullptr, double* const* push_dst = nullptr,
+                   const double* dmass_dev = nullptr);
 }  // namespace cmvg

@@ -174,7 +174,7 @@ void run_pagerank(cmvg_graph* g, const uint32_t* degrees, double alpha, uint32_t
 
 void pagerank_step(cmvg_graph* g, const double* q, const uint32_t* deg, double alpha, double dmass, int dangling,
                    const double* p_prev, double* p_next, double* q_next, double* partial, cudaStream_t st,
-                   const uint8_t* push_mask, double* const* push_dst) {
+                   const uint8_t* push_mask, double* const* push_dst, const double* dmass_dev) {
   StreamScratch scratch(g->device, (size_t)g->nblocks * 16 + 64, st);  // per launch (concurrent steps)
   PrArgs pr{};
   pr.push_mask = push_mask;
@@ -183,7 +183,7 @@ void pagerank_step(cmvg_graph* g, const double* q, const uint32_t* deg, double a
   pr.p_prev = p_prev;
   pr.q_next = q_next;
   pr.partial = scratch.as<double>();
-  pr.dmass = nullptr;
+  pr.dmass = dmass_dev;  // device scalar when given (no host round trip), else the host value
   pr.dmass_host = dmass;
   pr.alpha = alpha;
   pr.n = g->n;

@@ -157,6 +157,79 @@ def sharded_pagerank(step_fn: Callable, degrees_shard, n: int, plan: ShardPlan, 
     return p, it
 
 
+def sharded_pagerank_dev(step_fn: Callable, degrees_shard, n: int, plan: ShardPlan, rank: int, alpha: float = 0.15,
+                        iterations: int = 10, l1_tolerance: Optional[float] = None, dangling: str = "uniform",
+                        device=None, group=None, halo: Optional[HaloPlan] = None, push=None):
+    """sharded_pagerank with every per-iteration scalar kept on the device:
+    step_fn(q_full, alpha, dmass_dev, p_prev, p_next, q_next, part_out) reads
+    the dangling mass from dmass_dev[0] (the previous step's all-reduced
+    partial sums; cmvg_pagerank_step_dev), so an iteration is step ->
+    exchange -> all_reduce queued on the stream with no host round trip.  With
+    l1_tolerance the L1 step is read back every iteration (the stop rule of
+    pagerank.hpp:86-91 needs it); without it the loop never synchronises.
+    `push` (a PushExchange) fuses the q exchange into the step kernel.
+    Returns (p_shard, iterations_run)."""
+    import torch
+    import torch.distributed as dist
+
+    a, b = plan.bounds(rank)
+    rows = b - a
+    dt = torch.float64
+    deg = degrees_shard
+    single = plan.world == 1 and not dist.is_initialized()  # one process: no collectives at all
+
+    def all_reduce(t):
+        if not single:
+            dist.all_reduce(t, group=group)
+
+    p = torch.full((rows,), 1.0 / n, dtype=dt, device=device)
+    q_loc = torch.where(deg > 0, p / deg.clamp(min=1).to(dt), torch.zeros_like(p))
+    part = [torch.zeros(2, dtype=dt, device=device), torch.zeros(2, dtype=dt, device=device)]
+    part[0][0] = p[deg == 0].sum()
+    all_reduce(part[0])
+    p_next = torch.empty_like(p)
+    if push is not None:
+        q_bufs = push.qb
+        push.prime(q_loc)
+    else:
+        q_pad = torch.zeros(plan.world * plan.chunk, dtype=dt, device=device)
+        q_next = torch.zeros(plan.chunk, dtype=dt, device=device)
+        q_send = torch.zeros(plan.chunk, dtype=dt, device=device)
+        q_send[:rows] = q_loc
+        if halo is not None:
+            recv = torch.empty(halo.recv_entries, dtype=dt, device=device)
+
+        def exchange(q_shard):
+            if single:
+                q_pad[:rows] = q_shard[:rows]
+                return
+            if halo is None:
+                dist.all_gather_into_tensor(q_pad, q_shard, group=group)
+                return
+            q_pad[a:b] = q_shard[:rows]
+            dist.all_to_all_single(recv, q_shard.index_select(0, halo.send_idx), output_split_sizes=halo.recv_counts,
+                                   input_split_sizes=halo.send_counts, group=group)
+            q_pad.index_copy_(0, halo.recv_cols, recv)
+
+        exchange(q_send)
+    it = 0
+    for it in range(1, iterations + 1):
+        prev, cur = part[(it - 1) % 2], part[it % 2]
+        p_prev = p if l1_tolerance is not None else None
+        if push is not None:
+            c, nx = (it - 1) % 2, it % 2
+            step_fn(q_bufs[c], alpha, prev, p_prev, p_next, q_bufs[nx][a:b], cur, push=push, parity=nx)
+        else:
+            q_next.zero_()
+            step_fn(q_pad[:n], alpha, prev, p_prev, p_next, q_next[:rows], cur)
+            exchange(q_next)
+        all_reduce(cur)
+        p, p_next = p_next, p
+        if l1_tolerance is not None and float(cur[1].item()) <= l1_tolerance:
+            break
+    return p, it
+
+
 class PushExchange:
     """State of the fused exchange (world <= 8): two q buffers per rank in
     torch symmetric memory (peer-mapped over NVLink), the peer pointer tables
@@ -179,6 +252,19 @@ class PushExchange:
         self.qb = [self.buf[:n], self.buf[n:]]
         self.mask = plan_push(halo, plan, rank, device)
         self.recv = torch.empty(halo.recv_entries, dtype=torch.float64, device=device)
+
+    def prime(self, q_shard):
+        """Iteration 0's q: own rows into buffer 0, the halo by one all_to_all
+        (every later one is pushed by the step kernel)."""
+        import torch.distributed as dist
+
+        a, b = self.plan.bounds(self.rank)
+        q0 = self.qb[0]
+        q0[a:b] = q_shard
+        dist.all_to_all_single(self.recv, q_shard.index_select(0, self.halo.send_idx),
+                               output_split_sizes=self.halo.recv_counts, input_split_sizes=self.halo.send_counts,
+                               group=self.group)
+        q0.index_copy_(0, self.halo.recv_cols, self.recv)
 
     def run(self, graph, degrees_shard, alpha: float = 0.15, iterations: int = 10,
             l1_tolerance: Optional[float] = None, dangling: str = "uniform"):
@@ -221,6 +307,21 @@ class PushExchange:
         return p, it
 
 
+def gpu_step_fn_dev(graph, degrees_shard, dangling: str = "uniform"):
+    """The production step for sharded_pagerank_dev: the dangling mass stays on
+    the device (cmvg_pagerank_step_dev); with a PushExchange the q exchange is
+    fused into the kernel."""
+
+    def step(q_full, alpha, dmass_dev, p_prev, p_next, q_next, part, push=None, parity=0):
+        if push is None:
+            graph.pagerank_step_dev(q_full, degrees_shard, alpha, dmass_dev, dangling, p_prev, p_next, q_next, part)
+        else:
+            graph.pagerank_step_dev(q_full, degrees_shard, alpha, dmass_dev, dangling, p_prev, p_next, q_next, part,
+                                    push_mask=push.mask, push_dst=push.dst[parity])
+
+    return step
+
+
 def gpu_step_fn(graph, degrees_shard, dangling: str = "uniform"):
     """The production step: one fused gather+update kernel on this rank's shard."""
 
@@ -236,6 +337,8 @@ def gather_to_rank0(x_shard, plan: ShardPlan, rank: int, group=None):
     import torch.distributed as dist
 
     a, b = plan.bounds(rank)
+    if plan.world == 1 and not dist.is_initialized():
+        return x_shard[: plan.n].cpu().numpy()
     buf = torch.zeros(plan.chunk, dtype=x_shard.dtype, device=x_shard.device)
     buf[: b - a] = x_shard
     full = torch.zeros(plan.world * plan.chunk, dtype=x_shard.dtype, device=x_shard.device)

@@ -12,7 +12,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from oracle import pyoracle as O
-from paper_1708_07271_b200.distributed import plan_halo, plan_shards, sharded_pagerank
+from paper_1708_07271_b200.distributed import plan_halo, plan_shards, sharded_pagerank, sharded_pagerank_dev
 
 
 def _free_port():
@@ -33,7 +33,7 @@ def _graph(n, seed):
     return O.Csr.build(edges, n)
 
 
-def _worker(rank, world, port, n, block_rows, iters, tol, out, use_halo=False):
+def _worker(rank, world, port, n, block_rows, iters, tol, out, use_halo=False, dev_scalars=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     g = _graph(n, 5)
@@ -45,6 +45,8 @@ def _worker(rank, world, port, n, block_rows, iters, tol, out, use_halo=False):
 
     def step(q_full, alpha, dmass, p_prev, p_next, q_next, part):
         # oracle restatement of one shard's fused step (CPU stand-in for the kernel)
+        if torch.is_tensor(dmass):  # sharded_pagerank_dev: the all-reduced partials of the previous step
+            dmass = float(dmass[0])
         qf = q_full.numpy()
         y = np.array([qf[co[ro[i]:ro[i + 1]]].sum() for i in range(a, b)])
         pn = alpha / n + (1 - alpha) * (y + dmass / n)
@@ -69,8 +71,9 @@ def _worker(rank, world, port, n, block_rows, iters, tol, out, use_halo=False):
             q_full = torch.where(keep, q_full, torch.full_like(q_full, float("nan")))
         step(q_full, *args)
 
-    p, it = sharded_pagerank(poisoned_step, torch.from_numpy(deg[a:b].astype(np.int64)), n, plan, rank, 0.15, iters,
-                             tol, halo=halo)
+    driver = sharded_pagerank_dev if dev_scalars else sharded_pagerank
+    p, it = driver(poisoned_step, torch.from_numpy(deg[a:b].astype(np.int64)), n, plan, rank, 0.15, iters, tol,
+                   halo=halo)
     full = torch.zeros(plan.world * plan.chunk, dtype=torch.float64)
     buf = torch.zeros(plan.chunk, dtype=torch.float64)
     buf[: b - a] = p
@@ -80,14 +83,17 @@ def _worker(rank, world, port, n, block_rows, iters, tol, out, use_halo=False):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,n,block_rows,iters,tol,halo", [(2, 5000, 1024, 30, None, False),
-                                                               (2, 3000, 1024, 200, 1e-9, False),
-                                                               (3, 4100, 512, 20, None, False),
-                                                               (2, 5000, 1024, 30, None, True),
-                                                               (3, 4100, 512, 40, 1e-9, True)])
-def test_sharded_pagerank_matches_oracle(tmp_path, world, n, block_rows, iters, tol, halo):
+@pytest.mark.parametrize("world,n,block_rows,iters,tol,halo,dev", [(2, 5000, 1024, 30, None, False, False),
+                                                                   (2, 3000, 1024, 200, 1e-9, False, False),
+                                                                   (3, 4100, 512, 20, None, False, False),
+                                                                   (2, 5000, 1024, 30, None, True, False),
+                                                                   (3, 4100, 512, 40, 1e-9, True, False),
+                                                                   (2, 5000, 1024, 30, None, True, True),
+                                                                   (3, 4100, 512, 40, 1e-9, False, True),
+                                                                   (2, 3000, 1024, 200, 1e-9, True, True)])
+def test_sharded_pagerank_matches_oracle(tmp_path, world, n, block_rows, iters, tol, halo, dev):
     out = str(tmp_path / "p.npy")
-    mp.spawn(_worker, args=(world, _free_port(), n, block_rows, iters, tol, out, halo), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), n, block_rows, iters, tol, out, halo, dev), nprocs=world, join=True)
     got = np.load(out)
     p, it = got[:n], int(got[n])
     g = _graph(n, 5)

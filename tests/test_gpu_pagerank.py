@@ -114,6 +114,37 @@ def test_pagerank_shard_steps(cuda):
     assert rel(p.cpu().numpy(), want) <= 1e-12
 
 
+def test_pagerank_shard_steps_device_dmass(cuda):
+    """cmvg_pagerank_step_dev: the dangling mass is read from device memory
+    (the previous step's summed partials), so no value crosses to the host
+    between iterations; three shards on one GPU, 40 iterations, no sync."""
+    import torch
+
+    from paper_1708_07271_b200.distributed import plan_shards
+
+    g = make_graph(3, n=(1 << 15) + 4000)
+    n = g.n
+    s = bv_of_transpose(g)
+    plan = plan_shards(n, 3, 1024)
+    deg = torch.from_numpy(g.out_degrees().astype(np.int32)).cuda()
+    shards = [(a, b, P.BvGraph(s, P.CreateOptions(row_begin=a, row_end=b)))
+              for a, b in (plan.bounds(r) for r in range(3))]
+    p = torch.full((n,), 1.0 / n, dtype=torch.float64, device="cuda")
+    q = torch.where(deg > 0, p / deg.clamp(min=1).double(), torch.zeros_like(p))
+    tot = torch.zeros(2, dtype=torch.float64, device="cuda")
+    tot[0] = p[deg == 0].sum()
+    parts = torch.zeros((3, 2), dtype=torch.float64, device="cuda")
+    for _ in range(40):
+        p_next, q_next = torch.empty_like(p), torch.empty_like(q)
+        for r, (a, b, dgs) in enumerate(shards):
+            dgs.pagerank_step_dev(q, deg[a:b], 0.15, tot, "uniform", p[a:b], p_next[a:b], q_next[a:b], parts[r])
+        tot = parts.sum(0)  # the all_reduce of the multi-GPU driver
+        p, q = p_next, q_next
+    want, _ = oracle_pr(g, iterations=40)
+    assert rel(p.cpu().numpy(), want) <= 1e-12
+    assert abs(float(p.sum()) - 1.0) <= 1e-10
+
+
 @pytest.mark.parametrize("window", [1536, 256])
 def test_pagerank_shard_steps_halo_read_set(cuda, window):
     """Each shard's step sees q only at its own rows and its read_set() (every
