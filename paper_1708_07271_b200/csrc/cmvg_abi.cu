@@ -252,6 +252,81 @@ void cmvg_default_opts(cmvg_create_opts* o) {
   o->row_end = 0;
 }
 
+}  // extern "C"
+
+// Copy this shard's slice of the host-built layouts to the device.
+static void upload_layouts(cmvg_graph* g, BvdLayout& L, bool s, bool t, bool f) {
+  const uint32_t bb = g->block_begin, be = g->block_begin + g->nblocks;
+  if (s) {
+    const uint64_t s0 = L.sblocks[bb].word_offset;
+    const uint64_t s1 = L.sblocks[be - 1].word_offset + L.sblocks[be - 1].nwords;
+    std::vector<BvdBlockInfo> sbl(L.sblocks.begin() + bb, L.sblocks.begin() + be);
+    for (auto& b : sbl) b.word_offset -= s0;
+    std::vector<uint32_t> sw(L.swords.begin() + s0, L.swords.begin() + s1);
+    sw.resize(sw.size() + 2 * kBvsGuardWords, 0);
+    g->swords.upload(sw.data(), sw.size());
+    g->sblocks.upload(sbl.data(), sbl.size());
+    g->heavy_items = L.sstats.heavy_chunks;
+    g->s_stream_bytes = (s1 - s0) * 4;
+    g->sstats = L.sstats;
+    g->have_bvs = true;
+  }
+  if (t) {
+    const uint64_t t0 = L.tblocks[bb].word_offset;
+    const uint64_t t1 = L.tblocks[be - 1].word_offset + L.tblocks[be - 1].nwords;
+    std::vector<BvdBlockInfo> tbl(L.tblocks.begin() + bb, L.tblocks.begin() + be);
+    for (auto& b : tbl) b.word_offset -= t0;
+    std::vector<uint32_t> tw(L.twords.begin() + t0, L.twords.begin() + t1);
+    tw.resize(tw.size() + 64, 0);
+    g->twords.upload(tw.data(), tw.size());
+    g->tblocks.upload(tbl.data(), tbl.size());
+    g->t_stream_bytes = (t1 - t0) * 4;
+    g->tstats = L.tstats;
+    g->tfar_begin = L.tblocks[bb].pad[0];
+    g->tfar_end = be < L.tblocks.size() ? L.tblocks[be].pad[0] : (uint32_t)L.tstats.far_slots;
+    g->tile_ptr.upload(L.tile_ptr.data(), L.tile_ptr.size());
+    g->tile_blk.upload(L.tile_blk.data(), std::max<size_t>(1, L.tile_blk.size()));
+    g->farp_ptr.upload(L.farp_ptr.data(), L.farp_ptr.size());
+    if (L.farp.empty()) L.farp.assign(2, 0u);
+    g->farp.upload(L.farp.data(), L.farp.size());
+    g->have_bvt = true;
+  }
+  if (f) {
+    const uint64_t f0 = L.fblocks[bb].word_offset;
+    const uint64_t f1 = L.fblocks[be - 1].word_offset + L.fblocks[be - 1].nwords;
+    std::vector<BvfBlockInfo> fbl(L.fblocks.begin() + bb, L.fblocks.begin() + be);
+    for (auto& b : fbl) b.word_offset -= f0;
+    std::vector<uint32_t> fw(L.fwords.begin() + f0, L.fwords.begin() + f1);
+    fw.resize(fw.size() + 64, 0);
+    g->fwords.upload(fw.data(), fw.size());
+    g->fblocks.upload(fbl.data(), fbl.size());
+    g->f_stream_bytes = (f1 - f0) * 4;
+    g->fstats = L.fstats;
+  }
+}
+
+namespace cmvg {
+// The sliced (matmat) and target-sorted (scatter) layouts are built on their
+// first use: a handle that only gathers (A x, PageRank) never pays for them.
+void ensure_layouts(cmvg_graph* g, bool s, bool t) {
+  if ((!s || g->have_bvs) && (!t || g->have_bvt)) return;
+  std::lock_guard<std::mutex> lk(g->layout_mu);
+  s = s && !g->have_bvs;
+  t = t && !g->have_bvt;
+  if (!s && !t) return;
+  BvDecoded dec = bv_decode(*g->host_stream);
+  BvdOptions bo = g->build_opts;
+  bo.bvs = s;
+  bo.bvt = t;
+  bo.bvf = false;
+  BvdLayout L = build_bvd(dec, g->host_stream->params, bo);
+  DeviceGuard dg(g->device);
+  upload_layouts(g, L, s, t, false);
+}
+}  // namespace cmvg
+
+extern "C" {
+
 int cmvg_create(const cmvg_bvstream* s, const cmvg_create_opts* opts_in, cmvg_graph** out) {
   return guarded([&] {
     require(s && out, "null argument");
@@ -281,6 +356,8 @@ int cmvg_create(const cmvg_bvstream* s, const cmvg_create_opts* opts_in, cmvg_gr
     BvdOptions bo;
     bo.block_rows = o.block_rows;
     bo.window = o.window;
+    bo.bvs = false;  // the sliced (matmat) and target-sorted (scatter) layouts are built on first use
+    bo.bvt = false;
     BvdLayout L = build_bvd(dec, bs.params, bo);
 
     auto g = std::make_unique<cmvg_graph>();
@@ -292,10 +369,8 @@ int cmvg_create(const cmvg_bvstream* s, const cmvg_create_opts* opts_in, cmvg_gr
     g->row_begin = o.row_begin;
     g->row_end = row_end;
     g->block_begin = o.row_begin / o.block_rows;
-    uint32_t block_end = (uint32_t)(((uint64_t)row_end + o.block_rows - 1) / o.block_rows);
+    const uint32_t block_end = (uint32_t)(((uint64_t)row_end + o.block_rows - 1) / o.block_rows);
     g->nblocks = block_end - g->block_begin;
-    // staging cap: covers 99.5% of the blocks, at most 12K words (48 KB) so
-    // every kernel's shared-memory plan fits; larger blocks decode from global
     g->stream_cap_words = o.stream_cap_words
                               ? o.stream_cap_words
                               : std::min<uint32_t>(12288, std::max<uint32_t>(1024, (L.stats.p995_block_words + 255) & ~255u));
@@ -306,80 +381,39 @@ int cmvg_create(const cmvg_bvstream* s, const cmvg_create_opts* opts_in, cmvg_gr
     g->threads = o.lanes;
     g->bv_bits = bs.nbits;
     g->nseg = bs.segment_bit_offsets.size() - 1;
+    g->host_stream = std::make_shared<const BvStream>(bs);
+    g->build_opts = bo;
 
     DeviceGuard dg(o.device);
-    // shard slice of the layout
-    uint64_t w0 = L.blocks[g->block_begin].word_offset;
-    uint64_t w1 = L.blocks[block_end - 1].word_offset + L.blocks[block_end - 1].nwords;
-    std::vector<BvdBlockInfo> bl(L.blocks.begin() + g->block_begin, L.blocks.begin() + block_end);
-    for (auto& b : bl) b.word_offset -= w0;
-    (void)bl;  // BV-D stays on the host (layout export); the kernels read BV-S / BV-T
-    {
-      const uint64_t s0 = L.sblocks[g->block_begin].word_offset;
-      const uint64_t s1 = L.sblocks[block_end - 1].word_offset + L.sblocks[block_end - 1].nwords;
-      std::vector<BvdBlockInfo> sbl(L.sblocks.begin() + g->block_begin, L.sblocks.begin() + block_end);
-      for (auto& b : sbl) b.word_offset -= s0;
-      std::vector<uint32_t> sw(L.swords.begin() + s0, L.swords.begin() + s1);
-      sw.resize(sw.size() + 2 * kBvsGuardWords, 0);
-      g->swords.upload(sw.data(), sw.size());
-      g->sblocks.upload(sbl.data(), sbl.size());
-      g->heavy_items = L.sstats.heavy_chunks;
-      g->s_stream_bytes = (s1 - s0) * 4;
-      {  // read set: the blocks' x-windows and their out-of-window columns (bitmap, O(n))
-        std::vector<uint64_t> bm(((uint64_t)bs.n + 63) / 64, 0);
-        auto mark = [&](uint64_t c) { bm[c >> 6] |= 1ull << (c & 63); };
-        for (uint32_t b = g->block_begin; b < block_end; ++b) {
-          const uint64_t w0 = L.sblocks[b].wlo, w1 = std::min<uint64_t>(bs.n, w0 + L.dims.window);
-          for (uint64_t c = w0; c < w1; ++c) mark(c);
-          for (uint64_t q = L.rfar_ptr[b]; q < L.rfar_ptr[b + 1]; ++q) mark(L.rfar[q]);
-        }
-        std::vector<uint32_t>& rs = g->read_set;
-        rs.clear();
-        for (uint64_t wi = 0; wi < bm.size(); ++wi)
-          for (uint64_t v = bm[wi]; v; v &= v - 1) rs.push_back((uint32_t)(wi * 64 + __builtin_ctzll(v)));
+    {  // read set: the blocks' x-windows and their out-of-window columns (bitmap, O(n))
+      std::vector<uint64_t> bm(((uint64_t)bs.n + 63) / 64, 0);
+      auto mark = [&](uint64_t c) { bm[c >> 6] |= 1ull << (c & 63); };
+      for (uint32_t b = g->block_begin; b < block_end; ++b) {
+        const uint64_t w0 = L.blocks[b].wlo, w1 = std::min<uint64_t>(bs.n, w0 + L.dims.window);
+        for (uint64_t c = w0; c < w1; ++c) mark(c);
+        for (uint64_t q = L.rfar_ptr[b]; q < L.rfar_ptr[b + 1]; ++q) mark(L.rfar[q]);
       }
-      g->win_need.resize(sbl.size());
-      g->far_need.resize(sbl.size());
+      std::vector<uint32_t>& rs = g->read_set;
+      rs.clear();
+      for (uint64_t wi = 0; wi < bm.size(); ++wi)
+        for (uint64_t v = bm[wi]; v; v &= v - 1) rs.push_back((uint32_t)(wi * 64 + __builtin_ctzll(v)));
+    }
+    g->win_need.resize(g->nblocks);
+    g->far_need.resize(g->nblocks);
+    {
       uint64_t pm = 0, fm = 0;
-      for (size_t q = 0; q < sbl.size(); ++q) {
-        pm = std::max<uint64_t>(pm, (uint64_t)sbl[q].wlo + L.dims.window);
+      for (uint32_t q = 0; q < g->nblocks; ++q) {
+        const uint32_t b = g->block_begin + q;
+        pm = std::max<uint64_t>(pm, (uint64_t)L.blocks[b].wlo + L.dims.window);
         g->win_need[q] = (uint32_t)std::min<uint64_t>(pm, bs.n);
-        const uint32_t b = g->block_begin + (uint32_t)q;
         for (uint64_t r = L.rfar_ptr[b]; r < L.rfar_ptr[b + 1]; ++r) fm = std::max<uint64_t>(fm, (uint64_t)L.rfar[r] + 1);
         g->far_need[q] = (uint32_t)std::min<uint64_t>(fm, bs.n);
       }
-      // BV-T
-      const uint64_t t0 = L.tblocks[g->block_begin].word_offset;
-      const uint64_t t1 = L.tblocks[block_end - 1].word_offset + L.tblocks[block_end - 1].nwords;
-      std::vector<BvdBlockInfo> tbl(L.tblocks.begin() + g->block_begin, L.tblocks.begin() + block_end);
-      for (auto& b : tbl) b.word_offset -= t0;
-      std::vector<uint32_t> tw(L.twords.begin() + t0, L.twords.begin() + t1);
-      tw.resize(tw.size() + 64, 0);
-      g->twords.upload(tw.data(), tw.size());
-      g->tblocks.upload(tbl.data(), tbl.size());
-      g->t_stream_bytes = (t1 - t0) * 4;
-      g->tstats = L.tstats;
-      g->tfar_begin = L.tblocks[g->block_begin].pad[0];
-      g->tfar_end = block_end < L.tblocks.size() ? L.tblocks[block_end].pad[0] : (uint32_t)L.tstats.far_slots;
-      g->tile_ptr.upload(L.tile_ptr.data(), L.tile_ptr.size());
-      g->tile_blk.upload(L.tile_blk.data(), std::max<size_t>(1, L.tile_blk.size()));
-      g->farp_ptr.upload(L.farp_ptr.data(), L.farp_ptr.size());
-      if (L.farp.empty()) L.farp.assign(2, 0u);
-      g->farp.upload(L.farp.data(), L.farp.size());
-      g->sstats = L.sstats;
-      // BV-F
-      const uint64_t f0 = L.fblocks[g->block_begin].word_offset;
-      const uint64_t f1 = L.fblocks[block_end - 1].word_offset + L.fblocks[block_end - 1].nwords;
-      std::vector<BvfBlockInfo> fbl(L.fblocks.begin() + g->block_begin, L.fblocks.begin() + block_end);
-      for (auto& b : fbl) b.word_offset -= f0;
-      std::vector<uint32_t> fw(L.fwords.begin() + f0, L.fwords.begin() + f1);
-      fw.resize(fw.size() + 64, 0);
-      g->fwords.upload(fw.data(), fw.size());
-      g->fblocks.upload(fbl.data(), fbl.size());
-      g->f_stream_bytes = (f1 - f0) * 4;
-      g->fstats = L.fstats;
     }
+    upload_layouts(g.get(), L, false, false, true);
     // stats of the shard
+    const uint64_t w0 = L.blocks[g->block_begin].word_offset;
+    const uint64_t w1 = L.blocks[block_end - 1].word_offset + L.blocks[block_end - 1].nwords;
     g->stats.stream_bytes = (w1 - w0) * 4;
     g->stats.block_table_bytes = (uint64_t)g->nblocks * sizeof(BvdBlockInfo);
     g->stats.row_bits = L.stats.row_bits;  // whole graph

@@ -963,8 +963,8 @@ BvdLayout build_bvd(const BvDecoded& dec, const BvParams& bp, const BvdOptions& 
       L.blocks[b].nwords = (uint32_t)(out.nbits / 32);
       L.blocks[b].nesc = (uint32_t)(escs.size() / 4);
       auto tB = std::chrono::steady_clock::now();
-      emit_bvs(rps.data(), meta.data(), body, nr, lo, W, bp.min_interval, sstream[b], bst[b]);
-      {
+      if (opt.bvs) emit_bvs(rps.data(), meta.data(), body, nr, lo, W, bp.min_interval, sstream[b], bst[b]);
+      if (opt.bvf) {
         uint64_t maxdeg = 0;
         for (uint32_t k = 0; k < nr; ++k) maxdeg = std::max<uint64_t>(maxdeg, g.deg(r0 + k));
         emit_bvf(rps.data(), meta.data(), nr, lo, W, maxdeg, fstream[b], L.fblocks[b], fst[b]);
@@ -988,7 +988,7 @@ BvdLayout build_bvd(const BvDecoded& dec, const BvParams& bp, const BvdOptions& 
         fc.erase(std::unique(fc.begin(), fc.end()), fc.end());
       }
       auto tD = std::chrono::steady_clock::now();
-      emit_bvt(rps.data(), meta.data(), nr, B, lo, W, tstream[b], tfar[b], tst[b]);
+      if (opt.bvt) emit_bvt(rps.data(), meta.data(), nr, B, lo, W, tstream[b], tfar[b], tst[b]);
       auto tE = std::chrono::steady_clock::now();
       g_tim[0] += std::chrono::duration_cast<std::chrono::microseconds>(tB - tA).count();
       g_tim[1] += std::chrono::duration_cast<std::chrono::microseconds>(tC - tB).count();
@@ -1033,7 +1033,7 @@ BvdLayout build_bvd(const BvDecoded& dec, const BvParams& bp, const BvdOptions& 
     L.sblocks[b].nwords = (uint32_t)sstream[b].size();
     L.sblocks[b].nesc = 0;
     if (hitems > 0xffffffffull) throw std::runtime_error("BV-S: too many heavy-row work items");
-    sstream[b][3] = (uint32_t)hitems;  // the block's first heavy work item (global)
+    if (!sstream[b].empty()) sstream[b][3] = (uint32_t)hitems;  // the block's first heavy work item (global)
     hitems += bst[b].heavy_chunks;
     L.sstats.heavy_chunks += bst[b].heavy_chunks;
     soff += sstream[b].size();

@@ -9,6 +9,9 @@ namespace cmvg {
 struct BvdOptions {
   uint32_t block_rows = 1024;
   uint32_t window = 2048;
+  bool bvs = true;  // build the sliced layout (matmat)
+  bool bvt = true;  // build the target-sorted layout (scatter)
+  bool bvf = true;  // build the flat term layout (gather / PageRank)
 };
 
 struct BvdStats {

@@ -156,6 +156,11 @@ struct cmvg_graph {
   BvfStats fstats;
   std::atomic<unsigned> fgather_attr{0};
   std::atomic<uint32_t> fgather_res{0};  // resident CTAs of the BV-F gather (L2 prefetch distance)
+  // lazily built layouts (ensure_layouts): the host stream and build options
+  std::shared_ptr<const BvStream> host_stream;
+  BvdOptions build_opts;
+  std::atomic<bool> have_bvs{false}, have_bvt{false};
+  std::mutex layout_mu;
   // BV-T layout (this shard): scatter; combine tables (whole graph)
   DevBuf twords, tblocks, tile_ptr, tile_blk, farp_ptr, farp;
   uint32_t tfar_begin = 0, tfar_end = 0;
@@ -271,6 +276,8 @@ struct StreamScratch {
   StreamScratch(const StreamScratch&) = delete;
   StreamScratch& operator=(const StreamScratch&) = delete;
 };
+
+void ensure_layouts(cmvg_graph* g, bool sliced, bool target);
 
 // kernel entry points implemented in the other translation units
 template <typename XT, typename YT, bool PR>

@@ -6,6 +6,7 @@
 namespace cmvg {
 
 void launch_matmat(cmvg_graph* g, const float* X, float* Y, uint32_t k, cudaStream_t st) {
+  ensure_layouts(g, true, false);
   const BvsMmSmem L = bvs_mm_smem_layout(g->dims);
   CUDA_TRY(cudaFuncSetAttribute(bvs_matmat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
   for (uint32_t c0 = 0; c0 < k; c0 += kMmCols) {

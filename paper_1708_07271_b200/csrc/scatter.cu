@@ -7,6 +7,7 @@ namespace cmvg {
 
 template <typename T>
 void launch_scatter(cmvg_graph* g, const T* x, T* y, cudaStream_t st) {
+  ensure_layouts(g, false, true);
   const size_t W = g->dims.window;
   const size_t nst = (size_t)g->nblocks * W;
   const size_t nfar = (size_t)g->tfar_end - g->tfar_begin;
