@@ -340,7 +340,7 @@ int cmvg_create(const cmvg_bvstream* s, const cmvg_create_opts* opts_in, cmvg_gr
     require(o.lanes >= 32 && o.lanes <= 256 && (o.lanes & (o.lanes - 1)) == 0,
             "lanes (threads per block) must be a power of two in [32, 256]");
     require(o.block_rows <= 4 * o.lanes, "block_rows must be <= 4 x threads per block");
-    require(o.window <= kBvfXPer * kBvfThreads, "window must be <= 2048 entries");
+    require(o.window <= 3968, "window must be <= 3968 entries (the 13-bit BV-F term index)");
     require(o.interval_mode <= CMVG_INTERVALS_DIRECT, "bad interval_mode");
     uint32_t row_end = o.row_end ? o.row_end : bs.n;
     require(o.row_begin < row_end && row_end <= bs.n, "bad shard row range");

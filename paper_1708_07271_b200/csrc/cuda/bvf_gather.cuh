@@ -100,11 +100,13 @@ struct BvfTerms {
   uint32_t f0b;  // F0 * 8
   // one term: +-table[index] split at the block grid; bit 31 of `signw` is the
   // term's minus flag; a row end stores the row's sum at rowp and moves on
-  __device__ __forceinline__ void term(uint32_t c, uint32_t signw, double& ah, double& al, uint32_t& rowp) const {
+  // ev: the term's x value when it is an escape (loaded ahead, see esc_group)
+  __device__ __forceinline__ void term(uint32_t c, uint32_t signw, double& ah, double& al, uint32_t& rowp,
+                                       XT ev = XT(0)) const {
     const uint32_t off = (c << 3) & (kBvfIdxMask << 3);
     const bool e = ESC && (c & kBvfEsc);
     double v;
-    if (e) v = (double)__ldg(xfar + __ldg(esc + (off >> 3)));
+    if (e) v = (double)ev;
     else v = lds_f64(tab + off);
     const double sg = __hiloint2double((int)((signw & 0x80000000u) | 0x3ff00000u), 0);  // +-1
     if (SPLIT) {
@@ -127,6 +129,24 @@ struct BvfTerms {
     term(w & 0xffffu, w << 16, ah, al, rowp);
     term(w >> 16, w, ah, al, rowp);
   }
+  // escape blocks: 8 terms at a time, their escape columns and then their x
+  // values loaded together (independent loads in flight) before the sums
+  __device__ __forceinline__ void esc_group(const uint32_t* w4, double& ah, double& al, uint32_t& rowp) const {
+    uint32_t col[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t c = (w4[i >> 1] >> (16 * (i & 1))) & 0xffffu;
+      col[i] = (c & kBvfEsc) ? __ldg(esc + (c & kBvfIdxMask)) : 0xffffffffu;
+    }
+    XT ev[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ev[i] = col[i] != 0xffffffffu ? __ldg(xfar + col[i]) : XT(0);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      term(w4[i] & 0xffffu, w4[i] << 16, ah, al, rowp, ev[2 * i]);
+      term(w4[i] >> 16, w4[i], ah, al, rowp, ev[2 * i + 1]);
+    }
+  }
 };
 
 template <typename XT, bool SPLIT, bool ESC>
@@ -143,8 +163,13 @@ __device__ __forceinline__ void bvf_chunk(const BvfTerms<XT, SPLIT, ESC>& tm, co
 #pragma unroll
       for (int i = 0; i < 8; ++i) nx[i] = __ldg(cw + (size_t)(q + i) * nact);
     }
+    if constexpr (ESC) {
+      tm.esc_group(w, ah, al, rowp);
+      tm.esc_group(w + 4, ah, al, rowp);
+    } else {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) tm.word(w[i], ah, al, rowp);
+      for (int i = 0; i < 8; ++i) tm.word(w[i], ah, al, rowp);
+    }
     if (!more) break;
 #pragma unroll
     for (int i = 0; i < 8; ++i) w[i] = nx[i];
@@ -200,7 +225,10 @@ __global__ void __launch_bounds__(kBvfThreads, 4)
 #pragma unroll
   for (int i = 0; i < 8; ++i) w0[i] = active ? __ldg(cw + (size_t)i * nact) : 0u;
   const uint32_t srow = active ? (uint32_t)reinterpret_cast<const uint16_t*>(bs)[tid] : 0u;
-  const uint32_t E = CW ? (CW + kBvfThreads - 1) / kBvfThreads : (W + kBvfThreads - 1) / kBvfThreads;  // <= kBvfXPer
+  const uint32_t E = CW ? (CW + kBvfThreads - 1) / kBvfThreads : (W + kBvfThreads - 1) / kBvfThreads;
+  // windows of more than kBvfXPer entries per thread (W > 2048, generic shape
+  // only) stage through shared memory instead of registers
+  const bool wide = CW == 0 && E > kBvfXPer;
   const uint32_t j0 = tid * E;
   // a full chunk of an even count: paired 16-byte loads and stores
   const bool full = !(E & 1u) && j0 + E <= W && bi.wlo + j0 + E <= g.n && !(bi.wlo & 1u) &&
@@ -212,7 +240,7 @@ __global__ void __launch_bounds__(kBvfThreads, 4)
     for (uint32_t k = 0; k < kBvfXPer; k += 2) {
       const uint32_t j = j0 + k, c = bi.wlo + j;
       xv[k] = xv[k + 1] = 0.0;
-      if (k < E) {
+      if (k < E && !wide) {
         if (full) {
           const P2 v2 = __ldg(reinterpret_cast<const P2*>(x + c));
           xv[k] = (double)v2.x;
@@ -236,12 +264,20 @@ __global__ void __launch_bounds__(kBvfThreads, 4)
     if (e == 0x7ffu) nonfin = 1;
     else emax = max(emax, e);
   };
+  if (wide) {
+    for (uint32_t k = 0; k < E; ++k) {
+      const uint32_t j = j0 + k, c = bi.wlo + j;
+      const double v = (j < W && c < g.n) ? (double)__ldg(x + c) : 0.0;
+      if (j < W) tab[j] = v;
+      see(v);
+    }
+  }
 #pragma unroll
   for (uint32_t k = 0; k < kBvfXPer; k += 2) {
     see(xv[k]);
     see(xv[k + 1]);
     const uint32_t j = j0 + k;
-    if (k < E) {
+    if (k < E && !wide) {
       if (full) {
         *reinterpret_cast<double2*>(tab + j) = make_double2(xv[k], xv[k + 1]);
       } else {
@@ -282,9 +318,22 @@ __global__ void __launch_bounds__(kBvfThreads, 4)
   // ---- window prefix F (exclusive): F hi = sum h (exact), F lo = sum l
   {
     double sh = 0.0, sl = 0.0;
+    if (wide) {
+      for (uint32_t k = 0; k < E; ++k) {
+        const uint32_t j = j0 + k;
+        const double v = j < W ? tab[j] : 0.0;
+        if (kSplit) {
+          const double h = (v + sigma) - sigma;
+          sh += h;
+          sl += v - h;
+        } else {
+          sh += v;
+        }
+      }
+    }
 #pragma unroll
     for (uint32_t k = 0; k < kBvfXPer; ++k) {
-      if (k < E) {
+      if (k < E && !wide) {
         const double v = xv[k];
         if (kSplit) {
           const double h = (v + sigma) - sigma;
@@ -317,8 +366,25 @@ __global__ void __launch_bounds__(kBvfThreads, 4)
       blo += misc[16 + 2 * w + 1];
     }
     double* fhi = tab + F0;
+    if (wide) {
+      for (uint32_t k = 0; k < E; ++k) {
+        const uint32_t j = j0 + k;
+        if (j >= W) break;
+        const double v = tab[j];
+        fhi[j] = bh;
+        if (kSplit) flo[j] = blo;
+        if (kSplit) {
+          const double h = (v + sigma) - sigma;
+          bh += h;
+          blo += v - h;
+        } else {
+          bh += v;
+        }
+      }
+    }
 #pragma unroll
     for (uint32_t k = 0; k < kBvfXPer; k += 2) {
+      if (wide) break;
       const uint32_t j = j0 + k;
       double h0 = bh, l0 = blo;
       if (k < E) {

@@ -45,6 +45,13 @@ def test_bvf_social_unbounded_chains_and_escapes():
     assert info["max_depth"] > 3
 
 
+@pytest.mark.parametrize("window", [3072, 3968])
+def test_bvf_wide_window_social(window):
+    # community-sized windows (the power-law C4 graph's 4096-row communities)
+    g = make_graph(4, n=9000)
+    _check(g, bv_params(4), window=window, max_depth=1 << 30)
+
+
 def test_bvf_small_window_forces_slots_and_escapes():
     # a narrow window puts most columns outside it: far slots, then escapes
     g = make_graph(2, n=6000)

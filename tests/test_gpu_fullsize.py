@@ -85,7 +85,7 @@ def test_c4_gather_f32_full_size(cuda):
     g = make_graph(4)
     assert g.n == CONFIGS[4]["n"]
     s = P.BvStream.encode(g, bv_params(4))
-    dg = P.BvGraph(s)
+    dg = P.BvGraph(s, P.CreateOptions(window=3968))  # a window the size of the 4096-row communities
     assert dg.info()["max_depth"] > 3  # unbounded reference chains (R = infinity)
     x = x_uniform(g.n, 23).astype(np.float32)
     want = O.matvec_csr_raw(g.n, g.row_offsets, g.columns, x.astype(np.float64), O.threads())

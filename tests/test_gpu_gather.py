@@ -66,7 +66,7 @@ def test_gather_matches_matvec_ref(cuda):
     assert max_rel_err(dg.matvec(x), want) <= F64_TOL
 
 
-@pytest.mark.parametrize("lanes,block_rows,window", [(256, 1024, 2048), (256, 1024, 1536), (256, 1024, 1024),
+@pytest.mark.parametrize("lanes,block_rows,window", [(256, 1024, 2048), (256, 1024, 1536), (256, 1024, 1024), (256, 1024, 3968),
                                                       (256, 1024, 512), (256, 1024, 128)])
 def test_gather_layout_variants(cuda, lanes, block_rows, window):
     g = make_graph(2, n=(1 << 16) + 777)  # ragged last block

@@ -28,7 +28,17 @@ import paper_1708_07271_b200 as P  # noqa: E402
 from oracle import pyoracle as O  # noqa: E402
 
 SEED = 0x170807271
-PEAK = 6539.2
+
+
+def measured_peak():
+    """HBM GB/s from MEASURED_PEAKS.json (driver-written), else the profiling recipe's fallback."""
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        return 6650.0
+
+
+PEAK = measured_peak()
 
 
 def log(*a):
@@ -76,7 +86,7 @@ def graph(cfg, n):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="1,2,3,4,5")
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "configs_r1.json"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "configs_r2.json"))
     ap.add_argument("--scale", type=int, default=0, help="subtract from every n_log2 (quick runs)")
     args = ap.parse_args()
     res = {"gpu": torch.cuda.get_device_name(0), "host_threads": O.threads()}
@@ -107,10 +117,14 @@ def main():
         r["bits_per_edge"] = st["stream_bits"] / g.m
         r["max_depth"] = st["max_depth"]
         t0 = time.time()
-        dg = P.BvGraph(s, P.CreateOptions(window=1536))
+        dg = P.BvGraph(s, P.CreateOptions(window=3968 if cfg == 4 else 1536))  # C4: community-sized window
         r["handle_s"] = time.time() - t0
         info = dg.info()
-        r["device_layout_bytes"] = info["bvd_stream_bytes"] + info["bvd_block_table_bytes"]
+        r["device_layout"] = "BV-F (gather, PageRank)"
+        r["device_layout_bytes"] = info["bvf_stream_bytes"] + info["bvd_block_table_bytes"]
+        r["bvf_terms"] = info["bvf_terms"]
+        r["bvf_pad_terms"] = info["bvf_pad_terms"]
+        r["bvf_esc_terms"] = info["bvf_esc_terms"]
         r["window_coverage"] = info["window_coverage"]
         ro = src.row_offsets
         co = src.columns
@@ -142,6 +156,7 @@ def main():
                     wl = og.matvec(xh.astype(np.float64), th)
                     del og
                     ts_ = time_launch(lambda: dg.matvec(xd, yd, form="scatter"), flush=flush)
+                    r["bvt_stream_bytes"] = dg.info()["bvt_stream_bytes"]
                     e = rel_err(yd.double().cpu().numpy(), wl)
                     r[f"scatter_{dt}"] = {"s": ts_, "Gedges_s": g.m / ts_ / 1e9, "max_rel_err": e, "tol": tol,
                                           "pass": bool(e <= tol), "roofline_frac": alg / ts_ / 1e9 / PEAK}
@@ -167,7 +182,8 @@ def main():
             alg = S8 + n * (8 + 8 + 4) * 50 / 50
             r["pagerank"] = {"iterations": int(it), "s": tpr, "iter_per_s": it / tpr, "max_rel_err": e, "tol": 1e-12,
                              "sum_minus_1": float(abs(pn.sum() - 1.0)), "pass": bool(e <= 1e-12 and abs(pn.sum() - 1) <= 1e-10),
-                             "roofline_frac_per_iter": (S8 + n * 20) / (tpr / it) / 1e9 / PEAK}
+                             "roofline_frac_per_iter": (S8 + n * 28) / (tpr / it) / 1e9 / PEAK,
+                             "alg_bytes_per_iter": "ceil(S/8) + 8n (q) + 8n (p) + 8n (q') + 4n (d)"}
             del og
         if cfg == 5:
             k = 16
@@ -175,6 +191,7 @@ def main():
             Xd = torch.from_numpy(X).cuda()
             Yd = torch.empty_like(Xd)
             tm = time_launch(lambda: dg.matmat(Xd, Yd), reps=5, flush=flush)
+            r["bvs_stream_bytes"] = dg.info()["bvs_stream_bytes"]
             Y = Yd.cpu().numpy()
             errs = []
             for c in range(k):
