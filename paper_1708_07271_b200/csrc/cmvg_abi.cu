@@ -300,6 +300,25 @@ static void upload_layouts(cmvg_graph* g, BvdLayout& L, bool s, bool t, bool f) 
     fw.resize(fw.size() + 64, 0);
     g->fwords.upload(fw.data(), fw.size());
     g->fblocks.upload(fbl.data(), fbl.size());
+    {  // flat escape columns (the pre-gather's index list)
+      std::vector<uint32_t> ec, eb(fbl.size() + 1, 0);
+      g->fesc_base_h.assign(fbl.size() + 1, 0);
+      for (size_t q = 0; q < fbl.size(); ++q) {
+        const BvfBlockInfo& b = fbl[q];
+        if (b.flags & kBvfFlagEsc) {
+          const uint32_t* es = fw.data() + b.word_offset + b.esc_off;
+          const uint32_t ne = es[b.nact];
+          const uint32_t* cols = es + bvf_align4(b.nact + 1u);
+          ec.insert(ec.end(), cols, cols + ne);
+        }
+        if (ec.size() > 0xffffffffull) throw std::runtime_error("BV-F: more than 2^32 escape terms in one shard");
+        eb[q + 1] = (uint32_t)ec.size();
+        g->fesc_base_h[q + 1] = ec.size();
+      }
+      ec.resize(ec.size() + 4, 0u);
+      g->fesc.upload(ec.data(), ec.size());
+      g->fesc_base.upload(eb.data(), eb.size());
+    }
     g->f_stream_bytes = (f1 - f0) * 4;
     g->fstats = L.fstats;
   }

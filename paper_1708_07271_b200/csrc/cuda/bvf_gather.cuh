@@ -39,6 +39,7 @@ struct BvfDev {
   uint32_t row_begin;    // first row of the shard (y is shard-relative)
   uint32_t nlaunch;
   uint32_t ahead;  // L2 prefetch distance in blocks (about the CTAs resident at once; 0 = none)
+  const uint32_t* esc_base;  // first escape of each block of this launch (index into xe)
 };
 
 struct __align__(16) RowD {
@@ -94,8 +95,7 @@ template <typename XT, bool SPLIT, bool ESC>
 struct BvfTerms {
   uint32_t tab;    // shared address: x / slots / zero / F hi, 8 bytes per term index
   uint32_t flo_b;  // shared address of F lo minus F0 * 8 (the term's byte offset indexes it)
-  const uint32_t* esc;  // escape columns of this chunk (ESC)
-  const XT* xfar;
+  const XT* esc;  // x values of this chunk's escape terms, in term order (ESC; bvf_esc_gather)
   double sigma;
   uint32_t f0b;  // F0 * 8
   // one term: +-table[index] split at the block grid; bit 31 of `signw` is the
@@ -129,18 +129,15 @@ struct BvfTerms {
     term(w & 0xffffu, w << 16, ah, al, rowp);
     term(w >> 16, w, ah, al, rowp);
   }
-  // escape blocks: 8 terms at a time, their escape columns and then their x
-  // values loaded together (independent loads in flight) before the sums
+  // escape blocks: 8 terms at a time, the x values of their escapes (gathered
+  // ahead by bvf_esc_gather) loaded together before the sums
   __device__ __forceinline__ void esc_group(const uint32_t* w4, double& ah, double& al, uint32_t& rowp) const {
-    uint32_t col[8];
+    XT ev[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const uint32_t c = (w4[i >> 1] >> (16 * (i & 1))) & 0xffffu;
-      col[i] = (c & kBvfEsc) ? __ldg(esc + (c & kBvfIdxMask)) : 0xffffffffu;
+      ev[i] = (c & kBvfEsc) ? __ldg(esc + (c & kBvfIdxMask)) : XT(0);
     }
-    XT ev[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) ev[i] = col[i] != 0xffffffffu ? __ldg(xfar + col[i]) : XT(0);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       term(w4[i] & 0xffffu, w4[i] << 16, ah, al, rowp, ev[2 * i]);
@@ -176,11 +173,33 @@ __device__ __forceinline__ void bvf_chunk(const BvfTerms<XT, SPLIT, ESC>& tm, co
   }
 }
 
+// xe[i] = x[esc[i]] for the escape terms of a launch's blocks (columns outside
+// a block's x-window and far slots): one independent, fully parallel gather,
+// so the term loop streams the values instead of chasing column -> x.
+template <typename XT>
+__global__ void __launch_bounds__(256) bvf_esc_gather(const uint32_t* __restrict__ esc, uint64_t cnt,
+                                                      const XT* __restrict__ x, XT* __restrict__ xe) {
+  const uint64_t step = (uint64_t)gridDim.x * blockDim.x;
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 3 * step < cnt; i += 4 * step) {  // four independent gathers in flight per thread
+    uint32_t c[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) c[k] = __ldg(esc + i + k * step);
+    XT v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = __ldg(x + c[k]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) xe[i + k * step] = v[k];
+  }
+  for (; i < cnt; i += step) xe[i] = __ldg(x + __ldg(esc + i));
+}
+
 // CW, CB: compile-time window and block rows (0 = from BvfDev): the default
 // shape gets constant loop bounds and shared-memory offsets.
 template <typename XT, typename YT, bool PR, uint32_t CW = 0, uint32_t CB = 0>
 __global__ void __launch_bounds__(kBvfThreads, 4)
-    bvf_gather_kernel(BvfDev g, const XT* __restrict__ x, const XT* xfar, YT* __restrict__ y, PrArgs pr) {
+    bvf_gather_kernel(BvfDev g, const XT* __restrict__ x, const XT* xfar, const XT* __restrict__ xe,
+                      YT* __restrict__ y, PrArgs pr) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr bool kSplit = sizeof(XT) == 8;  // fp32 x: plain fp64 sums (error far inside the fp32 tolerance)
   const uint32_t W = CW ? CW : g.W, B = CB ? CB : g.B;
@@ -264,11 +283,11 @@ __global__ void __launch_bounds__(kBvfThreads, 4)
     if (e == 0x7ffu) nonfin = 1;
     else emax = max(emax, e);
   };
-  if (wide) {
-    for (uint32_t k = 0; k < E; ++k) {
-      const uint32_t j = j0 + k, c = bi.wlo + j;
-      const double v = (j < W && c < g.n) ? (double)__ldg(x + c) : 0.0;
-      if (j < W) tab[j] = v;
+  if (wide) {  // lane-consecutive (coalesced loads, conflict-free stores)
+    for (uint32_t j = tid; j < W; j += kBvfThreads) {
+      const uint32_t c = bi.wlo + j;
+      const double v = c < g.n ? (double)__ldg(x + c) : 0.0;
+      tab[j] = v;
       see(v);
     }
   }
@@ -288,11 +307,13 @@ __global__ void __launch_bounds__(kBvfThreads, 4)
   }
   see(fv);
   if (tid < nslot) tab[W + tid] = fv;
-  if (kSplit && (bi.flags & kBvfFlagEsc)) {  // escaped columns take part in the exponent
-    const uint32_t* escs = bs + bi.esc_off;
-    const uint32_t nesc = __ldg(escs + nact);
-    const uint32_t* ecol = escs + bvf_align4(nact + 1);
-    for (uint32_t i = tid; i < nesc; i += kBvfThreads) see((double)__ldg(xfar + __ldg(ecol + i)));
+  const XT* xeb = xe;  // this block's escape values
+  if (bi.flags & kBvfFlagEsc) {
+    xeb = xe + __ldg(g.esc_base + bl);
+    if (kSplit) {  // escaped columns take part in the exponent
+      const uint32_t nesc = __ldg(bs + bi.esc_off + nact);
+      for (uint32_t i = tid; i < nesc; i += kBvfThreads) see((double)__ldg(xeb + i));
+    }
   }
   if (tid == 0) tab[bvf_zero(W)] = 0.0;
   emax = __reduce_max_sync(0xffffffffu, emax);
@@ -318,10 +339,11 @@ __global__ void __launch_bounds__(kBvfThreads, 4)
   // ---- window prefix F (exclusive): F hi = sum h (exact), F lo = sum l
   {
     double sh = 0.0, sl = 0.0;
+    // wide: warp w owns the window segment [w S, (w + 1) S), read lane-consecutively
+    const uint32_t S = ((W + 8 * 32 - 1) / (8 * 32)) * 32, s0 = warp * S, s1 = min(W, s0 + S);
     if (wide) {
-      for (uint32_t k = 0; k < E; ++k) {
-        const uint32_t j = j0 + k;
-        const double v = j < W ? tab[j] : 0.0;
+      for (uint32_t j = s0 + lane; j < s1; j += 32) {
+        const double v = tab[j];
         if (kSplit) {
           const double h = (v + sigma) - sigma;
           sh += h;
@@ -367,19 +389,40 @@ __global__ void __launch_bounds__(kBvfThreads, 4)
     }
     double* fhi = tab + F0;
     if (wide) {
-      for (uint32_t k = 0; k < E; ++k) {
-        const uint32_t j = j0 + k;
-        if (j >= W) break;
-        const double v = tab[j];
-        fhi[j] = bh;
-        if (kSplit) flo[j] = blo;
+      // the warp's offset (totals of the warps before it), then a warp scan per round of 32
+      double wh = 0.0, wl = 0.0;
+      for (uint32_t w = 0; w < warp; ++w) {
+        wh += misc[16 + 2 * w];
+        wl += misc[16 + 2 * w + 1];
+      }
+      for (uint32_t jb = s0; jb < s1; jb += 32) {
+        const uint32_t j = jb + lane;
+        const double v = j < s1 ? tab[j] : 0.0;
+        double h = v, l = 0.0;
         if (kSplit) {
-          const double h = (v + sigma) - sigma;
-          bh += h;
-          blo += v - h;
-        } else {
-          bh += v;
+          h = (v + sigma) - sigma;
+          l = v - h;
         }
+        double ih2 = h, il2 = l;
+#pragma unroll
+        for (uint32_t o = 1; o < 32; o <<= 1) {
+          const double uh = __shfl_up_sync(0xffffffffu, ih2, o);
+          const double ul = kSplit ? __shfl_up_sync(0xffffffffu, il2, o) : 0.0;
+          if (lane >= o) {
+            ih2 += uh;
+            il2 += ul;
+          }
+        }
+        if (j < s1) {
+          fhi[j] = wh + (ih2 - h);
+          if (kSplit) flo[j] = wl + (il2 - l);
+        }
+        if (j + 1 == W) {  // F[W]
+          fhi[W] = wh + ih2;
+          if (kSplit) flo[W] = wl + il2;
+        }
+        wh += __shfl_sync(0xffffffffu, ih2, 31);
+        wl += __shfl_sync(0xffffffffu, il2, 31);
       }
     }
 #pragma unroll
@@ -424,7 +467,7 @@ __global__ void __launch_bounds__(kBvfThreads, 4)
         }
       }
     }
-    if (j0 < W && j0 + E >= W) {  // the thread holding the window's last entry writes F[W]
+    if (!wide && j0 < W && j0 + E >= W) {  // the thread holding the window's last entry writes F[W]
       fhi[W] = bh;
       if (kSplit) flo[W] = blo;
     }
@@ -439,11 +482,10 @@ __global__ void __launch_bounds__(kBvfThreads, 4)
     const uint32_t tabc = smem_u32(tab);
     const uint32_t flob = smem_u32(flo) - F0 * 8u;
     if (bi.flags & kBvfFlagEsc) {
-      BvfTerms<XT, kSplit, true> te{tabc, flob, bs + bi.esc_off + bvf_align4(nact + 1) + __ldg(bs + bi.esc_off + tid),
-                                    xfar, sigma, F0 * 8u};
+      BvfTerms<XT, kSplit, true> te{tabc, flob, xeb + __ldg(bs + bi.esc_off + tid), sigma, F0 * 8u};
       bvf_chunk(te, cw, nact, K / 2, w0, ah, al, rowp);
     } else {
-      BvfTerms<XT, kSplit, false> tm{tabc, flob, nullptr, xfar, sigma, F0 * 8u};
+      BvfTerms<XT, kSplit, false> tm{tabc, flob, nullptr, sigma, F0 * 8u};
       bvf_chunk(tm, cw, nact, K / 2, w0, ah, al, rowp);
     }
   }

@@ -43,7 +43,24 @@ void launch_bvf(cmvg_graph* g, const XT* x, const XT* xfar, YT* y, const PrArgs&
     }
     d.ahead = g->fgather_res & 0x7fffffffu;
   }
-  kern<<<b1 - b0, kBvfThreads, L.total, st>>>(d, x, xfar ? xfar : x, y, pr);
+  if (!xfar) xfar = x;
+  // escape terms: their x values gathered first (stream-ordered scratch, so
+  // concurrent products on distinct streams and graph captures stay independent)
+  const uint64_t e0 = g->fesc_base_h.empty() ? 0 : g->fesc_base_h[b0];
+  const uint64_t ne = g->fesc_base_h.empty() ? 0 : g->fesc_base_h[b1] - e0;
+  StreamScratch xe(g->device, ne * sizeof(XT), st);
+  if (ne) {
+    int sms = 148;
+    (void)cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
+    const uint64_t want = (ne + 1023) / 1024;
+    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)sms * 8));
+    bvf_esc_gather<XT><<<grid, 256, 0, st>>>(g->fesc.as<uint32_t>() + e0, ne, xfar, xe.as<XT>());
+    CUDA_TRY(cudaGetLastError());
+  }
+  d.esc_base = g->fesc_base.as<uint32_t>() + b0;
+  // the kernel indexes xe by the shard-global escape number
+  const XT* xe_base = ne ? xe.as<XT>() - e0 : x;
+  kern<<<b1 - b0, kBvfThreads, L.total, st>>>(d, x, xfar, xe_base, y, pr);
   CUDA_TRY(cudaGetLastError());
 }
 

@@ -853,7 +853,8 @@ BvdLayout build_bvd(const BvDecoded& dec, const BvParams& bp, const BvdOptions& 
   if (2 * W + kBvfSlots + 1 >= kBvfIdxMask) throw std::invalid_argument("window too large for the BV-F term index");
   parallel_for(nb, [&](uint64_t b0, uint64_t b1) {
     std::vector<RowParts> rps(B);
-    std::vector<uint32_t> plus, cols, depth(B), hdr(B), escs;
+    RowParts rp0;
+    std::vector<uint32_t> plus, cols, depth(B), hdr(B), escs, eff_r(B);
     std::vector<RowMeta> meta(B);
     BitWriter body;
     for (uint64_t b = b0; b < b1; ++b) {
@@ -869,12 +870,26 @@ BvdLayout build_bvd(const BvDecoded& dec, const BvParams& bp, const BvdOptions& 
       // pass 1: split rows, collect gathered columns, choose the x-window
       for (uint32_t k = 0; k < nr; ++k) {
         const uint32_t i = r0 + k;
-        const uint32_t r = dec.ref_dist[i];
+        uint32_t r = dec.ref_dist[i];
         if (r && k < r) throw std::runtime_error("BV-D: reference crosses a block");
-        depth[k] = r ? depth[k - r] + 1 : 0;
-        bdepth[b] = std::max(bdepth[b], depth[k]);
         RowParts& rp = rps[k];
         split_row(g, i, r, bp.min_interval, rp, plus);
+        if (r) {
+          // the reference's keep rule (ref_matrix.hpp:63-65: a reference is
+          // used only if it makes the row strictly shorter) applied to the
+          // product's terms: BV picks references by bits, and a copy that
+          // skips many entries can cost more adds than the plain row
+          const uint64_t tref = rp.minus.size() + rp.res.size() + 2ull * rp.ints.size();
+          RowParts& p0 = rp0;
+          split_row(g, i, 0, bp.min_interval, p0, plus);
+          if (p0.res.size() + 2ull * p0.ints.size() <= tref) {
+            std::swap(rp, p0);
+            r = 0;
+          }
+        }
+        eff_r[k] = r;
+        depth[k] = r ? depth[k - r] + 1 : 0;
+        bdepth[b] = std::max(bdepth[b], depth[k]);
         for (auto& iv : rp.ints) {
           cols.push_back(iv.first);
           cols.push_back(iv.first + iv.second - 1);
@@ -904,7 +919,7 @@ BvdLayout build_bvd(const BvDecoded& dec, const BvParams& bp, const BvdOptions& 
       // pass 2: headers (with the far flag) and bodies
       for (uint32_t k = 0; k < nr; ++k) {
         const uint32_t i = r0 + k;
-        const uint32_t r = dec.ref_dist[i];
+        const uint32_t r = eff_r[k];
         const RowParts& rp = rps[k];
         const uint32_t nm = (uint32_t)rp.minus.size(), ns = (uint32_t)rp.res.size(), ni = (uint32_t)rp.ints.size();
         int64_t dmin = 0, dmax = 0;

@@ -152,6 +152,11 @@ struct cmvg_graph {
   uint64_t s_stream_bytes = 0;
   // BV-F layout (this shard): gather, PageRank
   DevBuf fwords, fblocks;
+  // escape columns of the shard's BV-F blocks, flat in block order, and each
+  // block's first escape (nblocks + 1): the values x[fesc[i]] are gathered by
+  // one pre-pass per product (bvf_esc_gather) so the term loop streams them
+  DevBuf fesc, fesc_base;
+  std::vector<uint64_t> fesc_base_h;
   uint64_t f_stream_bytes = 0;
   BvfStats fstats;
   std::atomic<unsigned> fgather_attr{0};
@@ -190,7 +195,7 @@ struct cmvg_graph {
   }
   std::mutex host_mu;
   uint64_t device_bytes() const {
-    return words.bytes + blocks.bytes + swords.bytes + sblocks.bytes + fwords.bytes + fblocks.bytes + twords.bytes +
+    return words.bytes + blocks.bytes + swords.bytes + sblocks.bytes + fwords.bytes + fblocks.bytes + fesc.bytes + fesc_base.bytes + twords.bytes +
            tblocks.bytes + tile_ptr.bytes +
            tile_blk.bytes + farp_ptr.bytes + farp.bytes + bv_words.bytes + bv_seg.bytes;
   }
