@@ -101,6 +101,9 @@ struct BvfTerms {
   // one term: +-table[index] split at the block grid; bit 31 of `signw` is the
   // term's minus flag; a row end stores the row's sum at rowp and moves on
   // ev: the term's x value when it is an escape (loaded ahead, see esc_group)
+  // END: the term may end a row (the high term of a word; rows have an even
+  // number of terms, so the low term never does)
+  template <bool END>
   __device__ __forceinline__ void term(uint32_t c, uint32_t signw, double& ah, double& al, uint32_t& rowp,
                                        XT ev = XT(0)) const {
     const uint32_t off = (c << 3) & (kBvfIdxMask << 3);
@@ -118,7 +121,7 @@ struct BvfTerms {
     } else {
       ah = fma(sg, v, ah);
     }
-    if (c & kBvfEnd) {
+    if (END && (c & kBvfEnd)) {
       sts_f64x2(rowp, ah, al);
       ah = 0.0;
       al = 0.0;
@@ -126,8 +129,8 @@ struct BvfTerms {
     }
   }
   __device__ __forceinline__ void word(uint32_t w, double& ah, double& al, uint32_t& rowp) const {
-    term(w & 0xffffu, w << 16, ah, al, rowp);
-    term(w >> 16, w, ah, al, rowp);
+    term<false>(w & 0xffffu, w << 16, ah, al, rowp);
+    term<true>(w >> 16, w, ah, al, rowp);
   }
   // escape blocks: 8 terms at a time, the x values of their escapes (gathered
   // ahead by bvf_esc_gather) loaded together before the sums
@@ -140,8 +143,8 @@ struct BvfTerms {
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      term(w4[i] & 0xffffu, w4[i] << 16, ah, al, rowp, ev[2 * i]);
-      term(w4[i] >> 16, w4[i], ah, al, rowp, ev[2 * i + 1]);
+      term<false>(w4[i] & 0xffffu, w4[i] << 16, ah, al, rowp, ev[2 * i]);
+      term<true>(w4[i] >> 16, w4[i], ah, al, rowp, ev[2 * i + 1]);
     }
   }
 };

@@ -283,7 +283,10 @@ void emit_bvf(const RowParts* rps, const RowMeta* meta, uint32_t nr, uint64_t wl
         for (uint64_t c = iv.first; c < (uint64_t)iv.first + iv.second; ++c) xterm((uint32_t)c, false);
       }
     }
-    if (codes.size() == rstart.back()) {  // empty differential row: one padding term
+    // every row gets an even number of terms (padding terms read the zero
+    // entry): rows then end only on the second term of a code word, and the
+    // term loop needs one row-end store per word instead of one per term
+    while (codes.size() == rstart.back() || ((codes.size() - rstart.back()) & 1u)) {
       codes.push_back((uint16_t)ZERO);
       ecol.push_back(0);
       ++pad_terms;

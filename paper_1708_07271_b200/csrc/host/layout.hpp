@@ -219,8 +219,9 @@ __host__ __device__ constexpr uint32_t tmeta_rounds(uint32_t m) { return (m >> 1
 // inside the window the two terms +F[a - wlo + len], -F[a - wlo] (O(1),
 // PAPER.md:198-206).  Intervals reaching outside the window are written as
 // their columns.  Term (16 bits): index (13) | escape << 13 | end << 14 |
-// minus << 15; `end` marks a row's last term (every row has >= 1 term: an
-// empty row gets one padding term).  Escape terms (blocks whose far columns
+// minus << 15; `end` marks a row's last term (every row has an even number
+// >= 2 of terms, padded with zero-entry terms, so a row ends only on the
+// second (high) term of a code word).  Escape terms (blocks whose far columns
 // exceed the slots) read x[esc[escstart_t + index]] from global memory.
 // Work split: the block's N terms are cut into nact chunks of K terms
 // (K = 16 ceil(N / 4096), nact = ceil(N / K) <= 256; the last chunk padded);

@@ -24,6 +24,8 @@ def _check(g, params, window=1536, x=None, B=1024, max_depth=3):
         info, sr, r, slots, escstart, esccol, chunks = bvf_block(words, blocks[b])
         nr = min(B, g.n - b * B)
         ends = [int(np.sum((c & BVF_END) != 0)) for c in chunks]
+        # rows have an even number of terms: a row ends only on a word's high term
+        assert all(not np.any(c[0::2] & BVF_END) for c in chunks)
         assert sum(ends) == nr
         assert info["nact"] <= 256 and info["K"] % 16 == 0
         row = 0
