@@ -799,25 +799,8 @@ int cmvg_decode_csr(cmvg_graph* g, uint64_t* row_offsets, uint32_t* cols, int pt
     s.window = g->params.window;
     s.min_interval = g->params.min_interval;
     s.zeta_k = g->params.zeta_k;
-    DevBuf deg, segsum, segbase, err, dro, dcols;
-    deg.alloc((size_t)g->n * 4);
-    segsum.alloc(g->nseg * 8);
-    err.alloc(4);
-    CUDA_TRY(cudaMemsetAsync(err.p, 0, 4, st));
-    const int tpb = 64;
-    bv_seg_degrees<<<(unsigned)((g->nseg + tpb - 1) / tpb), tpb, 0, st>>>(s, deg.as<uint32_t>(), segsum.as<uint64_t>(),
-                                                                         err.as<int>());
-    CUDA_TRY(cudaGetLastError());
-    std::vector<uint64_t> hs(g->nseg), hb(g->nseg);
-    int herr = 0;
-    CUDA_TRY(cudaMemcpyAsync(hs.data(), segsum.p, g->nseg * 8, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaMemcpyAsync(&herr, err.p, 4, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
-    if (herr) throw AbiError(CMVG_ERR_CORRUPT, "BV stream corrupt (device degree pass, code " + std::to_string(herr) + ")");
-    uint64_t acc = 0;
-    for (uint64_t k = 0; k < g->nseg; ++k) { hb[k] = acc; acc += hs[k]; }
-    if (acc != g->m) throw AbiError(CMVG_ERR_CORRUPT, "BV stream corrupt: decoded edge count mismatch");
-    segbase.upload(hb.data(), hb.size());
+    // device-resident passes (bv_decode.cuh)
+    DevBuf dro, dcols;
     uint64_t* ro = row_offsets;
     uint32_t* co = cols;
     if (ptr_kind == CMVG_HOST) {
@@ -826,12 +809,58 @@ int cmvg_decode_csr(cmvg_graph* g, uint64_t* row_offsets, uint32_t* cols, int pt
       ro = dro.as<uint64_t>();
       co = dcols.as<uint32_t>();
     }
-    if (getenv("CMVG_SERIAL_DECODE"))  // the serial decoder, for tests
+    StreamScratch deg(g->device, (size_t)g->n * 4, st), err(g->device, 16, st);
+    CUDA_TRY(cudaMemsetAsync(err.p, 0, 4, st));
+    int herr = 0;
+    const int tpb = 64;
+    const bool tiles = kDecTileRows % s.seg_rows == 0 && kDecTileRows % kDecGroup == 0 && !getenv("CMVG_SERIAL_DECODE");
+    if (!tiles) {
+      // serial decoder (segments that do not tile; tests): per-segment parse
+      // and scan, then one thread per segment writes its rows
+      StreamScratch rbit(g->device, (size_t)g->n * 8, st), segsum(g->device, g->nseg * 8, st),
+          segbase(g->device, g->nseg * 8, st);
+      bv_index_rows<<<(unsigned)((g->nseg + tpb - 1) / tpb), tpb, 0, st>>>(s, deg.as<uint32_t>(), rbit.as<uint64_t>(),
+                                                                          segsum.as<uint64_t>(), err.as<int>());
+      CUDA_TRY(cudaGetLastError());
+      bv_scan_segments<<<1, 1024, 0, st>>>(segsum.as<uint64_t>(), g->nseg, 1, g->m, segbase.as<uint64_t>(),
+                                           err.as<int>());
+      CUDA_TRY(cudaGetLastError());
       bv_seg_decode<<<(unsigned)((g->nseg + tpb - 1) / tpb), tpb, 0, st>>>(s, segbase.as<uint64_t>(), ro, co,
                                                                           err.as<int>());
-    else
-      bv_seg_decode_warp<<<(unsigned)((g->nseg + 3) / 4), 128, 0, st>>>(s, segbase.as<uint64_t>(), ro, co,
-                                                                        err.as<int>());
+    } else {
+      const uint32_t ng = (uint32_t)(((uint64_t)g->n + kDecGroup - 1) / kDecGroup);
+      {  // the handle's row-group index: one serial pass per segment, once
+        std::lock_guard<std::mutex> lk(g->layout_mu);
+        if (!g->have_sync) {
+          g->bv_sync.alloc((size_t)ng * sizeof(DecSync));
+          bv_sync_index<<<(unsigned)((g->nseg + tpb - 1) / tpb), tpb, 0, st>>>(s, deg.as<uint32_t>(),
+                                                                              g->bv_sync.as<DecSync>(), err.as<int>());
+          CUDA_TRY(cudaGetLastError());
+          CUDA_TRY(cudaMemcpyAsync(&herr, err.p, 4, cudaMemcpyDeviceToHost, st));
+          CUDA_TRY(cudaStreamSynchronize(st));
+          if (herr) throw AbiError(CMVG_ERR_CORRUPT, "BV stream corrupt (device index pass, code " + std::to_string(herr) + ")");
+          g->have_sync = true;
+        }
+      }
+      StreamScratch rbit(g->device, (size_t)g->n * 8, st), gcnt(g->device, (size_t)ng * 8, st),
+          gbase(g->device, (size_t)ng * 8, st);
+      bv_index_groups<<<(ng + 127) / 128, 128, 0, st>>>(s, g->bv_sync.as<DecSync>(), deg.as<uint32_t>(),
+                                                        rbit.as<uint64_t>(), gcnt.as<uint64_t>(), err.as<int>());
+      CUDA_TRY(cudaGetLastError());
+      bv_scan_segments<<<1, 1024, 0, st>>>(gcnt.as<uint64_t>(), ng, kDecTileRows / kDecGroup, g->m,
+                                           gbase.as<uint64_t>(), err.as<int>());
+      CUDA_TRY(cudaGetLastError());
+      uint32_t cap = 24064;  // staging words: two CTAs of ~100 KB per SM
+      if (const char* e = getenv("CMVG_DECODE_CAP")) cap = (uint32_t)strtoul(e, nullptr, 10);
+      const uint32_t sm = dec_smem_bytes(cap);
+      if (g->decode_attr < sm) {
+        CUDA_TRY(cudaFuncSetAttribute(bv_decode_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        g->decode_attr = sm;
+      }
+      const uint32_t ntile = (uint32_t)(((uint64_t)g->n + kDecTileRows - 1) / kDecTileRows);
+      bv_decode_tiles<<<ntile, kDecThreads, sm, st>>>(s, deg.as<uint32_t>(), rbit.as<uint64_t>(), gbase.as<uint64_t>(),
+                                                      cap, ro, co, err.as<int>());
+    }
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaMemcpyAsync(&herr, err.p, 4, cudaMemcpyDeviceToHost, st));
     if (ptr_kind == CMVG_HOST) {

@@ -157,6 +157,9 @@ struct cmvg_graph {
   // one pre-pass per product (bvf_esc_gather) so the term loop streams them
   DevBuf fesc, fesc_base;
   std::vector<uint64_t> fesc_base_h;
+  uint32_t decode_attr = 0;  // dynamic shared memory set on bv_decode_tiles
+  DevBuf bv_sync;            // row-group index of the BV stream (built on the first decode)
+  bool have_sync = false;
   uint64_t f_stream_bytes = 0;
   BvfStats fstats;
   std::atomic<unsigned> fgather_attr{0};
@@ -197,7 +200,7 @@ struct cmvg_graph {
   uint64_t device_bytes() const {
     return words.bytes + blocks.bytes + swords.bytes + sblocks.bytes + fwords.bytes + fblocks.bytes + fesc.bytes + fesc_base.bytes + twords.bytes +
            tblocks.bytes + tile_ptr.bytes +
-           tile_blk.bytes + farp_ptr.bytes + farp.bytes + bv_words.bytes + bv_seg.bytes;
+           tile_blk.bytes + farp_ptr.bytes + farp.bytes + bv_words.bytes + bv_seg.bytes + bv_sync.bytes;
   }
   BvdDev dev() const {
     BvdDev d{};

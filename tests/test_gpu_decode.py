@@ -51,10 +51,9 @@ def test_decode_rejects_corruption(cuda):
         P.BvGraph(bad)  # the host builder validates the stream first
 
 
-def test_decode_warp_fallbacks_and_lists(cuda):
-    """The warp-cooperative decoder's per-warp lists overflow on purpose:
-    > 512 residuals, > 1024 copied entries, > 64 intervals, > 128 copy blocks
-    (serial row fallback), next to rows that fit; bit-exact either way."""
+def test_decode_long_rows_and_lists(cuda):
+    """Rows with > 512 residuals, > 1024 copied entries, > 64 intervals and
+    > 128 copy blocks next to short rows; bit-exact."""
     rng = np.random.default_rng(21)
     n = 6000
     rows = [sorted(set(rng.integers(0, n, 5).tolist())) for _ in range(n)]
@@ -67,4 +66,23 @@ def test_decode_warp_fallbacks_and_lists(cuda):
     g = csr_from_rows(rows)
     s = P.BvStream.encode(g, P.BvParams())
     ro, co = P.BvGraph(s).decode_csr()
+    assert np.array_equal(ro, g.row_offsets) and np.array_equal(co, g.columns)
+
+
+@pytest.mark.parametrize("cap", ["0", "4096"])
+def test_decode_unstaged_tiles(cuda, monkeypatch, cap):
+    """Tiles whose edges exceed the shared-memory staging buffer decode straight
+    into the output columns (CMVG_DECODE_CAP shrinks the buffer); bit-exact."""
+    monkeypatch.setenv("CMVG_DECODE_CAP", cap)
+    for cfg, n in ((2, (1 << 15) + 3), (4, 1 << 14)):
+        g = make_graph(cfg, n=n)
+        ro, co = P.BvGraph(P.BvStream.encode(g, bv_params(cfg))).decode_csr()
+        assert np.array_equal(ro, g.row_offsets) and np.array_equal(co, g.columns)
+
+
+def test_decode_serial_matches(cuda, monkeypatch):
+    """The serial thread-per-segment decoder (CMVG_SERIAL_DECODE) gives the same CSR."""
+    monkeypatch.setenv("CMVG_SERIAL_DECODE", "1")
+    g = make_graph(1, n=1 << 14)
+    ro, co = P.BvGraph(P.BvStream.encode(g, bv_params(1))).decode_csr()
     assert np.array_equal(ro, g.row_offsets) and np.array_equal(co, g.columns)
