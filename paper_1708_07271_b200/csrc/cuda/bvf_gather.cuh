@@ -50,19 +50,22 @@ constexpr uint32_t kBvfThreads = 256;
 constexpr uint32_t kBvfXPer = 8;  // window entries per thread (W <= 2048)
 
 struct BvfSmem {
-  uint32_t off_tab, off_flo, off_rows, off_rn, off_misc, total;
+  uint32_t off_tab, off_fhi, off_flo, off_rows, off_rn, off_misc, total;
 };
 // The x/F table region is dead after the term loop; the pointer-jumping chain
-// reuses it.
-__host__ __device__ inline BvfSmem bvf_smem_layout(uint32_t W, uint32_t B, bool lo) {
+// reuses it.  x window, far slots, zero entry and F hi are one table of
+// doubles; split (fp64 x): then F lo, and row records (sum hi, lo) of 16
+// bytes; plain (fp32 x): row records are the 8-byte sum.
+__host__ __device__ inline BvfSmem bvf_smem_layout(uint32_t W, uint32_t B, bool split) {
   BvfSmem s;
   uint32_t o = 0;
   s.off_tab = o;  // x window, far slots, zero entry, F hi
+  s.off_fhi = o + bvf_f0(W) * 8u;
   o = align16(o + (bvf_f0(W) + W + 1) * 8u);
   s.off_flo = o;  // F lo (split mode)
-  o = align16(o + (lo ? (W + 1) * 8u : 0u));
+  o = align16(o + (split ? (W + 1) * 8u : 0u));
   s.off_rows = o;
-  o = align16(o + B * 16u);
+  o = align16(o + B * (split ? 16u : 8u));
   s.off_rn = o;  // r per row, one byte each
   o = align16(o + kBvfRnWords * 8u);
   s.off_misc = o;  // warp maxima / totals / carries / epilogue scratch
@@ -86,6 +89,14 @@ __device__ __forceinline__ double lds_f64(uint32_t a) {
   double v;
   asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
   return v;
+}
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_f64(uint32_t a, double x) {
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(x) : "memory");
 }
 __device__ __forceinline__ void sts_f64x2(uint32_t a, double x, double y) {
   asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(x), "d"(y) : "memory");
@@ -122,10 +133,15 @@ struct BvfTerms {
       ah = fma(sg, v, ah);
     }
     if (END && (c & kBvfEnd)) {
-      sts_f64x2(rowp, ah, al);
+      if (SPLIT) {
+        sts_f64x2(rowp, ah, al);
+        rowp += 16;
+      } else {
+        sts_f64(rowp, ah);
+        rowp += 8;
+      }
       ah = 0.0;
       al = 0.0;
-      rowp += 16;
     }
   }
   __device__ __forceinline__ void word(uint32_t w, double& ah, double& al, uint32_t& rowp) const {
@@ -215,7 +231,11 @@ __global__ void __launch_bounds__(kBvfThreads, 4)
   const uint32_t K = bi.K, nact = bi.nact, nslot = bi.nslot;
   const uint32_t F0 = bvf_f0(W);
   double* tab = reinterpret_cast<double*>(smem + L.off_tab);
+  double* fhi = reinterpret_cast<double*>(smem + L.off_fhi);
   double* flo = reinterpret_cast<double*>(smem + L.off_flo);
+  constexpr uint32_t RS = kSplit ? 16u : 8u;  // row record bytes
+  auto put_x = [&](uint32_t j, double v) { tab[j] = v; };
+  auto get_x = [&](uint32_t j) -> double { return tab[j]; };
   char* rows = reinterpret_cast<char*>(smem + L.off_rows);
   uint8_t* r8 = reinterpret_cast<uint8_t*>(smem + L.off_rn);
   double* misc = reinterpret_cast<double*>(smem + L.off_misc);
@@ -290,7 +310,7 @@ __global__ void __launch_bounds__(kBvfThreads, 4)
     for (uint32_t j = tid; j < W; j += kBvfThreads) {
       const uint32_t c = bi.wlo + j;
       const double v = c < g.n ? (double)__ldg(x + c) : 0.0;
-      tab[j] = v;
+      put_x(j, v);
       see(v);
     }
   }
@@ -303,13 +323,13 @@ __global__ void __launch_bounds__(kBvfThreads, 4)
       if (full) {
         *reinterpret_cast<double2*>(tab + j) = make_double2(xv[k], xv[k + 1]);
       } else {
-        if (j < W) tab[j] = xv[k];
-        if (k + 1 < E && j + 1 < W) tab[j + 1] = xv[k + 1];
+        if (j < W) put_x(j, xv[k]);
+        if (k + 1 < E && j + 1 < W) put_x(j + 1, xv[k + 1]);
       }
     }
   }
   see(fv);
-  if (tid < nslot) tab[W + tid] = fv;
+  if (tid < nslot) put_x(W + tid, fv);
   const XT* xeb = xe;  // this block's escape values
   if (bi.flags & kBvfFlagEsc) {
     xeb = xe + __ldg(g.esc_base + bl);
@@ -318,7 +338,7 @@ __global__ void __launch_bounds__(kBvfThreads, 4)
       for (uint32_t i = tid; i < nesc; i += kBvfThreads) see((double)__ldg(xeb + i));
     }
   }
-  if (tid == 0) tab[bvf_zero(W)] = 0.0;
+  if (tid == 0) put_x(bvf_zero(W), 0.0);
   emax = __reduce_max_sync(0xffffffffu, emax);
   nonfin = __any_sync(0xffffffffu, nonfin);
   if (lane == 0) misc_u[warp] = emax | (nonfin << 16);
@@ -346,7 +366,7 @@ __global__ void __launch_bounds__(kBvfThreads, 4)
     const uint32_t S = ((W + 8 * 32 - 1) / (8 * 32)) * 32, s0 = warp * S, s1 = min(W, s0 + S);
     if (wide) {
       for (uint32_t j = s0 + lane; j < s1; j += 32) {
-        const double v = tab[j];
+        const double v = get_x(j);
         if (kSplit) {
           const double h = (v + sigma) - sigma;
           sh += h;
@@ -390,7 +410,6 @@ __global__ void __launch_bounds__(kBvfThreads, 4)
       bh += misc[16 + 2 * w];
       blo += misc[16 + 2 * w + 1];
     }
-    double* fhi = tab + F0;
     if (wide) {
       // the warp's offset (totals of the warps before it), then a warp scan per round of 32
       double wh = 0.0, wl = 0.0;
@@ -400,7 +419,7 @@ __global__ void __launch_bounds__(kBvfThreads, 4)
       }
       for (uint32_t jb = s0; jb < s1; jb += 32) {
         const uint32_t j = jb + lane;
-        const double v = j < s1 ? tab[j] : 0.0;
+        const double v = j < s1 ? get_x(j) : 0.0;
         double h = v, l = 0.0;
         if (kSplit) {
           h = (v + sigma) - sigma;
@@ -480,7 +499,7 @@ __global__ void __launch_bounds__(kBvfThreads, 4)
   // ---- terms
   double ah = 0.0, al = 0.0;
   const uint32_t rows_s = smem_u32(rows);
-  uint32_t rowp = rows_s + srow * 16u;
+  uint32_t rowp = rows_s + srow * RS;
   if (active) {
     const uint32_t tabc = smem_u32(tab);
     const uint32_t flob = smem_u32(flo) - F0 * 8u;
@@ -504,7 +523,7 @@ __global__ void __launch_bounds__(kBvfThreads, 4)
   // ---- carries: a row cut by chunk boundaries gets the tails of the chunks
   // before its end -- a segmented scan of the tails (segments start at the
   // chunks that end a row) in the warp, then across warps
-  const bool has_end = active && rowp != rows_s + srow * 16u;
+  const bool has_end = active && rowp != rows_s + srow * RS;
   double sh = ah, sl = al;
   bool sf = has_end;
   if (!__all_sync(0xffffffffu, has_end || !active)) {  // a chunk inside one row: segmented scan
@@ -539,16 +558,23 @@ __global__ void __launch_bounds__(kBvfThreads, 4)
         if (misc_u[8 + w]) break;
       }
     }
-    double2* rr = reinterpret_cast<double2*>(rows + bvf_slot(srow) * 16u);
-    double2 v = *rr;
-    v.x += ch;
-    v.y += cl;
-    *rr = v;
+    if constexpr (kSplit) {
+      double2* rr = reinterpret_cast<double2*>(rows + bvf_slot(srow) * 16u);
+      double2 v = *rr;
+      v.x += ch;
+      v.y += cl;
+      *rr = v;
+    } else {
+      reinterpret_cast<double*>(rows)[bvf_slot(srow)] += ch;
+    }
   }
   __syncthreads();  // #5
 
   // ---- reference chains and the store
-  auto rec = [&](uint32_t k) { return *reinterpret_cast<const double2*>(rows + bvf_slot(k) * 16u); };
+  auto rec = [&](uint32_t k) -> double2 {
+    if constexpr (kSplit) return *reinterpret_cast<const double2*>(rows + bvf_slot(k) * 16u);
+    else return make_double2(reinterpret_cast<const double*>(rows)[bvf_slot(k)], 0.0);
+  };
   YT* yb = y + (r0 - g.row_begin);
   auto walk = [&](auto& epi) {
     if (g.max_depth <= 3) {
@@ -615,7 +641,8 @@ __global__ void __launch_bounds__(kBvfThreads, 4)
         for (uint32_t q = 0; q < kMaxPer; ++q) {
           const uint32_t k = tid + q * kBvfThreads;
           if (k < nr) {
-            *reinterpret_cast<double2*>(rows + bvf_slot(k) * 16u) = make_double2(nh[q], nl[q]);
+            if constexpr (kSplit) *reinterpret_cast<double2*>(rows + bvf_slot(k) * 16u) = make_double2(nh[q], nl[q]);
+            else reinterpret_cast<double*>(rows)[bvf_slot(k)] = nh[q];
             ptr[k] = np_[q];
           }
         }
