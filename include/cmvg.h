@@ -159,6 +159,12 @@ int cmvg_bv_deserialize(const uint8_t* buf, uint64_t size, cmvg_bvstream** out);
 int cmvg_bv_from_words(uint32_t n, uint64_t m, const cmvg_bv_params* p, const uint32_t* words, uint64_t nbits,
                        const uint64_t* segment_bit_offsets, cmvg_bvstream** out);
 int cmvg_bv_decode_host(const cmvg_bvstream* s, cmvg_csr** out);
+/* Row i of the source adjacency, decoded from the stream (replaces
+ * cmv::reconstruct_row, ref_matrix.hpp:71-73): *deg gets the row's length;
+ * cols (room for cap entries; may be null to query the length) gets the
+ * sorted columns.  CMVG_ERR_RANGE (std::out_of_range) if i >= n,
+ * CMVG_ERR_INVALID if cap < the length and cols is not null. */
+int cmvg_bv_reconstruct_row(const cmvg_bvstream* s, uint32_t i, uint32_t* cols, uint64_t cap, uint64_t* deg);
 int cmvg_bv_get_stats(const cmvg_bvstream* s, cmvg_bv_stats* out);
 const uint32_t* cmvg_bv_words(const cmvg_bvstream* s, uint64_t* nwords);
 const uint64_t* cmvg_bv_segment_offsets(const cmvg_bvstream* s, uint64_t* count);

@@ -119,6 +119,7 @@ _SIGS = [
     ("cmvg_bv_from_words", C.c_int, [C.c_uint32, C.c_uint64, C.POINTER(_BvParamsC), _P, C.c_uint64, _P,
                                      C.POINTER(_P)]),
     ("cmvg_bv_decode_host", C.c_int, [_P, C.POINTER(_P)]),
+    ("cmvg_bv_reconstruct_row", C.c_int, [_P, C.c_uint32, _P, C.c_uint64, C.POINTER(C.c_uint64)]),
     ("cmvg_bv_get_stats", C.c_int, [_P, C.POINTER(_BvStatsC)]),
     ("cmvg_bv_words", _P, [_P, C.POINTER(C.c_uint64)]),
     ("cmvg_bv_segment_offsets", _P, [_P, C.POINTER(C.c_uint64)]),
@@ -394,6 +395,21 @@ class BvStream:
         finally:
             lib.cmvg_layout_free(h)
         return w, b
+
+    def reconstruct_row(self, i: int) -> np.ndarray:
+        """cmv::reconstruct_row (ref_matrix.hpp:71-73): row i of the source
+        adjacency, decoded from its segment of the stream; IndexError (the
+        reference's std::out_of_range) if i >= n."""
+        lib = load_library()
+        if i < 0:
+            raise IndexError("reconstruct_row: row index out of range")
+        if i >= self.n:
+            raise IndexError("reconstruct_row: row index out of range")
+        d = C.c_uint64()
+        _check(lib.cmvg_bv_reconstruct_row(self._h, i, None, 0, C.byref(d)))
+        out = np.empty(d.value, dtype=np.uint32)
+        _check(lib.cmvg_bv_reconstruct_row(self._h, i, out.ctypes.data, d.value, C.byref(d)))
+        return out
 
     def decode_host(self) -> CsrGraph:
         """CPU decode (the handle builder's path); tests compare it with the GPU decoder."""

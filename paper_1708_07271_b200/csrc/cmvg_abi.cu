@@ -171,6 +171,18 @@ int cmvg_bv_deserialize(const uint8_t* buf, uint64_t size, cmvg_bvstream** out) 
   });
 }
 
+int cmvg_bv_reconstruct_row(const cmvg_bvstream* s, uint32_t i, uint32_t* cols, uint64_t cap, uint64_t* deg) {
+  return guarded([&] {
+    require(s && deg, "null argument");
+    const std::vector<uint32_t> row = bv_reconstruct_row(s->s, i);
+    *deg = row.size();
+    if (cols) {
+      require(cap >= row.size(), "reconstruct_row: output too small");
+      std::copy(row.begin(), row.end(), cols);
+    }
+  });
+}
+
 int cmvg_bv_decode_host(const cmvg_bvstream* s, cmvg_csr** out) {
   return guarded([&] {
     require(s && out, "null argument");

@@ -236,6 +236,109 @@ BvStream bv_encode(const HostCsr& g, const BvParams& p) {
   return out;
 }
 
+namespace {
+// Decode rows [r0, rend) of segment sg (r0 = its first row) into c / roff
+// (roff[k] = start of row r0 + k in c); ref_dist (optional) gets each row's
+// reference distance.  The decoder validates every field and throws on a
+// corrupt stream; full = rend is the segment end (then the segment's bit
+// length is checked too).
+struct SegScratch {
+  std::vector<uint64_t> roff;
+  std::vector<uint32_t> depth, copied, expanded, merged, tmp;
+};
+void decode_segment_rows(const BvStream& s, uint64_t sg, uint32_t rend, std::vector<uint32_t>& c, SegScratch& w,
+                         uint8_t* ref_dist, uint32_t* degs) {
+  const BvParams& p = s.params;
+  const uint32_t seg = p.segment_rows;
+  const uint32_t R = p.max_ref ? p.max_ref : 0xffffffffu;
+  BitReader br(s.words.data(), s.words.size(), s.segment_bit_offsets[sg]);
+  const uint32_t r0 = (uint32_t)(sg * seg), r1 = (uint32_t)std::min<uint64_t>(s.n, (sg + 1) * seg);
+  std::vector<uint64_t>& roff = w.roff;
+  std::vector<uint32_t>&depth = w.depth, &copied = w.copied, &expanded = w.expanded, &merged = w.merged, &tmp = w.tmp;
+  depth.resize(seg);
+  c.clear();
+  roff.assign(1, 0);
+  for (uint32_t i = r0; i < rend; ++i) {
+    uint64_t d = br.gamma();
+    depth[i - r0] = 0;
+    if (d > s.n) throw std::runtime_error("BV stream corrupt: outdegree > n");
+    if (d == 0) { roff.push_back(c.size()); if (degs) degs[i - r0] = 0; continue; }
+    uint64_t r = p.window ? br.unary() : 0;
+    if (r > p.window || (r && i < r0 + r)) throw std::runtime_error("BV stream corrupt: bad reference");
+    copied.clear();
+    if (r) {
+      uint32_t j = i - (uint32_t)r;
+      if (depth[j - r0] >= R) throw std::runtime_error("BV stream corrupt: chain exceeds R");
+      depth[i - r0] = depth[j - r0] + 1;
+      if (ref_dist) ref_dist[i] = (uint8_t)r;
+      const uint32_t* Rl = c.data() + roff[j - r0];
+      uint64_t dr = roff[j - r0 + 1] - roff[j - r0];
+      uint64_t b = br.gamma();
+      if (b > dr + 1) throw std::runtime_error("BV stream corrupt: too many copy blocks");
+      uint64_t pos = 0;
+      bool cp = true;
+      for (uint64_t k = 0; k < b; ++k) {
+        uint64_t len = k == 0 ? br.gamma() : br.gamma() + 1;
+        if (pos + len > dr) throw std::runtime_error("BV stream corrupt: copy block overflow");
+        if (cp) copied.insert(copied.end(), Rl + pos, Rl + pos + len);
+        pos += len;
+        cp = !cp;
+      }
+      if (cp) copied.insert(copied.end(), Rl + pos, Rl + dr);
+    }
+    if (copied.size() > d) throw std::runtime_error("BV stream corrupt: copied > outdegree");
+    uint64_t extra = d - copied.size();
+    expanded.clear();
+    tmp.clear();
+    if (extra) {
+      uint64_t ni = br.gamma();
+      uint64_t prev_end = 0, in_int = 0;
+      for (uint64_t k = 0; k < ni; ++k) {
+        int64_t left = k == 0 ? (int64_t)i + unfold_signed(br.gamma()) : (int64_t)(prev_end + br.gamma() + 1);
+        uint64_t len = br.gamma() + p.min_interval;
+        if (left < 0 || (uint64_t)left + len > s.n) throw std::runtime_error("BV stream corrupt: interval out of range");
+        for (uint64_t t = 0; t < len; ++t) expanded.push_back((uint32_t)(left + t));
+        prev_end = (uint64_t)left + len;
+        in_int += len;
+      }
+      if (in_int > extra) throw std::runtime_error("BV stream corrupt: intervals exceed outdegree");
+      uint64_t nres = extra - in_int;
+      int64_t prev = 0;
+      for (uint64_t k = 0; k < nres; ++k) {
+        int64_t v = k == 0 ? (int64_t)i + unfold_signed(br.zeta(p.zeta_k)) : prev + (int64_t)br.zeta(p.zeta_k) + 1;
+        if (v < 0 || v >= (int64_t)s.n) throw std::runtime_error("BV stream corrupt: residual out of range");
+        tmp.push_back((uint32_t)v);
+        prev = v;
+      }
+    }
+    merged.resize(copied.size() + expanded.size());
+    std::merge(copied.begin(), copied.end(), expanded.begin(), expanded.end(), merged.begin());
+    size_t base = c.size();
+    c.resize(base + merged.size() + tmp.size());
+    std::merge(merged.begin(), merged.end(), tmp.begin(), tmp.end(), c.begin() + base);
+    for (size_t t = base + 1; t < c.size(); ++t)
+      if (c[t] <= c[t - 1]) throw std::runtime_error("BV stream corrupt: row not strictly increasing");
+    roff.push_back(c.size());
+    if (degs) degs[i - r0] = (uint32_t)d;
+  }
+  if (rend == r1 && br.pos() != s.segment_bit_offsets[sg + 1])
+    throw std::runtime_error("BV stream corrupt: segment length mismatch");
+}
+}  // namespace
+
+std::vector<uint32_t> bv_reconstruct_row(const BvStream& s, uint32_t i) {
+  if (i >= s.n) throw std::out_of_range("reconstruct_row: row index out of range");
+  const uint32_t seg = s.params.segment_rows;
+  const uint64_t sg = i / seg;
+  if (s.segment_bit_offsets.size() != ((uint64_t)s.n + seg - 1) / seg + 1)
+    throw std::runtime_error("BV stream: bad segment table");
+  std::vector<uint32_t> c;
+  SegScratch w;
+  decode_segment_rows(s, sg, i + 1, c, w, nullptr, nullptr);
+  const uint32_t k = i - (uint32_t)(sg * seg);
+  return std::vector<uint32_t>(c.begin() + w.roff[k], c.begin() + w.roff[k + 1]);
+}
+
 BvDecoded bv_decode(const BvStream& s) {
   const BvParams& p = s.params;
   uint32_t seg = p.segment_rows;
@@ -245,81 +348,12 @@ BvDecoded bv_decode(const BvStream& s) {
   std::vector<std::vector<uint32_t>> degs(nseg);
   BvDecoded out;
   out.ref_dist.assign(s.n, 0);
-  const uint32_t R = p.max_ref ? p.max_ref : 0xffffffffu;
-  uint64_t nwords = s.words.size();
   parallel_for(nseg, [&](uint64_t sb, uint64_t se) {
-    std::vector<uint64_t> roff;
-    std::vector<uint32_t> depth(seg), copied, expanded, merged, tmp;
+    SegScratch w;
     for (uint64_t sg = sb; sg < se; ++sg) {
-      BitReader br(s.words.data(), nwords, s.segment_bit_offsets[sg]);
-      uint32_t r0 = (uint32_t)(sg * seg), r1 = (uint32_t)std::min<uint64_t>(s.n, (sg + 1) * seg);
-      std::vector<uint32_t>& c = cols[sg];
-      roff.assign(1, 0);
-      degs[sg].resize(r1 - r0);
-      for (uint32_t i = r0; i < r1; ++i) {
-        uint64_t d = br.gamma();
-        depth[i - r0] = 0;
-        if (d > s.n) throw std::runtime_error("BV stream corrupt: outdegree > n");
-        if (d == 0) { roff.push_back(c.size()); degs[sg][i - r0] = 0; continue; }
-        uint64_t r = p.window ? br.unary() : 0;
-        if (r > p.window || (r && i < r0 + r)) throw std::runtime_error("BV stream corrupt: bad reference");
-        copied.clear();
-        if (r) {
-          uint32_t j = i - (uint32_t)r;
-          if (depth[j - r0] >= R) throw std::runtime_error("BV stream corrupt: chain exceeds R");
-          depth[i - r0] = depth[j - r0] + 1;
-          out.ref_dist[i] = (uint8_t)r;
-          const uint32_t* Rl = c.data() + roff[j - r0];
-          uint64_t dr = roff[j - r0 + 1] - roff[j - r0];
-          uint64_t b = br.gamma();
-          if (b > dr + 1) throw std::runtime_error("BV stream corrupt: too many copy blocks");
-          uint64_t pos = 0;
-          bool cp = true;
-          for (uint64_t k = 0; k < b; ++k) {
-            uint64_t len = k == 0 ? br.gamma() : br.gamma() + 1;
-            if (pos + len > dr) throw std::runtime_error("BV stream corrupt: copy block overflow");
-            if (cp) copied.insert(copied.end(), Rl + pos, Rl + pos + len);
-            pos += len;
-            cp = !cp;
-          }
-          if (cp) copied.insert(copied.end(), Rl + pos, Rl + dr);
-        }
-        if (copied.size() > d) throw std::runtime_error("BV stream corrupt: copied > outdegree");
-        uint64_t extra = d - copied.size();
-        expanded.clear();
-        tmp.clear();
-        if (extra) {
-          uint64_t ni = br.gamma();
-          uint64_t prev_end = 0, in_int = 0;
-          for (uint64_t k = 0; k < ni; ++k) {
-            int64_t left = k == 0 ? (int64_t)i + unfold_signed(br.gamma()) : (int64_t)(prev_end + br.gamma() + 1);
-            uint64_t len = br.gamma() + p.min_interval;
-            if (left < 0 || (uint64_t)left + len > s.n) throw std::runtime_error("BV stream corrupt: interval out of range");
-            for (uint64_t t = 0; t < len; ++t) expanded.push_back((uint32_t)(left + t));
-            prev_end = (uint64_t)left + len;
-            in_int += len;
-          }
-          if (in_int > extra) throw std::runtime_error("BV stream corrupt: intervals exceed outdegree");
-          uint64_t nres = extra - in_int;
-          int64_t prev = 0;
-          for (uint64_t k = 0; k < nres; ++k) {
-            int64_t v = k == 0 ? (int64_t)i + unfold_signed(br.zeta(p.zeta_k)) : prev + (int64_t)br.zeta(p.zeta_k) + 1;
-            if (v < 0 || v >= (int64_t)s.n) throw std::runtime_error("BV stream corrupt: residual out of range");
-            tmp.push_back((uint32_t)v);
-            prev = v;
-          }
-        }
-        merged.resize(copied.size() + expanded.size());
-        std::merge(copied.begin(), copied.end(), expanded.begin(), expanded.end(), merged.begin());
-        size_t base = c.size();
-        c.resize(base + merged.size() + tmp.size());
-        std::merge(merged.begin(), merged.end(), tmp.begin(), tmp.end(), c.begin() + base);
-        for (size_t t = base + 1; t < c.size(); ++t)
-          if (c[t] <= c[t - 1]) throw std::runtime_error("BV stream corrupt: row not strictly increasing");
-        roff.push_back(c.size());
-        degs[sg][i - r0] = (uint32_t)d;
-      }
-      if (br.pos() != s.segment_bit_offsets[sg + 1]) throw std::runtime_error("BV stream corrupt: segment length mismatch");
+      const uint32_t r1 = (uint32_t)std::min<uint64_t>(s.n, (sg + 1) * seg);
+      degs[sg].resize(r1 - sg * seg);
+      decode_segment_rows(s, sg, r1, cols[sg], w, out.ref_dist.data(), degs[sg].data());
     }
   });
   HostCsr& g = out.csr;

@@ -14,6 +14,7 @@
 //   u64 nbits | u64 nseg | u64 segment_bit_offsets[nseg + 1]
 //   u32 words[ceil(nbits / 32)]        (MSB-first bit stream, host/bits.hpp)
 //   u64 FNV-1a of every preceding byte
+#include <mutex>
 #include <cstdio>
 #include <cstring>
 #include <fstream>
@@ -137,6 +138,67 @@ BvStream decode_bv_container(const uint8_t* p, size_t len) {
       s.stats.max_depth = std::max(s.stats.max_depth, depth[i]);
     }
   }
+  // the encoder's edge statistics, recomputed from the decoded rows: copied =
+  // row and reference in common, minus = the reference's other entries, the
+  // extra entries split into maximal runs >= Lmin (intervals) and residuals
+  const HostCsr& g = d.csr;
+  std::mutex mu;
+  parallel_for(s.n, [&](uint64_t b0, uint64_t b1) {
+    BvStats t;
+    for (uint64_t i = b0; i < b1; ++i) {
+      const uint32_t r = d.ref_dist[i];
+      const uint32_t* L = g.row((uint32_t)i);
+      const uint32_t dl = g.deg((uint32_t)i);
+      uint64_t common = 0;
+      uint32_t run = 0, prev = 0;
+      bool have = false;
+      auto extra = [&](uint32_t c) {  // extras arrive in increasing order
+        if (have && c == prev + 1) {
+          ++run;
+        } else {
+          if (run) {
+            if (run >= s.params.min_interval) {
+              t.interval_edges += run;
+              ++t.intervals;
+            } else {
+              t.residual_edges += run;
+            }
+          }
+          run = 1;
+        }
+        prev = c;
+        have = true;
+      };
+      if (r) {
+        const uint32_t* R = g.row((uint32_t)i - r);
+        const uint32_t dr = g.deg((uint32_t)i - r);
+        uint32_t a = 0, b = 0;
+        while (a < dl) {
+          if (b < dr && R[b] < L[a]) ++b;
+          else if (b < dr && R[b] == L[a]) { ++common; ++a; ++b; }
+          else extra(L[a++]);
+        }
+        t.copied_edges += common;
+        t.minus_edges += dr - common;
+      } else {
+        for (uint32_t a = 0; a < dl; ++a) extra(L[a]);
+      }
+      if (run) {
+        if (run >= s.params.min_interval) {
+          t.interval_edges += run;
+          ++t.intervals;
+        } else {
+          t.residual_edges += run;
+        }
+      }
+    }
+    std::lock_guard<std::mutex> lk(mu);
+    s.stats.copied_edges += t.copied_edges;
+    s.stats.minus_edges += t.minus_edges;
+    s.stats.interval_edges += t.interval_edges;
+    s.stats.intervals += t.intervals;
+    s.stats.residual_edges += t.residual_edges;
+  });
   return s;
 }
 

@@ -136,6 +136,10 @@ HostCsr generate_social(const SocialParams& p);
 // ---- BV codec (bv_codec.cpp) ----------------------------------------------
 BvStream bv_encode(const HostCsr& g, const BvParams& p);
 BvDecoded bv_decode(const BvStream& s);
+// Row i of the source adjacency, decoded from its segment's start (references
+// never leave a segment): the reference's reconstruct_row
+// (ref_matrix.hpp:71-73).  std::out_of_range if i >= n.
+std::vector<uint32_t> bv_reconstruct_row(const BvStream& s, uint32_t i);
 HostCsr transpose_csr(const HostCsr& g);
 
 // ---- biclique covers (biclique.cpp; reference include/cmv/biclique.hpp) ----

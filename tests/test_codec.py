@@ -2,6 +2,7 @@
 decode round trip, corruption detection), the BV-D device-layout builder
 (re-decoded with the kernels' arithmetic in tests/layout_ref.py), and the
 C-ABI surface (library loads and exports every symbol include/cmvg.h declares)."""
+import ctypes
 import os
 import re
 
@@ -211,3 +212,20 @@ def test_compression_stats():
     e = P.compression_stats(P.BvStream.encode(csr_from_rows([[]] * 5),
                                               P.BvParams()))
     assert e.m_prime == 0 and e.ratio == 1.0 and e.ratio_by_convention
+
+
+@pytest.mark.parametrize("cfg,n,seg", [(1, 5000, 1024), (4, 3000, 1024), (2, 4000, 7)])
+def test_reconstruct_row_random_access(cfg, n, seg):
+    """reconstruct_row (ref_matrix.hpp:71-73): any row from the stream alone,
+    bit-exact; out_of_range past n (IndexError), also through the C ABI."""
+    g = make_graph(cfg, n=n)
+    s = P.BvStream.encode(g, bv_params(cfg) if seg == 1024 else P.BvParams(segment_rows=seg))
+    rows = rows_of(g)
+    rng = np.random.default_rng(cfg)
+    for i in list(rng.integers(0, n, 60)) + [0, n - 1, seg - 1, min(seg, n - 1)]:
+        assert s.reconstruct_row(int(i)).tolist() == rows[int(i)]
+    with pytest.raises(IndexError):
+        s.reconstruct_row(n)
+    lib = P.load_library()
+    d = ctypes.c_uint64()
+    assert lib.cmvg_bv_reconstruct_row(s._h, n, None, 0, ctypes.byref(d)) == 2  # CMVG_ERR_RANGE

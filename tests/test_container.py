@@ -119,3 +119,11 @@ def test_corrupt_contents_with_valid_checksum():
 def test_load_missing_file(tmp_path):
     with pytest.raises(ValueError):  # invalid_argument, as for an unusable path
         P.BvStream.load(str(tmp_path / "missing.cbv"))
+
+
+def test_loaded_stream_keeps_edge_statistics():
+    """A loaded container recomputes the encoder's edge statistics from the
+    decoded rows (cmv::stats on a loaded stream, ref_matrix.hpp:78-89)."""
+    g = P.CsrGraph.copy_model(6000, 10.0, seed=3)
+    s = P.BvStream.encode(g, P.BvParams())
+    assert P.BvStream.from_bytes(s.to_bytes()).stats() == s.stats()
