@@ -122,15 +122,21 @@ struct BvfTerms {
     double v;
     if (e) v = (double)ev;
     else v = lds_f64(tab + off);
-    const double sg = __hiloint2double((int)((signw & 0x80000000u) | 0x3ff00000u), 0);  // +-1
+    // the minus flag flips the sign bit of the value (and of its F lo part);
+    // the split of -v is the negated split of v up to the choice of h on a
+    // tie, and either choice keeps h a multiple of G and v - h exact
+    const uint32_t sm = signw & 0x80000000u;
+    v = __hiloint2double(__double2hiint(v) ^ (int)sm, __double2loint(v));
     if (SPLIT) {
-      double wl = 0.0;
-      if (off >= f0b && !e) wl = lds_f64(flo_b + off);
       const double h = (v + sigma) - sigma;
-      ah = fma(sg, h, ah);
-      al = fma(sg, (v - h) + wl, al);
+      ah += h;
+      al += v - h;
+      if (off >= f0b && !e) {  // F term: its lo part (a predicated load)
+        const double wl = lds_f64(flo_b + off);
+        al += __hiloint2double(__double2hiint(wl) ^ (int)sm, __double2loint(wl));
+      }
     } else {
-      ah = fma(sg, v, ah);
+      ah += v;
     }
     if (END && (c & kBvfEnd)) {
       if (SPLIT) {
