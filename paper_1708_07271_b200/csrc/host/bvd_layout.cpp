@@ -6,6 +6,7 @@
 #include <stdexcept>
 
 #include "bits.hpp"
+#include "bvf_block.hpp"
 
 #include <atomic>
 #include <chrono>
@@ -92,277 +93,6 @@ inline uint32_t bits32(const std::vector<uint32_t>& w, uint64_t pos, uint64_t en
   const uint64_t left = end - pos;
   if (left < 32) v &= ~0u << (32 - left);
   return v;
-}
-
-// Shared-memory bank schedule of a BV-F block: in term step j the 32 chunks of
-// a warp load table entries at once, 8 bytes each, in two half-warp phases of
-// 16 lanes; lanes of one phase hitting the same bank pair (index mod 16) at
-// different entries serialise.  A row's terms may be summed in any order, so
-// each row's terms are re-dealt to the row's positions (which stay fixed: the
-// chunking and the row ends do not move) greedily per phase, the most
-// constrained lane first, each lane taking the term whose bank pair is least
-// loaded in its phase (a term at an entry already loaded is free: broadcast).
-// F terms also load F lo (a second, predicated load): their placement counts
-// that load's conflicts plus one for opening it in a phase.  Measured on the
-// C2 generator: 5.6 + 2.4 -> 3.0 + 1.6 wavefronts per term step (ideal 2).
-void bvf_schedule_terms(std::vector<uint16_t>& codes, std::vector<uint32_t>& ecol, const std::vector<uint32_t>& rstart,
-                        uint32_t N, uint32_t K, uint32_t nact, uint32_t F0) {
-  const uint32_t nrows = (uint32_t)rstart.size();
-  std::vector<uint32_t> rowof(N);
-  for (uint32_t k = 0; k < nrows; ++k) {
-    const uint32_t e = k + 1 < nrows ? rstart[k + 1] : N;
-    for (uint32_t p = rstart[k]; p < e; ++p) rowof[p] = k;
-  }
-  // per-row pools: [pbeg[k], pend[k]) of (code without end flag, escape column)
-  std::vector<uint16_t> pc(codes.begin(), codes.begin() + N);
-  std::vector<uint32_t> pe(ecol.begin(), ecol.begin() + N);
-  for (auto& c : pc) c &= (uint16_t)~kBvfEnd;
-  std::vector<uint32_t> pend(nrows);
-  for (uint32_t k = 0; k < nrows; ++k) pend[k] = k + 1 < nrows ? rstart[k + 1] : N;
-  uint32_t lanes[16];
-  uint16_t seen[16][8], fseen[16][8];
-  uint8_t nseen[16], nfseen[16];
-  for (uint32_t j = 0; j < K; ++j) {
-    for (uint32_t h0 = 0; h0 < nact; h0 += 16) {
-      uint32_t nl = 0;
-      for (uint32_t t = h0; t < std::min(nact, h0 + 16); ++t)
-        if ((size_t)t * K + j < N) lanes[nl++] = t;
-      // most constrained (fewest remaining terms) first
-      std::sort(lanes, lanes + nl, [&](uint32_t a, uint32_t b) {
-        const uint32_t ra = rowof[(size_t)a * K + j], rb = rowof[(size_t)b * K + j];
-        return pend[ra] - rstart[ra] < pend[rb] - rstart[rb];
-      });
-      std::memset(nseen, 0, sizeof(nseen));
-      std::memset(nfseen, 0, sizeof(nfseen));
-      uint32_t nf = 0;  // F terms in this phase: their second (lo) load is a separate, predicated one
-      for (uint32_t q = 0; q < nl; ++q) {
-        const size_t pos = (size_t)lanes[q] * K + j;
-        const uint32_t k = rowof[pos];
-        uint32_t best = rstart[k], bcost = 0xffffffffu;
-        bool bdup = false;
-        for (uint32_t i = rstart[k]; i < pend[k]; ++i) {
-          const uint32_t c = pc[i];
-          uint32_t cost = 0;
-          bool dup = true;
-          if (!(c & kBvfEsc)) {
-            const uint32_t idx = c & kBvfIdxMask, bk = idx & 15u;
-            cost = nseen[bk];
-            dup = false;
-            for (uint32_t s = 0; s < std::min<uint32_t>(nseen[bk], 8); ++s)
-              if (seen[bk][s] == idx) {
-                cost = 0;
-                dup = true;
-              }
-            if (idx >= F0) {  // the F lo load: a first F term opens a wavefront, later ones may conflict
-              uint32_t fc = nfseen[bk];
-              for (uint32_t s = 0; s < std::min<uint32_t>(nfseen[bk], 8); ++s)
-                if (fseen[bk][s] == idx) fc = 0;
-              cost += fc + (nf == 0 ? 1u : 0u);
-            }
-          }
-          if (cost < bcost) {
-            bcost = cost;
-            best = i;
-            bdup = dup;
-            if (!cost) break;
-          }
-        }
-        const uint16_t c = pc[best];
-        const uint32_t e = pe[best];
-        // take it: the pool's last term fills its place
-        --pend[k];
-        pc[best] = pc[pend[k]];
-        pe[best] = pe[pend[k]];
-        codes[pos] = c;
-        ecol[pos] = e;
-        if (!bdup) {
-          const uint32_t bk = (c & kBvfIdxMask) & 15u;
-          if (nseen[bk] < 8) seen[bk][nseen[bk]] = (uint16_t)(c & kBvfIdxMask);
-          ++nseen[bk];
-        }
-        if (!(c & kBvfEsc) && (c & kBvfIdxMask) >= F0) {
-          const uint32_t idx = c & kBvfIdxMask, bk = idx & 15u;
-          bool have = false;
-          for (uint32_t s = 0; s < std::min<uint32_t>(nfseen[bk], 8); ++s) have |= fseen[bk][s] == idx;
-          if (!have) {
-            if (nfseen[bk] < 8) fseen[bk][nfseen[bk]] = (uint16_t)idx;
-            ++nfseen[bk];
-          }
-          ++nf;
-        }
-      }
-    }
-  }
-  for (uint32_t k = 0; k < nrows; ++k) {  // a row's last position ends it
-    const uint32_t e = k + 1 < nrows ? rstart[k + 1] : N;
-    codes[e - 1] |= (uint16_t)kBvfEnd;
-  }
-}
-
-// BV-F block stream from the block's rows (layout.hpp): the flat term list in
-// row order, cut into equal chunks (one per thread).
-void emit_bvf(const RowParts* rps, const RowMeta* meta, uint32_t nr, uint64_t wlo, uint32_t W, uint64_t maxdeg,
-              std::vector<uint32_t>& out, BvfBlockInfo& info, BvfStats& st) {
-  auto inwin = [&](uint64_t c) { return c >= wlo && c < wlo + W; };
-  auto int_inside = [&](const std::pair<uint32_t, uint32_t>& iv) {
-    return iv.first >= wlo && (uint64_t)iv.first + iv.second <= wlo + W;
-  };
-  // far columns, the most used ones first into the slots
-  thread_local std::vector<uint32_t> farc;
-  farc.clear();
-  for (uint32_t k = 0; k < nr; ++k) {
-    const RowParts& rp = rps[k];
-    for (uint32_t c : rp.minus)
-      if (!inwin(c)) farc.push_back(c);
-    for (uint32_t c : rp.res)
-      if (!inwin(c)) farc.push_back(c);
-    for (const auto& iv : rp.ints)
-      if (!int_inside(iv))
-        for (uint64_t c = iv.first; c < (uint64_t)iv.first + iv.second; ++c)
-          if (!inwin(c)) farc.push_back((uint32_t)c);
-  }
-  std::sort(farc.begin(), farc.end());
-  std::vector<std::pair<uint32_t, uint32_t>> freq;  // (-count, col)
-  for (size_t a = 0; a < farc.size();) {
-    size_t e = a;
-    while (e < farc.size() && farc[e] == farc[a]) ++e;
-    freq.push_back({(uint32_t)(0u - (uint32_t)(e - a)), farc[a]});
-    a = e;
-  }
-  std::sort(freq.begin(), freq.end());
-  const uint32_t nslot = (uint32_t)std::min<size_t>(freq.size(), kBvfSlots);
-  std::vector<std::pair<uint32_t, uint32_t>> slot;  // (col, slot), sorted by col
-  slot.reserve(nslot);
-  for (uint32_t s = 0; s < nslot; ++s) slot.push_back({freq[s].second, s});
-  std::sort(slot.begin(), slot.end());
-  const uint32_t F0 = bvf_f0(W), ZERO = bvf_zero(W);
-  thread_local std::vector<uint16_t> codes;
-  thread_local std::vector<uint32_t> ecol, rstart;
-  codes.clear();
-  ecol.clear();
-  rstart.clear();
-  uint64_t terms = 0, slot_terms = 0, esc_terms = 0, pad_terms = 0;
-  auto xterm = [&](uint32_t c, bool minus) {
-    uint32_t code;
-    if (inwin(c)) {
-      code = (uint32_t)(c - wlo);
-    } else {
-      auto it = std::lower_bound(slot.begin(), slot.end(), std::make_pair(c, 0u));
-      if (it != slot.end() && it->first == c) {
-        code = W + it->second;
-        ++slot_terms;
-      } else {
-        code = kBvfEsc;
-        ++esc_terms;
-      }
-    }
-    codes.push_back((uint16_t)(code | (minus ? kBvfMinus : 0u)));
-    ecol.push_back(c);
-    ++terms;
-  };
-  // exactness bound of the split accumulation (units of 2^E): a row's terms
-  // plus the transient of one F term; chain sums are differences of row sums
-  // (<= 2 max degree)
-  uint64_t umax = 0;
-  for (uint32_t k = 0; k < nr; ++k) {
-    rstart.push_back((uint32_t)codes.size());
-    const RowParts& rp = rps[k];
-    uint64_t u = rp.minus.size() + rp.res.size();
-    for (uint32_t c : rp.minus) xterm(c, true);
-    for (uint32_t c : rp.res) xterm(c, false);
-    for (const auto& iv : rp.ints) {
-      u += iv.second;
-      if (int_inside(iv)) {
-        const uint32_t a = (uint32_t)(iv.first - wlo);
-        codes.push_back((uint16_t)(F0 + a + iv.second));
-        ecol.push_back(0);
-        codes.push_back((uint16_t)((F0 + a) | kBvfMinus));
-        ecol.push_back(0);
-        terms += 2;
-      } else {
-        for (uint64_t c = iv.first; c < (uint64_t)iv.first + iv.second; ++c) xterm((uint32_t)c, false);
-      }
-    }
-    // every row gets an even number of terms (padding terms read the zero
-    // entry): rows then end only on the second term of a code word, and the
-    // term loop needs one row-end store per word instead of one per term
-    while (codes.size() == rstart.back() || ((codes.size() - rstart.back()) & 1u)) {
-      codes.push_back((uint16_t)ZERO);
-      ecol.push_back(0);
-      ++pad_terms;
-    }
-    codes.back() |= (uint16_t)kBvfEnd;
-    umax = std::max(umax, u);
-  }
-  const uint64_t N = codes.size();
-  const uint32_t K = 16u * (uint32_t)std::max<uint64_t>(1, (N + 4095) / 4096);
-  if (K > 0xffffu || K > kBvfIdxMask) throw std::runtime_error("BV-F: block too large");
-  const uint32_t nact = (uint32_t)((N + K - 1) / K);
-  pad_terms += (uint64_t)nact * K - N;
-  codes.resize((size_t)nact * K, (uint16_t)ZERO);
-  ecol.resize((size_t)nact * K, 0);
-  bvf_schedule_terms(codes, ecol, rstart, (uint32_t)N, K, nact, F0);
-  // escape terms: index within the chunk's escape segment
-  std::vector<uint32_t> escstart(nact + 1, 0), escc;
-  for (uint32_t t = 0; t < nact; ++t) {
-    uint32_t loc = 0;
-    for (uint32_t i = t * K; i < (t + 1) * K; ++i)
-      if (codes[i] & kBvfEsc) {
-        codes[i] = (uint16_t)((codes[i] & ~kBvfIdxMask) | loc++);
-        escc.push_back(ecol[i]);
-      }
-    escstart[t + 1] = escstart[t] + loc;
-  }
-  const uint32_t nesc = (uint32_t)escc.size();
-  // split grid: 2^cbits units per |x| <= 2^E, sums exact while < 2^53
-  const uint64_t bound = 2ull * W + umax + 2 * maxdeg + 2;
-  uint32_t lg = 0;
-  while ((1ull << lg) < bound) ++lg;
-  const uint32_t cbits = (uint32_t)std::max(8, std::min(40, 51 - (int)lg));
-  // stream
-  out.clear();
-  out.resize(bvf_far_off(nact), 0u);
-  uint16_t* sr = reinterpret_cast<uint16_t*>(out.data());
-  for (uint32_t t = 0; t < nact; ++t) {
-    const uint32_t i = t * K;
-    const uint32_t row = (uint32_t)(std::upper_bound(rstart.begin(), rstart.end(), i) - rstart.begin()) - 1u;
-    sr[t] = (uint16_t)row;
-  }
-  uint32_t* rn = out.data() + bvf_rn_off(nact);
-  for (uint32_t k = 0; k < nr; ++k) rn[k >> 3] |= (meta[k].r & 15u) << (4 * (k & 7));
-  for (uint32_t s = 0; s < nslot; ++s) out.push_back(freq[s].second);
-  out.resize(bvf_align4((uint32_t)out.size()), 0u);
-  const uint32_t esc_off = (uint32_t)out.size();
-  if (nesc) {
-    for (uint32_t t = 0; t <= nact; ++t) out.push_back(escstart[t]);  // + the total
-    out.resize(bvf_align4((uint32_t)out.size()), 0u);
-    for (uint32_t c : escc) out.push_back(c);
-    out.resize(bvf_align4((uint32_t)out.size()), 0u);
-  }
-  const uint32_t codes_off = (uint32_t)out.size();
-  out.resize((size_t)codes_off + (size_t)(K / 2) * nact, 0u);
-  for (uint32_t t = 0; t < nact; ++t)
-    for (uint32_t q = 0; q < K / 2; ++q)
-      out[(size_t)codes_off + (size_t)q * nact + t] =
-          (uint32_t)codes[(size_t)t * K + 2 * q] | ((uint32_t)codes[(size_t)t * K + 2 * q + 1] << 16);
-  out.resize(bvf_align4((uint32_t)out.size()), 0u);
-  info = BvfBlockInfo{};
-  info.wlo = (uint32_t)wlo;
-  info.K = (uint16_t)K;
-  info.nact = (uint16_t)nact;
-  info.nslot = (uint16_t)nslot;
-  info.cbits = (uint8_t)cbits;
-  info.flags = nesc ? kBvfFlagEsc : 0u;
-  info.codes_off = codes_off;
-  info.esc_off = esc_off;
-  info.nwords = (uint32_t)out.size();
-  st.terms += terms;
-  st.pad_terms += pad_terms;
-  st.slot_terms += slot_terms;
-  st.esc_terms += esc_terms;
-  st.esc_blocks += nesc ? 1 : 0;
-  st.max_K = std::max(st.max_K, K);
-  st.min_cbits = std::min<uint32_t>(st.min_cbits, cbits);
 }
 
 // BV-S block stream from the block's rows (layout.hpp).  Units and their
@@ -983,9 +713,32 @@ BvdLayout build_bvd(const BvDecoded& dec, const BvParams& bp, const BvdOptions& 
       auto tB = std::chrono::steady_clock::now();
       if (opt.bvs) emit_bvs(rps.data(), meta.data(), body, nr, lo, W, bp.min_interval, sstream[b], bst[b]);
       if (opt.bvf) {
-        uint64_t maxdeg = 0;
-        for (uint32_t k = 0; k < nr; ++k) maxdeg = std::max<uint64_t>(maxdeg, g.deg(r0 + k));
-        emit_bvf(rps.data(), meta.data(), nr, lo, W, maxdeg, fstream[b], L.fblocks[b], fst[b]);
+        // the shared host/device block builder (bvf_block.hpp)
+        const BvfRowsView view{g.row_offsets.data(), g.cols.data(), dec.ref_dist.data(), g.n};
+        uint64_t E = 0, Er = 0;
+        for (uint32_t k = 0; k < nr; ++k) {
+          const uint32_t i = r0 + k, r = dec.ref_dist[i];
+          E += g.deg(i);
+          if (r && k >= r) Er += g.deg(i - r);
+        }
+        thread_local std::vector<uint32_t> arena, obuf;
+        arena.resize(bvf_block_scratch_words(E, Er, nr, bp.min_interval));
+        obuf.assign(bvf_block_out_words(E, Er, nr, bp.min_interval), 0u);
+        BvfArena ar{arena.data(), arena.size(), 0};
+        const BvfBlockResult res = bvf_build_block(view, (uint32_t)b, B, W, bp.min_interval, ar, obuf.data(), obuf.size());
+        if (res.err) throw std::runtime_error("BV-F block build failed (code " + std::to_string(res.err) + ")");
+        fstream[b].assign(obuf.begin(), obuf.begin() + res.nwords);
+        L.fblocks[b] = res.info;
+        BvfStats& t = fst[b];
+        t.terms = res.terms;
+        t.pad_terms = res.pad_terms;
+        t.slot_terms = res.slot_terms;
+        t.esc_terms = res.esc_terms;
+        t.esc_blocks = (res.info.flags & kBvfFlagEsc) ? 1 : 0;
+        t.max_K = res.info.K;
+        t.min_cbits = res.info.cbits;
+        if (res.info.wlo != (uint32_t)lo || res.depth != bdepth[b] || res.adds != badds[b])
+          throw std::runtime_error("BV-F block builder disagrees with the BV-D pass (window / depth / adds)");
       }
       auto tC = std::chrono::steady_clock::now();
       {  // columns this block reads outside its x-window (read set of a shard)
