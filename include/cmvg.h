@@ -189,6 +189,13 @@ const uint32_t* cmvg_layout_swords(const cmvg_layout* l, uint64_t* nwords);
 const uint32_t* cmvg_layout_sblocks(const cmvg_layout* l, uint32_t* nblocks);
 /* BV-T words / block table */
 const uint32_t* cmvg_layout_twords(const cmvg_layout* l, uint64_t* nwords);
+/* The BV-F layout a device handle's products read (built on the GPU by
+ * cmvg_create unless CMVG_HOST_BUILD is set), copied to host memory: the
+ * shard's words (block word offsets relative to its first block) and its
+ * block table (8 u32 per block: BvfBlockInfo).  Null pointers query the
+ * counts.  (Test / inspection entry point; no reference counterpart.) */
+int cmvg_bvf_export(const cmvg_graph* g, uint32_t* words, uint64_t words_cap, uint32_t* blocks, uint64_t blocks_cap,
+                    uint64_t* nwords, uint32_t* nblocks, int* device_built);
 /* BV-F words / block table (8 u32 per block: BvfBlockInfo, host/layout.hpp) */
 const uint32_t* cmvg_layout_fwords(const cmvg_layout* l, uint64_t* nwords);
 const uint32_t* cmvg_layout_fblocks(const cmvg_layout* l, uint32_t* nblocks);

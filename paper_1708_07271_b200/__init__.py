@@ -129,6 +129,8 @@ _SIGS = [
     ("cmvg_destroy", C.c_int, [_P]),
     ("cmvg_layout_info", C.c_int, [_P, C.POINTER(_OptsC), C.POINTER(_InfoC)]),
     ("cmvg_layout_export", C.c_int, [_P, C.POINTER(_OptsC), C.POINTER(_P)]),
+    ("cmvg_bvf_export", C.c_int, [_P, _P, C.c_uint64, _P, C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint32),
+                                  C.POINTER(C.c_int)]),
     ("cmvg_layout_words", _P, [_P, C.POINTER(C.c_uint64)]),
     ("cmvg_layout_blocks", _P, [_P, C.POINTER(C.c_uint32)]),
     ("cmvg_layout_swords", _P, [_P, C.POINTER(C.c_uint64)]),
@@ -772,6 +774,20 @@ class BvGraph:
         out = np.empty(cnt.value, dtype=np.uint32)
         _check(lib.cmvg_read_set(self._h, out.ctypes.data if cnt.value else None, cnt.value, C.byref(cnt)))
         return out
+
+    def bvf_export(self):
+        """(words u32[], blocks u32[nblocks, 8], device_built) of the BV-F layout
+        this handle's products read (the same format as
+        BvStream.layout_export(kind="bvf"), block offsets relative to the
+        handle's first block)."""
+        lib = load_library()
+        nw, nb, dev = C.c_uint64(), C.c_uint32(), C.c_int()
+        _check(lib.cmvg_bvf_export(self._h, None, 0, None, 0, C.byref(nw), C.byref(nb), C.byref(dev)))
+        w = np.empty(nw.value, np.uint32)
+        b = np.empty((nb.value, 8), np.uint32)
+        _check(lib.cmvg_bvf_export(self._h, w.ctypes.data, w.size, b.ctypes.data, b.size, C.byref(nw), C.byref(nb),
+                                   C.byref(dev)))
+        return w, b, bool(dev.value)
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value and _lib_handle is not None:

@@ -2,6 +2,7 @@
 #include "cuda/bv_decode.cuh"
 #include "internal.hpp"
 
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -11,6 +12,116 @@ thread_local std::string g_last_error;
 }
 
 // ---------------------------------------------------------------------------
+namespace cmvg {
+// The columns of x a shard's gather reads: its blocks' x-windows, far slots
+// and escape columns (device-built handles: from the BV-F stream, on first use)
+void ensure_read_set(const cmvg_graph* g) {
+  if (g->have_read_set) return;
+  std::lock_guard<std::mutex> lk(const_cast<cmvg_graph*>(g)->layout_mu);
+  if (g->have_read_set) return;
+  DeviceGuard dg(g->device);
+  std::vector<BvfBlockInfo> bl(g->nblocks);
+  std::vector<uint32_t> w(g->f_stream_bytes / 4);
+  CUDA_TRY(cudaMemcpy(bl.data(), g->fblocks.p, bl.size() * sizeof(BvfBlockInfo), cudaMemcpyDeviceToHost));
+  if (!w.empty()) CUDA_TRY(cudaMemcpy(w.data(), g->fwords.p, w.size() * 4, cudaMemcpyDeviceToHost));
+  std::vector<uint64_t> bm(((uint64_t)g->n + 63) / 64, 0);
+  auto mark = [&](uint64_t c) { bm[c >> 6] |= 1ull << (c & 63); };
+  for (const BvfBlockInfo& b : bl) {
+    const uint64_t w1 = std::min<uint64_t>(g->n, (uint64_t)b.wlo + g->dims.window);
+    for (uint64_t c = b.wlo; c < w1; ++c) mark(c);
+    const uint32_t* s = w.data() + b.word_offset;
+    for (uint32_t q = 0; q < b.nslot; ++q) mark(s[bvf_far_off(b.nact) + q]);
+    if (b.flags & kBvfFlagEsc) {
+      const uint32_t* es = s + b.esc_off;
+      const uint32_t* ec = es + bvf_align4(b.nact + 1u);
+      for (uint32_t q = 0; q < es[b.nact]; ++q) mark(ec[q]);
+    }
+  }
+  std::vector<uint32_t>& rs = g->read_set;
+  rs.clear();
+  for (uint64_t wi = 0; wi < bm.size(); ++wi)
+    for (uint64_t v = bm[wi]; v; v &= v - 1) rs.push_back((uint32_t)(wi * 64 + __builtin_ctzll(v)));
+  g->have_read_set = true;
+}
+}  // namespace cmvg
+
+namespace cmvg {
+bool decode_tiles_ok(const cmvg_graph* g) {
+  return kDecTileRows % g->params.segment_rows == 0 && kDecTileRows % kDecGroup == 0 && !getenv("CMVG_SERIAL_DECODE");
+}
+
+// BV stream (device copy) -> CSR in device memory (+ each row's reference
+// distance when ref_out is given; the tile decoder only).  Throws on a
+// corrupt stream.
+void decode_device(cmvg_graph* g, uint64_t* ro, uint32_t* co, uint8_t* ref_out, cudaStream_t st) {
+  BvDev s{};
+  s.words = g->bv_words.as<uint32_t>();
+  s.seg_bits = g->bv_seg.as<uint64_t>();
+  s.n = g->n;
+  s.seg_rows = g->params.segment_rows;
+  s.nseg = (uint32_t)g->nseg;
+  s.window = g->params.window;
+  s.min_interval = g->params.min_interval;
+  s.zeta_k = g->params.zeta_k;
+  StreamScratch deg(g->device, (size_t)g->n * 4, st), err(g->device, 16, st);
+  CUDA_TRY(cudaMemsetAsync(err.p, 0, 4, st));
+  int herr = 0;
+  const int tpb = 64;
+  if (!decode_tiles_ok(g)) {
+    if (ref_out) throw std::logic_error("reference distances need the tile decoder");
+    // serial decoder (segments that do not tile; tests): per-segment parse
+    // and scan, then one thread per segment writes its rows
+    StreamScratch rbit(g->device, (size_t)g->n * 8, st), segsum(g->device, g->nseg * 8, st),
+        segbase(g->device, g->nseg * 8, st);
+    bv_index_rows<<<(unsigned)((g->nseg + tpb - 1) / tpb), tpb, 0, st>>>(s, deg.as<uint32_t>(), rbit.as<uint64_t>(),
+                                                                        segsum.as<uint64_t>(), err.as<int>());
+    CUDA_TRY(cudaGetLastError());
+    bv_scan_segments<<<1, 1024, 0, st>>>(segsum.as<uint64_t>(), g->nseg, 1, g->m, segbase.as<uint64_t>(),
+                                         err.as<int>());
+    CUDA_TRY(cudaGetLastError());
+    bv_seg_decode<<<(unsigned)((g->nseg + tpb - 1) / tpb), tpb, 0, st>>>(s, segbase.as<uint64_t>(), ro, co,
+                                                                        err.as<int>());
+  } else {
+    const uint32_t ng = (uint32_t)(((uint64_t)g->n + kDecGroup - 1) / kDecGroup);
+    {  // the handle's row-group index: one serial pass per segment, once
+      std::lock_guard<std::mutex> lk(g->layout_mu);
+      if (!g->have_sync) {
+        g->bv_sync.alloc((size_t)ng * sizeof(DecSync));
+        bv_sync_index<<<(unsigned)((g->nseg + tpb - 1) / tpb), tpb, 0, st>>>(s, deg.as<uint32_t>(),
+                                                                            g->bv_sync.as<DecSync>(), err.as<int>());
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaMemcpyAsync(&herr, err.p, 4, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        if (herr) throw AbiError(CMVG_ERR_CORRUPT, "BV stream corrupt (device index pass, code " + std::to_string(herr) + ")");
+        g->have_sync = true;
+      }
+    }
+    StreamScratch rbit(g->device, (size_t)g->n * 8, st), gcnt(g->device, (size_t)ng * 8, st),
+        gbase(g->device, (size_t)ng * 8, st);
+    bv_index_groups<<<(ng + 127) / 128, 128, 0, st>>>(s, g->bv_sync.as<DecSync>(), deg.as<uint32_t>(),
+                                                      rbit.as<uint64_t>(), gcnt.as<uint64_t>(), err.as<int>());
+    CUDA_TRY(cudaGetLastError());
+    bv_scan_segments<<<1, 1024, 0, st>>>(gcnt.as<uint64_t>(), ng, kDecTileRows / kDecGroup, g->m,
+                                         gbase.as<uint64_t>(), err.as<int>());
+    CUDA_TRY(cudaGetLastError());
+    uint32_t cap = 24064;  // staging words: two CTAs of ~100 KB per SM
+    if (const char* e = getenv("CMVG_DECODE_CAP")) cap = (uint32_t)strtoul(e, nullptr, 10);
+    const uint32_t sm = dec_smem_bytes(cap);
+    if (g->decode_attr < sm) {
+      CUDA_TRY(cudaFuncSetAttribute(bv_decode_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      g->decode_attr = sm;
+    }
+    const uint32_t ntile = (uint32_t)(((uint64_t)g->n + kDecTileRows - 1) / kDecTileRows);
+    bv_decode_tiles<<<ntile, kDecThreads, sm, st>>>(s, deg.as<uint32_t>(), rbit.as<uint64_t>(), gbase.as<uint64_t>(),
+                                                    cap, ro, co, err.as<int>(), ref_out);
+  }
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpyAsync(&herr, err.p, 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (herr) throw AbiError(CMVG_ERR_CORRUPT, "BV stream corrupt (device decode pass, code " + std::to_string(herr) + ")");
+}
+}  // namespace cmvg
+
 extern "C" {
 
 const char* cmvg_last_error(void) { return g_last_error.c_str(); }
@@ -382,75 +493,101 @@ int cmvg_create(const cmvg_bvstream* s, const cmvg_create_opts* opts_in, cmvg_gr
     CUDA_TRY(cudaGetDeviceCount(&ndev));
     require(o.device >= 0 && o.device < ndev, "no such CUDA device");
 
-    BvDecoded dec = bv_decode(bs);
-    if (dec.csr.m() != bs.m) throw std::runtime_error("BV stream corrupt: edge count mismatch");
     BvdOptions bo;
     bo.block_rows = o.block_rows;
     bo.window = o.window;
     bo.bvs = false;  // the sliced (matmat) and target-sorted (scatter) layouts are built on first use
     bo.bvt = false;
-    BvdLayout L = build_bvd(dec, bs.params, bo);
+    const uint32_t B = o.block_rows;
+    require(B && !(B & (B - 1)) && B % bs.params.segment_rows == 0 && B <= 1024,
+            "block_rows must be a power of two <= 1024 and a multiple of the BV segment");
+    require(o.window % 16 == 0 && o.window > 0, "window must be a positive multiple of 16");
 
     auto g = std::make_unique<cmvg_graph>();
     g->device = o.device;
     g->n = bs.n;
     g->m = bs.m;
     g->params = bs.params;
-    g->dims = L.dims;
     g->row_begin = o.row_begin;
     g->row_end = row_end;
     g->block_begin = o.row_begin / o.block_rows;
     const uint32_t block_end = (uint32_t)(((uint64_t)row_end + o.block_rows - 1) / o.block_rows);
     g->nblocks = block_end - g->block_begin;
-    g->stream_cap_words = o.stream_cap_words
-                              ? o.stream_cap_words
-                              : std::min<uint32_t>(12288, std::max<uint32_t>(1024, (L.stats.p995_block_words + 255) & ~255u));
-    g->stats.codes = L.stats.codes;
-    g->stats.window_coverage = L.stats.window_coverage;
-    g->stats.p995_block_words = L.stats.p995_block_words;
     g->interval_mode = o.interval_mode;
     g->threads = o.lanes;
     g->bv_bits = bs.nbits;
     g->nseg = bs.segment_bit_offsets.size() - 1;
+    static const bool timing = getenv("CMVG_BUILD_TIMING") != nullptr;
+    auto tc0 = std::chrono::steady_clock::now();
     g->host_stream = std::make_shared<const BvStream>(bs);
     g->build_opts = bo;
-
     DeviceGuard dg(o.device);
-    {  // read set: the blocks' x-windows and their out-of-window columns (bitmap, O(n))
-      std::vector<uint64_t> bm(((uint64_t)bs.n + 63) / 64, 0);
-      auto mark = [&](uint64_t c) { bm[c >> 6] |= 1ull << (c & 63); };
-      for (uint32_t b = g->block_begin; b < block_end; ++b) {
-        const uint64_t w0 = L.blocks[b].wlo, w1 = std::min<uint64_t>(bs.n, w0 + L.dims.window);
-        for (uint64_t c = w0; c < w1; ++c) mark(c);
-        for (uint64_t q = L.rfar_ptr[b]; q < L.rfar_ptr[b + 1]; ++q) mark(L.rfar[q]);
-      }
-      std::vector<uint32_t>& rs = g->read_set;
-      rs.clear();
-      for (uint64_t wi = 0; wi < bm.size(); ++wi)
-        for (uint64_t v = bm[wi]; v; v &= v - 1) rs.push_back((uint32_t)(wi * 64 + __builtin_ctzll(v)));
-    }
-    g->win_need.resize(g->nblocks);
-    g->far_need.resize(g->nblocks);
-    {
-      uint64_t pm = 0, fm = 0;
-      for (uint32_t q = 0; q < g->nblocks; ++q) {
-        const uint32_t b = g->block_begin + q;
-        pm = std::max<uint64_t>(pm, (uint64_t)L.blocks[b].wlo + L.dims.window);
-        g->win_need[q] = (uint32_t)std::min<uint64_t>(pm, bs.n);
-        for (uint64_t r = L.rfar_ptr[b]; r < L.rfar_ptr[b + 1]; ++r) fm = std::max<uint64_t>(fm, (uint64_t)L.rfar[r] + 1);
-        g->far_need[q] = (uint32_t)std::min<uint64_t>(fm, bs.n);
-      }
-    }
-    upload_layouts(g.get(), L, false, false, true);
-    // stats of the shard
-    const uint64_t w0 = L.blocks[g->block_begin].word_offset;
-    const uint64_t w1 = L.blocks[block_end - 1].word_offset + L.blocks[block_end - 1].nwords;
-    g->stats.stream_bytes = (w1 - w0) * 4;
-    g->stats.block_table_bytes = (uint64_t)g->nblocks * sizeof(BvdBlockInfo);
-    g->stats.row_bits = L.stats.row_bits;  // whole graph
-    g->adds = L.adds_per_product;
     g->bv_words.upload(bs.words.data(), bs.words.size());
     g->bv_seg.upload(bs.segment_bit_offsets.data(), bs.segment_bit_offsets.size());
+    if (timing)
+      fprintf(stderr, "[create] stream copy + upload %.2f ms\n",
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tc0).count());
+
+    // the BV-F layout: built on the GPU from the BV stream (bvf_build.cu), or
+    // on the host (CMVG_HOST_BUILD=1, and streams the tile decoder cannot serve)
+    bool built = false;
+    if (!getenv("CMVG_HOST_BUILD")) {
+      g->dims = BvdDims{bs.n, o.block_rows, o.window, bs.params.min_interval,
+                        (uint32_t)(((uint64_t)bs.n + o.block_rows - 1) / o.block_rows), 0, 0, 0};
+      DeviceBuildStats ds;
+      if (device_build_bvf(g.get(), 0, ds)) {
+        built = true;
+        g->device_built = true;
+        g->adds = ds.adds;
+        g->stats.window_coverage = ds.window_coverage;
+        g->stream_cap_words = o.stream_cap_words ? o.stream_cap_words : 1024u;
+      }
+    }
+    if (!built) {
+      BvDecoded dec = bv_decode(bs);
+      if (dec.csr.m() != bs.m) throw std::runtime_error("BV stream corrupt: edge count mismatch");
+      BvdLayout L = build_bvd(dec, bs.params, bo);
+      g->dims = L.dims;
+      g->stream_cap_words = o.stream_cap_words ? o.stream_cap_words
+                                               : std::min<uint32_t>(12288, std::max<uint32_t>(1024, (L.stats.p995_block_words + 255) & ~255u));
+      g->stats.codes = L.stats.codes;
+      g->stats.window_coverage = L.stats.window_coverage;
+      g->stats.p995_block_words = L.stats.p995_block_words;
+      {  // read set: the blocks' x-windows and their out-of-window columns (bitmap, O(n))
+        std::vector<uint64_t> bm(((uint64_t)bs.n + 63) / 64, 0);
+        auto mark = [&](uint64_t c) { bm[c >> 6] |= 1ull << (c & 63); };
+        for (uint32_t b = g->block_begin; b < block_end; ++b) {
+          const uint64_t w0 = L.blocks[b].wlo, w1 = std::min<uint64_t>(bs.n, w0 + L.dims.window);
+          for (uint64_t c = w0; c < w1; ++c) mark(c);
+          for (uint64_t q = L.rfar_ptr[b]; q < L.rfar_ptr[b + 1]; ++q) mark(L.rfar[q]);
+        }
+        std::vector<uint32_t>& rs = g->read_set;
+        rs.clear();
+        for (uint64_t wi = 0; wi < bm.size(); ++wi)
+          for (uint64_t v = bm[wi]; v; v &= v - 1) rs.push_back((uint32_t)(wi * 64 + __builtin_ctzll(v)));
+        g->have_read_set = true;
+      }
+      g->win_need.resize(g->nblocks);
+      g->far_need.resize(g->nblocks);
+      {
+        uint64_t pm = 0, fm = 0;
+        for (uint32_t q = 0; q < g->nblocks; ++q) {
+          const uint32_t b = g->block_begin + q;
+          pm = std::max<uint64_t>(pm, (uint64_t)L.blocks[b].wlo + L.dims.window);
+          g->win_need[q] = (uint32_t)std::min<uint64_t>(pm, bs.n);
+          for (uint64_t r = L.rfar_ptr[b]; r < L.rfar_ptr[b + 1]; ++r) fm = std::max<uint64_t>(fm, (uint64_t)L.rfar[r] + 1);
+          g->far_need[q] = (uint32_t)std::min<uint64_t>(fm, bs.n);
+        }
+      }
+      upload_layouts(g.get(), L, false, false, true);
+      // stats of the shard
+      const uint64_t w0 = L.blocks[g->block_begin].word_offset;
+      const uint64_t w1 = L.blocks[block_end - 1].word_offset + L.blocks[block_end - 1].nwords;
+      g->stats.stream_bytes = (w1 - w0) * 4;
+      g->stats.block_table_bytes = (uint64_t)g->nblocks * sizeof(BvdBlockInfo);
+      g->stats.row_bits = L.stats.row_bits;  // whole graph
+      g->adds = L.adds_per_product;
+    }
     *out = g.release();
   });
 }
@@ -598,9 +735,25 @@ int cmvg_graph_info_get(const cmvg_graph* g, cmvg_graph_info* o) {
   });
 }
 
+int cmvg_bvf_export(const cmvg_graph* g, uint32_t* words, uint64_t words_cap, uint32_t* blocks, uint64_t blocks_cap,
+                    uint64_t* nwords, uint32_t* nblocks, int* device_built) {
+  return guarded([&] {
+    require(g && nwords && nblocks, "null argument");
+    *nwords = g->f_stream_bytes / 4;
+    *nblocks = g->nblocks;
+    if (device_built) *device_built = g->device_built ? 1 : 0;
+    DeviceGuard dg(g->device);
+    if (words && words_cap >= *nwords && *nwords)
+      CUDA_TRY(cudaMemcpy(words, g->fwords.p, *nwords * 4, cudaMemcpyDeviceToHost));
+    if (blocks && blocks_cap >= (uint64_t)*nblocks * 8)
+      CUDA_TRY(cudaMemcpy(blocks, g->fblocks.p, (size_t)*nblocks * sizeof(BvfBlockInfo), cudaMemcpyDeviceToHost));
+  });
+}
+
 int cmvg_read_set(const cmvg_graph* g, uint32_t* cols, uint64_t cap, uint64_t* count) {
   return guarded([&] {
     require(g && count, "null argument");
+    ensure_read_set(g);
     *count = g->read_set.size();
     if (cols && cap >= g->read_set.size()) std::memcpy(cols, g->read_set.data(), g->read_set.size() * 4);
   });
@@ -797,21 +950,12 @@ int cmvg_matmat_f32(cmvg_graph* g, const float* X, float* Y, uint32_t k, int ptr
   });
 }
 
+
 int cmvg_decode_csr(cmvg_graph* g, uint64_t* row_offsets, uint32_t* cols, int ptr_kind, void* stream) {
   return guarded([&] {
     require(g && row_offsets && (cols || g->m == 0), "null argument");
     DeviceGuard dg(g->device);
     cudaStream_t st = (cudaStream_t)stream;
-    BvDev s{};
-    s.words = g->bv_words.as<uint32_t>();
-    s.seg_bits = g->bv_seg.as<uint64_t>();
-    s.n = g->n;
-    s.seg_rows = g->params.segment_rows;
-    s.nseg = (uint32_t)g->nseg;
-    s.window = g->params.window;
-    s.min_interval = g->params.min_interval;
-    s.zeta_k = g->params.zeta_k;
-    // device-resident passes (bv_decode.cuh)
     DevBuf dro, dcols;
     uint64_t* ro = row_offsets;
     uint32_t* co = cols;
@@ -821,66 +965,12 @@ int cmvg_decode_csr(cmvg_graph* g, uint64_t* row_offsets, uint32_t* cols, int pt
       ro = dro.as<uint64_t>();
       co = dcols.as<uint32_t>();
     }
-    StreamScratch deg(g->device, (size_t)g->n * 4, st), err(g->device, 16, st);
-    CUDA_TRY(cudaMemsetAsync(err.p, 0, 4, st));
-    int herr = 0;
-    const int tpb = 64;
-    const bool tiles = kDecTileRows % s.seg_rows == 0 && kDecTileRows % kDecGroup == 0 && !getenv("CMVG_SERIAL_DECODE");
-    if (!tiles) {
-      // serial decoder (segments that do not tile; tests): per-segment parse
-      // and scan, then one thread per segment writes its rows
-      StreamScratch rbit(g->device, (size_t)g->n * 8, st), segsum(g->device, g->nseg * 8, st),
-          segbase(g->device, g->nseg * 8, st);
-      bv_index_rows<<<(unsigned)((g->nseg + tpb - 1) / tpb), tpb, 0, st>>>(s, deg.as<uint32_t>(), rbit.as<uint64_t>(),
-                                                                          segsum.as<uint64_t>(), err.as<int>());
-      CUDA_TRY(cudaGetLastError());
-      bv_scan_segments<<<1, 1024, 0, st>>>(segsum.as<uint64_t>(), g->nseg, 1, g->m, segbase.as<uint64_t>(),
-                                           err.as<int>());
-      CUDA_TRY(cudaGetLastError());
-      bv_seg_decode<<<(unsigned)((g->nseg + tpb - 1) / tpb), tpb, 0, st>>>(s, segbase.as<uint64_t>(), ro, co,
-                                                                          err.as<int>());
-    } else {
-      const uint32_t ng = (uint32_t)(((uint64_t)g->n + kDecGroup - 1) / kDecGroup);
-      {  // the handle's row-group index: one serial pass per segment, once
-        std::lock_guard<std::mutex> lk(g->layout_mu);
-        if (!g->have_sync) {
-          g->bv_sync.alloc((size_t)ng * sizeof(DecSync));
-          bv_sync_index<<<(unsigned)((g->nseg + tpb - 1) / tpb), tpb, 0, st>>>(s, deg.as<uint32_t>(),
-                                                                              g->bv_sync.as<DecSync>(), err.as<int>());
-          CUDA_TRY(cudaGetLastError());
-          CUDA_TRY(cudaMemcpyAsync(&herr, err.p, 4, cudaMemcpyDeviceToHost, st));
-          CUDA_TRY(cudaStreamSynchronize(st));
-          if (herr) throw AbiError(CMVG_ERR_CORRUPT, "BV stream corrupt (device index pass, code " + std::to_string(herr) + ")");
-          g->have_sync = true;
-        }
-      }
-      StreamScratch rbit(g->device, (size_t)g->n * 8, st), gcnt(g->device, (size_t)ng * 8, st),
-          gbase(g->device, (size_t)ng * 8, st);
-      bv_index_groups<<<(ng + 127) / 128, 128, 0, st>>>(s, g->bv_sync.as<DecSync>(), deg.as<uint32_t>(),
-                                                        rbit.as<uint64_t>(), gcnt.as<uint64_t>(), err.as<int>());
-      CUDA_TRY(cudaGetLastError());
-      bv_scan_segments<<<1, 1024, 0, st>>>(gcnt.as<uint64_t>(), ng, kDecTileRows / kDecGroup, g->m,
-                                           gbase.as<uint64_t>(), err.as<int>());
-      CUDA_TRY(cudaGetLastError());
-      uint32_t cap = 24064;  // staging words: two CTAs of ~100 KB per SM
-      if (const char* e = getenv("CMVG_DECODE_CAP")) cap = (uint32_t)strtoul(e, nullptr, 10);
-      const uint32_t sm = dec_smem_bytes(cap);
-      if (g->decode_attr < sm) {
-        CUDA_TRY(cudaFuncSetAttribute(bv_decode_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        g->decode_attr = sm;
-      }
-      const uint32_t ntile = (uint32_t)(((uint64_t)g->n + kDecTileRows - 1) / kDecTileRows);
-      bv_decode_tiles<<<ntile, kDecThreads, sm, st>>>(s, deg.as<uint32_t>(), rbit.as<uint64_t>(), gbase.as<uint64_t>(),
-                                                      cap, ro, co, err.as<int>());
-    }
-    CUDA_TRY(cudaGetLastError());
-    CUDA_TRY(cudaMemcpyAsync(&herr, err.p, 4, cudaMemcpyDeviceToHost, st));
+    decode_device(g, ro, co, nullptr, st);
     if (ptr_kind == CMVG_HOST) {
       CUDA_TRY(cudaMemcpyAsync(row_offsets, ro, ((size_t)g->n + 1) * 8, cudaMemcpyDeviceToHost, st));
       if (g->m) CUDA_TRY(cudaMemcpyAsync(cols, co, g->m * 4, cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaStreamSynchronize(st));
     }
-    CUDA_TRY(cudaStreamSynchronize(st));
-    if (herr) throw AbiError(CMVG_ERR_CORRUPT, "BV stream corrupt (device decode pass, code " + std::to_string(herr) + ")");
   });
 }
 

@@ -614,7 +614,8 @@ __global__ void __launch_bounds__(kDecThreads, 2) bv_decode_tiles(BvDev s, const
                                                                const uint64_t* __restrict__ rbit,
                                                                const uint64_t* __restrict__ tile_base, uint32_t cap,
                                                                uint64_t* __restrict__ row_offsets,
-                                                               uint32_t* __restrict__ cols, int* __restrict__ err) {
+                                                               uint32_t* __restrict__ cols, int* __restrict__ err,
+                                                               uint8_t* __restrict__ ref_out = nullptr) {
   constexpr uint32_t T = kDecTileRows;
   extern __shared__ __align__(16) unsigned char dsm[];
   uint32_t* loff = reinterpret_cast<uint32_t*>(dsm);  // [T + 1]
@@ -650,6 +651,7 @@ __global__ void __launch_bounds__(kDecThreads, 2) bv_decode_tiles(BvDev s, const
       }
     }
     rr[k] = (uint8_t)r;
+    if (ref_out && k < nr) ref_out[r0 + k] = (uint8_t)r;  // the rows' reference distances (device layout build)
     dep[k] = r ? 0xffffu : 0u;
     lvl[k] = 0;
   }

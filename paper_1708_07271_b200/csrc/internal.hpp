@@ -182,7 +182,9 @@ struct cmvg_graph {
   DevBuf hx, hy;
   std::vector<uint32_t> win_need;  // per block: x prefix its window needs (prefix max)
   std::vector<uint32_t> far_need;  // per block: x prefix its out-of-window columns need (prefix max)
-  std::vector<uint32_t> read_set;  // sorted columns of x this shard's gather reads
+  mutable std::vector<uint32_t> read_set;  // sorted columns of x this shard's gather reads
+  mutable std::atomic<bool> have_read_set{false};  // (device-built handles: computed on first use)
+  bool device_built = false;                       // BV-F built on the device (no BV-D stats)
   cudaStream_t s_in = nullptr, s_comp = nullptr, s_out = nullptr;
   cudaEvent_t ev[32] = {};
   std::atomic<unsigned> gather_attr{0};  // kernel attributes set (bit per x type)
@@ -288,6 +290,18 @@ struct StreamScratch {
 void ensure_layouts(cmvg_graph* g, bool sliced, bool target);
 
 // kernel entry points implemented in the other translation units
+// device build of the BV-F layout (bvf_build.cu) and the device BV decoder
+// (cmvg_abi.cu)
+struct DeviceBuildStats {
+  uint64_t adds = 0;
+  uint32_t depth = 0;
+  double window_coverage = 1.0;
+};
+bool decode_tiles_ok(const cmvg_graph* g);
+void decode_device(cmvg_graph* g, uint64_t* ro, uint32_t* co, uint8_t* ref_out, cudaStream_t st);
+bool device_build_bvf(cmvg_graph* g, cudaStream_t st, DeviceBuildStats& ds);
+void ensure_read_set(const cmvg_graph* g);
+
 template <typename XT, typename YT, bool PR>
 void launch_bvf(cmvg_graph* g, const XT* x, const XT* xfar, YT* y, const PrArgs& pr, cudaStream_t st, uint32_t b0 = 0,
                 uint32_t b1 = 0xffffffffu);
