@@ -141,26 +141,43 @@ bool device_build_bvf(cmvg_graph* g, cudaStream_t st, DeviceBuildStats& ds) {
     std::unique_ptr<DevBuf> packed;
   };
   std::vector<Batch> batches;
+  // the batches (block ranges, arena and output offsets), then one arena and
+  // one output buffer sized for the largest batch, reused by every batch
+  struct Plan {
+    uint32_t q0, q1;
+    std::vector<uint64_t> aoff, ooff;
+  };
+  std::vector<Plan> plans;
+  uint64_t amax = 0, omax = 0;
   for (uint32_t q0 = 0; q0 < nb;) {
+    Plan p{q0, q0, {0}, {0}};
     uint64_t aw = 0, ow = 0;
-    uint32_t q1 = q0;
-    std::vector<uint64_t> aoff{0}, ooff{0};
-    while (q1 < nb) {
-      const uint32_t r0 = (bb + q1) * B, nr = std::min<uint32_t>(B, g->n - r0);
+    while (p.q1 < nb) {
+      const uint32_t q1 = p.q1, r0 = (bb + q1) * B, nr = std::min<uint32_t>(B, g->n - r0);
       const uint64_t a = bvf_block_scratch_words(E[q1], Er[q1], nr, lmin) + 64;
       const uint64_t o = (bvf_block_out_words(E[q1], Er[q1], nr, lmin) + 3) & ~3ull;
       if (q1 > q0 && aw + ow + a + o > budget) break;
       aw += a;
       ow += o;
-      aoff.push_back(aw);
-      ooff.push_back(ow);
-      ++q1;
+      p.aoff.push_back(aw);
+      p.ooff.push_back(ow);
+      ++p.q1;
     }
+    amax = std::max(amax, aw);
+    omax = std::max(omax, ow);
+    q0 = p.q1;
+    plans.push_back(std::move(p));
+  }
+  DevBuf arena, out;
+  arena.alloc(amax * 4);
+  out.alloc(omax * 4 + 16);
+  lap("alloc");
+  for (Plan& pl : plans) {
+    const uint32_t q0 = pl.q0, q1 = pl.q1;
+    std::vector<uint64_t>& aoff = pl.aoff;
+    std::vector<uint64_t>& ooff = pl.ooff;
     const uint32_t n1 = q1 - q0;
-    DevBuf arena, out, daoff, dooff, dres;
-    arena.alloc(aw * 4);
-    out.alloc(ow * 4 + 16);
-    lap("alloc");
+    DevBuf daoff, dooff, dres;
     daoff.upload(aoff.data(), aoff.size());
     dooff.upload(ooff.data(), ooff.size());
     dres.alloc((size_t)n1 * sizeof(BvfBlockResult));
@@ -189,9 +206,11 @@ bool device_build_bvf(cmvg_graph* g, cudaStream_t st, DeviceBuildStats& ds) {
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaStreamSynchronize(st));
     batches.push_back(std::move(bt));
-    q0 = q1;
     lap("pack");
   }
+  arena.free_now();
+  out.free_now();
+  lap("free");
   // final offsets, block table, packing
   std::vector<BvfBlockInfo> fbl(nb);
   std::vector<uint64_t> foff(nb + 1, 0), ebase(nb + 1, 0);
@@ -226,6 +245,7 @@ bool device_build_bvf(cmvg_graph* g, cudaStream_t st, DeviceBuildStats& ds) {
   }
   CUDA_TRY(cudaStreamSynchronize(st));
   batches.clear();
+  lap("concat");
   g->fblocks.upload(fbl.data(), fbl.size());
   {  // flat escape columns (the pre-gather's index list)
     std::vector<uint32_t> eb(nb + 1);
@@ -241,6 +261,7 @@ bool device_build_bvf(cmvg_graph* g, cudaStream_t st, DeviceBuildStats& ds) {
     g->fesc_base_h.assign(ebase.begin(), ebase.end());
     CUDA_TRY(cudaStreamSynchronize(st));
   }
+  lap("escapes");
   g->f_stream_bytes = foff[nb] * 4;
   fs.stream_bytes = foff[nb] * 4;
   g->fstats = fs;

@@ -519,7 +519,7 @@ int cmvg_create(const cmvg_bvstream* s, const cmvg_create_opts* opts_in, cmvg_gr
     g->nseg = bs.segment_bit_offsets.size() - 1;
     static const bool timing = getenv("CMVG_BUILD_TIMING") != nullptr;
     auto tc0 = std::chrono::steady_clock::now();
-    g->host_stream = std::make_shared<const BvStream>(bs);
+    g->host_stream = s->sp;
     g->build_opts = bo;
     DeviceGuard dg(o.device);
     g->bv_words.upload(bs.words.data(), bs.words.size());

@@ -59,15 +59,18 @@ struct BvfArena {
 };
 
 // arena words a block needs: E = the block's edges, Er = the edges of its
-// rows' references (sum of deg(i - r_i) over rows with r_i != 0), nr rows
-// (bounds of every allocation bvf_build_block makes, with its alignment)
+// rows' references (sum of deg(i - r_i) over rows with r_i != 0), nr rows.
+// Bounds of every allocation bvf_build_block makes (4-word aligned): minus
+// <= Er; a row's residual and interval entries <= its degree (<= E in all);
+// intervals <= E / Lmin; terms <= minus + residuals + max(2, len) per
+// interval + 2 pads per row <= Er + 2 E + 2 nr; far occurrences <= Er + E.
 CMVG_HD inline uint64_t bvf_block_nmax(uint64_t E, uint64_t Er, uint32_t nr, uint32_t lmin) {
-  const uint64_t ni = E / (lmin ? lmin : 1) + nr;
-  return 2 * Er + 4 * E + 2 * ni + 2 * (uint64_t)nr + 64;
+  (void)lmin;
+  return Er + 2 * E + 2 * (uint64_t)nr + 16;
 }
 CMVG_HD inline uint64_t bvf_block_scratch_words(uint64_t E, uint64_t Er, uint32_t nr, uint32_t lmin) {
-  const uint64_t ni = E / (lmin ? lmin : 1) + nr;
-  const uint64_t ncols = 2 * ni + Er + E, nfar = Er + 2 * E;
+  const uint64_t ni = E / (lmin ? lmin : 1) + 1;
+  const uint64_t ncols = 2 * ni + Er + E, nfar = Er + E;
   const uint64_t Nmax = bvf_block_nmax(E, Er, nr, lmin);
   const uint64_t Npad = Nmax + 16 * (Nmax / 4096 + 1);
   return 7 * ((uint64_t)nr + 1) + (Er + 1) + (E + 1) + 2 * (ni + 1) + 2 * (ncols + 1) + 260 + 2 * (nfar + 1) +
@@ -183,7 +186,7 @@ CMVG_HD inline BvfBlockResult bvf_build_block(const BvfRowsView& g, uint32_t b, 
       Er += g.ro[i - r + 1] - g.ro[i - r];
     }
   }
-  const uint64_t ni_cap = E / (lmin ? lmin : 1) + nr;
+  const uint64_t ni_cap = E / (lmin ? lmin : 1) + 1;
   uint32_t* eff = ar.take(nr);
   uint32_t* dep = ar.take(nr);
   uint32_t* mo = ar.take(nr + 1);
@@ -328,11 +331,8 @@ CMVG_HD inline BvfBlockResult bvf_build_block(const BvfRowsView& g, uint32_t b, 
     sidx[p] = s;
   }
   // ---- terms in row order
-  const uint64_t Ncap = (uint64_t)nm + ns + 2ull * nI + (nfar) + 2ull * nr + 64;
-  uint64_t Ncap_i = 0;  // terms of intervals written as columns
-  for (uint32_t t = 0; t < nI; ++t)
-    if (!int_inside(t)) Ncap_i += ilen[t];
-  const uint64_t Nmax = Ncap + Ncap_i;
+  uint64_t Nmax = (uint64_t)nm + ns + 2ull * nr + 16;  // + max(2, len) per interval
+  for (uint32_t t = 0; t < nI; ++t) Nmax += int_inside(t) ? 2u : ilen[t];
   const uint64_t Kmax = 16ull * mx<uint64_t>(1, (Nmax + 4095) / 4096);
   const uint64_t Npad = Nmax + Kmax;
   uint16_t* codes = reinterpret_cast<uint16_t*>(ar.take((Npad + 1) / 2 + 1));

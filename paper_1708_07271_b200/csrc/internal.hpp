@@ -92,6 +92,11 @@ struct DevBuf {
     }
     bytes = b;
   }
+  void free_now() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
   template <typename T>
   T* as() const {
     return reinterpret_cast<T*>(p);
@@ -127,7 +132,13 @@ struct cmvg_csr {
   HostCsr g;
 };
 struct cmvg_bvstream {
-  BvStream s;
+  // shared with the device handles built from it (they keep the stream for
+  // lazy layouts and row decodes without copying it)
+  std::shared_ptr<BvStream> sp = std::make_shared<BvStream>();
+  BvStream& s = *sp;
+  cmvg_bvstream() = default;
+  cmvg_bvstream(const cmvg_bvstream&) = delete;
+  cmvg_bvstream& operator=(const cmvg_bvstream&) = delete;
 };
 struct cmvg_layout {
   BvdLayout L;
