@@ -56,24 +56,24 @@ __global__ void bvf_block_sizes(const uint64_t* __restrict__ ro, const uint8_t* 
 
 // one block per warp: lane 0 runs the shared builder
 __global__ void __launch_bounds__(32) bvf_build_blocks(BvfRowsView g, uint32_t B, uint32_t W, uint32_t lmin, uint32_t b0,
-                                                       uint32_t nb, uint32_t* __restrict__ arena,
-                                                       const uint64_t* __restrict__ aoff, uint32_t* __restrict__ out,
-                                                       const uint64_t* __restrict__ ooff,
+                                                       const uint32_t* __restrict__ ids, uint32_t nb,
+                                                       uint32_t* __restrict__ arena, const uint64_t* __restrict__ aoff,
+                                                       uint32_t* __restrict__ out, const uint64_t* __restrict__ ooff,
                                                        BvfBlockResult* __restrict__ res) {
-  const uint32_t q = blockIdx.x;
-  if (q >= nb || threadIdx.x != 0) return;
-  BvfArena ar{arena + aoff[q], aoff[q + 1] - aoff[q], 0};
-  res[q] = bvf_build_block(g, b0 + q, B, W, lmin, ar, out + ooff[q], ooff[q + 1] - ooff[q]);
+  const uint32_t j = blockIdx.x;
+  if (j >= nb || threadIdx.x != 0) return;
+  BvfArena ar{arena + aoff[j], aoff[j + 1] - aoff[j], 0};
+  res[j] = bvf_build_block(g, b0 + ids[j], B, W, lmin, ar, out + ooff[j], ooff[j + 1] - ooff[j]);
 }
 
 // packs block q's words to its final offset
-__global__ void bvf_pack_blocks(const uint32_t* __restrict__ out, const uint64_t* __restrict__ ooff,
-                                const uint64_t* __restrict__ foff, const uint32_t* __restrict__ nwords,
-                                uint32_t* __restrict__ fwords) {
-  const uint32_t q = blockIdx.x;
-  const uint32_t* src = out + ooff[q];
-  uint32_t* dst = fwords + foff[q];
-  for (uint32_t i = threadIdx.x; i < nwords[q]; i += blockDim.x) dst[i] = src[i];
+__global__ void bvf_pack_blocks(const uint32_t* __restrict__ src_base, const uint64_t* __restrict__ src_off,
+                                const uint64_t* __restrict__ dst_off, const uint32_t* __restrict__ nwords,
+                                uint32_t* __restrict__ dst_base) {
+  const uint32_t j = blockIdx.x;
+  const uint32_t* src = src_base + src_off[j];
+  uint32_t* dst = dst_base + dst_off[j];
+  for (uint32_t i = threadIdx.x; i < nwords[j]; i += blockDim.x) dst[i] = src[i];
 }
 
 // the escape columns of block q (its stream's escape table) to the flat list
@@ -133,83 +133,92 @@ bool device_build_bvf(cmvg_graph* g, cudaStream_t st, DeviceBuildStats& ds) {
   uint64_t budget = 3ull << 30;  // words (12 GB) of arena + output per batch
   if (const char* e = getenv("CMVG_BUILD_BUDGET_WORDS")) budget = strtoull(e, nullptr, 10);
   std::vector<BvfBlockResult> res(nb);
-  // each batch's blocks are built into bounded per-block regions, then packed
-  // into a compact per-batch buffer (the bounded regions are freed)
-  struct Batch {
-    uint32_t q0, q1;
-    uint64_t words;
-    std::unique_ptr<DevBuf> packed;
-  };
-  std::vector<Batch> batches;
-  // the batches (block ranges, arena and output offsets), then one arena and
-  // one output buffer sized for the largest batch, reused by every batch
+  // Blocks are built in order of decreasing size (hub blocks of power-law
+  // graphs together, so they overlap instead of stretching every batch), in
+  // batches whose arenas fit the budget, into bounded per-block regions; each
+  // batch is then packed into a compact buffer (block-local offsets).
+  std::vector<uint64_t> need(nb);
+  for (uint32_t q = 0; q < nb; ++q) {
+    const uint32_t r0 = (bb + q) * B, nr = std::min<uint32_t>(B, g->n - r0);
+    need[q] = bvf_block_scratch_words(E[q], Er[q], nr, lmin);
+  }
+  std::vector<uint32_t> order(nb);
+  for (uint32_t q = 0; q < nb; ++q) order[q] = q;
+  std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return need[a] > need[b]; });
   struct Plan {
-    uint32_t q0, q1;
+    std::vector<uint32_t> ids;
     std::vector<uint64_t> aoff, ooff;
   };
   std::vector<Plan> plans;
   uint64_t amax = 0, omax = 0;
-  for (uint32_t q0 = 0; q0 < nb;) {
-    Plan p{q0, q0, {0}, {0}};
+  for (uint32_t k = 0; k < nb;) {
+    Plan p{{}, {0}, {0}};
     uint64_t aw = 0, ow = 0;
-    while (p.q1 < nb) {
-      const uint32_t q1 = p.q1, r0 = (bb + q1) * B, nr = std::min<uint32_t>(B, g->n - r0);
-      const uint64_t a = bvf_block_scratch_words(E[q1], Er[q1], nr, lmin) + 64;
-      const uint64_t o = (bvf_block_out_words(E[q1], Er[q1], nr, lmin) + 3) & ~3ull;
-      if (q1 > q0 && aw + ow + a + o > budget) break;
+    while (k < nb) {
+      const uint32_t q = order[k], r0 = (bb + q) * B, nr = std::min<uint32_t>(B, g->n - r0);
+      const uint64_t a = need[q] + 64;
+      const uint64_t o = (bvf_block_out_words(E[q], Er[q], nr, lmin) + 3) & ~3ull;
+      if (!p.ids.empty() && aw + ow + a + o > budget) break;
       aw += a;
       ow += o;
+      p.ids.push_back(q);
       p.aoff.push_back(aw);
       p.ooff.push_back(ow);
-      ++p.q1;
+      ++k;
     }
     amax = std::max(amax, aw);
     omax = std::max(omax, ow);
-    q0 = p.q1;
     plans.push_back(std::move(p));
   }
-  DevBuf arena, out;
-  arena.alloc(amax * 4);
-  out.alloc(omax * 4 + 16);
-  lap("alloc");
-  for (Plan& pl : plans) {
-    const uint32_t q0 = pl.q0, q1 = pl.q1;
-    std::vector<uint64_t>& aoff = pl.aoff;
-    std::vector<uint64_t>& ooff = pl.ooff;
-    const uint32_t n1 = q1 - q0;
-    DevBuf daoff, dooff, dres;
-    daoff.upload(aoff.data(), aoff.size());
-    dooff.upload(ooff.data(), ooff.size());
-    dres.alloc((size_t)n1 * sizeof(BvfBlockResult));
-    bvf_build_blocks<<<n1, 32, 0, st>>>(view, B, W, lmin, bb + q0, n1, arena.as<uint32_t>(), daoff.as<uint64_t>(),
-                                        out.as<uint32_t>(), dooff.as<uint64_t>(), dres.as<BvfBlockResult>());
-    CUDA_TRY(cudaGetLastError());
-    CUDA_TRY(cudaMemcpyAsync(res.data() + q0, dres.p, (size_t)n1 * sizeof(BvfBlockResult), cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
-    lap("build");
-    std::vector<uint64_t> poff(n1 + 1, 0);
-    std::vector<uint32_t> nw(n1);
-    for (uint32_t q = q0; q < q1; ++q) {
-      if (res[q].err)
-        throw std::runtime_error("BV-F device build: block " + std::to_string(bb + q) + " failed (code " +
-                                 std::to_string(res[q].err) + ")");
-      nw[q - q0] = res[q].nwords;
-      poff[q - q0 + 1] = poff[q - q0] + res[q].nwords;
+  struct Batch {
+    std::vector<uint32_t> ids;
+    std::vector<uint64_t> poff;  // block-local offsets in `packed`
+    std::unique_ptr<DevBuf> packed;
+  };
+  std::vector<Batch> batches;
+  {
+    DevBuf arena, out;
+    arena.alloc(amax * 4);
+    out.alloc(omax * 4 + 16);
+    lap("alloc");
+    for (Plan& pl : plans) {
+      const uint32_t n1 = (uint32_t)pl.ids.size();
+      DevBuf dids, daoff, dooff, dres;
+      dids.upload(pl.ids.data(), n1);
+      daoff.upload(pl.aoff.data(), pl.aoff.size());
+      dooff.upload(pl.ooff.data(), pl.ooff.size());
+      dres.alloc((size_t)n1 * sizeof(BvfBlockResult));
+      bvf_build_blocks<<<n1, 32, 0, st>>>(view, B, W, lmin, bb, dids.as<uint32_t>(), n1, arena.as<uint32_t>(),
+                                          daoff.as<uint64_t>(), out.as<uint32_t>(), dooff.as<uint64_t>(),
+                                          dres.as<BvfBlockResult>());
+      CUDA_TRY(cudaGetLastError());
+      std::vector<BvfBlockResult> br(n1);
+      CUDA_TRY(cudaMemcpyAsync(br.data(), dres.p, (size_t)n1 * sizeof(BvfBlockResult), cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaStreamSynchronize(st));
+      lap("build");
+      Batch bt{pl.ids, std::vector<uint64_t>(n1 + 1, 0), std::unique_ptr<DevBuf>(new DevBuf)};
+      std::vector<uint32_t> nw(n1);
+      for (uint32_t j = 0; j < n1; ++j) {
+        const uint32_t q = pl.ids[j];
+        if (br[j].err)
+          throw std::runtime_error("BV-F device build: block " + std::to_string(bb + q) + " failed (code " +
+                                   std::to_string(br[j].err) + ")");
+        res[q] = br[j];
+        nw[j] = br[j].nwords;
+        bt.poff[j + 1] = bt.poff[j] + br[j].nwords;
+      }
+      bt.packed->alloc(bt.poff[n1] * 4 + 16);
+      DevBuf dpoff, dnw;
+      dpoff.upload(bt.poff.data(), n1);
+      dnw.upload(nw.data(), n1);
+      bvf_pack_blocks<<<n1, 256, 0, st>>>(out.as<uint32_t>(), dooff.as<uint64_t>(), dpoff.as<uint64_t>(),
+                                          dnw.as<uint32_t>(), bt.packed->as<uint32_t>());
+      CUDA_TRY(cudaGetLastError());
+      CUDA_TRY(cudaStreamSynchronize(st));
+      batches.push_back(std::move(bt));
+      lap("pack");
     }
-    Batch bt{q0, q1, poff[n1], std::unique_ptr<DevBuf>(new DevBuf)};
-    bt.packed->alloc(poff[n1] * 4 + 16);
-    DevBuf dpoff, dnw;
-    dpoff.upload(poff.data(), n1);
-    dnw.upload(nw.data(), n1);
-    bvf_pack_blocks<<<n1, 256, 0, st>>>(out.as<uint32_t>(), dooff.as<uint64_t>(), dpoff.as<uint64_t>(),
-                                        dnw.as<uint32_t>(), bt.packed->as<uint32_t>());
-    CUDA_TRY(cudaGetLastError());
-    CUDA_TRY(cudaStreamSynchronize(st));
-    batches.push_back(std::move(bt));
-    lap("pack");
   }
-  arena.free_now();
-  out.free_now();
   lap("free");
   // final offsets, block table, packing
   std::vector<BvfBlockInfo> fbl(nb);
@@ -238,12 +247,24 @@ bool device_build_bvf(cmvg_graph* g, cudaStream_t st, DeviceBuildStats& ds) {
   if (ebase[nb] > 0xffffffffull) throw std::runtime_error("BV-F: more than 2^32 escape terms in one shard");
   g->fwords.alloc((foff[nb] + 64) * 4);
   CUDA_TRY(cudaMemsetAsync(g->fwords.p, 0, (foff[nb] + 64) * 4, st));
-  for (Batch& bt : batches) {
-    if (bt.words)
-      CUDA_TRY(cudaMemcpyAsync(g->fwords.as<uint32_t>() + foff[bt.q0], bt.packed->p, bt.words * 4,
-                               cudaMemcpyDeviceToDevice, st));
+  for (Batch& bt : batches) {  // each batch's blocks to their final offsets
+    const uint32_t n1 = (uint32_t)bt.ids.size();
+    std::vector<uint64_t> dst(n1);
+    std::vector<uint32_t> nw(n1);
+    for (uint32_t j = 0; j < n1; ++j) {
+      dst[j] = foff[bt.ids[j]];
+      nw[j] = res[bt.ids[j]].nwords;
+    }
+    DevBuf dsrc, ddst, dnw;
+    dsrc.upload(bt.poff.data(), n1);
+    ddst.upload(dst.data(), n1);
+    dnw.upload(nw.data(), n1);
+    bvf_pack_blocks<<<n1, 256, 0, st>>>(bt.packed->as<uint32_t>(), dsrc.as<uint64_t>(), ddst.as<uint64_t>(),
+                                        dnw.as<uint32_t>(), g->fwords.as<uint32_t>());
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaStreamSynchronize(st));
+    bt.packed.reset();
   }
-  CUDA_TRY(cudaStreamSynchronize(st));
   batches.clear();
   lap("concat");
   g->fblocks.upload(fbl.data(), fbl.size());
