@@ -2,7 +2,10 @@
 #include "cuda/bv_decode.cuh"
 #include "internal.hpp"
 
+#include <atomic>
 #include <chrono>
+#include <condition_variable>
+#include <thread>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -789,8 +792,28 @@ const void* mapped_host(const void* p) {
 // rare columns outside the window (`far`) straight from the mapped host x;
 // each chunk's y rows go back while later chunks upload -- H2D, compute and
 // D2H overlap across chunks (PCIe is full duplex).
+// Host memcpy over `threads` threads (pageable <-> pinned staging).
+void par_copy(void* dst, const void* src, size_t bytes, unsigned threads) {
+  if (bytes < (size_t(1) << 20) || threads <= 1) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  const size_t part = ((bytes + threads - 1) / threads + 63) & ~size_t(63);
+  std::vector<std::thread> th;
+  for (unsigned t = 1; t < threads && (size_t)t * part < bytes; ++t) {
+    const size_t a = (size_t)t * part, b = std::min(bytes, a + part);
+    th.emplace_back([=] { std::memcpy((char*)dst + a, (const char*)src + a, b - a); });
+  }
+  std::memcpy(dst, src, std::min(bytes, part));
+  for (auto& t : th) t.join();
+}
+
+// ux / uy (pageable x and y): x and y are then the handle's pinned staging
+// buffers; each chunk's x range is copied ux -> x just before its upload, and
+// a second host thread copies each chunk's y rows y -> uy as soon as their
+// download completes, so the host copies overlap the transfers and kernels.
 template <typename T>
-void gather_host_pipelined(cmvg_graph* g, const T* x, T* y, const T* xmapped) {
+void gather_host_pipelined(cmvg_graph* g, const T* x, T* y, const T* xmapped, const T* ux = nullptr, T* uy = nullptr) {
   const uint32_t nb = g->nblocks, B = g->dims.block_rows;
   // chunk boundaries (in blocks): a ramp up (1/4, 1/2, 3/4 of a chunk: the
   // first D2H starts early), equal chunks, then 1/2, 1/4, 1/8, 1/8 (a short
@@ -828,6 +851,40 @@ void gather_host_pipelined(cmvg_graph* g, const T* x, T* y, const T* xmapped) {
   // the last non-empty chunk uploads the rest of x
   uint32_t last = C - 1;
   while (last > 0 && cut[last] == cut[last + 1]) --last;
+  const unsigned cth = std::max(1u, std::min(8u, host_threads() / 2));
+  // pageable y: the chunks' download events, consumed by the y-copier thread
+  std::vector<std::pair<size_t, size_t>> yrange(C, {0, 0});
+  std::vector<cudaEvent_t> yev(C, nullptr);
+  std::mutex ymu;
+  std::condition_variable ycv;
+  uint32_t yposted = 0;
+  bool yabort = false;
+  std::atomic<bool> yfail{false};
+  std::thread ycopier;
+  if (uy) {
+    for (uint32_t c = 0; c < C; ++c) CUDA_TRY(cudaEventCreateWithFlags(&yev[c], cudaEventDisableTiming));
+    ycopier = std::thread([&] {
+      for (uint32_t c = 0; c < C; ++c) {
+        {
+          std::unique_lock<std::mutex> lk(ymu);
+          ycv.wait(lk, [&] { return yabort || yposted > c; });
+          if (yabort) return;
+        }
+        if (yrange[c].second > yrange[c].first) {
+          if (cudaEventSynchronize(yev[c]) != cudaSuccess) {
+            yfail = true;
+            return;
+          }
+          par_copy(uy + yrange[c].first, y + yrange[c].first, (yrange[c].second - yrange[c].first) * sizeof(T), cth);
+        }
+      }
+    });
+  }
+  auto post_y = [&](uint32_t c) {  // chunks < c may be copied out
+    std::lock_guard<std::mutex> lk(ymu);
+    yposted = c;
+    ycv.notify_one();
+  };
   try {
   for (uint32_t c = 0; c <= last; ++c) {
     const uint32_t b0 = cut[c], b1 = cut[c + 1];
@@ -838,6 +895,7 @@ void gather_host_pipelined(cmvg_graph* g, const T* x, T* y, const T* xmapped) {
     constexpr size_t kLookahead = size_t(1) << 16;
     size_t need = c == last ? g->n : std::min<size_t>(g->n, g->win_need[b1 - 1] + kLookahead);
     if (need > xdone) {
+      if (ux) par_copy(const_cast<T*>(x) + xdone, ux + xdone, (need - xdone) * sizeof(T), cth);
       CUDA_TRY(cudaMemcpyAsync(hx + xdone, x + xdone, (need - xdone) * sizeof(T), cudaMemcpyHostToDevice, g->s_in));
       xdone = need;
     }
@@ -856,15 +914,35 @@ void gather_host_pipelined(cmvg_graph* g, const T* x, T* y, const T* xmapped) {
     const size_t r0 = std::min(nrows, (size_t)b0 * B), r1 = std::min(nrows, (size_t)b1 * B);
     if (r1 > r0) CUDA_TRY(cudaMemcpyAsync(y + r0, hy + r0, (r1 - r0) * sizeof(T), cudaMemcpyDeviceToHost, g->s_out));
     if (trace) CUDA_TRY(cudaEventRecord(tev[3 * c + 2], g->s_out));
+    if (uy) {
+      yrange[c] = {r0, r1};
+      CUDA_TRY(cudaEventRecord(yev[c], g->s_out));
+      post_y(c + 1);
+    }
   }
+  if (uy) post_y(C);
   } catch (...) {
     // copies already queued must not outlive the call (they read the caller's buffers)
     (void)cudaStreamSynchronize(g->s_in);
     (void)cudaStreamSynchronize(g->s_comp);
     (void)cudaStreamSynchronize(g->s_out);
+    if (uy) {
+      {
+        std::lock_guard<std::mutex> lk(ymu);
+        yabort = true;
+      }
+      ycv.notify_one();
+      ycopier.join();
+      for (auto& e : yev) cudaEventDestroy(e);
+    }
     throw;
   }
   CUDA_TRY(cudaStreamSynchronize(g->s_out));
+  if (uy) {
+    ycopier.join();
+    for (auto& e : yev) cudaEventDestroy(e);
+    if (yfail) throw AbiError(CMVG_ERR_CUDA, "pipelined host gather: a download failed");
+  }
   if (trace) {
     for (uint32_t c = 0; c < C; ++c) {
       float a = 0, b = 0, d = 0;
@@ -905,11 +983,18 @@ int matvec_impl(cmvg_graph* g, const T* x, T* y, int form, int ptr_kind, void* s
     g->hy.alloc(nout * sizeof(T) + 64);
     if (form == CMVG_GATHER) {
       const T* xm = static_cast<const T*>(mapped_host(x));
+      if (st) CUDA_TRY(cudaStreamSynchronize(st));  // the caller's prior work on x / y
       if (xm && mapped_host(y)) {
-        if (st) CUDA_TRY(cudaStreamSynchronize(st));  // the caller's prior work on x / y
         gather_host_pipelined<T>(g, x, y, xm);
         return;
       }
+      // pageable (std::vector spans, numpy arrays): the same pipeline through
+      // the handle's pinned staging buffers, host copies overlapped
+      g->px.alloc(nin * sizeof(T) + 64);
+      g->py.alloc(nout * sizeof(T) + 64);
+      const T* pxm = static_cast<const T*>(mapped_host(g->px.p));
+      gather_host_pipelined<T>(g, g->px.as<T>(), g->py.as<T>(), pxm, x, y);
+      return;
     }
     CUDA_TRY(cudaMemcpyAsync(g->hx.p, x, nin * sizeof(T), cudaMemcpyHostToDevice, st));
     run(g->hx.as<T>(), g->hy.as<T>());

@@ -108,6 +108,34 @@ struct DevBuf {
   }
 };
 
+// Pinned (page-locked, mapped) host memory, grown on demand.
+struct PinnedBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  PinnedBuf() = default;
+  PinnedBuf(const PinnedBuf&) = delete;
+  PinnedBuf& operator=(const PinnedBuf&) = delete;
+  ~PinnedBuf() {
+    if (p) cudaFreeHost(p);
+  }
+  void alloc(size_t b) {
+    if (p && bytes >= b) return;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaHostAlloc(&p, b, cudaHostAllocMapped | cudaHostAllocPortable);
+    if (e != cudaSuccess) {
+      p = nullptr;
+      throw AbiError(CMVG_ERR_NOMEM, std::string("cudaHostAlloc(") + std::to_string(b) + "): " + cudaGetErrorString(e));
+    }
+    bytes = b;
+  }
+  template <typename T>
+  T* as() const {
+    return reinterpret_cast<T*>(p);
+  }
+};
+
 struct DeviceGuard {
   int prev = -1;
   explicit DeviceGuard(int dev) {
@@ -191,6 +219,7 @@ struct cmvg_graph {
   uint64_t nseg = 0;
   // staging for host-pointer calls; streams/events of the pipelined gather
   DevBuf hx, hy;
+  PinnedBuf px, py;  // pinned staging of pageable host x / y (the pipelined host path)
   std::vector<uint32_t> win_need;  // per block: x prefix its window needs (prefix max)
   std::vector<uint32_t> far_need;  // per block: x prefix its out-of-window columns need (prefix max)
   mutable std::vector<uint32_t> read_set;  // sorted columns of x this shard's gather reads

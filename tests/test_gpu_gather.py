@@ -221,6 +221,25 @@ def test_gather_host_pinned_pipelined_shard(cuda):
     assert max_rel_err(yp.numpy(), want) <= F64_TOL
 
 
+@pytest.mark.parametrize("n,shard", [(20000, False), ((1 << 16) + 7, False), ((1 << 17) + 99, True)])
+def test_gather_host_pageable_staged(cuda, n, shard):
+    # pageable host x / y (numpy, std::vector spans): the same pipeline through
+    # the handle's pinned staging buffers, host copies overlapped with the
+    # transfers; n = 20000 has 20 blocks (an empty last pipeline chunk)
+    g = make_graph(2, n=n)
+    s = P.BvStream.encode(g, bv_params(2))
+    a, b = (32768, g.n) if shard else (0, g.n)
+    dg = P.BvGraph(s, P.CreateOptions(row_begin=a, row_end=b))
+    for dtype, tol in ((np.float64, F64_TOL), (np.float32, F32_TOL)):
+        x = x_uniform(g.n, 7).astype(dtype)
+        want = oracle_csr(g).matvec(x.astype(np.float64), 8)[a:b]
+        y = np.full(b - a, np.nan, dtype=dtype)
+        for _ in range(2):
+            dg.matvec(x, y)
+            assert max_rel_err(y, want) <= tol
+            y[:] = np.nan
+
+
 @pytest.mark.parametrize("deg", [3.0, 12.0, 40.0, 150.0])
 def test_csr_baseline_matches_oracle(cuda, deg):
     """The uncompressed comparison kernel (matvec_csr on the GPU, csr.hpp:48-55)
