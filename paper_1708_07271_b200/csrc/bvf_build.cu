@@ -297,6 +297,22 @@ bool device_build_bvf(cmvg_graph* g, cudaStream_t st, DeviceBuildStats& ds) {
     g->far_need[q] = (uint32_t)std::min<uint64_t>(fm, g->n);
   }
   g->dims.max_depth = std::max(g->dims.max_depth, depth);
+  if (timing) {
+    double cyc[6] = {0};
+    uint64_t mx = 0;
+    for (uint32_t q = 0; q < nb; ++q) {
+      uint64_t t = 0;
+      for (int k = 0; k < 6; ++k) {
+        cyc[k] += (double)res[q].cyc[k];
+        t += res[q].cyc[k];
+      }
+      mx = std::max(mx, t);
+    }
+    fprintf(stderr, "[device build] per-block Mcycles (mean): splits %.2f window %.2f far %.2f terms %.2f schedule %.2f "
+                    "stream %.2f; slowest block %.1f\n",
+            cyc[0] / nb / 1e6, cyc[1] / nb / 1e6, cyc[2] / nb / 1e6, cyc[3] / nb / 1e6, cyc[4] / nb / 1e6,
+            cyc[5] / nb / 1e6, (double)mx / 1e6);
+  }
   lap("finish");
   ds.adds = adds;
   ds.depth = depth;

@@ -44,7 +44,16 @@ struct BvfBlockResult {
   uint32_t max_deg;
   uint64_t terms, pad_terms, slot_terms, esc_terms;
   int err;                // 0 ok; 1 arena or output too small; 2 bad reference; 3 block too large
+  uint64_t cyc[6];        // (device) clock cycles per phase: splits, window, far slots, terms, schedule, stream
 };
+
+CMVG_HD inline uint64_t bvfb_clock() {
+#ifdef __CUDA_ARCH__
+  return clock64();
+#else
+  return 0;
+#endif
+}
 
 struct BvfArena {
   uint32_t* base;
@@ -173,6 +182,12 @@ CMVG_HD inline BvfBlockResult bvf_build_block(const BvfRowsView& g, uint32_t b, 
     R.err = e;
     return R;
   };
+  uint64_t tc = bvfb_clock();
+  auto tick = [&](int ph) {
+    const uint64_t t = bvfb_clock();
+    R.cyc[ph] += t - tc;
+    tc = t;
+  };
   // ---- per-row splits (capacities from the rows' degrees)
   uint64_t E = 0, Er = 0;
   uint32_t maxdeg = 0;
@@ -229,6 +244,7 @@ CMVG_HD inline BvfBlockResult bvf_build_block(const BvfRowsView& g, uint32_t b, 
   R.depth = depth;
   R.adds = adds;
   R.max_deg = maxdeg;
+  tick(0);
   // ---- the x-window: the W-column range holding most gathered columns
   const uint64_t ncols = 2ull * nI + nm + ns;
   uint32_t* cols = ar.take(ncols + 1);
@@ -268,6 +284,7 @@ CMVG_HD inline BvfBlockResult bvf_build_block(const BvfRowsView& g, uint32_t b, 
   }
   lo &= ~15ull;
   const uint64_t wlo = lo;
+  tick(1);
   auto inwin = [&](uint64_t c) { return c >= wlo && c < wlo + W; };
   auto int_inside = [&](uint32_t t) { return ist[t] >= wlo && (uint64_t)ist[t] + ilen[t] <= wlo + W; };
   {
@@ -330,6 +347,7 @@ CMVG_HD inline BvfBlockResult bvf_build_block(const BvfRowsView& g, uint32_t b, 
     scol[p] = c;
     sidx[p] = s;
   }
+  tick(2);
   // ---- terms in row order
   uint64_t Nmax = (uint64_t)nm + ns + 2ull * nr + 16;  // + max(2, len) per interval
   for (uint32_t t = 0; t < nI; ++t) Nmax += int_inside(t) ? 2u : ilen[t];
@@ -401,6 +419,7 @@ CMVG_HD inline BvfBlockResult bvf_build_block(const BvfRowsView& g, uint32_t b, 
     codes[q] = (uint16_t)ZERO;
     ecol[q] = 0;
   }
+  tick(3);
   // ---- bank schedule (layout.hpp; host/bvd_layout.cpp, bvf_schedule_terms):
   // in term step j the 32 chunks of a warp load table entries at once, in two
   // half-warp phases of 16 lanes; a row's terms may be summed in any order, so
@@ -503,6 +522,7 @@ CMVG_HD inline BvfBlockResult bvf_build_block(const BvfRowsView& g, uint32_t b, 
     }
     for (uint32_t k = 0; k < nr; ++k) codes[rstart[k + 1] - 1] |= (uint16_t)kBvfEnd;  // a row's last position ends it
   }
+  tick(4);
   // ---- escape terms: index within the chunk's escape segment
   uint32_t nesc = 0;
   for (uint32_t t = 0; t < nact; ++t) {
@@ -581,6 +601,7 @@ CMVG_HD inline BvfBlockResult bvf_build_block(const BvfRowsView& g, uint32_t b, 
   info.codes_off = codes_off;
   info.esc_off = esc_off;
   info.nwords = (uint32_t)o;
+  tick(5);
   R.terms = terms;
   R.pad_terms = pad_terms;
   R.slot_terms = slot_terms;
