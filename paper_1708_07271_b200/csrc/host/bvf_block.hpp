@@ -446,26 +446,33 @@ CMVG_HD inline BvfBlockResult bvf_build_block(const BvfRowsView& g, uint32_t b, 
     for (uint32_t j = 0; j < K; ++j) {
       for (uint32_t h0 = 0; h0 < nact; h0 += 16) {
         uint32_t nl = 0;
+        uint32_t lrow[16], lkey[16];
         for (uint32_t t = h0; t < mn(nact, h0 + 16); ++t)
-          if ((uint64_t)t * K + j < N) lanes[nl++] = t;
+          if ((uint64_t)t * K + j < N) {
+            const uint32_t k = rowof[(uint64_t)t * K + j];
+            lanes[nl] = t;
+            lrow[nl] = k;
+            lkey[nl++] = pend[k] - rstart[k];
+          }
         // most constrained (fewest remaining terms) first; stable
         for (uint32_t a = 1; a < nl; ++a) {
-          const uint32_t v = lanes[a];
-          const uint32_t rv = rowof[(uint64_t)v * K + j], kv = pend[rv] - rstart[rv];
+          const uint32_t v = lanes[a], rv = lrow[a], kv = lkey[a];
           uint32_t p = a;
-          while (p > 0) {
-            const uint32_t u = lanes[p - 1], ru = rowof[(uint64_t)u * K + j];
-            if (!(kv < pend[ru] - rstart[ru])) break;
-            lanes[p] = u;
+          while (p > 0 && kv < lkey[p - 1]) {
+            lanes[p] = lanes[p - 1];
+            lrow[p] = lrow[p - 1];
+            lkey[p] = lkey[p - 1];
             --p;
           }
           lanes[p] = v;
+          lrow[p] = rv;
+          lkey[p] = kv;
         }
         for (int q = 0; q < 16; ++q) nseen[q] = nfseen[q] = 0;
         uint32_t nf = 0;
         for (uint32_t q = 0; q < nl; ++q) {
           const uint64_t pos = (uint64_t)lanes[q] * K + j;
-          const uint32_t k = rowof[pos];
+          const uint32_t k = lrow[q];
           uint32_t best_i = rstart[k], bcost = 0xffffffffu;
           bool bdup = false;
           for (uint32_t i = rstart[k]; i < pend[k]; ++i) {
