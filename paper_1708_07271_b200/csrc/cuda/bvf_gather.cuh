@@ -201,22 +201,59 @@ __device__ __forceinline__ void bvf_chunk(const BvfTerms<XT, SPLIT, ESC>& tm, co
 // xe[i] = x[esc[i]] for the escape terms of a launch's blocks (columns outside
 // a block's x-window and far slots): one independent, fully parallel gather,
 // so the term loop streams the values instead of chasing column -> x.
+// L2 eviction hints (createpolicy + L2::cache_hint): the escape columns and
+// xe stream through L2 once (evict_first) while the gathered x lines stay
+// (evict_last) -- at C4 x (134 MB of fp32) is about the size of L2 and the
+// gathers hit it repeatedly
+__device__ __forceinline__ uint64_t l2_policy_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint32_t ld_hint(const uint32_t* a, uint64_t pol) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ float ld_hint(const float* a, uint64_t pol) {
+  float v;
+  asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ld_hint(const double* a, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_hint(float* a, float v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(a), "f"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_hint(double* a, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
+}
+
 template <typename XT>
 __global__ void __launch_bounds__(256) bvf_esc_gather(const uint32_t* __restrict__ esc, uint64_t cnt,
                                                       const XT* __restrict__ x, XT* __restrict__ xe) {
   const uint64_t step = (uint64_t)gridDim.x * blockDim.x;
   uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t pf = l2_policy_first(), pl = l2_policy_last();
   for (; i + 3 * step < cnt; i += 4 * step) {  // four independent gathers in flight per thread
     uint32_t c[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) c[k] = __ldg(esc + i + k * step);
+    for (int k = 0; k < 4; ++k) c[k] = ld_hint(esc + i + k * step, pf);
     XT v[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) v[k] = __ldg(x + c[k]);
+    for (int k = 0; k < 4; ++k) v[k] = ld_hint(x + c[k], pl);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) xe[i + k * step] = v[k];
+    for (int k = 0; k < 4; ++k) st_hint(xe + i + k * step, v[k], pf);
   }
-  for (; i < cnt; i += step) xe[i] = __ldg(x + __ldg(esc + i));
+  for (; i < cnt; i += step) st_hint(xe + i, ld_hint(x + ld_hint(esc + i, pf), pl), pf);
 }
 
 // CW, CB: compile-time window and block rows (0 = from BvfDev): the default
@@ -264,7 +301,14 @@ __global__ void __launch_bounds__(kBvfThreads, 4)
   if (tid == 64 && g.ahead && bl + g.ahead / 2 < g.nlaunch) {
     // half a wave ahead (its table entry was prefetched half a wave ago)
     const BvfBlockInfo nb = g.blocks[bl + g.ahead / 2];
-    bulk_prefetch_l2(g.words + nb.word_offset, nb.nwords * 4u);
+    // its header and terms; not its escape column table (read by the
+    // escape pre-gather, never by this kernel: ~1 GB per product at C4)
+    if (nb.flags & kBvfFlagEsc) {
+      bulk_prefetch_l2(g.words + nb.word_offset, nb.esc_off * 4u);
+      bulk_prefetch_l2(g.words + nb.word_offset + nb.codes_off, (nb.nwords - nb.codes_off) * 4u);
+    } else {
+      bulk_prefetch_l2(g.words + nb.word_offset, nb.nwords * 4u);
+    }
     const uint32_t xe = min(nb.wlo + W, g.n);
     const uint32_t xb = ((xe > nb.wlo ? xe - nb.wlo : 0u) * (uint32_t)sizeof(XT)) & ~15u;
     if (xb && (reinterpret_cast<uintptr_t>(x + nb.wlo) & 15u) == 0) bulk_prefetch_l2(x + nb.wlo, xb);
