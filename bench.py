@@ -525,7 +525,8 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "e2e_pageable": e2e_pageable,
-            "gpu_launches": args.steps,
+            # the gather kernel per step, plus the escape pre-gather when the shard has escape terms
+            "gpu_launches": args.steps * (2 if info.get("bvf_esc_terms", 0) else 1),
             "clocks": clocks,
             "parity_max_rel_err_vs_matvec_csr": parity,
             "csr_baseline": csr_base,
