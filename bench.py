@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--no-parity", action="store_true", help="skip the oracle parity checks (profiling runs)")
     ap.add_argument("--pr-log2", type=int, default=24, help="PageRank leg: n = 2^pr_log2 (full C3: 26)")
     ap.add_argument("--pr-iters", type=int, default=20)
+    ap.add_argument("--pr-exchange", choices=["halo", "push"], default="halo",
+                    help="PageRank leg at N > 1: halo all_to_all (NCCL) or the fused push of q' into the peers' "
+                         "symmetric-memory buffers from the step kernel")
     return ap.parse_args()
 
 
@@ -290,7 +293,13 @@ def pagerank_leg(args, dev, rank, world, plan_fn, flush):
         halo = D.plan_halo(dg.read_set(), plan, rank, device=dev)
     iters = args.pr_iters
 
+    push = None
+    if world > 1 and args.pr_exchange == "push":
+        push = D.PushExchange(n, plan, rank, halo, device=dev)
+
     def run(k):
+        if push is not None:
+            return push.run(dg, deg, alpha=0.15, iterations=k)
         return D.sharded_pagerank_dev(step, deg, n, plan, rank, 0.15, k, None, device=dev, halo=halo)
 
     run(3)  # warm-up (attributes, NCCL)
@@ -306,7 +315,8 @@ def pagerank_leg(args, dev, rank, world, plan_fn, flush):
     torch.cuda.synchronize()
     ms = max_over_ranks(ea.elapsed_time(eb), dev, world)
     out = {"iter_s": iters / (ms * 1e-3), "ms_per_iter": ms / iters, "iterations": iters, "n": n, "m": g.m,
-           "exchange": "halo all_to_all (NCCL), scalars device resident" if world > 1 else "none (1 GPU)",
+           "exchange": ("fused push of q' into the peers' symmetric memory from the step kernel" if push is not None
+                        else "halo all_to_all (NCCL), scalars device resident") if world > 1 else "none (1 GPU)",
            "what": f"PageRank alpha=0.15 kUniform on BV(A^T), C3 generator at n=2^{args.pr_log2}, rows sharded x{world}; "
                    "timed region = the whole iteration loop incl. initialisation (CUDA events, max over ranks)"}
     full = D.gather_to_rank0(p, plan, rank)
