@@ -12,6 +12,6 @@ python tools/mm_diag.py 24 16 >> gpurun_out/others_$TAG.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:bvs_matmat_kernel -s 2 -c 1 \
     -o gpurun_out/prof_matmat_$TAG python tools/mm_diag.py 24 16 >> gpurun_out/others_$TAG.log 2>&1
 python tools/pr_diag.py 26 20 >> gpurun_out/others_$TAG.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:bvs_gather_kernel -s 10 -c 1 \
+ncu --set full --import-source on --clock-control none -k regex:bvf_gather_kernel -s 10 -c 1 \
     --graph-profiling node -o gpurun_out/prof_pagerank_$TAG python tools/pr_diag.py 26 5 >> gpurun_out/others_$TAG.log 2>&1
 echo done $TAG
