@@ -131,7 +131,15 @@ bool device_build_bvf(cmvg_graph* g, cudaStream_t st, DeviceBuildStats& ds) {
   }
   lap("sizes");
   // batches of blocks whose arenas fit the budget
-  uint64_t budget = 3ull << 30;  // words (12 GB) of arena + output per batch
+  // words of arena + output per batch: 12 GB, or a quarter of the free device
+  // memory when less is free (CMVG_BUILD_BUDGET_WORDS overrides)
+  uint64_t budget = 3ull << 30;
+  {
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) budget = std::min<uint64_t>(budget, fr / 16);
+    (void)cudaGetLastError();
+    budget = std::max<uint64_t>(budget, 1ull << 24);
+  }
   if (const char* e = getenv("CMVG_BUILD_BUDGET_WORDS")) budget = strtoull(e, nullptr, 10);
   std::vector<BvfBlockResult> res(nb);
   // Blocks are built in order of decreasing size (hub blocks of power-law

@@ -538,7 +538,17 @@ int cmvg_create(const cmvg_bvstream* s, const cmvg_create_opts* opts_in, cmvg_gr
       g->dims = BvdDims{bs.n, o.block_rows, o.window, bs.params.min_interval,
                         (uint32_t)(((uint64_t)bs.n + o.block_rows - 1) / o.block_rows), 0, 0, 0};
       DeviceBuildStats ds;
-      if (device_build_bvf(g.get(), 0, ds)) {
+      bool ok = false;
+      try {
+        ok = device_build_bvf(g.get(), 0, ds);
+      } catch (const AbiError& e) {
+        if (e.code != CMVG_ERR_NOMEM) throw;  // a corrupt stream stays an error
+        (void)cudaGetLastError();
+        g->fwords.free_now();
+        g->fesc.free_now();
+        ok = false;  // not enough device memory for the build's arenas: the host build below
+      }
+      if (ok) {
         built = true;
         g->device_built = true;
         g->adds = ds.adds;

@@ -98,3 +98,29 @@ def test_bvf_signed_values_and_cancellation():
     scale = np.array([np.sum(np.abs(x[co[ro[i]:ro[i + 1]]])) for i in range(g.n)])
     assert np.all(np.abs(y - exact) <= 1e-15 * scale + 1e-300)
     assert np.all(np.abs(want - exact) <= 1e-13 * scale + 1e-300)
+
+
+@pytest.mark.parametrize("window,lmin", [(16, 2), (16, 4), (64, 2), (1536, 2)])
+def test_bvf_builder_bounds_adversarial(window, lmin):
+    """The shared block builder (host/bvf_block.hpp) runs in arenas sized by
+    its worst-case bounds (the device build allocates exactly those): windows
+    of 16 columns (nearly every column far: slots, then escapes), intervals as
+    short as the encoder allows (Lmin = 2), dense and copied rows -- every block must build (no arena
+    or output overflow) and evaluate exactly."""
+    rng = np.random.default_rng(11 + window + lmin)
+    n = 5000
+    rows = []
+    for i in range(n):
+        kind = i % 4
+        if kind == 0:
+            rows.append(sorted(set(rng.integers(0, n, 60).tolist())))          # scattered
+        elif kind == 1:
+            a = int(rng.integers(0, n - 200))
+            rows.append(list(range(a, a + int(rng.integers(1, 150)))))          # one long run
+        elif kind == 2 and i > 0:
+            rows.append(sorted(set(rows[i - 1][::2] + rng.integers(0, n, 5).tolist())))  # copies with skips
+        else:
+            rows.append([])
+    g = csr_from_rows(rows)
+    params = P.BvParams(min_interval=lmin)
+    _check(g, params, window=window)
