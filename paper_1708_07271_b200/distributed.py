@@ -192,37 +192,38 @@ def sharded_pagerank_dev(step_fn: Callable, degrees_shard, n: int, plan: ShardPl
         q_bufs = push.qb
         push.prime(q_loc)
     else:
-        q_pad = torch.zeros(plan.world * plan.chunk, dtype=dt, device=device)
-        q_next = torch.zeros(plan.chunk, dtype=dt, device=device)
-        q_send = torch.zeros(plan.chunk, dtype=dt, device=device)
-        q_send[:rows] = q_loc
+        # two full-length q vectors: iteration t reads buffer (t - 1) % 2 and the
+        # step writes its own rows of buffer t % 2 in place, so no copy of the
+        # shard's rows is made (at 1 GPU the loop is the step kernel alone)
+        q_bufs = [torch.zeros(plan.world * plan.chunk, dtype=dt, device=device) for _ in range(2)]
         if halo is not None:
             recv = torch.empty(halo.recv_entries, dtype=dt, device=device)
+        elif not single:
+            q_send = torch.zeros(plan.chunk, dtype=dt, device=device)
 
-        def exchange(q_shard):
+        def exchange(qb):  # this shard's rows are in qb[a:b]
             if single:
-                q_pad[:rows] = q_shard[:rows]
                 return
             if halo is None:
-                dist.all_gather_into_tensor(q_pad, q_shard, group=group)
+                q_send[:rows] = qb[a:b]
+                dist.all_gather_into_tensor(qb, q_send, group=group)
                 return
-            q_pad[a:b] = q_shard[:rows]
-            dist.all_to_all_single(recv, q_shard.index_select(0, halo.send_idx), output_split_sizes=halo.recv_counts,
+            dist.all_to_all_single(recv, qb[a:b].index_select(0, halo.send_idx), output_split_sizes=halo.recv_counts,
                                    input_split_sizes=halo.send_counts, group=group)
-            q_pad.index_copy_(0, halo.recv_cols, recv)
+            qb.index_copy_(0, halo.recv_cols, recv)
 
-        exchange(q_send)
+        q_bufs[0][a:b] = q_loc
+        exchange(q_bufs[0])
     it = 0
     for it in range(1, iterations + 1):
         prev, cur = part[(it - 1) % 2], part[it % 2]
         p_prev = p if l1_tolerance is not None else None
+        c, nx = (it - 1) % 2, it % 2
         if push is not None:
-            c, nx = (it - 1) % 2, it % 2
             step_fn(q_bufs[c], alpha, prev, p_prev, p_next, q_bufs[nx][a:b], cur, push=push, parity=nx)
         else:
-            q_next.zero_()
-            step_fn(q_pad[:n], alpha, prev, p_prev, p_next, q_next[:rows], cur)
-            exchange(q_next)
+            step_fn(q_bufs[c][:n], alpha, prev, p_prev, p_next, q_bufs[nx][a:b], cur)
+            exchange(q_bufs[nx])
         all_reduce(cur)
         p, p_next = p_next, p
         if l1_tolerance is not None and float(cur[1].item()) <= l1_tolerance:

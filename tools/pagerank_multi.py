@@ -31,8 +31,8 @@ def main():
     import torch.distributed as dist
 
     import paper_1708_07271_b200 as P
-    from paper_1708_07271_b200.distributed import (PushExchange, gather_to_rank0, gpu_step_fn, plan_halo,
-                                                   plan_shards, sharded_pagerank)
+    from paper_1708_07271_b200.distributed import (PushExchange, gather_to_rank0, gpu_step_fn_dev, plan_halo,
+                                                   plan_shards, sharded_pagerank_dev)
 
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
@@ -52,13 +52,13 @@ def main():
     deg_all = g.out_degrees()
     deg = torch.from_numpy(deg_all[a:b].astype(np.int32)).to(dev)
     halo = plan_halo(dg.read_set(), plan, rank, device=dev) if args.exchange != "full" else None
-    step = gpu_step_fn(dg, deg)
+    step = gpu_step_fn_dev(dg, deg)  # every per-iteration scalar stays on the device
     push = PushExchange(n, plan, rank, halo, device=dev) if args.exchange == "push" else None
 
     def run(iters):
         if push is not None:
             return push.run(dg, deg, iterations=iters)
-        return sharded_pagerank(step, deg, n, plan, rank, iterations=iters, device=dev, halo=halo)
+        return sharded_pagerank_dev(step, deg, n, plan, rank, iterations=iters, device=dev, halo=halo)
     run(2)  # warm-up
     torch.cuda.synchronize()
     dist.barrier()
