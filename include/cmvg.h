@@ -53,6 +53,11 @@ extern "C" {
 /* product forms */
 #define CMVG_GATHER 0  /* y = A * x^T  (row i of y = sum over row i of A)     */
 #define CMVG_SCATTER 1 /* y = x * A    (computed on A's own compression)      */
+#define CMVG_LEFT 2    /* y = x * A    as (A^T) x on the transpose's compression,
+                          the reference's matvec_ref_left (ref_matvec.hpp:37-41):
+                          A^T, its references (cmv::compress's rule) and its
+                          layout are built on the GPU on first use; whole-graph
+                          handles only */
 /* pointer kinds */
 #define CMVG_HOST 0   /* host buffers: H2D/D2H inside the call              */
 #define CMVG_DEVICE 1 /* device buffers on the handle's device (16-B aligned) */

@@ -646,9 +646,12 @@ class BvGraph:
         return int(load_library().cmvg_adds_per_product(self._h))
 
     def matvec(self, x, y=None, form: str = "gather", stream: Optional[int] = None):
-        """y = A x^T ("gather") or y = x A ("scatter").  numpy in -> numpy out
-        (host copies inside the call); CUDA tensors in -> CUDA tensors out."""
-        formc = {"gather": 0, "scatter": 1}[form]
+        """y = A x^T ("gather") or y = x A: "scatter" on A's own compression
+        (atomic-free segmented sums), or "left" as (A^T) x on the transpose's
+        compression -- the reference's matvec_ref_left, built on the GPU on
+        first use (whole-graph handles).  numpy in -> numpy out (host copies
+        inside the call); CUDA tensors in -> CUDA tensors out."""
+        formc = {"gather": 0, "scatter": 1, "left": 2}[form]
         dtype = np.float64 if (x.dtype == np.float64 or str(x.dtype) == "torch.float64") else np.float32
         nout = (self.row_end - self.row_begin) if form == "gather" else self.n
         if len(x) != self.n:

@@ -98,6 +98,19 @@ __global__ void bvf_pack_escapes(const uint32_t* __restrict__ fwords, const BvfB
 // stream's segments; throws on a corrupt stream.
 bool device_build_bvf(cmvg_graph* g, cudaStream_t st, DeviceBuildStats& ds) {
   if (!decode_tiles_ok(g)) return false;
+  // decode (whole graph: references stay inside 1024-row segments)
+  DevBuf dro, dco, dref;
+  dro.alloc(((size_t)g->n + 1) * 8);
+  dco.alloc(g->m * 4 + 16);
+  dref.alloc((size_t)g->n + 16);
+  decode_device(g, dro.as<uint64_t>(), dco.as<uint32_t>(), dref.as<uint8_t>(), st);
+  const BvfRowsView view{dro.as<uint64_t>(), dco.as<uint32_t>(), dref.as<uint8_t>(), g->n};
+  return build_bvf_from_rows(g, view, st, ds);
+}
+
+// The BV-F layout of g's blocks from device rows with reference distances
+// (the decoded BV stream, or a transposed graph's chosen references).
+bool build_bvf_from_rows(cmvg_graph* g, const BvfRowsView& view, cudaStream_t st, DeviceBuildStats& ds) {
   static const bool timing = getenv("CMVG_BUILD_TIMING") != nullptr;
   auto t0 = std::chrono::steady_clock::now();
   auto lap = [&](const char* what) {
@@ -108,14 +121,7 @@ bool device_build_bvf(cmvg_graph* g, cudaStream_t st, DeviceBuildStats& ds) {
     t0 = t1;
   };
   const uint32_t B = g->dims.block_rows, W = g->dims.window, lmin = g->params.min_interval;
-  // decode (whole graph: references stay inside 1024-row segments)
-  DevBuf dro, dco, dref;
-  dro.alloc(((size_t)g->n + 1) * 8);
-  dco.alloc(g->m * 4 + 16);
-  dref.alloc((size_t)g->n + 16);
-  decode_device(g, dro.as<uint64_t>(), dco.as<uint32_t>(), dref.as<uint8_t>(), st);
-  const BvfRowsView view{dro.as<uint64_t>(), dco.as<uint32_t>(), dref.as<uint8_t>(), g->n};
-  lap("decode");
+  lap("rows");
   const uint32_t nb = g->nblocks, bb = g->block_begin;
   // per-block sizes
   std::vector<uint64_t> E(nb), Er(nb);

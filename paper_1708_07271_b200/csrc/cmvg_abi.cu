@@ -969,12 +969,25 @@ void gather_host_pipelined(cmvg_graph* g, const T* x, T* y, const T* xmapped, co
   }
 }
 
+// the A^T handle of g (CMVG_LEFT), built on first use
+cmvg_graph* ensure_left(cmvg_graph* g) {
+  std::lock_guard<std::mutex> lk(g->left_mu);
+  if (!g->left) g->left = build_left_handle(g, 0);
+  return g->left.get();
+}
+
 template <typename T>
 int matvec_impl(cmvg_graph* g, const T* x, T* y, int form, int ptr_kind, void* stream) {
   return guarded([&] {
     require(g && x && y, "null argument");
-    require(form == CMVG_GATHER || form == CMVG_SCATTER, "bad form");
+    require(form == CMVG_GATHER || form == CMVG_SCATTER || form == CMVG_LEFT, "bad form");
     require(ptr_kind == CMVG_HOST || ptr_kind == CMVG_DEVICE, "bad ptr_kind");
+    if (form == CMVG_LEFT) {  // x A = (A^T) x: the gather on the transpose's layout
+      require(g->row_begin == 0 && g->row_end == g->n, "x A (CMVG_LEFT) needs a whole-graph handle");
+      DeviceGuard dg0(g->device);
+      g = ensure_left(g);
+      form = CMVG_GATHER;
+    }
     DeviceGuard dg(g->device);
     cudaStream_t st = (cudaStream_t)stream;
     const size_t nin = g->n;

@@ -225,6 +225,8 @@ struct cmvg_graph {
   mutable std::vector<uint32_t> read_set;  // sorted columns of x this shard's gather reads
   mutable std::atomic<bool> have_read_set{false};  // (device-built handles: computed on first use)
   bool device_built = false;                       // BV-F built on the device (no BV-D stats)
+  std::unique_ptr<cmvg_graph> left;  // A^T's handle (x A as (A^T) x, CMVG_LEFT), built on first use
+  std::mutex left_mu;
   cudaStream_t s_in = nullptr, s_comp = nullptr, s_out = nullptr;
   cudaEvent_t ev[32] = {};
   std::atomic<unsigned> gather_attr{0};  // kernel attributes set (bit per x type)
@@ -242,7 +244,8 @@ struct cmvg_graph {
   uint64_t device_bytes() const {
     return words.bytes + blocks.bytes + swords.bytes + sblocks.bytes + fwords.bytes + fblocks.bytes + fesc.bytes + fesc_base.bytes + twords.bytes +
            tblocks.bytes + tile_ptr.bytes +
-           tile_blk.bytes + farp_ptr.bytes + farp.bytes + bv_words.bytes + bv_seg.bytes + bv_sync.bytes;
+           tile_blk.bytes + farp_ptr.bytes + farp.bytes + bv_words.bytes + bv_seg.bytes + bv_sync.bytes +
+           (left ? left->device_bytes() : 0);
   }
   BvdDev dev() const {
     BvdDev d{};
@@ -340,6 +343,9 @@ struct DeviceBuildStats {
 bool decode_tiles_ok(const cmvg_graph* g);
 void decode_device(cmvg_graph* g, uint64_t* ro, uint32_t* co, uint8_t* ref_out, cudaStream_t st);
 bool device_build_bvf(cmvg_graph* g, cudaStream_t st, DeviceBuildStats& ds);
+struct BvfRowsView;
+bool build_bvf_from_rows(cmvg_graph* g, const BvfRowsView& view, cudaStream_t st, DeviceBuildStats& ds);
+std::unique_ptr<cmvg_graph> build_left_handle(cmvg_graph* g, cudaStream_t st);
 void ensure_read_set(const cmvg_graph* g);
 
 template <typename XT, typename YT, bool PR>

@@ -62,6 +62,9 @@ def test_c2_scatter_full_size(cuda, c2, dtype):
     want = at.matvec(x.astype(np.float64), O.threads())
     y = dg.matvec(torch.from_numpy(x).cuda(), form="scatter").cpu().numpy()
     assert max_rel_err(y, want) <= (F64_TOL if dtype == "f64" else F32_TOL)
+    # the reference's way: (A^T) x on the transpose's compression (built on the GPU)
+    y = dg.matvec(torch.from_numpy(x).cuda(), form="left").cpu().numpy()
+    assert max_rel_err(y, want) <= (F64_TOL if dtype == "f64" else F32_TOL)
 
 
 def test_c3_pagerank_full_size(cuda):

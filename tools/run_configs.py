@@ -160,6 +160,16 @@ def main():
                     e = rel_err(yd.double().cpu().numpy(), wl)
                     r[f"scatter_{dt}"] = {"s": ts_, "Gedges_s": g.m / ts_ / 1e9, "max_rel_err": e, "tol": tol,
                                           "pass": bool(e <= tol), "roofline_frac": alg / ts_ / 1e9 / PEAK}
+                    # x A the reference's way: (A^T) x on the transpose's compression, built on the GPU
+                    t0 = time.time()
+                    dg.matvec(xd, yd, form="left")
+                    torch.cuda.synchronize()
+                    first = time.time() - t0
+                    ts_ = time_launch(lambda: dg.matvec(xd, yd, form="left"), flush=flush)
+                    e = rel_err(yd.double().cpu().numpy(), wl)
+                    r[f"left_{dt}"] = {"s": ts_, "Gedges_s": g.m / ts_ / 1e9, "max_rel_err": e, "tol": tol,
+                                       "pass": bool(e <= tol), "roofline_frac": alg / ts_ / 1e9 / PEAK,
+                                       "first_call_s (A^T layout built on the GPU)": first}
                 del xd, yd
         if cfg == 3:
             deg = g.out_degrees()
