@@ -274,7 +274,8 @@ def parser() -> argparse.ArgumentParser:
     g.add_argument("--vector", help="text file, one value per line")
     g.add_argument("--uniform", action="store_true", help="x uniform in [0, 1) (seeded)")
     q.add_argument("--seed", type=int, default=1)
-    q.add_argument("--form", choices=["gather", "scatter"], default="gather")
+    q.add_argument("--form", choices=["gather", "scatter", "left"], default="gather",
+                   help="gather: A x^T; scatter: x A on A's compression; left: x A as (A^T) x (reference matvec_ref_left)")
     q.add_argument("--window", type=int, default=7)
     q.add_argument("--device", type=int, default=0)
     q.add_argument("--out", default=None)
