@@ -226,6 +226,8 @@ struct cmvg_graph {
   mutable std::atomic<bool> have_read_set{false};  // (device-built handles: computed on first use)
   bool device_built = false;                       // BV-F built on the device (no BV-D stats)
   std::unique_ptr<cmvg_graph> left;  // A^T's handle (x A as (A^T) x, CMVG_LEFT), built on first use
+  DevBuf pr_buf[6];                  // the device PageRank loop's p, p', q, q', partials, scalars (reused)
+  std::mutex pr_mu;
   std::mutex left_mu;
   cudaStream_t s_in = nullptr, s_comp = nullptr, s_out = nullptr;
   cudaEvent_t ev[32] = {};

@@ -67,7 +67,17 @@ void launch_pr_step(cmvg_graph* g, const double* q, PrArgs pr, double* p_next, c
 void run_pagerank(cmvg_graph* g, const uint32_t* degrees, double alpha, uint32_t iters, double l1_tol, int dangling,
                   const double* start, double* ranks, uint32_t* iters_run, int ptr_kind, cudaStream_t st) {
   const uint32_t n = g->n;
-  DevBuf ddeg, p0, p1, q0, q1, part, scal;
+  // the iteration's vectors live in the handle (allocated once: a C3 call
+  // would otherwise spend more time in cudaMalloc / cudaFree of its 2 GB than
+  // in several iterations); concurrent calls on one handle are serialised
+  std::lock_guard<std::mutex> lk(g->pr_mu);
+  DevBuf ddeg;
+  DevBuf& p0 = g->pr_buf[0];
+  DevBuf& p1 = g->pr_buf[1];
+  DevBuf& q0 = g->pr_buf[2];
+  DevBuf& q1 = g->pr_buf[3];
+  DevBuf& part = g->pr_buf[4];
+  DevBuf& scal = g->pr_buf[5];
   const uint32_t* deg = degrees;
   DevBuf dstart;
   const double* p0v = start;  // restart distribution (null = uniform)
