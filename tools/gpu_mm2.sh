@@ -1,0 +1,5 @@
+timeout 900 python -m pytest tests/test_gpu_scatter_matmat.py -q -x -k "matmat" > gpurun_out/mm2.log 2>&1
+python tools/mm_diag.py 24 16 >> gpurun_out/mm2.log 2>&1
+CMVG_MATMAT_BVS=1 python tools/mm_diag.py 24 16 >> gpurun_out/mm2.log 2>&1
+python tools/mm_diag.py 27 16 >> gpurun_out/mm2.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_fullsize.py -q -x -k "c5" >> gpurun_out/mm2.log 2>&1
