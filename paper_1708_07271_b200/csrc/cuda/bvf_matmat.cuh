@@ -252,8 +252,13 @@ __global__ void __launch_bounds__(kBmmT, 2)
     }
   }
   // ---- the x table rows (own window entries, far slots, the zero row)
+  // a thread's rows are 6 x 16 bytes apart, so lanes 4..7 of each quarter warp
+  // store theirs rotated by one row: the 8 lanes of a 16-byte store phase
+  // then hit 8 different bank groups
+  const bool rot = (tid >> 2) & 1u;
+  static_assert(E == 6, "the store rotation assumes 6 rows per thread");
 #pragma unroll
-  for (uint32_t q = 0; q < E; ++q) tab[j0 + q] = xv[q];
+  for (uint32_t q = 0; q < E; ++q) tab[j0 + (rot ? (q + 1) % E : q)] = rot ? xv[(q + 1) % E] : xv[q];
   if (tid < nslot) tab[W + tid] = fv;
   if (tid == 0) tab[bvf_zero(W)] = make_float4(0.f, 0.f, 0.f, 0.f);
   // ---- window prefix per column: F hi = sum h (exact), F lo = sum l
@@ -312,10 +317,11 @@ __global__ void __launch_bounds__(kBmmT, 2)
     }
   }
   float4* fhi = tab + F0;
+  float4 fh[E], fl[E];
 #pragma unroll
   for (uint32_t q = 0; q < E; ++q) {
-    fhi[j0 + q] = make_float4(bh[0], bh[1], bh[2], bh[3]);
-    flo[j0 + q] = make_float4(blo[0], blo[1], blo[2], blo[3]);
+    fh[q] = make_float4(bh[0], bh[1], bh[2], bh[3]);
+    fl[q] = make_float4(blo[0], blo[1], blo[2], blo[3]);
     const float x4[4] = {xv[q].x, xv[q].y, xv[q].z, xv[q].w};
 #pragma unroll
     for (uint32_t c = 0; c < 4; ++c) {
@@ -324,6 +330,11 @@ __global__ void __launch_bounds__(kBmmT, 2)
       bh[c] += h;
       blo[c] += l;
     }
+  }
+#pragma unroll
+  for (uint32_t q = 0; q < E; ++q) {
+    fhi[j0 + (rot ? (q + 1) % E : q)] = rot ? fh[(q + 1) % E] : fh[q];
+    flo[j0 + (rot ? (q + 1) % E : q)] = rot ? fl[(q + 1) % E] : fl[q];
   }
   if (tid == T - 1) {  // F[W]
     fhi[W] = make_float4(bh[0], bh[1], bh[2], bh[3]);
