@@ -426,7 +426,9 @@ CMVG_HD inline BvfBlockResult bvf_build_block(const BvfRowsView& g, uint32_t b, 
   // each row's terms are re-dealt to the row's positions, most constrained
   // lane first, each taking the term whose bank pair (index mod 16) is least
   // loaded in its phase (an entry already loaded is free); F terms also count
-  // their F lo load.
+  // their F lo load.  Ties go to the term whose 16-byte bank group (index mod
+  // 8) is least loaded in the lane's quarter warp: the phase of the
+  // multi-vector kernel's 16-byte table loads (cuda/bvf_matmat.cuh).
   {
     uint32_t* rowof = ar.take(N + 1);
     uint16_t* pc = reinterpret_cast<uint16_t*>(ar.take((N + 1) / 2 + 1));
@@ -442,7 +444,7 @@ CMVG_HD inline BvfBlockResult bvf_build_block(const BvfRowsView& g, uint32_t b, 
     for (uint32_t k = 0; k < nr; ++k) pend[k] = rstart[k + 1];
     uint32_t lanes[16];
     uint16_t seen[16][8], fseen[16][8];
-    uint8_t nseen[16], nfseen[16];
+    uint8_t nseen[16], nfseen[16], qseen[16];  // qseen: per quarter warp, per 16-byte bank group
     for (uint32_t j = 0; j < K; ++j) {
       for (uint32_t h0 = 0; h0 < nact; h0 += 16) {
         uint32_t nl = 0;
@@ -468,11 +470,12 @@ CMVG_HD inline BvfBlockResult bvf_build_block(const BvfRowsView& g, uint32_t b, 
           lrow[p] = rv;
           lkey[p] = kv;
         }
-        for (int q = 0; q < 16; ++q) nseen[q] = nfseen[q] = 0;
+        for (int q = 0; q < 16; ++q) nseen[q] = nfseen[q] = qseen[q] = 0;
         uint32_t nf = 0;
         for (uint32_t q = 0; q < nl; ++q) {
           const uint64_t pos = (uint64_t)lanes[q] * K + j;
           const uint32_t k = lrow[q];
+          uint8_t* qs = qseen + (((lanes[q] - h0) >> 3) << 3);
           uint32_t best_i = rstart[k], bcost = 0xffffffffu;
           bool bdup = false;
           for (uint32_t i = rstart[k]; i < pend[k]; ++i) {
@@ -494,6 +497,7 @@ CMVG_HD inline BvfBlockResult bvf_build_block(const BvfRowsView& g, uint32_t b, 
                   if (fseen[bk][s] == idx) fc = 0;
                 cost += fc + (nf == 0 ? 1u : 0u);
               }
+              cost = cost * 64u + (dup ? 0u : qs[idx & 7u]);
             }
             if (cost < bcost) {
               bcost = cost;
@@ -509,6 +513,7 @@ CMVG_HD inline BvfBlockResult bvf_build_block(const BvfRowsView& g, uint32_t b, 
           pe[best_i] = pe[pend[k]];
           codes[pos] = c;
           ecol[pos] = e;
+          if (!bdup && !(c & kBvfEsc)) ++qs[c & 7u];
           if (!bdup) {
             const uint32_t bk = (c & kBvfIdxMask) & 15u;
             if (nseen[bk] < 8) seen[bk][nseen[bk]] = (uint16_t)(c & kBvfIdxMask);
