@@ -610,7 +610,7 @@ __host__ __device__ constexpr uint32_t dec_smem_bytes(uint32_t cap_words) {
 // reference depth (counting sort in shared memory); each depth level is one
 // barrier-separated phase whose rows the warps take from a shared queue, a
 // lane taking the next row as soon as its current one is done.
-__global__ void __launch_bounds__(kDecThreads, 2) bv_decode_tiles(BvDev s, const uint32_t* __restrict__ deg,
+__global__ void __launch_bounds__(kDecThreads, 4) bv_decode_tiles(BvDev s, const uint32_t* __restrict__ deg,
                                                                const uint64_t* __restrict__ rbit,
                                                                const uint64_t* __restrict__ tile_base, uint32_t cap,
                                                                uint64_t* __restrict__ row_offsets,
