@@ -29,12 +29,16 @@ namespace cmvg {
 
 constexpr uint32_t kBmmCols = 4;          // columns per pass
 constexpr uint32_t kBmmW = 1536, kBmmB = 1024, kBmmT = 256, kBmmXPer = kBmmW / kBmmT;
+static_assert(kBmmB * 16u == 16384u, "the row-end store addresses the l plane at +16384");
 
 struct BmmSmem {
   uint32_t off_tab, off_flo, off_rows, off_rn, off_misc, total;
 };
 // one table of 16-byte rows: x window, far slots, zero row, then F hi; F lo;
-// row records (h[4], l[4]) of 32 bytes
+// row records as two planes of 16-byte rows, h[4] of every row then l[4]
+// (consecutive rows in consecutive bank groups: a quarter warp's record loads
+// of 8 consecutive rows are conflict-free; 32-byte records put rows p and
+// p + 4 in the same banks)
 __host__ __device__ constexpr BmmSmem bmm_smem_layout() {
   return BmmSmem{0u,
                  (bvf_f0(kBmmW) + kBmmW + 1) * 16u,
@@ -113,10 +117,10 @@ struct BmmTerms {
     }
     if (END) {  // a row end: predicated stores of the row's sums, then restart
       const uint32_t end = c & kBvfEnd;
-      const uint32_t p = rows + rowp * 32u;
+      const uint32_t p = rows + rowp * 16u;  // h plane; the l plane B x 16 bytes after it
       asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t"
                    "@p st.shared.v4.f32 [%1], {%2, %3, %4, %5};\n\t"
-                   "@p st.shared.v4.f32 [%1+16], {%6, %7, %8, %9};\n\t}" ::"r"(end),
+                   "@p st.shared.v4.f32 [%1+16384], {%6, %7, %8, %9};\n\t}" ::"r"(end),
                    "r"(p), "f"(a.h[0]), "f"(a.h[1]), "f"(a.h[2]), "f"(a.h[3]), "f"(a.l[0]), "f"(a.l[1]), "f"(a.l[2]),
                    "f"(a.l[3]));
       rowp += end ? 1u : 0u;
@@ -443,8 +447,8 @@ __global__ void __launch_bounds__(kBmmT, 2)
         if (miscu[32 + w]) break;
       }
     }
-    float4* rr = reinterpret_cast<float4*>(smem + L.off_rows + srow * 32u);
-    float4 a = rr[0], c2 = rr[1];
+    float4* rr = reinterpret_cast<float4*>(smem + L.off_rows) + srow;
+    float4 a = rr[0], c2 = rr[B];
     a.x += ch[0];
     a.y += ch[1];
     a.z += ch[2];
@@ -454,7 +458,7 @@ __global__ void __launch_bounds__(kBmmT, 2)
     c2.z += ch[6];
     c2.w += ch[7];
     rr[0] = a;
-    rr[1] = c2;
+    rr[B] = c2;
   }
   __syncthreads();  // #5
 
@@ -482,14 +486,14 @@ __global__ void __launch_bounds__(kBmmT, 2)
   };
   if (g.max_depth <= 3) {
     for (uint32_t k = tid; k < nr; k += T) {
-      float4 h = rec[2 * k], l = rec[2 * k + 1];
+      float4 h = rec[k], l = rec[B + k];
       uint32_t p = k, r = r8[k];
 #pragma unroll
       for (int d = 0; d < 3; ++d) {
         if (r) {
           p -= r;
-          add4(h, rec[2 * p]);
-          add4(l, rec[2 * p + 1]);
+          add4(h, rec[p]);
+          add4(l, rec[B + p]);
           r = r8[p];
         }
       }
@@ -518,11 +522,11 @@ __global__ void __launch_bounds__(kBmmT, 2)
         const uint32_t k = tid + q * T;
         if (k < nr) {
           const uint32_t p = ptr[k];
-          float4 h = rw[2 * k], l = rw[2 * k + 1];
+          float4 h = rw[k], l = rw[B + k];
           uint16_t pn = kNone;
           if (p != kNone) {
-            add4(h, rw[2 * p]);
-            add4(l, rw[2 * p + 1]);
+            add4(h, rw[p]);
+            add4(l, rw[B + p]);
             pn = ptr[p];
           }
           nh[q] = h;
@@ -536,14 +540,14 @@ __global__ void __launch_bounds__(kBmmT, 2)
       for (uint32_t q = 0; q < kMaxPer; ++q) {
         const uint32_t k = tid + q * T;
         if (k < nr) {
-          rw[2 * k] = nh[q];
-          rw[2 * k + 1] = nl[q];
+          rw[k] = nh[q];
+          rw[B + k] = nl[q];
           ptr[k] = np_[q];
         }
       }
       any = __syncthreads_or(more);
     }
-    for (uint32_t k = tid; k < nr; k += T) store(k, rw[2 * k], rw[2 * k + 1]);
+    for (uint32_t k = tid; k < nr; k += T) store(k, rw[k], rw[B + k]);
   }
 }
 
