@@ -53,8 +53,13 @@ def parse():
     ap.add_argument("--cpu-sample-seconds", type=float, default=20.0)
     ap.add_argument("--no-pagerank", action="store_true", help="skip the sharded PageRank leg")
     ap.add_argument("--no-parity", action="store_true", help="skip the oracle parity checks (profiling runs)")
-    ap.add_argument("--pr-log2", type=int, default=24, help="PageRank leg: n = 2^pr_log2 (full C3: 26)")
-    ap.add_argument("--pr-iters", type=int, default=20)
+    ap.add_argument("--pr-log2", type=int, default=0,
+                    help="PageRank leg: n = 2^pr_log2 (default: the full C3 size 26 at 1 GPU, 24 under torchrun, "
+                         "where every rank generates the whole graph)")
+    ap.add_argument("--pr-iters", type=int, default=50, help="PageRank leg iterations (C3: 50)")
+    ap.add_argument("--c4-log2", type=int, default=25,
+                    help="C4 leg (social graph, R = unbounded, y = A x^T in fp32, rows sharded): n = 2^c4_log2 "
+                         "(BASELINE.json configs[3]: 25); 0 skips it")
     ap.add_argument("--pr-exchange", choices=["halo", "push"], default="halo",
                     help="PageRank leg at N > 1: halo all_to_all (NCCL) or the fused push of q' into the peers' "
                          "symmetric-memory buffers from the step kernel")
@@ -277,7 +282,7 @@ def pagerank_leg(args, dev, rank, world, plan_fn, flush):
 
     n = 1 << args.pr_log2
     t0 = time.time()
-    g = P.CsrGraph.copy_model(n, 24.0, 0.7, 0.8, seed=SEED + 3)
+    g = P.CsrGraph.copy_model(n, 24.0, 0.7, 0.8, seed=SEED + 3)  # C3 generator (tests/helpers.py CONFIGS[3])
     at = g.transpose()
     s = P.BvStream.encode(at, P.BvParams(window=7, max_ref=3, min_interval=4, zeta_k=3, segment_rows=1024))
     plan = D.plan_shards(n, world, args.block_rows)
@@ -330,6 +335,63 @@ def pagerank_leg(args, dev, rank, world, plan_fn, flush):
     return out
 
 
+def c4_leg(args, dev, rank, world, flush):
+    """C4 (BASELINE.json configs[3]): the social generator (Zipf 2.1 out-degrees,
+    80% of successors in the node's 4096-node community), BV w=7 with
+    unbounded reference chains, one y = A x^T in fp32 per step; rows sharded
+    over the ranks (block-aligned, x replicated, y sharded, no collective:
+    strong scaling), a community-sized x-window (3968 entries).  Steps timed by
+    CUDA events with the L2 flushed before each, max over ranks; parity on
+    rank 0 against the oracle's matvec_csr of the fp32 x in fp64 (1e-5)."""
+    import torch
+
+    import paper_1708_07271_b200 as P
+    from paper_1708_07271_b200 import distributed as D
+
+    n = 1 << args.c4_log2
+    t0 = time.time()
+    g = P.CsrGraph.social(n, seed=SEED + 4)
+    s = P.BvStream.encode(g, P.BvParams(window=7, max_ref=0, min_interval=4, zeta_k=3, segment_rows=1024))
+    plan = D.plan_shards(n, world, args.block_rows)
+    a, b = plan.bounds(rank)
+    dg = P.BvGraph(s, P.CreateOptions(device=dev.index, block_rows=args.block_rows, window=3968,
+                                      row_begin=a, row_end=b))
+    info = dg.info()
+    log(f"[rank {rank}] C4 graph n={n} m={g.m} ({s.stats()['stream_bits'] / g.m:.2f} bits/edge) rows [{a},{b}) "
+        f"ready in {time.time() - t0:.1f}s, depth {info['max_depth']}")
+    x64 = x_uniform(n, SEED + 40, "f64")
+    x = torch.from_numpy(x64.astype(np.float32)).to(dev)
+    y = torch.empty(b - a, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    def step():
+        dg.matvec(x, y, stream=stream.cuda_stream)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    times = timed_events(step, args.steps, flush, stream)
+    ms = max_over_ranks(float(times.mean()), dev, world)
+    out = {"gedges_s": g.m / (ms * 1e-3) / 1e9, "ms": ms, "n": n, "m": g.m, "shard_rows_rank0": [a, b],
+           "bits_per_edge": s.stats()["stream_bits"] / g.m, "max_depth": info["max_depth"],
+           "window": 3968, "window_coverage": info.get("window_coverage"),
+           "escape_terms_rank0": info.get("bvf_esc_terms"),
+           "what": f"C4 social graph (R = unbounded) y = A x^T fp32 at n=2^{args.c4_log2}, rows sharded x{world} "
+                   "(x replicated, y sharded, no collective); escape pre-gather + gather per step, CUDA events, "
+                   "L2 flushed before each step, max over ranks"}
+    if rank == 0 and world == 1 and not args.no_parity:
+        from oracle import pyoracle as O
+        want = O.matvec_csr_raw(n, g.row_offsets, g.columns, x64.astype(np.float32).astype(np.float64), O.threads())
+        got = y.double().cpu().numpy()
+        den = np.abs(want)
+        err = np.abs(got - want)
+        out["parity_max_rel_err"] = float(np.max(np.where(den > 0, err / np.where(den > 0, den, 1.0), err)))
+    del dg
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -338,6 +400,8 @@ def run_ours(args):
     from paper_1708_07271_b200 import distributed as D
 
     rank, world, local = dist_env()
+    if not args.pr_log2:  # the full C3 size at 1 GPU; under torchrun every rank generates the whole graph
+        args.pr_log2 = 26 if world == 1 else 24
     if world != args.gpus:
         args.gpus = world
     torch.cuda.set_device(local)
@@ -503,9 +567,12 @@ def run_ours(args):
                "cpu_model": cpu_model(), "csr_legs": cpu_csr_legs(g.n, g.row_offsets, g.columns, g.m, x64)}
 
     pagerank = None
+    del dg
     if not args.no_pagerank:
-        del dg
         pagerank = pagerank_leg(args, dev, rank, world, D.plan_shards, flush)
+    c4 = None
+    if args.c4_log2:
+        c4 = c4_leg(args, dev, rank, world, flush)
 
     secondary = {}
     if args.secondary and rank == 0 and world == 1:
@@ -543,6 +610,7 @@ def run_ours(args):
             "kernel_ms": {"mean": t_rank, "median": float(np.median(times)), "min": float(times.min()),
                           "max": float(times.max())},
             "pagerank": pagerank,
+            "c4": c4,
         }
         if secondary:
             out["secondary"] = secondary
