@@ -57,9 +57,10 @@ def parse():
                     help="PageRank leg: n = 2^pr_log2 (default: the full C3 size 26 at 1 GPU, 24 under torchrun, "
                          "where every rank generates the whole graph)")
     ap.add_argument("--pr-iters", type=int, default=50, help="PageRank leg iterations (C3: 50)")
-    ap.add_argument("--c4-log2", type=int, default=25,
+    ap.add_argument("--c4-log2", type=int, default=-1,
                     help="C4 leg (social graph, R = unbounded, y = A x^T in fp32, rows sharded): n = 2^c4_log2 "
-                         "(BASELINE.json configs[3]: 25); 0 skips it")
+                         "(BASELINE.json configs[3]: 25); 0 skips it; default 25 at 1-2 GPUs, skipped at more "
+                         "(every rank generates and encodes the whole 1e9-edge graph on the shared host cores)")
     ap.add_argument("--pr-exchange", choices=["halo", "push"], default="halo",
                     help="PageRank leg at N > 1: halo all_to_all (NCCL) or the fused push of q' into the peers' "
                          "symmetric-memory buffers from the step kernel")
@@ -402,6 +403,8 @@ def run_ours(args):
     rank, world, local = dist_env()
     if not args.pr_log2:  # the full C3 size at 1 GPU; under torchrun every rank generates the whole graph
         args.pr_log2 = 26 if world == 1 else 24
+    if args.c4_log2 < 0:
+        args.c4_log2 = 25 if world <= 2 else 0
     if world != args.gpus:
         args.gpus = world
     torch.cuda.set_device(local)

@@ -920,6 +920,7 @@ void gather_host_pipelined(cmvg_graph* g, const T* x, T* y, const T* xmapped, co
     // else from the mapped host x -- PCIe round trips that queue behind the
     // H2D stream
     const bool far_on_device = g->far_need.empty() || g->far_need[b1 - 1] <= xdone;
+    if (trace && !far_on_device) std::fprintf(stderr, "chunk %2u: far columns from mapped host x\n", c);
     launch_gather<T, T>(g, hx, hy, g->s_comp, far_on_device ? hx : xmapped, b0, b1);
     CUDA_TRY(cudaEventRecord(g->ev[2 * c + 1], g->s_comp));
     if (trace) CUDA_TRY(cudaEventRecord(tev[3 * c + 1], g->s_comp));

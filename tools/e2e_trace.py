@@ -51,6 +51,25 @@ d2h = t(lambda: yp.copy_(yd, non_blocking=True))
 bi = t(both)
 print(f"{mb:.0f} MB: H2D {h2d:.3f} ms ({mb / h2d:.1f} GB/s)  D2H {d2h:.3f} ms ({mb / d2h:.1f} GB/s)  "
       f"both at once {bi:.3f} ms")
+sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+
+
+def chunked(C=16):  # the pipeline's copy pattern without kernels: D2H chunk c after H2D chunk c
+    step = (n + C - 1) // C
+    for c in range(C):
+        lo, hi = c * step, min(n, (c + 1) * step)
+        with torch.cuda.stream(sa):
+            xd[lo:hi].copy_(xp[lo:hi], non_blocking=True)
+            e = torch.cuda.Event()
+            e.record(sa)
+        with torch.cuda.stream(sb):
+            sb.wait_event(e)
+            yp[lo:hi].copy_(yd[lo:hi], non_blocking=True)
+    sb.synchronize()
+    sa.synchronize()
+
+
+print(f"chunked copy pattern (16 chunks, D2H c after H2D c): {t(chunked):.3f} ms; 8 chunks {t(lambda: chunked(8)):.3f}")
 xn, yn = xp.numpy(), yp.numpy()
 e = t(lambda: dg.matvec(xn, yn))
 dev = t(lambda: dg.matvec(xd, yd))
