@@ -7,7 +7,8 @@
 // One CTA of 256 threads per block of B rows (reference chains never leave a
 // block), 3 CTAs per SM:
 //   1. staging: the x-window x[wlo, wlo + W) and the block's far columns go to
-//      a shared-memory table; each x is split exactly at a block-wide grid
+//      a shared-memory table (fp64 x, default shape: one TMA bulk copy per
+//      warp straight into the table, awaited on the warp's mbarrier); each x is split exactly at a block-wide grid
 //      G = 2^(E - cbits) (E: the block's largest exponent) into
 //      h = (x + s) - s, a multiple of G, and l = x - h (both exact), and the
 //      window's exclusive prefix F = (sum h, sum l) is written after it.  Sums
@@ -28,6 +29,10 @@
 #include <type_traits>
 
 #include "bvs_gather.cuh"
+
+#ifndef BVF_TMA
+#define BVF_TMA 1
+#endif
 
 namespace cmvg {
 
@@ -313,6 +318,20 @@ __global__ void __launch_bounds__(kBvfThreads, 4)
     const uint32_t xb = ((xe > nb.wlo ? xe - nb.wlo : 0u) * (uint32_t)sizeof(XT)) & ~15u;
     if (xb && (reinterpret_cast<uintptr_t>(x + nb.wlo) & 15u) == 0) bulk_prefetch_l2(x + nb.wlo, xb);
   }
+  // default shape, fp64 x: each warp's 192 window entries come by one TMA bulk
+  // copy straight into the table (the raw x values are its entries), issued
+  // before the other loads and awaited on the warp's own mbarrier -- no
+  // per-thread global loads and table stores for the window
+  constexpr bool kTma = BVF_TMA && kSplit && CW == 1536;
+  bool tma = false;
+  const uint32_t mbar = smem_u32(misc + 48 + warp);
+  if constexpr (kTma) {
+    tma = !(bi.wlo & 1u) && bi.wlo + CW <= g.n && (reinterpret_cast<uintptr_t>(x) & 15u) == 0;
+    if (tma) {
+      if (lane == 0) bulk_load_init(mbar, smem_u32(tab + warp * 192u), x + bi.wlo + warp * 192u, 192u * 8u);
+      __syncwarp();
+    }
+  }
   uint32_t w0[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) w0[i] = active ? __ldg(cw + (size_t)i * nact) : 0u;
@@ -332,7 +351,7 @@ __global__ void __launch_bounds__(kBvfThreads, 4)
     for (uint32_t k = 0; k < kBvfXPer; k += 2) {
       const uint32_t j = j0 + k, c = bi.wlo + j;
       xv[k] = xv[k + 1] = 0.0;
-      if (k < E && !wide) {
+      if (k < E && !wide && !tma) {
         if (full) {
           const P2 v2 = __ldg(reinterpret_cast<const P2*>(x + c));
           xv[k] = (double)v2.x;
@@ -348,6 +367,17 @@ __global__ void __launch_bounds__(kBvfThreads, 4)
   const uint32_t far_off = bvf_far_off(nact);
   if (tid < nslot) fv = (double)__ldg(xfar + __ldg(bs + far_off + tid));
   const uint32_t rnw = tid < kBvfRnWords ? __ldg(bs + bvf_rn_off(nact) + tid) : 0u;  // stored after the loop
+  if constexpr (kTma) {
+    if (tma) {
+      mbar_wait(mbar, 0);
+#pragma unroll
+      for (uint32_t k = 0; k < 6; k += 2) {
+        const double2 v2 = *reinterpret_cast<const double2*>(tab + j0 + k);
+        xv[k] = v2.x;
+        xv[k + 1] = v2.y;
+      }
+    }
+  }
 
   // ---- block exponent (finite values), non-finite flag; the x table
   uint32_t emax = 0, nonfin = 0;
@@ -369,7 +399,7 @@ __global__ void __launch_bounds__(kBvfThreads, 4)
     see(xv[k]);
     see(xv[k + 1]);
     const uint32_t j = j0 + k;
-    if (k < E && !wide) {
+    if (k < E && !wide && !tma) {
       if (full) {
         *reinterpret_cast<double2*>(tab + j) = make_double2(xv[k], xv[k + 1]);
       } else {

@@ -1,5 +1,5 @@
-// Thin inline-PTX helpers for sm_100a: the TMA bulk L2 prefetch and an
-// asynchronous global -> shared copy (cp.async).
+// Thin inline-PTX helpers for sm_100a: the TMA bulk L2 prefetch, the TMA bulk
+// global -> shared copy with an mbarrier, and cp.async.
 #pragma once
 #include <cstdint>
 
@@ -20,6 +20,33 @@ template <int BYTES>
 __device__ __forceinline__ void cp_async(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_u32(dst)), "l"(src), "n"(BYTES) : "memory");
 }
+// TMA bulk copy of [src, src + bytes) (16-B aligned, bytes a multiple of 16)
+// into shared memory, completion counted on the mbarrier at shared address
+// mb (initialised here for one arrival: the issuing thread's expect_tx).
+__device__ __forceinline__ void bulk_load_init(uint32_t mb, uint32_t dst, const void* src, uint32_t bytes) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(mb)
+               : "memory");
+}
+// wait for phase `parity` of the mbarrier at shared address mb
+__device__ __forceinline__ void mbar_wait(uint32_t mb, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "MBAR_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@p bra MBAR_DONE;\n"
+      "bra MBAR_WAIT;\n"
+      "MBAR_DONE:\n"
+      "}" ::"r"(mb),
+      "r"(parity)
+      : "memory");
+}
+
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 }  // namespace cmvg

@@ -30,6 +30,7 @@ for _ in range(int(os.environ.get("PR_DIAG_REPS", "1"))):  # min over repetition
     b.record()
     torch.cuda.synchronize()
     ms = min(ms, a.elapsed_time(b))
+    print(f"  rep: {a.elapsed_time(b) / it:.3f} ms/iter")
 print(f"n=2^{nlog} m={g.m} iters={it} ms/iter={ms / it:.3f} iter/s={it / ms * 1e3:.1f} build_s={tb:.1f} "
       f"Gedges/s={g.m * it / ms / 1e6:.1f}")
 if os.environ.get("PR_DIAG_INFO"):
