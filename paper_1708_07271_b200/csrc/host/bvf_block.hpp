@@ -535,16 +535,9 @@ CMVG_HD inline BvfBlockResult bvf_build_block(const BvfRowsView& g, uint32_t b, 
     for (uint32_t k = 0; k < nr; ++k) codes[rstart[k + 1] - 1] |= (uint16_t)kBvfEnd;  // a row's last position ends it
   }
   tick(4);
-  // ---- escape terms: index within the chunk's escape segment
+  // ---- escape terms: counted here, ordered and indexed with the stream below
   uint32_t nesc = 0;
-  for (uint32_t t = 0; t < nact; ++t) {
-    uint32_t loc = 0;
-    for (uint64_t i = (uint64_t)t * K; i < (uint64_t)(t + 1) * K; ++i)
-      if (codes[i] & kBvfEsc) {
-        codes[i] = (uint16_t)((codes[i] & ~kBvfIdxMask) | loc++);
-        ++nesc;
-      }
-  }
+  for (uint64_t i = 0; i < (uint64_t)nact * K; ++i) nesc += (codes[i] & kBvfEsc) ? 1u : 0u;
   // split grid: 2^cbits units per |x| <= 2^E, sums exact while < 2^53
   const uint64_t bound = 2ull * W + umax + 2ull * maxdeg + 2;
   uint32_t lg = 0;
@@ -584,15 +577,53 @@ CMVG_HD inline BvfBlockResult bvf_build_block(const BvfRowsView& g, uint32_t b, 
   align4();
   const uint32_t esc_off = (uint32_t)o;
   if (nesc) {
-    uint32_t acc = 0;
-    for (uint32_t t = 0; t < nact; ++t) {
-      put(acc);
-      for (uint64_t i = (uint64_t)t * K; i < (uint64_t)(t + 1) * K; ++i) acc += (codes[i] & kBvfEsc) ? 1u : 0u;
-    }
-    put(acc);  // the total
+    // The x values of a block's escapes are gathered ahead into one list; a
+    // term holds its value's index relative to its chunk's start.  The 32
+    // chunks of a warp are interleaved: their escapes are ordered by term
+    // position, then lane, so the lanes of a warp (in lockstep over the term
+    // positions) load adjacent values -- whole sectors instead of one value
+    // per sector.  A chunk's start is the place of its first escape; a group
+    // whose list would outgrow the 13-bit index keeps chunk-major order.
+    for (uint32_t t = 0; t <= nact; ++t) put(0u);
     align4();
-    for (uint64_t i = 0; i < (uint64_t)nact * K; ++i)
-      if (codes[i] & kBvfEsc) put(ecol[i]);
+    const uint64_t col0 = o;
+    uint32_t p = 0;
+    for (uint32_t t0 = 0; t0 < nact; t0 += 32) {
+      const uint32_t t1 = mn<uint32_t>(t0 + 32, nact);
+      uint32_t gt = 0;
+      for (uint64_t i = (uint64_t)t0 * K; i < (uint64_t)t1 * K; ++i) gt += (codes[i] & kBvfEsc) ? 1u : 0u;
+      if (!gt) continue;
+      uint32_t gstart[32];
+      if (gt <= kBvfIdxMask + 1u) {
+        uint32_t seen = 0;
+        for (uint32_t i = 0; i < K; ++i)
+          for (uint32_t t = t0; t < t1; ++t) {
+            const uint64_t ci = (uint64_t)t * K + i;
+            if (!(codes[ci] & kBvfEsc)) continue;
+            if (!((seen >> (t - t0)) & 1u)) {
+              seen |= 1u << (t - t0);
+              gstart[t - t0] = p;
+              if (esc_off + t < out_cap) out[esc_off + t] = p;
+            }
+            codes[ci] = (uint16_t)((codes[ci] & ~kBvfIdxMask) | (p - gstart[t - t0]));
+            if (col0 + p < out_cap) out[col0 + p] = ecol[ci];
+            ++p;
+          }
+      } else {
+        for (uint32_t t = t0; t < t1; ++t) {
+          if (esc_off + t < out_cap) out[esc_off + t] = p;
+          uint32_t loc = 0;
+          for (uint64_t ci = (uint64_t)t * K; ci < (uint64_t)(t + 1) * K; ++ci)
+            if (codes[ci] & kBvfEsc) {
+              codes[ci] = (uint16_t)((codes[ci] & ~kBvfIdxMask) | loc++);
+              if (col0 + p < out_cap) out[col0 + p] = ecol[ci];
+              ++p;
+            }
+        }
+      }
+    }
+    if (esc_off + nact < out_cap) out[esc_off + nact] = p;  // the total
+    o = col0 + p;
     align4();
   }
   const uint32_t codes_off = (uint32_t)o;

@@ -232,8 +232,10 @@ __host__ __device__ constexpr uint32_t tmeta_rounds(uint32_t m) { return (m >> 1
 //   [0, align4(ceil(nact/2)))   u16 first row of each chunk
 //   [.., + kBvfRnWords)         reference distance r of each row, 4 bits (8 per word)
 //   [.., + align4(nslot))       far slot columns
-//   esc_off: (escape blocks) u32 first escape of each chunk [align4(nact)], then
-//                            the escape columns [align4(nesc)]
+//   esc_off: (escape blocks) u32 first escape of each chunk and the total
+//                            [align4(nact + 1)], then the escape columns
+//                            [align4(nesc)], the 32 chunks of a warp interleaved
+//                            (by term position, then lane: bvf_block.hpp)
 //   codes_off: K/2 x nact words, word q of chunk t at codes_off + q nact + t
 //     (two terms per word, the first in the low half: coalesced loads)
 constexpr uint32_t kBvfSlots = 127;    // far slots per block (the next entry is the zero entry; odd: F0 even)
