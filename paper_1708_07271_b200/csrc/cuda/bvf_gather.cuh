@@ -581,10 +581,16 @@ __global__ void __launch_bounds__(kBvfThreads, 4)
   const uint32_t rows_s = smem_u32(rows);
   uint32_t rowp = rows_s + srow * RS;
   if (active) {
-    const uint32_t tabc = smem_u32(tab);
+    uint32_t tabc = smem_u32(tab);
     const uint32_t flob = smem_u32(flo) - F0 * 8u;
     if (bi.flags & kBvfFlagEsc) {
-      BvfTerms<XT, kSplit, true> te{tabc, flob, xeb + __ldg(bs + bi.esc_off + tid), sigma, F0 * 8u};
+      // the table address and the chunk's escape pointer held in registers
+      // (opaque to the compiler, which otherwise rebuilds the shared-window
+      // base and a 64-bit element offset for every term)
+      const XT* escp = xeb + __ldg(bs + bi.esc_off + tid);
+      asm volatile("" : "+r"(tabc));
+      asm volatile("" : "+l"(escp));
+      BvfTerms<XT, kSplit, true> te{tabc, flob, escp, sigma, F0 * 8u};
       bvf_chunk(te, cw, nact, K / 2, w0, ah, al, rowp);
     } else {
       BvfTerms<XT, kSplit, false> tm{tabc, flob, nullptr, sigma, F0 * 8u};
