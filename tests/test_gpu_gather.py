@@ -320,3 +320,27 @@ def test_gather_hub_rows_concurrent_streams(cuda):
     ref = oracle_csr(g)
     for x, w in zip(xs, want):
         assert max_rel_err(w, ref.matvec(x.cpu().numpy(), 8)) <= F64_TOL
+
+
+def test_gather_window_bulk_copy_and_fallbacks(cuda):
+    """fp64 products at the default shape take the x-window by a TMA bulk copy
+    (the ABI's 16-byte aligned device buffers, whole window in range); windows
+    cut by the end of the graph take the per-thread path.  Both fill the same
+    table: wide-range values, a graph whose last windows run past n, and the
+    device- and host-pointer calls must agree bit for bit."""
+    import torch
+
+    for n in ((1 << 16) + 517, 1 << 16, 1536 + 3):  # last window past n; all windows whole; a single cut window
+        g = make_graph(2, n=n)
+        s = P.BvStream.encode(g, bv_params(2))
+        dg = P.BvGraph(s, P.CreateOptions())
+        ref = oracle_csr(g)
+        x = x_uniform(n, 5)
+        x[::97] *= 2.0**-40  # wide dynamic range inside every window (block grid split)
+        want = ref.matvec(x, 8)
+        xd = torch.from_numpy(x).cuda()
+        yd = torch.empty_like(xd)
+        dg.matvec(xd, yd)
+        y = yd.cpu().numpy()
+        assert max_rel_err(y, want) <= F64_TOL
+        assert np.array_equal(dg.matvec(x), y)
