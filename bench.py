@@ -568,6 +568,16 @@ def run_ours(args):
                                                        budget_s=args.cpu_sample_seconds)
         cpu = {"value": v / 1e9, "unit": "Gedges/s", "cores": cores, "kind": "port", "sample": sample,
                "cpu_model": cpu_model(), "csr_legs": cpu_csr_legs(g.n, g.row_offsets, g.columns, g.m, x64)}
+        # SURVEY.md §8d (iii), informational: the product on the north-star format on one core --
+        # the host codec's BV decode of the whole stream, then matvec_csr on one thread
+        t0 = time.perf_counter()
+        gd = s.decode_host()
+        t_dec = time.perf_counter() - t0
+        t_csr = cpu["csr_legs"]["matvec_csr_1t"]["ms"] * 1e-3
+        cpu["bv_decode_product_1t"] = {"gedges_s": g.m / (t_dec + t_csr) / 1e9, "decode_s": t_dec,
+                                       "product_s": t_csr, "threads": 1,
+                                       "decoded_bit_exact": bool(np.array_equal(gd.columns, g.columns))}
+        del gd
 
     pagerank = None
     del dg
