@@ -5,7 +5,7 @@
 // (pagerank.hpp:83-102).
 //
 // One CTA of 256 threads per block of B rows (reference chains never leave a
-// block), 3 CTAs per SM:
+// block), 4 CTAs per SM at the default shape:
 //   1. staging: the x-window x[wlo, wlo + W) and the block's far columns go to
 //      a shared-memory table (fp64 x, default shape: one TMA bulk copy per
 //      warp straight into the table, awaited on the warp's mbarrier); each x is split exactly at a block-wide grid
